@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 real-space force evaluations, atom-steps/s (BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl mine|reference]
+
+A "step" is one real-space force evaluation of the configured workload with
+the neighbour lists rebuilt every 20 steps inside the timed region (K = 20
+gives exactly one rebuild + 20 evaluations, the config-4 recipe). Default
+workload: BASELINE.json config 4 (333,333 rigid 3-site waters, 999,999
+atoms, L = 215.3 A: Halgren vdW on H-reduced sites at 9 A + real-space
+multipole Ewald (alpha 0.5446) at 7 A + Ewald/Thole permanent field + PCG
+induced dipoles to 1e-5 D), which fits one B200 and is the config the
+1/2/4/8-GPU metric is quoted on. Synthetic seeded inputs (no dataset).
+
+`value` is device-resident throughput (inputs already in HBM; CUDA events on
+the engine stream); `e2e` is the same through the C ABI with host buffers:
+every step uploads the coordinates (H2D) and reads back forces and energies
+(D2H). `--impl reference` times the reference's own CPU implementation
+(oracle/_ref + the closed-form port for kernels it lacks) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REBUILD_EVERY = 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if p[5 + k].lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+class Workload:
+    def __init__(self, config: int, device: int, seed: int):
+        import paper_1906_01211_b200 as m
+        self.m = m
+        self.config = config
+        c = m.CONFIGS[config]
+        self.c = c
+        self.sys = m.water_box(c["n_mol"], c["box"], seed, c["model"])
+        self.n = self.sys.n_sites
+        self.eng = m.Engine(self.n, device=device)
+        self.eng.upload_system(self.sys)
+        if c["model"] == "charmm":
+            self.p = m.CharmmParams(c["cutoff"], c["alpha"], m.ELECTRIC, 0, 1)
+            self.lists = [(c["cutoff"] + c["skin"], 0, m.SITES_ATOMIC)]
+        else:
+            terms = {1: m.TERM_VDW | m.TERM_MPOLE, 2: m.TERM_POLAR}.get(
+                config, m.TERM_VDW | m.TERM_MPOLE | m.TERM_POLAR)
+            self.p = m.AmoebaParams(c["vdw_cutoff"], 0.07, 0.12, c["elec_cutoff"], c["alpha"],
+                                    m.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
+            self.lists = [(c["elec_cutoff"] + c["skin"], 0, m.SITES_ATOMIC)]
+            if terms & m.TERM_VDW:
+                self.lists.append((c["vdw_cutoff"] + c["skin"], 1, m.SITES_VDW))
+        self.tables = {}
+        self.rebuild()
+
+    def rebuild(self):
+        for cut, lid, sites in self.lists:
+            self.tables[lid] = self.eng.build_neighbor_table(cut, list_id=lid, sites=sites)
+
+    def step(self):
+        if self.c["model"] == "charmm":
+            self.eng.charmm_step(self.tables[0], self.p)
+        else:
+            vdw = self.tables.get(1, self.tables[0])
+            self.eng.amoeba_step(vdw, self.tables[0], self.p)
+
+    def run(self, steps: int):
+        for k in range(steps):
+            if k % REBUILD_EVERY == 0:
+                self.rebuild()
+            self.step()
+
+    # roofline: (kernel name) -> algorithmic flops per launch
+    def algorithmic_flops(self, kernel: str) -> float | None:
+        from paper_1906_01211_b200.flops import PER_PAIR
+        c = self.c
+        if kernel not in PER_PAIR:
+            return None
+        if kernel in ("lj", "ewald_real", "lj_ewald"):
+            lid, cut, excl = 0, c.get("cutoff", 9.0), True
+        elif kernel == "halgren":
+            lid, cut, excl = 1, c["vdw_cutoff"], True
+        elif kernel in ("mpole", "perm_field"):
+            lid, cut, excl = 0, c["elec_cutoff"], True
+        else:  # T mat-vec: every pair, intramolecular included
+            lid, cut, excl = 0, c["elec_cutoff"], False
+        directed, _ = self.eng.count_within(self.tables[lid], cut, excl)
+        return PER_PAIR[kernel] * directed / 2.0
+
+
+def run_mine(args, world, rank, local):
+    import paper_1906_01211_b200 as m
+    device = local
+    wl = Workload(args.config, device, args.seed + rank)
+    eng = wl.eng
+    peak = m.fp64_peak_tflops(device)
+    for _ in range(args.warmup):
+        wl.step()
+    wl.rebuild()
+
+    barrier = None
+    if world > 1:
+        import torch.distributed as dist
+        barrier = dist.barrier
+    # ---- device-resident timed region
+    if barrier:
+        barrier()
+    eng.synchronize()
+    eng.profile_reset()
+    eng.profile(True)
+    launches0 = eng.launch_count()
+    with ClockSampler(device) as clk:
+        eng.timer_start()
+        wl.run(args.steps)
+        ms = eng.timer_stop()
+    launches = eng.launch_count() - launches0
+    eng.profile(False)
+    prof = eng.profile_report()
+    if barrier:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    energies, virial, iters, rms = eng.fetch_energies()
+
+    # ---- roofline of the dominant kernel
+    top = max(prof.items(), key=lambda kv: kv[1][1])
+    name, (cnt, tot_ms) = top
+    avg_ms = tot_ms / cnt
+    flops = wl.algorithmic_flops(name)
+    roof = None
+    if flops is not None:
+        achieved = flops / (avg_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "kernel": name, "achieved": round(achieved, 3),
+                "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "avg_launch_ms": round(avg_ms, 4),
+                "peak_source": "measured DFMA probe (MEASURED_PEAKS.json has no FP64 figure)",
+                "flops_per_launch": flops,
+                "share_of_step": round(tot_ms / ms, 4)}
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        x, y, z = wl.sys.x.copy(), wl.sys.y.copy(), wl.sys.z.copy()
+        for _ in range(2):
+            eng.upload_positions(x, y, z)
+            wl.step()
+            eng.fetch_forces()
+        wl.rebuild()
+        if barrier:
+            barrier()
+        eng.synchronize()
+        t0 = time.perf_counter()
+        eng.timer_start()
+        for k in range(args.steps):
+            eng.upload_positions(x, y, z)            # H2D 24 B/atom
+            if k % REBUILD_EVERY == 0:
+                wl.rebuild()
+            wl.step()
+            f = eng.fetch_forces()                   # D2H 24 B/atom
+            e = eng.fetch_energies()                 # D2H energies/virial
+        e2e_ms = eng.timer_stop()
+        wall_ms = (time.perf_counter() - t0) * 1e3
+        e2e_ms = max(e2e_ms, wall_ms)
+        if barrier:
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": world * wl.n * args.steps / (e2e_ms * 1e-3), "unit": "atom-steps/s",
+               "h2d_bytes_per_step": 24 * wl.n, "d2h_bytes_per_step": 24 * wl.n + 8 * (4 + 9 + 2),
+               "ms_per_step": e2e_ms / args.steps}
+        del f, e
+
+    out = {
+        "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
+        "value": world * wl.n * args.steps / (ms * 1e-3),
+        "unit": "atom-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded 3-site water fixture, BASELINE.json generator rules)",
+        "config": {"workload": f"BASELINE config {args.config}: {wl.c['n_mol']} waters "
+                               f"({wl.n} atoms), L={wl.c['box']} A, "
+                               + ("LJ + Ewald charge 9 A" if wl.c["model"] == "charmm" else
+                                  "Halgren 9 A + multipole Ewald 7 A + Thole/Ewald PCG 1e-5 D"),
+                   "n_atoms": wl.n, "rebuild_every": REBUILD_EVERY,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (lists > 126 MB)"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "energies_kcal_mol": [float(v) for v in energies[:3]],
+        "pcg_iters": int(iters),
+        "pcg_rms_debye": float(rms),
+        "fp64_peak_tflops_measured": round(peak, 3),
+        "kernel_ms": {k: round(v[1] / max(v[0], 1), 4) for k, v in sorted(prof.items())},
+        "kernel_share": {k: round(v[1] / ms, 4) for k, v in sorted(prof.items())},
+    }
+    return out, wl
+
+
+def cpu_baseline(args, pcg_iters):
+    from oracle import cpu_reference
+    steps, warmup = (3, 1) if args.config != 0 else (20, 3)
+    threads = 1
+    r = cpu_reference.run(args.config, threads, steps, warmup, args.seed, pcg_iters)
+    return {"value": r["value"], "unit": "atom-steps/s", "cores": threads, "kind": "reference",
+            "sample": f"{r['n_sample_atoms']}-atom box of the same generator/density, "
+                      f"{steps} steps after {warmup} warm-up; oracle/_ref Vec kernels "
+                      f"({r['isa']}) + closed-form port for multipoles/field",
+            "s_per_step": r["s_per_step"]}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    from oracle import cpu_reference
+    threads = os.cpu_count() or 1
+    r = cpu_reference.run(args.config, threads, args.steps, args.warmup, args.seed, 10)
+    return {
+        "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
+        "impl": "reference",
+        "value": r["value"],
+        "unit": "atom-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": r["s_per_step"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded 3-site water fixture)",
+        "config": {"workload": f"BASELINE config {args.config} (CPU sample: "
+                               f"{r['n_sample_atoms']} atoms per replica)",
+                   "threads": threads},
+        "cpu_baseline": {"value": r["value"], "unit": "atom-steps/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{threads} independent replicas of a "
+                                   f"{r['n_sample_atoms']}-atom box (reference shards model); "
+                                   f"oracle/_ref Vec kernels ({r['isa']}) + closed-form port "
+                                   "for multipoles/field"},
+        "e2e": {"value": r["value"], "unit": "atom-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "mine" and world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, wl = run_mine(args, world, rank, local)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(args, max(out["pcg_iters"], 1))
+        except Exception as e:  # the CPU leg is a reported baseline, not the product
+            out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,241 @@
+/*
+ * mdg.h -- C ABI of the B200-native (sm_100a) FP64 real-space pair engine.
+ *
+ * Drop-in boundary for the reference `mdvec` hot path (/root/reference/proj).
+ * The reference has no FFI; its boundary is the C++ header API. Each entry
+ * point below names the reference interface it replaces (file:line). A C++
+ * wrapper that keeps the reference signatures and exception types lives in
+ * include/mdvec_gpu.hpp; the Python mirror in paper_1906_01211_b200/mdvec.py.
+ *
+ * Conventions
+ *  - Every function returns an int status: 0 OK, 1 CONTRACT (reference
+ *    ContractViolation), 2 CAPACITY (CapacityError), 3 SINGULARITY,
+ *    4 CONVERGENCE (ConvergenceError), 5 CUDA, 6 COMM. mdg_last_error()
+ *    returns a thread-local message for the last failure.
+ *  - Host arrays are in the caller's site order (the reference's). The
+ *    context keeps a spatially sorted copy on the device and permutes at the
+ *    boundary; results are bit-for-bit independent of the caller's order only
+ *    up to FP summation order.
+ *  - Outputs are OVERWRITTEN (reference `out.reset()`, e.g.
+ *    proj/src/kernels_scalar.cpp:13). Results are ready on return
+ *    (synchronous), as in the reference.
+ *  - Per-site vectors (forces, fields, dipoles, torques) are SoA
+ *    (x[], y[], z[]) like ForceAccumulator / FieldArrays /
+ *    PolarizationState (proj/include/mdvec/kernels.hpp:21-34,
+ *    polar.hpp:74-84, system.hpp:36-42). Any output pointer may be NULL.
+ *  - virial9: row-major W_ab = sum over pairs of d_a F_b, d = r_i - r_j
+ *    (minimum image), F = force on i from j. Not in the reference.
+ *  - A context is single-stream and not thread-safe; use one per thread
+ *    (reference SPEC: concurrent calls on disjoint outputs).
+ */
+#ifndef MDG_H
+#define MDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDG_OK 0
+#define MDG_CONTRACT 1
+#define MDG_CAPACITY 2
+#define MDG_SINGULARITY 3
+#define MDG_CONVERGENCE 4
+#define MDG_CUDA 5
+#define MDG_COMM 6
+
+#define MDG_MAX_LISTS 4
+#define MDG_SITES_ATOMIC 0 /* list over atomic positions */
+#define MDG_SITES_VDW 1    /* list over Halgren-reduced vdW sites */
+
+#define MDG_MAX_NEIGHBORS 2560 /* proj/include/mdvec/common.hpp:10 (half list) */
+
+typedef struct mdg_ctx mdg_ctx;
+
+const char* mdg_last_error(void);
+int mdg_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+/* One device, one stream, capacity fixed at create time (the reference's
+ * preallocation contract, proj/tests/test_layout.cpp:215-237).
+ * max_pairs_per_atom bounds the FULL (both-direction) list per site; 0 picks
+ * 2 * MDG_MAX_NEIGHBORS. */
+int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pairs_per_atom);
+int mdg_ctx_destroy(mdg_ctx* ctx);
+int mdg_ctx_synchronize(mdg_ctx* ctx);
+/* cudaStream_t of the context, for callers that time on it. */
+void* mdg_ctx_stream(mdg_ctx* ctx);
+
+/* ---- system ------------------------------------------------------------- */
+/* Replaces ParticleSystem (proj/include/mdvec/system.hpp:12-25); validation
+ * as ParticleSystem::validate (proj/src/system.cpp:9-28). Sets the site
+ * order (spatial sort) used until the next mdg_system_upload. */
+int mdg_system_upload(mdg_ctx* ctx, int64_t n, double lx, double ly, double lz,
+                      const double* x, const double* y, const double* z, const double* charge,
+                      const double* lj_sigma, const double* lj_epsilon, const double* hal_r0,
+                      const double* hal_epsilon, const double* polarizability);
+/* New coordinates for the same sites (one MD step's input). Lists are kept. */
+int mdg_positions_upload(mdg_ctx* ctx, const double* x, const double* y, const double* z);
+/* Topology (no reference counterpart): molecule ids (exclusion groups; NULL =
+ * every site its own group) and the Halgren reduction parent/factor (NULL =
+ * no reduction: vdW sites = atoms). */
+int mdg_topology_upload(mdg_ctx* ctx, const int32_t* molecule, const int32_t* hred_parent,
+                        const double* hred_factor);
+/* Permanent multipoles (no reference counterpart): dipole[3n] (x,y,z per
+ * site), quadrupole[6n] traceless (xx,xy,xz,yy,yz,zz per site, Tinker's
+ * convention: Theta/3). NULL zeroes the term. Charges come from the system. */
+int mdg_multipoles_upload(mdg_ctx* ctx, const double* dipole, const double* quadrupole);
+
+/* ---- neighbour lists ---------------------------------------------------- */
+/* Replaces build_cell_grid + build_neighbor_table
+ * (proj/include/mdvec/neighbors.hpp:43-50, proj/src/neighbors_vec.cpp:8-94).
+ * Contract checks as proj/src/neighbors.cpp:10-17 (cutoff > 0, <= L/2).
+ * The device list holds every pair (both directions) within list_cutoff. */
+int mdg_nlist_build(mdg_ctx* ctx, int list_id, double list_cutoff, int sites);
+/* half_pairs = number of (i<j) pairs; padded_slots = reference-layout total. */
+int mdg_nlist_size(mdg_ctx* ctx, int list_id, int64_t* half_pairs, int64_t* padded_slots);
+/* Reference NeighborTable layout (proj/include/mdvec/neighbors.hpp:22-41):
+ * pairs stored on the lower site index, segments padded to 16 with the last
+ * neighbour as sentinel, so table_pairs() (neighbors.cpp:59-72) applies.
+ * Neighbours within a segment are ascending. */
+int mdg_nlist_export(mdg_ctx* ctx, int list_id, uint32_t* nnvlst, uint32_t* nvloop8,
+                     uint32_t* nvloop16, uint64_t* offset, int32_t* indices,
+                     int64_t indices_cap);
+/* Feeds a reference-layout table (e.g. one built by the reference, or
+ * exclusion-filtered) so a kernel runs on exactly that pair set. */
+int mdg_nlist_import(mdg_ctx* ctx, int list_id, double list_cutoff, int sites,
+                     const uint32_t* nnvlst, const uint64_t* offset, const int32_t* indices);
+
+/* ---- nonpolar kernels ----------------------------------------------------
+ * exclude != 0 skips pairs of one molecule. electric multiplies Coulomb
+ * terms (reference: 1.0; SI-ish MD: 332.063713). On a list over vdW sites
+ * the forces are chain-ruled back onto atoms. */
+/* lj_forces_{scalar,vectorized}, proj/include/mdvec/kernels.hpp:101-105 */
+int mdg_lj_forces(mdg_ctx* ctx, int list_id, double cutoff, int shift, int exclude,
+                  double* fx, double* fy, double* fz, double* energy, double* virial9);
+/* ewald_real_forces_*, proj/include/mdvec/kernels.hpp:107-114 */
+int mdg_ewald_real_forces(mdg_ctx* ctx, int list_id, double alpha, double cutoff,
+                          double electric, int exclude, double* fx, double* fy, double* fz,
+                          double* energy, double* virial9);
+/* halgren_forces_*, proj/include/mdvec/polar.hpp:86-91 */
+int mdg_halgren_forces(mdg_ctx* ctx, int list_id, double cutoff, double delta, double gamma,
+                       int exclude, double* fx, double* fy, double* fz, double* energy,
+                       double* virial9);
+
+/* ---- polarization ------------------------------------------------------- */
+/* dipole_field_matvec_* (proj/include/mdvec/polar.hpp:95-104) generalised
+ * to real-space Ewald: rr3 = B1 - (1-l3)/r^3, rr5 = B2 - 3(1-l5)/r^5. At
+ * alpha = 0 this is the reference Thole-only T. All list pairs (u-scale 1). */
+int mdg_tmatvec(mdg_ctx* ctx, int list_id, double alpha, double cutoff, double thole_a,
+                const double* mux, const double* muy, const double* muz, double* ex,
+                double* ey, double* ez);
+/* permanent_field_* (proj/include/mdvec/polar.hpp:107-112) generalised to
+ * q + mu + Theta and real-space Ewald (Thole l3/l5/l7). At alpha = 0 with no
+ * multipoles uploaded this is the reference charge-only field. */
+int mdg_perm_field(mdg_ctx* ctx, int list_id, double alpha, double cutoff, double thole_a,
+                   int exclude, double* ex, double* ey, double* ez);
+/* jacobi_polarization_solve (proj/include/mdvec/polar.hpp:115-118), same
+ * max-norm stopping rule, on the device. */
+int mdg_polar_solve_jacobi(mdg_ctx* ctx, int list_id, double cutoff, double thole_a, double tol,
+                           int64_t max_iter, double* mux, double* muy, double* muz,
+                           int64_t* iters, double* last_residual);
+/* Diagonal-preconditioned CG for (alpha^-1 - T) mu = E_perm (no reference
+ * counterpart; the reference solver is Jacobi). mu0 = alpha E. Stops when
+ * sqrt(sum|dmu|^2/n) * 4.80321 < tol_debye. E_perm from mdg_perm_field with
+ * the same alpha/cutoff/thole_a and exclude_perm. */
+int mdg_polar_solve_pcg(mdg_ctx* ctx, int list_id, double alpha, double cutoff, double thole_a,
+                        int exclude_perm, double tol_debye, int64_t max_iter, double* mux,
+                        double* muy, double* muz, int64_t* iters, double* last_rms_debye);
+
+/* ---- permanent multipoles (empole1 analogue, no reference counterpart) ---- */
+/* Real-space Ewald q/mu/Theta energy, translational forces, torques (global
+ * frame) and pair virial. */
+int mdg_mpole_forces(mdg_ctx* ctx, int list_id, double alpha, double cutoff, double electric,
+                     int exclude, double* fx, double* fy, double* fz, double* tx, double* ty,
+                     double* tz, double* energy, double* virial9);
+
+/* ---- fused steps (device-resident; the bench's hot path) ----------------- */
+typedef struct {
+  double cutoff;    /* LJ and Ewald cutoff (A) */
+  double alpha;     /* Ewald alpha (1/A) */
+  double electric;  /* Coulomb constant */
+  int shift;        /* LJ shift */
+  int exclude;      /* intramolecular exclusions */
+} mdg_charmm_params;
+
+/* Config-0 step: fused LJ + real-space Ewald charge energy, forces, virial
+ * over list list_id. Results stay on the device (mdg_fetch_forces). */
+int mdg_charmm_step(mdg_ctx* ctx, int list_id, const mdg_charmm_params* p);
+
+typedef struct {
+  double vdw_cutoff, delta, gamma;          /* Halgren */
+  double elec_cutoff, alpha, electric;      /* multipoles, field, T */
+  double thole_a, tol_debye;
+  int64_t max_iter;
+  int exclude;                              /* 1-2/1-3 (intramolecular) scale 0 */
+  int terms;                                /* bit 0 vdW, 1 multipoles, 2 polarization */
+} mdg_amoeba_params;
+
+#define MDG_TERM_VDW 1
+#define MDG_TERM_MPOLE 2
+#define MDG_TERM_POLAR 4
+
+/* Config-1..4 step: Halgren vdW (list vdw_list, reduced sites) + permanent
+ * multipoles + permanent field + PCG induced dipoles (list elec_list).
+ * Results stay on the device. */
+int mdg_amoeba_step(mdg_ctx* ctx, int vdw_list, int elec_list, const mdg_amoeba_params* p);
+
+/* Results of the last step / kernel, copied to host (caller order).
+ * energies[4] = {vdw, coulomb or multipole, polarization (0 here), unused}. */
+int mdg_fetch_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz);
+int mdg_fetch_torques(mdg_ctx* ctx, double* tx, double* ty, double* tz);
+int mdg_fetch_dipoles(mdg_ctx* ctx, double* mux, double* muy, double* muz);
+int mdg_fetch_energies(mdg_ctx* ctx, double* energies4, double* virial9, int64_t* pcg_iters,
+                       double* pcg_rms);
+
+/* ---- instrumentation ---------------------------------------------------- */
+/* CUDA events on the context stream: start records, stop records, waits and
+ * returns the elapsed device milliseconds. */
+int mdg_timer_start(mdg_ctx* ctx);
+int mdg_timer_stop(mdg_ctx* ctx, double* ms);
+/* Counts kernel launches issued by this context since creation/reset. */
+int64_t mdg_launch_count(mdg_ctx* ctx);
+/* When enabled, every launch is bracketed by CUDA events on the context
+ * stream and accumulated per kernel name. */
+int mdg_profile_enable(mdg_ctx* ctx, int enable);
+int mdg_profile_reset(mdg_ctx* ctx);
+/* Writes "name count total_ms\n" lines into buf (NUL terminated). */
+int mdg_profile_report(mdg_ctx* ctx, char* buf, int64_t buf_len);
+
+/* FP64 DFMA-chain peak probe on `device` (TFLOP/s, best of 5). */
+int mdg_probe_fp64_peak(int device, double* tflops);
+/* Directed (both-direction) pairs of list_id within cutoff (minus excluded
+ * pairs when exclude != 0) and total list slots: roofline numerators. */
+int mdg_nlist_count_within(mdg_ctx* ctx, int list_id, double cutoff, int exclude,
+                           int64_t* directed_pairs, int64_t* list_slots);
+
+/* ---- synthetic water fixtures (BASELINE.json configs) -------------------- */
+/* n_mol rigid 3-site waters (O,H,H per molecule, molecule-major) in a cubic
+ * box of edge L, jittered lattice + uniform random orientation, std::
+ * mt19937_64(seed). Outputs (length 3*n_mol unless noted):
+ *   x,y,z (wrapped into [0,L)), molecule, charge, lj_sigma, lj_epsilon,
+ *   hal_r0, hal_epsilon, polarizability, hred_parent, hred_factor,
+ *   dipole[9*n_mol], quadrupole[18*n_mol].
+ * model: 0 = CHARMM-style (config 0), 1 = AMOEBA-style (configs 1-4). */
+int mdg_water_generate(int64_t n_mol, double box, uint64_t seed, int model, double* x,
+                       double* y, double* z, int32_t* molecule, double* charge,
+                       double* lj_sigma, double* lj_epsilon, double* hal_r0,
+                       double* hal_epsilon, double* polarizability, int32_t* hred_parent,
+                       double* hred_factor, double* dipole, double* quadrupole);
+/* Host helper: Halgren-reduced site coordinates, bit-identical to the
+ * device's (r_red = r_p + f*wrap1(r_i - r_p), re-wrapped into [0,L)). */
+int mdg_reduce_sites_host(int64_t n, double lx, double ly, double lz, const double* x,
+                          const double* y, const double* z, const int32_t* parent,
+                          const double* factor, double* xr, double* yr, double* zr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -531,3 +531,52 @@ class RefHandle:
             raise err
         self.ref._check(rc)
         return np.stack(m, 1)
+
+
+# ------------------------------------------------------------ CPU-baseline port
+def fast_port_path() -> str:
+    isa = ref_isa()
+    p = os.path.join(HERE, f"libmdo_fast_{isa}.so")
+    if not os.path.exists(p) or os.path.getmtime(p) < os.path.getmtime(os.path.join(HERE, "mdo_fast.c")):
+        subprocess.check_call(["make", "-s", "-C", HERE, "fast"])
+    return p
+
+
+class FastPort:
+    """mdo_fast.c: closed-form half-list CPU kernels (the CPU baseline's port leg)."""
+
+    def __init__(self, path: str | None = None):
+        self.lib = C.CDLL(path or fast_port_path())
+        L = self.lib
+        L.mdf_mpole.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double, C.c_double,
+                                C.c_double, C.c_int, _dp, _dp, _dp]
+        L.mdf_perm_field.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double,
+                                     C.c_double, C.c_double, C.c_int, _dp]
+        L.mdf_tmatvec.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double,
+                                  C.c_double, C.c_double, _dp, _dp]
+
+    def mpole(self, s, t, alpha, cutoff, electric=1.0, exclude=True, st=None, tt=None):
+        st = st or s.as_struct()
+        tt = tt or t.as_struct()
+        f = np.zeros((s.n, 3))
+        tq = np.zeros((s.n, 3))
+        e = C.c_double()
+        self.lib.mdf_mpole(C.byref(st), C.byref(tt), alpha, cutoff, electric, int(exclude),
+                           _ptr(f), _ptr(tq), C.byref(e))
+        return f, tq, e.value
+
+    def perm_field(self, s, t, alpha, cutoff, thole_a, exclude=True, st=None, tt=None):
+        st = st or s.as_struct()
+        tt = tt or t.as_struct()
+        e = np.zeros((s.n, 3))
+        self.lib.mdf_perm_field(C.byref(st), C.byref(tt), alpha, cutoff, thole_a, int(exclude),
+                                _ptr(e))
+        return e
+
+    def tmatvec(self, s, t, alpha, cutoff, thole_a, mu, st=None, tt=None):
+        st = st or s.as_struct()
+        tt = tt or t.as_struct()
+        mu = np.ascontiguousarray(mu, np.float64)
+        e = np.zeros((s.n, 3))
+        self.lib.mdf_tmatvec(C.byref(st), C.byref(tt), alpha, cutoff, thole_a, _ptr(mu), _ptr(e))
+        return e

@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) FP64 real-space pair engine: a drop-in for the
+reference mdvec hot path (neighbour lists, LJ / Ewald / Halgren pair kernels,
+Thole/Ewald polarization, real-space multipoles) behind a C ABI."""
+from .mdvec import (  # noqa: F401
+    CONFIGS, DEBYE, ELECTRIC, SITES_ATOMIC, SITES_VDW, AmoebaParams, CapacityError,
+    CharmmParams, ContractViolation, ConvergenceError, CudaError, Engine, EwaldRealParams,
+    FieldArrays, ForceAccumulator, HalgrenParams, LjParams, NeighborTable, ParticleSystem,
+    PolarizationState, PolarParams, SingularityError, load_library, reduce_sites_host,
+    water_box)

@@ -1,0 +1,804 @@
+// abi.cpp -- extern "C" boundary (include/mdg.h): validation with the
+// reference's contract checks and error taxonomy, host<->device staging,
+// spatial sort, list import/export in the reference NeighborTable layout,
+// and the fused steps. No kernels here; they live in the .cu files.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "mdg_internal.h"
+
+using mdg::throw_error;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MDG_OK;
+  } catch (const mdg::Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return MDG_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MDG_CUDA;
+  }
+}
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw_error(MDG_CONTRACT, msg);
+}
+
+void need_ctx(mdg_ctx* c) { need(c != nullptr, "null context"); }
+
+void need_system(mdg_ctx* c) {
+  need_ctx(c);
+  need(c->has_system, "no system uploaded");
+}
+
+template <class T>
+void dalloc(T** p, size_t count) {
+  MDG_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+}
+
+void set_device(mdg_ctx* c) { MDG_CUDA_CHECK(cudaSetDevice(c->device)); }
+
+mdg::DevList& need_list(mdg_ctx* c, int list_id) {
+  need(list_id >= 0 && list_id < MDG_MAX_LISTS, "list id out of range");
+  mdg::DevList& L = c->lists[list_id];
+  need(L.valid, "neighbour list not built");
+  return L;
+}
+
+// proj/src/kernels_impl.hpp:14-16
+void need_kernel_cutoff(const mdg::DevList& L, double cutoff) {
+  need(cutoff > 0 && cutoff <= L.cutoff,
+       "kernel: cutoff must be positive and within the list cutoff");
+}
+
+// Morton interleave of three 21-bit cell coordinates
+uint64_t spread3(uint64_t v) {
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+// Spatial order: Morton order over ~2 A cells, stable in the caller's index,
+// so every 32-site group (one warp) is a compact blob of space.
+void spatial_sort(mdg_ctx* c, const double* x, const double* y, const double* z) {
+  const int64_t n = c->n;
+  const int nx = std::max(1, (int)(c->lx / 2.0)), ny = std::max(1, (int)(c->ly / 2.0)),
+            nz = std::max(1, (int)(c->lz / 2.0));
+  std::vector<uint64_t> key(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int cx = std::min(nx - 1, (int)(x[i] / c->lx * nx));
+    const int cy = std::min(ny - 1, (int)(y[i] / c->ly * ny));
+    const int cz = std::min(nz - 1, (int)(z[i] / c->lz * nz));
+    key[i] = spread3(cx) | spread3(cy) << 1 | spread3(cz) << 2;
+  }
+  c->perm.resize(n);
+  std::iota(c->perm.begin(), c->perm.end(), 0);
+  std::stable_sort(c->perm.begin(), c->perm.end(),
+                   [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  c->iperm.resize(n);
+  for (int64_t s = 0; s < n; ++s) c->iperm[c->perm[s]] = (int32_t)s;
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_perm, c->perm.data(), n * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+}
+
+void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays) {
+  const int64_t n = c->n;
+  for (size_t a = 0; a < arrays.size(); ++a)
+    std::memcpy(c->h_stage + a * n, arrays[a], n * sizeof(double));
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+}
+
+// sorted double4 vector -> caller-order SoA host arrays (NULL entries skipped)
+void vec_out(mdg_ctx* c, const double4* v, double* ox, double* oy, double* oz) {
+  if (!ox && !oy && !oz) return;
+  const int64_t n = c->n;
+  mdg::gather_vec_to_caller(c, v, c->d_stage);
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_stage, c->d_stage, 3 * n * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+  MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (ox) std::memcpy(ox, c->h_stage, n * sizeof(double));
+  if (oy) std::memcpy(oy, c->h_stage + n, n * sizeof(double));
+  if (oz) std::memcpy(oz, c->h_stage + 2 * n, n * sizeof(double));
+}
+
+void vec_in(mdg_ctx* c, const double* ix, const double* iy, const double* iz, double4* v) {
+  stage_in(c, {ix, iy, iz});
+  mdg::scatter_vec_from_caller(c, c->d_stage, v);
+}
+
+void sym_virial(const double* s6, double* w9) {
+  // s6: xx xy xz yy yz zz
+  w9[0] = s6[0]; w9[1] = s6[1]; w9[2] = s6[2];
+  w9[3] = s6[1]; w9[4] = s6[3]; w9[5] = s6[4];
+  w9[6] = s6[2]; w9[7] = s6[4]; w9[8] = s6[5];
+}
+
+int64_t pad_count(int64_t n, int64_t m) { return (n + m - 1) & ~(m - 1); }
+
+}  // namespace
+
+extern "C" {
+
+const char* mdg_last_error(void) { return g_err.c_str(); }
+
+int mdg_version(void) { return 1; }
+
+int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pairs_per_atom) {
+  return guard([&] {
+    need(out != nullptr, "null output pointer");
+    need(n_capacity > 0 && n_capacity < (int64_t)1 << 30, "n_capacity out of range");
+    auto* c = new mdg_ctx();
+    *out = nullptr;
+    try {
+      c->device = device;
+      set_device(c);
+      c->n_cap = n_capacity;
+      c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
+      MDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      const size_t n = (size_t)n_capacity;
+      dalloc(&c->d_perm, n);
+      dalloc(&c->pos, n);
+      dalloc(&c->vsite, n);
+      dalloc(&c->vdwp, n);
+      dalloc(&c->polp, n);
+      dalloc(&c->mol, n);
+      dalloc(&c->hpar, n);
+      dalloc(&c->hfac, n);
+      dalloc(&c->child_start, n + 1);
+      dalloc(&c->child, n);
+      dalloc(&c->mp, 3 * n);
+      dalloc(&c->cell_of, n);
+      dalloc(&c->cell_atoms, n);
+      dalloc(&c->d_flag, 8);
+      for (double4** v : {&c->force, &c->force2, &c->torque, &c->field, &c->eperm, &c->mu,
+                          &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q, &c->vin})
+        dalloc(v, n);
+      dalloc(&c->results, 64);
+      MDG_CUDA_CHECK(cudaMemset(c->results, 0, 64 * sizeof(double)));
+      MDG_CUDA_CHECK(cudaMallocHost(&c->h_results, 64 * sizeof(double)));
+      c->stage_bytes = 12 * n * sizeof(double);
+      MDG_CUDA_CHECK(cudaMallocHost(&c->h_stage, c->stage_bytes));
+      dalloc(&c->d_stage, 12 * n);
+      mdg::ensure_partials(c, mdg::grid_for(n_capacity));
+    } catch (...) {
+      mdg_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int mdg_ctx_destroy(mdg_ctx* c) {
+  if (!c) return MDG_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ptrs[] = {c->d_perm, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
+                  c->child_start, c->child, c->mp, c->cell_of, c->cell_start, c->cell_fill,
+                  c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
+                  c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->partials, c->results,
+                  c->d_stage};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& L : c->lists) {
+    if (L.nbr) cudaFree(L.nbr);
+    if (L.cnt) cudaFree(L.cnt);
+  }
+  if (c->h_results) cudaFreeHost(c->h_results);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (auto& pe : c->pending) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->timer_a) cudaEventDestroy(c->timer_a);
+  if (c->timer_b) cudaEventDestroy(c->timer_b);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return MDG_OK;
+}
+
+int mdg_ctx_synchronize(mdg_ctx* c) {
+  return guard([&] {
+    need_ctx(c);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+void* mdg_ctx_stream(mdg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int mdg_system_upload(mdg_ctx* c, int64_t n, double lx, double ly, double lz, const double* x,
+                      const double* y, const double* z, const double* charge,
+                      const double* lj_sigma, const double* lj_epsilon, const double* hal_r0,
+                      const double* hal_epsilon, const double* polarizability) {
+  return guard([&] {
+    need_ctx(c);
+    set_device(c);
+    // OrthorhombicBox::validate (proj/include/mdvec/pbc.hpp:14-19)
+    need(lx > 0 && ly > 0 && lz > 0 && std::isfinite(lx) && std::isfinite(ly) &&
+             std::isfinite(lz),
+         "OrthorhombicBox: edges must be positive and finite");
+    need(n >= 1 && n <= c->n_cap, "ParticleSystem: site count outside the context capacity");
+    need(x && y && z && charge && lj_sigma && lj_epsilon && hal_r0 && hal_epsilon &&
+             polarizability,
+         "ParticleSystem: null array");
+    // proj/src/system.cpp:18-27
+    const double L[3] = {lx, ly, lz};
+    const double* p[3] = {x, y, z};
+    for (int a = 0; a < 3; ++a)
+      for (int64_t i = 0; i < n; ++i)
+        need(p[a][i] >= 0.0 && p[a][i] < L[a], "ParticleSystem: position outside the box");
+    c->n = n;
+    c->lx = lx;
+    c->ly = ly;
+    c->lz = lz;
+    for (auto& Lst : c->lists) Lst.valid = false;
+    c->has_mpoles = c->has_hred = c->has_mol = false;
+    spatial_sort(c, x, y, z);
+    stage_in(c, {x, y, z, charge, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, polarizability});
+    mdg::pack_system(c);
+    // identity topology: every site its own group, no reduction
+    std::vector<int32_t> ident(n);
+    std::iota(ident.begin(), ident.end(), 0);
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->mol, ident.data(), n * 4, cudaMemcpyHostToDevice,
+                                   c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->hpar, ident.data(), n * 4, cudaMemcpyHostToDevice,
+                                   c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->mp, 0, 3 * n * sizeof(double4), c->stream));
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->has_system = true;
+  });
+}
+
+int mdg_positions_upload(mdg_ctx* c, const double* x, const double* y, const double* z) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(x && y && z, "null position array");
+    const double L[3] = {c->lx, c->ly, c->lz};
+    const double* p[3] = {x, y, z};
+    for (int a = 0; a < 3; ++a)
+      for (int64_t i = 0; i < c->n; ++i)
+        need(p[a][i] >= 0.0 && p[a][i] < L[a], "ParticleSystem: position outside the box");
+    stage_in(c, {x, y, z});
+    mdg::pack_positions(c);
+  });
+}
+
+int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred_parent,
+                        const double* hred_factor) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    const int64_t n = c->n;
+    std::vector<int32_t> mol(n), par(n);
+    std::vector<double> fac(n, 1.0);
+    for (int64_t s = 0; s < n; ++s) {
+      const int32_t o = c->perm[s];
+      mol[s] = molecule ? molecule[o] : o;
+      if (hred_parent) {
+        const int32_t po = hred_parent[o];
+        need(po >= 0 && po < n, "topology: reduction parent out of range");
+        par[s] = c->iperm[po];
+        fac[s] = hred_factor ? hred_factor[o] : 1.0;
+      } else {
+        par[s] = (int32_t)s;
+      }
+    }
+    // children CSR (sorted indices) for the chain rule; a parent must be its own parent
+    std::vector<int32_t> start(n + 1, 0), child;
+    for (int64_t s = 0; s < n; ++s)
+      if (par[s] != s) {
+        need(par[par[s]] == par[s], "topology: reduction parents must not be reduced");
+        start[par[s] + 1]++;
+      }
+    for (int64_t s = 0; s < n; ++s) start[s + 1] += start[s];
+    child.resize(std::max<int32_t>(start[n], 1));
+    std::vector<int32_t> fill(start.begin(), start.end() - 1);
+    for (int64_t s = 0; s < n; ++s)
+      if (par[s] != s) child[fill[par[s]]++] = (int32_t)s;
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->mol, mol.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->hpar, par.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->hfac, fac.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->child_start, start.data(), (n + 1) * 4,
+                                   cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->child, child.data(), child.size() * 4,
+                                   cudaMemcpyHostToDevice, c->stream));
+    c->has_mol = molecule != nullptr;
+    c->has_hred = hred_parent != nullptr;
+    if (c->has_hred) mdg::run_reduce_sites(c);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int mdg_multipoles_upload(mdg_ctx* c, const double* dipole, const double* quadrupole) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    const int64_t n = c->n;
+    std::vector<double> mp(12 * n, 0.0);
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t o = c->perm[s];
+      double* m = &mp[12 * s];
+      if (dipole) {
+        m[0] = dipole[3 * o];
+        m[1] = dipole[3 * o + 1];
+        m[2] = dipole[3 * o + 2];
+      }
+      if (quadrupole) {
+        const double* q = quadrupole + 6 * o;
+        m[3] = q[0];  // xx
+        m[4] = q[1];  // xy
+        m[5] = q[2];  // xz
+        m[6] = q[3];  // yy
+        m[7] = q[4];  // yz
+        m[8] = q[5];  // zz
+      }
+    }
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->mp, mp.data(), 12 * n * sizeof(double),
+                                   cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->has_mpoles = dipole != nullptr || quadrupole != nullptr;
+  });
+}
+
+int mdg_nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(list_id >= 0 && list_id < MDG_MAX_LISTS, "list id out of range");
+    need(sites == MDG_SITES_ATOMIC || sites == MDG_SITES_VDW, "unknown site kind");
+    // proj/src/neighbors.cpp:12-17
+    need(list_cutoff > 0 && std::isfinite(list_cutoff), "build_cell_grid: cutoff must be positive");
+    need(list_cutoff <= 0.5 * std::min(c->lx, std::min(c->ly, c->lz)),
+         "build_cell_grid: cutoff exceeds half the smallest box edge");
+    mdg::nlist_build(c, list_id, list_cutoff, sites);
+  });
+}
+
+int mdg_nlist_size(mdg_ctx* c, int list_id, int64_t* half_pairs, int64_t* padded_slots) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    if (half_pairs) *half_pairs = L.half_pairs;
+    if (padded_slots) {
+      std::vector<int32_t> cnt(c->n), nbr(L.nbr_elems);
+      MDG_CUDA_CHECK(cudaMemcpy(cnt.data(), L.cnt, c->n * 4, cudaMemcpyDeviceToHost));
+      MDG_CUDA_CHECK(cudaMemcpy(nbr.data(), L.nbr, ((c->n + 31) / 32) * (size_t)L.cap * 32 * 4,
+                                cudaMemcpyDeviceToHost));
+      std::vector<int64_t> upper(c->n, 0);
+      for (int64_t s = 0; s < c->n; ++s) {
+        const int32_t o = c->perm[s];
+        const int32_t* row = nbr.data() + (size_t)(s >> 5) * L.cap * 32 + (s & 31);
+        for (int32_t k = 0; k < cnt[s]; ++k)
+          if (c->perm[row[(size_t)k * 32]] > o) upper[o]++;
+      }
+      int64_t tot = 0;
+      for (int64_t i = 0; i < c->n; ++i) tot += pad_count(upper[i], 16);
+      *padded_slots = tot;
+    }
+  });
+}
+
+int mdg_nlist_export(mdg_ctx* c, int list_id, uint32_t* nnvlst, uint32_t* nvloop8,
+                     uint32_t* nvloop16, uint64_t* offset, int32_t* indices,
+                     int64_t indices_cap) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    const int64_t n = c->n;
+    std::vector<int32_t> cnt(n), nbr(((n + 31) / 32) * (size_t)L.cap * 32);
+    MDG_CUDA_CHECK(cudaMemcpy(cnt.data(), L.cnt, n * 4, cudaMemcpyDeviceToHost));
+    MDG_CUDA_CHECK(cudaMemcpy(nbr.data(), L.nbr, nbr.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<std::vector<int32_t>> rows(n);
+    for (int64_t s = 0; s < n; ++s) {
+      const int32_t o = c->perm[s];
+      const int32_t* row = nbr.data() + (size_t)(s >> 5) * L.cap * 32 + (s & 31);
+      for (int32_t k = 0; k < cnt[s]; ++k) {
+        const int32_t jo = c->perm[row[(size_t)k * 32]];
+        if (jo > o) rows[o].push_back(jo);
+      }
+    }
+    int64_t pos = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      auto& r = rows[i];
+      std::sort(r.begin(), r.end());
+      if ((int64_t)r.size() > MDG_MAX_NEIGHBORS)
+        throw_error(MDG_CAPACITY, "neighbor table: site " + std::to_string(i) +
+                                      " exceeds the per-site neighbor capacity");
+      const int64_t k = (int64_t)r.size(), p16 = pad_count(k, 16);
+      if (nnvlst) nnvlst[i] = (uint32_t)k;
+      if (nvloop8) nvloop8[i] = (uint32_t)pad_count(k, 8);
+      if (nvloop16) nvloop16[i] = (uint32_t)p16;
+      if (offset) offset[i] = (uint64_t)pos;
+      if (indices) {
+        need(pos + p16 <= indices_cap, "nlist_export: indices capacity too small");
+        const int32_t sentinel = k ? r.back() : 0;
+        for (int64_t q = 0; q < p16; ++q) indices[pos + q] = q < k ? r[q] : sentinel;
+      }
+      pos += p16;
+    }
+  });
+}
+
+int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
+                     const uint32_t* nnvlst, const uint64_t* offset, const int32_t* indices) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(list_id >= 0 && list_id < MDG_MAX_LISTS, "list id out of range");
+    need(nnvlst && offset && indices, "nlist_import: null array");
+    need(list_cutoff > 0, "nlist_import: cutoff must be positive");
+    const int64_t n = c->n;
+    std::vector<std::vector<int32_t>> rows(n);
+    for (int64_t i = 0; i < n; ++i)
+      for (uint32_t k = 0; k < nnvlst[i]; ++k) {
+        const int32_t j = indices[offset[i] + k];
+        need(j >= 0 && j < n && j != i, "nlist_import: neighbour index out of range");
+        rows[c->iperm[i]].push_back(c->iperm[j]);
+        rows[c->iperm[j]].push_back((int32_t)c->iperm[i]);
+      }
+    int32_t mx = 0;
+    for (auto& r : rows) {
+      std::sort(r.begin(), r.end());
+      mx = std::max<int32_t>(mx, (int32_t)r.size());
+    }
+    need(mx <= c->max_pairs, "nlist_import: a site exceeds the context's pair capacity");
+    mdg::DevList& L = c->lists[list_id];
+    const int32_t cap = std::max<int32_t>(8, (mx + 7) & ~7);
+    const size_t groups = (n + 31) / 32;
+    const size_t need_el = groups * (size_t)cap * 32;
+    if (need_el > L.nbr_elems) {
+      if (L.nbr) cudaFree(L.nbr);
+      L.nbr = nullptr;
+      MDG_CUDA_CHECK(cudaMalloc(&L.nbr, need_el * 4));
+      L.nbr_elems = need_el;
+    }
+    if (!L.cnt) MDG_CUDA_CHECK(cudaMalloc(&L.cnt, (size_t)c->n_cap * 4));
+    std::vector<int32_t> ell(need_el, 0), cnt(n);
+    int64_t sum = 0;
+    for (int64_t s = 0; s < n; ++s) {
+      cnt[s] = (int32_t)rows[s].size();
+      sum += cnt[s];
+      for (size_t k = 0; k < rows[s].size(); ++k)
+        ell[((size_t)(s >> 5) * cap + k) * 32 + (s & 31)] = rows[s][k];
+    }
+    MDG_CUDA_CHECK(cudaMemcpy(L.nbr, ell.data(), need_el * 4, cudaMemcpyHostToDevice));
+    MDG_CUDA_CHECK(cudaMemcpy(L.cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice));
+    L.cap = cap;
+    L.valid = true;
+    L.cutoff = list_cutoff;
+    L.sites = sites;
+    L.max_cnt = mx;
+    L.half_pairs = sum / 2;
+  });
+}
+
+// ---- kernels -----------------------------------------------------------------
+
+static void nonpolar_call(mdg_ctx* c, int list_id, const mdg::NonpolarArgs& a, double* fx,
+                          double* fy, double* fz, double* energy, double* virial9) {
+  need_system(c);
+  set_device(c);
+  mdg::DevList& L = need_list(c, list_id);
+  need_kernel_cutoff(L, a.cutoff);
+  mdg::run_nonpolar(c, list_id, a);
+  vec_out(c, c->force, fx, fy, fz);
+  mdg::fetch_results(c);
+  if (energy) *energy = a.do_lj ? c->h_results[0] : c->h_results[1];
+  if (virial9) sym_virial(c->h_results + 2, virial9);
+}
+
+int mdg_lj_forces(mdg_ctx* c, int list_id, double cutoff, int shift, int exclude, double* fx,
+                  double* fy, double* fz, double* energy, double* virial9) {
+  return guard([&] {
+    mdg::NonpolarArgs a{1, 0, shift, exclude, cutoff, 0.0, 1.0};
+    nonpolar_call(c, list_id, a, fx, fy, fz, energy, virial9);
+  });
+}
+
+int mdg_ewald_real_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
+                          int exclude, double* fx, double* fy, double* fz, double* energy,
+                          double* virial9) {
+  return guard([&] {
+    need(alpha >= 0, "ewald: alpha must be nonnegative");  // kernels_scalar.cpp:58
+    mdg::NonpolarArgs a{0, 1, 0, exclude, cutoff, alpha, electric};
+    nonpolar_call(c, list_id, a, fx, fy, fz, energy, virial9);
+  });
+}
+
+int mdg_halgren_forces(mdg_ctx* c, int list_id, double cutoff, double delta, double gamma,
+                       int exclude, double* fx, double* fy, double* fz, double* energy,
+                       double* virial9) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    mdg::run_halgren(c, list_id, cutoff, delta, gamma, exclude);
+    vec_out(c, c->force, fx, fy, fz);
+    mdg::fetch_results(c);
+    if (energy) *energy = c->h_results[0];
+    if (virial9) sym_virial(c->h_results + 2, virial9);
+  });
+}
+
+int mdg_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                const double* mux, const double* muy, const double* muz, double* ex,
+                double* ey, double* ez) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    need(alpha >= 0, "tmatvec: alpha must be nonnegative");
+    need(mux && muy && muz, "dipole_field_matvec: dipole array size mismatch");
+    need(L.sites == MDG_SITES_ATOMIC, "tmatvec needs a list over atomic sites");
+    vec_in(c, mux, muy, muz, c->vin);
+    mdg::run_tmatvec(c, list_id, alpha, cutoff, thole_a, c->vin, c->field);
+    vec_out(c, c->field, ex, ey, ez);
+  });
+}
+
+int mdg_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                   int exclude, double* ex, double* ey, double* ez) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    need(alpha >= 0, "perm_field: alpha must be nonnegative");
+    need(L.sites == MDG_SITES_ATOMIC, "perm_field needs a list over atomic sites");
+    mdg::run_perm_field(c, list_id, alpha, cutoff, thole_a, exclude, c->field);
+    vec_out(c, c->field, ex, ey, ez);
+  });
+}
+
+int mdg_polar_solve_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, double tol,
+                           int64_t max_iter, double* mux, double* muy, double* muz,
+                           int64_t* iters, double* last_residual) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    // proj/src/polar_scalar.cpp:165-166
+    need(tol > 0, "jacobi_polarization_solve: tol must be positive");
+    need(max_iter >= 1, "jacobi_polarization_solve: max_iter must be >= 1");
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    mdg::run_perm_field(c, list_id, 0.0, cutoff, thole_a, 0, c->eperm);
+    double resid = 0;
+    try {
+      const int64_t it = mdg::run_jacobi(c, list_id, cutoff, thole_a, tol, max_iter, &resid);
+      if (iters) *iters = it;
+    } catch (const mdg::Error&) {
+      if (last_residual) *last_residual = resid;
+      if (iters) *iters = max_iter;
+      throw;
+    }
+    if (last_residual) *last_residual = resid;
+    vec_out(c, c->mu, mux, muy, muz);
+  });
+}
+
+int mdg_polar_solve_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                        int exclude_perm, double tol_debye, int64_t max_iter, double* mux,
+                        double* muy, double* muz, int64_t* iters, double* last_rms_debye) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(tol_debye > 0, "pcg: tol must be positive");
+    need(max_iter >= 1, "pcg: max_iter must be >= 1");
+    need(alpha >= 0, "pcg: alpha must be nonnegative");
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    mdg::run_perm_field(c, list_id, alpha, cutoff, thole_a, exclude_perm, c->eperm);
+    double rms = 0;
+    try {
+      const int64_t it = mdg::run_pcg(c, list_id, alpha, cutoff, thole_a, tol_debye, max_iter,
+                                      &rms);
+      if (iters) *iters = it;
+    } catch (const mdg::Error&) {
+      if (last_rms_debye) *last_rms_debye = rms;
+      if (iters) *iters = max_iter;
+      throw;
+    }
+    if (last_rms_debye) *last_rms_debye = rms;
+    vec_out(c, c->mu, mux, muy, muz);
+  });
+}
+
+int mdg_mpole_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
+                     int exclude, double* fx, double* fy, double* fz, double* tx, double* ty,
+                     double* tz, double* energy, double* virial9) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    need(alpha >= 0, "mpole: alpha must be nonnegative");
+    need(L.sites == MDG_SITES_ATOMIC, "mpole needs a list over atomic sites");
+    mdg::run_mpole(c, list_id, alpha, cutoff, electric, exclude, false);
+    vec_out(c, c->force, fx, fy, fz);
+    vec_out(c, c->torque, tx, ty, tz);
+    mdg::fetch_results(c);
+    if (energy) *energy = c->h_results[10];
+    if (virial9) std::memcpy(virial9, c->h_results + 11, 9 * sizeof(double));
+  });
+}
+
+// ---- fused steps ---------------------------------------------------------------
+
+int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
+  return guard([&] {
+    need_system(c);
+    need(p != nullptr, "null params");
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, p->cutoff);
+    need(L.sites == MDG_SITES_ATOMIC, "charmm step needs a list over atomic sites");
+    mdg::NonpolarArgs a{1, 1, p->shift, p->exclude, p->cutoff, p->alpha, p->electric};
+    mdg::run_nonpolar(c, list_id, a);
+    c->pcg_iters = 0;
+  });
+}
+
+int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  return guard([&] {
+    need_system(c);
+    need(p != nullptr, "null params");
+    mdg::DevList& Lv = need_list(c, vdw_list);
+    mdg::DevList& Le = need_list(c, elec_list);
+    need_kernel_cutoff(Lv, p->vdw_cutoff);
+    need_kernel_cutoff(Le, p->elec_cutoff);
+    need(Le.sites == MDG_SITES_ATOMIC, "electrostatics need a list over atomic sites");
+    const int terms = p->terms ? p->terms : (MDG_TERM_VDW | MDG_TERM_MPOLE | MDG_TERM_POLAR);
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 48 * sizeof(double), c->stream));
+    if (terms & MDG_TERM_VDW) {
+      mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
+    } else {
+      mdg::zero_vec(c, c->force);
+    }
+    if (terms & MDG_TERM_MPOLE) {
+      mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
+    } else {
+      mdg::zero_vec(c, c->torque);
+    }
+    c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
+    c->pcg_rms = 0;
+    if (terms & MDG_TERM_POLAR) {
+      mdg::run_perm_field(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude,
+                          c->eperm);
+      double rms = 0;
+      c->pcg_iters = mdg::run_pcg(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a,
+                                  p->tol_debye, p->max_iter, &rms);
+      c->pcg_rms = rms;
+      mdg::polar_energy(c, p->electric, 40);
+    }
+  });
+}
+
+int mdg_timer_start(mdg_ctx* c) {
+  return guard([&] {
+    need_ctx(c);
+    set_device(c);
+    if (!c->timer_a) {
+      MDG_CUDA_CHECK(cudaEventCreate(&c->timer_a));
+      MDG_CUDA_CHECK(cudaEventCreate(&c->timer_b));
+    }
+    MDG_CUDA_CHECK(cudaEventRecord(c->timer_a, c->stream));
+  });
+}
+
+int mdg_timer_stop(mdg_ctx* c, double* ms) {
+  return guard([&] {
+    need_ctx(c);
+    need(c->timer_a != nullptr, "timer not started");
+    MDG_CUDA_CHECK(cudaEventRecord(c->timer_b, c->stream));
+    MDG_CUDA_CHECK(cudaEventSynchronize(c->timer_b));
+    float f = 0;
+    MDG_CUDA_CHECK(cudaEventElapsedTime(&f, c->timer_a, c->timer_b));
+    if (ms) *ms = f;
+  });
+}
+
+int mdg_fetch_forces(mdg_ctx* c, double* fx, double* fy, double* fz) {
+  return guard([&] {
+    need_system(c);
+    vec_out(c, c->force, fx, fy, fz);
+  });
+}
+
+int mdg_fetch_torques(mdg_ctx* c, double* tx, double* ty, double* tz) {
+  return guard([&] {
+    need_system(c);
+    vec_out(c, c->torque, tx, ty, tz);
+  });
+}
+
+int mdg_fetch_dipoles(mdg_ctx* c, double* mux, double* muy, double* muz) {
+  return guard([&] {
+    need_system(c);
+    vec_out(c, c->mu, mux, muy, muz);
+  });
+}
+
+// energies: {vdw (lj or halgren), coulomb/multipole, polarization, 0}
+int mdg_fetch_energies(mdg_ctx* c, double* energies4, double* virial9, int64_t* pcg_iters,
+                       double* pcg_rms) {
+  return guard([&] {
+    need_system(c);
+    mdg::fetch_results(c);
+    const double* r = c->h_results;
+    double w[9];
+    sym_virial(r + 2, w);
+    const bool amoeba = c->pcg_iters != 0;
+    if (energies4) {
+      energies4[0] = r[0];
+      energies4[1] = amoeba ? r[10] : r[1];
+      energies4[2] = amoeba ? r[40] : 0.0;
+      energies4[3] = 0.0;
+    }
+    if (virial9) {
+      for (int k = 0; k < 9; ++k) virial9[k] = w[k] + (amoeba ? r[11 + k] : 0.0);
+    }
+    if (pcg_iters) *pcg_iters = c->pcg_iters > 0 ? c->pcg_iters : 0;
+    if (pcg_rms) *pcg_rms = c->pcg_rms;
+  });
+}
+
+int64_t mdg_launch_count(mdg_ctx* c) { return c ? c->launches : 0; }
+
+int mdg_profile_enable(mdg_ctx* c, int enable) {
+  return guard([&] {
+    need_ctx(c);
+    mdg::flush_profile(c);
+    c->profile = enable != 0;
+  });
+}
+
+int mdg_profile_reset(mdg_ctx* c) {
+  return guard([&] {
+    need_ctx(c);
+    mdg::flush_profile(c);
+    c->prof.clear();
+  });
+}
+
+int mdg_profile_report(mdg_ctx* c, char* buf, int64_t buf_len) {
+  return guard([&] {
+    need_ctx(c);
+    need(buf && buf_len > 0, "null buffer");
+    mdg::flush_profile(c);
+    std::string s;
+    char line[256];
+    for (auto& kv : c->prof) {
+      snprintf(line, sizeof line, "%s %lld %.6f\n", kv.first.c_str(),
+               (long long)kv.second.count, kv.second.ms);
+      s += line;
+    }
+    need((int64_t)s.size() < buf_len, "profile report buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// common.cuh -- device helpers shared by every pair kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mdg_internal.h"
+
+namespace mdg {
+
+// proj/include/mdvec/pbc.hpp:27-31, op for op: DMUL, FRND (round-half-even
+// = nearbyint), DFMA, DSETP, DADD. The explicit _rn intrinsics forbid
+// contraction so pair membership is bit-identical to the reference.
+__device__ __forceinline__ double wrap1(double d, double L, double invL, double halfL) {
+  const double t = __fma_rn(-rint(__dmul_rn(d, invL)), L, d);
+  return (t >= halfL) ? __dsub_rn(t, L) : t;
+}
+
+// proj/include/mdvec/pbc.hpp:35-37
+__device__ __forceinline__ double dist2(double dx, double dy, double dz) {
+  return __fma_rn(dx, dx, __fma_rn(dy, dy, __dmul_rn(dz, dz)));
+}
+
+// d = r_i - r_j, minimum image; returns r2
+__device__ __forceinline__ double min_image(const Box& b, double xi, double yi, double zi,
+                                            double xj, double yj, double zj, double& dx,
+                                            double& dy, double& dz) {
+  dx = wrap1(__dsub_rn(xi, xj), b.lx, b.ix, b.hx);
+  dy = wrap1(__dsub_rn(yi, yj), b.ly, b.iy, b.hy);
+  dz = wrap1(__dsub_rn(zi, zj), b.lz, b.iz, b.hz);
+  return dist2(dx, dy, dz);
+}
+
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  double4 v;
+  const double2* q = reinterpret_cast<const double2*>(p);
+  double2 a = __ldg(q), b = __ldg(q + 1);
+  v.x = a.x; v.y = a.y; v.z = b.x; v.w = b.y;
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of NV values into partials[blockIdx.x][*].
+// Block size must be kBlock (4 warps).
+template <int NV>
+__device__ __forceinline__ void block_store_partials(double (&v)[NV], double* partials) {
+  __shared__ double red[kBlock / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double s = warp_sum(v[k]);
+    if (lane == 0) red[warp][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kBlock / 32; ++w) s += red[w][threadIdx.x];
+    partials[(size_t)blockIdx.x * kRedVals + threadIdx.x] = s;
+  }
+}
+
+// Thole factors (proj/include/mdvec/polar.hpp:55-62) with per-site
+// pdamp = alpha^(1/6): u = r/(pd_i pd_j). l7 for the quadrupole field.
+__device__ __forceinline__ void thole3(double r, double pdij, double a, double& l3, double& l5) {
+  const double u = r / pdij;
+  const double au3 = a * u * u * u;
+  const double ex = exp(-au3);
+  l3 = 1.0 - ex;
+  l5 = 1.0 - (1.0 + au3) * ex;
+}
+
+__device__ __forceinline__ void thole7(double r, double pdij, double a, double& l3, double& l5,
+                                       double& l7) {
+  const double u = r / pdij;
+  const double au3 = a * u * u * u;
+  const double ex = exp(-au3);
+  l3 = 1.0 - ex;
+  l5 = 1.0 - (1.0 + au3) * ex;
+  l7 = 1.0 - (1.0 + au3 + 0.6 * au3 * au3) * ex;
+}
+
+// Tinker bn recursion for real-space Ewald: B0 = erfc(ar)/r,
+// Bn = ((2n-1) B(n-1) + (2a^2)^n/(a sqrt(pi)) exp(-a^2 r^2)) / r^2.
+template <int NMAX>
+__device__ __forceinline__ void ewald_bn(double r, double r2, double inv_r2, double alpha,
+                                         double (&bn)[NMAX + 1]) {
+  const double ralpha = alpha * r;
+  bn[0] = erfc(ralpha) / r;
+  const double alsq2 = 2.0 * alpha * alpha;
+  double alsq2n = (alpha > 0) ? 1.0 / (1.7724538509055160273 * alpha) : 0.0;
+  const double exp2a = exp(-ralpha * ralpha);
+#pragma unroll
+  for (int k = 1; k <= NMAX; ++k) {
+    alsq2n *= alsq2;
+    bn[k] = ((double)(2 * k - 1) * bn[k - 1] + alsq2n * exp2a) * inv_r2;
+  }
+}
+
+struct ListView {
+  const int32_t* nbr;
+  const int32_t* cnt;
+  int32_t cap;
+};
+
+__device__ __forceinline__ const int32_t* list_row(const ListView& L, int i) {
+  return L.nbr + (size_t)(i >> 5) * (size_t)L.cap * 32 + (i & 31);
+}
+
+}  // namespace mdg

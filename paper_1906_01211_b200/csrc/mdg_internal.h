@@ -1,0 +1,214 @@
+// mdg_internal.h -- context, device layout and shared device helpers.
+//
+// Device data layout (HBM, all in the context's spatially sorted order):
+//   pos    double4[n]   x, y, z, charge                 (32 B, one sector)
+//   vsite  double4[n]   Halgren-reduced x, y, z, 0       (vdW lists)
+//   vdwp   double4[n]   lj_sigma, sqrt(lj_eps), hal_r0, sqrt(hal_eps)
+//   polp   double2[n]   polarizability, polarizability^(1/6)
+//   mol    int32[n]     exclusion group
+//   mp     double4[3n]  (mux,muy,muz,Qxx) (Qxy,Qxz,Qyy,Qyz) (Qzz,0,0,0)
+//   lists  sliced ELL:  nbr[(g*cap + k)*32 + lane] = j for site i = 32 g + lane,
+//                       cnt[i] neighbours (both directions) within the list cutoff
+//   vectors (forces, fields, dipoles, CG) double4[n], w unused.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/mdg.h"
+
+namespace mdg {
+
+constexpr int kBlock = 128;      // pair-kernel block: 4 warps = 4 site groups
+constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
+constexpr int kMaxBlocksRed = 1 << 20;
+
+struct Box {
+  double lx, ly, lz, ix, iy, iz, hx, hy, hz;
+};
+
+inline Box make_box(double lx, double ly, double lz) {
+  // host-computed reciprocals and halves, as proj/src/kernels_scalar.cpp:16-17
+  return Box{lx, ly, lz, 1.0 / lx, 1.0 / ly, 1.0 / lz, 0.5 * lx, 0.5 * ly, 0.5 * lz};
+}
+
+struct Grid {
+  int ncx, ncy, ncz;
+  double ex, ey, ez;
+};
+
+struct DevList {
+  bool valid = false;
+  double cutoff = 0;
+  int sites = 0;
+  int32_t cap = 0;              // ELL width (slots per site)
+  int32_t* nbr = nullptr;
+  int32_t* cnt = nullptr;
+  size_t nbr_elems = 0;
+  int64_t half_pairs = 0;
+  int32_t max_cnt = 0;
+};
+
+struct ProfEntry {
+  int64_t count = 0;
+  double ms = 0;
+};
+
+struct PendingEvent {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+}  // namespace mdg
+
+struct mdg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_cap = 0;
+  int32_t max_pairs = 0;
+
+  // system
+  int64_t n = 0;
+  double lx = 0, ly = 0, lz = 0;
+  bool has_system = false, has_mpoles = false, has_hred = false, has_mol = false;
+  std::vector<int32_t> perm;   // sorted -> caller index
+  std::vector<int32_t> iperm;  // caller -> sorted index
+
+  // device arrays (sorted order)
+  int32_t* d_perm = nullptr;
+  double4* pos = nullptr;
+  double4* vsite = nullptr;
+  double4* vdwp = nullptr;
+  double2* polp = nullptr;
+  int32_t* mol = nullptr;
+  int32_t* hpar = nullptr;
+  double* hfac = nullptr;
+  int32_t* child_start = nullptr;  // CSR of Halgren children per parent
+  int32_t* child = nullptr;
+  double4* mp = nullptr;
+
+  // cell grid scratch
+  int32_t* cell_of = nullptr;
+  int32_t* cell_start = nullptr;
+  int32_t* cell_fill = nullptr;
+  int32_t* cell_atoms = nullptr;
+  int64_t cell_cap = 0;
+  int32_t* d_flag = nullptr;  // device error/overflow flags [8]
+
+  // vectors
+  double4* force = nullptr;
+  double4* force2 = nullptr;
+  double4* torque = nullptr;
+  double4* field = nullptr;
+  double4* eperm = nullptr;
+  double4* mu = nullptr;
+  double4* cg_r = nullptr;
+  double4* cg_z = nullptr;
+  double4* cg_p = nullptr;
+  double4* cg_q = nullptr;
+  double4* vin = nullptr;  // generic input vector (dipoles for tmatvec)
+
+  // reductions
+  double* partials = nullptr;
+  int64_t partial_blocks = 0;
+  double* results = nullptr;    // device result slots
+  double* h_results = nullptr;  // pinned mirror
+
+  // staging
+  double* h_stage = nullptr;
+  double* d_stage = nullptr;
+  size_t stage_bytes = 0;
+
+  mdg::DevList lists[MDG_MAX_LISTS];
+
+  // last step
+  double energies[4] = {0, 0, 0, 0};
+  double virial[9] = {0};
+  int64_t pcg_iters = 0;
+  double pcg_rms = 0;
+
+  // instrumentation
+  int64_t launches = 0;
+  bool profile = false;
+  std::map<std::string, mdg::ProfEntry> prof;
+  std::vector<mdg::PendingEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+};
+
+namespace mdg {
+
+// ---- error handling -----------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void throw_error(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define MDG_CUDA_CHECK(x) ::mdg::cuda_check((x), #x)
+
+// ---- launch bookkeeping -------------------------------------------------
+void launch_begin(mdg_ctx* c, const char* name);
+void launch_end(mdg_ctx* c, const char* name);
+void flush_profile(mdg_ctx* c);
+
+#define MDG_LAUNCH(ctx, name, grid, block, smem, kernel, ...)                  \
+  do {                                                                         \
+    ::mdg::launch_begin((ctx), (name));                                        \
+    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);           \
+    ::mdg::launch_end((ctx), (name));                                          \
+  } while (0)
+
+inline unsigned grid_for(int64_t n, int block = kBlock) {
+  return (unsigned)((n + block - 1) / block);
+}
+
+// ---- host entry points implemented in the .cu files -----------------------
+void ensure_partials(mdg_ctx* c, int64_t blocks);
+// Sum per-block partials [blocks][kRedVals] in fixed order into
+// results[slot .. slot+nvals), scaled by `scale`.
+void finalize_partials(mdg_ctx* c, int64_t blocks, int nvals, int slot, double scale);
+void fetch_results(mdg_ctx* c);
+
+void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites);
+
+struct NonpolarArgs {
+  int do_lj, do_coul, shift, exclude;
+  double cutoff, alpha, electric;
+};
+// Writes c->force (sorted), energies into results[0] (lj) and results[1]
+// (coulomb), virial into results[2..10].
+void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a);
+// Halgren on list (atomic or reduced sites); writes c->force (atoms),
+// results[0] energy, results[2..10] virial.
+void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double gamma,
+                 int exclude);
+// E = T v (c->vin -> out), alpha >= 0.
+void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                 const double4* in, double4* out);
+void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                    int exclude, double4* out);
+// Returns iterations; throws CONVERGENCE (with last_rms set) on failure.
+int64_t run_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                double tol_debye, int64_t max_iter, double* last_rms);
+int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, double tol,
+                   int64_t max_iter, double* last_resid);
+void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
+               int exclude, bool accumulate);
+void run_reduce_sites(mdg_ctx* c);
+
+// permutation helpers (device kernels)
+void scatter_sorted_scalar(mdg_ctx* c, const double* d_src, double* d_dst_sorted);
+void gather_vec_to_caller(mdg_ctx* c, const double4* sorted, double* d_dst_soa);
+void scatter_vec_from_caller(mdg_ctx* c, const double* d_src_soa, double4* sorted);
+void zero_vec(mdg_ctx* c, double4* v);
+void pack_system(mdg_ctx* c);
+void pack_positions(mdg_ctx* c);
+void polar_energy(mdg_ctx* c, double electric, int slot);
+
+}  // namespace mdg

@@ -1,0 +1,204 @@
+// mpole.cu -- real-space Ewald permanent-multipole energy, forces, torques
+// and pair virial (the empole1 analogue; no counterpart in the reference,
+// which covers charges only: SPEC.md:9).
+//
+// Pair energy with R = r_i - r_j and G_n = B_n(R) (Ewald bn recursion):
+//   U = C0 G0 + C1 G1 + C2 G2 + C3 G3 + C4 G4
+//   C0 = qi qj
+//   C1 = qi dj.R - qj di.R + di.dj
+//   C2 = qi R.Qj.R + qj R.Qi.R - (di.R)(dj.R) + 2 (di.QjR - dj.QiR + Qi:Qj)
+//   C3 = -(di.R)(R.Qj.R) + (R.Qi.R)(dj.R) - 4 (QiR).(QjR)
+//   C4 = (R.Qi.R)(R.Qj.R)
+// (Tinker's stored quadrupole Q = Theta/3.) dG_n/dR = -R G_{n+1} gives the
+// force F_i = -dU/dR; the torque on i is -mu_i x dU/dmu_i plus the
+// quadrupole term from dU/dQ_i. The oracle (oracle/mdo.c mdo_mpole) computes
+// the same quantities from generic Cartesian T-tensors instead.
+#include "common.cuh"
+
+namespace mdg {
+
+struct MKArgs {
+  int64_t n_i;
+  const double4* __restrict__ pos;
+  const double4* __restrict__ mp;
+  const int32_t* __restrict__ mol;
+  ListView L;
+  Box b;
+  double c2, alpha, electric;
+  double4* __restrict__ force;
+  double4* __restrict__ torque;
+  double* __restrict__ partials;
+  int accumulate;  // force/torque += instead of =
+};
+
+struct Quad {
+  double xx, xy, xz, yy, yz, zz;
+};
+
+__device__ __forceinline__ void qmul(const Quad& Q, double x, double y, double z, double& ox,
+                                     double& oy, double& oz) {
+  ox = Q.xx * x + Q.xy * y + Q.xz * z;
+  oy = Q.xy * x + Q.yy * y + Q.yz * z;
+  oz = Q.xz * x + Q.yz * y + Q.zz * z;
+}
+
+// partial slots: 0 energy, 1..9 virial (row-major)
+template <bool EXCL>
+__global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (i < a.n_i) {
+    const double4 pi = a.pos[i];
+    const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
+    const double qi = pi.w;
+    const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
+    const Quad Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
+    const int32_t mi = EXCL ? a.mol[i] : 0;
+    const int cnt = a.L.cnt[i];
+    const int32_t* row = list_row(a.L, (int)i);
+    double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(row + (size_t)k * 32);
+      const double4 pj = ldg4(a.pos + j);
+      double x, y, z;
+      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
+      if (!(r2 <= a.c2)) continue;
+      if (EXCL && __ldg(a.mol + j) == mi) continue;
+      const double4 m0j = ldg4(a.mp + 3 * (size_t)j), m1j = ldg4(a.mp + 3 * (size_t)j + 1);
+      const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
+      const double qj = pj.w, djx = m0j.x, djy = m0j.y, djz = m0j.z;
+      const double r = sqrt(r2);
+      const double inv_r2 = 1.0 / r2;
+      double G[6];
+      ewald_bn<5>(r, r2, inv_r2, a.alpha, G);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) G[q] *= a.electric;
+
+      double vix, viy, viz, vjx, vjy, vjz;
+      qmul(Qi, x, y, z, vix, viy, viz);
+      qmul(Qj, x, y, z, vjx, vjy, vjz);
+      const double dir = dix * x + diy * y + diz * z;
+      const double djr = djx * x + djy * y + djz * z;
+      const double qir = x * vix + y * viy + z * viz;
+      const double qjr = x * vjx + y * vjy + z * vjz;
+      const double dij = dix * djx + diy * djy + diz * djz;
+      const double diqj = dix * vjx + diy * vjy + diz * vjz;
+      const double djqi = djx * vix + djy * viy + djz * viz;
+      const double qiqj = Qi.xx * Qj.xx + Qi.yy * Qj.yy + Qi.zz * Qj.zz +
+                          2.0 * (Qi.xy * Qj.xy + Qi.xz * Qj.xz + Qi.yz * Qj.yz);
+      const double qvv = vix * vjx + viy * vjy + viz * vjz;
+      const double C0 = qi * qj;
+      const double C1 = qi * djr - qj * dir + dij;
+      const double C2 = qi * qjr + qj * qir - dir * djr + 2.0 * (diqj - djqi + qiqj);
+      const double C3 = -dir * qjr + qir * djr - 4.0 * qvv;
+      const double C4 = qir * qjr;
+      acc[0] += C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4];
+
+      // gradient dU/dR
+      double a1x, a1y, a1z, a2x, a2y, a2z, b1x, b1y, b1z, b2x, b2y, b2z;
+      qmul(Qj, dix, diy, diz, a1x, a1y, a1z);  // Qj di
+      qmul(Qi, djx, djy, djz, a2x, a2y, a2z);  // Qi dj
+      qmul(Qi, vjx, vjy, vjz, b1x, b1y, b1z);  // Qi vj
+      qmul(Qj, vix, viy, viz, b2x, b2y, b2z);  // Qj vi
+      const double s = C0 * G[1] + C1 * G[2] + C2 * G[3] + C3 * G[4] + C4 * G[5];
+      const double gx = G[1] * (qi * djx - qj * dix) +
+                        G[2] * (2.0 * (qi * vjx + qj * vix) - djr * dix - dir * djx +
+                                2.0 * (a1x - a2x)) +
+                        G[3] * (-qjr * dix - 2.0 * dir * vjx + 2.0 * djr * vix + qir * djx -
+                                4.0 * (b1x + b2x)) +
+                        G[4] * 2.0 * (qjr * vix + qir * vjx) - s * x;
+      const double gy = G[1] * (qi * djy - qj * diy) +
+                        G[2] * (2.0 * (qi * vjy + qj * viy) - djr * diy - dir * djy +
+                                2.0 * (a1y - a2y)) +
+                        G[3] * (-qjr * diy - 2.0 * dir * vjy + 2.0 * djr * viy + qir * djy -
+                                4.0 * (b1y + b2y)) +
+                        G[4] * 2.0 * (qjr * viy + qir * vjy) - s * y;
+      const double gz = G[1] * (qi * djz - qj * diz) +
+                        G[2] * (2.0 * (qi * vjz + qj * viz) - djr * diz - dir * djz +
+                                2.0 * (a1z - a2z)) +
+                        G[3] * (-qjr * diz - 2.0 * dir * vjz + 2.0 * djr * viz + qir * djz -
+                                4.0 * (b1z + b2z)) +
+                        G[4] * 2.0 * (qjr * viz + qir * vjz) - s * z;
+      fx -= gx;
+      fy -= gy;
+      fz -= gz;
+      acc[1] -= x * gx;
+      acc[2] -= x * gy;
+      acc[3] -= x * gz;
+      acc[4] -= y * gx;
+      acc[5] -= y * gy;
+      acc[6] -= y * gz;
+      acc[7] -= z * gx;
+      acc[8] -= z * gy;
+      acc[9] -= z * gz;
+
+      // dipole torque: tau = gmu x di, gmu = dU/d(di)
+      const double c1 = G[1] * qj + G[2] * djr + G[3] * qjr;  // coefficient of -R
+      const double gmx = G[1] * djx + 2.0 * G[2] * vjx - c1 * x;
+      const double gmy = G[1] * djy + 2.0 * G[2] * vjy - c1 * y;
+      const double gmz = G[1] * djz + 2.0 * G[2] * vjz - c1 * z;
+      tx += gmy * diz - gmz * diy;
+      ty += gmz * dix - gmx * diz;
+      tz += gmx * diy - gmy * dix;
+      // quadrupole torque: GQ = dU/dQi (symmetric); tau_a = -eps_abc (Qi GQ - GQ Qi)_bc
+      const double crr = G[2] * qj + G[3] * djr + G[4] * qjr;  // coefficient of R R^T
+      const double g2 = 2.0 * G[2];
+      const double g3 = 2.0 * G[3];
+      Quad GQ;
+      GQ.xx = crr * x * x - G[2] * (2.0 * djx * x) + g2 * Qj.xx - g3 * (2.0 * x * vjx);
+      GQ.yy = crr * y * y - G[2] * (2.0 * djy * y) + g2 * Qj.yy - g3 * (2.0 * y * vjy);
+      GQ.zz = crr * z * z - G[2] * (2.0 * djz * z) + g2 * Qj.zz - g3 * (2.0 * z * vjz);
+      GQ.xy = crr * x * y - G[2] * (djx * y + x * djy) + g2 * Qj.xy - g3 * (x * vjy + vjx * y);
+      GQ.xz = crr * x * z - G[2] * (djx * z + x * djz) + g2 * Qj.xz - g3 * (x * vjz + vjx * z);
+      GQ.yz = crr * y * z - G[2] * (djy * z + y * djz) + g2 * Qj.yz - g3 * (y * vjz + vjy * z);
+      // M = Qi GQ - GQ Qi (antisymmetric); tau = (M_zy - M_yz, M_xz - M_zx, M_yx - M_xy)
+      //   = 2 (M_zy, M_xz, M_yx)
+      const double Mzy = (Qi.xz * GQ.xy + Qi.yz * GQ.yy + Qi.zz * GQ.yz) -
+                         (GQ.xz * Qi.xy + GQ.yz * Qi.yy + GQ.zz * Qi.yz);
+      const double Mxz = (Qi.xx * GQ.xz + Qi.xy * GQ.yz + Qi.xz * GQ.zz) -
+                         (GQ.xx * Qi.xz + GQ.xy * Qi.yz + GQ.xz * Qi.zz);
+      const double Myx = (Qi.xy * GQ.xx + Qi.yy * GQ.xy + Qi.yz * GQ.xz) -
+                         (GQ.xy * Qi.xx + GQ.yy * Qi.xy + GQ.yz * Qi.xz);
+      tx += 2.0 * Mzy;
+      ty += 2.0 * Mxz;
+      tz += 2.0 * Myx;
+    }
+    if (a.accumulate) {
+      const double4 f0 = a.force[i];
+      fx += f0.x;
+      fy += f0.y;
+      fz += f0.z;
+    }
+    a.force[i] = make_double4(fx, fy, fz, 0.0);
+    a.torque[i] = make_double4(tx, ty, tz, 0.0);
+  }
+  block_store_partials<10>(acc, a.partials);
+}
+
+void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
+               int exclude, bool accumulate) {
+  const DevList& L = c->lists[list_id];
+  MKArgs k;
+  k.n_i = c->n;
+  k.pos = c->pos;
+  k.mp = c->mp;
+  k.mol = c->mol;
+  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = cutoff * cutoff;
+  k.alpha = alpha;
+  k.electric = electric;
+  k.force = c->force;
+  k.torque = c->torque;
+  const int64_t blocks = grid_for(c->n);
+  ensure_partials(c, blocks);
+  k.partials = c->partials;
+  k.accumulate = accumulate ? 1 : 0;
+  if (exclude && c->has_mol)
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, k_mpole<true>, k);
+  else
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, k_mpole<false>, k);
+  finalize_partials(c, blocks, 10, 10, 0.5);
+}
+
+}  // namespace mdg

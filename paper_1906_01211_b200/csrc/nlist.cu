@@ -1,0 +1,255 @@
+// nlist.cu -- neighbour-list construction on the device.
+//
+// Replaces build_cell_grid + build_neighbor_table
+// (proj/src/neighbors.cpp:10-36, proj/src/neighbors_vec.cpp:8-94).
+// 1. cell id per site (grid nc = max(1, floor(L / cutoff)) per axis, as the
+//    reference), counting sort of site ids into cells (histogram, scan,
+//    scatter, then a per-cell sort so the order is deterministic);
+// 2. one thread per site sweeps the deduplicated 27-cell stencil and keeps
+//    every j != i with dist2(wrap1(r_i - r_j)) <= cutoff^2 -- the exact
+//    reference predicate, so the pair SET is bit-identical;
+// 3. output is a FULL list (both directions) in sliced-ELL layout so the pair
+//    kernels need no j-side scatter (no atomics) and read indices coalesced.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace mdg {
+
+__global__ void k_cell_assign(int64_t n, const double4* __restrict__ P, Grid g,
+                              int32_t* __restrict__ cell_of, int32_t* __restrict__ count) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = P[i];
+  // proj/src/neighbors.cpp:28-30
+  const int cx = min(g.ncx - 1, (int)(p.x / g.ex));
+  const int cy = min(g.ncy - 1, (int)(p.y / g.ey));
+  const int cz = min(g.ncz - 1, (int)(p.z / g.ez));
+  const int c = (cx * g.ncy + cy) * g.ncz + cz;
+  cell_of[i] = c;
+  atomicAdd(&count[c], 1);
+}
+
+// Exclusive scan of count[0..m) into start[0..m]; one block of 1024 threads,
+// each owning a contiguous chunk (m is at most a few 10^5 cells).
+__global__ void k_scan(int64_t m, const int32_t* count, int32_t* __restrict__ start,
+                       int32_t* fill) {
+  __shared__ int32_t sums[1024];
+  const int t = threadIdx.x;
+  const int64_t chunk = (m + 1023) / 1024;
+  const int64_t b = t * chunk, e = min(m, b + chunk);
+  int32_t s = 0;
+  for (int64_t k = b; k < e; ++k) s += count[k];
+  sums[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    int32_t v = (t >= o) ? sums[t - o] : 0;
+    __syncthreads();
+    sums[t] += v;
+    __syncthreads();
+  }
+  int32_t run = sums[t] - s;
+  for (int64_t k = b; k < e; ++k) {
+    const int32_t v = count[k];  // count may alias fill
+    start[k] = run;
+    fill[k] = run;
+    run += v;
+  }
+  if (t == 1023) start[m] = sums[1023];
+}
+
+__global__ void k_cell_fill(int64_t n, const int32_t* __restrict__ cell_of,
+                            int32_t* __restrict__ fill, int32_t* __restrict__ atoms) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t slot = atomicAdd(&fill[cell_of[i]], 1);
+  atoms[slot] = (int32_t)i;
+}
+
+// insertion sort of each cell's ids (cells hold O(100) sites)
+__global__ void k_cell_sort(int64_t m, const int32_t* __restrict__ start,
+                            int32_t* __restrict__ atoms) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const int32_t b = start[c], e = start[c + 1];
+  for (int32_t k = b + 1; k < e; ++k) {
+    const int32_t v = atoms[k];
+    int32_t q = k - 1;
+    while (q >= b && atoms[q] > v) {
+      atoms[q + 1] = atoms[q];
+      --q;
+    }
+    atoms[q + 1] = v;
+  }
+}
+
+__device__ __forceinline__ int axis_cells(int c, int nc, int (&out)[3]) {
+  // periodic neighbours c-1, c, c+1, deduplicated (nc == 1 or 2 collapse)
+  if (nc == 1) { out[0] = 0; return 1; }
+  if (nc == 2) { out[0] = 0; out[1] = 1; return 2; }
+  out[0] = (c + nc - 1) % nc;
+  out[1] = c;
+  out[2] = (c + 1) % nc;
+  return 3;
+}
+
+__global__ void __launch_bounds__(kBlock) k_nlist_build(
+    int64_t n_i, const double4* __restrict__ P, const int32_t* __restrict__ cell_of, Grid g,
+    const int32_t* __restrict__ start, const int32_t* __restrict__ atoms, Box b, double c2,
+    int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+    const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_i) return;
+  const double4 pi = P[i];
+  const int c = cell_of[i];
+  const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+  int xs[3], ys[3], zs[3];
+  const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
+            nz = axis_cells(cz, g.ncz, zs);
+  int32_t* out = nbr + (size_t)(i >> 5) * (size_t)cap * 32 + (i & 31);
+  int32_t k = 0;
+  // reference capacity rule: the half list stores a pair on the lower
+  // caller index and caps it at kMaxNeighbors (proj/src/neighbors_vec.cpp:80-83)
+  const int32_t oi = perm[i];
+  int32_t upper = 0;
+  for (int a = 0; a < nx; ++a)
+    for (int bb = 0; bb < ny; ++bb)
+      for (int q = 0; q < nz; ++q) {
+        const int cell = (xs[a] * g.ncy + ys[bb]) * g.ncz + zs[q];
+        const int32_t e = start[cell + 1];
+        for (int32_t s = start[cell]; s < e; ++s) {
+          const int32_t j = atoms[s];
+          if (j == (int32_t)i) continue;
+          const double4 pj = ldg4(P + j);
+          double dx, dy, dz;
+          const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+          if (r2 <= c2) {
+            if (k < cap) out[(size_t)k * 32] = j;
+            ++k;
+            upper += (__ldg(perm + j) > oi) ? 1 : 0;
+          }
+        }
+      }
+  cnt[i] = k;
+  if (upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+}
+
+// max and sum of counts -> results[slot], results[slot+1]
+__global__ void k_count_stats(int64_t n, const int32_t* __restrict__ cnt,
+                              double* __restrict__ results, int slot) {
+  __shared__ long long s_sum[256];
+  __shared__ int s_max[256];
+  long long sum = 0;
+  int mx = 0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    const int v = cnt[i];
+    sum += v;
+    mx = max(mx, v);
+  }
+  s_sum[threadIdx.x] = sum;
+  s_max[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+      s_max[threadIdx.x] = max(s_max[threadIdx.x], s_max[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    results[slot] = (double)s_max[0];
+    results[slot + 1] = (double)s_sum[0];
+  }
+}
+
+static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
+  const int64_t groups = (c->n + 31) / 32;
+  const size_t need = (size_t)groups * (size_t)cap * 32;
+  if (need > L.nbr_elems) {
+    if (L.nbr) cudaFree(L.nbr);
+    L.nbr = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&L.nbr, need * sizeof(int32_t)));
+    L.nbr_elems = need;
+  }
+  if (!L.cnt) MDG_CUDA_CHECK(cudaMalloc(&L.cnt, (size_t)c->n_cap * sizeof(int32_t)));
+  L.cap = cap;
+}
+
+void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
+  DevList& L = c->lists[list_id];
+  const double4* P = (sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+  Grid g;
+  g.ncx = std::max(1, (int)(c->lx / list_cutoff));
+  g.ncy = std::max(1, (int)(c->ly / list_cutoff));
+  g.ncz = std::max(1, (int)(c->lz / list_cutoff));
+  g.ex = c->lx / g.ncx;
+  g.ey = c->ly / g.ncy;
+  g.ez = c->lz / g.ncz;
+  const int64_t ncell = (int64_t)g.ncx * g.ncy * g.ncz;
+  if (ncell + 1 > c->cell_cap) {
+    if (c->cell_start) cudaFree(c->cell_start);
+    if (c->cell_fill) cudaFree(c->cell_fill);
+    c->cell_start = c->cell_fill = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&c->cell_start, (ncell + 1) * sizeof(int32_t)));
+    MDG_CUDA_CHECK(cudaMalloc(&c->cell_fill, (ncell + 1) * sizeof(int32_t)));
+    c->cell_cap = ncell + 1;
+  }
+  const int64_t n = c->n;
+  MDG_CUDA_CHECK(cudaMemsetAsync(c->cell_fill, 0, ncell * sizeof(int32_t), c->stream));
+  MDG_LAUNCH(c, "cell_assign", grid_for(n, 256), 256, 0, k_cell_assign, n, P, g, c->cell_of,
+             c->cell_fill);
+  // k_scan reads counts from cell_fill and rewrites it as the fill cursor
+  MDG_LAUNCH(c, "cell_scan", 1, 1024, 0, k_scan, ncell, c->cell_fill, c->cell_start,
+             c->cell_fill);
+  MDG_LAUNCH(c, "cell_fill", grid_for(n, 256), 256, 0, k_cell_fill, n, c->cell_of, c->cell_fill,
+             c->cell_atoms);
+  MDG_LAUNCH(c, "cell_sort", grid_for(ncell, 128), 128, 0, k_cell_sort, ncell, c->cell_start,
+             c->cell_atoms);
+
+  // capacity: density estimate, grown to the measured maximum if exceeded
+  const double vol = c->lx * c->ly * c->lz;
+  const double expect = (double)n / vol * 4.18879020478639 * list_cutoff * list_cutoff *
+                        list_cutoff;
+  int32_t cap = (int32_t)std::min<double>((double)c->max_pairs, 1.35 * expect + 48.0);
+  cap = std::max<int32_t>(32, (cap + 7) & ~7);
+  if (L.cap > cap && L.nbr) cap = std::min(L.cap, c->max_pairs);
+  const Box b = make_box(c->lx, c->ly, c->lz);
+  const double c2 = list_cutoff * list_cutoff;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    ensure_list_storage(c, L, cap);
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int32_t), c->stream));
+    MDG_LAUNCH(c, "nlist_build", grid_for(n), kBlock, 0, k_nlist_build, n, P, c->cell_of, g,
+               c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm, c->d_flag);
+    MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, n, L.cnt, c->results, 60);
+    int32_t bad_site = 0;
+    MDG_CUDA_CHECK(cudaMemcpyAsync(&bad_site, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    fetch_results(c);
+    if (bad_site != 0x7f7f7f7f) {
+      L.valid = false;
+      throw_error(MDG_CAPACITY, "neighbor table: site " + std::to_string(bad_site) +
+                                    " exceeds the per-site neighbor capacity");
+    }
+    const int32_t mx = (int32_t)c->h_results[60];
+    const int64_t sum = (int64_t)c->h_results[61];
+    if (mx > c->max_pairs) {
+      L.valid = false;
+      throw_error(MDG_CAPACITY, "neighbor table: a site exceeds the per-site neighbor capacity (" +
+                                    std::to_string(mx) + " > " + std::to_string(c->max_pairs) +
+                                    ")");
+    }
+    if (mx <= cap) {
+      L.valid = true;
+      L.cutoff = list_cutoff;
+      L.sites = sites;
+      L.max_cnt = mx;
+      L.half_pairs = sum / 2;
+      return;
+    }
+    cap = std::min<int32_t>(c->max_pairs, (mx + 7) & ~7);
+  }
+  throw_error(MDG_CUDA, "nlist_build: capacity retry failed");
+}
+
+}  // namespace mdg

@@ -1,0 +1,263 @@
+// nonpolar.cu -- Lennard-Jones, real-space Ewald charge and Halgren 14-7.
+//
+// One thread per i site over its full (both-direction) neighbour row: the
+// i-side force accumulates in registers and is written once, so there are
+// no j-side atomics and results are deterministic. Energies and virials are
+// counted twice over the full list and halved in the fixed-order finalize.
+// Pair arithmetic follows the reference: proj/include/mdvec/kernels.hpp:42-64
+// (LJ, Ewald) and proj/src/polar_vec.cpp:74-116 (Halgren one-division form).
+#include "common.cuh"
+
+namespace mdg {
+
+struct NonpolarKArgs {
+  int64_t n_i;
+  const double4* __restrict__ pos;
+  const double4* __restrict__ vdwp;
+  const int32_t* __restrict__ mol;
+  ListView L;
+  Box b;
+  double c2, alpha, electric;
+  double4* __restrict__ force;
+  double* __restrict__ partials;
+};
+
+// partial slots: 0 E_lj, 1 E_coul, 2..7 virial (xx xy xz yy yz zz)
+template <bool LJ, bool COUL, bool SHIFT, bool EXCL>
+__global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (i < a.n_i) {
+    const double4 pi = a.pos[i];
+    double4 vi = make_double4(0, 0, 0, 0);
+    if (LJ) vi = a.vdwp[i];
+    const int32_t mi = EXCL ? a.mol[i] : 0;
+    const int cnt = a.L.cnt[i];
+    const int32_t* row = list_row(a.L, (int)i);
+    double fx = 0, fy = 0, fz = 0;
+    const double two_over_sqrt_pi = 1.1283791670955126;
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(row + (size_t)k * 32);
+      const double4 pj = ldg4(a.pos + j);
+      double dx, dy, dz;
+      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      if (!(r2 <= a.c2)) continue;
+      if (EXCL && __ldg(a.mol + j) == mi) continue;
+      double fs = 0.0;
+      if (LJ) {
+        const double4 vj = ldg4(a.vdwp + j);
+        const double sij = 0.5 * (vi.x + vj.x);
+        const double eij = vi.y * vj.y;
+        const double inv_r2 = 1.0 / r2;
+        const double s2 = sij * sij * inv_r2;
+        const double s6 = s2 * s2 * s2;
+        const double s12 = s6 * s6;
+        double u = 4.0 * eij * (s12 - s6);
+        if (SHIFT) {
+          const double sc2 = sij * sij / a.c2;
+          const double sc6 = sc2 * sc2 * sc2;
+          u -= 4.0 * eij * (sc6 * sc6 - sc6);
+        }
+        acc[0] += u;
+        fs += 24.0 * eij * (2.0 * s12 - s6) * inv_r2;
+      }
+      if (COUL) {
+        const double r = sqrt(r2);
+        const double inv_r = 1.0 / r;
+        const double qq = a.electric * pi.w * pj.w;
+        const double ee = erfc(a.alpha * r) * inv_r;
+        const double g = a.alpha * two_over_sqrt_pi * exp(-a.alpha * a.alpha * r2);
+        acc[1] += qq * ee;
+        fs += qq * (ee + g) * inv_r * inv_r;
+      }
+      const double px = fs * dx, py = fs * dy, pz = fs * dz;
+      fx += px;
+      fy += py;
+      fz += pz;
+      acc[2] += dx * px;
+      acc[3] += dx * py;
+      acc[4] += dx * pz;
+      acc[5] += dy * py;
+      acc[6] += dy * pz;
+      acc[7] += dz * pz;
+    }
+    a.force[i] = make_double4(fx, fy, fz, 0.0);
+  }
+  block_store_partials<8>(acc, a.partials);
+}
+
+template <bool LJ, bool COUL>
+static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
+                      const char* name) {
+  const unsigned g = grid_for(k.n_i);
+#define NP_CASE(S, E)                                                            \
+  if (shift == S && excl == E) {                                               \
+    MDG_LAUNCH(c, name, g, kBlock, 0, (k_nonpolar<LJ, COUL, S, E>), k);         \
+    return;                                                                    \
+  }
+  NP_CASE(false, false)
+  NP_CASE(false, true)
+  NP_CASE(true, false)
+  NP_CASE(true, true)
+#undef NP_CASE
+}
+
+void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
+  const DevList& L = c->lists[list_id];
+  NonpolarKArgs k;
+  k.n_i = c->n;
+  k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+  k.vdwp = c->vdwp;
+  k.mol = c->mol;
+  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = a.cutoff * a.cutoff;
+  k.alpha = a.alpha;
+  k.electric = a.electric;
+  k.force = (L.sites == MDG_SITES_VDW) ? c->force2 : c->force;
+  const int64_t blocks = grid_for(c->n);
+  ensure_partials(c, blocks);
+  k.partials = c->partials;
+  if (L.sites == MDG_SITES_VDW && a.do_coul)
+    throw_error(MDG_CONTRACT, "coulomb terms need a list over atomic sites");
+  const bool shift = a.shift != 0, excl = a.exclude != 0 && c->has_mol;
+  if (a.do_lj && a.do_coul) launch_np<true, true>(c, k, shift, excl, "lj_ewald");
+  else if (a.do_lj) launch_np<true, false>(c, k, shift, excl, "lj");
+  else launch_np<false, true>(c, k, shift, excl, "ewald_real");
+  finalize_partials(c, blocks, 8, 0, 0.5);
+}
+
+// ---- Halgren buffered 14-7 -------------------------------------------------
+struct HalgrenKArgs {
+  int64_t n_i;
+  const double4* __restrict__ site;
+  const double4* __restrict__ vdwp;
+  const int32_t* __restrict__ mol;
+  ListView L;
+  Box b;
+  double c2, delta, gamma;
+  double4* __restrict__ force;
+  double* __restrict__ partials;
+};
+
+template <bool EXCL>
+__global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (i < a.n_i) {
+    const double4 pi = a.site[i];
+    const double4 vi = a.vdwp[i];
+    const int32_t mi = EXCL ? a.mol[i] : 0;
+    const int cnt = a.L.cnt[i];
+    const int32_t* row = list_row(a.L, (int)i);
+    const double delta = a.delta, gamma = a.gamma;
+    double fx = 0, fy = 0, fz = 0;
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(row + (size_t)k * 32);
+      const double4 pj = ldg4(a.site + j);
+      double dx, dy, dz;
+      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      if (!(r2 <= a.c2)) continue;
+      if (EXCL && __ldg(a.mol + j) == mi) continue;
+      const double4 vj = ldg4(a.vdwp + j);
+      // proj/src/polar_vec.cpp:78-107: all reciprocals from one division
+      const double r = sqrt(r2);
+      const double r0 = 0.5 * (vi.z + vj.z);
+      const double eij = vi.w * vj.w;
+      const double r0_2 = r0 * r0;
+      const double r0_3 = r0_2 * r0;
+      const double r0_6 = r0_3 * r0_3;
+      const double r0_7 = r0_6 * r0;
+      const double r3 = r2 * r;
+      const double r6 = r3 * r3;
+      const double r7 = r6 * r;
+      const double e1 = r + delta * r0;
+      const double e2 = r7 + gamma * r0_7;
+      const double r0r = r0 * r;
+      const double q = 1.0 / (e1 * e2 * r0r);
+      const double inv_e1 = q * e2 * r0r;
+      const double inv_e2 = q * e1 * r0r;
+      const double inv_r0r = q * e1 * e2;
+      const double t1 = (1.0 + delta) * r0 * inv_e1;
+      const double t2 = t1 * t1;
+      const double t4 = t2 * t2;
+      const double t7 = t4 * t2 * t1;
+      const double g1 = (1.0 + gamma) * r0_7 * inv_e2;
+      const double bb = g1 - 2.0;
+      const double u = eij * t7 * bb;
+      const double dudrho = -7.0 * eij * t7 * (bb * r0 * inv_e1 + r6 * r0 * g1 * inv_e2);
+      const double fs = -dudrho * inv_r0r;
+      acc[0] += u;
+      const double px = fs * dx, py = fs * dy, pz = fs * dz;
+      fx += px;
+      fy += py;
+      fz += pz;
+      acc[2] += dx * px;
+      acc[3] += dx * py;
+      acc[4] += dx * pz;
+      acc[5] += dy * py;
+      acc[6] += dy * pz;
+      acc[7] += dz * pz;
+    }
+    a.force[i] = make_double4(fx, fy, fz, 0.0);
+  }
+  block_store_partials<8>(acc, a.partials);
+}
+
+// F_atom[i] = f_i F_site[i] + sum over children c of (1 - f_c) F_site[c]
+// (children CSR built on the host from hred_parent; sorted indices).
+__global__ void k_chain_rule(int64_t n, const double4* __restrict__ fsite,
+                             const int32_t* __restrict__ par, const double* __restrict__ fac,
+                             const int32_t* __restrict__ child_start,
+                             const int32_t* __restrict__ child, double4* __restrict__ fatom) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 fi = fsite[i];
+  double fx, fy, fz;
+  if (par[i] == i) {
+    fx = fi.x; fy = fi.y; fz = fi.z;
+  } else {
+    const double f = fac[i];
+    fx = f * fi.x; fy = f * fi.y; fz = f * fi.z;
+  }
+  for (int32_t k = child_start[i]; k < child_start[i + 1]; ++k) {
+    const int32_t cc = child[k];
+    const double g = 1.0 - fac[cc];
+    const double4 fc = fsite[cc];
+    fx += g * fc.x;
+    fy += g * fc.y;
+    fz += g * fc.z;
+  }
+  fatom[i] = make_double4(fx, fy, fz, 0.0);
+}
+
+void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double gamma,
+                 int exclude) {
+  const DevList& L = c->lists[list_id];
+  HalgrenKArgs k;
+  k.n_i = c->n;
+  const bool reduced = (L.sites == MDG_SITES_VDW);
+  k.site = reduced ? c->vsite : c->pos;
+  k.vdwp = c->vdwp;
+  k.mol = c->mol;
+  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = cutoff * cutoff;
+  k.delta = delta;
+  k.gamma = gamma;
+  k.force = reduced ? c->force2 : c->force;
+  const int64_t blocks = grid_for(c->n);
+  ensure_partials(c, blocks);
+  k.partials = c->partials;
+  if (exclude && c->has_mol)
+    MDG_LAUNCH(c, "halgren", (unsigned)blocks, kBlock, 0, k_halgren<true>, k);
+  else
+    MDG_LAUNCH(c, "halgren", (unsigned)blocks, kBlock, 0, k_halgren<false>, k);
+  finalize_partials(c, blocks, 8, 0, 0.5);
+  if (reduced) {
+    MDG_LAUNCH(c, "chain_rule", grid_for(c->n, 256), 256, 0, k_chain_rule, c->n, c->force2,
+               c->hpar, c->hfac, c->child_start, c->child, c->force);
+  }
+}
+
+}  // namespace mdg

@@ -1,0 +1,434 @@
+// polar.cu -- Thole/Ewald dipole-field mat-vec, permanent multipole field,
+// and the on-device induced-dipole solvers (PCG with fused dots; Jacobi).
+//
+// Reference: proj/src/polar_scalar.cpp:69-198 (Thole-only T, charge-only
+// field, Jacobi). With alpha > 0 the pair tensors are the real-space Ewald
+// ones, rr3 = B1 - (1-l3)/r^3, rr5 = B2 - 3(1-l5)/r^5, rr7 = B3 - 15(1-l7)/r^7;
+// at alpha == 0 the kernels use the reference's l3/r^3, 3 l5/r^5 forms.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace mdg {
+
+struct TKArgs {
+  int64_t n_i;
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  ListView L;
+  Box b;
+  double c2, alpha, thole_a;
+  const double4* __restrict__ in;
+  double4* __restrict__ out;
+  // PCG fusion: q = p/alpha_i - T p, partial p.q
+  double* __restrict__ partials;
+};
+
+template <bool EWALD, bool PCG>
+__global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < a.n_i) {
+    const double4 pi = a.pos[i];
+    const double2 ai = a.polp[i];
+    const int cnt = a.L.cnt[i];
+    const int32_t* row = list_row(a.L, (int)i);
+    double ex = 0, ey = 0, ez = 0;
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(row + (size_t)k * 32);
+      const double4 pj = ldg4(a.pos + j);
+      double dx, dy, dz;
+      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      if (!(r2 <= a.c2)) continue;
+      const double2 aj = __ldg(a.polp + j);
+      const double4 mj = ldg4(a.in + j);
+      const double r = sqrt(r2);
+      double l3, l5;
+      thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
+      double rr3, rr5;
+      if (EWALD) {
+        const double inv_r2 = 1.0 / r2;
+        double bn[3];
+        ewald_bn<2>(r, r2, inv_r2, a.alpha, bn);
+        const double b3 = inv_r2 / r;
+        rr3 = bn[1] - (1.0 - l3) * b3;
+        rr5 = bn[2] - (1.0 - l5) * 3.0 * b3 * inv_r2;
+      } else {
+        const double r3 = r2 * r;
+        rr3 = l3 / r3;
+        rr5 = 3.0 * l5 / (r3 * r2);
+      }
+      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
+      ex += rr5 * dot * dx - rr3 * mj.x;
+      ey += rr5 * dot * dy - rr3 * mj.y;
+      ez += rr5 * dot * dz - rr3 * mj.z;
+    }
+    if (PCG) {
+      const double4 p = a.in[i];
+      const double inva = 1.0 / ai.x;
+      const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
+      a.out[i] = make_double4(qx, qy, qz, 0.0);
+      acc[0] = p.x * qx + p.y * qy + p.z * qz;
+    } else {
+      a.out[i] = make_double4(ex, ey, ez, 0.0);
+    }
+  }
+  if (PCG) block_store_partials<1>(acc, a.partials);
+}
+
+static TKArgs t_args(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                     const double4* in, double4* out) {
+  const DevList& L = c->lists[list_id];
+  TKArgs k;
+  k.n_i = c->n;
+  k.pos = c->pos;
+  k.polp = c->polp;
+  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = cutoff * cutoff;
+  k.alpha = alpha;
+  k.thole_a = thole_a;
+  k.in = in;
+  k.out = out;
+  k.partials = c->partials;
+  return k;
+}
+
+void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                 const double4* in, double4* out) {
+  TKArgs k = t_args(c, list_id, alpha, cutoff, thole_a, in, out);
+  if (alpha > 0)
+    MDG_LAUNCH(c, "tmatvec", grid_for(c->n), kBlock, 0, (k_tmatvec<true, false>), k);
+  else
+    MDG_LAUNCH(c, "tmatvec", grid_for(c->n), kBlock, 0, (k_tmatvec<false, false>), k);
+}
+
+// ---- permanent field ----------------------------------------------------------
+struct FKArgs {
+  int64_t n_i;
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  const double4* __restrict__ mp;
+  const int32_t* __restrict__ mol;
+  ListView L;
+  Box b;
+  double c2, alpha, thole_a;
+  double4* __restrict__ out;
+};
+
+// E_i = sum_j R (rr3 q_j + rr5 mu_j.R + rr7 R.Q_j.R) - rr3 mu_j - 2 rr5 Q_j R,
+// R = r_i - r_j (field of a point multipole; Tinker's stored Q = Theta/3).
+template <bool EWALD, bool MPOLE, bool EXCL>
+__global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (i >= a.n_i) return;
+  const double4 pi = a.pos[i];
+  const double2 ai = a.polp[i];
+  const int32_t mi = EXCL ? a.mol[i] : 0;
+  const int cnt = a.L.cnt[i];
+  const int32_t* row = list_row(a.L, (int)i);
+  double ex = 0, ey = 0, ez = 0;
+  for (int k = 0; k < cnt; ++k) {
+    const int32_t j = __ldg(row + (size_t)k * 32);
+    const double4 pj = ldg4(a.pos + j);
+    double dx, dy, dz;
+    const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+    if (!(r2 <= a.c2)) continue;
+    if (EXCL && __ldg(a.mol + j) == mi) continue;
+    const double2 aj = __ldg(a.polp + j);
+    const double r = sqrt(r2);
+    if (!MPOLE) {
+      double l3, l5;
+      thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
+      double rr3;
+      if (EWALD) {
+        const double inv_r2 = 1.0 / r2;
+        double bn[2];
+        ewald_bn<1>(r, r2, inv_r2, a.alpha, bn);
+        rr3 = bn[1] - (1.0 - l3) * inv_r2 / r;
+      } else {
+        rr3 = l3 / (r2 * r);  // proj/src/polar_scalar.cpp:143
+      }
+      const double c = rr3 * pj.w;
+      ex += c * dx;
+      ey += c * dy;
+      ez += c * dz;
+    } else {
+      double l3, l5, l7;
+      thole7(r, ai.y * aj.y, a.thole_a, l3, l5, l7);
+      const double inv_r2 = 1.0 / r2;
+      const double b1 = inv_r2 / r, b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
+      double rr3, rr5, rr7;
+      if (EWALD) {
+        double bn[4];
+        ewald_bn<3>(r, r2, inv_r2, a.alpha, bn);
+        rr3 = bn[1] - (1.0 - l3) * b1;
+        rr5 = bn[2] - (1.0 - l5) * b2;
+        rr7 = bn[3] - (1.0 - l7) * b3;
+      } else {
+        rr3 = l3 * b1;
+        rr5 = l5 * b2;
+        rr7 = l7 * b3;
+      }
+      const double4 m0 = ldg4(a.mp + 3 * (size_t)j);
+      const double4 m1 = ldg4(a.mp + 3 * (size_t)j + 1);
+      const double qzz = __ldg(&a.mp[3 * (size_t)j + 2].x);
+      // Q R with Q = [[m0.w, m1.x, m1.y], [m1.x, m1.z, m1.w], [m1.y, m1.w, qzz]]
+      const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
+      const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
+      const double qz = m1.y * dx + m1.w * dy + qzz * dz;
+      const double dr = m0.x * dx + m0.y * dy + m0.z * dz;
+      const double qr = dx * qx + dy * qy + dz * qz;
+      const double cc = rr3 * pj.w + rr5 * dr + rr7 * qr;
+      const double t5 = 2.0 * rr5;
+      ex += cc * dx - rr3 * m0.x - t5 * qx;
+      ey += cc * dy - rr3 * m0.y - t5 * qy;
+      ez += cc * dz - rr3 * m0.z - t5 * qz;
+    }
+  }
+  a.out[i] = make_double4(ex, ey, ez, 0.0);
+}
+
+void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                    int exclude, double4* out) {
+  const DevList& L = c->lists[list_id];
+  FKArgs k;
+  k.n_i = c->n;
+  k.pos = c->pos;
+  k.polp = c->polp;
+  k.mp = c->mp;
+  k.mol = c->mol;
+  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = cutoff * cutoff;
+  k.alpha = alpha;
+  k.thole_a = thole_a;
+  k.out = out;
+  const bool ew = alpha > 0, mp = c->has_mpoles, ex = exclude && c->has_mol;
+  const unsigned g = grid_for(c->n);
+#define PF_CASE(E, M, X)                                                         \
+  if (ew == E && mp == M && ex == X) {                                         \
+    MDG_LAUNCH(c, "perm_field", g, kBlock, 0, (k_perm_field<E, M, X>), k);      \
+    return;                                                                    \
+  }
+  PF_CASE(false, false, false)
+  PF_CASE(false, false, true)
+  PF_CASE(false, true, false)
+  PF_CASE(false, true, true)
+  PF_CASE(true, false, false)
+  PF_CASE(true, false, true)
+  PF_CASE(true, true, false)
+  PF_CASE(true, true, true)
+#undef PF_CASE
+}
+
+// ---- PCG ----------------------------------------------------------------------
+// result slots: 20 p.q, 21 rz_old, 22 rz_new, 23 sum|dmu|^2, 24 beta, 25 rms (D),
+// 26 a_k, 27 converged flag
+constexpr double kDebye = 4.80321;
+
+// mu0 = alpha E; r0 = E - mu0/alpha + T mu0 (t = T mu0); z = alpha r; p = z
+__global__ void __launch_bounds__(kBlock) k_cg_init(int64_t n, const double2* __restrict__ polp,
+                                                    const double4* __restrict__ e,
+                                                    const double4* __restrict__ t,
+                                                    double4* __restrict__ mu,
+                                                    double4* __restrict__ r,
+                                                    double4* __restrict__ z,
+                                                    double4* __restrict__ p,
+                                                    double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < n) {
+    const double al = polp[i].x;
+    const double4 E = e[i], T = t[i], m = mu[i];
+    const double inva = 1.0 / al;
+    const double rx = E.x - (m.x * inva - T.x), ry = E.y - (m.y * inva - T.y),
+                 rz = E.z - (m.z * inva - T.z);
+    r[i] = make_double4(rx, ry, rz, 0.0);
+    const double4 zz = make_double4(al * rx, al * ry, al * rz, 0.0);
+    z[i] = zz;
+    p[i] = zz;
+    acc[0] = rx * zz.x + ry * zz.y + rz * zz.z;
+  }
+  block_store_partials<1>(acc, partials);
+}
+
+__global__ void k_mu0(int64_t n, const double2* __restrict__ polp, const double4* __restrict__ e,
+                      double4* __restrict__ mu) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double al = polp[i].x;
+    const double4 E = e[i];
+    mu[i] = make_double4(al * E.x, al * E.y, al * E.z, 0.0);
+  }
+}
+
+// mu += a p; r -= a q; z = alpha r; partials: r.z, |a p|^2
+__global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* __restrict__ polp,
+                                                      const double* __restrict__ res,
+                                                      const double4* __restrict__ p,
+                                                      const double4* __restrict__ q,
+                                                      double4* __restrict__ mu,
+                                                      double4* __restrict__ r,
+                                                      double4* __restrict__ z,
+                                                      double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[2] = {0.0, 0.0};
+  if (i < n) {
+    const double ak = res[26];
+    const double al = polp[i].x;
+    const double4 pp = p[i], qq = q[i], m = mu[i], rr = r[i];
+    const double dx = ak * pp.x, dy = ak * pp.y, dz = ak * pp.z;
+    mu[i] = make_double4(m.x + dx, m.y + dy, m.z + dz, 0.0);
+    const double rx = rr.x - ak * qq.x, ry = rr.y - ak * qq.y, rz = rr.z - ak * qq.z;
+    r[i] = make_double4(rx, ry, rz, 0.0);
+    const double zx = al * rx, zy = al * ry, zz = al * rz;
+    z[i] = make_double4(zx, zy, zz, 0.0);
+    acc[0] = rx * zx + ry * zy + rz * zz;
+    acc[1] = dx * dx + dy * dy + dz * dz;
+  }
+  block_store_partials<2>(acc, partials);
+}
+
+// p = z + beta p
+__global__ void k_cg_dir(int64_t n, const double* __restrict__ res, const double4* __restrict__ z,
+                         double4* __restrict__ p) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double bk = res[24];
+    const double4 zz = z[i], pp = p[i];
+    p[i] = make_double4(zz.x + bk * pp.x, zz.y + bk * pp.y, zz.z + bk * pp.z, 0.0);
+  }
+}
+
+// Fixed-order sums of the CG partials plus the scalar recurrences.
+// mode 0: rz0 -> res[21]; mode 1: p.q -> a = rz/pq -> res[26];
+// mode 2: rz_new, dsum -> beta, rms, converged.
+__global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks, int mode,
+                             int64_t n, double tol, double* __restrict__ res) {
+  __shared__ double s[2][256];
+  const int nv = (mode == 2) ? 2 : 1;
+  for (int v = 0; v < nv; ++v) {
+    double acc = 0.0;
+    for (int64_t b = threadIdx.x; b < blocks; b += 256) acc += partials[b * kRedVals + v];
+    s[v][threadIdx.x] = acc;
+  }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int v = 0; v < nv; ++v) s[v][threadIdx.x] += s[v][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (mode == 0) {
+      res[21] = s[0][0];
+      res[27] = 0.0;
+    } else if (mode == 1) {
+      res[20] = s[0][0];
+      res[26] = res[21] / s[0][0];
+    } else {
+      const double rz_new = s[0][0];
+      res[22] = rz_new;
+      res[23] = s[1][0];
+      const double rms = sqrt(s[1][0] / (double)n) * kDebye;
+      res[25] = rms;
+      res[24] = rz_new / res[21];
+      res[21] = rz_new;
+      res[27] = (rms < tol) ? 1.0 : 0.0;
+    }
+  }
+}
+
+int64_t run_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                double tol_debye, int64_t max_iter, double* last_rms) {
+  const int64_t n = c->n;
+  const int64_t blocks = grid_for(n);
+  ensure_partials(c, blocks);
+  // c->eperm holds the permanent field
+  MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
+  run_tmatvec(c, list_id, alpha, cutoff, thole_a, c->mu, c->cg_q);
+  MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
+             c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
+  MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
+             c->results);
+  TKArgs k = t_args(c, list_id, alpha, cutoff, thole_a, c->cg_p, c->cg_q);
+  for (int64_t it = 1; it <= max_iter; ++it) {
+    if (alpha > 0)
+      MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, (k_tmatvec<true, true>), k);
+    else
+      MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, (k_tmatvec<false, true>), k);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 1, n, tol_debye,
+               c->results);
+    MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
+               c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
+               c->results);
+    fetch_results(c);
+    *last_rms = c->h_results[25];
+    if (c->h_results[27] != 0.0) return it;
+    MDG_LAUNCH(c, "cg_dir", grid_for(n, 256), 256, 0, k_cg_dir, n, c->results, c->cg_z, c->cg_p);
+  }
+  throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
+}
+
+// ---- Jacobi (reference semantics) ------------------------------------------------
+// mu_new = alpha (E + T mu); resid = max |mu_new - mu| (block max -> partials)
+__global__ void __launch_bounds__(kBlock) k_jacobi_update(int64_t n, const double2* __restrict__ polp,
+                                                          const double4* __restrict__ e,
+                                                          const double4* __restrict__ t,
+                                                          double4* __restrict__ mu,
+                                                          double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double m = 0.0;
+  if (i < n) {
+    const double al = polp[i].x;
+    const double4 E = e[i], T = t[i], old = mu[i];
+    const double nx = al * (E.x + T.x), ny = al * (E.y + T.y), nz = al * (E.z + T.z);
+    m = fmax(fabs(nx - old.x), fmax(fabs(ny - old.y), fabs(nz - old.z)));
+    mu[i] = make_double4(nx, ny, nz, 0.0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  __shared__ double red[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kBlock / 32; ++w) s = fmax(s, red[w]);
+    partials[(size_t)blockIdx.x * kRedVals] = s;
+  }
+}
+
+__global__ void k_max_partials(const double* __restrict__ partials, int64_t blocks,
+                               double* __restrict__ res, int slot) {
+  __shared__ double s[256];
+  double m = 0.0;
+  for (int64_t b = threadIdx.x; b < blocks; b += 256) m = fmax(m, partials[b * kRedVals]);
+  s[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] = fmax(s[threadIdx.x], s[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) res[slot] = s[0];
+}
+
+int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, double tol,
+                   int64_t max_iter, double* last_resid) {
+  const int64_t n = c->n;
+  const int64_t blocks = grid_for(n);
+  ensure_partials(c, blocks);
+  zero_vec(c, c->mu);
+  for (int64_t it = 1; it <= max_iter; ++it) {
+    run_tmatvec(c, list_id, 0.0, cutoff, thole_a, c->mu, c->cg_q);
+    MDG_LAUNCH(c, "jacobi_update", (unsigned)blocks, kBlock, 0, k_jacobi_update, n, c->polp,
+               c->eperm, c->cg_q, c->mu, c->partials);
+    MDG_LAUNCH(c, "max_partials", 1, 256, 0, k_max_partials, c->partials, blocks, c->results, 30);
+    fetch_results(c);
+    *last_resid = c->h_results[30];
+    if (*last_resid <= tol) return it;
+  }
+  throw_error(MDG_CONVERGENCE, "jacobi_polarization_solve: no convergence after max_iter");
+}
+
+}  // namespace mdg

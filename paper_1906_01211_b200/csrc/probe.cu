@@ -1,0 +1,111 @@
+// probe.cu -- measurement helpers: FP64 DFMA peak probe (MEASURED_PEAKS.json
+// has no FP64 figure) and in-cutoff pair counts for roofline numerators.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace mdg {
+
+// 8 independent DFMA chains per thread, 148 x 8 blocks of 256 threads:
+// saturates the FP64 pipes; 2 flops per DFMA.
+__global__ void __launch_bounds__(256) k_dfma_peak(int iters, double seed, double* out) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4,
+         a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 123.456) out[0] = s;  // keep the chains alive
+}
+
+// pairs (full list, i != j) within cutoff, optionally excluding same-molecule
+// pairs: slot = total directed pairs
+__global__ void __launch_bounds__(kBlock) k_count_within(int64_t n, const double4* __restrict__ P,
+                                                         const int32_t* __restrict__ mol,
+                                                         int excl, ListView L, Box b, double c2,
+                                                         double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[2] = {0.0, 0.0};
+  if (i < n) {
+    const double4 pi = P[i];
+    const int cnt = L.cnt[i];
+    const int32_t* row = list_row(L, (int)i);
+    const int32_t mi = mol[i];
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(row + (size_t)k * 32);
+      const double4 pj = ldg4(P + j);
+      double dx, dy, dz;
+      const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      if (r2 <= c2 && !(excl && __ldg(mol + j) == mi)) acc[0] += 1.0;
+    }
+    acc[1] = (double)cnt;
+  }
+  block_store_partials<2>(acc, partials);
+}
+
+}  // namespace mdg
+
+extern "C" int mdg_probe_fp64_peak(int device, double* tflops) {
+  try {
+    mdg::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    int sms = 0;
+    mdg::cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device),
+                    "attr");
+    double* out;
+    mdg::cuda_check(cudaMalloc(&out, 8), "malloc");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, iters = 4096;
+    mdg::k_dfma_peak<<<blocks, 256>>>(64, 1.0, out);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(a);
+      mdg::k_dfma_peak<<<blocks, 256>>>(iters, 1.0, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (ms < best) best = ms;
+    }
+    mdg::cuda_check(cudaGetLastError(), "k_dfma_peak");
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 256;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    return MDG_OK;
+  } catch (const mdg::Error& e) {
+    return e.code;
+  }
+}
+
+extern "C" int mdg_nlist_count_within(mdg_ctx* c, int list_id, double cutoff, int exclude,
+                                      int64_t* directed_pairs, int64_t* list_slots) {
+  try {
+    if (!c || !c->has_system || list_id < 0 || list_id >= MDG_MAX_LISTS ||
+        !c->lists[list_id].valid)
+      return MDG_CONTRACT;
+    mdg::cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+    const mdg::DevList& L = c->lists[list_id];
+    const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+    const int64_t blocks = mdg::grid_for(c->n);
+    mdg::ensure_partials(c, blocks);
+    mdg::Box b = mdg::make_box(c->lx, c->ly, c->lz);
+    MDG_LAUNCH(c, "count_within", (unsigned)blocks, mdg::kBlock, 0, mdg::k_count_within, c->n, P,
+               c->mol, (exclude && c->has_mol) ? 1 : 0, mdg::ListView{L.nbr, L.cnt, L.cap}, b,
+               cutoff * cutoff, c->partials);
+    mdg::finalize_partials(c, blocks, 2, 50, 1.0);
+    mdg::fetch_results(c);
+    if (directed_pairs) *directed_pairs = (int64_t)c->h_results[50];
+    if (list_slots) *list_slots = (int64_t)c->h_results[51];
+    return MDG_OK;
+  } catch (const mdg::Error& e) {
+    return e.code;
+  }
+}

@@ -1,0 +1,390 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+identical seeded inputs. Mirrors the reference suites
+(proj/tests/test_neighbors.cpp, test_kernels.cpp, test_polar.cpp,
+acceptance.cpp). Tolerances (BASELINE.json north_star): pair sets bit-exact,
+energies 1e-9 relative, forces 1e-8 x RMS force per component, induced
+dipoles within the 1e-5 D solver tolerance."""
+import numpy as np
+import pytest
+
+from conftest import force_err_max, force_err_rms, rel, to_oracle_system
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-9
+F_TOL = 1e-8
+
+
+def uniform(oracle, n, box, seed, min_sep=0.8):
+    return oracle.generate_system("uniform", n, (box, box, box), seed, min_sep)
+
+
+# ---------------------------------------------------------------- neighbour lists
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [32, 150, 700])
+def test_pairs_match_brute_force(engine, oracle, seed, n):
+    """proj/tests/test_neighbors.cpp:137-148 -- masked builder == O(N^2) oracle."""
+    s = uniform(oracle, n, 14.0, seed)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.4)
+    np.testing.assert_array_equal(t.pairs(), oracle.brute_force_pairs(s, 3.4))
+
+
+def test_pairs_match_reference_table_water(engine, oracle, mdg):
+    """Config-0 water box at the 11 A list: pair set identical to the oracle's
+    reference-layout table (itself identical to the reference, test_oracle.py)."""
+    s = mdg.water_box(1000, 31.04, 1, "charmm")
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(11.0)
+    o = oracle.build_table(to_oracle_system(s), 11.0)
+    np.testing.assert_array_equal(t.pairs(), o.pairs())
+    nn, n8, n16, off, idx = t.export()
+    # reference layout invariants (proj/tests/test_neighbors.cpp:40-66)
+    assert np.all(n16 % 16 == 0) and np.all(n8 % 8 == 0)
+    assert np.all(off % 16 == 0)
+    for i in range(0, len(nn), 97):
+        seg = idx[off[i]: off[i] + n16[i]]
+        if nn[i]:
+            assert np.all(seg[nn[i]:] == seg[nn[i] - 1])  # sentinel = last neighbour
+            assert np.all(seg[: nn[i]] > i)               # stored on the lower index
+
+
+def two_site(oracle, a, b, box):
+    from oracle.oracle import System
+    one = np.ones(2)
+    return System((box, box, box), np.array([a, b]), np.array([5.0, 5.0]),
+                  np.array([5.0, 5.0]), np.array([1.0, 1.0]), one.copy(), one.copy(),
+                  one.copy(), one.copy(), one.copy())
+
+
+def test_two_site_cases(engine, oracle):
+    """proj/tests/test_neighbors.cpp:81-109"""
+    s = two_site(oracle, 1.0, 3.0, 10.0)
+    engine.upload_system(s)
+    assert engine.build_neighbor_table(2.5).pairs().tolist() == [[0, 1]]
+    s = two_site(oracle, 0.8, 9.2, 10.0)  # neighbours only through the image
+    engine.upload_system(s)
+    assert engine.build_neighbor_table(2.0).pairs().tolist() == [[0, 1]]
+    s = two_site(oracle, 1.0, 6.0, 10.0)
+    engine.upload_system(s)
+    assert len(engine.build_neighbor_table(2.0).pairs()) == 0
+
+
+def test_eight_corners(engine, oracle):
+    """proj/tests/test_neighbors.cpp:111-135: all C(8,2) pairs via images."""
+    from oracle.oracle import System
+    g = np.array([[0.2 + 3.6 * a, 0.2 + 3.6 * b, 0.2 + 3.6 * c]
+                  for a in range(2) for b in range(2) for c in range(2)])
+    one = np.ones(8)
+    s = System((4.0, 4.0, 4.0), g[:, 0].copy(), g[:, 1].copy(), g[:, 2].copy(), np.zeros(8),
+               one, one, one, one, one)
+    engine.upload_system(s)
+    p = engine.build_neighbor_table(1.5).pairs()
+    assert len(p) == 28
+    np.testing.assert_array_equal(p, oracle.brute_force_pairs(s, 1.5))
+
+
+def test_lattice_system(engine, oracle):
+    """proj/tests/test_neighbors.cpp:206-212"""
+    s = oracle.generate_system("lattice", 216, (8.0, 8.0, 8.0), 2)
+    engine.upload_system(s)
+    np.testing.assert_array_equal(engine.build_neighbor_table(2.5).pairs(),
+                                  oracle.brute_force_pairs(s, 2.5))
+
+
+def test_invalid_cutoffs(engine, oracle, mdg):
+    """proj/tests/test_neighbors.cpp:224-230"""
+    s = uniform(oracle, 20, 10.0, 1)
+    engine.upload_system(s)
+    with pytest.raises(mdg.ContractViolation):
+        engine.build_neighbor_table(0.0)
+    with pytest.raises(mdg.ContractViolation):
+        engine.build_neighbor_table(6.1)
+
+
+def test_capacity_overflow(mdg, oracle):
+    """proj/tests/test_neighbors.cpp:214-222: a dense box overflows the
+    per-site capacity and raises CapacityError."""
+    s = oracle.generate_system("uniform", 6000, (9.0, 9.0, 9.0), 8, 0.05)
+    e = mdg.Engine(6000)
+    try:
+        e.upload_system(s)
+        with pytest.raises(mdg.CapacityError):
+            e.build_neighbor_table(4.4)
+    finally:
+        e.close()
+
+
+def test_position_outside_box_rejected(engine, oracle, mdg):
+    s = uniform(oracle, 20, 10.0, 1)
+    s.x[3] = 10.0
+    with pytest.raises(mdg.ContractViolation):
+        engine.upload_system(s)
+
+
+# ------------------------------------------------------------------ pair kernels
+def test_lj_closed_form(engine, oracle, mdg):
+    """proj/tests/test_kernels.cpp:72-84 (r^2 = 4, sigma = eps = 1): exact."""
+    s = two_site(oracle, 1.0, 3.0, 10.0)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.0)
+    out = engine.lj_forces(t, mdg.LjParams(3.0))
+    assert out.energy == -0.0615234375
+    assert out.fx[0] == -0.0908203125 * -2.0 and out.fx[1] == -out.fx[0]
+
+
+def test_ewald_closed_form(engine, oracle, mdg):
+    """proj/tests/test_kernels.cpp:86-97 (r = 3, alpha = 0.4)."""
+    s = two_site(oracle, 1.0, 4.0, 10.0)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.5)
+    out = engine.ewald_real_forces(t, mdg.EwaldRealParams(0.4, 3.5))
+    assert out.energy == pytest.approx(0.02989534059012154, rel=1e-14)
+    assert -out.fx[0] / 3.0 == pytest.approx(0.015203675487948578, rel=1e-14)
+    out = engine.ewald_real_forces(t, mdg.EwaldRealParams(0.0, 3.5))
+    assert out.energy == pytest.approx(1.0 / 3.0, rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [16, 100, 333])
+def test_nonpolar_random(engine, oracle, mdg, seed, n):
+    """proj/tests/test_kernels.cpp:111-143 with the GPU in place of the Vec path."""
+    s = uniform(oracle, n, 12.0, seed)
+    t_o = oracle.build_table(s, 3.7)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.7)
+    for kind in ("lj", "ewald", "halgren"):
+        if kind == "lj":
+            fo, eo, wo = oracle.lj(s, t_o, 3.0)
+            g = engine.lj_forces(t, mdg.LjParams(3.0))
+        elif kind == "ewald":
+            fo, eo, wo = oracle.ewald_real(s, t_o, 0.4, 3.7)
+            g = engine.ewald_real_forces(t, mdg.EwaldRealParams(0.4, 3.7))
+        else:
+            fo, eo, wo = oracle.halgren(s, t_o, 3.0)
+            g = engine.halgren_forces(t, mdg.HalgrenParams(3.0))
+        assert rel(g.energy, eo) <= E_TOL, kind
+        assert force_err_rms(g.forces, fo) <= F_TOL, kind
+        assert force_err_max(g.forces, fo) <= 1e-9, kind  # reference bench metric
+        np.testing.assert_allclose(g.virial, wo, rtol=0, atol=1e-9 * np.abs(wo).max() + 1e-300)
+
+
+def test_lj_shift(engine, oracle, mdg):
+    """proj/tests/test_kernels.cpp:288-310"""
+    s = uniform(oracle, 200, 12.0, 9)
+    t_o = oracle.build_table(s, 3.4)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.4)
+    fo, eo, _ = oracle.lj(s, t_o, 3.0, shift=True)
+    g = engine.lj_forces(t, mdg.LjParams(3.0, True))
+    assert rel(g.energy, eo) <= E_TOL
+    assert force_err_rms(g.forces, fo) <= F_TOL
+
+
+def test_kernel_cutoff_contract(engine, oracle, mdg):
+    """proj/tests/test_kernels.cpp:312-326: kernel cutoff beyond the list."""
+    s = uniform(oracle, 50, 12.0, 2)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.0)
+    with pytest.raises(mdg.ContractViolation):
+        engine.lj_forces(t, mdg.LjParams(3.5))
+    with pytest.raises(mdg.ContractViolation):
+        engine.ewald_real_forces(t, mdg.EwaldRealParams(-1.0, 3.0))
+
+
+def test_config0_water_with_exclusions(engine, oracle, mdg):
+    """Config 0 (BASELINE.json): 1000 waters, LJ + Ewald (alpha 0.35) at 9 A on
+    the 11 A list, intramolecular pairs excluded, electric constant applied.
+    Oracle: the reference kernels on an exclusion-filtered table."""
+    s = mdg.water_box(1000, 31.04, 1, "charmm")
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 11.0)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(11.0)
+    fo, eo, wo = oracle.lj(so, t_o, 9.0, exclude=True)
+    g = engine.lj_forces(t, mdg.LjParams(9.0), exclude=True)
+    assert rel(g.energy, eo) <= E_TOL
+    assert force_err_rms(g.forces, fo) <= F_TOL
+    fo, eo, wo = oracle.ewald_real(so, t_o, 0.35, 9.0, mdg.ELECTRIC, exclude=True)
+    g = engine.ewald_real_forces(t, mdg.EwaldRealParams(0.35, 9.0), mdg.ELECTRIC,
+                                 exclude=True)
+    assert rel(g.energy, eo) <= E_TOL
+    assert force_err_rms(g.forces, fo) <= F_TOL
+    np.testing.assert_allclose(g.virial, wo, rtol=0, atol=1e-9 * np.abs(wo).max())
+    # the fused step gives the same sums
+    p = mdg.CharmmParams(9.0, 0.35, mdg.ELECTRIC, 0, 1)
+    engine.charmm_step(t, p)
+    e, w, _, _ = engine.fetch_energies()
+    f = engine.fetch_forces()
+    flj, elj, wlj = oracle.lj(so, t_o, 9.0, exclude=True)
+    fe, ee, we = oracle.ewald_real(so, t_o, 0.35, 9.0, mdg.ELECTRIC, exclude=True)
+    assert rel(e[0], elj) <= E_TOL and rel(e[1], ee) <= E_TOL
+    assert force_err_rms(f, flj + fe) <= F_TOL
+    np.testing.assert_allclose(w, wlj + we, rtol=0, atol=1e-9 * np.abs(wlj + we).max())
+
+
+def test_imported_reference_table(engine, oracle, mdg):
+    """A reference-layout table (exclusion-filtered) fed
+    through mdg_nlist_import: the kernels see exactly that pair set."""
+    s = mdg.water_box(216, 18.6, 3, "charmm")
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 8.0).filtered(s.molecule)
+    engine.upload_system(s)
+    t = engine.import_table(t_o.nnvlst, t_o.offset, t_o.indices, 8.0)
+    np.testing.assert_array_equal(t.pairs(), t_o.pairs())
+    fo, eo, _ = oracle.ewald_real(so, t_o, 0.35, 8.0)
+    g = engine.ewald_real_forces(t, mdg.EwaldRealParams(0.35, 8.0))
+    assert rel(g.energy, eo) <= E_TOL
+    assert force_err_rms(g.forces, fo) <= F_TOL
+
+
+def test_halgren_reduced_sites(engine, oracle, mdg):
+    """Config-1 vdW: Halgren on H-reduced sites (factor 0.91), forces chain-ruled
+    onto atoms; oracle = reference kernel on host-reduced coordinates."""
+    s = mdg.water_box(1000, 31.04, 2, "amoeba")
+    xr, yr, zr = oracle.reduce_sites(to_oracle_system(s), s.hred_parent, s.hred_factor)
+    hx, hy, hz = mdg.reduce_sites_host(s)
+    assert np.array_equal(xr, hx) and np.array_equal(yr, hy) and np.array_equal(zr, hz)
+    so = to_oracle_system(s)
+    so.x, so.y, so.z = xr, yr, zr
+    t_o = oracle.build_table(so, 11.0)
+    fred, eo, wo = oracle.halgren(so, t_o, 9.0, exclude=True)
+    fo = oracle.reduce_forces(s.hred_parent, s.hred_factor, fred)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+    np.testing.assert_array_equal(t.pairs(), t_o.pairs())  # device reduction is bit-exact
+    g = engine.halgren_forces(t, mdg.HalgrenParams(9.0), exclude=True)
+    assert rel(g.energy, eo) <= E_TOL
+    assert force_err_rms(g.forces, fo) <= F_TOL
+
+
+# ------------------------------------------------------------------ polarization
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_reference_fields(engine, oracle, mdg, seed):
+    """proj/tests/test_polar.cpp:173-207: T mat-vec and charge field (alpha = 0)."""
+    s = uniform(oracle, 260, 12.0, seed)
+    t_o = oracle.build_table(s, 3.4)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.4)
+    mu = oracle.random_dipoles(s.n, seed + 100)
+    eo = oracle.tmatvec_thole(s, t_o, 3.0, 0.39, mu)
+    st = mdg.PolarizationState(mu[:, 0], mu[:, 1], mu[:, 2], 0.39)
+    g = engine.dipole_field_matvec(t, st, mdg.PolarParams(3.0, 0.39)).field
+    assert force_err_max(g, eo) <= 1e-9
+    eo = oracle.perm_field_thole(s, t_o, 3.0, 0.39)
+    g = engine.permanent_field(t, mdg.PolarParams(3.0, 0.39)).field
+    assert force_err_max(g, eo) <= 1e-9
+
+
+def test_hand_fields(engine, oracle, mdg):
+    """proj/tests/test_polar.cpp:117-171"""
+    from oracle.oracle import System
+    one = np.ones(2)
+    s = System((10.0,) * 3, np.array([2.0, 2.0]), np.array([2.0, 2.0]), np.array([2.0, 4.0]),
+               np.array([-3.0, 3.0]), one, one, one, one, one)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.0)
+    st = mdg.PolarizationState(np.zeros(2), np.zeros(2), np.array([0.0, 1.0]), 1e9)
+    f = engine.dipole_field_matvec(t, st, mdg.PolarParams(3.0, 1e9)).field
+    assert f[0] == pytest.approx([0, 0, 0.25], abs=1e-12)
+    st = mdg.PolarizationState(np.array([0.0, 1.0]), np.zeros(2), np.zeros(2), 1e9)
+    f = engine.dipole_field_matvec(t, st, mdg.PolarParams(3.0, 1e9)).field
+    assert f[0] == pytest.approx([-0.125, 0, 0], abs=1e-12)
+    f = engine.permanent_field(t, mdg.PolarParams(3.0, 1e9)).field
+    assert f[0][2] == pytest.approx(-0.75, abs=1e-12) and f[1][2] == pytest.approx(-0.75, abs=1e-12)
+
+
+def test_jacobi_matches_oracle(engine, oracle, mdg):
+    """proj/tests/test_polar.cpp:298-376 (converging small systems)."""
+    for n in (6, 15):
+        s = uniform(oracle, n, 9.0, 21)
+        t_o = oracle.build_table(s, 3.0)
+        mu_o, _ = oracle.jacobi(s, t_o, 3.0, 0.39, 1e-12, 500)
+        engine.upload_system(s)
+        t = engine.build_neighbor_table(3.0)
+        st = engine.jacobi_polarization_solve(t, mdg.PolarParams(3.0, 0.39), 1e-12, 500)
+        assert np.max(np.abs(st.mu - mu_o)) <= 1e-10 * max(1.0, np.abs(mu_o).max())
+
+
+def test_jacobi_nonconvergence(engine, oracle, mdg):
+    """proj/tests/test_polar.cpp:378-389"""
+    s = uniform(oracle, 30, 9.0, 13)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(3.0)
+    with pytest.raises(mdg.ConvergenceError) as ei:
+        engine.jacobi_polarization_solve(t, mdg.PolarParams(3.0, 0.39), 1e-300, 2)
+    assert ei.value.last_residual > 0
+
+
+def amoeba_small(mdg, n_mol=1000, box=31.04, seed=4):
+    return mdg.water_box(n_mol, box, seed, "amoeba")
+
+
+def test_ewald_tmatvec_and_field(engine, oracle, mdg):
+    """Ewald + Thole T and q/mu/Theta field (extensions) vs the oracle."""
+    s = amoeba_small(mdg)
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 9.0)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.0)
+    mu = oracle.random_dipoles(s.n_sites, 7, 0.05)
+    eo = oracle.tmatvec_ewald(so, t_o, 0.5446, 7.0, 0.39, mu)
+    st = mdg.PolarizationState(mu[:, 0], mu[:, 1], mu[:, 2], 0.39)
+    g = engine.dipole_field_matvec(t, st, mdg.PolarParams(7.0, 0.39), alpha=0.5446).field
+    assert force_err_rms(g, eo) <= F_TOL
+    eo = oracle.perm_field_ewald(so, t_o, 0.5446, 7.0, 0.39, exclude=True)
+    g = engine.permanent_field(t, mdg.PolarParams(7.0, 0.39), alpha=0.5446, exclude=True).field
+    assert force_err_rms(g, eo) <= F_TOL
+
+
+def test_pcg_matches_oracle(engine, oracle, mdg):
+    """Config-2 solver on a 3000-atom box: same iterations (+-1) and dipoles
+    within the 1e-5 D tolerance."""
+    s = amoeba_small(mdg)
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 9.0)
+    ep = oracle.perm_field_ewald(so, t_o, 0.5446, 7.0, 0.39, exclude=True)
+    mu_o, it_o, rms_o = oracle.pcg(so, t_o, 0.5446, 7.0, 0.39, ep, 1e-5, 100)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.0)
+    st = engine.polar_solve_pcg(t, mdg.PolarParams(7.0, 0.39), alpha=0.5446, tol_debye=1e-5,
+                                max_iter=100, exclude_perm=True)
+    assert abs(st.iterations - it_o) <= 1
+    d = np.sqrt(np.mean(np.sum((st.mu - mu_o) ** 2, 1))) * mdg.DEBYE
+    assert d < 1e-5
+
+
+def test_mpole_matches_oracle(engine, oracle, mdg):
+    """Real-space multipole energy/forces/torques/virial vs the T-tensor oracle."""
+    s = amoeba_small(mdg, 343, 21.0, 5)
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 9.0)
+    fo, to, eo, wo = oracle.mpole(so, t_o, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.0)
+    f, tq, e, w = engine.mpole_forces(t, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+    assert rel(e, eo) <= E_TOL
+    assert force_err_rms(f, fo) <= F_TOL
+    assert force_err_rms(tq, to) <= F_TOL
+    np.testing.assert_allclose(w, wo, rtol=0, atol=1e-9 * np.abs(wo).max())
+
+
+def test_amoeba_step_composes(engine, oracle, mdg):
+    """The fused config-1..4 step == its parts."""
+    s = amoeba_small(mdg, 343, 21.0, 6)
+    engine.upload_system(s)
+    tv = engine.build_neighbor_table(10.0, list_id=1, sites=mdg.SITES_VDW)
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1)
+    engine.amoeba_step(tv, te, p)
+    e, w, iters, rms = engine.fetch_energies()
+    f = engine.fetch_forces()
+    mu = engine.fetch_dipoles()
+    hv = engine.halgren_forces(tv, mdg.HalgrenParams(9.0), exclude=True)
+    fm, _, em, wm = engine.mpole_forces(te, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+    st = engine.polar_solve_pcg(te, mdg.PolarParams(7.0, 0.39), 0.5446, 1e-5, 100, True)
+    assert e[0] == hv.energy and e[1] == em
+    assert np.array_equal(f, hv.forces + fm)
+    assert iters == st.iterations and rms < 1e-5
+    assert np.array_equal(mu, st.mu)
+    np.testing.assert_allclose(w, hv.virial + wm, rtol=1e-12, atol=1e-12)
