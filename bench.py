@@ -156,22 +156,46 @@ class Workload:
                 self.rebuild()
             self.step()
 
-    # roofline: (kernel name) -> algorithmic flops per launch
-    def algorithmic_flops(self, kernel: str) -> float | None:
-        from paper_1906_01211_b200.flops import PER_PAIR
-        c = self.c
-        if kernel not in PER_PAIR:
+    # roofline: (kernel name) -> ("fp64", flops) | ("hbm", bytes) per launch
+    def algorithmic_work(self, kernel: str):
+        from paper_1906_01211_b200.flops import PAIRS_OF, PER_PAIR_FLOPS, stream_bytes
+        if kernel not in PAIRS_OF:
             return None
-        if kernel in ("lj", "ewald_real", "lj_ewald"):
-            lid, cut, excl = 0, c.get("cutoff", 9.0), True
-        elif kernel == "halgren":
-            lid, cut, excl = 1, c["vdw_cutoff"], True
-        elif kernel in ("mpole", "perm_field"):
-            lid, cut, excl = 0, c["elec_cutoff"], True
-        else:  # T mat-vec: every pair, intramolecular included
-            lid, cut, excl = 0, c["elec_cutoff"], False
-        directed, _ = self.eng.count_within(self.tables[lid], cut, excl)
-        return PER_PAIR[kernel] * directed / 2.0
+        role, key, excl = PAIRS_OF[kernel]
+        lid = 1 if role == "vdw" else 0
+        directed, _ = self.eng.count_within(self.tables[lid], self.c[key], excl)
+        if kernel in PER_PAIR_FLOPS:
+            return "fp64", PER_PAIR_FLOPS[kernel] * directed / 2.0
+        return "hbm", stream_bytes(kernel, self.n, directed)
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
+    work = wl.algorithmic_work(name)
+    if work is None:
+        return None
+    avg_ms = tot_ms / cnt
+    kind, amount = work
+    if kind == "fp64":
+        achieved = amount / (avg_ms * 1e-3) / 1e12
+        peak, unit, src = fp64_peak, "TFLOP/s", "measured DFMA probe in this run (of measured)"
+    else:
+        achieved = amount / (avg_ms * 1e-3) / 1e9
+        peak, src = hbm_peak()
+        unit = "GB/s"
+    return {"bound": "fp64" if kind == "fp64" else "hbm", "kernel": name,
+            "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "avg_launch_ms": round(avg_ms, 4), "peak_source": src,
+            ("flops_per_launch" if kind == "fp64" else "bytes_per_launch"): amount,
+            "share_of_step": round(tot_ms / step_ms, 4)}
 
 
 def run_mine(args, world, rank, local):
@@ -210,20 +234,19 @@ def run_mine(args, world, rank, local):
         ms = float(t.item())
     energies, virial, iters, rms = eng.fetch_energies()
 
-    # ---- roofline of the dominant kernel
-    top = max(prof.items(), key=lambda kv: kv[1][1])
-    name, (cnt, tot_ms) = top
-    avg_ms = tot_ms / cnt
-    flops = wl.algorithmic_flops(name)
+    # ---- roofline of the dominant kernel (+ every pair kernel, for the record)
+    ranked = sorted(prof.items(), key=lambda kv: -kv[1][1])
     roof = None
-    if flops is not None:
-        achieved = flops / (avg_ms * 1e-3) / 1e12
-        roof = {"bound": "fp64", "kernel": name, "achieved": round(achieved, 3),
-                "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "avg_launch_ms": round(avg_ms, 4),
-                "peak_source": "measured DFMA probe (MEASURED_PEAKS.json has no FP64 figure)",
-                "flops_per_launch": flops,
-                "share_of_step": round(tot_ms / ms, 4)}
+    others = {}
+    for name, (cnt, tot_ms) in ranked:
+        r = roofline_of(wl, name, cnt, tot_ms, ms, peak)
+        if r is None:
+            continue
+        if roof is None:
+            roof = r
+        else:
+            others[name] = {k: r[k] for k in ("bound", "achieved", "unit", "frac",
+                                              "avg_launch_ms", "share_of_step")}
 
     # ---- end to end through the C ABI with host buffers
     e2e = None
@@ -283,6 +306,7 @@ def run_mine(args, world, rank, local):
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": roof,
+        "roofline_other_kernels": others,
         "clocks": clk.summary(),
         "energies_kcal_mol": [float(v) for v in energies[:3]],
         "pcg_iters": int(iters),

@@ -192,6 +192,8 @@ int mdg_amoeba_step(mdg_ctx* ctx, int vdw_list, int elec_list, const mdg_amoeba_
 int mdg_fetch_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz);
 int mdg_fetch_torques(mdg_ctx* ctx, double* tx, double* ty, double* tz);
 int mdg_fetch_dipoles(mdg_ctx* ctx, double* mux, double* muy, double* muz);
+/* Permanent field (PCG right-hand side) of the last step / PCG solve. */
+int mdg_fetch_perm_field(mdg_ctx* ctx, double* ex, double* ey, double* ez);
 int mdg_fetch_energies(mdg_ctx* ctx, double* energies4, double* virial9, int64_t* pcg_iters,
                        double* pcg_rms);
 

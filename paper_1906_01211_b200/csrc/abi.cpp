@@ -612,11 +612,12 @@ int mdg_polar_solve_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, do
     need(alpha >= 0, "pcg: alpha must be nonnegative");
     mdg::DevList& L = need_list(c, list_id);
     need_kernel_cutoff(L, cutoff);
-    mdg::run_perm_field(c, list_id, alpha, cutoff, thole_a, exclude_perm, c->eperm);
+    need(L.sites == MDG_SITES_ATOMIC, "pcg needs a list over atomic sites");
+    mdg::prune_list(c, list_id, cutoff);
+    mdg::run_field_tpre(c, alpha, thole_a, exclude_perm);
     double rms = 0;
     try {
-      const int64_t it = mdg::run_pcg(c, list_id, alpha, cutoff, thole_a, tol_debye, max_iter,
-                                      &rms);
+      const int64_t it = mdg::run_pcg_pre(c, tol_debye, max_iter, &rms);
       if (iters) *iters = it;
     } catch (const mdg::Error&) {
       if (last_rms_debye) *last_rms_debye = rms;
@@ -678,19 +679,19 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
     } else {
       mdg::zero_vec(c, c->force);
     }
+    // one pruned 7 A list per step feeds the multipole, field and T kernels
+    if (terms & (MDG_TERM_MPOLE | MDG_TERM_POLAR)) mdg::prune_list(c, elec_list, p->elec_cutoff);
     if (terms & MDG_TERM_MPOLE) {
-      mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
+      mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
     } else {
       mdg::zero_vec(c, c->torque);
     }
     c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
     c->pcg_rms = 0;
     if (terms & MDG_TERM_POLAR) {
-      mdg::run_perm_field(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude,
-                          c->eperm);
+      mdg::run_field_tpre(c, p->alpha, p->thole_a, p->exclude);
       double rms = 0;
-      c->pcg_iters = mdg::run_pcg(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a,
-                                  p->tol_debye, p->max_iter, &rms);
+      c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
       c->pcg_rms = rms;
       mdg::polar_energy(c, p->electric, 40);
     }
@@ -739,6 +740,13 @@ int mdg_fetch_dipoles(mdg_ctx* c, double* mux, double* muy, double* muz) {
   return guard([&] {
     need_system(c);
     vec_out(c, c->mu, mux, muy, muz);
+  });
+}
+
+int mdg_fetch_perm_field(mdg_ctx* c, double* ex, double* ey, double* ez) {
+  return guard([&] {
+    need_system(c);
+    vec_out(c, c->eperm, ex, ey, ez);
   });
 }
 

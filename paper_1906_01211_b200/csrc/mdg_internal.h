@@ -53,6 +53,21 @@ struct DevList {
   int32_t max_cnt = 0;
 };
 
+// Pruned list: the pairs of a source list within a kernel cutoff, compacted
+// per site (same sliced-ELL layout), j | 0x80000000 when i, j share a
+// molecule; trr holds the Ewald/Thole T pair tensor (rr3, rr5) per slot.
+struct PrunedList {
+  bool valid = false;
+  int src = -1;
+  double cutoff = 0;
+  int32_t cap = 0;
+  int32_t* nbr = nullptr;
+  int32_t* cnt = nullptr;
+  double2* trr = nullptr;
+  size_t elems = 0;
+  int64_t directed = 0;
+};
+
 struct ProfEntry {
   int64_t count = 0;
   double ms = 0;
@@ -124,6 +139,7 @@ struct mdg_ctx {
   size_t stage_bytes = 0;
 
   mdg::DevList lists[MDG_MAX_LISTS];
+  mdg::PrunedList plist;
 
   // last step
   double energies[4] = {0, 0, 0, 0};
@@ -176,6 +192,8 @@ void finalize_partials(mdg_ctx* c, int64_t blocks, int nvals, int slot, double s
 void fetch_results(mdg_ctx* c);
 
 void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites);
+// max and sum of per-site counts -> results[slot], results[slot + 1]
+void count_stats(mdg_ctx* c, const int32_t* cnt, int slot);
 
 struct NonpolarArgs {
   int do_lj, do_coul, shift, exclude;
@@ -200,6 +218,15 @@ int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, doubl
                    int64_t max_iter, double* last_resid);
 void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
                int exclude, bool accumulate);
+// multipoles over the pruned list (c->plist)
+void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate);
+// Prune list_id to `cutoff` into c->plist (exclusion flags from c->mol).
+void prune_list(mdg_ctx* c, int list_id, double cutoff);
+// Permanent field over c->plist into c->eperm, storing T pair tensors in
+// c->plist.trr (one pass: shared bn/Thole terms).
+void run_field_tpre(mdg_ctx* c, double alpha, double thole_a, int exclude);
+// PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
+int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
 void run_reduce_sites(mdg_ctx* c);
 
 // permutation helpers (device kernels)

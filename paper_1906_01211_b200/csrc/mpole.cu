@@ -43,7 +43,7 @@ __device__ __forceinline__ void qmul(const Quad& Q, double x, double y, double z
 }
 
 // partial slots: 0 energy, 1..9 virial (row-major)
-template <bool EXCL>
+template <bool EXCL, bool PRUNED>
 __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
   const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
   double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -58,12 +58,14 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
     const int32_t* row = list_row(a.L, (int)i);
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(row + (size_t)k * 32);
+      const int32_t raw = __ldg(row + (size_t)k * 32);
+      if (PRUNED && EXCL && raw < 0) continue;  // same molecule (flag bit)
+      const int32_t j = PRUNED ? (raw & 0x7fffffff) : raw;
       const double4 pj = ldg4(a.pos + j);
       double x, y, z;
       const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
-      if (!(r2 <= a.c2)) continue;
-      if (EXCL && __ldg(a.mol + j) == mi) continue;
+      if (!PRUNED && !(r2 <= a.c2)) continue;
+      if (!PRUNED && EXCL && __ldg(a.mol + j) == mi) continue;
       const double4 m0j = ldg4(a.mp + 3 * (size_t)j), m1j = ldg4(a.mp + 3 * (size_t)j + 1);
       const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
       const double qj = pj.w, djx = m0j.x, djy = m0j.y, djz = m0j.z;
@@ -195,9 +197,34 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;
   if (exclude && c->has_mol)
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, k_mpole<true>, k);
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<true, false>), k);
   else
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, k_mpole<false>, k);
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<false, false>), k);
+  finalize_partials(c, blocks, 10, 10, 0.5);
+}
+
+void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate) {
+  const PrunedList& P = c->plist;
+  MKArgs k;
+  k.n_i = c->n;
+  k.pos = c->pos;
+  k.mp = c->mp;
+  k.mol = c->mol;
+  k.L = ListView{P.nbr, P.cnt, P.cap};
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.c2 = P.cutoff * P.cutoff;
+  k.alpha = alpha;
+  k.electric = electric;
+  k.force = c->force;
+  k.torque = c->torque;
+  const int64_t blocks = grid_for(c->n);
+  ensure_partials(c, blocks);
+  k.partials = c->partials;
+  k.accumulate = accumulate ? 1 : 0;
+  if (exclude && c->has_mol)
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<true, true>), k);
+  else
+    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<false, true>), k);
   finalize_partials(c, blocks, 10, 10, 0.5);
 }
 

@@ -163,6 +163,10 @@ __global__ void k_count_stats(int64_t n, const int32_t* __restrict__ cnt,
   }
 }
 
+void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
+  MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, c->n, cnt, c->results, slot);
+}
+
 static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
   const int64_t groups = (c->n + 31) / 32;
   const size_t need = (size_t)groups * (size_t)cap * 32;

@@ -5,6 +5,7 @@
 // field, Jacobi). With alpha > 0 the pair tensors are the real-space Ewald
 // ones, rr3 = B1 - (1-l3)/r^3, rr5 = B2 - 3(1-l5)/r^5, rr7 = B3 - 15(1-l7)/r^7;
 // at alpha == 0 the kernels use the reference's l3/r^3, 3 l5/r^5 forms.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -429,6 +430,254 @@ int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, doubl
     if (*last_resid <= tol) return it;
   }
   throw_error(MDG_CONVERGENCE, "jacobi_polarization_solve: no convergence after max_iter");
+}
+
+// =============================================================================
+// Pruned list + precomputed T: the 7 A kernels of one step share one pass
+// over the 9 A list. The pair tensors (rr3, rr5) do not change during the
+// solve, so the PCG mat-vec streams them (16 B/slot) instead of recomputing
+// erfc/exp/sqrt/div every iteration: the solve becomes HBM-bound.
+// =============================================================================
+
+__global__ void __launch_bounds__(kBlock) k_prune(int64_t n, const double4* __restrict__ P,
+                                                  const int32_t* __restrict__ mol, ListView src,
+                                                  Box b, double c2, int32_t cap,
+                                                  int32_t* __restrict__ out,
+                                                  int32_t* __restrict__ ocnt) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (i >= n) return;
+  const double4 pi = P[i];
+  const int32_t mi = mol[i];
+  const int cnt = src.cnt[i];
+  const int32_t* row = list_row(src, (int)i);
+  int32_t* orow = out + (size_t)(i >> 5) * (size_t)cap * 32 + (i & 31);
+  int32_t k2 = 0;
+  for (int k = 0; k < cnt; ++k) {
+    const int32_t j = __ldg(row + (size_t)k * 32);
+    const double4 pj = ldg4(P + j);
+    double dx, dy, dz;
+    const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+    if (r2 <= c2) {
+      if (k2 < cap) orow[(size_t)k2 * 32] = (__ldg(mol + j) == mi) ? (j | (int32_t)0x80000000) : j;
+      ++k2;
+    }
+  }
+  ocnt[i] = k2;
+}
+
+void prune_list(mdg_ctx* c, int list_id, double cutoff) {
+  const DevList& L = c->lists[list_id];
+  PrunedList& P = c->plist;
+  const int64_t n = c->n;
+  const double vol = c->lx * c->ly * c->lz;
+  const double expect = (double)n / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
+  int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
+  cap = std::max<int32_t>(32, (cap + 7) & ~7);
+  if (P.cap > cap) cap = std::min(P.cap, L.cap);
+  const Box b = make_box(c->lx, c->ly, c->lz);
+  const double4* X = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const size_t need = (size_t)((n + 31) / 32) * (size_t)cap * 32;
+    if (need > P.elems) {
+      if (P.nbr) cudaFree(P.nbr);
+      if (P.trr) cudaFree(P.trr);
+      P.nbr = nullptr;
+      P.trr = nullptr;
+      MDG_CUDA_CHECK(cudaMalloc(&P.nbr, need * sizeof(int32_t)));
+      MDG_CUDA_CHECK(cudaMalloc(&P.trr, need * sizeof(double2)));
+      P.elems = need;
+    }
+    if (!P.cnt) MDG_CUDA_CHECK(cudaMalloc(&P.cnt, (size_t)c->n_cap * sizeof(int32_t)));
+    P.cap = cap;
+    MDG_LAUNCH(c, "prune", grid_for(n), kBlock, 0, k_prune, n, X, c->mol,
+               ListView{L.nbr, L.cnt, L.cap}, b, cutoff * cutoff, cap, P.nbr, P.cnt);
+    count_stats(c, P.cnt, 62);
+    fetch_results(c);
+    const int32_t mx = (int32_t)c->h_results[62];
+    if (mx <= cap) {
+      P.valid = true;
+      P.src = list_id;
+      P.cutoff = cutoff;
+      P.directed = (int64_t)c->h_results[63];
+      return;
+    }
+    cap = (mx + 7) & ~7;
+  }
+  throw_error(MDG_CUDA, "prune_list: capacity retry failed");
+}
+
+struct FTArgs {
+  int64_t n;
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  const double4* __restrict__ mp;
+  ListView L;  // pruned
+  double2* __restrict__ trr;
+  Box b;
+  double alpha, thole_a;
+  double4* __restrict__ out;
+};
+
+// One pass over the pruned list: T tensors for every pair (u-scale 1) and the
+// permanent field of q + mu + Theta from non-excluded pairs (d-scale 0).
+template <bool MPOLE, bool EXCL>
+__global__ void __launch_bounds__(kBlock) k_field_tpre(FTArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (i >= a.n) return;
+  const double4 pi = a.pos[i];
+  const double2 ai = a.polp[i];
+  const int cnt = a.L.cnt[i];
+  const size_t base = (size_t)(i >> 5) * (size_t)a.L.cap * 32 + (i & 31);
+  double ex = 0, ey = 0, ez = 0;
+  for (int k = 0; k < cnt; ++k) {
+    const int32_t raw = __ldg(a.L.nbr + base + (size_t)k * 32);
+    const int32_t j = raw & 0x7fffffff;
+    const double4 pj = ldg4(a.pos + j);
+    double dx, dy, dz;
+    const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+    const double2 aj = __ldg(a.polp + j);
+    const double r = sqrt(r2);
+    const double inv_r2 = 1.0 / r2;
+    double l3, l5, l7;
+    thole7(r, ai.y * aj.y, a.thole_a, l3, l5, l7);
+    double bn[4];
+    ewald_bn<3>(r, r2, inv_r2, a.alpha, bn);
+    const double b1 = inv_r2 / r, b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
+    const double rr3 = bn[1] - (1.0 - l3) * b1;
+    const double rr5 = bn[2] - (1.0 - l5) * b2;
+    a.trr[base + (size_t)k * 32] = make_double2(rr3, rr5);
+    if (EXCL && raw < 0) continue;
+    if (!MPOLE) {
+      const double cq = rr3 * pj.w;
+      ex += cq * dx;
+      ey += cq * dy;
+      ez += cq * dz;
+    } else {
+      const double rr7 = bn[3] - (1.0 - l7) * b3;
+      const double4 m0 = ldg4(a.mp + 3 * (size_t)j);
+      const double4 m1 = ldg4(a.mp + 3 * (size_t)j + 1);
+      const double qzz = __ldg(&a.mp[3 * (size_t)j + 2].x);
+      const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
+      const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
+      const double qz = m1.y * dx + m1.w * dy + qzz * dz;
+      const double dr = m0.x * dx + m0.y * dy + m0.z * dz;
+      const double qr = dx * qx + dy * qy + dz * qz;
+      const double cc = rr3 * pj.w + rr5 * dr + rr7 * qr;
+      const double t5 = 2.0 * rr5;
+      ex += cc * dx - rr3 * m0.x - t5 * qx;
+      ey += cc * dy - rr3 * m0.y - t5 * qy;
+      ez += cc * dz - rr3 * m0.z - t5 * qz;
+    }
+  }
+  a.out[i] = make_double4(ex, ey, ez, 0.0);
+}
+
+void run_field_tpre(mdg_ctx* c, double alpha, double thole_a, int exclude) {
+  PrunedList& P = c->plist;
+  FTArgs k;
+  k.n = c->n;
+  k.pos = c->pos;
+  k.polp = c->polp;
+  k.mp = c->mp;
+  k.L = ListView{P.nbr, P.cnt, P.cap};
+  k.trr = P.trr;
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.alpha = alpha;
+  k.thole_a = thole_a;
+  k.out = c->eperm;
+  const bool mp = c->has_mpoles, ex = exclude && c->has_mol;
+  const unsigned g = grid_for(c->n);
+  if (mp && ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<true, true>), k);
+  else if (mp) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<true, false>), k);
+  else if (ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<false, true>), k);
+  else MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<false, false>), k);
+}
+
+struct TPArgs {
+  int64_t n;
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  ListView L;
+  const double2* __restrict__ trr;
+  Box b;
+  const double4* __restrict__ in;
+  double4* __restrict__ out;
+  double* __restrict__ partials;
+};
+
+// E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; PCG form
+// writes q = p/alpha - T p and the block partial of p.q.
+template <bool PCG>
+__global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < a.n) {
+    const double4 pi = a.pos[i];
+    const int cnt = a.L.cnt[i];
+    const size_t base = (size_t)(i >> 5) * (size_t)a.L.cap * 32 + (i & 31);
+    double ex = 0, ey = 0, ez = 0;
+    for (int k = 0; k < cnt; ++k) {
+      const int32_t j = __ldg(a.L.nbr + base + (size_t)k * 32) & 0x7fffffff;
+      const double2 rr = __ldg(a.trr + base + (size_t)k * 32);
+      const double4 pj = ldg4(a.pos + j);
+      const double4 mj = ldg4(a.in + j);
+      double dx, dy, dz;
+      min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
+      ex += rr.y * dot * dx - rr.x * mj.x;
+      ey += rr.y * dot * dy - rr.x * mj.y;
+      ez += rr.y * dot * dz - rr.x * mj.z;
+    }
+    if (PCG) {
+      const double4 p = a.in[i];
+      const double inva = 1.0 / a.polp[i].x;
+      const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
+      a.out[i] = make_double4(qx, qy, qz, 0.0);
+      acc[0] = p.x * qx + p.y * qy + p.z * qz;
+    } else {
+      a.out[i] = make_double4(ex, ey, ez, 0.0);
+    }
+  }
+  if (PCG) block_store_partials<1>(acc, a.partials);
+}
+
+int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
+  const int64_t n = c->n;
+  const int64_t blocks = grid_for(n);
+  ensure_partials(c, blocks);
+  PrunedList& P = c->plist;
+  TPArgs k;
+  k.n = n;
+  k.pos = c->pos;
+  k.polp = c->polp;
+  k.L = ListView{P.nbr, P.cnt, P.cap};
+  k.trr = P.trr;
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.partials = c->partials;
+  MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
+  k.in = c->mu;
+  k.out = c->cg_q;
+  MDG_LAUNCH(c, "tmatvec_pre", (unsigned)blocks, kBlock, 0, k_tmatvec_pre<false>, k);
+  MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
+             c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
+  MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
+             c->results);
+  k.in = c->cg_p;
+  k.out = c->cg_q;
+  for (int64_t it = 1; it <= max_iter; ++it) {
+    MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, k_tmatvec_pre<true>, k);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 1, n, tol_debye,
+               c->results);
+    MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
+               c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
+               c->results);
+    fetch_results(c);
+    *last_rms = c->h_results[25];
+    if (c->h_results[27] != 0.0) return it;
+    MDG_LAUNCH(c, "cg_dir", grid_for(n, 256), 256, 0, k_cg_dir, n, c->results, c->cg_z, c->cg_p);
+  }
+  throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
 }
 
 }  // namespace mdg

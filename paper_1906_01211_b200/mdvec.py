@@ -108,6 +108,7 @@ SIGNATURES = {
     "mdg_fetch_torques": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_fetch_dipoles": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_fetch_energies": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _dp]),
+    "mdg_fetch_perm_field": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mdg_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_profile_reset": (C.c_int, [C.c_void_p]),
@@ -491,6 +492,11 @@ class Engine:
         mx, my, mz = self._vec3()
         check(self.lib.mdg_fetch_dipoles(self.ctx, _p(mx), _p(my), _p(mz)))
         return np.stack([mx, my, mz], 1)
+
+    def fetch_perm_field(self) -> np.ndarray:
+        ex, ey, ez = self._vec3()
+        check(self.lib.mdg_fetch_perm_field(self.ctx, _p(ex), _p(ey), _p(ez)))
+        return np.stack([ex, ey, ez], 1)
 
     def fetch_energies(self):
         e = np.zeros(4)

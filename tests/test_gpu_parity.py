@@ -352,6 +352,8 @@ def test_pcg_matches_oracle(engine, oracle, mdg):
     assert abs(st.iterations - it_o) <= 1
     d = np.sqrt(np.mean(np.sum((st.mu - mu_o) ** 2, 1))) * mdg.DEBYE
     assert d < 1e-5
+    # the fused field + T-precompute pass produced the same right-hand side
+    assert force_err_rms(engine.fetch_perm_field(), ep) <= F_TOL
 
 
 def test_mpole_matches_oracle(engine, oracle, mdg):
