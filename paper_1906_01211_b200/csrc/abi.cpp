@@ -203,6 +203,9 @@ int mdg_ctx_destroy(mdg_ctx* c) {
     if (L.nbr) cudaFree(L.nbr);
     if (L.cnt) cudaFree(L.cnt);
   }
+  if (c->plist.nbr) cudaFree(c->plist.nbr);
+  if (c->plist.cnt) cudaFree(c->plist.cnt);
+  if (c->plist.trr) cudaFree(c->plist.trr);
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& pe : c->pending) {
@@ -382,16 +385,15 @@ int mdg_nlist_size(mdg_ctx* c, int list_id, int64_t* half_pairs, int64_t* padded
     mdg::DevList& L = need_list(c, list_id);
     if (half_pairs) *half_pairs = L.half_pairs;
     if (padded_slots) {
-      std::vector<int32_t> cnt(c->n), nbr(L.nbr_elems);
+      std::vector<int32_t> cnt(c->n), nbr((size_t)c->n * L.cap);
       MDG_CUDA_CHECK(cudaMemcpy(cnt.data(), L.cnt, c->n * 4, cudaMemcpyDeviceToHost));
-      MDG_CUDA_CHECK(cudaMemcpy(nbr.data(), L.nbr, ((c->n + 31) / 32) * (size_t)L.cap * 32 * 4,
-                                cudaMemcpyDeviceToHost));
+      MDG_CUDA_CHECK(cudaMemcpy(nbr.data(), L.nbr, nbr.size() * 4, cudaMemcpyDeviceToHost));
       std::vector<int64_t> upper(c->n, 0);
       for (int64_t s = 0; s < c->n; ++s) {
         const int32_t o = c->perm[s];
-        const int32_t* row = nbr.data() + (size_t)(s >> 5) * L.cap * 32 + (s & 31);
+        const int32_t* row = nbr.data() + (size_t)s * L.cap;
         for (int32_t k = 0; k < cnt[s]; ++k)
-          if (c->perm[row[(size_t)k * 32]] > o) upper[o]++;
+          if (c->perm[row[k]] > o) upper[o]++;
       }
       int64_t tot = 0;
       for (int64_t i = 0; i < c->n; ++i) tot += pad_count(upper[i], 16);
@@ -408,15 +410,15 @@ int mdg_nlist_export(mdg_ctx* c, int list_id, uint32_t* nnvlst, uint32_t* nvloop
     set_device(c);
     mdg::DevList& L = need_list(c, list_id);
     const int64_t n = c->n;
-    std::vector<int32_t> cnt(n), nbr(((n + 31) / 32) * (size_t)L.cap * 32);
+    std::vector<int32_t> cnt(n), nbr((size_t)n * L.cap);
     MDG_CUDA_CHECK(cudaMemcpy(cnt.data(), L.cnt, n * 4, cudaMemcpyDeviceToHost));
     MDG_CUDA_CHECK(cudaMemcpy(nbr.data(), L.nbr, nbr.size() * 4, cudaMemcpyDeviceToHost));
     std::vector<std::vector<int32_t>> rows(n);
     for (int64_t s = 0; s < n; ++s) {
       const int32_t o = c->perm[s];
-      const int32_t* row = nbr.data() + (size_t)(s >> 5) * L.cap * 32 + (s & 31);
+      const int32_t* row = nbr.data() + (size_t)s * L.cap;
       for (int32_t k = 0; k < cnt[s]; ++k) {
-        const int32_t jo = c->perm[row[(size_t)k * 32]];
+        const int32_t jo = c->perm[row[k]];
         if (jo > o) rows[o].push_back(jo);
       }
     }
@@ -466,9 +468,8 @@ int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
     }
     need(mx <= c->max_pairs, "nlist_import: a site exceeds the context's pair capacity");
     mdg::DevList& L = c->lists[list_id];
-    const int32_t cap = std::max<int32_t>(8, (mx + 7) & ~7);
-    const size_t groups = (n + 31) / 32;
-    const size_t need_el = groups * (size_t)cap * 32;
+    const int32_t cap = std::max<int32_t>(32, (mx + 31) & ~31);
+    const size_t need_el = (size_t)n * (size_t)cap;
     if (need_el > L.nbr_elems) {
       if (L.nbr) cudaFree(L.nbr);
       L.nbr = nullptr;
@@ -482,7 +483,7 @@ int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
       cnt[s] = (int32_t)rows[s].size();
       sum += cnt[s];
       for (size_t k = 0; k < rows[s].size(); ++k)
-        ell[((size_t)(s >> 5) * cap + k) * 32 + (s & 31)] = rows[s][k];
+        ell[(size_t)s * cap + k] = rows[s][k];
     }
     MDG_CUDA_CHECK(cudaMemcpy(L.nbr, ell.data(), need_el * 4, cudaMemcpyHostToDevice));
     MDG_CUDA_CHECK(cudaMemcpy(L.cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice));
@@ -613,8 +614,7 @@ int mdg_polar_solve_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, do
     mdg::DevList& L = need_list(c, list_id);
     need_kernel_cutoff(L, cutoff);
     need(L.sites == MDG_SITES_ATOMIC, "pcg needs a list over atomic sites");
-    mdg::prune_list(c, list_id, cutoff);
-    mdg::run_field_tpre(c, alpha, thole_a, exclude_perm);
+    mdg::run_field_tpre(c, list_id, alpha, cutoff, thole_a, exclude_perm);
     double rms = 0;
     try {
       const int64_t it = mdg::run_pcg_pre(c, tol_debye, max_iter, &rms);
@@ -679,17 +679,20 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
     } else {
       mdg::zero_vec(c, c->force);
     }
-    // one pruned 7 A list per step feeds the multipole, field and T kernels
-    if (terms & (MDG_TERM_MPOLE | MDG_TERM_POLAR)) mdg::prune_list(c, elec_list, p->elec_cutoff);
+    // With polarization, one pass over the 9 A list prunes it to 7 A, stores
+    // the T tensors and computes the permanent field; the multipole kernel
+    // then runs on the pruned rows.
+    const bool polar = (terms & MDG_TERM_POLAR) != 0;
+    if (polar) mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
     if (terms & MDG_TERM_MPOLE) {
-      mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
+      if (polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
+      else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
     } else {
       mdg::zero_vec(c, c->torque);
     }
     c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
     c->pcg_rms = 0;
-    if (terms & MDG_TERM_POLAR) {
-      mdg::run_field_tpre(c, p->alpha, p->thole_a, p->exclude);
+    if (polar) {
       double rms = 0;
       c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
       c->pcg_rms = rms;

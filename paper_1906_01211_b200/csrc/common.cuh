@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "mdg_internal.h"
 
 namespace mdg {
@@ -101,14 +103,85 @@ __device__ __forceinline__ void ewald_bn(double r, double r2, double inv_r2, dou
   }
 }
 
+// Neighbour lists are row-major: site i's row starts at nbr + i * cap (cap a
+// multiple of 32, so every row is 128-B aligned) and holds cnt[i] entries.
 struct ListView {
   const int32_t* nbr;
   const int32_t* cnt;
   int32_t cap;
 };
 
-__device__ __forceinline__ const int32_t* list_row(const ListView& L, int i) {
-  return L.nbr + (size_t)(i >> 5) * (size_t)L.cap * 32 + (i & 31);
+__device__ __forceinline__ const int32_t* list_row(const ListView& L, int64_t i) {
+  return L.nbr + (size_t)i * (size_t)L.cap;
+}
+
+// ---- warp-per-site execution ------------------------------------------------
+// One warp walks one site's row 32 slots at a time (coalesced 128-B index
+// loads), evaluates the cheap prologue (minimum image, cutoff, exclusion) on
+// every slot, and compacts the in-range pairs with a ballot into a per-warp
+// shared-memory ring. The expensive pair body then always runs on 32 live
+// lanes; only the final drain of a row is partial. Each warp owns `ipw`
+// consecutive (spatially adjacent) sites, so a block's rows share cache lines.
+constexpr int kWarps = kBlock / 32;
+constexpr int kRing = 64;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_allsum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct Ring {
+  double4* q;  // kRing entries: (dx, dy, dz, j as bits)
+  int head;    // warp-uniform
+  int count;   // warp-uniform
+};
+
+__device__ __forceinline__ void ring_push(Ring& r, bool in, double dx, double dy, double dz,
+                                          int32_t j) {
+  const unsigned m = __ballot_sync(0xffffffffu, in);
+  if (in) {
+    const int pos = (r.head + r.count + __popc(m & lanemask_lt())) & (kRing - 1);
+    r.q[pos] = make_double4(dx, dy, dz, __longlong_as_double((long long)j));
+  }
+  r.count += __popc(m);
+  __syncwarp();
+}
+
+// Take `take` (<= 32) entries; lane l gets entry l when l < take.
+__device__ __forceinline__ double4 ring_take(Ring& r, int take, int lane) {
+  double4 e = make_double4(0, 0, 0, 0);
+  if (lane < take) e = r.q[(r.head + lane) & (kRing - 1)];
+  r.head = (r.head + take) & (kRing - 1);
+  r.count -= take;
+  __syncwarp();
+  return e;
+}
+
+__device__ __forceinline__ int32_t ring_j(const double4& e) {
+  return (int32_t)__double_as_longlong(e.w);
+}
+
+// sites per warp: enough blocks to fill 148 SMs several times over
+inline int sites_per_warp(int64_t n) {
+  const int64_t ipw = n / (148LL * kWarps * 16);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(8, ipw));
+}
+
+inline unsigned warp_grid(int64_t n, int ipw) {
+  return (unsigned)((n + (int64_t)kWarps * ipw - 1) / ((int64_t)kWarps * ipw));
 }
 
 }  // namespace mdg

@@ -220,11 +220,11 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
                int exclude, bool accumulate);
 // multipoles over the pruned list (c->plist)
 void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate);
-// Prune list_id to `cutoff` into c->plist (exclusion flags from c->mol).
-void prune_list(mdg_ctx* c, int list_id, double cutoff);
-// Permanent field over c->plist into c->eperm, storing T pair tensors in
-// c->plist.trr (one pass: shared bn/Thole terms).
-void run_field_tpre(mdg_ctx* c, double alpha, double thole_a, int exclude);
+// One pass over list_id: prune to `cutoff` into c->plist (exclusion flag in
+// bit 31), store the Ewald/Thole T pair tensors in c->plist.trr, and write
+// the permanent field into c->eperm.
+void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                    int exclude);
 // PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
 void run_reduce_sites(mdg_ctx* c);

@@ -19,6 +19,7 @@ namespace mdg {
 
 struct MKArgs {
   int64_t n_i;
+  int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ mp;
   const int32_t* __restrict__ mol;
@@ -45,9 +46,13 @@ __device__ __forceinline__ void qmul(const Quad& Q, double x, double y, double z
 // partial slots: 0 energy, 1..9 virial (row-major)
 template <bool EXCL, bool PRUNED>
 __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  __shared__ double4 ring_mem[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < a.n_i) {
+  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
     const double4 pi = a.pos[i];
     const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
     const double qi = pi.w;
@@ -55,17 +60,13 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
     const Quad Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
     const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
-    const int32_t* row = list_row(a.L, (int)i);
+    const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t raw = __ldg(row + (size_t)k * 32);
-      if (PRUNED && EXCL && raw < 0) continue;  // same molecule (flag bit)
-      const int32_t j = PRUNED ? (raw & 0x7fffffff) : raw;
+    auto body = [&](const double4& e) {
+      const int32_t j = ring_j(e);
+      const double x = e.x, y = e.y, z = e.z;
+      const double r2 = dist2(x, y, z);
       const double4 pj = ldg4(a.pos + j);
-      double x, y, z;
-      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
-      if (!PRUNED && !(r2 <= a.c2)) continue;
-      if (!PRUNED && EXCL && __ldg(a.mol + j) == mi) continue;
       const double4 m0j = ldg4(a.mp + 3 * (size_t)j), m1j = ldg4(a.mp + 3 * (size_t)j + 1);
       const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
       const double qj = pj.w, djx = m0j.x, djy = m0j.y, djz = m0j.z;
@@ -164,15 +165,47 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       tx += 2.0 * Mzy;
       ty += 2.0 * Mxz;
       tz += 2.0 * Myx;
+    };
+    for (int base = 0; base < cnt; base += 32) {
+      const int k = base + lane;
+      bool in = false;
+      double x = 0, y = 0, z = 0;
+      int32_t j = 0;
+      if (k < cnt) {
+        const int32_t raw = __ldg(row + k);
+        j = raw & 0x7fffffff;
+        const double4 pj = ldg4(a.pos + j);
+        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
+        if (PRUNED) {
+          in = !(EXCL && raw < 0);  // same molecule (flag bit)
+        } else {
+          in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+        }
+      }
+      ring_push(ring, in, x, y, z, j);
+      if (ring.count >= 32) body(ring_take(ring, 32, lane));
     }
-    if (a.accumulate) {
-      const double4 f0 = a.force[i];
-      fx += f0.x;
-      fy += f0.y;
-      fz += f0.z;
+    if (ring.count > 0) {
+      const int take = ring.count;
+      const double4 e = ring_take(ring, take, lane);
+      if (lane < take) body(e);
     }
-    a.force[i] = make_double4(fx, fy, fz, 0.0);
-    a.torque[i] = make_double4(tx, ty, tz, 0.0);
+    fx = warp_allsum(fx);
+    fy = warp_allsum(fy);
+    fz = warp_allsum(fz);
+    tx = warp_allsum(tx);
+    ty = warp_allsum(ty);
+    tz = warp_allsum(tz);
+    if (lane == 0) {
+      if (a.accumulate) {
+        const double4 f0 = a.force[i];
+        fx += f0.x;
+        fy += f0.y;
+        fz += f0.z;
+      }
+      a.force[i] = make_double4(fx, fy, fz, 0.0);
+      a.torque[i] = make_double4(tx, ty, tz, 0.0);
+    }
   }
   block_store_partials<10>(acc, a.partials);
 }
@@ -182,6 +215,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   const DevList& L = c->lists[list_id];
   MKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -192,7 +226,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = grid_for(c->n);
+  const int64_t blocks = warp_grid(c->n, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;
@@ -207,6 +241,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   const PrunedList& P = c->plist;
   MKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -217,7 +252,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = grid_for(c->n);
+  const int64_t blocks = warp_grid(c->n, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;

@@ -94,45 +94,63 @@ __device__ __forceinline__ int axis_cells(int c, int nc, int (&out)[3]) {
   return 3;
 }
 
+// Warp per site: lanes sweep a cell's sites 32 at a time (coalesced cell
+// reads), a ballot compacts the hits, and the row is written contiguously
+// (full 128-B lines), so the 2-4 GB list costs one pass of HBM writes.
 __global__ void __launch_bounds__(kBlock) k_nlist_build(
-    int64_t n_i, const double4* __restrict__ P, const int32_t* __restrict__ cell_of, Grid g,
-    const int32_t* __restrict__ start, const int32_t* __restrict__ atoms, Box b, double c2,
-    int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+    int64_t n_i, int ipw, const double4* __restrict__ P, const int32_t* __restrict__ cell_of,
+    Grid g, const int32_t* __restrict__ start, const int32_t* __restrict__ atoms, Box b,
+    double c2, int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
     const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_i) return;
-  const double4 pi = P[i];
-  const int c = cell_of[i];
-  const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
-  int xs[3], ys[3], zs[3];
-  const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
-            nz = axis_cells(cz, g.ncz, zs);
-  int32_t* out = nbr + (size_t)(i >> 5) * (size_t)cap * 32 + (i & 31);
-  int32_t k = 0;
-  // reference capacity rule: the half list stores a pair on the lower
-  // caller index and caps it at kMaxNeighbors (proj/src/neighbors_vec.cpp:80-83)
-  const int32_t oi = perm[i];
-  int32_t upper = 0;
-  for (int a = 0; a < nx; ++a)
-    for (int bb = 0; bb < ny; ++bb)
-      for (int q = 0; q < nz; ++q) {
-        const int cell = (xs[a] * g.ncy + ys[bb]) * g.ncz + zs[q];
-        const int32_t e = start[cell + 1];
-        for (int32_t s = start[cell]; s < e; ++s) {
-          const int32_t j = atoms[s];
-          if (j == (int32_t)i) continue;
-          const double4 pj = ldg4(P + j);
-          double dx, dy, dz;
-          const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          if (r2 <= c2) {
-            if (k < cap) out[(size_t)k * 32] = j;
-            ++k;
-            upper += (__ldg(perm + j) > oi) ? 1 : 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t i0 = w * ipw, i1 = min(n_i, i0 + ipw);
+  for (int64_t i = i0; i < i1; ++i) {
+    const double4 pi = P[i];
+    const int c = cell_of[i];
+    const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
+    int xs[3], ys[3], zs[3];
+    const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
+              nz = axis_cells(cz, g.ncz, zs);
+    int32_t* out = nbr + (size_t)i * (size_t)cap;
+    int32_t k = 0;  // warp-uniform row length
+    // reference capacity rule: the half list stores a pair on the lower
+    // caller index and caps it at kMaxNeighbors (proj/src/neighbors_vec.cpp:80-83)
+    const int32_t oi = perm[i];
+    int32_t upper = 0;
+    for (int a = 0; a < nx; ++a)
+      for (int bb = 0; bb < ny; ++bb)
+        for (int q = 0; q < nz; ++q) {
+          const int cell = (xs[a] * g.ncy + ys[bb]) * g.ncz + zs[q];
+          const int32_t e = start[cell + 1];
+          for (int32_t s0 = start[cell]; s0 < e; s0 += 32) {
+            const int32_t s = s0 + lane;
+            bool in = false;
+            int32_t j = 0;
+            if (s < e) {
+              j = __ldg(atoms + s);
+              if (j != (int32_t)i) {
+                const double4 pj = ldg4(P + j);
+                double dx, dy, dz;
+                const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+                in = (r2 <= c2);
+              }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            if (in) {
+              const int32_t pos = k + __popc(m & lanemask_lt());
+              if (pos < cap) out[pos] = j;
+              upper += (__ldg(perm + j) > oi) ? 1 : 0;
+            }
+            k += __popc(m);
           }
         }
-      }
-  cnt[i] = k;
-  if (upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+    upper = warp_allsum_i(upper);
+    if (lane == 0) {
+      cnt[i] = k;
+      if (upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+    }
+  }
 }
 
 // max and sum of counts -> results[slot], results[slot+1]
@@ -168,8 +186,7 @@ void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
 }
 
 static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
-  const int64_t groups = (c->n + 31) / 32;
-  const size_t need = (size_t)groups * (size_t)cap * 32;
+  const size_t need = (size_t)c->n * (size_t)cap;
   if (need > L.nbr_elems) {
     if (L.nbr) cudaFree(L.nbr);
     L.nbr = nullptr;
@@ -216,15 +233,17 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
   const double expect = (double)n / vol * 4.18879020478639 * list_cutoff * list_cutoff *
                         list_cutoff;
   int32_t cap = (int32_t)std::min<double>((double)c->max_pairs, 1.35 * expect + 48.0);
-  cap = std::max<int32_t>(32, (cap + 7) & ~7);
-  if (L.cap > cap && L.nbr) cap = std::min(L.cap, c->max_pairs);
+  cap = std::max<int32_t>(32, (cap + 31) & ~31);
+  if (L.cap > cap && L.nbr) cap = L.cap;
   const Box b = make_box(c->lx, c->ly, c->lz);
   const double c2 = list_cutoff * list_cutoff;
+  const int ipw = sites_per_warp(n);
   for (int attempt = 0; attempt < 2; ++attempt) {
     ensure_list_storage(c, L, cap);
     MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int32_t), c->stream));
-    MDG_LAUNCH(c, "nlist_build", grid_for(n), kBlock, 0, k_nlist_build, n, P, c->cell_of, g,
-               c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm, c->d_flag);
+    MDG_LAUNCH(c, "nlist_build", warp_grid(n, ipw), kBlock, 0, k_nlist_build, n, ipw, P,
+               c->cell_of, g, c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm,
+               c->d_flag);
     MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, n, L.cnt, c->results, 60);
     int32_t bad_site = 0;
     MDG_CUDA_CHECK(cudaMemcpyAsync(&bad_site, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
@@ -251,7 +270,7 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
       L.half_pairs = sum / 2;
       return;
     }
-    cap = std::min<int32_t>(c->max_pairs, (mx + 7) & ~7);
+    cap = (mx + 31) & ~31;
   }
   throw_error(MDG_CUDA, "nlist_build: capacity retry failed");
 }

@@ -1,9 +1,11 @@
 // nonpolar.cu -- Lennard-Jones, real-space Ewald charge and Halgren 14-7.
 //
-// One thread per i site over its full (both-direction) neighbour row: the
-// i-side force accumulates in registers and is written once, so there are
-// no j-side atomics and results are deterministic. Energies and virials are
-// counted twice over the full list and halved in the fixed-order finalize.
+// Warp per i site over its full (both-direction) row (common.cuh): the
+// prologue (minimum image, cutoff, exclusion) runs on every list slot, the
+// in-range pairs are ballot-compacted so the pair body runs on full warps,
+// the i-side force is a warp reduction written once -- no j-side scatter, no
+// atomics, deterministic sums. Energies and virials are counted twice over
+// the full list and halved in the fixed-order finalize.
 // Pair arithmetic follows the reference: proj/include/mdvec/kernels.hpp:42-64
 // (LJ, Ewald) and proj/src/polar_vec.cpp:74-116 (Halgren one-division form).
 #include "common.cuh"
@@ -12,6 +14,7 @@ namespace mdg {
 
 struct NonpolarKArgs {
   int64_t n_i;
+  int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ vdwp;
   const int32_t* __restrict__ mol;
@@ -25,24 +28,26 @@ struct NonpolarKArgs {
 // partial slots: 0 E_lj, 1 E_coul, 2..7 virial (xx xy xz yy yz zz)
 template <bool LJ, bool COUL, bool SHIFT, bool EXCL>
 __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  __shared__ double4 ring_mem[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < a.n_i) {
+  const double two_over_sqrt_pi = 1.1283791670955126;
+  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
     const double4 pi = a.pos[i];
     double4 vi = make_double4(0, 0, 0, 0);
     if (LJ) vi = a.vdwp[i];
     const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
-    const int32_t* row = list_row(a.L, (int)i);
+    const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0;
-    const double two_over_sqrt_pi = 1.1283791670955126;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(row + (size_t)k * 32);
+    auto body = [&](const double4& e) {
+      const int32_t j = ring_j(e);
+      const double dx = e.x, dy = e.y, dz = e.z;
+      const double r2 = dist2(dx, dy, dz);
       const double4 pj = ldg4(a.pos + j);
-      double dx, dy, dz;
-      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      if (!(r2 <= a.c2)) continue;
-      if (EXCL && __ldg(a.mol + j) == mi) continue;
       double fs = 0.0;
       if (LJ) {
         const double4 vj = ldg4(a.vdwp + j);
@@ -80,8 +85,30 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       acc[5] += dy * py;
       acc[6] += dy * pz;
       acc[7] += dz * pz;
+    };
+    for (int base = 0; base < cnt; base += 32) {
+      const int k = base + lane;
+      bool in = false;
+      double dx = 0, dy = 0, dz = 0;
+      int32_t j = 0;
+      if (k < cnt) {
+        j = __ldg(row + k);
+        const double4 pj = ldg4(a.pos + j);
+        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+        in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+      }
+      ring_push(ring, in, dx, dy, dz, j);
+      if (ring.count >= 32) body(ring_take(ring, 32, lane));
     }
-    a.force[i] = make_double4(fx, fy, fz, 0.0);
+    if (ring.count > 0) {
+      const int take = ring.count;
+      const double4 e = ring_take(ring, take, lane);
+      if (lane < take) body(e);
+    }
+    fx = warp_allsum(fx);
+    fy = warp_allsum(fy);
+    fz = warp_allsum(fz);
+    if (lane == 0) a.force[i] = make_double4(fx, fy, fz, 0.0);
   }
   block_store_partials<8>(acc, a.partials);
 }
@@ -89,7 +116,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
 template <bool LJ, bool COUL>
 static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
                       const char* name) {
-  const unsigned g = grid_for(k.n_i);
+  const unsigned g = warp_grid(k.n_i, k.ipw);
 #define NP_CASE(S, E)                                                            \
   if (shift == S && excl == E) {                                               \
     MDG_LAUNCH(c, name, g, kBlock, 0, (k_nonpolar<LJ, COUL, S, E>), k);         \
@@ -106,6 +133,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   const DevList& L = c->lists[list_id];
   NonpolarKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
   k.mol = c->mol;
@@ -115,7 +143,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.alpha = a.alpha;
   k.electric = a.electric;
   k.force = (L.sites == MDG_SITES_VDW) ? c->force2 : c->force;
-  const int64_t blocks = grid_for(c->n);
+  const int64_t blocks = warp_grid(c->n, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   if (L.sites == MDG_SITES_VDW && a.do_coul)
@@ -130,6 +158,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
 // ---- Halgren buffered 14-7 -------------------------------------------------
 struct HalgrenKArgs {
   int64_t n_i;
+  int ipw;
   const double4* __restrict__ site;
   const double4* __restrict__ vdwp;
   const int32_t* __restrict__ mol;
@@ -142,23 +171,24 @@ struct HalgrenKArgs {
 
 template <bool EXCL>
 __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  __shared__ double4 ring_mem[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < a.n_i) {
+  const double delta = a.delta, gamma = a.gamma;
+  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
     const double4 pi = a.site[i];
     const double4 vi = a.vdwp[i];
     const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
-    const int32_t* row = list_row(a.L, (int)i);
-    const double delta = a.delta, gamma = a.gamma;
+    const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(row + (size_t)k * 32);
-      const double4 pj = ldg4(a.site + j);
-      double dx, dy, dz;
-      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      if (!(r2 <= a.c2)) continue;
-      if (EXCL && __ldg(a.mol + j) == mi) continue;
+    auto body = [&](const double4& e) {
+      const int32_t j = ring_j(e);
+      const double dx = e.x, dy = e.y, dz = e.z;
+      const double r2 = dist2(dx, dy, dz);
       const double4 vj = ldg4(a.vdwp + j);
       // proj/src/polar_vec.cpp:78-107: all reciprocals from one division
       const double r = sqrt(r2);
@@ -198,8 +228,30 @@ __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
       acc[5] += dy * py;
       acc[6] += dy * pz;
       acc[7] += dz * pz;
+    };
+    for (int base = 0; base < cnt; base += 32) {
+      const int k = base + lane;
+      bool in = false;
+      double dx = 0, dy = 0, dz = 0;
+      int32_t j = 0;
+      if (k < cnt) {
+        j = __ldg(row + k);
+        const double4 pj = ldg4(a.site + j);
+        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+        in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+      }
+      ring_push(ring, in, dx, dy, dz, j);
+      if (ring.count >= 32) body(ring_take(ring, 32, lane));
     }
-    a.force[i] = make_double4(fx, fy, fz, 0.0);
+    if (ring.count > 0) {
+      const int take = ring.count;
+      const double4 e = ring_take(ring, take, lane);
+      if (lane < take) body(e);
+    }
+    fx = warp_allsum(fx);
+    fy = warp_allsum(fy);
+    fz = warp_allsum(fz);
+    if (lane == 0) a.force[i] = make_double4(fx, fy, fz, 0.0);
   }
   block_store_partials<8>(acc, a.partials);
 }
@@ -236,6 +288,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   const DevList& L = c->lists[list_id];
   HalgrenKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   const bool reduced = (L.sites == MDG_SITES_VDW);
   k.site = reduced ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
@@ -246,7 +299,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.delta = delta;
   k.gamma = gamma;
   k.force = reduced ? c->force2 : c->force;
-  const int64_t blocks = grid_for(c->n);
+  const int64_t blocks = warp_grid(c->n, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   if (exclude && c->has_mol)

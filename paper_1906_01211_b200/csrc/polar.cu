@@ -5,6 +5,13 @@
 // field, Jacobi). With alpha > 0 the pair tensors are the real-space Ewald
 // ones, rr3 = B1 - (1-l3)/r^3, rr5 = B2 - 3(1-l5)/r^5, rr7 = B3 - 15(1-l7)/r^7;
 // at alpha == 0 the kernels use the reference's l3/r^3, 3 l5/r^5 forms.
+//
+// In the AMOEBA step the 7 A kernels share one pass over the 9 A list
+// (k_field_tpre): it compacts the in-range pairs into a pruned row (exclusion
+// flag in the index sign bit), stores the T pair tensors (rr3, rr5) beside
+// them and accumulates the permanent field. The tensors do not change during
+// the solve, so every PCG mat-vec streams 20 B per pair instead of
+// recomputing erfc/exp/sqrt/div: the solve is HBM-bound.
 #include <algorithm>
 #include <cmath>
 
@@ -12,8 +19,10 @@
 
 namespace mdg {
 
+// ---- on-the-fly T mat-vec (reference dipole_field_matvec, Ewald generalised)
 struct TKArgs {
   int64_t n_i;
+  int ipw;
   const double4* __restrict__ pos;
   const double2* __restrict__ polp;
   ListView L;
@@ -21,26 +30,25 @@ struct TKArgs {
   double c2, alpha, thole_a;
   const double4* __restrict__ in;
   double4* __restrict__ out;
-  // PCG fusion: q = p/alpha_i - T p, partial p.q
-  double* __restrict__ partials;
 };
 
-template <bool EWALD, bool PCG>
+template <bool EWALD>
 __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  double acc[1] = {0.0};
-  if (i < a.n_i) {
+  __shared__ double4 ring_mem[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
+  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
     const double4 pi = a.pos[i];
     const double2 ai = a.polp[i];
     const int cnt = a.L.cnt[i];
-    const int32_t* row = list_row(a.L, (int)i);
+    const int32_t* row = list_row(a.L, i);
     double ex = 0, ey = 0, ez = 0;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(row + (size_t)k * 32);
-      const double4 pj = ldg4(a.pos + j);
-      double dx, dy, dz;
-      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      if (!(r2 <= a.c2)) continue;
+    auto body = [&](const double4& e) {
+      const int32_t j = ring_j(e);
+      const double dx = e.x, dy = e.y, dz = e.z;
+      const double r2 = dist2(dx, dy, dz);
       const double2 aj = __ldg(a.polp + j);
       const double4 mj = ldg4(a.in + j);
       const double r = sqrt(r2);
@@ -63,25 +71,38 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
       ex += rr5 * dot * dx - rr3 * mj.x;
       ey += rr5 * dot * dy - rr3 * mj.y;
       ez += rr5 * dot * dz - rr3 * mj.z;
+    };
+    for (int base = 0; base < cnt; base += 32) {
+      const int k = base + lane;
+      bool in = false;
+      double dx = 0, dy = 0, dz = 0;
+      int32_t j = 0;
+      if (k < cnt) {
+        j = __ldg(row + k) & 0x7fffffff;
+        const double4 pj = ldg4(a.pos + j);
+        in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
+      }
+      ring_push(ring, in, dx, dy, dz, j);
+      if (ring.count >= 32) body(ring_take(ring, 32, lane));
     }
-    if (PCG) {
-      const double4 p = a.in[i];
-      const double inva = 1.0 / ai.x;
-      const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
-      a.out[i] = make_double4(qx, qy, qz, 0.0);
-      acc[0] = p.x * qx + p.y * qy + p.z * qz;
-    } else {
-      a.out[i] = make_double4(ex, ey, ez, 0.0);
+    if (ring.count > 0) {
+      const int take = ring.count;
+      const double4 e = ring_take(ring, take, lane);
+      if (lane < take) body(e);
     }
+    ex = warp_allsum(ex);
+    ey = warp_allsum(ey);
+    ez = warp_allsum(ez);
+    if (lane == 0) a.out[i] = make_double4(ex, ey, ez, 0.0);
   }
-  if (PCG) block_store_partials<1>(acc, a.partials);
 }
 
-static TKArgs t_args(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
-                     const double4* in, double4* out) {
+void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                 const double4* in, double4* out) {
   const DevList& L = c->lists[list_id];
   TKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   k.pos = c->pos;
   k.polp = c->polp;
   k.L = ListView{L.nbr, L.cnt, L.cap};
@@ -91,22 +112,15 @@ static TKArgs t_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   k.thole_a = thole_a;
   k.in = in;
   k.out = out;
-  k.partials = c->partials;
-  return k;
-}
-
-void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
-                 const double4* in, double4* out) {
-  TKArgs k = t_args(c, list_id, alpha, cutoff, thole_a, in, out);
-  if (alpha > 0)
-    MDG_LAUNCH(c, "tmatvec", grid_for(c->n), kBlock, 0, (k_tmatvec<true, false>), k);
-  else
-    MDG_LAUNCH(c, "tmatvec", grid_for(c->n), kBlock, 0, (k_tmatvec<false, false>), k);
+  const unsigned g = warp_grid(c->n, k.ipw);
+  if (alpha > 0) MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<true>, k);
+  else MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<false>, k);
 }
 
 // ---- permanent field ----------------------------------------------------------
 struct FKArgs {
   int64_t n_i;
+  int ipw;
   const double4* __restrict__ pos;
   const double2* __restrict__ polp;
   const double4* __restrict__ mp;
@@ -115,50 +129,83 @@ struct FKArgs {
   Box b;
   double c2, alpha, thole_a;
   double4* __restrict__ out;
+  // field_tpre outputs: pruned rows, T tensors, counts
+  int32_t* __restrict__ pnbr;
+  double2* __restrict__ trr;
+  int32_t* __restrict__ pcnt;
+  int32_t pcap;
 };
 
-// E_i = sum_j R (rr3 q_j + rr5 mu_j.R + rr7 R.Q_j.R) - rr3 mu_j - 2 rr5 Q_j R,
-// R = r_i - r_j (field of a point multipole; Tinker's stored Q = Theta/3).
-template <bool EWALD, bool MPOLE, bool EXCL>
+// Field at i of the multipole of j, R = r_i - r_j (Tinker's stored Q = Theta/3):
+// E = R (rr3 q + rr5 mu.R + rr7 R.Q.R) - rr3 mu - 2 rr5 Q R
+__device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int32_t j, double qj,
+                                            double dx, double dy, double dz, double rr3,
+                                            double rr5, double rr7, double& ex, double& ey,
+                                            double& ez) {
+  const double4 m0 = ldg4(mp + 3 * (size_t)j);
+  const double4 m1 = ldg4(mp + 3 * (size_t)j + 1);
+  const double qzz = __ldg(&mp[3 * (size_t)j + 2].x);
+  const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
+  const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
+  const double qz = m1.y * dx + m1.w * dy + qzz * dz;
+  const double dr = m0.x * dx + m0.y * dy + m0.z * dz;
+  const double qr = dx * qx + dy * qy + dz * qz;
+  const double cc = rr3 * qj + rr5 * dr + rr7 * qr;
+  const double t5 = 2.0 * rr5;
+  ex += cc * dx - rr3 * m0.x - t5 * qx;
+  ey += cc * dy - rr3 * m0.y - t5 * qy;
+  ez += cc * dz - rr3 * m0.z - t5 * qz;
+}
+
+// TPRE: also write the pruned row (all pairs within the cutoff, exclusion
+// flag in bit 31) and its T tensors; the field skips excluded pairs.
+template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE>
 __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  if (i >= a.n_i) return;
-  const double4 pi = a.pos[i];
-  const double2 ai = a.polp[i];
-  const int32_t mi = EXCL ? a.mol[i] : 0;
-  const int cnt = a.L.cnt[i];
-  const int32_t* row = list_row(a.L, (int)i);
-  double ex = 0, ey = 0, ez = 0;
-  for (int k = 0; k < cnt; ++k) {
-    const int32_t j = __ldg(row + (size_t)k * 32);
-    const double4 pj = ldg4(a.pos + j);
-    double dx, dy, dz;
-    const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-    if (!(r2 <= a.c2)) continue;
-    if (EXCL && __ldg(a.mol + j) == mi) continue;
-    const double2 aj = __ldg(a.polp + j);
-    const double r = sqrt(r2);
-    if (!MPOLE) {
-      double l3, l5;
-      thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
-      double rr3;
-      if (EWALD) {
-        const double inv_r2 = 1.0 / r2;
-        double bn[2];
-        ewald_bn<1>(r, r2, inv_r2, a.alpha, bn);
-        rr3 = bn[1] - (1.0 - l3) * inv_r2 / r;
-      } else {
-        rr3 = l3 / (r2 * r);  // proj/src/polar_scalar.cpp:143
+  __shared__ double4 ring_mem[kWarps][kRing];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
+  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
+    const double4 pi = a.pos[i];
+    const double2 ai = a.polp[i];
+    const int32_t mi = a.mol[i];
+    const int cnt = a.L.cnt[i];
+    const int32_t* row = list_row(a.L, i);
+    int32_t* prow = TPRE ? a.pnbr + (size_t)i * a.pcap : nullptr;
+    double2* trow = TPRE ? a.trr + (size_t)i * a.pcap : nullptr;
+    int32_t pn = 0;  // warp-uniform pruned length
+    double ex = 0, ey = 0, ez = 0;
+    auto body = [&](const double4& e, bool live) {
+      const int32_t raw = ring_j(e);
+      const int32_t j = raw & 0x7fffffff;
+      const double dx = e.x, dy = e.y, dz = e.z;
+      const double r2 = dist2(dx, dy, dz);
+      const double2 aj = __ldg(a.polp + j);
+      const double4 pj = ldg4(a.pos + j);
+      const double r = sqrt(r2);
+      const double inv_r2 = 1.0 / r2;
+      const double b1 = inv_r2 / r;
+      if (!MPOLE && !TPRE) {
+        double l3, l5;
+        thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
+        double rr3;
+        if (EWALD) {
+          double bn[2];
+          ewald_bn<1>(r, r2, inv_r2, a.alpha, bn);
+          rr3 = bn[1] - (1.0 - l3) * b1;
+        } else {
+          rr3 = l3 / (r2 * r);  // proj/src/polar_scalar.cpp:143
+        }
+        const double cq = rr3 * pj.w;
+        ex += cq * dx;
+        ey += cq * dy;
+        ez += cq * dz;
+        return;
       }
-      const double c = rr3 * pj.w;
-      ex += c * dx;
-      ey += c * dy;
-      ez += c * dz;
-    } else {
       double l3, l5, l7;
       thole7(r, ai.y * aj.y, a.thole_a, l3, l5, l7);
-      const double inv_r2 = 1.0 / r2;
-      const double b1 = inv_r2 / r, b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
+      const double b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
       double rr3, rr5, rr7;
       if (EWALD) {
         double bn[4];
@@ -171,30 +218,61 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
         rr5 = l5 * b2;
         rr7 = l7 * b3;
       }
-      const double4 m0 = ldg4(a.mp + 3 * (size_t)j);
-      const double4 m1 = ldg4(a.mp + 3 * (size_t)j + 1);
-      const double qzz = __ldg(&a.mp[3 * (size_t)j + 2].x);
-      // Q R with Q = [[m0.w, m1.x, m1.y], [m1.x, m1.z, m1.w], [m1.y, m1.w, qzz]]
-      const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
-      const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
-      const double qz = m1.y * dx + m1.w * dy + qzz * dz;
-      const double dr = m0.x * dx + m0.y * dy + m0.z * dz;
-      const double qr = dx * qx + dy * qy + dz * qz;
-      const double cc = rr3 * pj.w + rr5 * dr + rr7 * qr;
-      const double t5 = 2.0 * rr5;
-      ex += cc * dx - rr3 * m0.x - t5 * qx;
-      ey += cc * dy - rr3 * m0.y - t5 * qy;
-      ez += cc * dz - rr3 * m0.z - t5 * qz;
+      if (TPRE && live && pn + lane < a.pcap) {  // overflow -> host retries larger
+        prow[pn + lane] = raw;
+        trow[pn + lane] = make_double2(rr3, rr5);
+      }
+      if (!live || (EXCL && raw < 0)) return;
+      if (MPOLE) {
+        mpole_field(a.mp, j, pj.w, dx, dy, dz, rr3, rr5, rr7, ex, ey, ez);
+      } else {
+        const double cq = rr3 * pj.w;
+        ex += cq * dx;
+        ey += cq * dy;
+        ez += cq * dz;
+      }
+    };
+    for (int base = 0; base < cnt; base += 32) {
+      const int k = base + lane;
+      bool in = false;
+      double dx = 0, dy = 0, dz = 0;
+      int32_t raw = 0;
+      if (k < cnt) {
+        const int32_t j = __ldg(row + k) & 0x7fffffff;
+        const double4 pj = ldg4(a.pos + j);
+        in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
+        const bool same = __ldg(a.mol + j) == mi;
+        if (!TPRE && EXCL && same) in = false;
+        raw = (TPRE && same) ? (j | (int32_t)0x80000000) : j;
+      }
+      ring_push(ring, in, dx, dy, dz, raw);
+      if (ring.count >= 32) {
+        body(ring_take(ring, 32, lane), true);
+        pn += 32;
+      }
+    }
+    if (ring.count > 0) {
+      const int take = ring.count;
+      const double4 e = ring_take(ring, take, lane);
+      if (lane < take) body(e, true);
+      pn += take;
+    }
+    ex = warp_allsum(ex);
+    ey = warp_allsum(ey);
+    ez = warp_allsum(ez);
+    if (lane == 0) {
+      a.out[i] = make_double4(ex, ey, ez, 0.0);
+      if (TPRE) a.pcnt[i] = pn;
     }
   }
-  a.out[i] = make_double4(ex, ey, ez, 0.0);
 }
 
-void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
-                    int exclude, double4* out) {
+static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                     double4* out) {
   const DevList& L = c->lists[list_id];
   FKArgs k;
   k.n_i = c->n;
+  k.ipw = sites_per_warp(c->n);
   k.pos = c->pos;
   k.polp = c->polp;
   k.mp = c->mp;
@@ -205,11 +283,21 @@ void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double
   k.alpha = alpha;
   k.thole_a = thole_a;
   k.out = out;
+  k.pnbr = nullptr;
+  k.trr = nullptr;
+  k.pcnt = nullptr;
+  k.pcap = 0;
+  return k;
+}
+
+void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                    int exclude, double4* out) {
+  FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, out);
   const bool ew = alpha > 0, mp = c->has_mpoles, ex = exclude && c->has_mol;
-  const unsigned g = grid_for(c->n);
+  const unsigned g = warp_grid(c->n, k.ipw);
 #define PF_CASE(E, M, X)                                                         \
   if (ew == E && mp == M && ex == X) {                                         \
-    MDG_LAUNCH(c, "perm_field", g, kBlock, 0, (k_perm_field<E, M, X>), k);      \
+    MDG_LAUNCH(c, "perm_field", g, kBlock, 0, (k_perm_field<E, M, X, false>), k); \
     return;                                                                    \
   }
   PF_CASE(false, false, false)
@@ -223,7 +311,117 @@ void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double
 #undef PF_CASE
 }
 
-// ---- PCG ----------------------------------------------------------------------
+void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                    int exclude) {
+  const DevList& L = c->lists[list_id];
+  PrunedList& P = c->plist;
+  const int64_t n = c->n;
+  const double vol = c->lx * c->ly * c->lz;
+  const double expect = (double)n / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
+  int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
+  cap = std::max<int32_t>(32, (cap + 31) & ~31);
+  if (P.cap > cap) cap = std::min(P.cap, L.cap);
+  const bool mp = c->has_mpoles, ex = exclude && c->has_mol;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const size_t need = (size_t)n * (size_t)cap;
+    if (need > P.elems) {
+      if (P.nbr) cudaFree(P.nbr);
+      if (P.trr) cudaFree(P.trr);
+      P.nbr = nullptr;
+      P.trr = nullptr;
+      MDG_CUDA_CHECK(cudaMalloc(&P.nbr, need * sizeof(int32_t)));
+      MDG_CUDA_CHECK(cudaMalloc(&P.trr, need * sizeof(double2)));
+      P.elems = need;
+    }
+    if (!P.cnt) MDG_CUDA_CHECK(cudaMalloc(&P.cnt, (size_t)c->n_cap * sizeof(int32_t)));
+    P.cap = cap;
+    FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, c->eperm);
+    k.pnbr = P.nbr;
+    k.trr = P.trr;
+    k.pcnt = P.cnt;
+    k.pcap = cap;
+    const unsigned g = warp_grid(n, k.ipw);
+    // rows longer than cap are counted, not written; the retry below grows cap
+    if (mp && ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, true, true, true>), k);
+    else if (mp) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, true, false, true>), k);
+    else if (ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, false, true, true>), k);
+    else MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, false, false, true>), k);
+    count_stats(c, P.cnt, 62);
+    fetch_results(c);
+    const int32_t mx = (int32_t)c->h_results[62];
+    if (mx <= cap) {
+      P.valid = true;
+      P.src = list_id;
+      P.cutoff = cutoff;
+      P.directed = (int64_t)c->h_results[63];
+      return;
+    }
+    cap = (mx + 31) & ~31;
+  }
+  throw_error(MDG_CUDA, "field_tpre: capacity retry failed");
+}
+
+// ---- streaming T mat-vec over the pruned rows --------------------------------
+struct TPArgs {
+  int64_t n;
+  int ipw;
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  const int32_t* __restrict__ pnbr;
+  const int32_t* __restrict__ pcnt;
+  const double2* __restrict__ trr;
+  int32_t pcap;
+  Box b;
+  const double4* __restrict__ in;
+  double4* __restrict__ out;
+  double* __restrict__ partials;
+};
+
+// E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; the PCG form
+// writes q = p/alpha - T p and the block partial of p.q.
+template <bool PCG>
+__global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
+  double acc[1] = {0.0};
+  const int64_t i0 = w * a.ipw, i1 = min(a.n, i0 + a.ipw);
+  for (int64_t i = i0; i < i1; ++i) {
+    const double4 pi = a.pos[i];
+    const int cnt = a.pcnt[i];
+    const int32_t* row = a.pnbr + (size_t)i * a.pcap;
+    const double2* trow = a.trr + (size_t)i * a.pcap;
+    double ex = 0, ey = 0, ez = 0;
+    for (int k = lane; k < cnt; k += 32) {
+      const int32_t j = __ldg(row + k) & 0x7fffffff;
+      const double2 rr = __ldg(trow + k);
+      const double4 pj = ldg4(a.pos + j);
+      const double4 mj = ldg4(a.in + j);
+      double dx, dy, dz;
+      min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
+      ex += rr.y * dot * dx - rr.x * mj.x;
+      ey += rr.y * dot * dy - rr.x * mj.y;
+      ez += rr.y * dot * dz - rr.x * mj.z;
+    }
+    ex = warp_allsum(ex);
+    ey = warp_allsum(ey);
+    ez = warp_allsum(ez);
+    if (lane == 0) {
+      if (PCG) {
+        const double4 p = a.in[i];
+        const double inva = 1.0 / a.polp[i].x;
+        const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
+        a.out[i] = make_double4(qx, qy, qz, 0.0);
+        acc[0] += p.x * qx + p.y * qy + p.z * qz;
+      } else {
+        a.out[i] = make_double4(ex, ey, ez, 0.0);
+      }
+    }
+  }
+  if (PCG) block_store_partials<1>(acc, a.partials);
+}
+
+// ---- PCG vector kernels ------------------------------------------------------
 // result slots: 20 p.q, 21 rz_old, 22 rz_new, 23 sum|dmu|^2, 24 beta, 25 rms (D),
 // 26 a_k, 27 converged flag
 constexpr double kDebye = 4.80321;
@@ -340,25 +538,36 @@ __global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks
   }
 }
 
-int64_t run_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
-                double tol_debye, int64_t max_iter, double* last_rms) {
+int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
   const int64_t n = c->n;
   const int64_t blocks = grid_for(n);
-  ensure_partials(c, blocks);
-  // c->eperm holds the permanent field
+  PrunedList& P = c->plist;
+  TPArgs k;
+  k.n = n;
+  k.ipw = sites_per_warp(n);
+  const int64_t tblocks = warp_grid(n, k.ipw);
+  ensure_partials(c, std::max(blocks, tblocks));
+  k.pos = c->pos;
+  k.polp = c->polp;
+  k.pnbr = P.nbr;
+  k.pcnt = P.cnt;
+  k.trr = P.trr;
+  k.pcap = P.cap;
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.partials = c->partials;
   MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
-  run_tmatvec(c, list_id, alpha, cutoff, thole_a, c->mu, c->cg_q);
+  k.in = c->mu;
+  k.out = c->cg_q;
+  MDG_LAUNCH(c, "tmatvec_pre", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<false>, k);
   MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
              c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
   MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
              c->results);
-  TKArgs k = t_args(c, list_id, alpha, cutoff, thole_a, c->cg_p, c->cg_q);
+  k.in = c->cg_p;
+  k.out = c->cg_q;
   for (int64_t it = 1; it <= max_iter; ++it) {
-    if (alpha > 0)
-      MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, (k_tmatvec<true, true>), k);
-    else
-      MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, (k_tmatvec<false, true>), k);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 1, n, tol_debye,
+    MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<true>, k);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, tblocks, 1, n, tol_debye,
                c->results);
     MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
                c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
@@ -430,254 +639,6 @@ int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, doubl
     if (*last_resid <= tol) return it;
   }
   throw_error(MDG_CONVERGENCE, "jacobi_polarization_solve: no convergence after max_iter");
-}
-
-// =============================================================================
-// Pruned list + precomputed T: the 7 A kernels of one step share one pass
-// over the 9 A list. The pair tensors (rr3, rr5) do not change during the
-// solve, so the PCG mat-vec streams them (16 B/slot) instead of recomputing
-// erfc/exp/sqrt/div every iteration: the solve becomes HBM-bound.
-// =============================================================================
-
-__global__ void __launch_bounds__(kBlock) k_prune(int64_t n, const double4* __restrict__ P,
-                                                  const int32_t* __restrict__ mol, ListView src,
-                                                  Box b, double c2, int32_t cap,
-                                                  int32_t* __restrict__ out,
-                                                  int32_t* __restrict__ ocnt) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  if (i >= n) return;
-  const double4 pi = P[i];
-  const int32_t mi = mol[i];
-  const int cnt = src.cnt[i];
-  const int32_t* row = list_row(src, (int)i);
-  int32_t* orow = out + (size_t)(i >> 5) * (size_t)cap * 32 + (i & 31);
-  int32_t k2 = 0;
-  for (int k = 0; k < cnt; ++k) {
-    const int32_t j = __ldg(row + (size_t)k * 32);
-    const double4 pj = ldg4(P + j);
-    double dx, dy, dz;
-    const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-    if (r2 <= c2) {
-      if (k2 < cap) orow[(size_t)k2 * 32] = (__ldg(mol + j) == mi) ? (j | (int32_t)0x80000000) : j;
-      ++k2;
-    }
-  }
-  ocnt[i] = k2;
-}
-
-void prune_list(mdg_ctx* c, int list_id, double cutoff) {
-  const DevList& L = c->lists[list_id];
-  PrunedList& P = c->plist;
-  const int64_t n = c->n;
-  const double vol = c->lx * c->ly * c->lz;
-  const double expect = (double)n / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
-  int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
-  cap = std::max<int32_t>(32, (cap + 7) & ~7);
-  if (P.cap > cap) cap = std::min(P.cap, L.cap);
-  const Box b = make_box(c->lx, c->ly, c->lz);
-  const double4* X = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const size_t need = (size_t)((n + 31) / 32) * (size_t)cap * 32;
-    if (need > P.elems) {
-      if (P.nbr) cudaFree(P.nbr);
-      if (P.trr) cudaFree(P.trr);
-      P.nbr = nullptr;
-      P.trr = nullptr;
-      MDG_CUDA_CHECK(cudaMalloc(&P.nbr, need * sizeof(int32_t)));
-      MDG_CUDA_CHECK(cudaMalloc(&P.trr, need * sizeof(double2)));
-      P.elems = need;
-    }
-    if (!P.cnt) MDG_CUDA_CHECK(cudaMalloc(&P.cnt, (size_t)c->n_cap * sizeof(int32_t)));
-    P.cap = cap;
-    MDG_LAUNCH(c, "prune", grid_for(n), kBlock, 0, k_prune, n, X, c->mol,
-               ListView{L.nbr, L.cnt, L.cap}, b, cutoff * cutoff, cap, P.nbr, P.cnt);
-    count_stats(c, P.cnt, 62);
-    fetch_results(c);
-    const int32_t mx = (int32_t)c->h_results[62];
-    if (mx <= cap) {
-      P.valid = true;
-      P.src = list_id;
-      P.cutoff = cutoff;
-      P.directed = (int64_t)c->h_results[63];
-      return;
-    }
-    cap = (mx + 7) & ~7;
-  }
-  throw_error(MDG_CUDA, "prune_list: capacity retry failed");
-}
-
-struct FTArgs {
-  int64_t n;
-  const double4* __restrict__ pos;
-  const double2* __restrict__ polp;
-  const double4* __restrict__ mp;
-  ListView L;  // pruned
-  double2* __restrict__ trr;
-  Box b;
-  double alpha, thole_a;
-  double4* __restrict__ out;
-};
-
-// One pass over the pruned list: T tensors for every pair (u-scale 1) and the
-// permanent field of q + mu + Theta from non-excluded pairs (d-scale 0).
-template <bool MPOLE, bool EXCL>
-__global__ void __launch_bounds__(kBlock) k_field_tpre(FTArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  if (i >= a.n) return;
-  const double4 pi = a.pos[i];
-  const double2 ai = a.polp[i];
-  const int cnt = a.L.cnt[i];
-  const size_t base = (size_t)(i >> 5) * (size_t)a.L.cap * 32 + (i & 31);
-  double ex = 0, ey = 0, ez = 0;
-  for (int k = 0; k < cnt; ++k) {
-    const int32_t raw = __ldg(a.L.nbr + base + (size_t)k * 32);
-    const int32_t j = raw & 0x7fffffff;
-    const double4 pj = ldg4(a.pos + j);
-    double dx, dy, dz;
-    const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-    const double2 aj = __ldg(a.polp + j);
-    const double r = sqrt(r2);
-    const double inv_r2 = 1.0 / r2;
-    double l3, l5, l7;
-    thole7(r, ai.y * aj.y, a.thole_a, l3, l5, l7);
-    double bn[4];
-    ewald_bn<3>(r, r2, inv_r2, a.alpha, bn);
-    const double b1 = inv_r2 / r, b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
-    const double rr3 = bn[1] - (1.0 - l3) * b1;
-    const double rr5 = bn[2] - (1.0 - l5) * b2;
-    a.trr[base + (size_t)k * 32] = make_double2(rr3, rr5);
-    if (EXCL && raw < 0) continue;
-    if (!MPOLE) {
-      const double cq = rr3 * pj.w;
-      ex += cq * dx;
-      ey += cq * dy;
-      ez += cq * dz;
-    } else {
-      const double rr7 = bn[3] - (1.0 - l7) * b3;
-      const double4 m0 = ldg4(a.mp + 3 * (size_t)j);
-      const double4 m1 = ldg4(a.mp + 3 * (size_t)j + 1);
-      const double qzz = __ldg(&a.mp[3 * (size_t)j + 2].x);
-      const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
-      const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
-      const double qz = m1.y * dx + m1.w * dy + qzz * dz;
-      const double dr = m0.x * dx + m0.y * dy + m0.z * dz;
-      const double qr = dx * qx + dy * qy + dz * qz;
-      const double cc = rr3 * pj.w + rr5 * dr + rr7 * qr;
-      const double t5 = 2.0 * rr5;
-      ex += cc * dx - rr3 * m0.x - t5 * qx;
-      ey += cc * dy - rr3 * m0.y - t5 * qy;
-      ez += cc * dz - rr3 * m0.z - t5 * qz;
-    }
-  }
-  a.out[i] = make_double4(ex, ey, ez, 0.0);
-}
-
-void run_field_tpre(mdg_ctx* c, double alpha, double thole_a, int exclude) {
-  PrunedList& P = c->plist;
-  FTArgs k;
-  k.n = c->n;
-  k.pos = c->pos;
-  k.polp = c->polp;
-  k.mp = c->mp;
-  k.L = ListView{P.nbr, P.cnt, P.cap};
-  k.trr = P.trr;
-  k.b = make_box(c->lx, c->ly, c->lz);
-  k.alpha = alpha;
-  k.thole_a = thole_a;
-  k.out = c->eperm;
-  const bool mp = c->has_mpoles, ex = exclude && c->has_mol;
-  const unsigned g = grid_for(c->n);
-  if (mp && ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<true, true>), k);
-  else if (mp) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<true, false>), k);
-  else if (ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<false, true>), k);
-  else MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_field_tpre<false, false>), k);
-}
-
-struct TPArgs {
-  int64_t n;
-  const double4* __restrict__ pos;
-  const double2* __restrict__ polp;
-  ListView L;
-  const double2* __restrict__ trr;
-  Box b;
-  const double4* __restrict__ in;
-  double4* __restrict__ out;
-  double* __restrict__ partials;
-};
-
-// E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; PCG form
-// writes q = p/alpha - T p and the block partial of p.q.
-template <bool PCG>
-__global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  double acc[1] = {0.0};
-  if (i < a.n) {
-    const double4 pi = a.pos[i];
-    const int cnt = a.L.cnt[i];
-    const size_t base = (size_t)(i >> 5) * (size_t)a.L.cap * 32 + (i & 31);
-    double ex = 0, ey = 0, ez = 0;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(a.L.nbr + base + (size_t)k * 32) & 0x7fffffff;
-      const double2 rr = __ldg(a.trr + base + (size_t)k * 32);
-      const double4 pj = ldg4(a.pos + j);
-      const double4 mj = ldg4(a.in + j);
-      double dx, dy, dz;
-      min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
-      ex += rr.y * dot * dx - rr.x * mj.x;
-      ey += rr.y * dot * dy - rr.x * mj.y;
-      ez += rr.y * dot * dz - rr.x * mj.z;
-    }
-    if (PCG) {
-      const double4 p = a.in[i];
-      const double inva = 1.0 / a.polp[i].x;
-      const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
-      a.out[i] = make_double4(qx, qy, qz, 0.0);
-      acc[0] = p.x * qx + p.y * qy + p.z * qz;
-    } else {
-      a.out[i] = make_double4(ex, ey, ez, 0.0);
-    }
-  }
-  if (PCG) block_store_partials<1>(acc, a.partials);
-}
-
-int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
-  const int64_t n = c->n;
-  const int64_t blocks = grid_for(n);
-  ensure_partials(c, blocks);
-  PrunedList& P = c->plist;
-  TPArgs k;
-  k.n = n;
-  k.pos = c->pos;
-  k.polp = c->polp;
-  k.L = ListView{P.nbr, P.cnt, P.cap};
-  k.trr = P.trr;
-  k.b = make_box(c->lx, c->ly, c->lz);
-  k.partials = c->partials;
-  MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
-  k.in = c->mu;
-  k.out = c->cg_q;
-  MDG_LAUNCH(c, "tmatvec_pre", (unsigned)blocks, kBlock, 0, k_tmatvec_pre<false>, k);
-  MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
-             c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
-  MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
-             c->results);
-  k.in = c->cg_p;
-  k.out = c->cg_q;
-  for (int64_t it = 1; it <= max_iter; ++it) {
-    MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)blocks, kBlock, 0, k_tmatvec_pre<true>, k);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 1, n, tol_debye,
-               c->results);
-    MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
-               c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
-               c->results);
-    fetch_results(c);
-    *last_rms = c->h_results[25];
-    if (c->h_results[27] != 0.0) return it;
-    MDG_LAUNCH(c, "cg_dir", grid_for(n, 256), 256, 0, k_cg_dir, n, c->results, c->cg_z, c->cg_p);
-  }
-  throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
 }
 
 }  // namespace mdg

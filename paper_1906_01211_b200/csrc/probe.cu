@@ -34,10 +34,10 @@ __global__ void __launch_bounds__(kBlock) k_count_within(int64_t n, const double
   if (i < n) {
     const double4 pi = P[i];
     const int cnt = L.cnt[i];
-    const int32_t* row = list_row(L, (int)i);
+    const int32_t* row = list_row(L, i);
     const int32_t mi = mol[i];
     for (int k = 0; k < cnt; ++k) {
-      const int32_t j = __ldg(row + (size_t)k * 32);
+      const int32_t j = __ldg(row + k) & 0x7fffffff;
       const double4 pj = ldg4(P + j);
       double dx, dy, dz;
       const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
