@@ -174,6 +174,46 @@ __device__ __forceinline__ int32_t ring_j(const double4& e) {
   return (int32_t)__double_as_longlong(e.w);
 }
 
+// Walk one site's row with the warp: software-pipelined so the index load of
+// chunk c+2 and the position gather of chunk c+1 are in flight while chunk c
+// is tested and compacted and the body runs (the kernels are latency-bound
+// otherwise). pro(raw, pj, dx, dy, dz) -> in-range?; body(entry, slot) runs
+// on compacted entries, slot = running index of the entry in the row's
+// in-range sequence (for kernels that write a pruned row). Returns the number
+// of in-range entries.
+template <class Pro, class Body>
+__device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt, int lane,
+                                       const double4* __restrict__ P, Ring& ring, Pro&& pro,
+                                       Body&& body) {
+  int32_t ja = (lane < cnt) ? __ldg(row + lane) : 0;
+  double4 pa = ldg4(P + (ja & 0x7fffffff));
+  int32_t jb = (32 + lane < cnt) ? __ldg(row + 32 + lane) : 0;
+  int taken = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    double4 pb = make_double4(0, 0, 0, 0);
+    int32_t jc = 0;
+    if (base + 32 < cnt) pb = ldg4(P + (jb & 0x7fffffff));
+    if (base + 64 + lane < cnt) jc = __ldg(row + base + 64 + lane);
+    double dx = 0, dy = 0, dz = 0;
+    const bool in = (base + lane < cnt) && pro(ja, pa, dx, dy, dz);
+    ring_push(ring, in, dx, dy, dz, ja);
+    if (ring.count >= 32) {
+      body(ring_take(ring, 32, lane), taken + lane);
+      taken += 32;
+    }
+    ja = jb;
+    pa = pb;
+    jb = jc;
+  }
+  if (ring.count > 0) {
+    const int take = ring.count;
+    const double4 e = ring_take(ring, take, lane);
+    if (lane < take) body(e, taken + lane);
+    taken += take;
+  }
+  return taken;
+}
+
 // sites per warp: enough blocks to fill 148 SMs several times over
 inline int sites_per_warp(int64_t n) {
   const int64_t ipw = n / (148LL * kWarps * 16);

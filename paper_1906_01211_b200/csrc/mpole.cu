@@ -166,30 +166,17 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       ty += 2.0 * Mxz;
       tz += 2.0 * Myx;
     };
-    for (int base = 0; base < cnt; base += 32) {
-      const int k = base + lane;
-      bool in = false;
-      double x = 0, y = 0, z = 0;
-      int32_t j = 0;
-      if (k < cnt) {
-        const int32_t raw = __ldg(row + k);
-        j = raw & 0x7fffffff;
-        const double4 pj = ldg4(a.pos + j);
-        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
-        if (PRUNED) {
-          in = !(EXCL && raw < 0);  // same molecule (flag bit)
-        } else {
-          in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
-        }
-      }
-      ring_push(ring, in, x, y, z, j);
-      if (ring.count >= 32) body(ring_take(ring, 32, lane));
-    }
-    if (ring.count > 0) {
-      const int take = ring.count;
-      const double4 e = ring_take(ring, take, lane);
-      if (lane < take) body(e);
-    }
+    run_row(
+        row, cnt, lane, a.pos, ring,
+        [&](int32_t& raw, const double4& pj, double& x, double& y, double& z) {
+          const int32_t j = raw & 0x7fffffff;
+          const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
+          const bool keep = PRUNED ? !(EXCL && raw < 0)  // same molecule (flag bit)
+                                   : (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+          raw = j;
+          return keep;
+        },
+        [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
     fy = warp_allsum(fy);
     fz = warp_allsum(fz);

@@ -86,25 +86,13 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       acc[6] += dy * pz;
       acc[7] += dz * pz;
     };
-    for (int base = 0; base < cnt; base += 32) {
-      const int k = base + lane;
-      bool in = false;
-      double dx = 0, dy = 0, dz = 0;
-      int32_t j = 0;
-      if (k < cnt) {
-        j = __ldg(row + k);
-        const double4 pj = ldg4(a.pos + j);
-        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-        in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
-      }
-      ring_push(ring, in, dx, dy, dz, j);
-      if (ring.count >= 32) body(ring_take(ring, 32, lane));
-    }
-    if (ring.count > 0) {
-      const int take = ring.count;
-      const double4 e = ring_take(ring, take, lane);
-      if (lane < take) body(e);
-    }
+    run_row(
+        row, cnt, lane, a.pos, ring,
+        [&](int32_t j, const double4& pj, double& dx, double& dy, double& dz) {
+          const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+          return (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+        },
+        [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
     fy = warp_allsum(fy);
     fz = warp_allsum(fz);
@@ -229,25 +217,13 @@ __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
       acc[6] += dy * pz;
       acc[7] += dz * pz;
     };
-    for (int base = 0; base < cnt; base += 32) {
-      const int k = base + lane;
-      bool in = false;
-      double dx = 0, dy = 0, dz = 0;
-      int32_t j = 0;
-      if (k < cnt) {
-        j = __ldg(row + k);
-        const double4 pj = ldg4(a.site + j);
-        const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-        in = (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
-      }
-      ring_push(ring, in, dx, dy, dz, j);
-      if (ring.count >= 32) body(ring_take(ring, 32, lane));
-    }
-    if (ring.count > 0) {
-      const int take = ring.count;
-      const double4 e = ring_take(ring, take, lane);
-      if (lane < take) body(e);
-    }
+    run_row(
+        row, cnt, lane, a.site, ring,
+        [&](int32_t j, const double4& pj, double& dx, double& dy, double& dz) {
+          const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+          return (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+        },
+        [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
     fy = warp_allsum(fy);
     fz = warp_allsum(fz);

@@ -72,24 +72,13 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
       ey += rr5 * dot * dy - rr3 * mj.y;
       ez += rr5 * dot * dz - rr3 * mj.z;
     };
-    for (int base = 0; base < cnt; base += 32) {
-      const int k = base + lane;
-      bool in = false;
-      double dx = 0, dy = 0, dz = 0;
-      int32_t j = 0;
-      if (k < cnt) {
-        j = __ldg(row + k) & 0x7fffffff;
-        const double4 pj = ldg4(a.pos + j);
-        in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
-      }
-      ring_push(ring, in, dx, dy, dz, j);
-      if (ring.count >= 32) body(ring_take(ring, 32, lane));
-    }
-    if (ring.count > 0) {
-      const int take = ring.count;
-      const double4 e = ring_take(ring, take, lane);
-      if (lane < take) body(e);
-    }
+    run_row(
+        row, cnt, lane, a.pos, ring,
+        [&](int32_t& raw, const double4& pj, double& dx, double& dy, double& dz) {
+          raw &= 0x7fffffff;
+          return min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
+        },
+        [&](const double4& e, int) { body(e); });
     ex = warp_allsum(ex);
     ey = warp_allsum(ey);
     ez = warp_allsum(ez);
@@ -174,9 +163,8 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
     const int32_t* row = list_row(a.L, i);
     int32_t* prow = TPRE ? a.pnbr + (size_t)i * a.pcap : nullptr;
     double2* trow = TPRE ? a.trr + (size_t)i * a.pcap : nullptr;
-    int32_t pn = 0;  // warp-uniform pruned length
     double ex = 0, ey = 0, ez = 0;
-    auto body = [&](const double4& e, bool live) {
+    auto body = [&](const double4& e, int slot) {
       const int32_t raw = ring_j(e);
       const int32_t j = raw & 0x7fffffff;
       const double dx = e.x, dy = e.y, dz = e.z;
@@ -218,11 +206,11 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
         rr5 = l5 * b2;
         rr7 = l7 * b3;
       }
-      if (TPRE && live && pn + lane < a.pcap) {  // overflow -> host retries larger
-        prow[pn + lane] = raw;
-        trow[pn + lane] = make_double2(rr3, rr5);
+      if (TPRE && slot < a.pcap) {  // overflow -> host retries larger
+        prow[slot] = raw;
+        trow[slot] = make_double2(rr3, rr5);
       }
-      if (!live || (EXCL && raw < 0)) return;
+      if (EXCL && raw < 0) return;
       if (MPOLE) {
         mpole_field(a.mp, j, pj.w, dx, dy, dz, rr3, rr5, rr7, ex, ey, ez);
       } else {
@@ -232,31 +220,17 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
         ez += cq * dz;
       }
     };
-    for (int base = 0; base < cnt; base += 32) {
-      const int k = base + lane;
-      bool in = false;
-      double dx = 0, dy = 0, dz = 0;
-      int32_t raw = 0;
-      if (k < cnt) {
-        const int32_t j = __ldg(row + k) & 0x7fffffff;
-        const double4 pj = ldg4(a.pos + j);
-        in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
-        const bool same = __ldg(a.mol + j) == mi;
-        if (!TPRE && EXCL && same) in = false;
-        raw = (TPRE && same) ? (j | (int32_t)0x80000000) : j;
-      }
-      ring_push(ring, in, dx, dy, dz, raw);
-      if (ring.count >= 32) {
-        body(ring_take(ring, 32, lane), true);
-        pn += 32;
-      }
-    }
-    if (ring.count > 0) {
-      const int take = ring.count;
-      const double4 e = ring_take(ring, take, lane);
-      if (lane < take) body(e, true);
-      pn += take;
-    }
+    const int pn = run_row(
+        row, cnt, lane, a.pos, ring,
+        [&](int32_t& raw, const double4& pj, double& dx, double& dy, double& dz) {
+          const int32_t j = raw & 0x7fffffff;
+          bool in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
+          const bool same = __ldg(a.mol + j) == mi;
+          if (!TPRE && EXCL && same) in = false;
+          raw = (TPRE && same) ? (j | (int32_t)0x80000000) : j;
+          return in;
+        },
+        body);
     ex = warp_allsum(ex);
     ey = warp_allsum(ey);
     ez = warp_allsum(ez);
@@ -391,17 +365,35 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
     const int32_t* row = a.pnbr + (size_t)i * a.pcap;
     const double2* trow = a.trr + (size_t)i * a.pcap;
     double ex = 0, ey = 0, ez = 0;
-    for (int k = lane; k < cnt; k += 32) {
-      const int32_t j = __ldg(row + k) & 0x7fffffff;
-      const double2 rr = __ldg(trow + k);
-      const double4 pj = ldg4(a.pos + j);
-      const double4 mj = ldg4(a.in + j);
-      double dx, dy, dz;
-      min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
-      ex += rr.y * dot * dx - rr.x * mj.x;
-      ey += rr.y * dot * dy - rr.x * mj.y;
-      ez += rr.y * dot * dz - rr.x * mj.z;
+    // 4 slots per lane per round: all index/tensor loads, then all gathers,
+    // then the math -- 8 independent gathers in flight per lane. Slots past
+    // the row end carry rr = 0 and contribute exactly 0.
+    constexpr int U = 4;
+    for (int k0 = lane; k0 < cnt; k0 += 32 * U) {
+      int32_t jj[U];
+      double2 rr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + 32 * u;
+        const bool v = k < cnt;
+        jj[u] = v ? (__ldg(row + k) & 0x7fffffff) : (int32_t)i;
+        rr[u] = v ? __ldg(trow + k) : make_double2(0.0, 0.0);
+      }
+      double4 pj[U], mj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pj[u] = ldg4(a.pos + jj[u]);
+        mj[u] = ldg4(a.in + jj[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double dx, dy, dz;
+        min_image(a.b, pi.x, pi.y, pi.z, pj[u].x, pj[u].y, pj[u].z, dx, dy, dz);
+        const double dot = mj[u].x * dx + mj[u].y * dy + mj[u].z * dz;
+        ex += rr[u].y * dot * dx - rr[u].x * mj[u].x;
+        ey += rr[u].y * dot * dy - rr[u].x * mj[u].y;
+        ez += rr[u].y * dot * dz - rr[u].x * mj[u].z;
+      }
     }
     ex = warp_allsum(ex);
     ey = warp_allsum(ey);
