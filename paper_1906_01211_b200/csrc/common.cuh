@@ -32,11 +32,14 @@ __device__ __forceinline__ double min_image(const Box& b, double xi, double yi, 
   return dist2(dx, dy, dz);
 }
 
+// One 256-bit read-only load per lane (sm_100a LDG.E.ENL2.256): a gathered
+// 32-B record costs one L1 wavefront per distinct sector instead of two
+// LDG.128 instructions. All double4 arrays are 32-B aligned.
 __device__ __forceinline__ double4 ldg4(const double4* p) {
   double4 v;
-  const double2* q = reinterpret_cast<const double2*>(p);
-  double2 a = __ldg(q), b = __ldg(q + 1);
-  v.x = a.x; v.y = a.y; v.z = b.x; v.w = b.y;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
   return v;
 }
 

@@ -17,6 +17,10 @@
 
 #include "common.cuh"
 
+#ifndef MDG_TPRE_UNROLL
+#define MDG_TPRE_UNROLL 1
+#endif
+
 namespace mdg {
 
 // ---- on-the-fly T mat-vec (reference dipole_field_matvec, Ewald generalised)
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
     // 4 slots per lane per round: all index/tensor loads, then all gathers,
     // then the math -- 8 independent gathers in flight per lane. Slots past
     // the row end carry rr = 0 and contribute exactly 0.
-    constexpr int U = 4;
+    constexpr int U = MDG_TPRE_UNROLL;
     for (int k0 = lane; k0 < cnt; k0 += 32 * U) {
       int32_t jj[U];
       double2 rr[U];
@@ -376,8 +380,10 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
       for (int u = 0; u < U; ++u) {
         const int k = k0 + 32 * u;
         const bool v = k < cnt;
-        jj[u] = v ? (__ldg(row + k) & 0x7fffffff) : (int32_t)i;
-        rr[u] = v ? __ldg(trow + k) : make_double2(0.0, 0.0);
+        // streamed once per mat-vec: evict-first so the gathered positions
+        // and dipoles (64 MB) stay resident in L2
+        jj[u] = v ? (__ldcs(row + k) & 0x7fffffff) : (int32_t)i;
+        rr[u] = v ? __ldcs(trow + k) : make_double2(0.0, 0.0);
       }
       double4 pj[U], mj[U];
 #pragma unroll

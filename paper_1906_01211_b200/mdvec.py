@@ -17,7 +17,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdg.so")
+# MDG_LIB points at an alternative build of the same ABI (kernel experiments)
+LIB_PATH = os.environ.get("MDG_LIB", os.path.join(_HERE, "libmdg.so"))
 ROOT = os.path.dirname(_HERE)
 
 kMaxNeighbors = 2560  # proj/include/mdvec/common.hpp:10
