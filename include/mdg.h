@@ -197,6 +197,43 @@ int mdg_fetch_perm_field(mdg_ctx* ctx, double* ex, double* ey, double* ez);
 int mdg_fetch_energies(mdg_ctx* ctx, double* energies4, double* virial9, int64_t* pcg_iters,
                        double* pcg_rms);
 
+/* ---- spatial domain decomposition (one context per GPU / rank) ----------- */
+/* Device vectors addressable by the halo exchange. */
+#define MDG_VEC_POS 0    /* x, y, z (charges stay) */
+#define MDG_VEC_MU 1     /* induced dipoles */
+#define MDG_VEC_P 2      /* PCG search direction */
+#define MDG_VEC_FORCE 3
+#define MDG_VEC_TORQUE 4
+#define MDG_VEC_EPERM 5
+
+/* Like mdg_system_upload, but only the first n_owned caller sites are owned
+ * by this context (their rows are computed: forces, fields, dipoles); the
+ * rest are the halo (inputs only). n_global counts every site of every
+ * domain (PCG RMS normalisation). n_owned == n reproduces mdg_system_upload. */
+int mdg_system_upload_owned(mdg_ctx* ctx, int64_t n, int64_t n_owned, int64_t n_global,
+                            double lx, double ly, double lz, const double* x, const double* y,
+                            const double* z, const double* charge, const double* lj_sigma,
+                            const double* lj_epsilon, const double* hal_r0,
+                            const double* hal_epsilon, const double* polarizability);
+/* Multi-domain hooks used inside the PCG solve: exchange(user, vec_id) must
+ * refresh the halo entries of vec_id (via mdg_vec_pack / mdg_vec_unpack);
+ * allreduce(user, vals, n) sums n doubles over all domains in place. Return
+ * 0 on success. NULL hooks = single domain. */
+typedef int (*mdg_exchange_fn)(void* user, int vec_id);
+typedef int (*mdg_allreduce_fn)(void* user, double* vals, int n);
+int mdg_set_comm(mdg_ctx* ctx, mdg_exchange_fn exchange, mdg_allreduce_fn allreduce, void* user);
+/* Gather 3 doubles per listed caller-order site of vec_id into out[3*count]
+ * (x,y,z interleaved) / scatter them back. Host buffers. */
+int mdg_vec_pack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count, double* out);
+int mdg_vec_unpack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count,
+                   const double* in);
+/* Same with device-resident index and data buffers (e.g. NCCL send/recv
+ * buffers); ordered on the context stream, returns after completion. */
+int mdg_vec_pack_dev(mdg_ctx* ctx, int vec_id, const int32_t* d_sites, int64_t count,
+                     double* d_out);
+int mdg_vec_unpack_dev(mdg_ctx* ctx, int vec_id, const int32_t* d_sites, int64_t count,
+                       const double* d_in);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* CUDA events on the context stream: start records, stop records, waits and
  * returns the elapsed device milliseconds. */

@@ -92,11 +92,15 @@ void spatial_sort(mdg_ctx* c, const double* x, const double* y, const double* z)
   }
   c->perm.resize(n);
   std::iota(c->perm.begin(), c->perm.end(), 0);
-  std::stable_sort(c->perm.begin(), c->perm.end(),
-                   [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  // owned sites first (rows), then the halo; each part in Morton order
+  auto by_key = [&](int32_t a, int32_t b) { return key[a] < key[b]; };
+  std::stable_sort(c->perm.begin(), c->perm.begin() + c->n_own, by_key);
+  std::stable_sort(c->perm.begin() + c->n_own, c->perm.end(), by_key);
   c->iperm.resize(n);
   for (int64_t s = 0; s < n; ++s) c->iperm[c->perm[s]] = (int32_t)s;
   MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_perm, c->perm.data(), n * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_iperm, c->iperm.data(), n * sizeof(int32_t),
                                  cudaMemcpyHostToDevice, c->stream));
 }
 
@@ -157,6 +161,8 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       MDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       const size_t n = (size_t)n_capacity;
       dalloc(&c->d_perm, n);
+      dalloc(&c->d_iperm, n);
+      dalloc(&c->d_idx, n);
       dalloc(&c->pos, n);
       dalloc(&c->vsite, n);
       dalloc(&c->vdwp, n);
@@ -192,7 +198,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (!c) return MDG_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ptrs[] = {c->d_perm, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
+  void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->partials, c->results,
@@ -233,9 +239,22 @@ int mdg_system_upload(mdg_ctx* c, int64_t n, double lx, double ly, double lz, co
                       const double* y, const double* z, const double* charge,
                       const double* lj_sigma, const double* lj_epsilon, const double* hal_r0,
                       const double* hal_epsilon, const double* polarizability) {
+  return mdg_system_upload_owned(c, n, n, n, lx, ly, lz, x, y, z, charge, lj_sigma, lj_epsilon,
+                                 hal_r0, hal_epsilon, polarizability);
+}
+
+int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_global,
+                            double lx, double ly, double lz, const double* x, const double* y,
+                            const double* z, const double* charge, const double* lj_sigma,
+                            const double* lj_epsilon, const double* hal_r0,
+                            const double* hal_epsilon, const double* polarizability) {
   return guard([&] {
     need_ctx(c);
     set_device(c);
+    need(n_owned >= 1 && n_owned <= n, "system: owned count must be in [1, n]");
+    need(n_global >= n, "system: global count must cover the local sites");
+    c->n_own = n_owned;
+    c->n_global = n_global;
     // OrthorhombicBox::validate (proj/include/mdvec/pbc.hpp:14-19)
     need(lx > 0 && ly > 0 && lz > 0 && std::isfinite(lx) && std::isfinite(ly) &&
              std::isfinite(lz),
@@ -269,6 +288,79 @@ int mdg_system_upload(mdg_ctx* c, int64_t n, double lx, double ly, double lz, co
     MDG_CUDA_CHECK(cudaMemsetAsync(c->mp, 0, 3 * n * sizeof(double4), c->stream));
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     c->has_system = true;
+  });
+}
+
+int mdg_set_comm(mdg_ctx* c, mdg_exchange_fn exchange, mdg_allreduce_fn allreduce, void* user) {
+  return guard([&] {
+    need_ctx(c);
+    need((exchange == nullptr) == (allreduce == nullptr), "set_comm: give both hooks or none");
+    c->comm_exchange = exchange;
+    c->comm_allreduce = allreduce;
+    c->comm_user = user;
+  });
+}
+
+int mdg_vec_pack(mdg_ctx* c, int vec_id, const int32_t* sites, int64_t count, double* out) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(count >= 0 && count <= c->n, "vec_pack: count out of range");
+    if (count == 0) return;
+    for (int64_t k = 0; k < count; ++k)
+      need(sites[k] >= 0 && sites[k] < c->n, "vec_pack: site out of range");
+    int32_t* hidx = reinterpret_cast<int32_t*>(c->h_stage + 3 * count);
+    std::memcpy(hidx, sites, count * sizeof(int32_t));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_idx, hidx, count * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, c->stream));
+    mdg::vec_pack(c, vec_id, c->d_idx, count, c->d_stage);
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_stage, c->d_stage, 3 * count * sizeof(double),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::memcpy(out, c->h_stage, 3 * count * sizeof(double));
+  });
+}
+
+int mdg_vec_unpack(mdg_ctx* c, int vec_id, const int32_t* sites, int64_t count,
+                   const double* in) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(count >= 0 && count <= c->n, "vec_unpack: count out of range");
+    if (count == 0) return;
+    for (int64_t k = 0; k < count; ++k)
+      need(sites[k] >= 0 && sites[k] < c->n, "vec_unpack: site out of range");
+    int32_t* hidx = reinterpret_cast<int32_t*>(c->h_stage + 3 * count);
+    std::memcpy(c->h_stage, in, 3 * count * sizeof(double));
+    std::memcpy(hidx, sites, count * sizeof(int32_t));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_idx, hidx, count * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, 3 * count * sizeof(double),
+                                   cudaMemcpyHostToDevice, c->stream));
+    mdg::vec_unpack(c, vec_id, c->d_idx, count, c->d_stage);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int mdg_vec_pack_dev(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
+                     double* d_out) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(count >= 0 && count <= c->n, "vec_pack_dev: count out of range");
+    mdg::vec_pack(c, vec_id, d_sites, count, d_out);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int mdg_vec_unpack_dev(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
+                       const double* d_in) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(count >= 0 && count <= c->n, "vec_unpack_dev: count out of range");
+    mdg::vec_unpack(c, vec_id, d_sites, count, d_in);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -230,6 +230,55 @@ void pack_positions(mdg_ctx* c) {
   if (c->has_hred) run_reduce_sites(c);
 }
 
+// ---- halo exchange: pack / unpack 3 doubles per listed caller-order site ----
+__global__ void k_vec_pack(int64_t count, const int32_t* __restrict__ sites,
+                           const int32_t* __restrict__ iperm, const double4* __restrict__ v,
+                           double* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const double4 a = v[iperm[sites[k]]];
+  out[3 * k] = a.x;
+  out[3 * k + 1] = a.y;
+  out[3 * k + 2] = a.z;
+}
+
+__global__ void k_vec_unpack(int64_t count, const int32_t* __restrict__ sites,
+                             const int32_t* __restrict__ iperm, const double* __restrict__ in,
+                             double4* __restrict__ v) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  double4* a = v + iperm[sites[k]];
+  a->x = in[3 * k];
+  a->y = in[3 * k + 1];
+  a->z = in[3 * k + 2];
+}
+
+double4* vec_by_id(mdg_ctx* c, int vec_id) {
+  switch (vec_id) {
+    case MDG_VEC_POS: return c->pos;
+    case MDG_VEC_MU: return c->mu;
+    case MDG_VEC_P: return c->cg_p;
+    case MDG_VEC_FORCE: return c->force;
+    case MDG_VEC_TORQUE: return c->torque;
+    case MDG_VEC_EPERM: return c->eperm;
+    default: throw_error(MDG_CONTRACT, "unknown vector id");
+  }
+}
+
+void vec_pack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count, double* d_out) {
+  if (count <= 0) return;
+  MDG_LAUNCH(c, "halo_pack", grid_for(count, 256), 256, 0, k_vec_pack, count, d_sites, c->d_iperm,
+             vec_by_id(c, vec_id), d_out);
+}
+
+void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
+                const double* d_in) {
+  if (count <= 0) return;
+  MDG_LAUNCH(c, "halo_unpack", grid_for(count, 256), 256, 0, k_vec_unpack, count, d_sites,
+             c->d_iperm, d_in, vec_by_id(c, vec_id));
+  if (vec_id == MDG_VEC_POS && c->has_hred) run_reduce_sites(c);
+}
+
 // -E_pol = 1/2 sum mu . E_perm ; results[slot] = -0.5 * electric * sum
 __global__ void __launch_bounds__(kBlock) k_dot4(int64_t n, const double4* __restrict__ a,
                                                  const double4* __restrict__ b,
@@ -244,9 +293,10 @@ __global__ void __launch_bounds__(kBlock) k_dot4(int64_t n, const double4* __res
 }
 
 void polar_energy(mdg_ctx* c, double electric, int slot) {
-  const int64_t blocks = grid_for(c->n);
+  const int64_t blocks = grid_for(c->n_own);
   ensure_partials(c, blocks);
-  MDG_LAUNCH(c, "dot", (unsigned)blocks, kBlock, 0, k_dot4, c->n, c->mu, c->eperm, c->partials);
+  MDG_LAUNCH(c, "dot", (unsigned)blocks, kBlock, 0, k_dot4, c->n_own, c->mu, c->eperm,
+             c->partials);
   finalize_partials(c, blocks, 1, slot, -0.5 * electric);
 }
 

@@ -86,8 +86,19 @@ struct mdg_ctx {
   int64_t n_cap = 0;
   int32_t max_pairs = 0;
 
-  // system
+  // system: sites [0, n_own) are owned (their rows are computed), sites
+  // [n_own, n) are the halo of a spatial domain (inputs only); single-domain
+  // runs have n_own == n. n_global counts all sites of all domains.
   int64_t n = 0;
+  int64_t n_own = 0;
+  int64_t n_global = 0;
+  // multi-domain hooks (NULL = single domain): halo exchange of a device
+  // vector before a mat-vec, and a sum all-reduce of host scalars.
+  int (*comm_exchange)(void* user, int vec_id) = nullptr;
+  int (*comm_allreduce)(void* user, double* vals, int n) = nullptr;
+  void* comm_user = nullptr;
+  int32_t* d_iperm = nullptr;  // caller -> sorted index
+  int32_t* d_idx = nullptr;    // staging for halo index lists
   double lx = 0, ly = 0, lz = 0;
   bool has_system = false, has_mpoles = false, has_hred = false, has_mol = false;
   std::vector<int32_t> perm;   // sorted -> caller index
@@ -235,6 +246,10 @@ void gather_vec_to_caller(mdg_ctx* c, const double4* sorted, double* d_dst_soa);
 void scatter_vec_from_caller(mdg_ctx* c, const double* d_src_soa, double4* sorted);
 void zero_vec(mdg_ctx* c, double4* v);
 void pack_system(mdg_ctx* c);
+double4* vec_by_id(mdg_ctx* c, int vec_id);
+void vec_pack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count, double* d_out);
+void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
+                const double* d_in);
 void pack_positions(mdg_ctx* c);
 void polar_energy(mdg_ctx* c, double electric, int slot);
 

@@ -201,8 +201,8 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
                int exclude, bool accumulate) {
   const DevList& L = c->lists[list_id];
   MKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -213,7 +213,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = warp_grid(c->n, k.ipw);
+  const int64_t blocks = warp_grid(c->n_own, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;
@@ -227,8 +227,8 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
 void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate) {
   const PrunedList& P = c->plist;
   MKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -239,7 +239,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = warp_grid(c->n, k.ipw);
+  const int64_t blocks = warp_grid(c->n_own, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;

@@ -182,11 +182,11 @@ __global__ void k_count_stats(int64_t n, const int32_t* __restrict__ cnt,
 }
 
 void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
-  MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, c->n, cnt, c->results, slot);
+  MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, c->n_own, cnt, c->results, slot);
 }
 
 static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
-  const size_t need = (size_t)c->n * (size_t)cap;
+  const size_t need = (size_t)c->n_own * (size_t)cap;
   if (need > L.nbr_elems) {
     if (L.nbr) cudaFree(L.nbr);
     L.nbr = nullptr;
@@ -230,21 +230,22 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
 
   // capacity: density estimate, grown to the measured maximum if exceeded
   const double vol = c->lx * c->ly * c->lz;
-  const double expect = (double)n / vol * 4.18879020478639 * list_cutoff * list_cutoff *
+  const double expect = (double)c->n_global / vol * 4.18879020478639 * list_cutoff * list_cutoff *
                         list_cutoff;
   int32_t cap = (int32_t)std::min<double>((double)c->max_pairs, 1.35 * expect + 48.0);
   cap = std::max<int32_t>(32, (cap + 31) & ~31);
   if (L.cap > cap && L.nbr) cap = L.cap;
   const Box b = make_box(c->lx, c->ly, c->lz);
   const double c2 = list_cutoff * list_cutoff;
-  const int ipw = sites_per_warp(n);
+  const int64_t rows = c->n_own;  // rows for owned sites; candidates span the halo too
+  const int ipw = sites_per_warp(rows);
   for (int attempt = 0; attempt < 2; ++attempt) {
     ensure_list_storage(c, L, cap);
     MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int32_t), c->stream));
-    MDG_LAUNCH(c, "nlist_build", warp_grid(n, ipw), kBlock, 0, k_nlist_build, n, ipw, P,
+    MDG_LAUNCH(c, "nlist_build", warp_grid(rows, ipw), kBlock, 0, k_nlist_build, rows, ipw, P,
                c->cell_of, g, c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm,
                c->d_flag);
-    MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, n, L.cnt, c->results, 60);
+    count_stats(c, L.cnt, 60);
     int32_t bad_site = 0;
     MDG_CUDA_CHECK(cudaMemcpyAsync(&bad_site, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
                                    c->stream));

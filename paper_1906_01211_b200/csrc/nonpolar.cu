@@ -120,8 +120,8 @@ static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
 void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   const DevList& L = c->lists[list_id];
   NonpolarKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
   k.mol = c->mol;
@@ -131,7 +131,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.alpha = a.alpha;
   k.electric = a.electric;
   k.force = (L.sites == MDG_SITES_VDW) ? c->force2 : c->force;
-  const int64_t blocks = warp_grid(c->n, k.ipw);
+  const int64_t blocks = warp_grid(c->n_own, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   if (L.sites == MDG_SITES_VDW && a.do_coul)
@@ -263,8 +263,8 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
                  int exclude) {
   const DevList& L = c->lists[list_id];
   HalgrenKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   const bool reduced = (L.sites == MDG_SITES_VDW);
   k.site = reduced ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
@@ -275,7 +275,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.delta = delta;
   k.gamma = gamma;
   k.force = reduced ? c->force2 : c->force;
-  const int64_t blocks = warp_grid(c->n, k.ipw);
+  const int64_t blocks = warp_grid(c->n_own, k.ipw);
   ensure_partials(c, blocks);
   k.partials = c->partials;
   if (exclude && c->has_mol)
@@ -284,7 +284,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
     MDG_LAUNCH(c, "halgren", (unsigned)blocks, kBlock, 0, k_halgren<false>, k);
   finalize_partials(c, blocks, 8, 0, 0.5);
   if (reduced) {
-    MDG_LAUNCH(c, "chain_rule", grid_for(c->n, 256), 256, 0, k_chain_rule, c->n, c->force2,
+    MDG_LAUNCH(c, "chain_rule", grid_for(c->n_own, 256), 256, 0, k_chain_rule, c->n_own, c->force2,
                c->hpar, c->hfac, c->child_start, c->child, c->force);
   }
 }

@@ -94,8 +94,8 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
                  const double4* in, double4* out) {
   const DevList& L = c->lists[list_id];
   TKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.polp = c->polp;
   k.L = ListView{L.nbr, L.cnt, L.cap};
@@ -105,7 +105,7 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
   k.thole_a = thole_a;
   k.in = in;
   k.out = out;
-  const unsigned g = warp_grid(c->n, k.ipw);
+  const unsigned g = warp_grid(c->n_own, k.ipw);
   if (alpha > 0) MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<true>, k);
   else MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<false>, k);
 }
@@ -249,8 +249,8 @@ static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
                      double4* out) {
   const DevList& L = c->lists[list_id];
   FKArgs k;
-  k.n_i = c->n;
-  k.ipw = sites_per_warp(c->n);
+  k.n_i = c->n_own;
+  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.polp = c->polp;
   k.mp = c->mp;
@@ -272,7 +272,7 @@ void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double
                     int exclude, double4* out) {
   FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, out);
   const bool ew = alpha > 0, mp = c->has_mpoles, ex = exclude && c->has_mol;
-  const unsigned g = warp_grid(c->n, k.ipw);
+  const unsigned g = warp_grid(c->n_own, k.ipw);
 #define PF_CASE(E, M, X)                                                         \
   if (ew == E && mp == M && ex == X) {                                         \
     MDG_LAUNCH(c, "perm_field", g, kBlock, 0, (k_perm_field<E, M, X, false>), k); \
@@ -293,9 +293,9 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
                     int exclude) {
   const DevList& L = c->lists[list_id];
   PrunedList& P = c->plist;
-  const int64_t n = c->n;
+  const int64_t n = c->n_own;
   const double vol = c->lx * c->ly * c->lz;
-  const double expect = (double)n / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
+  const double expect = (double)c->n_global / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
   int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
   cap = std::max<int32_t>(32, (cap + 31) & ~31);
   if (P.cap > cap) cap = std::min(P.cap, L.cap);
@@ -536,8 +536,33 @@ __global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks
   }
 }
 
+// host-side value -> device result slot (stream-ordered)
+static void put_result(mdg_ctx* c, int slot, double v) {
+  c->h_results[slot] = v;
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->results + slot, c->h_results + slot, sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+}
+
+static void dd_exchange(mdg_ctx* c, int vec_id) {
+  MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  if (c->comm_exchange(c->comm_user, vec_id) != 0)
+    throw_error(MDG_COMM, "halo exchange callback failed");
+}
+
+static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
+  if (c->comm_allreduce(c->comm_user, v, nv) != 0)
+    throw_error(MDG_COMM, "all-reduce callback failed");
+}
+
+// PCG over the stored T tensors. Single domain: every scalar recurrence stays
+// on the device (k_cg_scalars) and the host reads one flag per iteration.
+// Multi-domain (comm hooks set): the halo of mu / p is exchanged before each
+// mat-vec, and the local partial sums are all-reduced on the host before the
+// scalars are formed, so every rank takes identical steps.
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
-  const int64_t n = c->n;
+  const int64_t n = c->n_own;
+  const bool dd = c->comm_allreduce != nullptr;
+  const double n_glob = (double)(c->n_global > 0 ? c->n_global : n);
   const int64_t blocks = grid_for(n);
   PrunedList& P = c->plist;
   TPArgs k;
@@ -554,6 +579,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   k.b = make_box(c->lx, c->ly, c->lz);
   k.partials = c->partials;
   MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
+  if (dd) dd_exchange(c, MDG_VEC_MU);
   k.in = c->mu;
   k.out = c->cg_q;
   MDG_LAUNCH(c, "tmatvec_pre", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<false>, k);
@@ -561,19 +587,44 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
              c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
   MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
              c->results);
+  double rz = 0.0;  // global r.z (multi-domain path)
+  if (dd) {
+    fetch_results(c);
+    rz = c->h_results[21];
+    dd_allreduce(c, &rz, 1);
+    put_result(c, 21, rz);
+  }
   k.in = c->cg_p;
   k.out = c->cg_q;
   for (int64_t it = 1; it <= max_iter; ++it) {
+    if (dd) dd_exchange(c, MDG_VEC_P);
     MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<true>, k);
     MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, tblocks, 1, n, tol_debye,
                c->results);
+    if (dd) {
+      fetch_results(c);
+      double pq = c->h_results[20];
+      dd_allreduce(c, &pq, 1);
+      put_result(c, 26, rz / pq);  // a_k from global sums
+    }
     MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
                c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
     MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
                c->results);
     fetch_results(c);
-    *last_rms = c->h_results[25];
-    if (c->h_results[27] != 0.0) return it;
+    if (dd) {
+      double v[2] = {c->h_results[22], c->h_results[23]};  // local rz_new, sum |dmu|^2
+      dd_allreduce(c, v, 2);
+      const double rms = std::sqrt(v[1] / n_glob) * kDebye;
+      put_result(c, 24, v[0] / rz);  // beta
+      rz = v[0];
+      put_result(c, 21, rz);
+      *last_rms = rms;
+      if (rms < tol_debye) return it;
+    } else {
+      *last_rms = c->h_results[25];
+      if (c->h_results[27] != 0.0) return it;
+    }
     MDG_LAUNCH(c, "cg_dir", grid_for(n, 256), 256, 0, k_cg_dir, n, c->results, c->cg_z, c->cg_p);
   }
   throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
@@ -623,7 +674,7 @@ __global__ void k_max_partials(const double* __restrict__ partials, int64_t bloc
 
 int64_t run_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_a, double tol,
                    int64_t max_iter, double* last_resid) {
-  const int64_t n = c->n;
+  const int64_t n = c->n_own;
   const int64_t blocks = grid_for(n);
   ensure_partials(c, blocks);
   zero_vec(c, c->mu);

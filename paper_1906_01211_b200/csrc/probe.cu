@@ -94,10 +94,10 @@ extern "C" int mdg_nlist_count_within(mdg_ctx* c, int list_id, double cutoff, in
     mdg::cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
     const mdg::DevList& L = c->lists[list_id];
     const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
-    const int64_t blocks = mdg::grid_for(c->n);
+    const int64_t blocks = mdg::grid_for(c->n_own);
     mdg::ensure_partials(c, blocks);
     mdg::Box b = mdg::make_box(c->lx, c->ly, c->lz);
-    MDG_LAUNCH(c, "count_within", (unsigned)blocks, mdg::kBlock, 0, mdg::k_count_within, c->n, P,
+    MDG_LAUNCH(c, "count_within", (unsigned)blocks, mdg::kBlock, 0, mdg::k_count_within, c->n_own, P,
                c->mol, (exclude && c->has_mol) ? 1 : 0, mdg::ListView{L.nbr, L.cnt, L.cap}, b,
                cutoff * cutoff, c->partials);
     mdg::finalize_partials(c, blocks, 2, 50, 1.0);

@@ -114,6 +114,13 @@ SIGNATURES = {
     "mdg_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_profile_reset": (C.c_int, [C.c_void_p]),
     "mdg_profile_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+    "mdg_system_upload_owned": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                          C.c_double, C.c_double, C.c_double] + [_dp] * 9),
+    "mdg_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
+    "mdg_vec_unpack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
+    "mdg_vec_pack_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
+    "mdg_vec_unpack_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
     "mdg_timer_start": (C.c_int, [C.c_void_p]),
     "mdg_timer_stop": (C.c_int, [C.c_void_p, _dp]),
     "mdg_probe_fp64_peak": (C.c_int, [C.c_int, _dp]),
@@ -343,6 +350,18 @@ class Engine:
         quad = getattr(s, "quadrupole", None)
         if dip is not None or quad is not None:
             self.upload_multipoles(dip, quad)
+
+    def vec_pack(self, vec_id: int, sites) -> np.ndarray:
+        """3 doubles per listed (caller-order) site of a device vector."""
+        idx = np.ascontiguousarray(sites, np.int32)
+        out = np.zeros(3 * len(idx))
+        check(self.lib.mdg_vec_pack(self.ctx, vec_id, _p(idx, _ip), len(idx), _p(out)))
+        return out
+
+    def vec_unpack(self, vec_id: int, sites, data) -> None:
+        idx = np.ascontiguousarray(sites, np.int32)
+        buf = _f64(data)
+        check(self.lib.mdg_vec_unpack(self.ctx, vec_id, _p(idx, _ip), len(idx), _p(buf)))
 
     def upload_positions(self, x, y, z):
         x, y, z = _f64(x), _f64(y), _f64(z)
