@@ -145,12 +145,12 @@ def local_system(s, plan: Plan):
 class TorchComm:
     """torch.distributed: NCCL (device buffers) or gloo (host buffers)."""
 
-    def __init__(self, device: int | None = None):
+    def __init__(self, device: int | None = None, group=None):
         import torch
         import torch.distributed as dist
-        self.torch, self.dist = torch, dist
+        self.torch, self.dist, self.group = torch, dist, group
         self.rank, self.size = dist.get_rank(), dist.get_world_size()
-        self.cuda = dist.get_backend() == "nccl"
+        self.cuda = dist.get_backend(group) == "nccl"
         self.device = torch.device(f"cuda:{device}") if self.cuda else torch.device("cpu")
 
     def exchange(self, sends: dict, recv_counts: dict) -> dict:
@@ -159,10 +159,10 @@ class TorchComm:
         reqs, out = [], {}
         for q, n in recv_counts.items():
             out[q] = t.empty(n, dtype=t.float64, device=self.device)
-            reqs.append(self.dist.irecv(out[q], src=q))
+            reqs.append(self.dist.irecv(out[q], src=q, group=self.group))
         for q, buf in sends.items():
             tb = buf if isinstance(buf, t.Tensor) else t.from_numpy(np.ascontiguousarray(buf))
-            reqs.append(self.dist.isend(tb.to(self.device), dst=q))
+            reqs.append(self.dist.isend(tb.to(self.device), dst=q, group=self.group))
         for r in reqs:
             r.wait()
         if self.cuda:
@@ -172,7 +172,7 @@ class TorchComm:
     def allreduce(self, vals: np.ndarray) -> np.ndarray:
         t = self.torch
         buf = t.from_numpy(np.array(vals, np.float64)).to(self.device)
-        self.dist.all_reduce(buf)
+        self.dist.all_reduce(buf, group=self.group)
         return buf.cpu().numpy()
 
 
@@ -350,6 +350,20 @@ class DDEngine:
     def owned_dipoles(self):
         mu = self.eng.fetch_dipoles()
         return self.plan.owned, mu[: self.plan.n_owned]
+
+    def check_halo(self, s) -> bool:
+        """Self-check of the exchange path: refresh the halo coordinates and
+        compare them with the global fixture every rank holds."""
+        if not len(self.plan.halo):
+            return True
+        n_own = self.plan.n_owned
+        halo_local = np.arange(n_own, n_own + len(self.plan.halo), dtype=np.int32)
+        # scramble the halo, then let the exchange restore it
+        self.eng.vec_unpack(VEC_POS, halo_local, np.zeros(3 * len(halo_local)))
+        self.exchange(VEC_POS)
+        got = self.eng.vec_pack(VEC_POS, halo_local).reshape(-1, 3)
+        want = np.stack([np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)], 1)[self.plan.halo]
+        return bool(np.array_equal(got, want))
 
     def close(self):
         self.eng.lib.mdg_set_comm(self.eng.ctx, None, None, None)
