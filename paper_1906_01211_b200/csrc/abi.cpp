@@ -177,7 +177,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       dalloc(&c->cell_atoms, n);
       dalloc(&c->d_flag, 8);
       for (double4** v : {&c->force, &c->force2, &c->torque, &c->field, &c->eperm, &c->mu,
-                          &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q, &c->vin})
+                          &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q, &c->vin, &c->pq4})
         dalloc(v, n);
       dalloc(&c->results, 64);
       MDG_CUDA_CHECK(cudaMemset(c->results, 0, 64 * sizeof(double)));
@@ -201,7 +201,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
-                  c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->partials, c->results,
+                  c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
+                  c->results,
                   c->d_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);

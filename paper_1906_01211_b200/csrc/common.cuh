@@ -184,21 +184,28 @@ __device__ __forceinline__ int32_t ring_j(const double4& e) {
 // on compacted entries, slot = running index of the entry in the row's
 // in-range sequence (for kernels that write a pruned row). Returns the number
 // of in-range entries.
+// `mol` (may be NULL) is gathered with the positions so the exclusion test
+// does not wait on its own load; pro(raw, pj, mol_j, dx, dy, dz).
 template <class Pro, class Body>
 __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt, int lane,
-                                       const double4* __restrict__ P, Ring& ring, Pro&& pro,
+                                       const double4* __restrict__ P,
+                                       const int32_t* __restrict__ mol, Ring& ring, Pro&& pro,
                                        Body&& body) {
   int32_t ja = (lane < cnt) ? __ldg(row + lane) : 0;
   double4 pa = ldg4(P + (ja & 0x7fffffff));
+  int32_t ma = mol ? __ldg(mol + (ja & 0x7fffffff)) : 0;
   int32_t jb = (32 + lane < cnt) ? __ldg(row + 32 + lane) : 0;
   int taken = 0;
   for (int base = 0; base < cnt; base += 32) {
     double4 pb = make_double4(0, 0, 0, 0);
-    int32_t jc = 0;
-    if (base + 32 < cnt) pb = ldg4(P + (jb & 0x7fffffff));
+    int32_t jc = 0, mb = 0;
+    if (base + 32 < cnt) {
+      pb = ldg4(P + (jb & 0x7fffffff));
+      if (mol) mb = __ldg(mol + (jb & 0x7fffffff));
+    }
     if (base + 64 + lane < cnt) jc = __ldg(row + base + 64 + lane);
     double dx = 0, dy = 0, dz = 0;
-    const bool in = (base + lane < cnt) && pro(ja, pa, dx, dy, dz);
+    const bool in = (base + lane < cnt) && pro(ja, pa, ma, dx, dy, dz);
     ring_push(ring, in, dx, dy, dz, ja);
     if (ring.count >= 32) {
       body(ring_take(ring, 32, lane), taken + lane);
@@ -206,6 +213,7 @@ __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt,
     }
     ja = jb;
     pa = pb;
+    ma = mb;
     jb = jc;
   }
   if (ring.count > 0) {
@@ -216,6 +224,13 @@ __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt,
   }
   return taken;
 }
+
+// Site loop of a warp-per-site kernel launched by MDG_LAUNCH_SITES: block b
+// owns sites [b*ipb, (b+1)*ipb), its warps take every kWarps-th site.
+#define MDG_SITE_LOOP(i, n, ipb)                                                 \
+  for (int64_t i = (int64_t)blockIdx.x * (ipb) + (threadIdx.x >> 5),            \
+               i##_end = min((int64_t)(n), ((int64_t)blockIdx.x + 1) * (ipb));  \
+       i < i##_end; i += kWarps)
 
 // sites per warp: enough blocks to fill 148 SMs several times over
 inline int sites_per_warp(int64_t n) {

@@ -2,6 +2,8 @@
 // reductions, permutation between the caller's order and the device's
 // spatially sorted order, Halgren site reduction.
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -56,6 +58,30 @@ void flush_profile(mdg_ctx* c) {
     c->event_pool.push_back(pe.b);
   }
   c->pending.clear();
+}
+
+int64_t sites_per_block(const void* kernel, int64_t n) {
+  static std::mutex mu;
+  static std::map<const void*, int> occ;
+  static int sms = 0;
+  int nb;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (sms == 0) {
+      int dev = 0;
+      MDG_CUDA_CHECK(cudaGetDevice(&dev));
+      MDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    auto it = occ.find(kernel);
+    if (it == occ.end()) {
+      int v = 0;
+      MDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, kBlock, 0));
+      it = occ.emplace(kernel, std::max(1, v)).first;
+    }
+    nb = it->second;
+  }
+  const int64_t blocks = (int64_t)sms * nb;
+  return std::max<int64_t>(kWarps, (n + blocks - 1) / blocks);
 }
 
 void ensure_partials(mdg_ctx* c, int64_t blocks) {
@@ -193,21 +219,24 @@ void run_reduce_sites(mdg_ctx* c) {
 __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
                               const double* __restrict__ st, double4* __restrict__ pos,
                               double4* __restrict__ vsite, double4* __restrict__ vdwp,
-                              double2* __restrict__ polp) {
+                              double2* __restrict__ polp, double4* __restrict__ pq4) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t o = perm[s];
   const double x = st[o], y = st[n + o], z = st[2 * n + o];
-  pos[s] = make_double4(x, y, z, st[3 * n + o]);
+  const double q = st[3 * n + o];
+  pos[s] = make_double4(x, y, z, q);
   vsite[s] = make_double4(x, y, z, 0.0);
   vdwp[s] = make_double4(st[4 * n + o], sqrt(st[5 * n + o]), st[6 * n + o], sqrt(st[7 * n + o]));
   const double pol = st[8 * n + o];
-  polp[s] = make_double2(pol, cbrt(sqrt(pol)));
+  const double pd = cbrt(sqrt(pol));
+  polp[s] = make_double2(pol, pd);
+  pq4[s] = make_double4(pol, pd, q, 0.0);
 }
 
 void pack_system(mdg_ctx* c) {
   MDG_LAUNCH(c, "pack_system", grid_for(c->n, 256), 256, 0, k_pack_system, c->n, c->d_perm,
-             c->d_stage, c->pos, c->vsite, c->vdwp, c->polp);
+             c->d_stage, c->pos, c->vsite, c->vdwp, c->polp, c->pq4);
 }
 
 // staging: x y z (caller order); keeps charges

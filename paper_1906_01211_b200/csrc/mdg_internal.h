@@ -110,6 +110,7 @@ struct mdg_ctx {
   double4* vsite = nullptr;
   double4* vdwp = nullptr;
   double2* polp = nullptr;
+  double4* pq4 = nullptr;  // (polarizability, polarizability^(1/6), charge, 0)
   int32_t* mol = nullptr;
   int32_t* hpar = nullptr;
   double* hfac = nullptr;
@@ -165,6 +166,7 @@ struct mdg_ctx {
   std::vector<mdg::PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+  int64_t last_grid = 0;  // blocks of the last MDG_LAUNCH_SITES launch
 };
 
 namespace mdg {
@@ -194,6 +196,25 @@ void flush_profile(mdg_ctx* c);
 inline unsigned grid_for(int64_t n, int block = kBlock) {
   return (unsigned)((n + block - 1) / block);
 }
+
+// Warp-per-site kernels run exactly one wave: (#SMs x resident blocks per
+// SM) blocks, each walking a contiguous (Morton-ordered, spatially compact)
+// range of sites with its warps interleaved, so an SM's live neighbour data
+// is a sliding window that stays in L1. Returns sites per block.
+int64_t sites_per_block(const void* kernel, int64_t n);
+
+// Launch a warp-per-site kernel whose args struct has `ipw` (sites per block)
+// and `partials`; records the grid in ctx->last_grid for the finalize.
+#define MDG_LAUNCH_SITES(ctx, name, n, args, kernel)                             \
+  do {                                                                         \
+    const int64_t _ipb = ::mdg::sites_per_block((const void*)(kernel), (n));   \
+    (args).ipw = (int)_ipb;                                                    \
+    const int64_t _g = ((n) + _ipb - 1) / _ipb;                                \
+    ::mdg::ensure_partials((ctx), _g);                                         \
+    (args).partials = (ctx)->partials;                                         \
+    (ctx)->last_grid = _g;                                                     \
+    MDG_LAUNCH((ctx), (name), (unsigned)_g, ::mdg::kBlock, 0, kernel, (args)); \
+  } while (0)
 
 // ---- host entry points implemented in the .cu files -----------------------
 void ensure_partials(mdg_ctx* c, int64_t blocks);

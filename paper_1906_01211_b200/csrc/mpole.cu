@@ -48,11 +48,9 @@ template <bool EXCL, bool PRUNED>
 __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
     const double qi = pi.w;
@@ -167,12 +165,12 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       tz += 2.0 * Myx;
     };
     run_row(
-        row, cnt, lane, a.pos, ring,
-        [&](int32_t& raw, const double4& pj, double& x, double& y, double& z) {
+        row, cnt, lane, a.pos, (EXCL && !PRUNED) ? a.mol : nullptr, ring,
+        [&](int32_t& raw, const double4& pj, int32_t mj, double& x, double& y, double& z) {
           const int32_t j = raw & 0x7fffffff;
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
           const bool keep = PRUNED ? !(EXCL && raw < 0)  // same molecule (flag bit)
-                                   : (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+                                   : (r2 <= a.c2) && !(EXCL && mj == mi);
           raw = j;
           return keep;
         },
@@ -202,7 +200,6 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   const DevList& L = c->lists[list_id];
   MKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -213,22 +210,18 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = warp_grid(c->n_own, k.ipw);
-  ensure_partials(c, blocks);
-  k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;
   if (exclude && c->has_mol)
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<true, false>), k);
+    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, false>));
   else
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<false, false>), k);
-  finalize_partials(c, blocks, 10, 10, 0.5);
+    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, false>));
+  finalize_partials(c, c->last_grid, 10, 10, 0.5);
 }
 
 void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate) {
   const PrunedList& P = c->plist;
   MKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
@@ -239,15 +232,12 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.electric = electric;
   k.force = c->force;
   k.torque = c->torque;
-  const int64_t blocks = warp_grid(c->n_own, k.ipw);
-  ensure_partials(c, blocks);
-  k.partials = c->partials;
   k.accumulate = accumulate ? 1 : 0;
   if (exclude && c->has_mol)
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<true, true>), k);
+    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, true>));
   else
-    MDG_LAUNCH(c, "mpole", (unsigned)blocks, kBlock, 0, (k_mpole<false, true>), k);
-  finalize_partials(c, blocks, 10, 10, 0.5);
+    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, true>));
+  finalize_partials(c, c->last_grid, 10, 10, 0.5);
 }
 
 }  // namespace mdg

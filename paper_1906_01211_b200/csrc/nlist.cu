@@ -103,9 +103,7 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
     double c2, int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
     const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t i0 = w * ipw, i1 = min(n_i, i0 + ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, n_i, ipw) {
     const double4 pi = P[i];
     const int c = cell_of[i];
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
@@ -238,11 +236,12 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
   const Box b = make_box(c->lx, c->ly, c->lz);
   const double c2 = list_cutoff * list_cutoff;
   const int64_t rows = c->n_own;  // rows for owned sites; candidates span the halo too
-  const int ipw = sites_per_warp(rows);
+  const int64_t ipb = sites_per_block((const void*)k_nlist_build, rows);
+  const unsigned ngrid = (unsigned)((rows + ipb - 1) / ipb);
   for (int attempt = 0; attempt < 2; ++attempt) {
     ensure_list_storage(c, L, cap);
     MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int32_t), c->stream));
-    MDG_LAUNCH(c, "nlist_build", warp_grid(rows, ipw), kBlock, 0, k_nlist_build, rows, ipw, P,
+    MDG_LAUNCH(c, "nlist_build", ngrid, kBlock, 0, k_nlist_build, rows, (int)ipb, P,
                c->cell_of, g, c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm,
                c->d_flag);
     count_stats(c, L.cnt, 60);

@@ -30,12 +30,10 @@ template <bool LJ, bool COUL, bool SHIFT, bool EXCL>
 __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const double two_over_sqrt_pi = 1.1283791670955126;
-  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     double4 vi = make_double4(0, 0, 0, 0);
     if (LJ) vi = a.vdwp[i];
@@ -87,10 +85,10 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       acc[7] += dz * pz;
     };
     run_row(
-        row, cnt, lane, a.pos, ring,
-        [&](int32_t j, const double4& pj, double& dx, double& dy, double& dz) {
+        row, cnt, lane, a.pos, EXCL ? a.mol : nullptr, ring,
+        [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+          return (r2 <= a.c2) && !(EXCL && mj == mi);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
@@ -104,10 +102,10 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
 template <bool LJ, bool COUL>
 static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
                       const char* name) {
-  const unsigned g = warp_grid(k.n_i, k.ipw);
+  NonpolarKArgs kk = k;
 #define NP_CASE(S, E)                                                            \
   if (shift == S && excl == E) {                                               \
-    MDG_LAUNCH(c, name, g, kBlock, 0, (k_nonpolar<LJ, COUL, S, E>), k);         \
+    MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E>));        \
     return;                                                                    \
   }
   NP_CASE(false, false)
@@ -121,7 +119,6 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   const DevList& L = c->lists[list_id];
   NonpolarKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
   k.mol = c->mol;
@@ -131,16 +128,13 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.alpha = a.alpha;
   k.electric = a.electric;
   k.force = (L.sites == MDG_SITES_VDW) ? c->force2 : c->force;
-  const int64_t blocks = warp_grid(c->n_own, k.ipw);
-  ensure_partials(c, blocks);
-  k.partials = c->partials;
   if (L.sites == MDG_SITES_VDW && a.do_coul)
     throw_error(MDG_CONTRACT, "coulomb terms need a list over atomic sites");
   const bool shift = a.shift != 0, excl = a.exclude != 0 && c->has_mol;
   if (a.do_lj && a.do_coul) launch_np<true, true>(c, k, shift, excl, "lj_ewald");
   else if (a.do_lj) launch_np<true, false>(c, k, shift, excl, "lj");
   else launch_np<false, true>(c, k, shift, excl, "ewald_real");
-  finalize_partials(c, blocks, 8, 0, 0.5);
+  finalize_partials(c, c->last_grid, 8, 0, 0.5);
 }
 
 // ---- Halgren buffered 14-7 -------------------------------------------------
@@ -161,12 +155,10 @@ template <bool EXCL>
 __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const double delta = a.delta, gamma = a.gamma;
-  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.site[i];
     const double4 vi = a.vdwp[i];
     const int32_t mi = EXCL ? a.mol[i] : 0;
@@ -218,10 +210,10 @@ __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
       acc[7] += dz * pz;
     };
     run_row(
-        row, cnt, lane, a.site, ring,
-        [&](int32_t j, const double4& pj, double& dx, double& dy, double& dz) {
+        row, cnt, lane, a.site, EXCL ? a.mol : nullptr, ring,
+        [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && __ldg(a.mol + j) == mi);
+          return (r2 <= a.c2) && !(EXCL && mj == mi);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
@@ -264,7 +256,6 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   const DevList& L = c->lists[list_id];
   HalgrenKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   const bool reduced = (L.sites == MDG_SITES_VDW);
   k.site = reduced ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
@@ -275,14 +266,11 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.delta = delta;
   k.gamma = gamma;
   k.force = reduced ? c->force2 : c->force;
-  const int64_t blocks = warp_grid(c->n_own, k.ipw);
-  ensure_partials(c, blocks);
-  k.partials = c->partials;
   if (exclude && c->has_mol)
-    MDG_LAUNCH(c, "halgren", (unsigned)blocks, kBlock, 0, k_halgren<true>, k);
+    MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, k_halgren<true>);
   else
-    MDG_LAUNCH(c, "halgren", (unsigned)blocks, kBlock, 0, k_halgren<false>, k);
-  finalize_partials(c, blocks, 8, 0, 0.5);
+    MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, k_halgren<false>);
+  finalize_partials(c, c->last_grid, 8, 0, 0.5);
   if (reduced) {
     MDG_LAUNCH(c, "chain_rule", grid_for(c->n_own, 256), 256, 0, k_chain_rule, c->n_own, c->force2,
                c->hpar, c->hfac, c->child_start, c->child, c->force);

@@ -34,16 +34,15 @@ struct TKArgs {
   double c2, alpha, thole_a;
   const double4* __restrict__ in;
   double4* __restrict__ out;
+  double* __restrict__ partials;  // unused (launch macro contract)
 };
 
 template <bool EWALD>
 __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
-  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     const double2 ai = a.polp[i];
     const int cnt = a.L.cnt[i];
@@ -77,8 +76,8 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
       ez += rr5 * dot * dz - rr3 * mj.z;
     };
     run_row(
-        row, cnt, lane, a.pos, ring,
-        [&](int32_t& raw, const double4& pj, double& dx, double& dy, double& dz) {
+        row, cnt, lane, a.pos, nullptr, ring,
+        [&](int32_t& raw, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           raw &= 0x7fffffff;
           return min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
         },
@@ -95,7 +94,6 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
   const DevList& L = c->lists[list_id];
   TKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.polp = c->polp;
   k.L = ListView{L.nbr, L.cnt, L.cap};
@@ -105,9 +103,8 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
   k.thole_a = thole_a;
   k.in = in;
   k.out = out;
-  const unsigned g = warp_grid(c->n_own, k.ipw);
-  if (alpha > 0) MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<true>, k);
-  else MDG_LAUNCH(c, "tmatvec", g, kBlock, 0, k_tmatvec<false>, k);
+  if (alpha > 0) MDG_LAUNCH_SITES(c, "tmatvec", k.n_i, k, k_tmatvec<true>);
+  else MDG_LAUNCH_SITES(c, "tmatvec", k.n_i, k, k_tmatvec<false>);
 }
 
 // ---- permanent field ----------------------------------------------------------
@@ -127,6 +124,8 @@ struct FKArgs {
   double2* __restrict__ trr;
   int32_t* __restrict__ pcnt;
   int32_t pcap;
+  double* __restrict__ partials;  // unused (launch macro contract)
+  const double4* __restrict__ pq4;
 };
 
 // Field at i of the multipole of j, R = r_i - r_j (Tinker's stored Q = Theta/3):
@@ -156,10 +155,8 @@ template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE>
 __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
-  const int64_t i0 = w * a.ipw, i1 = min(a.n_i, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     const double2 ai = a.polp[i];
     const int32_t mi = a.mol[i];
@@ -173,8 +170,10 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
       const int32_t j = raw & 0x7fffffff;
       const double dx = e.x, dy = e.y, dz = e.z;
       const double r2 = dist2(dx, dy, dz);
-      const double2 aj = __ldg(a.polp + j);
-      const double4 pj = ldg4(a.pos + j);
+      // (polarizability, polarizability^(1/6), charge) of j in one 32-B load
+      const double4 xj = ldg4(a.pq4 + j);
+      const double2 aj = make_double2(xj.x, xj.y);
+      const double4 pj = make_double4(0.0, 0.0, 0.0, xj.z);
       const double r = sqrt(r2);
       const double inv_r2 = 1.0 / r2;
       const double b1 = inv_r2 / r;
@@ -225,11 +224,11 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
       }
     };
     const int pn = run_row(
-        row, cnt, lane, a.pos, ring,
-        [&](int32_t& raw, const double4& pj, double& dx, double& dy, double& dz) {
+        row, cnt, lane, a.pos, a.mol, ring,
+        [&](int32_t& raw, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const int32_t j = raw & 0x7fffffff;
           bool in = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.c2;
-          const bool same = __ldg(a.mol + j) == mi;
+          const bool same = mj == mi;
           if (!TPRE && EXCL && same) in = false;
           raw = (TPRE && same) ? (j | (int32_t)0x80000000) : j;
           return in;
@@ -250,9 +249,9 @@ static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   const DevList& L = c->lists[list_id];
   FKArgs k;
   k.n_i = c->n_own;
-  k.ipw = sites_per_warp(c->n_own);
   k.pos = c->pos;
   k.polp = c->polp;
+  k.pq4 = c->pq4;
   k.mp = c->mp;
   k.mol = c->mol;
   k.L = ListView{L.nbr, L.cnt, L.cap};
@@ -272,10 +271,9 @@ void run_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double
                     int exclude, double4* out) {
   FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, out);
   const bool ew = alpha > 0, mp = c->has_mpoles, ex = exclude && c->has_mol;
-  const unsigned g = warp_grid(c->n_own, k.ipw);
 #define PF_CASE(E, M, X)                                                         \
   if (ew == E && mp == M && ex == X) {                                         \
-    MDG_LAUNCH(c, "perm_field", g, kBlock, 0, (k_perm_field<E, M, X, false>), k); \
+    MDG_LAUNCH_SITES(c, "perm_field", k.n_i, k, (k_perm_field<E, M, X, false>)); \
     return;                                                                    \
   }
   PF_CASE(false, false, false)
@@ -318,12 +316,11 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
     k.trr = P.trr;
     k.pcnt = P.cnt;
     k.pcap = cap;
-    const unsigned g = warp_grid(n, k.ipw);
     // rows longer than cap are counted, not written; the retry below grows cap
-    if (mp && ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, true, true, true>), k);
-    else if (mp) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, true, false, true>), k);
-    else if (ex) MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, false, true, true>), k);
-    else MDG_LAUNCH(c, "field_tpre", g, kBlock, 0, (k_perm_field<true, false, false, true>), k);
+    if (mp && ex) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, true, true, true>));
+    else if (mp) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, true, false, true>));
+    else if (ex) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, false, true, true>));
+    else MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, false, false, true>));
     count_stats(c, P.cnt, 62);
     fetch_results(c);
     const int32_t mx = (int32_t)c->h_results[62];
@@ -360,10 +357,8 @@ struct TPArgs {
 template <bool PCG>
 __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)kBlock + threadIdx.x) >> 5;
   double acc[1] = {0.0};
-  const int64_t i0 = w * a.ipw, i1 = min(a.n, i0 + a.ipw);
-  for (int64_t i = i0; i < i1; ++i) {
+  MDG_SITE_LOOP(i, a.n, a.ipw) {
     const double4 pi = a.pos[i];
     const int cnt = a.pcnt[i];
     const int32_t* row = a.pnbr + (size_t)i * a.pcap;
@@ -567,9 +562,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   PrunedList& P = c->plist;
   TPArgs k;
   k.n = n;
-  k.ipw = sites_per_warp(n);
-  const int64_t tblocks = warp_grid(n, k.ipw);
-  ensure_partials(c, std::max(blocks, tblocks));
+  ensure_partials(c, blocks);
   k.pos = c->pos;
   k.polp = c->polp;
   k.pnbr = P.nbr;
@@ -582,7 +575,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   if (dd) dd_exchange(c, MDG_VEC_MU);
   k.in = c->mu;
   k.out = c->cg_q;
-  MDG_LAUNCH(c, "tmatvec_pre", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<false>, k);
+  MDG_LAUNCH_SITES(c, "tmatvec_pre", n, k, k_tmatvec_pre<false>);
   MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
              c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
   MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
@@ -598,9 +591,9 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   k.out = c->cg_q;
   for (int64_t it = 1; it <= max_iter; ++it) {
     if (dd) dd_exchange(c, MDG_VEC_P);
-    MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)tblocks, kBlock, 0, k_tmatvec_pre<true>, k);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, tblocks, 1, n, tol_debye,
-               c->results);
+    MDG_LAUNCH_SITES(c, "tmatvec_pcg", n, k, k_tmatvec_pre<true>);
+    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, c->last_grid, 1, n,
+               tol_debye, c->results);
     if (dd) {
       fetch_results(c);
       double pq = c->h_results[20];
