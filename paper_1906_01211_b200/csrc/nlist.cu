@@ -84,14 +84,29 @@ __global__ void k_cell_sort(int64_t m, const int32_t* __restrict__ start,
   }
 }
 
-__device__ __forceinline__ int axis_cells(int c, int nc, int (&out)[3]) {
-  // periodic neighbours c-1, c, c+1, deduplicated (nc == 1 or 2 collapse)
-  if (nc == 1) { out[0] = 0; return 1; }
-  if (nc == 2) { out[0] = 0; out[1] = 1; return 2; }
-  out[0] = (c + nc - 1) % nc;
-  out[1] = c;
-  out[2] = (c + 1) % nc;
-  return 3;
+// Cells have edge >= cutoff / kReach, so every partner is within kReach cells
+// per axis. x, y: the deduplicated periodic cells c-kReach .. c+kReach; z: the
+// same cells as at most two contiguous runs, each one contiguous range of the
+// cell-sorted site array (cells are numbered z-fastest).
+constexpr int kReach = 2;
+constexpr int kSpan = 2 * kReach + 1;
+
+__device__ __forceinline__ int axis_cells(int c, int nc, int (&out)[kSpan]) {
+  if (kSpan >= nc) {
+    for (int k = 0; k < nc; ++k) out[k] = k;
+    return nc;
+  }
+  for (int d = -kReach; d <= kReach; ++d) out[d + kReach] = (c + d + nc) % nc;
+  return kSpan;
+}
+
+__device__ __forceinline__ int axis_runs(int c, int nc, int (&lo)[2], int (&hi)[2]) {
+  if (kSpan >= nc) { lo[0] = 0; hi[0] = nc - 1; return 1; }
+  const int a = c - kReach, b = c + kReach;
+  if (a < 0) { lo[0] = 0; hi[0] = b; lo[1] = a + nc; hi[1] = nc - 1; return 2; }
+  if (b >= nc) { lo[0] = a; hi[0] = nc - 1; lo[1] = 0; hi[1] = b - nc; return 2; }
+  lo[0] = a; hi[0] = b;
+  return 1;
 }
 
 // Warp per site: lanes sweep a cell's sites 32 at a time (coalesced cell
@@ -107,9 +122,9 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
     const double4 pi = P[i];
     const int c = cell_of[i];
     const int cz = c % g.ncz, cy = (c / g.ncz) % g.ncy, cx = c / (g.ncz * g.ncy);
-    int xs[3], ys[3], zs[3];
+    int xs[kSpan], ys[kSpan], zlo[2], zhi[2];
     const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
-              nz = axis_cells(cz, g.ncz, zs);
+              nz = axis_runs(cz, g.ncz, zlo, zhi);
     int32_t* out = nbr + (size_t)i * (size_t)cap;
     int32_t k = 0;  // warp-uniform row length
     // reference capacity rule: the half list stores a pair on the lower
@@ -119,9 +134,9 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
     for (int a = 0; a < nx; ++a)
       for (int bb = 0; bb < ny; ++bb)
         for (int q = 0; q < nz; ++q) {
-          const int cell = (xs[a] * g.ncy + ys[bb]) * g.ncz + zs[q];
-          const int32_t e = start[cell + 1];
-          for (int32_t s0 = start[cell]; s0 < e; s0 += 32) {
+          const int col = (xs[a] * g.ncy + ys[bb]) * g.ncz;
+          const int32_t e = start[col + zhi[q] + 1];
+          for (int32_t s0 = start[col + zlo[q]]; s0 < e; s0 += 32) {
             const int32_t s = s0 + lane;
             bool in = false;
             int32_t j = 0;
@@ -199,9 +214,12 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
   DevList& L = c->lists[list_id];
   const double4* P = (sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   Grid g;
-  g.ncx = std::max(1, (int)(c->lx / list_cutoff));
-  g.ncy = std::max(1, (int)(c->ly / list_cutoff));
-  g.ncz = std::max(1, (int)(c->lz / list_cutoff));
+  // edge >= list_cutoff / kReach: the (2 kReach + 1)^3 stencil covers a
+  // sphere-sized region with ~40% fewer candidates than 27 full-size cells
+  const double cell_min = list_cutoff / kReach;
+  g.ncx = std::max(1, (int)(c->lx / cell_min));
+  g.ncy = std::max(1, (int)(c->ly / cell_min));
+  g.ncz = std::max(1, (int)(c->lz / cell_min));
   g.ex = c->lx / g.ncx;
   g.ey = c->ly / g.ncy;
   g.ez = c->lz / g.ncz;
