@@ -176,6 +176,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       dalloc(&c->cell_of, n);
       dalloc(&c->cell_atoms, n);
       dalloc(&c->d_flag, 8);
+      MDG_CUDA_CHECK(cudaMemset(c->d_flag, 0, 8 * sizeof(int32_t)));
       for (double4** v : {&c->force, &c->force2, &c->torque, &c->field, &c->eperm, &c->mu,
                           &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q, &c->vin, &c->pq4})
         dalloc(v, n);
@@ -582,6 +583,7 @@ int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
     MDG_CUDA_CHECK(cudaMemcpy(L.cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice));
     L.cap = cap;
     L.valid = true;
+    L.version = ++c->epoch;
     L.cutoff = list_cutoff;
     L.sites = sites;
     L.max_cnt = mx;

@@ -23,7 +23,10 @@
 
 namespace mdg {
 
-constexpr int kBlock = 128;      // pair-kernel block: 4 warps = 4 site groups
+#ifndef MDG_BLOCK
+#define MDG_BLOCK 128
+#endif
+constexpr int kBlock = MDG_BLOCK;  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
 constexpr int kMaxBlocksRed = 1 << 20;
 
@@ -51,6 +54,7 @@ struct DevList {
   size_t nbr_elems = 0;
   int64_t half_pairs = 0;
   int32_t max_cnt = 0;
+  int64_t version = 0;          // bumped by every (re)build / import
 };
 
 // Pruned list: the pairs of a source list within a kernel cutoff, compacted
@@ -152,6 +156,7 @@ struct mdg_ctx {
 
   mdg::DevList lists[MDG_MAX_LISTS];
   mdg::PrunedList plist;
+  int64_t epoch = 0;  // source of DevList::version
 
   // last step
   double energies[4] = {0, 0, 0, 0};
@@ -260,6 +265,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
 // PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
 void run_reduce_sites(mdg_ctx* c);
+
 
 // permutation helpers (device kernels)
 void scatter_sorted_scalar(mdg_ctx* c, const double* d_src, double* d_dst_sorted);

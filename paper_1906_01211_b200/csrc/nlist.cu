@@ -167,35 +167,131 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
 }
 
 // max and sum of counts -> results[slot], results[slot+1]
+// max and sum of cnt[0..n) over the whole GPU in one launch: block partials
+// go to integer atomics in flag[1] (max), flag[2..3] (sum, int64) and the
+// last block to finish publishes them and resets the scratch (integer
+// arithmetic, so the result is order-independent).
 __global__ void k_count_stats(int64_t n, const int32_t* __restrict__ cnt,
-                              double* __restrict__ results, int slot) {
-  __shared__ long long s_sum[256];
-  __shared__ int s_max[256];
+                              double* __restrict__ results, int slot, int32_t* __restrict__ flag) {
+  __shared__ long long s_sum[8];
+  __shared__ int s_max[8];
+  __shared__ bool last;
   long long sum = 0;
   int mx = 0;
-  for (int64_t i = threadIdx.x; i < n; i += 256) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
     const int v = cnt[i];
     sum += v;
     mx = max(mx, v);
   }
-  s_sum[threadIdx.x] = sum;
-  s_max[threadIdx.x] = mx;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
-      s_max[threadIdx.x] = max(s_max[threadIdx.x], s_max[threadIdx.x + w]);
-    }
-    __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_sum[warp] = sum; s_max[warp] = mx; }
+  __syncthreads();
+  unsigned long long* gsum = reinterpret_cast<unsigned long long*>(flag + 2);
   if (threadIdx.x == 0) {
-    results[slot] = (double)s_max[0];
-    results[slot + 1] = (double)s_sum[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { sum += s_sum[w]; mx = max(mx, s_max[w]); }
+    atomicMax(flag + 1, mx);
+    atomicAdd(gsum, (unsigned long long)sum);
+    __threadfence();
+    last = (atomicAdd(flag + 4, 1) == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    results[slot] = (double)*(volatile int*)(flag + 1);
+    results[slot + 1] = (double)(long long)*(volatile unsigned long long*)gsum;
+    flag[1] = 0;
+    *gsum = 0ull;
+    flag[4] = 0;
   }
 }
 
 void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
-  MDG_LAUNCH(c, "count_stats", 1, 256, 0, k_count_stats, c->n_own, cnt, c->results, slot);
+  const unsigned blocks = (unsigned)std::min<int64_t>(296, std::max<int64_t>(1, grid_for(c->n_own, 256)));
+  MDG_LAUNCH(c, "count_stats", blocks, 256, 0, k_count_stats, c->n_own, cnt, c->results, slot,
+             c->d_flag);
+}
+
+// Sort every row ascending by j: with Morton-ordered sites, consecutive j of
+// a sorted row share cache lines, so the pair kernels' 32-lane gathers touch
+// fewer lines. Bitonic network over the warp: element e = r * 32 + lane lives
+// in register r of `lane`; strides < 32 exchange by shuffle, larger ones
+// within the lane. R = padded row length / 32 (a power of two).
+template <int R>
+__global__ void __launch_bounds__(kBlock) k_sort_rows(int64_t n, int32_t* __restrict__ nbr,
+                                                    const int32_t* __restrict__ cnt, int32_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
+  for (int64_t i = blockIdx.x * (int64_t)(kBlock / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const int m = cnt[i];
+    if (m < 2) continue;
+    int32_t* row = nbr + (size_t)i * cap;
+    int32_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = r * 32 + lane;
+      v[r] = (e < m) ? row[e] : 0x7fffffff;
+    }
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= 32) {
+          const int jr = j >> 5;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if ((r & jr) == 0) {
+              const int e = r * 32 + lane;
+              const bool asc = (e & k) == 0;
+              const int32_t a = v[r], b = v[r | jr];
+              if ((a > b) == asc) { v[r] = b; v[r | jr] = a; }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int e = r * 32 + lane;
+            const int32_t b = __shfl_xor_sync(0xffffffffu, v[r], j);
+            const bool keep_min = ((e & j) == 0) == ((e & k) == 0);
+            v[r] = keep_min ? min(v[r], b) : max(v[r], b);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = r * 32 + lane;
+      if (e < m) row[e] = v[r];
+    }
+  }
+}
+
+static void sort_rows(mdg_ctx* c, DevList& L, int32_t max_cnt) {
+  static const int enabled = [] {
+    const char* e = getenv("MDG_SORT_ROWS");
+    return e ? atoi(e) : 1;
+  }();
+  // rows longer than 512 slots (the 11-A vdW list) keep the cell-walk order:
+  // measured on config 4, their sort cost more than the Halgren kernel gained
+  if (!enabled || max_cnt < 2 || max_cnt > 512) return;
+  const int64_t rows = c->n_own;
+  const unsigned grid = (unsigned)std::min<int64_t>(148 * 16, (rows + 3) / 4);
+  const int need = (max_cnt + 31) / 32;
+  if (need <= 1)
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<1>, rows, L.nbr, L.cnt, L.cap);
+  else if (need <= 2)
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<2>, rows, L.nbr, L.cnt, L.cap);
+  else if (need <= 4)
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<4>, rows, L.nbr, L.cnt, L.cap);
+  else if (need <= 8)
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<8>, rows, L.nbr, L.cnt, L.cap);
+  else if (need <= 16)
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<16>, rows, L.nbr, L.cnt, L.cap);
 }
 
 static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
@@ -281,7 +377,9 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
                                     ")");
     }
     if (mx <= cap) {
+      sort_rows(c, L, mx);
       L.valid = true;
+      L.version = ++c->epoch;
       L.cutoff = list_cutoff;
       L.sites = sites;
       L.max_cnt = mx;
