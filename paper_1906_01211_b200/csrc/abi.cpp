@@ -3,7 +3,10 @@
 // spatial sort, list import/export in the reference NeighborTable layout,
 // and the fused steps. No kernels here; they live in the .cu files.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -104,10 +107,45 @@ void spatial_sort(mdg_ctx* c, const double* x, const double* y, const double* z)
                                  cudaMemcpyHostToDevice, c->stream));
 }
 
-void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays) {
+// Host-side copies of the per-step vectors (24 B/site each way) run on up to
+// 8 threads: a single-threaded memcpy into pinned memory was most of the
+// end-to-end overhead at 10^6 sites.
+void host_parallel(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t T = std::min<int64_t>(std::min<unsigned>(8, hw), std::max<int64_t>(1, n >> 16));
+  if (T <= 1) {
+    f(0, n);
+    return;
+  }
+  const int64_t chunk = (n + T - 1) / T;
+  std::vector<std::thread> th;
+  for (int64_t t = 1; t < T; ++t) {
+    const int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b < e) th.emplace_back(f, b, e);
+  }
+  f(0, std::min(n, chunk));
+  for (auto& x : th) x.join();
+}
+
+// Copy caller arrays into the pinned stage and upload them. With `box`, the
+// first three arrays are positions and are checked to lie in [0, L) in the
+// same pass (the ParticleSystem contract, proj/src/system.cpp).
+void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double* box = nullptr) {
   const int64_t n = c->n;
-  for (size_t a = 0; a < arrays.size(); ++a)
-    std::memcpy(c->h_stage + a * n, arrays[a], n * sizeof(double));
+  std::atomic<bool> bad{false};
+  host_parallel(n, [&](int64_t b, int64_t e) {
+    for (size_t a = 0; a < arrays.size(); ++a) {
+      const double* src = arrays[a];
+      std::memcpy(c->h_stage + a * n + b, src + b, (e - b) * sizeof(double));
+      if (box && a < 3) {
+        const double L = box[a];
+        bool ok = true;
+        for (int64_t i = b; i < e; ++i) ok &= (src[i] >= 0.0) & (src[i] < L);
+        if (!ok) bad = true;
+      }
+    }
+  });
+  need(!bad, "ParticleSystem: position outside the box");
   MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
                                  cudaMemcpyHostToDevice, c->stream));
 }
@@ -120,9 +158,11 @@ void vec_out(mdg_ctx* c, const double4* v, double* ox, double* oy, double* oz) {
   MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_stage, c->d_stage, 3 * n * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));
   MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  if (ox) std::memcpy(ox, c->h_stage, n * sizeof(double));
-  if (oy) std::memcpy(oy, c->h_stage + n, n * sizeof(double));
-  if (oz) std::memcpy(oz, c->h_stage + 2 * n, n * sizeof(double));
+  double* outs[3] = {ox, oy, oz};
+  host_parallel(n, [&](int64_t b, int64_t e) {
+    for (int a = 0; a < 3; ++a)
+      if (outs[a]) std::memcpy(outs[a] + b, c->h_stage + a * n + b, (e - b) * sizeof(double));
+  });
 }
 
 void vec_in(mdg_ctx* c, const double* ix, const double* iy, const double* iz, double4* v) {
@@ -372,11 +412,7 @@ int mdg_positions_upload(mdg_ctx* c, const double* x, const double* y, const dou
     set_device(c);
     need(x && y && z, "null position array");
     const double L[3] = {c->lx, c->ly, c->lz};
-    const double* p[3] = {x, y, z};
-    for (int a = 0; a < 3; ++a)
-      for (int64_t i = 0; i < c->n; ++i)
-        need(p[a][i] >= 0.0 && p[a][i] < L[a], "ParticleSystem: position outside the box");
-    stage_in(c, {x, y, z});
+    stage_in(c, {x, y, z}, L);
     mdg::pack_positions(c);
   });
 }

@@ -21,6 +21,15 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MDG_LIB", os.path.join(_HERE, "libmdg.so"))
 ROOT = os.path.dirname(_HERE)
 
+def _aos(x, y, z):
+    """(n, 3) view of three SoA component arrays (no copy when they are the
+    rows of one (3, n) block, as Engine._vec3 allocates them)."""
+    b = x.base
+    if b is not None and b.ndim == 2 and b.shape[0] == 3 and y.base is b and z.base is b:
+        return b.T
+    return np.stack([x, y, z], 1)
+
+
 kMaxNeighbors = 2560  # proj/include/mdvec/common.hpp:10
 SITES_ATOMIC, SITES_VDW = 0, 1
 ELECTRIC = 332.063713  # kcal A / (mol e^2)
@@ -413,7 +422,10 @@ class Engine:
 
     # ---- kernels -------------------------------------------------------------------
     def _vec3(self):
-        return np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
+        # three rows of one (3, n) block: _aos() returns its (n, 3) view
+        # without another copy of the data
+        b = np.zeros((3, self.n))
+        return b[0], b[1], b[2]
 
     def lj_forces(self, t: NeighborTable, p: LjParams, exclude: bool = False) -> ForceAccumulator:
         fx, fy, fz = self._vec3()
@@ -489,7 +501,7 @@ class Engine:
         check(self.lib.mdg_mpole_forces(self.ctx, t.list_id, alpha, cutoff, electric,
                                         int(exclude), _p(fx), _p(fy), _p(fz), _p(tx), _p(ty),
                                         _p(tz), C.byref(e), _p(w)))
-        return (np.stack([fx, fy, fz], 1), np.stack([tx, ty, tz], 1), e.value, w.reshape(3, 3))
+        return (_aos(fx, fy, fz), _aos(tx, ty, tz), e.value, w.reshape(3, 3))
 
     # ---- fused steps ----------------------------------------------------------------
     def charmm_step(self, t: NeighborTable, p: CharmmParams):
@@ -501,22 +513,22 @@ class Engine:
     def fetch_forces(self) -> np.ndarray:
         fx, fy, fz = self._vec3()
         check(self.lib.mdg_fetch_forces(self.ctx, _p(fx), _p(fy), _p(fz)))
-        return np.stack([fx, fy, fz], 1)
+        return _aos(fx, fy, fz)
 
     def fetch_torques(self) -> np.ndarray:
         tx, ty, tz = self._vec3()
         check(self.lib.mdg_fetch_torques(self.ctx, _p(tx), _p(ty), _p(tz)))
-        return np.stack([tx, ty, tz], 1)
+        return _aos(tx, ty, tz)
 
     def fetch_dipoles(self) -> np.ndarray:
         mx, my, mz = self._vec3()
         check(self.lib.mdg_fetch_dipoles(self.ctx, _p(mx), _p(my), _p(mz)))
-        return np.stack([mx, my, mz], 1)
+        return _aos(mx, my, mz)
 
     def fetch_perm_field(self) -> np.ndarray:
         ex, ey, ez = self._vec3()
         check(self.lib.mdg_fetch_perm_field(self.ctx, _p(ex), _p(ey), _p(ez)))
-        return np.stack([ex, ey, ez], 1)
+        return _aos(ex, ey, ez)
 
     def fetch_energies(self):
         e = np.zeros(4)
