@@ -222,6 +222,14 @@ int mdg_system_upload_owned(mdg_ctx* ctx, int64_t n, int64_t n_owned, int64_t n_
 typedef int (*mdg_exchange_fn)(void* user, int vec_id);
 typedef int (*mdg_allreduce_fn)(void* user, double* vals, int n);
 int mdg_set_comm(mdg_ctx* ctx, mdg_exchange_fn exchange, mdg_allreduce_fn allreduce, void* user);
+/* Pair-sum mode of the Halgren and multipole kernels. Default (0): each
+ * owned-owned pair is evaluated once (Newton's third law, as the reference's
+ * half lists do) and the partner's force/torque is added with FP64 atomics,
+ * so the last bits of forces can vary run to run. 1: every site sums its
+ * full row in a fixed order (twice the pair arithmetic, bitwise
+ * reproducible). The environment variable MDG_DETERMINISTIC sets the
+ * default of new contexts. Energies and virials are reproducible in both. */
+int mdg_set_deterministic(mdg_ctx* ctx, int on);
 /* Gather 3 doubles per listed caller-order site of vec_id into out[3*count]
  * (x,y,z interleaved) / scatter them back. Host buffers. */
 int mdg_vec_pack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count, double* out);

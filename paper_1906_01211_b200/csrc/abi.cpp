@@ -8,6 +8,7 @@
 #include <functional>
 #include <thread>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -195,6 +196,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
     *out = nullptr;
     try {
       c->device = device;
+      if (const char* d = getenv("MDG_DETERMINISTIC")) c->deterministic = atoi(d) != 0;
       set_device(c);
       c->n_cap = n_capacity;
       c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
@@ -340,6 +342,13 @@ int mdg_set_comm(mdg_ctx* c, mdg_exchange_fn exchange, mdg_allreduce_fn allreduc
     c->comm_exchange = exchange;
     c->comm_allreduce = allreduce;
     c->comm_user = user;
+  });
+}
+
+int mdg_set_deterministic(mdg_ctx* c, int on) {
+  return guard([&] {
+    need_ctx(c);
+    c->deterministic = on != 0;
   });
 }
 
@@ -619,6 +628,7 @@ int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
     MDG_CUDA_CHECK(cudaMemcpy(L.cnt, cnt.data(), n * 4, cudaMemcpyHostToDevice));
     L.cap = cap;
     L.valid = true;
+    L.sorted = true;  // rows std::sort-ed above
     L.version = ++c->epoch;
     L.cutoff = list_cutoff;
     L.sites = sites;

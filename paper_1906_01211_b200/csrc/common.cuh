@@ -112,10 +112,38 @@ struct ListView {
   const int32_t* nbr;
   const int32_t* cnt;
   int32_t cap;
+  bool sorted = false;  // rows ascending in (j & 0x7fffffff)
 };
 
 __device__ __forceinline__ const int32_t* list_row(const ListView& L, int64_t i) {
   return L.nbr + (size_t)i * (size_t)L.cap;
+}
+
+// First slot of a sorted row whose neighbour (flag bit masked) is > i: the
+// half-row kernels walk only that suffix. Two dependent probes: 32 evenly
+// spaced slots, then the <= 31 slots between the bracketing probes. Rows
+// longer than 1024 return 0 (the kernels' prologue still drops j < i).
+__device__ __forceinline__ int row_suffix(const int32_t* __restrict__ row, int cnt, int64_t i,
+                                          int lane) {
+  if (cnt == 0 || cnt > 1024) return 0;
+  const int step = (cnt + 31) >> 5;
+  const int nvalid = (cnt + step - 1) / step;
+  const bool v = lane < nvalid;
+  const bool gt = v && (int64_t)(__ldg(row + lane * step) & 0x7fffffff) > i;
+  const unsigned m = __ballot_sync(0xffffffffu, gt);
+  int lo, hi;
+  if (m == 0) {
+    lo = (nvalid - 1) * step + 1;
+    hi = cnt;
+  } else {
+    const int p = __ffs(m) - 1;
+    if (p == 0) return 0;
+    lo = (p - 1) * step + 1;
+    hi = p * step;
+  }
+  const bool gt2 = (lo + lane < hi) && (int64_t)(__ldg(row + lo + lane) & 0x7fffffff) > i;
+  const unsigned m2 = __ballot_sync(0xffffffffu, gt2);
+  return m2 ? lo + __ffs(m2) - 1 : hi;
 }
 
 // ---- warp-per-site execution ------------------------------------------------

@@ -7,8 +7,8 @@
 //   polp   double2[n]   polarizability, polarizability^(1/6)
 //   mol    int32[n]     exclusion group
 //   mp     double4[3n]  (mux,muy,muz,Qxx) (Qxy,Qxz,Qyy,Qyz) (Qzz,0,0,0)
-//   lists  sliced ELL:  nbr[(g*cap + k)*32 + lane] = j for site i = 32 g + lane,
-//                       cnt[i] neighbours (both directions) within the list cutoff
+//   lists  row-major:   nbr[i*cap + k] = j (cap a multiple of 32), cnt[i]
+//                       neighbours (both directions) within the list cutoff
 //   vectors (forces, fields, dipoles, CG) double4[n], w unused.
 #pragma once
 
@@ -55,6 +55,7 @@ struct DevList {
   int64_t half_pairs = 0;
   int32_t max_cnt = 0;
   int64_t version = 0;          // bumped by every (re)build / import
+  bool sorted = false;          // every row ascending in j
 };
 
 // Pruned list: the pairs of a source list within a kernel cutoff, compacted
@@ -70,6 +71,7 @@ struct PrunedList {
   double2* trr = nullptr;
   size_t elems = 0;
   int64_t directed = 0;
+  bool sorted = false;  // rows ascending in (j & 0x7fffffff) (source sorted)
 };
 
 struct ProfEntry {
@@ -157,6 +159,8 @@ struct mdg_ctx {
   mdg::DevList lists[MDG_MAX_LISTS];
   mdg::PrunedList plist;
   int64_t epoch = 0;  // source of DevList::version
+  // full-row (bitwise reproducible) pair sums instead of half rows + atomics
+  bool deterministic = false;
 
   // last step
   double energies[4] = {0, 0, 0, 0};

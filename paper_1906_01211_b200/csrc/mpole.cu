@@ -44,7 +44,11 @@ __device__ __forceinline__ void qmul(const Quad& Q, double x, double y, double z
 }
 
 // partial slots: 0 energy, 1..9 virial (row-major)
-template <bool EXCL, bool PRUNED>
+// HALF (default): each owned-owned pair once, in the row of its lower sorted
+// index; the partner gets F_j = -F_i and its own torque (the i-side formulas
+// with i <-> j and R -> -R) through FP64 atomics. Halo pairs stay in the
+// owned row at energy/virial weight 1/2. !HALF: full rows, no atomics.
+template <bool EXCL, bool PRUNED, bool HALF>
 __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -93,7 +97,9 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       const double C2 = qi * qjr + qj * qir - dir * djr + 2.0 * (diqj - djqi + qiqj);
       const double C3 = -dir * qjr + qir * djr - 4.0 * qvv;
       const double C4 = qir * qjr;
-      acc[0] += C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4];
+      const bool jside = HALF && j < a.n_i;
+      const double w = (HALF && !jside) ? 0.5 : 1.0;
+      acc[0] += w * (C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4]);
 
       // gradient dU/dR
       double a1x, a1y, a1z, a2x, a2y, a2z, b1x, b1y, b1z, b2x, b2y, b2z;
@@ -123,15 +129,15 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       fx -= gx;
       fy -= gy;
       fz -= gz;
-      acc[1] -= x * gx;
-      acc[2] -= x * gy;
-      acc[3] -= x * gz;
-      acc[4] -= y * gx;
-      acc[5] -= y * gy;
-      acc[6] -= y * gz;
-      acc[7] -= z * gx;
-      acc[8] -= z * gy;
-      acc[9] -= z * gz;
+      acc[1] -= w * (x * gx);
+      acc[2] -= w * (x * gy);
+      acc[3] -= w * (x * gz);
+      acc[4] -= w * (y * gx);
+      acc[5] -= w * (y * gy);
+      acc[6] -= w * (y * gz);
+      acc[7] -= w * (z * gx);
+      acc[8] -= w * (z * gy);
+      acc[9] -= w * (z * gz);
 
       // dipole torque: tau = gmu x di, gmu = dU/d(di)
       const double c1 = G[1] * qj + G[2] * djr + G[3] * qjr;  // coefficient of -R
@@ -163,16 +169,51 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       tx += 2.0 * Mzy;
       ty += 2.0 * Mxz;
       tz += 2.0 * Myx;
+      if (jside) {
+        // partner j: same formulas with (qi, di, Qi) <-> (qj, dj, Qj), R -> -R
+        const double c1j = G[1] * qi - G[2] * dir + G[3] * qir;
+        const double hx = G[1] * dix - 2.0 * G[2] * vix + c1j * x;
+        const double hy = G[1] * diy - 2.0 * G[2] * viy + c1j * y;
+        const double hz = G[1] * diz - 2.0 * G[2] * viz + c1j * z;
+        double ux = hy * djz - hz * djy;
+        double uy = hz * djx - hx * djz;
+        double uz = hx * djy - hy * djx;
+        const double crj = G[2] * qi - G[3] * dir + G[4] * qir;
+        Quad H;
+        H.xx = crj * x * x + G[2] * (2.0 * dix * x) + g2 * Qi.xx - g3 * (2.0 * x * vix);
+        H.yy = crj * y * y + G[2] * (2.0 * diy * y) + g2 * Qi.yy - g3 * (2.0 * y * viy);
+        H.zz = crj * z * z + G[2] * (2.0 * diz * z) + g2 * Qi.zz - g3 * (2.0 * z * viz);
+        H.xy = crj * x * y + G[2] * (dix * y + x * diy) + g2 * Qi.xy - g3 * (x * viy + vix * y);
+        H.xz = crj * x * z + G[2] * (dix * z + x * diz) + g2 * Qi.xz - g3 * (x * viz + vix * z);
+        H.yz = crj * y * z + G[2] * (diy * z + y * diz) + g2 * Qi.yz - g3 * (y * viz + viy * z);
+        const double Nzy = (Qj.xz * H.xy + Qj.yz * H.yy + Qj.zz * H.yz) -
+                           (H.xz * Qj.xy + H.yz * Qj.yy + H.zz * Qj.yz);
+        const double Nxz = (Qj.xx * H.xz + Qj.xy * H.yz + Qj.xz * H.zz) -
+                           (H.xx * Qj.xz + H.xy * Qj.yz + H.xz * Qj.zz);
+        const double Nyx = (Qj.xy * H.xx + Qj.yy * H.xy + Qj.yz * H.xz) -
+                           (H.xy * Qj.xx + H.yy * Qj.xy + H.yz * Qj.xz);
+        ux += 2.0 * Nzy;
+        uy += 2.0 * Nxz;
+        uz += 2.0 * Nyx;
+        atomicAdd(&a.force[j].x, gx);
+        atomicAdd(&a.force[j].y, gy);
+        atomicAdd(&a.force[j].z, gz);
+        atomicAdd(&a.torque[j].x, ux);
+        atomicAdd(&a.torque[j].y, uy);
+        atomicAdd(&a.torque[j].z, uz);
+      }
     };
+    // half rows: a sorted row's pairs with j > i are its suffix
+    const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row, cnt, lane, a.pos, (EXCL && !PRUNED) ? a.mol : nullptr, ring,
+        row + start, cnt - start, lane, a.pos, (EXCL && !PRUNED) ? a.mol : nullptr, ring,
         [&](int32_t& raw, const double4& pj, int32_t mj, double& x, double& y, double& z) {
           const int32_t j = raw & 0x7fffffff;
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
           const bool keep = PRUNED ? !(EXCL && raw < 0)  // same molecule (flag bit)
                                    : (r2 <= a.c2) && !(EXCL && mj == mi);
           raw = j;
-          return keep;
+          return keep && !(HALF && j < i);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
@@ -182,17 +223,42 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
     ty = warp_allsum(ty);
     tz = warp_allsum(tz);
     if (lane == 0) {
-      if (a.accumulate) {
-        const double4 f0 = a.force[i];
-        fx += f0.x;
-        fy += f0.y;
-        fz += f0.z;
+      if (HALF) {  // force / torque were zeroed or hold the accumulated base
+        atomicAdd(&a.force[i].x, fx);
+        atomicAdd(&a.force[i].y, fy);
+        atomicAdd(&a.force[i].z, fz);
+        atomicAdd(&a.torque[i].x, tx);
+        atomicAdd(&a.torque[i].y, ty);
+        atomicAdd(&a.torque[i].z, tz);
+      } else {
+        if (a.accumulate) {
+          const double4 f0 = a.force[i];
+          fx += f0.x;
+          fy += f0.y;
+          fz += f0.z;
+        }
+        a.force[i] = make_double4(fx, fy, fz, 0.0);
+        a.torque[i] = make_double4(tx, ty, tz, 0.0);
       }
-      a.force[i] = make_double4(fx, fy, fz, 0.0);
-      a.torque[i] = make_double4(tx, ty, tz, 0.0);
     }
   }
   block_store_partials<10>(acc, a.partials);
+}
+
+template <bool PRUNED>
+static void launch_mpole(mdg_ctx* c, MKArgs& k, bool ex) {
+  if (c->deterministic) {
+    if (ex) MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, PRUNED, false>));
+    else MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, PRUNED, false>));
+    finalize_partials(c, c->last_grid, 10, 10, 0.5);
+    return;
+  }
+  const size_t bytes = (size_t)k.n_i * sizeof(double4);
+  if (!k.accumulate) MDG_CUDA_CHECK(cudaMemsetAsync(k.force, 0, bytes, c->stream));
+  MDG_CUDA_CHECK(cudaMemsetAsync(k.torque, 0, bytes, c->stream));
+  if (ex) MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, PRUNED, true>));
+  else MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, PRUNED, true>));
+  finalize_partials(c, c->last_grid, 10, 10, 1.0);
 }
 
 void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double electric,
@@ -203,7 +269,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.alpha = alpha;
@@ -211,11 +277,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.force = c->force;
   k.torque = c->torque;
   k.accumulate = accumulate ? 1 : 0;
-  if (exclude && c->has_mol)
-    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, false>));
-  else
-    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, false>));
-  finalize_partials(c, c->last_grid, 10, 10, 0.5);
+  launch_mpole<false>(c, k, exclude && c->has_mol);
 }
 
 void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bool accumulate) {
@@ -225,7 +287,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.pos = c->pos;
   k.mp = c->mp;
   k.mol = c->mol;
-  k.L = ListView{P.nbr, P.cnt, P.cap};
+  k.L = ListView{P.nbr, P.cnt, P.cap, P.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = P.cutoff * P.cutoff;
   k.alpha = alpha;
@@ -233,11 +295,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.force = c->force;
   k.torque = c->torque;
   k.accumulate = accumulate ? 1 : 0;
-  if (exclude && c->has_mol)
-    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<true, true>));
-  else
-    MDG_LAUNCH_SITES(c, "mpole", k.n_i, k, (k_mpole<false, true>));
-  finalize_partials(c, c->last_grid, 10, 10, 0.5);
+  launch_mpole<true>(c, k, exclude && c->has_mol);
 }
 
 }  // namespace mdg

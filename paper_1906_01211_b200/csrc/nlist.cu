@@ -271,14 +271,14 @@ __global__ void __launch_bounds__(kBlock) k_sort_rows(int64_t n, int32_t* __rest
   }
 }
 
-static void sort_rows(mdg_ctx* c, DevList& L, int32_t max_cnt) {
+static bool sort_rows(mdg_ctx* c, DevList& L, int32_t max_cnt) {
   static const int enabled = [] {
     const char* e = getenv("MDG_SORT_ROWS");
     return e ? atoi(e) : 1;
   }();
-  // rows longer than 512 slots (the 11-A vdW list) keep the cell-walk order:
-  // measured on config 4, their sort cost more than the Halgren kernel gained
-  if (!enabled || max_cnt < 2 || max_cnt > 512) return;
+  // sorted rows also let the half-row kernels start at the first j > i
+  if (!enabled || max_cnt > 1024) return false;
+  if (max_cnt < 2) return true;
   const int64_t rows = c->n_own;
   const unsigned grid = (unsigned)std::min<int64_t>(148 * 16, (rows + 3) / 4);
   const int need = (max_cnt + 31) / 32;
@@ -292,6 +292,9 @@ static void sort_rows(mdg_ctx* c, DevList& L, int32_t max_cnt) {
     MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<8>, rows, L.nbr, L.cnt, L.cap);
   else if (need <= 16)
     MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<16>, rows, L.nbr, L.cnt, L.cap);
+  else
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<32>, rows, L.nbr, L.cnt, L.cap);
+  return true;
 }
 
 static void ensure_list_storage(mdg_ctx* c, DevList& L, int32_t cap) {
@@ -377,7 +380,7 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
                                     ")");
     }
     if (mx <= cap) {
-      sort_rows(c, L, mx);
+      L.sorted = sort_rows(c, L, mx);
       L.valid = true;
       L.version = ++c->epoch;
       L.cutoff = list_cutoff;

@@ -1,11 +1,14 @@
 // nonpolar.cu -- Lennard-Jones, real-space Ewald charge and Halgren 14-7.
 //
-// Warp per i site over its full (both-direction) row (common.cuh): the
-// prologue (minimum image, cutoff, exclusion) runs on every list slot, the
-// in-range pairs are ballot-compacted so the pair body runs on full warps,
-// the i-side force is a warp reduction written once -- no j-side scatter, no
-// atomics, deterministic sums. Energies and virials are counted twice over
-// the full list and halved in the fixed-order finalize.
+// Warp per i site over its (both-direction) row (common.cuh): the prologue
+// (minimum image, cutoff, exclusion) runs on every list slot, the in-range
+// pairs are ballot-compacted so the pair body runs on full warps, the i-side
+// force is a warp reduction. Default (HALF): an owned-owned pair is evaluated
+// once, in the row of its lower sorted index, and the partner's force is
+// added with an FP64 atomic (Newton's third law, as the reference's half
+// lists). Deterministic mode (!HALF): every row is summed in full, no
+// atomics, each pair counted twice and the energies/virials halved in the
+// fixed-order finalize.
 // Pair arithmetic follows the reference: proj/include/mdvec/kernels.hpp:42-64
 // (LJ, Ewald) and proj/src/polar_vec.cpp:74-116 (Halgren one-division form).
 #include "common.cuh"
@@ -26,7 +29,7 @@ struct NonpolarKArgs {
 };
 
 // partial slots: 0 E_lj, 1 E_coul, 2..7 virial (xx xy xz yy yz zz)
-template <bool LJ, bool COUL, bool SHIFT, bool EXCL>
+template <bool LJ, bool COUL, bool SHIFT, bool EXCL, bool HALF>
 __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -47,6 +50,8 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       const double r2 = dist2(dx, dy, dz);
       const double4 pj = ldg4(a.pos + j);
       double fs = 0.0;
+      // pair weight: 1/2 for a halo partner (the other domain has the mirror)
+      const double w = (HALF && j >= a.n_i) ? 0.5 : 1.0;
       if (LJ) {
         const double4 vj = ldg4(a.vdwp + j);
         const double sij = 0.5 * (vi.x + vj.x);
@@ -61,7 +66,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
           const double sc6 = sc2 * sc2 * sc2;
           u -= 4.0 * eij * (sc6 * sc6 - sc6);
         }
-        acc[0] += u;
+        acc[0] += w * u;
         fs += 24.0 * eij * (2.0 * s12 - s6) * inv_r2;
       }
       if (COUL) {
@@ -70,43 +75,59 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
         const double qq = a.electric * pi.w * pj.w;
         const double ee = erfc(a.alpha * r) * inv_r;
         const double g = a.alpha * two_over_sqrt_pi * exp(-a.alpha * a.alpha * r2);
-        acc[1] += qq * ee;
+        acc[1] += w * (qq * ee);
         fs += qq * (ee + g) * inv_r * inv_r;
       }
       const double px = fs * dx, py = fs * dy, pz = fs * dz;
       fx += px;
       fy += py;
       fz += pz;
-      acc[2] += dx * px;
-      acc[3] += dx * py;
-      acc[4] += dx * pz;
-      acc[5] += dy * py;
-      acc[6] += dy * pz;
-      acc[7] += dz * pz;
+      if (HALF && j < a.n_i) {
+        atomicAdd(&a.force[j].x, -px);
+        atomicAdd(&a.force[j].y, -py);
+        atomicAdd(&a.force[j].z, -pz);
+      }
+      acc[2] += w * (dx * px);
+      acc[3] += w * (dx * py);
+      acc[4] += w * (dx * pz);
+      acc[5] += w * (dy * py);
+      acc[6] += w * (dy * pz);
+      acc[7] += w * (dz * pz);
     };
+    // half rows: a sorted row's pairs with j > i are its suffix
+    const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row, cnt, lane, a.pos, EXCL ? a.mol : nullptr, ring,
+        row + start, cnt - start, lane, a.pos, EXCL ? a.mol : nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && mj == mi);
+          return (r2 <= a.c2) && !(EXCL && mj == mi) && !(HALF && j < i);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
     fy = warp_allsum(fy);
     fz = warp_allsum(fz);
-    if (lane == 0) a.force[i] = make_double4(fx, fy, fz, 0.0);
+    if (lane == 0) {
+      if (HALF) {
+        atomicAdd(&a.force[i].x, fx);
+        atomicAdd(&a.force[i].y, fy);
+        atomicAdd(&a.force[i].z, fz);
+      } else {
+        a.force[i] = make_double4(fx, fy, fz, 0.0);
+      }
+    }
   }
   block_store_partials<8>(acc, a.partials);
 }
 
 template <bool LJ, bool COUL>
-static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
+static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl, bool half,
                       const char* name) {
   NonpolarKArgs kk = k;
-#define NP_CASE(S, E)                                                            \
-  if (shift == S && excl == E) {                                               \
-    MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E>));        \
-    return;                                                                    \
+#define NP_CASE(S, E)                                                              \
+  if (shift == S && excl == E) {                                                 \
+    if (half) MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, true>));  \
+    else MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, false>));      \
+    return;                                                                      \
   }
   NP_CASE(false, false)
   NP_CASE(false, true)
@@ -122,7 +143,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = a.cutoff * a.cutoff;
   k.alpha = a.alpha;
@@ -131,10 +152,12 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   if (L.sites == MDG_SITES_VDW && a.do_coul)
     throw_error(MDG_CONTRACT, "coulomb terms need a list over atomic sites");
   const bool shift = a.shift != 0, excl = a.exclude != 0 && c->has_mol;
-  if (a.do_lj && a.do_coul) launch_np<true, true>(c, k, shift, excl, "lj_ewald");
-  else if (a.do_lj) launch_np<true, false>(c, k, shift, excl, "lj");
-  else launch_np<false, true>(c, k, shift, excl, "ewald_real");
-  finalize_partials(c, c->last_grid, 8, 0, 0.5);
+  const bool half = !c->deterministic;
+  if (half) MDG_CUDA_CHECK(cudaMemsetAsync(k.force, 0, (size_t)k.n_i * sizeof(double4), c->stream));
+  if (a.do_lj && a.do_coul) launch_np<true, true>(c, k, shift, excl, half, "lj_ewald");
+  else if (a.do_lj) launch_np<true, false>(c, k, shift, excl, half, "lj");
+  else launch_np<false, true>(c, k, shift, excl, half, "ewald_real");
+  finalize_partials(c, c->last_grid, 8, 0, half ? 1.0 : 0.5);
 }
 
 // ---- Halgren buffered 14-7 -------------------------------------------------
@@ -151,7 +174,12 @@ struct HalgrenKArgs {
   double* __restrict__ partials;
 };
 
-template <bool EXCL>
+// HALF: each owned-owned pair once (in the row of its lower sorted index)
+// with the partner's force added atomically; pairs with a halo partner stay
+// in the owned row only (their mirror is the other domain's). Energy and
+// virial are weighted 1 (owned pair) or 1/2 (halo pair), finalize scale 1.
+// !HALF: full rows, each pair in both rows at weight 1/2 (finalize scale).
+template <bool EXCL, bool HALF>
 __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -197,29 +225,49 @@ __global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
       const double u = eij * t7 * bb;
       const double dudrho = -7.0 * eij * t7 * (bb * r0 * inv_e1 + r6 * r0 * g1 * inv_e2);
       const double fs = -dudrho * inv_r0r;
-      acc[0] += u;
       const double px = fs * dx, py = fs * dy, pz = fs * dz;
       fx += px;
       fy += py;
       fz += pz;
-      acc[2] += dx * px;
-      acc[3] += dx * py;
-      acc[4] += dx * pz;
-      acc[5] += dy * py;
-      acc[6] += dy * pz;
-      acc[7] += dz * pz;
+      double w = 1.0;
+      if (HALF) {
+        if (j < a.n_i) {
+          atomicAdd(&a.force[j].x, -px);
+          atomicAdd(&a.force[j].y, -py);
+          atomicAdd(&a.force[j].z, -pz);
+        } else {
+          w = 0.5;
+        }
+      }
+      acc[0] += w * u;
+      acc[2] += w * (dx * px);
+      acc[3] += w * (dx * py);
+      acc[4] += w * (dx * pz);
+      acc[5] += w * (dy * py);
+      acc[6] += w * (dy * pz);
+      acc[7] += w * (dz * pz);
     };
+    // half rows: a sorted row's pairs with j > i are its suffix
+    const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row, cnt, lane, a.site, EXCL ? a.mol : nullptr, ring,
+        row + start, cnt - start, lane, a.site, EXCL ? a.mol : nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && mj == mi);
+          return (r2 <= a.c2) && !(EXCL && mj == mi) && !(HALF && j < i);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
     fy = warp_allsum(fy);
     fz = warp_allsum(fz);
-    if (lane == 0) a.force[i] = make_double4(fx, fy, fz, 0.0);
+    if (lane == 0) {
+      if (HALF) {
+        atomicAdd(&a.force[i].x, fx);
+        atomicAdd(&a.force[i].y, fy);
+        atomicAdd(&a.force[i].z, fz);
+      } else {
+        a.force[i] = make_double4(fx, fy, fz, 0.0);
+      }
+    }
   }
   block_store_partials<8>(acc, a.partials);
 }
@@ -260,17 +308,23 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.site = reduced ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.delta = delta;
   k.gamma = gamma;
   k.force = reduced ? c->force2 : c->force;
-  if (exclude && c->has_mol)
-    MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, k_halgren<true>);
-  else
-    MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, k_halgren<false>);
-  finalize_partials(c, c->last_grid, 8, 0, 0.5);
+  const bool ex = exclude && c->has_mol;
+  if (c->deterministic) {
+    if (ex) MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<true, false>));
+    else MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<false, false>));
+    finalize_partials(c, c->last_grid, 8, 0, 0.5);
+  } else {
+    MDG_CUDA_CHECK(cudaMemsetAsync(k.force, 0, (size_t)k.n_i * sizeof(double4), c->stream));
+    if (ex) MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<true, true>));
+    else MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<false, true>));
+    finalize_partials(c, c->last_grid, 8, 0, 1.0);
+  }
   if (reduced) {
     MDG_LAUNCH(c, "chain_rule", grid_for(c->n_own, 256), 256, 0, k_chain_rule, c->n_own, c->force2,
                c->hpar, c->hfac, c->child_start, c->child, c->force);

@@ -126,6 +126,7 @@ SIGNATURES = {
     "mdg_system_upload_owned": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                           C.c_double, C.c_double, C.c_double] + [_dp] * 9),
     "mdg_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mdg_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_unpack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_pack_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
@@ -559,6 +560,11 @@ class Engine:
         ms = C.c_double()
         check(self.lib.mdg_timer_stop(self.ctx, C.byref(ms)))
         return ms.value
+
+    def set_deterministic(self, on: bool = True):
+        """Full-row pair sums (bitwise reproducible forces/torques) instead of
+        the default half rows with atomic partner updates (mdg.h)."""
+        check(self.lib.mdg_set_deterministic(self.ctx, int(on)))
 
     def launch_count(self) -> int:
         return int(self.lib.mdg_launch_count(self.ctx))

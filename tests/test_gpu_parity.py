@@ -386,7 +386,42 @@ def test_amoeba_step_composes(engine, oracle, mdg):
     fm, _, em, wm = engine.mpole_forces(te, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
     st = engine.polar_solve_pcg(te, mdg.PolarParams(7.0, 0.39), 0.5446, 1e-5, 100, True)
     assert e[0] == hv.energy and e[1] == em
-    assert np.array_equal(f, hv.forces + fm)
+    # partner forces arrive through atomics (default half-row mode): the sum
+    # order, not the terms, can differ between the fused step and its parts
+    np.testing.assert_allclose(f, hv.forces + fm, rtol=0, atol=1e-12 * np.abs(f).max())
     assert iters == st.iterations and rms < 1e-5
     assert np.array_equal(mu, st.mu)
     np.testing.assert_allclose(w, hv.virial + wm, rtol=1e-12, atol=1e-12)
+
+
+def test_half_rows_match_deterministic_full_rows(engine, mdg):
+    """Default mode (each owned pair once, partner force/torque by atomics)
+    against the deterministic full-row mode, and the latter bitwise
+    reproducible run to run."""
+    s = amoeba_small(mdg, 343, 21.0, 7)
+    engine.upload_system(s)
+    tv = engine.build_neighbor_table(10.0, list_id=1, sites=mdg.SITES_VDW)
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1)
+    out = {}
+    for mode in (False, True, True):
+        engine.set_deterministic(mode)
+        engine.amoeba_step(tv, te, p)
+        e, w, it, _ = engine.fetch_energies()
+        f = engine.fetch_forces()
+        _, tq, _, _ = engine.mpole_forces(te, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+        cp = mdg.CharmmParams(9.0, 0.35, mdg.ELECTRIC, 0, 1)
+        engine.charmm_step(te, cp)
+        fc = engine.fetch_forces()
+        ec = engine.fetch_energies()[0]
+        out.setdefault(mode, []).append((e, w, f, tq, fc, ec))
+    engine.set_deterministic(False)
+    (e0, w0, f0, t0, fc0, ec0), = out[False]
+    (e1, w1, f1, t1, fc1, ec1), (e2, w2, f2, t2, fc2, ec2) = out[True]
+    for a, b in ((f1, f2), (t1, t2), (fc1, fc2), (e1, e2), (w1, w2), (ec1, ec2)):
+        assert np.array_equal(a, b)
+    np.testing.assert_allclose(e0, e1, rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(ec0, ec1, rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(w0, w1, rtol=0, atol=1e-11 * np.abs(w1).max())
+    for a, b in ((f0, f1), (t0, t1), (fc0, fc1)):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-12 * np.abs(b).max())
