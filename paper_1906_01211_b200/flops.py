@@ -4,9 +4,10 @@ FP64-bound kernels: FLOPs per in-cutoff HALF pair. Weights: add/sub/mul = 1,
 fma = 2; special functions at their sm_100a libdevice fast-path cost: div 15,
 sqrt 13, exp 31, erfc 112; FRND/DSETP are not flops. Prologue P (3 sub +
 3 wrap1 + dist2) = 20. These are the reference formulation's counts (one
-evaluation per pair, both sides updated); the device kernels evaluate each
-pair once per direction, so the algorithmic rate they achieve is at most half
-of their executed rate.
+evaluation per pair, both sides updated). The default device kernels do the
+same (half rows, partner update by atomics); field_tpre and the deterministic
+mode evaluate each pair once per direction, so there the algorithmic rate is
+at most half of the executed rate.
 
 HBM-bound kernels: algorithmic DRAM bytes per launch (streamed list slots
 plus per-site vectors; gathers of neighbour data are cache traffic).
