@@ -177,6 +177,16 @@ def hbm_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def ncu_traffic(name):
+    """DRAM bytes per launch of `name` from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)["kernels"].get(name)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
     work = wl.algorithmic_work(name)
     if work is None:
@@ -192,7 +202,7 @@ def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
         unit = "GB/s"
     return {"bound": "fp64" if kind == "fp64" else "hbm", "kernel": name,
             "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
             "avg_launch_ms": round(avg_ms, 4), "peak_source": src,
             ("flops_per_launch" if kind == "fp64" else "bytes_per_launch"): amount,
             "share_of_step": round(tot_ms / step_ms, 4)}
