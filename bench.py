@@ -187,6 +187,15 @@ def ncu_traffic(name):
         return None
 
 
+def ncu_executed(name):
+    """ncu-measured executed FP64 rate of `name` (profiles/ncu_fp64_executed.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fp64_executed.json")) as f:
+            return json.load(f)["kernels"].get(name)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
     work = wl.algorithmic_work(name)
     if work is None:
@@ -205,7 +214,8 @@ def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
             "avg_launch_ms": round(avg_ms, 4), "peak_source": src,
             ("flops_per_launch" if kind == "fp64" else "bytes_per_launch"): amount,
-            "share_of_step": round(tot_ms / step_ms, 4)}
+            "share_of_step": round(tot_ms / step_ms, 4),
+            "ncu_executed_fp64": ncu_executed(name)}
 
 
 def run_mine(args, world, rank, local):
@@ -256,7 +266,8 @@ def run_mine(args, world, rank, local):
             roof = r
         else:
             others[name] = {k: r[k] for k in ("bound", "achieved", "unit", "frac",
-                                              "avg_launch_ms", "share_of_step")}
+                                              "avg_launch_ms", "share_of_step",
+                                              "ncu_executed_fp64")}
 
     # ---- end to end through the C ABI with host buffers
     e2e = None
