@@ -156,6 +156,19 @@ int mdg_mpole_forces(mdg_ctx* ctx, int list_id, double alpha, double cutoff, dou
                      int exclude, double* fx, double* fy, double* fz, double* tx, double* ty,
                      double* tz, double* energy, double* virial9);
 
+/* ---- polarization forces (epolar1 analogue) -------------- */
+/* Forces, torques on the permanent multipoles and pair virial of the
+ * polarization energy at fixed induced dipoles mu (caller order, e*A; NULL =
+ * the context's dipoles from its last solve): F = -dE/dr of
+ * E = 1/2 mu.a^-1.mu - 1/2 mu.T.mu - mu.E_perm with the same Ewald + Thole
+ * T and field as mdg_polar_solve_pcg / mdg_perm_field (exact forces at the
+ * converged solution). pair_energy = the mu-dependent pair part of E
+ * (E = pair_energy + 1/2 sum mu^2/alpha). */
+int mdg_polar_forces(mdg_ctx* ctx, int list_id, double alpha, double cutoff, double thole_a,
+                     double electric, int exclude, const double* mux, const double* muy,
+                     const double* muz, double* fx, double* fy, double* fz, double* tx,
+                     double* ty, double* tz, double* pair_energy, double* virial9);
+
 /* ---- fused steps (device-resident; the bench's hot path) ----------------- */
 typedef struct {
   double cutoff;    /* LJ and Ewald cutoff (A) */
@@ -175,12 +188,15 @@ typedef struct {
   double thole_a, tol_debye;
   int64_t max_iter;
   int exclude;                              /* 1-2/1-3 (intramolecular) scale 0 */
-  int terms;                                /* bit 0 vdW, 1 multipoles, 2 polarization */
+  int terms;                                /* MDG_TERM_* bits (0 = VDW|MPOLE|POLAR) */
 } mdg_amoeba_params;
 
 #define MDG_TERM_VDW 1
 #define MDG_TERM_MPOLE 2
 #define MDG_TERM_POLAR 4
+/* with POLAR: add the polarization forces/torques/virial at the converged
+ * dipoles (8(f)#1) to the step's results */
+#define MDG_TERM_POLAR_FORCE 8
 
 /* Config-1..4 step: Halgren vdW (list vdw_list, reduced sites) + permanent
  * multipoles + permanent field + PCG induced dipoles (list elec_list).

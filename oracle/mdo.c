@@ -1153,6 +1153,100 @@ int mdo_mpole_field_tensor(const mdo_system* s, const mdo_table* t, double alpha
   return MDO_OK;
 }
 
+/* Thole lambda9 (EXTENSION): with lambda3..9 the damped radial functions
+ * G_n = B_n - (1 - lambda_{2n+1}) g_n obey dG_n/dR = -R G_{n+1} like the
+ * undamped ones, so the generic tensors apply to the damped interaction. */
+static double thole_l9(double r, double ai, double aj, double a) {
+  const double u = r / cbrt(sqrt(ai * aj));
+  const double s1 = a * u * u * u;
+  return 1.0 - (1.0 + s1 + (18.0 / 35.0) * s1 * s1 + (9.0 / 35.0) * s1 * s1 * s1) * exp(-s1);
+}
+
+int mdo_polar_forces(const mdo_system* s, const mdo_table* t, double alpha, double cutoff,
+                     double thole_a, double electric, int exclude, const double* mu,
+                     double* f, double* torque, double* energy, double* virial) {
+  int rc = validate_kernel(s, t, cutoff);
+  if (rc) return rc;
+  const size_t n = s->n;
+  memset(f, 0, 3 * n * sizeof(double));
+  memset(torque, 0, 3 * n * sizeof(double));
+  double w[9] = {0};
+  double etot = 0.0;
+  const double c2 = cutoff * cutoff;
+  box_t b = make_box(s->lx, s->ly, s->lz);
+  tens_t T, Tm;
+  static const double Z[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double Zq[3][3];
+  memcpy(Zq, Z, sizeof Zq);
+  for (size_t i = 0; i < n; ++i) {
+    const int32_t* idx = t->indices + t->offset[i];
+    for (uint32_t k = 0; k < t->nnvlst[i]; ++k) {
+      const size_t j = (size_t)idx[k];
+      double d[3];
+      const double r2 = pair_d(s, &b, i, j, &d[0], &d[1], &d[2]);
+      if (!(r2 <= c2)) continue;
+      if (!(r2 > 0)) return fail(MDO_SINGULARITY, "polar_forces: coincident sites");
+      const int excl = excluded(s, exclude, i, j);
+      const double r = sqrt(r2);
+      double bn[5], g[5], l3, l5, l7;
+      mdo_ewald_bn(r, alpha, 4, bn);
+      bare_bn(r, 4, g);
+      thole_core(r, s->polarizability[i], s->polarizability[j], thole_a, &l3, &l5, &l7);
+      const double l9 = thole_l9(r, s->polarizability[i], s->polarizability[j], thole_a);
+      double G[6];
+      G[0] = 0.0; /* no charge-charge term */
+      G[1] = bn[1] - (1.0 - l3) * g[1];
+      G[2] = bn[2] - (1.0 - l5) * g[2];
+      G[3] = bn[3] - (1.0 - l7) * g[3];
+      G[4] = bn[4] - (1.0 - l9) * g[4];
+      G[5] = 0.0; /* rank-5 tensors only meet zero quadrupole products */
+      build_tensors(d, G, &T);
+      double Qi[3][3], Qj[3][3];
+      quad3(s->quadrupole ? s->quadrupole + 6 * i : zero6, Qi);
+      quad3(s->quadrupole ? s->quadrupole + 6 * j : zero6, Qj);
+      const double* di = s->dipole ? s->dipole + 3 * i : zero3v;
+      const double* dj = s->dipole ? s->dipole + 3 * j : zero3v;
+      const double* ui = mu + 3 * i;
+      const double* uj = mu + 3 * j;
+      const double qi = excl ? 0.0 : s->charge[i], qj = excl ? 0.0 : s->charge[j];
+      /* U = -mu_i.T_ij.mu_j (all pairs) - mu_i.E_{j->i} - mu_j.E_{i->j}
+       * (d-scale: not for same-molecule pairs), all in the tensor form */
+      double u = pair_energy_tensor(0.0, ui, Zq, 0.0, uj, Zq, &T, 0, 0);
+      if (!excl) {
+        u += pair_energy_tensor(0.0, ui, Zq, qj, dj, Qj, &T, 0, 0);
+        u += pair_energy_tensor(qi, di, Qi, 0.0, uj, Zq, &T, 0, 0);
+      }
+      etot += electric * u;
+      double fi[3];
+      for (int e = 0; e < 3; ++e) {
+        double du = pair_energy_tensor(0.0, ui, Zq, 0.0, uj, Zq, &T, 1, e);
+        if (!excl) {
+          du += pair_energy_tensor(0.0, ui, Zq, qj, dj, Qj, &T, 1, e);
+          du += pair_energy_tensor(qi, di, Qi, 0.0, uj, Zq, &T, 1, e);
+        }
+        fi[e] = -electric * du;
+        f[3 * i + e] += fi[e];
+        f[3 * j + e] -= fi[e];
+      }
+      add_virial(w, d[0], d[1], d[2], fi[0], fi[1], fi[2]);
+      if (excl) continue;
+      /* torques on the permanent multipoles in the induced field */
+      double gmu[3], gQ[3][3], tau[3];
+      pair_grad_i(0.0, uj, Zq, &T, gmu, gQ);
+      torque_from_grads(di, Qi, gmu, gQ, tau);
+      for (int a = 0; a < 3; ++a) torque[3 * i + a] += electric * tau[a];
+      double dm[3] = {-d[0], -d[1], -d[2]};
+      build_tensors(dm, G, &Tm);
+      pair_grad_i(0.0, ui, Zq, &Tm, gmu, gQ);
+      torque_from_grads(dj, Qj, gmu, gQ, tau);
+      for (int a = 0; a < 3; ++a) torque[3 * j + a] += electric * tau[a];
+    }
+  }
+  if (energy) *energy = etot;
+  if (virial) memcpy(virial, w, sizeof w);
+  return MDO_OK;
+}
+
 int mdo_pcg(const mdo_system* s, const mdo_table* t, double alpha, double cutoff,
             double thole_a, const double* eperm, double tol_debye, size_t max_iter,
             double* mu, size_t* iters, double* last_rms) {

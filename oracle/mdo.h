@@ -139,6 +139,21 @@ int mdo_mpole(const mdo_system* s, const mdo_table* t, double alpha, double cuto
 int mdo_mpole_field_tensor(const mdo_system* s, const mdo_table* t, double alpha,
                            double cutoff, int exclude, double* e /*3n*/);
 
+/* Polarization forces at fixed induced dipoles mu (EXTENSION, SURVEY 8(f)#1,
+ * the epolar1 analogue). With the variational energy
+ *   E(mu) = 1/2 mu.alpha^-1.mu - 1/2 mu.T.mu - mu.E_perm
+ * (stationary at the PCG solution, where E = -1/2 mu.E_perm), the force is
+ * -dE/dr at fixed mu: pair energy U_ij = -mu_i.T_ij.mu_j - mu_i.E_{j->i}
+ * - mu_j.E_{i->j} with the Ewald + Thole damped radial functions of T and
+ * the permanent field (the field terms skipped for same-molecule pairs when
+ * exclude != 0), differentiated through the generic Cartesian tensors.
+ * energy = electric * sum U_ij (the mu-dependent part, add
+ * 1/2 mu.alpha^-1.mu for E); torque = torques on the permanent multipoles
+ * from the induced dipoles' field. */
+int mdo_polar_forces(const mdo_system* s, const mdo_table* t, double alpha, double cutoff,
+                     double thole_a, double electric, int exclude, const double* mu /*3n*/,
+                     double* f /*3n*/, double* torque /*3n*/, double* energy, double* virial);
+
 /* Diagonal-preconditioned CG for (alpha^-1 - T) mu = E_perm with
  * mdo_tmatvec_ewald as T. mu0 = alpha E. Converged when
  * sqrt(sum |dmu|^2 / n) * debye < tol_debye. */

@@ -369,6 +369,21 @@ class Oracle:
                                        _ptr(w)))
         return f, tq, e.value, w.reshape(3, 3)
 
+    def polar_forces(self, s, t, alpha, cutoff, thole_a, mu, electric=1.0, exclude=True):
+        """Polarization forces/torques/pair energy/virial at fixed dipoles mu
+        (mdo.h mdo_polar_forces; the epolar1 analogue, SURVEY 8(f)#1)."""
+        st, tt = s.as_struct(), t.as_struct()
+        mu = np.ascontiguousarray(mu, np.float64)
+        f = np.zeros((s.n, 3))
+        tq = np.zeros((s.n, 3))
+        e = C.c_double()
+        w = np.zeros(9)
+        self._check(self.lib.mdo_polar_forces(C.byref(st), C.byref(tt), C.c_double(alpha),
+                                              C.c_double(cutoff), C.c_double(thole_a),
+                                              C.c_double(electric), C.c_int(int(exclude)),
+                                              _ptr(mu), _ptr(f), _ptr(tq), C.byref(e), _ptr(w)))
+        return f, tq, e.value, w.reshape(3, 3)
+
     def pcg(self, s, t, alpha, cutoff, thole_a, eperm, tol_debye=1e-5, max_iter=100):
         st, tt = s.as_struct(), t.as_struct()
         eperm = np.ascontiguousarray(eperm, np.float64)

@@ -5,6 +5,6 @@ from .mdvec import (  # noqa: F401
     CONFIGS, DEBYE, ELECTRIC, SITES_ATOMIC, SITES_VDW, AmoebaParams, CapacityError,
     CharmmParams, ContractViolation, ConvergenceError, CudaError, Engine, EwaldRealParams,
     FieldArrays, ForceAccumulator, HalgrenParams, LjParams, NeighborTable, ParticleSystem,
-    PolarizationState, PolarParams, SingularityError, TERM_MPOLE, TERM_POLAR, TERM_VDW,
+    PolarizationState, PolarParams, SingularityError, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE, TERM_VDW,
     fp64_peak_tflops, load_library, reduce_sites_host,
     water_box)

@@ -222,9 +222,9 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       for (double4** v : {&c->force, &c->force2, &c->torque, &c->field, &c->eperm, &c->mu,
                           &c->cg_r, &c->cg_z, &c->cg_p, &c->cg_q, &c->vin, &c->pq4})
         dalloc(v, n);
-      dalloc(&c->results, 64);
-      MDG_CUDA_CHECK(cudaMemset(c->results, 0, 64 * sizeof(double)));
-      MDG_CUDA_CHECK(cudaMallocHost(&c->h_results, 64 * sizeof(double)));
+      dalloc(&c->results, mdg::kResultSlots);
+      MDG_CUDA_CHECK(cudaMemset(c->results, 0, mdg::kResultSlots * sizeof(double)));
+      MDG_CUDA_CHECK(cudaMallocHost(&c->h_results, mdg::kResultSlots * sizeof(double)));
       c->stage_bytes = 12 * n * sizeof(double);
       MDG_CUDA_CHECK(cudaMallocHost(&c->h_stage, c->stage_bytes));
       dalloc(&c->d_stage, 12 * n);
@@ -789,6 +789,29 @@ int mdg_mpole_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   });
 }
 
+int mdg_polar_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                     double electric, int exclude, const double* mux, const double* muy,
+                     const double* muz, double* fx, double* fy, double* fz, double* tx,
+                     double* ty, double* tz, double* pair_energy, double* virial9) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::DevList& L = need_list(c, list_id);
+    need_kernel_cutoff(L, cutoff);
+    need(alpha >= 0, "polar_forces: alpha must be nonnegative");
+    need(L.sites == MDG_SITES_ATOMIC, "polar_forces needs a list over atomic sites");
+    need((mux == nullptr) == (muy == nullptr) && (mux == nullptr) == (muz == nullptr),
+         "polar_forces: give all three dipole components or none");
+    if (mux) vec_in(c, mux, muy, muz, c->mu);
+    mdg::run_polar_force(c, list_id, alpha, cutoff, thole_a, electric, exclude, false);
+    vec_out(c, c->force, fx, fy, fz);
+    vec_out(c, c->torque, tx, ty, tz);
+    mdg::fetch_results(c);
+    if (pair_energy) *pair_energy = c->h_results[70];
+    if (virial9) std::memcpy(virial9, c->h_results + 71, 9 * sizeof(double));
+  });
+}
+
 // ---- fused steps ---------------------------------------------------------------
 
 int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
@@ -814,7 +837,10 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
     need_kernel_cutoff(Le, p->elec_cutoff);
     need(Le.sites == MDG_SITES_ATOMIC, "electrostatics need a list over atomic sites");
     const int terms = p->terms ? p->terms : (MDG_TERM_VDW | MDG_TERM_MPOLE | MDG_TERM_POLAR);
-    MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 48 * sizeof(double), c->stream));
+    need(!(terms & MDG_TERM_POLAR_FORCE) || (terms & MDG_TERM_POLAR),
+         "amoeba_step: polarization forces need the polarization solve");
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
+    c->has_polar_force = false;
     if (terms & MDG_TERM_VDW) {
       mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
     } else {
@@ -838,6 +864,12 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
       c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
       c->pcg_rms = rms;
       mdg::polar_energy(c, p->electric, 40);
+      if (terms & MDG_TERM_POLAR_FORCE) {
+        // the PCG leaves the halo dipoles at mu0: refresh them first
+        mdg::exchange_halo(c, MDG_VEC_MU);
+        mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
+        c->has_polar_force = true;
+      }
     }
   });
 }
@@ -911,7 +943,8 @@ int mdg_fetch_energies(mdg_ctx* c, double* energies4, double* virial9, int64_t* 
       energies4[3] = 0.0;
     }
     if (virial9) {
-      for (int k = 0; k < 9; ++k) virial9[k] = w[k] + (amoeba ? r[11 + k] : 0.0);
+      for (int k = 0; k < 9; ++k)
+        virial9[k] = w[k] + (amoeba ? r[11 + k] : 0.0) + (c->has_polar_force ? r[71 + k] : 0.0);
     }
     if (pcg_iters) *pcg_iters = c->pcg_iters > 0 ? c->pcg_iters : 0;
     if (pcg_rms) *pcg_rms = c->pcg_rms;

@@ -125,7 +125,7 @@ void finalize_partials(mdg_ctx* c, int64_t blocks, int nvals, int slot, double s
 }
 
 void fetch_results(mdg_ctx* c) {
-  MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_results, c->results, 64 * sizeof(double),
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_results, c->results, kResultSlots * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));
   MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }

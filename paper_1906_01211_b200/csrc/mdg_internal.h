@@ -28,6 +28,10 @@ namespace mdg {
 #endif
 constexpr int kBlock = MDG_BLOCK;  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
+// device result slots: 0-9 nonpolar, 10-19 multipoles, 20-27 PCG, 30 Jacobi,
+// 40 polarization energy, 50-51 count_within, 60-63 list stats,
+// 70-79 polarization forces (pair energy, virial)
+constexpr int kResultSlots = 96;
 constexpr int kMaxBlocksRed = 1 << 20;
 
 struct Box {
@@ -161,6 +165,7 @@ struct mdg_ctx {
   int64_t epoch = 0;  // source of DevList::version
   // full-row (bitwise reproducible) pair sums instead of half rows + atomics
   bool deterministic = false;
+  bool has_polar_force = false;  // last AMOEBA step added polarization forces
 
   // last step
   double energies[4] = {0, 0, 0, 0};
@@ -269,6 +274,14 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
 // PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
 void run_reduce_sites(mdg_ctx* c);
+// polarization forces at c->mu (polforce.cu); results slots 70 (pair
+// energy), 71..79 (virial); accumulate adds to c->force / c->torque
+void run_polar_force(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
+                     double electric, int exclude, bool accumulate);
+void run_polar_force_pruned(mdg_ctx* c, double alpha, double thole_a, double electric,
+                            int exclude, bool accumulate);
+// multi-domain: refresh the halo entries of vec_id through the comm hook
+void exchange_halo(mdg_ctx* c, int vec_id);
 
 
 // permutation helpers (device kernels)

@@ -545,6 +545,10 @@ static void dd_exchange(mdg_ctx* c, int vec_id) {
     throw_error(MDG_COMM, "halo exchange callback failed");
 }
 
+void exchange_halo(mdg_ctx* c, int vec_id) {
+  if (c->comm_exchange) dd_exchange(c, vec_id);
+}
+
 static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
   if (c->comm_allreduce(c->comm_user, v, nv) != 0)
     throw_error(MDG_COMM, "all-reduce callback failed");

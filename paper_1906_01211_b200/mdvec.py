@@ -112,6 +112,9 @@ SIGNATURES = {
                                       _dp]),
     "mdg_mpole_forces": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double,
                                    C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "mdg_polar_forces": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                   _dp, _dp, _dp, _dp]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_amoeba_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "mdg_fetch_forces": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
@@ -155,7 +158,7 @@ class AmoebaParams(C.Structure):
                 ("exclude", C.c_int), ("terms", C.c_int)]
 
 
-TERM_VDW, TERM_MPOLE, TERM_POLAR = 1, 2, 4
+TERM_VDW, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE = 1, 2, 4, 8
 
 
 _lib = None
@@ -502,6 +505,25 @@ class Engine:
         check(self.lib.mdg_mpole_forces(self.ctx, t.list_id, alpha, cutoff, electric,
                                         int(exclude), _p(fx), _p(fy), _p(fz), _p(tx), _p(ty),
                                         _p(tz), C.byref(e), _p(w)))
+        return (_aos(fx, fy, fz), _aos(tx, ty, tz), e.value, w.reshape(3, 3))
+
+    def polar_forces(self, t: NeighborTable, p: "PolarParams", alpha: float,
+                     electric: float = 1.0, mu=None, exclude: bool = True):
+        """Polarization forces, torques on the permanent multipoles, pair
+        energy and pair virial at dipoles mu ((n, 3), caller order; None = the
+        context's last solve). mdg.h mdg_polar_forces."""
+        fx, fy, fz = self._vec3()
+        tx, ty, tz = self._vec3()
+        e = C.c_double()
+        w = np.zeros(9)
+        mx = my = mz = None
+        if mu is not None:
+            mu = np.asarray(mu, np.float64)
+            mx, my, mz = _f64(mu[:, 0]), _f64(mu[:, 1]), _f64(mu[:, 2])
+        check(self.lib.mdg_polar_forces(self.ctx, t.list_id, alpha, p.cutoff, p.thole_a,
+                                        electric, int(exclude), _p(mx), _p(my), _p(mz), _p(fx),
+                                        _p(fy), _p(fz), _p(tx), _p(ty), _p(tz), C.byref(e),
+                                        _p(w)))
         return (_aos(fx, fy, fz), _aos(tx, ty, tz), e.value, w.reshape(3, 3))
 
     # ---- fused steps ----------------------------------------------------------------

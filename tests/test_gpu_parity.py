@@ -425,3 +425,47 @@ def test_half_rows_match_deterministic_full_rows(engine, mdg):
     np.testing.assert_allclose(w0, w1, rtol=0, atol=1e-11 * np.abs(w1).max())
     for a, b in ((f0, f1), (t0, t1), (fc0, fc1)):
         np.testing.assert_allclose(a, b, rtol=0, atol=1e-12 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_polar_forces_match_oracle(engine, oracle, mdg, deterministic):
+    """Polarization forces/torques/virial at fixed dipoles (8(f)#1) vs the
+    tensor oracle (itself pinned by finite differences, test_oracle.py)."""
+    s = amoeba_small(mdg, 343, 21.0, 9)
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 9.0)
+    ep = oracle.perm_field_ewald(so, t_o, 0.5446, 7.0, 0.39, exclude=True)
+    mu, _, _ = oracle.pcg(so, t_o, 0.5446, 7.0, 0.39, ep, 1e-8, 200)
+    fo, to, eo, wo = oracle.polar_forces(so, t_o, 0.5446, 7.0, 0.39, mu, mdg.ELECTRIC)
+    engine.upload_system(s)
+    engine.set_deterministic(deterministic)
+    t = engine.build_neighbor_table(9.0)
+    f, tq, e, w = engine.polar_forces(t, mdg.PolarParams(7.0, 0.39), 0.5446, mdg.ELECTRIC, mu=mu)
+    engine.set_deterministic(False)
+    assert rel(e, eo) <= E_TOL
+    assert force_err_rms(f, fo) <= F_TOL
+    assert force_err_rms(tq, to) <= F_TOL
+    np.testing.assert_allclose(w, wo, rtol=0, atol=1e-9 * np.abs(wo).max())
+
+
+def test_amoeba_step_with_polar_forces_composes(engine, mdg):
+    """TERM_POLAR_FORCE adds exactly the polarization forces at the step's
+    own converged dipoles (pruned-row kernel == full-list API)."""
+    s = amoeba_small(mdg, 343, 21.0, 10)
+    engine.upload_system(s)
+    tv = engine.build_neighbor_table(10.0, list_id=1, sites=mdg.SITES_VDW)
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    base = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, base)
+    engine.amoeba_step(tv, te, p)
+    f0 = engine.fetch_forces()
+    _, w0, _, _ = engine.fetch_energies()
+    p.terms = base | mdg.TERM_POLAR_FORCE
+    engine.amoeba_step(tv, te, p)
+    f1 = engine.fetch_forces()
+    e1, w1, _, _ = engine.fetch_energies()
+    mu = engine.fetch_dipoles()
+    fp, _, _, wp = engine.polar_forces(te, mdg.PolarParams(7.0, 0.39), 0.5446, mdg.ELECTRIC, mu=mu)
+    scale = np.abs(f1).max()
+    np.testing.assert_allclose(f1 - f0, fp, rtol=0, atol=1e-10 * scale)
+    np.testing.assert_allclose(w1 - w0, wp, rtol=0, atol=1e-9 * np.abs(wp).max())

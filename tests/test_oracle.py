@@ -465,3 +465,53 @@ def test_fast_port_matches_tensor_oracle(oracle):
         mu = s.dipole
         eo = oracle.tmatvec_ewald(s, t, alpha, 8.0, 0.39, mu)
         assert np.abs(fp.tmatvec(s, t, alpha, 8.0, 0.39, mu) - eo).max() <= 1e-12 * np.abs(eo).max()
+
+
+# ---------------------------------------------------------------- polarization forces
+def _epol(oracle, s, t, alpha, thole=0.39, cutoff=9.0, electric=1.0):
+    """E_pol = -1/2 mu*.E_perm at the (tightly) converged dipoles."""
+    ep = oracle.perm_field_ewald(s, t, alpha, cutoff, thole, exclude=True)
+    mu, _, _ = oracle.pcg(s, t, alpha, cutoff, thole, ep, 1e-13, 1000)
+    return -0.5 * electric * float(np.sum(mu * ep)), mu, ep
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.45])
+def test_polar_energy_is_variational(oracle, alpha):
+    """At the solution, sum U_ij + 1/2 mu.alpha^-1.mu == -1/2 mu.E_perm."""
+    s = mpole_system(oracle, seed=11)
+    t = oracle.build_table(s, 9.0)
+    e, mu, ep = _epol(oracle, s, t, alpha)
+    _, _, epair, _ = oracle.polar_forces(s, t, alpha, 9.0, 0.39, mu)
+    eself = 0.5 * float(np.sum(mu * mu / s.polarizability[:, None]))
+    assert epair + eself == pytest.approx(e, rel=1e-9)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.45])
+def test_polar_forces_are_gradients(oracle, alpha):
+    """Forces at fixed mu == -dE_pol/dr with mu re-solved at every displacement
+    (the Hellmann-Feynman property of the stationary polarization energy)."""
+    s = mpole_system(oracle, seed=12)
+    t = oracle.build_table(s, 9.0)
+    _, mu, _ = _epol(oracle, s, t, alpha)
+    f, _, _, w = oracle.polar_forces(s, t, alpha, 9.0, 0.39, mu)
+    num = fd_forces(lambda q: _epol(oracle, q, t, alpha)[0], s, h=1e-5)
+    assert np.abs(num - f).max() <= 2e-6 * max(1.0, np.abs(f).max())
+    # momentum conservation (pair forces); the pair virial of these
+    # non-central forces is not symmetric
+    assert np.abs(f.sum(0)).max() <= 1e-10 * np.abs(f).max()
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.45])
+def test_polar_torques_by_rotation(oracle, alpha):
+    """Torque on the permanent multipoles == -dE_pol/dtheta (re-solved)."""
+    s = mpole_system(oracle, seed=13)
+    t = oracle.build_table(s, 9.0)
+    _, mu, _ = _epol(oracle, s, t, alpha)
+    _, tq, _, _ = oracle.polar_forces(s, t, alpha, 9.0, 0.39, mu)
+    h = 1e-5
+    for i in (1, 5, 9):
+        for a in range(3):
+            up = _epol(oracle, rotate_site(s, i, a, h), t, alpha)[0]
+            dn = _epol(oracle, rotate_site(s, i, a, -h), t, alpha)[0]
+            assert tq[i, a] == pytest.approx(-(up - dn) / (2 * h),
+                                             abs=2e-6 * max(1, np.abs(tq).max()))
