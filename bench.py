@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-polar-forces", action="store_true",
+                    help="skip the extra timing of the step with polarization forces")
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
 
@@ -304,6 +306,32 @@ def run_mine(args, world, rank, local):
                "ms_per_step": e2e_ms / args.steps}
         del f, e
 
+    # ---- 8(f)#1 extension, reported beside the headline (not in it): the
+    # same step plus polarization forces/torques at the converged dipoles
+    polar_forces = None
+    m_ = wl.m
+    if getattr(wl.p, "terms", 0) & m_.TERM_POLAR and not args.no_polar_forces:
+        base = wl.p.terms
+        wl.p.terms = base | m_.TERM_POLAR_FORCE
+        wl.step()
+        wl.rebuild()
+        if barrier:
+            barrier()
+        eng.synchronize()
+        eng.timer_start()
+        wl.run(args.steps)
+        pms = eng.timer_stop()
+        wl.p.terms = base
+        if barrier:
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor([pms], dtype=torch.float64, device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pms = float(t.item())
+        polar_forces = {"what": "same step + polarization forces/torques (TERM_POLAR_FORCE)",
+                        "value": world * wl.n * args.steps / (pms * 1e-3),
+                        "unit": "atom-steps/s", "ms_per_step": pms / args.steps}
+
     out = {
         "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
         "value": world * wl.n * args.steps / (ms * 1e-3),
@@ -325,6 +353,7 @@ def run_mine(args, world, rank, local):
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (lists > 126 MB)"},
         "e2e": e2e,
+        "with_polar_forces": polar_forces,
         "gpu_launches": launches,
         "roofline": roof,
         "roofline_other_kernels": others,
