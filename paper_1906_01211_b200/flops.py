@@ -24,6 +24,10 @@ PER_PAIR_FLOPS = {
     "perm_field": 350,      # q + mu + Theta, Ewald + Thole
     "field_tpre": 350,      # the same field; the T tensors it stores are a by-product
     "mpole": 570,           # energy + force + torque, q + mu + Theta
+    # polarization forces (8(f)#1): P + Thole l3..l9 (exp + 12) + Ewald B0..4
+    # (erfc + exp + sqrt + div + 16) + rr3..9 (12) + h (25) + f, g with
+    # gradients (2 x 75) + dipole/quadrupole torques on both sites (2 x 60)
+    "polar_force": 20 + 43 + 187 + 12 + 25 + 150 + 120,
 }
 
 # (kernel) -> which pairs its unit counts: (list role, cutoff key, excluded?)
@@ -33,6 +37,7 @@ PAIRS_OF = {
     "mpole": ("elec", "elec_cutoff", True), "perm_field": ("elec", "elec_cutoff", True),
     "field_tpre": ("elec", "elec_cutoff", True), "tmatvec": ("elec", "elec_cutoff", False),
     "tmatvec_pcg": ("elec", "elec_cutoff", False), "tmatvec_pre": ("elec", "elec_cutoff", False),
+    "polar_force": ("elec", "elec_cutoff", False),
 }
 
 

@@ -49,10 +49,12 @@ def run_domains(mdg, s, size, params, lists):
     return F, MU, out[0][3], out[0][4], out[0][5]
 
 
-@pytest.mark.parametrize("size", [2, 4])
-def test_domains_match_single_gpu(mdg, size):
+@pytest.mark.parametrize("size,polar_forces", [(2, False), (4, False), (2, True)])
+def test_domains_match_single_gpu(mdg, size, polar_forces):
     s = mdg.water_box(1728, 37.26, 5, "amoeba")
-    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, 0)
+    terms = (mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
+             if polar_forces else 0)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
     lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
     with mdg.Engine(s.n_sites) as e:
         e.upload_system(s)
