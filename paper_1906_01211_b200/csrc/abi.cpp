@@ -200,7 +200,13 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       set_device(c);
       c->n_cap = n_capacity;
       c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
-      MDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      {
+        // the context stream carries the step's critical path (field -> PCG);
+        // it outranks the aux stream (Halgren, multipoles) at block dispatch
+        int lo = 0, hi = 0;
+        MDG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        MDG_CUDA_CHECK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+      }
       const size_t n = (size_t)n_capacity;
       dalloc(&c->d_perm, n);
       dalloc(&c->d_iperm, n);
@@ -241,6 +247,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (!c) return MDG_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
@@ -266,6 +273,10 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->timer_a) cudaEventDestroy(c->timer_a);
   if (c->timer_b) cudaEventDestroy(c->timer_b);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->aux_partials) cudaFree(c->aux_partials);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_tpre, c->ev_join})
+    if (e) cudaEventDestroy(e);
   delete c;
   return MDG_OK;
 }
@@ -827,6 +838,24 @@ int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
   });
 }
 
+// Halgren + multipoles on the aux stream beside field + PCG (MDG_OVERLAP=0: one stream)
+static bool overlap_enabled(mdg_ctx* c) {
+  static const int env = [] {
+    const char* e = getenv("MDG_OVERLAP");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env) return false;
+  if (!c->aux_stream) {
+    // the aux chain fills what the critical path (field -> PCG) leaves idle
+    int lo = 0, hi = 0;
+    MDG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    MDG_CUDA_CHECK(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, lo));
+    for (cudaEvent_t* e : {&c->ev_fork, &c->ev_tpre, &c->ev_join})
+      MDG_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  return true;
+}
+
 int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
   return guard([&] {
     need_system(c);
@@ -841,21 +870,52 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
          "amoeba_step: polarization forces need the polarization solve");
     MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
     c->has_polar_force = false;
-    if (terms & MDG_TERM_VDW) {
-      mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
-    } else {
-      mdg::zero_vec(c, c->force);
+    // Two independent chains: [aux] Halgren -> multipoles (after the pruned
+    // rows exist) and [main] permanent field + T -> PCG. Joined before the
+    // polarization forces, which add to the same force/torque arrays.
+    const bool ov = overlap_enabled(c);
+    if (ov) {
+      MDG_CUDA_CHECK(cudaEventRecord(c->ev_fork, c->stream));
+      MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
+    }
+    // the main stream always ends behind the aux chain, also when a later
+    // stage throws (e.g. ConvergenceError from the PCG)
+    struct Join {
+      mdg_ctx* c;
+      bool on;
+      ~Join() {
+        if (!on) return;
+        cudaEventRecord(c->ev_join, c->aux_stream);
+        cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+      }
+    } join{c, ov};
+    {
+      mdg::AuxScope aux(c, ov);
+      if (terms & MDG_TERM_VDW) {
+        mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
+      } else {
+        mdg::zero_vec(c, c->force);
+      }
     }
     // With polarization, one pass over the 9 A list prunes it to 7 A, stores
     // the T tensors and computes the permanent field; the multipole kernel
     // then runs on the pruned rows.
     const bool polar = (terms & MDG_TERM_POLAR) != 0;
-    if (polar) mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
-    if (terms & MDG_TERM_MPOLE) {
-      if (polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
-      else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
-    } else {
-      mdg::zero_vec(c, c->torque);
+    if (polar) {
+      mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
+      if (ov) {
+        MDG_CUDA_CHECK(cudaEventRecord(c->ev_tpre, c->stream));
+        MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
+      }
+    }
+    {
+      mdg::AuxScope aux(c, ov);
+      if (terms & MDG_TERM_MPOLE) {
+        if (polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
+        else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
+      } else {
+        mdg::zero_vec(c, c->torque);
+      }
     }
     c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
     c->pcg_rms = 0;
@@ -864,12 +924,16 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
       c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
       c->pcg_rms = rms;
       mdg::polar_energy(c, p->electric, 40);
-      if (terms & MDG_TERM_POLAR_FORCE) {
-        // the PCG leaves the halo dipoles at mu0: refresh them first
-        mdg::exchange_halo(c, MDG_VEC_MU);
-        mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
-        c->has_polar_force = true;
-      }
+    }
+    if (ov) {  // polarization forces add to the aux chain's force/torque
+      MDG_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux_stream));
+      MDG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    }
+    if (polar && (terms & MDG_TERM_POLAR_FORCE)) {
+      // the PCG leaves the halo dipoles at mu0: refresh them first
+      mdg::exchange_halo(c, MDG_VEC_MU);
+      mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
+      c->has_polar_force = true;
     }
   });
 }

@@ -166,6 +166,12 @@ struct mdg_ctx {
   // full-row (bitwise reproducible) pair sums instead of half rows + atomics
   bool deterministic = false;
   bool has_polar_force = false;  // last AMOEBA step added polarization forces
+  // second stream of the AMOEBA step: Halgren + multipoles run beside the
+  // permanent field + PCG (independent work); its own block partials
+  cudaStream_t aux_stream = nullptr;
+  double* aux_partials = nullptr;
+  int64_t aux_partial_blocks = 0;
+  cudaEvent_t ev_fork = nullptr, ev_tpre = nullptr, ev_join = nullptr;
 
   // last step
   double energies[4] = {0, 0, 0, 0};
@@ -229,6 +235,35 @@ int64_t sites_per_block(const void* kernel, int64_t n);
     (ctx)->last_grid = _g;                                                     \
     MDG_LAUNCH((ctx), (name), (unsigned)_g, ::mdg::kBlock, 0, kernel, (args)); \
   } while (0)
+
+// Launches inside this scope go to the context's aux stream with its own
+// partials buffer (no-op when !on).
+struct AuxScope {
+  mdg_ctx* c;
+  bool on;
+  cudaStream_t s;
+  double* p;
+  int64_t pb;
+  AuxScope(mdg_ctx* c_, bool on_) : c(c_), on(on_) {
+    if (!on) return;
+    s = c->stream;
+    p = c->partials;
+    pb = c->partial_blocks;
+    c->stream = c->aux_stream;
+    c->partials = c->aux_partials;
+    c->partial_blocks = c->aux_partial_blocks;
+  }
+  ~AuxScope() {
+    if (!on) return;
+    c->aux_partials = c->partials;
+    c->aux_partial_blocks = c->partial_blocks;
+    c->stream = s;
+    c->partials = p;
+    c->partial_blocks = pb;
+  }
+  AuxScope(const AuxScope&) = delete;
+  AuxScope& operator=(const AuxScope&) = delete;
+};
 
 // ---- host entry points implemented in the .cu files -----------------------
 void ensure_partials(mdg_ctx* c, int64_t blocks);
