@@ -246,6 +246,11 @@ int mdg_set_comm(mdg_ctx* ctx, mdg_exchange_fn exchange, mdg_allreduce_fn allred
  * reproducible). The environment variable MDG_DETERMINISTIC sets the
  * default of new contexts. Energies and virials are reproducible in both. */
 int mdg_set_deterministic(mdg_ctx* ctx, int on);
+/* AMOEBA step scheduling. Default (1): Halgren and the multipoles run on a
+ * low-priority second stream beside the field -> PCG chain; 0: one stream
+ * (kernel-by-kernel profiling). MDG_OVERLAP=0 sets the default of new
+ * contexts. Results are the same either way. */
+int mdg_set_overlap(mdg_ctx* ctx, int on);
 /* Gather 3 doubles per listed caller-order site of vec_id into out[3*count]
  * (x,y,z interleaved) / scatter them back. Host buffers. */
 int mdg_vec_pack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count, double* out);

@@ -197,6 +197,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
     try {
       c->device = device;
       if (const char* d = getenv("MDG_DETERMINISTIC")) c->deterministic = atoi(d) != 0;
+      if (const char* o = getenv("MDG_OVERLAP")) c->overlap = atoi(o) != 0;
       set_device(c);
       c->n_cap = n_capacity;
       c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
@@ -360,6 +361,13 @@ int mdg_set_deterministic(mdg_ctx* c, int on) {
   return guard([&] {
     need_ctx(c);
     c->deterministic = on != 0;
+  });
+}
+
+int mdg_set_overlap(mdg_ctx* c, int on) {
+  return guard([&] {
+    need_ctx(c);
+    c->overlap = on != 0;
   });
 }
 
@@ -840,11 +848,7 @@ int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
 
 // Halgren + multipoles on the aux stream beside field + PCG (MDG_OVERLAP=0: one stream)
 static bool overlap_enabled(mdg_ctx* c) {
-  static const int env = [] {
-    const char* e = getenv("MDG_OVERLAP");
-    return e ? atoi(e) : 1;
-  }();
-  if (!env) return false;
+  if (!c->overlap) return false;
   if (!c->aux_stream) {
     // the aux chain fills what the critical path (field -> PCG) leaves idle
     int lo = 0, hi = 0;

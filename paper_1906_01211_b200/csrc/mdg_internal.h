@@ -165,6 +165,7 @@ struct mdg_ctx {
   int64_t epoch = 0;  // source of DevList::version
   // full-row (bitwise reproducible) pair sums instead of half rows + atomics
   bool deterministic = false;
+  bool overlap = true;  // AMOEBA step on two streams (mdg_set_overlap)
   bool has_polar_force = false;  // last AMOEBA step added polarization forces
   // second stream of the AMOEBA step: Halgren + multipoles run beside the
   // permanent field + PCG (independent work); its own block partials

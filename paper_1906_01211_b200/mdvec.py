@@ -130,6 +130,7 @@ SIGNATURES = {
                                           C.c_double, C.c_double, C.c_double] + [_dp] * 9),
     "mdg_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mdg_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_unpack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_pack_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
@@ -587,6 +588,10 @@ class Engine:
         """Full-row pair sums (bitwise reproducible forces/torques) instead of
         the default half rows with atomic partner updates (mdg.h)."""
         check(self.lib.mdg_set_deterministic(self.ctx, int(on)))
+
+    def set_overlap(self, on: bool = True):
+        """AMOEBA step on two streams (default) or one (mdg.h)."""
+        check(self.lib.mdg_set_overlap(self.ctx, int(on)))
 
     def launch_count(self) -> int:
         return int(self.lib.mdg_launch_count(self.ctx))
