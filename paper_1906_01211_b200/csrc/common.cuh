@@ -70,18 +70,18 @@ __device__ __forceinline__ void block_store_partials(double (&v)[NV], double* pa
 }
 
 // Thole factors (proj/include/mdvec/polar.hpp:55-62) with per-site
-// pdamp = alpha^(1/6): u = r/(pd_i pd_j). l7 for the quadrupole field.
-__device__ __forceinline__ void thole3(double r, double pdij, double a, double& l3, double& l5) {
-  const double u = r / pdij;
+// pdamp = alpha^(1/6): u = r/(pd_i pd_j), formed by the callers as
+// r * ipd_i * ipd_j from the stored inverses (no division). l7 for the
+// quadrupole field.
+__device__ __forceinline__ void thole3(double u, double a, double& l3, double& l5) {
   const double au3 = a * u * u * u;
   const double ex = exp(-au3);
   l3 = 1.0 - ex;
   l5 = 1.0 - (1.0 + au3) * ex;
 }
 
-__device__ __forceinline__ void thole7(double r, double pdij, double a, double& l3, double& l5,
+__device__ __forceinline__ void thole7(double u, double a, double& l3, double& l5,
                                        double& l7) {
-  const double u = r / pdij;
   const double au3 = a * u * u * u;
   const double ex = exp(-au3);
   l3 = 1.0 - ex;
@@ -91,11 +91,12 @@ __device__ __forceinline__ void thole7(double r, double pdij, double a, double& 
 
 // Tinker bn recursion for real-space Ewald: B0 = erfc(ar)/r,
 // Bn = ((2n-1) B(n-1) + (2a^2)^n/(a sqrt(pi)) exp(-a^2 r^2)) / r^2.
+// Callers pass 1/r (their one division per pair) and 1/r^2 = (1/r)^2.
 template <int NMAX>
-__device__ __forceinline__ void ewald_bn(double r, double r2, double inv_r2, double alpha,
+__device__ __forceinline__ void ewald_bn(double r, double inv_r, double inv_r2, double alpha,
                                          double (&bn)[NMAX + 1]) {
   const double ralpha = alpha * r;
-  bn[0] = erfc(ralpha) / r;
+  bn[0] = erfc(ralpha) * inv_r;
   const double alsq2 = 2.0 * alpha * alpha;
   double alsq2n = (alpha > 0) ? 1.0 / (1.7724538509055160273 * alpha) : 0.0;
   const double exp2a = exp(-ralpha * ralpha);
@@ -145,6 +146,20 @@ __device__ __forceinline__ int row_suffix(const int32_t* __restrict__ row, int c
   const unsigned m2 = __ballot_sync(0xffffffffu, gt2);
   return m2 ? lo + __ffs(m2) - 1 : hi;
 }
+
+// Minimum resident blocks per SM of the warp-per-site pair kernels (register
+// caps); tuned per kernel on config 4, overridable for experiments.
+// (An explicit minimum of 1 lifts nvcc's default register heuristic and
+// costs occupancy: multipoles 5.04 ms at 204 registers vs 4.4 at <= 170.)
+#ifndef MDG_MPOLE_MINB
+#define MDG_MPOLE_MINB 3
+#endif
+#ifndef MDG_HALGREN_MINB
+#define MDG_HALGREN_MINB 5
+#endif
+#ifndef MDG_POLFORCE_MINB
+#define MDG_POLFORCE_MINB 3
+#endif
 
 // ---- warp-per-site execution ------------------------------------------------
 // One warp walks one site's row 32 slots at a time (coalesced 128-B index

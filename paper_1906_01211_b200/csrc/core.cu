@@ -239,7 +239,7 @@ __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
   const double pol = st[8 * n + o];
   const double pd = cbrt(sqrt(pol));
   polp[s] = make_double2(pol, pd);
-  pq4[s] = make_double4(pol, pd, q, 0.0);
+  pq4[s] = make_double4(pol, pd, q, 1.0 / pd);  // w: 1/pdamp (Thole u = r ipd_i ipd_j)
 }
 
 void pack_system(mdg_ctx* c) {

@@ -49,7 +49,7 @@ __device__ __forceinline__ void qmul(const Quad& Q, double x, double y, double z
 // with i <-> j and R -> -R) through FP64 atomics. Halo pairs stay in the
 // owned row at energy/virial weight 1/2. !HALF: full rows, no atomics.
 template <bool EXCL, bool PRUNED, bool HALF>
-__global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
+__global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
@@ -73,9 +73,10 @@ __global__ void __launch_bounds__(kBlock) k_mpole(MKArgs a) {
       const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
       const double qj = pj.w, djx = m0j.x, djy = m0j.y, djz = m0j.z;
       const double r = sqrt(r2);
-      const double inv_r2 = 1.0 / r2;
+      const double inv_r = 1.0 / r;
+      const double inv_r2 = inv_r * inv_r;
       double G[6];
-      ewald_bn<5>(r, r2, inv_r2, a.alpha, G);
+      ewald_bn<5>(r, inv_r, inv_r2, a.alpha, G);
 #pragma unroll
       for (int q = 0; q < 6; ++q) G[q] *= a.electric;
 

@@ -180,7 +180,7 @@ struct HalgrenKArgs {
 // virial are weighted 1 (owned pair) or 1/2 (halo pair), finalize scale 1.
 // !HALF: full rows, each pair in both rows at weight 1/2 (finalize scale).
 template <bool EXCL, bool HALF>
-__global__ void __launch_bounds__(kBlock) k_halgren(HalgrenKArgs a) {
+__global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};

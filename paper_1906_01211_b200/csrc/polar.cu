@@ -17,6 +17,11 @@
 
 #include "common.cuh"
 
+// field_tpre: 6 resident blocks per SM (<= 85 registers) measured fastest
+// (4.25 ms vs 4.54 unconstrained at 112 registers; 4/5/7/8 slower)
+#ifndef MDG_PF_MINB
+#define MDG_PF_MINB 6
+#endif
 #ifndef MDG_TPRE_UNROLL
 #define MDG_TPRE_UNROLL 1
 #endif
@@ -29,6 +34,7 @@ struct TKArgs {
   int ipw;
   const double4* __restrict__ pos;
   const double2* __restrict__ polp;
+  const double4* __restrict__ pq4;
   ListView L;
   Box b;
   double c2, alpha, thole_a;
@@ -44,7 +50,7 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
-    const double2 ai = a.polp[i];
+    const double ipdi = a.pq4[i].w;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double ex = 0, ey = 0, ez = 0;
@@ -52,17 +58,18 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec(TKArgs a) {
       const int32_t j = ring_j(e);
       const double dx = e.x, dy = e.y, dz = e.z;
       const double r2 = dist2(dx, dy, dz);
-      const double2 aj = __ldg(a.polp + j);
+      const double ipdj = __ldg(&a.pq4[j].w);
       const double4 mj = ldg4(a.in + j);
       const double r = sqrt(r2);
       double l3, l5;
-      thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
+      thole3(r * ipdi * ipdj, a.thole_a, l3, l5);
       double rr3, rr5;
       if (EWALD) {
-        const double inv_r2 = 1.0 / r2;
+        const double inv_r = 1.0 / r;
+        const double inv_r2 = inv_r * inv_r;
         double bn[3];
-        ewald_bn<2>(r, r2, inv_r2, a.alpha, bn);
-        const double b3 = inv_r2 / r;
+        ewald_bn<2>(r, inv_r, inv_r2, a.alpha, bn);
+        const double b3 = inv_r2 * inv_r;
         rr3 = bn[1] - (1.0 - l3) * b3;
         rr5 = bn[2] - (1.0 - l5) * 3.0 * b3 * inv_r2;
       } else {
@@ -96,6 +103,7 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
   k.n_i = c->n_own;
   k.pos = c->pos;
   k.polp = c->polp;
+  k.pq4 = c->pq4;
   k.L = ListView{L.nbr, L.cnt, L.cap};
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
@@ -152,13 +160,13 @@ __device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int3
 // TPRE: also write the pruned row (all pairs within the cutoff, exclusion
 // flag in bit 31) and its T tensors; the field skips excluded pairs.
 template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE>
-__global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
+__global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
-    const double2 ai = a.polp[i];
+    const double ipdi = a.pq4[i].w;
     const int32_t mi = a.mol[i];
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
@@ -170,20 +178,21 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
       const int32_t j = raw & 0x7fffffff;
       const double dx = e.x, dy = e.y, dz = e.z;
       const double r2 = dist2(dx, dy, dz);
-      // (polarizability, polarizability^(1/6), charge) of j in one 32-B load
+      // (polarizability, pdamp, charge, 1/pdamp) of j in one 32-B load
       const double4 xj = ldg4(a.pq4 + j);
-      const double2 aj = make_double2(xj.x, xj.y);
       const double4 pj = make_double4(0.0, 0.0, 0.0, xj.z);
       const double r = sqrt(r2);
-      const double inv_r2 = 1.0 / r2;
-      const double b1 = inv_r2 / r;
+      const double inv_r = 1.0 / r;
+      const double inv_r2 = inv_r * inv_r;
+      const double b1 = inv_r2 * inv_r;
+      const double u = r * ipdi * xj.w;
       if (!MPOLE && !TPRE) {
         double l3, l5;
-        thole3(r, ai.y * aj.y, a.thole_a, l3, l5);
+        thole3(u, a.thole_a, l3, l5);
         double rr3;
         if (EWALD) {
           double bn[2];
-          ewald_bn<1>(r, r2, inv_r2, a.alpha, bn);
+          ewald_bn<1>(r, inv_r, inv_r2, a.alpha, bn);
           rr3 = bn[1] - (1.0 - l3) * b1;
         } else {
           rr3 = l3 / (r2 * r);  // proj/src/polar_scalar.cpp:143
@@ -195,12 +204,12 @@ __global__ void __launch_bounds__(kBlock) k_perm_field(FKArgs a) {
         return;
       }
       double l3, l5, l7;
-      thole7(r, ai.y * aj.y, a.thole_a, l3, l5, l7);
+      thole7(u, a.thole_a, l3, l5, l7);
       const double b2 = 3.0 * b1 * inv_r2, b3 = 5.0 * b2 * inv_r2;
       double rr3, rr5, rr7;
       if (EWALD) {
         double bn[4];
-        ewald_bn<3>(r, r2, inv_r2, a.alpha, bn);
+        ewald_bn<3>(r, inv_r, inv_r2, a.alpha, bn);
         rr3 = bn[1] - (1.0 - l3) * b1;
         rr5 = bn[2] - (1.0 - l5) * b2;
         rr7 = bn[3] - (1.0 - l7) * b3;

@@ -24,7 +24,7 @@ struct PFArgs {
   int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ mp;
-  const double4* __restrict__ pq4;  // (alpha, alpha^(1/6), q, 0)
+  const double4* __restrict__ pq4;  // (alpha, alpha^(1/6), q, alpha^(-1/6))
   const double4* __restrict__ mu;
   const int32_t* __restrict__ mol;
   ListView L;
@@ -70,7 +70,7 @@ __device__ __forceinline__ Sym3 gq(double e, double rr5, double rr7, double s, d
 
 // partial slots: 0 pair energy, 1..9 virial (row-major)
 template <bool EXCL, bool PRUNED, bool HALF>
-__global__ void __launch_bounds__(kBlock) k_polar_force(PFArgs a) {
+__global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kBlock) k_polar_force(PFArgs a) {
     const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
     const Sym3 Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
     const double4 ui = a.mu[i];
-    const double pdi = a.pq4[i].y;
+    const double ipdi = a.pq4[i].w;  // 1 / pdamp_i
     const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
@@ -97,9 +97,10 @@ __global__ void __launch_bounds__(kBlock) k_polar_force(PFArgs a) {
       const double4 pj = ldg4(a.pq4 + j);  // (alpha, pdamp, q)
       const double4 uj = ldg4(a.mu + j);
       const double r = sqrt(r2);
-      const double inv_r2 = 1.0 / r2;
+      const double inv_r = 1.0 / r;
+      const double inv_r2 = inv_r * inv_r;
       // Thole lambda3..9 (exponential damping, u = r / (pd_i pd_j))
-      const double u = r / (pdi * pj.y);
+      const double u = r * ipdi * pj.w;
       const double s1 = a.thole_a * u * u * u;
       const double ex = exp(-s1);
       const double s2 = s1 * s1;
@@ -108,8 +109,8 @@ __global__ void __launch_bounds__(kBlock) k_polar_force(PFArgs a) {
       const double l7 = 1.0 - (1.0 + s1 + 0.6 * s2) * ex;
       const double l9 = 1.0 - (1.0 + s1 + (18.0 / 35.0) * s2 + (9.0 / 35.0) * s2 * s1) * ex;
       double bn[5];
-      ewald_bn<4>(r, r2, inv_r2, a.alpha, bn);
-      const double g1 = inv_r2 / r, g2 = 3.0 * g1 * inv_r2, g3 = 5.0 * g2 * inv_r2,
+      ewald_bn<4>(r, inv_r, inv_r2, a.alpha, bn);
+      const double g1 = inv_r2 * inv_r, g2 = 3.0 * g1 * inv_r2, g3 = 5.0 * g2 * inv_r2,
                    g4 = 7.0 * g3 * inv_r2;
       const double rr3 = bn[1] - (1.0 - l3) * g1;
       const double rr5 = bn[2] - (1.0 - l5) * g2;
