@@ -279,6 +279,9 @@ int mdg_profile_report(mdg_ctx* ctx, char* buf, int64_t buf_len);
 
 /* FP64 DFMA-chain peak probe on `device` (TFLOP/s, best of 5). */
 int mdg_probe_fp64_peak(int device, double* tflops);
+/* The pair kernels' device erfc (exp(-x^2) * erfcx polynomial, common.cuh)
+ * evaluated at n host points: accuracy check against a host erfc. */
+int mdg_probe_erfc(int device, const double* x, int64_t n, double* out);
 /* Directed (both-direction) pairs of list_id within cutoff (minus excluded
  * pairs when exclude != 0) and total list slots: roofline numerators. */
 int mdg_nlist_count_within(mdg_ctx* ctx, int list_id, double cutoff, int exclude,

@@ -89,6 +89,41 @@ __device__ __forceinline__ void thole7(double u, double a, double& l3, double& l
   l7 = 1.0 - (1.0 + au3 + 0.6 * au3 * au3) * ex;
 }
 
+// erfc(x) from the exp(-x^2) the Ewald recursion computes anyway:
+// erfc = exp(-x^2) * erfcx(x), erfcx on [0, 6] a degree-18 polynomial in
+// t = (x - 3)/(x + 3) (tools/fit_erfcx.py: max relative error 4.4e-16 in
+// double Horner). Coefficients sit in the constant bank, so the DFMAs take
+// them as operands (the library erfc materialises its constants with UMOVs
+// and recomputes exp(-x^2) internally). Beyond x = 6 (erfc < 2e-17) or for
+// NaN the library function is used.
+static __constant__ double kErfcx[19] = {
+    0.17900115118138996,     -0.32623356004303744,    0.24560380171233284,
+    -0.15011593650073177,    0.07166583719787115,     -0.024392499321270803,
+    0.004269136332174619,    0.0007077465012785561,   -0.0005970618259925815,
+    4.525468578951527e-05,   6.405418474854186e-05,   -1.285998407416855e-05,
+    -7.962426888254932e-06,  2.146772173006056e-06,   1.2424066961151949e-06,
+    -3.9301447303001125e-07, -3.9867716616971016e-07, -1.1020487050346528e-07,
+    -1.1194382877771014e-08};
+
+__device__ __forceinline__ double rcp_nr(double d) {
+  float f;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)d));
+  double y = (double)f;  // ~1e-7, two Newton steps -> full double precision
+  double e = __fma_rn(-d, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-d, y, 1.0);
+  return __fma_rn(y, e, y);
+}
+
+__device__ __forceinline__ double erfc_from_exp(double x, double exp_mx2) {
+  if (!(x <= 6.0)) return erfc(x);
+  const double t = (x - 3.0) * rcp_nr(x + 3.0);
+  double p = kErfcx[18];
+#pragma unroll
+  for (int k = 17; k >= 0; --k) p = __fma_rn(p, t, kErfcx[k]);
+  return exp_mx2 * p;
+}
+
 // Tinker bn recursion for real-space Ewald: B0 = erfc(ar)/r,
 // Bn = ((2n-1) B(n-1) + (2a^2)^n/(a sqrt(pi)) exp(-a^2 r^2)) / r^2.
 // Callers pass 1/r (their one division per pair) and 1/r^2 = (1/r)^2.
@@ -96,10 +131,10 @@ template <int NMAX>
 __device__ __forceinline__ void ewald_bn(double r, double inv_r, double inv_r2, double alpha,
                                          double (&bn)[NMAX + 1]) {
   const double ralpha = alpha * r;
-  bn[0] = erfc(ralpha) * inv_r;
   const double alsq2 = 2.0 * alpha * alpha;
   double alsq2n = (alpha > 0) ? 1.0 / (1.7724538509055160273 * alpha) : 0.0;
   const double exp2a = exp(-ralpha * ralpha);
+  bn[0] = erfc_from_exp(ralpha, exp2a) * inv_r;
 #pragma unroll
   for (int k = 1; k <= NMAX; ++k) {
     alsq2n *= alsq2;

@@ -73,8 +73,10 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
         const double r = sqrt(r2);
         const double inv_r = 1.0 / r;
         const double qq = a.electric * pi.w * pj.w;
-        const double ee = erfc(a.alpha * r) * inv_r;
-        const double g = a.alpha * two_over_sqrt_pi * exp(-a.alpha * a.alpha * r2);
+        const double ar = a.alpha * r;
+        const double ex2 = exp(-ar * ar);
+        const double ee = erfc_from_exp(ar, ex2) * inv_r;
+        const double g = a.alpha * two_over_sqrt_pi * ex2;
         acc[1] += w * (qq * ee);
         fs += qq * (ee + g) * inv_r * inv_r;
       }

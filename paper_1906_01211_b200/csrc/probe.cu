@@ -48,7 +48,31 @@ __global__ void __launch_bounds__(kBlock) k_count_within(int64_t n, const double
   block_store_partials<2>(acc, partials);
 }
 
+__global__ void k_erfc_probe(int64_t n, const double* __restrict__ x, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = erfc_from_exp(x[i], exp(-x[i] * x[i]));
+}
+
 }  // namespace mdg
+
+extern "C" int mdg_probe_erfc(int device, const double* x, int64_t n, double* out) {
+  try {
+    if (!x || !out || n < 0) mdg::throw_error(MDG_CONTRACT, "probe_erfc: bad arguments");
+    mdg::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    double *dx = nullptr, *dy = nullptr;
+    mdg::cuda_check(cudaMalloc(&dx, (size_t)n * 8 + 8), "malloc");
+    mdg::cuda_check(cudaMalloc(&dy, (size_t)n * 8 + 8), "malloc");
+    mdg::cuda_check(cudaMemcpy(dx, x, (size_t)n * 8, cudaMemcpyHostToDevice), "h2d");
+    mdg::k_erfc_probe<<<(unsigned)((n + 255) / 256 + 1), 256>>>(n, dx, dy);
+    mdg::cuda_check(cudaGetLastError(), "k_erfc_probe");
+    mdg::cuda_check(cudaMemcpy(out, dy, (size_t)n * 8, cudaMemcpyDeviceToHost), "d2h");
+    cudaFree(dx);
+    cudaFree(dy);
+    return MDG_OK;
+  } catch (const mdg::Error& e) {
+    return e.code;
+  }
+}
 
 extern "C" int mdg_probe_fp64_peak(int device, double* tflops) {
   try {

@@ -138,6 +138,7 @@ SIGNATURES = {
     "mdg_timer_start": (C.c_int, [C.c_void_p]),
     "mdg_timer_stop": (C.c_int, [C.c_void_p, _dp]),
     "mdg_probe_fp64_peak": (C.c_int, [C.c_int, _dp]),
+    "mdg_probe_erfc": (C.c_int, [C.c_int, _dp, C.c_int64, _dp]),
     "mdg_nlist_count_within": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, _i64p,
                                          _i64p]),
     "mdg_water_generate": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp,
@@ -617,6 +618,14 @@ def fp64_peak_tflops(device: int = 0) -> float:
     v = C.c_double()
     check(load_library().mdg_probe_fp64_peak(device, C.byref(v)))
     return v.value
+
+
+def device_erfc(x, device: int = 0) -> np.ndarray:
+    """The pair kernels' erfc evaluated on the device (accuracy probe)."""
+    x = _f64(x)
+    out = np.zeros_like(x)
+    check(load_library().mdg_probe_erfc(device, _p(x), len(x), _p(out)))
+    return out
 
 
 # ---- fixtures ------------------------------------------------------------------------
