@@ -295,14 +295,20 @@ def run_mine(args, world, rank, local):
                                               "avg_launch_ms", "share_of_step",
                                               "ncu_executed_fp64", "timing")}
 
+    m_host_array = wl.m.host_array
     # ---- end to end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        x, y, z = wl.sys.x.copy(), wl.sys.y.copy(), wl.sys.z.copy()
+        # the step's host buffers live in page-locked memory (the public
+        # host_array): coordinates DMA'd in, forces DMA'd out, no staging copy
+        xyz = m_host_array((3, wl.n))
+        xyz[0], xyz[1], xyz[2] = wl.sys.x, wl.sys.y, wl.sys.z
+        x, y, z = xyz[0], xyz[1], xyz[2]
+        fbuf = m_host_array((3, wl.n))
         for _ in range(2):
             eng.upload_positions(x, y, z)
             wl.step()
-            eng.fetch_forces()
+            eng.fetch_forces(out=fbuf)
         wl.rebuild()
         if barrier:
             barrier()
@@ -314,7 +320,7 @@ def run_mine(args, world, rank, local):
             if k % REBUILD_EVERY == 0:
                 wl.rebuild()
             wl.step()
-            f = eng.fetch_forces()                   # D2H 24 B/atom
+            f = eng.fetch_forces(out=fbuf)           # D2H 24 B/atom
             e = eng.fetch_energies()                 # D2H energies/virial
         e2e_ms = eng.timer_stop()
         wall_ms = (time.perf_counter() - t0) * 1e3

@@ -277,6 +277,12 @@ int mdg_profile_reset(mdg_ctx* ctx);
 /* Writes "name count total_ms\n" lines into buf (NUL terminated). */
 int mdg_profile_report(mdg_ctx* ctx, char* buf, int64_t buf_len);
 
+/* Page-locked host buffers: per-step inputs/outputs that live here skip the
+ * staging copy (positions are DMA'd straight from them, results straight
+ * into them). Any pointer works with every call; pinned ones are faster. */
+int mdg_host_alloc(void** ptr, int64_t bytes);
+int mdg_host_free(void* ptr);
+
 /* FP64 DFMA-chain peak probe on `device` (TFLOP/s, best of 5). */
 int mdg_probe_fp64_peak(int device, double* tflops);
 /* The pair kernels' device erfc (exp(-x^2) * erfcx polynomial, common.cuh)

@@ -6,5 +6,5 @@ from .mdvec import (  # noqa: F401
     CharmmParams, ContractViolation, ConvergenceError, CudaError, Engine, EwaldRealParams,
     FieldArrays, ForceAccumulator, HalgrenParams, LjParams, NeighborTable, ParticleSystem,
     PolarizationState, PolarParams, SingularityError, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE, TERM_VDW,
-    fp64_peak_tflops, load_library, reduce_sites_host,
+    fp64_peak_tflops, host_array, load_library, reduce_sites_host,
     water_box)

@@ -128,16 +128,33 @@ void host_parallel(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
   for (auto& x : th) x.join();
 }
 
-// Copy caller arrays into the pinned stage and upload them. With `box`, the
-// first three arrays are positions and are checked to lie in [0, L) in the
-// same pass (the ParticleSystem contract, proj/src/system.cpp).
+static bool is_pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Copy caller arrays into the pinned stage and upload them (or, when every
+// array is page-locked, DMA them directly). With `box`, the first three
+// arrays are positions and are checked to lie in [0, L) (the ParticleSystem
+// contract, proj/src/system.cpp) -- on the host, overlapping the DMA.
 void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double* box = nullptr) {
   const int64_t n = c->n;
+  bool pinned = true;
+  for (const double* a : arrays) pinned = pinned && is_pinned(a);
+  if (pinned)
+    for (size_t a = 0; a < arrays.size(); ++a)
+      MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage + a * n, arrays[a], n * sizeof(double),
+                                     cudaMemcpyHostToDevice, c->stream));
   std::atomic<bool> bad{false};
   host_parallel(n, [&](int64_t b, int64_t e) {
     for (size_t a = 0; a < arrays.size(); ++a) {
       const double* src = arrays[a];
-      std::memcpy(c->h_stage + a * n + b, src + b, (e - b) * sizeof(double));
+      if (!pinned) std::memcpy(c->h_stage + a * n + b, src + b, (e - b) * sizeof(double));
       if (box && a < 3) {
         const double L = box[a];
         bool ok = true;
@@ -147,8 +164,9 @@ void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double
     }
   });
   need(!bad, "ParticleSystem: position outside the box");
-  MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
-                                 cudaMemcpyHostToDevice, c->stream));
+  if (!pinned)
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
+                                   cudaMemcpyHostToDevice, c->stream));
 }
 
 // sorted double4 vector -> caller-order SoA host arrays (NULL entries skipped)
@@ -156,10 +174,20 @@ void vec_out(mdg_ctx* c, const double4* v, double* ox, double* oy, double* oz) {
   if (!ox && !oy && !oz) return;
   const int64_t n = c->n;
   mdg::gather_vec_to_caller(c, v, c->d_stage);
+  double* outs[3] = {ox, oy, oz};
+  bool pinned = true;
+  for (double* o : outs) pinned = pinned && (!o || is_pinned(o));
+  if (pinned) {
+    for (int a = 0; a < 3; ++a)
+      if (outs[a])
+        MDG_CUDA_CHECK(cudaMemcpyAsync(outs[a], c->d_stage + a * n, n * sizeof(double),
+                                       cudaMemcpyDeviceToHost, c->stream));
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   MDG_CUDA_CHECK(cudaMemcpyAsync(c->h_stage, c->d_stage, 3 * n * sizeof(double),
                                  cudaMemcpyDeviceToHost, c->stream));
   MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  double* outs[3] = {ox, oy, oz};
   host_parallel(n, [&](int64_t b, int64_t e) {
     for (int a = 0; a < 3; ++a)
       if (outs[a]) std::memcpy(outs[a] + b, c->h_stage + a * n + b, (e - b) * sizeof(double));
@@ -361,6 +389,19 @@ int mdg_set_deterministic(mdg_ctx* c, int on) {
   return guard([&] {
     need_ctx(c);
     c->deterministic = on != 0;
+  });
+}
+
+int mdg_host_alloc(void** ptr, int64_t bytes) {
+  return guard([&] {
+    need(ptr != nullptr && bytes > 0, "host_alloc: bad arguments");
+    MDG_CUDA_CHECK(cudaHostAlloc(ptr, (size_t)bytes, cudaHostAllocPortable));
+  });
+}
+
+int mdg_host_free(void* ptr) {
+  return guard([&] {
+    if (ptr) MDG_CUDA_CHECK(cudaFreeHost(ptr));
   });
 }
 

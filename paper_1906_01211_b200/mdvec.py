@@ -22,11 +22,16 @@ LIB_PATH = os.environ.get("MDG_LIB", os.path.join(_HERE, "libmdg.so"))
 ROOT = os.path.dirname(_HERE)
 
 def _aos(x, y, z):
-    """(n, 3) view of three SoA component arrays (no copy when they are the
-    rows of one (3, n) block, as Engine._vec3 allocates them)."""
-    b = x.base
-    if b is not None and b.ndim == 2 and b.shape[0] == 3 and y.base is b and z.base is b:
-        return b.T
+    """(n, 3) view of three SoA component arrays: no copy when they are
+    consecutive rows of one (3, n) block (as Engine._vec3 and host_array
+    blocks are), else a stacked copy."""
+    n = len(x)
+    step = n * x.itemsize
+    if (n and x.dtype == y.dtype == z.dtype and x.flags.c_contiguous and y.flags.c_contiguous
+            and z.flags.c_contiguous and y.ctypes.data - x.ctypes.data == step
+            and z.ctypes.data - y.ctypes.data == step):
+        return np.lib.stride_tricks.as_strided(x, shape=(n, 3), strides=(x.itemsize, step),
+                                               writeable=True)
     return np.stack([x, y, z], 1)
 
 
@@ -139,6 +144,8 @@ SIGNATURES = {
     "mdg_timer_stop": (C.c_int, [C.c_void_p, _dp]),
     "mdg_probe_fp64_peak": (C.c_int, [C.c_int, _dp]),
     "mdg_probe_erfc": (C.c_int, [C.c_int, _dp, C.c_int64, _dp]),
+    "mdg_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64]),
+    "mdg_host_free": (C.c_int, [C.c_void_p]),
     "mdg_nlist_count_within": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, _i64p,
                                          _i64p]),
     "mdg_water_generate": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp,
@@ -535,8 +542,14 @@ class Engine:
     def amoeba_step(self, vdw: NeighborTable, elec: NeighborTable, p: AmoebaParams):
         check(self.lib.mdg_amoeba_step(self.ctx, vdw.list_id, elec.list_id, C.byref(p)))
 
-    def fetch_forces(self) -> np.ndarray:
-        fx, fy, fz = self._vec3()
+    def fetch_forces(self, out=None) -> np.ndarray:
+        """(n, 3) forces; `out` = an optional (3, n) float64 block (e.g. a
+        host_array, which is filled by DMA without a staging copy)."""
+        if out is None:
+            fx, fy, fz = self._vec3()
+        else:
+            assert out.shape == (3, self.n) and out.dtype == np.float64 and out.flags.c_contiguous
+            fx, fy, fz = out[0], out[1], out[2]
         check(self.lib.mdg_fetch_forces(self.ctx, _p(fx), _p(fy), _p(fz)))
         return _aos(fx, fy, fz)
 
@@ -618,6 +631,31 @@ def fp64_peak_tflops(device: int = 0) -> float:
     v = C.c_double()
     check(load_library().mdg_probe_fp64_peak(device, C.byref(v)))
     return v.value
+
+
+class _Pinned:
+    """Owner of one page-locked allocation (freed with the last view)."""
+
+    def __init__(self, nbytes: int):
+        self.lib = load_library()
+        self.ptr = C.c_void_p()
+        check(self.lib.mdg_host_alloc(C.byref(self.ptr), nbytes))
+
+    def __del__(self):
+        if self.ptr:
+            self.lib.mdg_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def host_array(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (mdg_host_alloc): per-step
+    coordinates / results kept here are DMA'd without a staging copy."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape))
+    owner = _Pinned(max(1, n * dt.itemsize))
+    buf = (C.c_char * max(1, n * dt.itemsize)).from_address(owner.ptr.value)
+    buf._owner = owner  # the array's base keeps the allocation alive
+    return np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
 
 
 def device_erfc(x, device: int = 0) -> np.ndarray:
