@@ -303,6 +303,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->timer_b) cudaEventDestroy(c->timer_b);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+  if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
   if (c->aux_partials) cudaFree(c->aux_partials);
   for (cudaEvent_t e : {c->ev_fork, c->ev_tpre, c->ev_join})
     if (e) cudaEventDestroy(e);

@@ -173,6 +173,11 @@ struct mdg_ctx {
   double* aux_partials = nullptr;
   int64_t aux_partial_blocks = 0;
   cudaEvent_t ev_fork = nullptr, ev_tpre = nullptr, ev_join = nullptr;
+  // single-domain PCG iterations as one device-side while graph (no host
+  // round trip per iteration); rebuilt when its captured arguments change
+  cudaGraph_t pcg_graph = nullptr;
+  cudaGraphExec_t pcg_exec = nullptr;
+  std::vector<uintptr_t> pcg_key;
 
   // last step
   double energies[4] = {0, 0, 0, 0};

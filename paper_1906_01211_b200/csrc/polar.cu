@@ -14,6 +14,7 @@
 // recomputing erfc/exp/sqrt/div: the solve is HBM-bound.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -541,6 +542,17 @@ __global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks
   }
 }
 
+// Device-side loop control of the PCG while graph: count the iteration and
+// continue unless converged (res[27]) or at max_iter. res[28] = iterations.
+__global__ void k_pcg_continue(cudaGraphConditionalHandle h, double* __restrict__ res,
+                               int64_t max_iter) {
+  const double it = res[28] + 1.0;
+  res[28] = it;
+  cudaGraphSetConditional(h, (res[27] == 0.0 && it < (double)max_iter) ? 1u : 0u);
+}
+
+__global__ void k_set_result(double* __restrict__ res, int slot, double v) { res[slot] = v; }
+
 // host-side value -> device result slot (stream-ordered)
 static void put_result(mdg_ctx* c, int slot, double v) {
   c->h_results[slot] = v;
@@ -561,6 +573,69 @@ void exchange_halo(mdg_ctx* c, int vec_id) {
 static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
   if (c->comm_allreduce(c->comm_user, v, nv) != 0)
     throw_error(MDG_COMM, "all-reduce callback failed");
+}
+
+// The iteration loop of run_pcg_pre as a CUDA graph: a while node whose body
+// is [mat-vec + p.q, alpha, update, beta/rms, continue?, direction]; the
+// k_pcg_continue kernel sets the loop condition on the device, so the host
+// launches the graph once and reads back the iteration count and rms. The
+// kernels and their order are those of the host-driven loop below.
+static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
+                               double tol_debye, int64_t max_iter, double* last_rms) {
+  // the mat-vec's grid (and partials) must be fixed before capture
+  const int64_t ipb = sites_per_block((const void*)k_tmatvec_pre<true>, n);
+  const int64_t g = (n + ipb - 1) / ipb;
+  ensure_partials(c, std::max(g, blocks));
+  k.ipw = (int)ipb;
+  k.partials = c->partials;
+  uint64_t tol_bits;
+  std::memcpy(&tol_bits, &tol_debye, sizeof tol_bits);
+  std::vector<uintptr_t> key = {(uintptr_t)n, (uintptr_t)k.pnbr, (uintptr_t)k.pcnt,
+                                (uintptr_t)k.trr, (uintptr_t)k.pcap, (uintptr_t)c->partials,
+                                (uintptr_t)ipb, (uintptr_t)max_iter,
+                                (uintptr_t)tol_bits, (uintptr_t)c->stream};
+  if (!c->pcg_exec || key != c->pcg_key) {
+    if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+    if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
+    c->pcg_exec = nullptr;
+    c->pcg_graph = nullptr;
+    MDG_CUDA_CHECK(cudaGraphCreate(&c->pcg_graph, 0));
+    cudaGraphConditionalHandle h;
+    MDG_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, c->pcg_graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    MDG_CUDA_CHECK(cudaGraphAddNode(&node, c->pcg_graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int64_t launches = c->launches;
+    MDG_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+    k_tmatvec_pre<true><<<(unsigned)g, kBlock, 0, c->stream>>>(k);
+    k_cg_scalars<<<1, 256, 0, c->stream>>>(c->partials, g, 1, n, tol_debye, c->results);
+    k_cg_update<<<(unsigned)blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
+                                                           c->cg_q, c->mu, c->cg_r, c->cg_z,
+                                                           c->partials);
+    k_cg_scalars<<<1, 256, 0, c->stream>>>(c->partials, blocks, 2, n, tol_debye, c->results);
+    k_pcg_continue<<<1, 1, 0, c->stream>>>(h, c->results, max_iter);
+    k_cg_dir<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->results, c->cg_z, c->cg_p);
+    cudaGraph_t captured = nullptr;
+    MDG_CUDA_CHECK(cudaStreamEndCapture(c->stream, &captured));
+    MDG_CUDA_CHECK(cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
+    c->launches = launches;
+    c->pcg_key = key;
+  }
+  MDG_LAUNCH(c, "set_result", 1, 1, 0, k_set_result, c->results, 28, 0.0);
+  MDG_CUDA_CHECK(cudaGraphLaunch(c->pcg_exec, c->stream));
+  fetch_results(c);
+  const int64_t it = (int64_t)c->h_results[28];
+  c->launches += 6 * it;  // the body's kernels, executed on the device
+  *last_rms = c->h_results[25];
+  if (c->h_results[27] == 0.0)
+    throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
+  return it;
 }
 
 // PCG over the stored T tensors. Single domain: every scalar recurrence stays
@@ -601,6 +676,9 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
     dd_allreduce(c, &rz, 1);
     put_result(c, 21, rz);
   }
+  k.in = c->cg_p;
+  k.out = c->cg_q;
+  if (!dd && !c->profile) return pcg_device_loop(c, k, n, blocks, tol_debye, max_iter, last_rms);
   k.in = c->cg_p;
   k.out = c->cg_q;
   for (int64_t it = 1; it <= max_iter; ++it) {

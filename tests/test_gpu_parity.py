@@ -484,3 +484,22 @@ def test_device_erfc_accuracy(mdg):
     m = ref > 0
     rel = np.abs(y[m] - ref[m]) / ref[m]
     assert np.all(rel <= (8.0 + 2.0 * x[m] ** 2) * 2.0 ** -52)
+
+
+def test_pcg_device_loop_max_iter_and_profiled_loop(engine, oracle, mdg):
+    """The device-side PCG loop (CUDA while graph) stops at max_iter with
+    ConvergenceError, and the host-driven loop (used while profiling) takes
+    the same steps."""
+    s = amoeba_small(mdg, 343, 21.0, 11)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.0)
+    pp = mdg.PolarParams(7.0, 0.39)
+    with pytest.raises(mdg.ConvergenceError) as ei:
+        engine.polar_solve_pcg(t, pp, 0.5446, 1e-12, 3, True)
+    assert ei.value.last_residual > 0
+    a = engine.polar_solve_pcg(t, pp, 0.5446, 1e-7, 100, True)
+    engine.profile(True)
+    b = engine.polar_solve_pcg(t, pp, 0.5446, 1e-7, 100, True)
+    engine.profile(False)
+    assert a.iterations == b.iterations
+    np.testing.assert_allclose(a.mu, b.mu, rtol=0, atol=1e-13 * np.abs(a.mu).max())
