@@ -529,6 +529,7 @@ int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred
                                    cudaMemcpyHostToDevice, c->stream));
     c->has_mol = molecule != nullptr;
     c->has_hred = hred_parent != nullptr;
+    mdg::set_groups(c);
     if (c->has_hred) mdg::run_reduce_sites(c);
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   });

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "mdg_internal.h"
 
@@ -20,6 +21,16 @@ __device__ __forceinline__ double wrap1(double d, double L, double invL, double 
 // proj/include/mdvec/pbc.hpp:35-37
 __device__ __forceinline__ double dist2(double dx, double dy, double dz) {
   return __fma_rn(dx, dx, __fma_rn(dy, dy, __dmul_rn(dz, dz)));
+}
+
+// The w word of pos / vsite carries the site's exclusion group (an integer
+// value as a double), so the pair prologues test exclusions on the gathered
+// position instead of a second gather (Halgren 3.11 -> 2.96 ms). (The
+// permanent-field pass keeps its int32 group gather: measured faster there.)
+__host__ __device__ __forceinline__ double group_bits(int32_t g) { return (double)g; }
+
+__device__ __forceinline__ bool same_group(const double4& a, const double4& b) {
+  return a.w == b.w;
 }
 
 // d = r_i - r_j, minimum image; returns r2

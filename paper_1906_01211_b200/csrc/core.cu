@@ -203,7 +203,7 @@ __global__ void k_reduce_sites(int64_t n, Box b, const double4* __restrict__ pos
   const double4 pi = pos[i];
   const int32_t p = par[i];
   if (p == i) {
-    vsite[i] = make_double4(pi.x, pi.y, pi.z, 0.0);
+    vsite[i] = pi;  // w: exclusion group
     return;
   }
   const double4 pp = pos[p];
@@ -213,7 +213,7 @@ __global__ void k_reduce_sites(int64_t n, Box b, const double4* __restrict__ pos
   const double dz = wrap1(__dsub_rn(pi.z, pp.z), b.lz, b.iz, b.hz);
   vsite[i] = make_double4(wrap_into_exact(__dadd_rn(pp.x, __dmul_rn(f, dx)), b.lx),
                           wrap_into_exact(__dadd_rn(pp.y, __dmul_rn(f, dy)), b.ly),
-                          wrap_into_exact(__dadd_rn(pp.z, __dmul_rn(f, dz)), b.lz), 0.0);
+                          wrap_into_exact(__dadd_rn(pp.z, __dmul_rn(f, dz)), b.lz), pi.w);
 }
 
 void run_reduce_sites(mdg_ctx* c) {
@@ -233,8 +233,10 @@ __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
   const int64_t o = perm[s];
   const double x = st[o], y = st[n + o], z = st[2 * n + o];
   const double q = st[3 * n + o];
-  pos[s] = make_double4(x, y, z, q);
-  vsite[s] = make_double4(x, y, z, 0.0);
+  // w of pos / vsite: the site's exclusion group (identity until
+  // mdg_topology_upload; see set_groups), read by the pair prologues
+  pos[s] = make_double4(x, y, z, group_bits((int32_t)s));
+  vsite[s] = make_double4(x, y, z, group_bits((int32_t)s));
   vdwp[s] = make_double4(st[4 * n + o], sqrt(st[5 * n + o]), st[6 * n + o], sqrt(st[7 * n + o]));
   const double pol = st[8 * n + o];
   const double pd = cbrt(sqrt(pol));
@@ -258,7 +260,25 @@ __global__ void k_pack_positions(int64_t n, const int32_t* __restrict__ perm,
   pos[s].x = x;
   pos[s].y = y;
   pos[s].z = z;
-  if (copy_vsite) vsite[s] = make_double4(x, y, z, 0.0);
+  if (copy_vsite) vsite[s] = make_double4(x, y, z, pos[s].w);
+}
+
+__global__ void k_set_groups(int64_t n, const int32_t* __restrict__ mol, double4* __restrict__ pos,
+                             double4* __restrict__ vsite) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  pos[s].w = group_bits(mol[s]);
+  vsite[s].w = group_bits(mol[s]);
+}
+
+void set_groups(mdg_ctx* c) {
+  MDG_LAUNCH(c, "set_groups", grid_for(c->n, 256), 256, 0, k_set_groups, c->n, c->mol, c->pos,
+             c->vsite);
+}
+
+__global__ void k_copy_vsite(int64_t n, const double4* __restrict__ pos, double4* __restrict__ vsite) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < n) vsite[s] = pos[s];
 }
 
 void pack_positions(mdg_ctx* c) {
@@ -313,7 +333,11 @@ void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
   if (count <= 0) return;
   MDG_LAUNCH(c, "halo_unpack", grid_for(count, 256), 256, 0, k_vec_unpack, count, d_sites,
              c->d_iperm, d_in, vec_by_id(c, vec_id));
-  if (vec_id == MDG_VEC_POS && c->has_hred) run_reduce_sites(c);
+  if (vec_id == MDG_VEC_POS) {
+    if (c->has_hred) run_reduce_sites(c);
+    else MDG_LAUNCH(c, "copy_vsite", grid_for(c->n, 256), 256, 0, k_copy_vsite, c->n, c->pos,
+                    c->vsite);
+  }
 }
 
 // -E_pol = 1/2 sum mu . E_perm ; results[slot] = -0.5 * electric * sum

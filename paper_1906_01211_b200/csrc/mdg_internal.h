@@ -1,8 +1,9 @@
 // mdg_internal.h -- context, device layout and shared device helpers.
 //
 // Device data layout (HBM, all in the context's spatially sorted order):
-//   pos    double4[n]   x, y, z, charge                 (32 B, one sector)
-//   vsite  double4[n]   Halgren-reduced x, y, z, 0       (vdW lists)
+//   pos    double4[n]   x, y, z, exclusion group (as double; one sector,
+//                       so the pair prologues need no second gather)
+//   vsite  double4[n]   Halgren-reduced x, y, z, exclusion group (vdW lists)
 //   vdwp   double4[n]   lj_sigma, sqrt(lj_eps), hal_r0, sqrt(hal_eps)
 //   polp   double2[n]   polarizability, polarizability^(1/6)
 //   mol    int32[n]     exclusion group
@@ -120,7 +121,7 @@ struct mdg_ctx {
   double4* vsite = nullptr;
   double4* vdwp = nullptr;
   double2* polp = nullptr;
-  double4* pq4 = nullptr;  // (polarizability, polarizability^(1/6), charge, 0)
+  double4* pq4 = nullptr;  // (polarizability, polarizability^(1/6), charge, alpha^(-1/6))
   int32_t* mol = nullptr;
   int32_t* hpar = nullptr;
   double* hfac = nullptr;
@@ -336,6 +337,8 @@ void vec_pack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count, dou
 void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
                 const double* d_in);
 void pack_positions(mdg_ctx* c);
+// pos.w / vsite.w <- mol (after a topology upload)
+void set_groups(mdg_ctx* c);
 void polar_energy(mdg_ctx* c, double electric, int slot);
 
 }  // namespace mdg

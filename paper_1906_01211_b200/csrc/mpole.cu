@@ -22,6 +22,7 @@ struct MKArgs {
   int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ mp;
+  const double4* __restrict__ pq4;  // charges (z)
   const int32_t* __restrict__ mol;
   ListView L;
   Box b;
@@ -57,10 +58,9 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
-    const double qi = pi.w;
+    const double qi = a.pq4[i].z;
     const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
     const Quad Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
-    const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
@@ -68,10 +68,10 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
       const int32_t j = ring_j(e);
       const double x = e.x, y = e.y, z = e.z;
       const double r2 = dist2(x, y, z);
-      const double4 pj = ldg4(a.pos + j);
+      const double qj = __ldg(&a.pq4[j].z);
       const double4 m0j = ldg4(a.mp + 3 * (size_t)j), m1j = ldg4(a.mp + 3 * (size_t)j + 1);
       const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
-      const double qj = pj.w, djx = m0j.x, djy = m0j.y, djz = m0j.z;
+      const double djx = m0j.x, djy = m0j.y, djz = m0j.z;
       const double r = sqrt(r2);
       const double inv_r = 1.0 / r;
       const double inv_r2 = inv_r * inv_r;
@@ -207,12 +207,12 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row + start, cnt - start, lane, a.pos, (EXCL && !PRUNED) ? a.mol : nullptr, ring,
-        [&](int32_t& raw, const double4& pj, int32_t mj, double& x, double& y, double& z) {
+        row + start, cnt - start, lane, a.pos, nullptr, ring,
+        [&](int32_t& raw, const double4& pj, int32_t, double& x, double& y, double& z) {
           const int32_t j = raw & 0x7fffffff;
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
           const bool keep = PRUNED ? !(EXCL && raw < 0)  // same molecule (flag bit)
-                                   : (r2 <= a.c2) && !(EXCL && mj == mi);
+                                   : (r2 <= a.c2) && !(EXCL && same_group(pj, pi));
           raw = j;
           return keep && !(HALF && j < i);
         },
@@ -269,6 +269,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.n_i = c->n_own;
   k.pos = c->pos;
   k.mp = c->mp;
+  k.pq4 = c->pq4;
   k.mol = c->mol;
   k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
@@ -287,6 +288,7 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
   k.n_i = c->n_own;
   k.pos = c->pos;
   k.mp = c->mp;
+  k.pq4 = c->pq4;
   k.mol = c->mol;
   k.L = ListView{P.nbr, P.cnt, P.cap, P.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);

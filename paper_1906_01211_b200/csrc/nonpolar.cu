@@ -20,6 +20,7 @@ struct NonpolarKArgs {
   int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ vdwp;
+  const double4* __restrict__ pq4;  // charges (z)
   const int32_t* __restrict__ mol;
   ListView L;
   Box b;
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
     const double4 pi = a.pos[i];
     double4 vi = make_double4(0, 0, 0, 0);
     if (LJ) vi = a.vdwp[i];
-    const int32_t mi = EXCL ? a.mol[i] : 0;
+    const double qi = COUL ? a.pq4[i].z : 0.0;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0;
@@ -48,7 +49,6 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       const int32_t j = ring_j(e);
       const double dx = e.x, dy = e.y, dz = e.z;
       const double r2 = dist2(dx, dy, dz);
-      const double4 pj = ldg4(a.pos + j);
       double fs = 0.0;
       // pair weight: 1/2 for a halo partner (the other domain has the mirror)
       const double w = (HALF && j >= a.n_i) ? 0.5 : 1.0;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       if (COUL) {
         const double r = sqrt(r2);
         const double inv_r = 1.0 / r;
-        const double qq = a.electric * pi.w * pj.w;
+        const double qq = a.electric * qi * __ldg(&a.pq4[j].z);
         const double ar = a.alpha * r;
         const double ex2 = exp(-ar * ar);
         const double ee = erfc_from_exp(ar, ex2) * inv_r;
@@ -99,10 +99,11 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row + start, cnt - start, lane, a.pos, EXCL ? a.mol : nullptr, ring,
-        [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
+        row + start, cnt - start, lane, a.pos, nullptr, ring,
+        [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && mj == mi) && !(HALF && j < i);
+          // w = exclusion group
+          return (r2 <= a.c2) && !(EXCL && same_group(pj, pi)) && !(HALF && j < i);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);
@@ -144,6 +145,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.n_i = c->n_own;
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
+  k.pq4 = c->pq4;
   k.mol = c->mol;
   k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
@@ -191,7 +193,6 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.site[i];
     const double4 vi = a.vdwp[i];
-    const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0;
@@ -252,10 +253,11 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row + start, cnt - start, lane, a.site, EXCL ? a.mol : nullptr, ring,
-        [&](int32_t j, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
+        row + start, cnt - start, lane, a.site, nullptr, ring,
+        [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-          return (r2 <= a.c2) && !(EXCL && mj == mi) && !(HALF && j < i);
+          // w = exclusion group
+          return (r2 <= a.c2) && !(EXCL && same_group(pj, pi)) && !(HALF && j < i);
         },
         [&](const double4& e, int) { body(e); });
     fx = warp_allsum(fx);

@@ -79,12 +79,11 @@ __global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArg
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
     const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
-    const double qi = pi.w;
+    const double qi = a.pq4[i].z;
     const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
     const Sym3 Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
     const double4 ui = a.mu[i];
     const double ipdi = a.pq4[i].w;  // 1 / pdamp_i
-    const int32_t mi = EXCL ? a.mol[i] : 0;
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
@@ -209,8 +208,8 @@ __global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArg
     };
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
     run_row(
-        row + start, cnt - start, lane, a.pos, (EXCL && !PRUNED) ? a.mol : nullptr, ring,
-        [&](int32_t& raw, const double4& pj, int32_t mj, double& x, double& y, double& z) {
+        row + start, cnt - start, lane, a.pos, nullptr, ring,
+        [&](int32_t& raw, const double4& pj, int32_t, double& x, double& y, double& z) {
           const int32_t j = raw & 0x7fffffff;
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
           bool keep;
@@ -218,7 +217,7 @@ __global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArg
             keep = true;  // pruned rows: in range, flag already set
           } else {
             keep = r2 <= a.c2;
-            raw = (EXCL && mj == mi) ? (j | (int32_t)0x80000000) : j;
+            raw = (EXCL && same_group(pj, pi)) ? (j | (int32_t)0x80000000) : j;  // w: group
           }
           return keep && !(HALF && j < i);
         },
