@@ -117,7 +117,14 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
     Grid g, const int32_t* __restrict__ start, const int32_t* __restrict__ atoms, Box b,
     double c2, int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
     const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
-  const int lane = threadIdx.x & 31;
+  // per warp: the site's candidate runs (contiguous ranges of the cell-sorted
+  // site array) and their exclusive prefix lengths
+  constexpr int kMaxRuns = kSpan * kSpan * 2;  // <= 64: two per lane
+  static_assert(kMaxRuns <= 64, "candidate runs: two per lane");
+  __shared__ int32_t run_s[kWarps][64], run_p[kWarps][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* rs = run_s[warp];
+  int32_t* rp = run_p[warp];
   MDG_SITE_LOOP(i, n_i, ipw) {
     const double4 pi = P[i];
     const int c = cell_of[i];
@@ -125,44 +132,77 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
     int xs[kSpan], ys[kSpan], zlo[2], zhi[2];
     const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
               nz = axis_runs(cz, g.ncz, zlo, zhi);
+    const int nruns = nx * ny * nz;
+    // runs in the same (x, y, z-run) order as the cell walk; lane r takes run
+    // r and r + 32, then a warp scan of the lengths
+    int len0 = 0, len1 = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      int len = 0;
+      if (r < nruns) {
+        const int q = r % nz, ab = r / nz;
+        const int col = (xs[ab / ny] * g.ncy + ys[ab % ny]) * g.ncz;
+        const int32_t s0 = start[col + zlo[q]];
+        rs[r] = s0;
+        len = start[col + zhi[q] + 1] - s0;
+      }
+      if (h == 0) len0 = len; else len1 = len;
+    }
+    int inc0 = len0, inc1 = len1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(0xffffffffu, inc0, o);
+      const int t1 = __shfl_up_sync(0xffffffffu, inc1, o);
+      if (lane >= o) { inc0 += t0; inc1 += t1; }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+    rp[lane] = inc0 - len0;
+    rp[lane + 32] = tot0 + inc1 - len1;
+    const int total = tot0 + __shfl_sync(0xffffffffu, inc1, 31);
+    __syncwarp();
+    // virtual candidate index v -> site-array slot (run by binary search)
+    auto slot_of = [&](int v) {
+      int lo = 0, hi = nruns - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= v) lo = mid; else hi = mid - 1;
+      }
+      return rs[lo] + (v - rp[lo]);
+    };
     int32_t* out = nbr + (size_t)i * (size_t)cap;
     int32_t k = 0;  // warp-uniform row length
-    // reference capacity rule: the half list stores a pair on the lower
-    // caller index and caps it at kMaxNeighbors (proj/src/neighbors_vec.cpp:80-83)
-    const int32_t oi = perm[i];
-    int32_t upper = 0;
-    for (int a = 0; a < nx; ++a)
-      for (int bb = 0; bb < ny; ++bb)
-        for (int q = 0; q < nz; ++q) {
-          const int col = (xs[a] * g.ncy + ys[bb]) * g.ncz;
-          const int32_t e = start[col + zhi[q] + 1];
-          for (int32_t s0 = start[col + zlo[q]]; s0 < e; s0 += 32) {
-            const int32_t s = s0 + lane;
-            bool in = false;
-            int32_t j = 0;
-            if (s < e) {
-              j = __ldg(atoms + s);
-              if (j != (int32_t)i) {
-                const double4 pj = ldg4(P + j);
-                double dx, dy, dz;
-                const double r2 = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-                in = (r2 <= c2);
-              }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, in);
-            if (in) {
-              const int32_t pos = k + __popc(m & lanemask_lt());
-              if (pos < cap) out[pos] = j;
-              upper += (__ldg(perm + j) > oi) ? 1 : 0;
-            }
-            k += __popc(m);
-          }
-        }
-    upper = warp_allsum_i(upper);
-    if (lane == 0) {
-      cnt[i] = k;
-      if (upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+    // software pipeline: candidate indices one chunk ahead of the test
+    int32_t ja = (lane < total) ? __ldg(atoms + slot_of(lane)) : (int32_t)i;
+    for (int base = 0; base < total; base += 32) {
+      const int vn = base + 32 + lane;
+      const int32_t jb = (vn < total) ? __ldg(atoms + slot_of(vn)) : (int32_t)i;
+      bool in = false;
+      if (ja != (int32_t)i) {
+        const double4 pj = ldg4(P + ja);
+        double dx, dy, dz;
+        in = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= c2;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int32_t pos = k + __popc(m & lanemask_lt());
+        if (pos < cap) out[pos] = ja;
+      }
+      k += __popc(m);
+      ja = jb;
     }
+    __syncwarp();
+    if (lane == 0) cnt[i] = k;
+    // reference capacity rule: the half list stores a pair on the lower
+    // caller index and caps it at kMaxNeighbors (proj/src/neighbors_vec.cpp:80-83).
+    // Only a row longer than the cap can break it: count its upper pairs.
+    if (k > MDG_MAX_NEIGHBORS && k <= cap) {
+      const int32_t oi = perm[i];
+      int32_t upper = 0;
+      for (int e = lane; e < k; e += 32) upper += (__ldg(perm + out[e]) > oi) ? 1 : 0;
+      upper = warp_allsum_i(upper);
+      if (lane == 0 && upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+    }  // (k > cap: the host retries with the true maximum, then counts)
   }
 }
 
