@@ -503,3 +503,38 @@ def test_pcg_device_loop_max_iter_and_profiled_loop(engine, oracle, mdg):
     engine.profile(False)
     assert a.iterations == b.iterations
     np.testing.assert_allclose(a.mu, b.mu, rtol=0, atol=1e-13 * np.abs(a.mu).max())
+
+
+def test_config4_full_size_properties(mdg):
+    """BASELINE config 4 at full size (999,999 atoms), through size-independent
+    properties: the 9 A list's pair count equals a KD-tree count, pair forces
+    sum to zero, the default (half-row, atomic) and deterministic (full-row)
+    modes agree, the PCG converges in the oracle's iteration count range."""
+    from scipy.spatial import cKDTree
+    s = mdg.water_box(333333, 215.3, 1, "amoeba")
+    n = s.n_sites
+    with mdg.Engine(n) as e:
+        e.upload_system(s)
+        te = e.build_neighbor_table(9.0, list_id=0)
+        tv = e.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+        # pair count of the atomic 9 A list vs a periodic KD-tree
+        pos = np.stack([s.x, s.y, s.z], 1)
+        tree = cKDTree(pos, boxsize=215.3)
+        half = (tree.count_neighbors(tree, 9.0) - n) // 2
+        assert e.table_size(te)[0] == half
+        p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1,
+                             mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE)
+        out = []
+        for det in (False, True):
+            e.set_deterministic(det)
+            e.amoeba_step(tv, te, p)
+            en, w, it, rms = e.fetch_energies()
+            out.append((en, w, it, rms, e.fetch_forces().copy(), e.fetch_torques().copy()))
+        e.set_deterministic(False)
+    (en0, w0, it0, rms0, f0, t0), (en1, w1, it1, rms1, f1, t1) = out
+    frms = np.sqrt(np.mean(f0 ** 2))
+    assert np.abs(f0.sum(0)).max() <= 1e-9 * frms * np.sqrt(n)
+    assert np.abs(f0 - f1).max() <= 1e-8 * frms
+    assert np.abs(t0 - t1).max() <= 1e-8 * np.sqrt(np.mean(t1 ** 2))
+    np.testing.assert_allclose(en0[:3], en1[:3], rtol=1e-9)
+    assert 6 <= it0 <= 12 and abs(it0 - it1) <= 1 and rms0 < 1e-5
