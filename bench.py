@@ -471,6 +471,37 @@ def run_dd(args, world, rank, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     en, w, iters, rms = eng.energies()
+
+    # ---- end to end through the public DD API: every step each rank uploads
+    # its owned coordinates (H2D) and refreshes its halo by exchange, and
+    # reads back its owned forces (D2H) and the all-reduced energies
+    e2e = None
+    if not args.no_e2e:
+        x, y, z = np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)
+        for _ in range(2):
+            eng.update_positions(x, y, z)
+            step(tables)
+            eng.owned_forces()
+        tables = eng.build_lists(lists)
+        dist.barrier()
+        eng.eng.synchronize()
+        t0 = time.perf_counter()
+        eng.eng.timer_start()
+        for k in range(args.steps):
+            eng.update_positions(x, y, z)
+            if k % REBUILD_EVERY == 0:
+                tables = eng.build_lists(lists)
+            step(tables)
+            _, f = eng.owned_forces()
+            eng.energies()
+        e_ms = max(eng.eng.timer_stop(), (time.perf_counter() - t0) * 1e3)
+        t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": eng.n_global * args.steps / (e_ms * 1e-3), "unit": "atom-steps/s",
+               "h2d_bytes_per_step": 24 * eng.n_global,
+               "d2h_bytes_per_step": 24 * eng.n_global + 8 * (4 + 9) * world,
+               "ms_per_step": e_ms / args.steps}
     out = {
         "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
         "value": eng.n_global * args.steps / (ms * 1e-3),
@@ -492,7 +523,7 @@ def run_dd(args, world, rank, local):
                    "owned_sites_rank0": plans[0].n_owned,
                    "halo_sites_rank0": int(len(plans[0].halo)),
                    "l2": "inputs larger than L2 (lists > 126 MB)"},
-        "e2e": None,
+        "e2e": e2e,
         "gpu_launches": launches,
         "roofline": None,
         "clocks": clk.summary(),

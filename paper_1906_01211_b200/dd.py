@@ -5,9 +5,11 @@ grid (1x1x1, 2x1x1, 2x2x1, 2x2x2, ...); a rank OWNS the molecules whose anchor
 site (the first site of the molecule, the water oxygen) lies in its slab, so
 exclusions and the Halgren reduction parent stay local. Its HALO is every
 other molecule with a site within `halo_width` (list cutoff + intramolecular
-extent) of the slab, periodic images included. With full (both-direction)
-neighbour lists each rank computes complete forces, fields and dipoles for
-its owned sites from owned + halo data: there is no force return. Per step
+extent) of the slab, periodic images included. Each rank evaluates the rows
+of its owned sites (owned-owned pairs once with atomic partner updates, pairs
+with a halo partner in the owned row only, energy weight 1/2), so its owned
+forces, fields and dipoles are complete from owned + halo data: there is no
+force return. Per step
 the halo coordinates are refreshed; inside the PCG solve the halo of mu (once)
 and of the search direction p (every iteration) is exchanged and the CG
 scalars are all-reduced (mdg_set_comm hooks, called from the C++ solver), so
