@@ -87,6 +87,16 @@ int mdg_topology_upload(mdg_ctx* ctx, const int32_t* molecule, const int32_t* hr
  * site), quadrupole[6n] traceless (xx,xy,xz,yy,yz,zz per site, Tinker's
  * convention: Theta/3). NULL zeroes the term. Charges come from the system. */
 int mdg_multipoles_upload(mdg_ctx* ctx, const double* dipole, const double* quadrupole);
+/* Local multipole frames (Tinker conventions): per site
+ * frame_type 0 = none (multipoles global), 1 = z-then-x, 2 = bisector, with
+ * zatom / xatom the caller-order frame atoms (same molecule). dipole[3n] and
+ * quadrupole[6n] are then given in the local frame; every multipole entry
+ * point rotates them to the global frame at the current positions, and the
+ * multipole / polarization torques are turned into forces on the frame atoms
+ * (included in the returned forces; torques are still reported). NULL
+ * frame_type removes the frames. */
+int mdg_frames_upload(mdg_ctx* ctx, const int32_t* frame_type, const int32_t* zatom,
+                      const int32_t* xatom, const double* dipole, const double* quadrupole);
 
 /* ---- neighbour lists ---------------------------------------------------- */
 /* Replaces build_cell_grid + build_neighbor_table

@@ -278,7 +278,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
-                  c->child_start, c->child, c->mp, c->cell_of, c->cell_start, c->cell_fill,
+                  c->child_start, c->child, c->mp, c->frame, c->mploc, c->fbuf, c->fref_start,
+                  c->fref, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
                   c->results,
@@ -360,7 +361,7 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
     c->ly = ly;
     c->lz = lz;
     for (auto& Lst : c->lists) Lst.valid = false;
-    c->has_mpoles = c->has_hred = c->has_mol = false;
+    c->has_mpoles = c->has_hred = c->has_mol = c->has_frames = false;
     spatial_sort(c, x, y, z);
     stage_in(c, {x, y, z, charge, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, polarizability});
     mdg::pack_system(c);
@@ -535,6 +536,81 @@ int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred
   });
 }
 
+int mdg_frames_upload(mdg_ctx* c, const int32_t* frame_type, const int32_t* zatom,
+                      const int32_t* xatom, const double* dipole, const double* quadrupole) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    const int64_t n = c->n;
+    if (!frame_type) {
+      c->has_frames = false;
+      return;
+    }
+    need(zatom && xatom, "frames: zatom and xatom are required");
+    std::vector<int32_t> fr(4 * n, 0);
+    std::vector<int32_t> cnt(n + 1, 0);
+    bool any = false;
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t o = c->perm[s];
+      const int32_t t = frame_type[o];
+      need(t >= 0 && t <= 2, "frames: frame type must be 0, 1 or 2");
+      if (t == 0) continue;
+      const int32_t zo = zatom[o], xo = xatom[o];
+      need(zo >= 0 && zo < n && xo >= 0 && xo < n && zo != o && xo != o && zo != xo,
+           "frames: zatom / xatom must be two other sites");
+      fr[4 * s] = t;
+      fr[4 * s + 1] = c->iperm[zo];
+      fr[4 * s + 2] = c->iperm[xo];
+      any = true;
+      // references that the owned gather can collect: owned site -> owned atom
+      if (s < c->n_own) {
+        if (fr[4 * s + 1] < c->n_own) ++cnt[fr[4 * s + 1] + 1];
+        if (fr[4 * s + 2] < c->n_own) ++cnt[fr[4 * s + 2] + 1];
+      }
+    }
+    for (int64_t a = 0; a < n; ++a) cnt[a + 1] += cnt[a];
+    std::vector<int32_t> ref(std::max<int32_t>(cnt[n], 1)), fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t s = 0; s < c->n_own; ++s) {
+      if (fr[4 * s] == 0) continue;
+      for (int role = 0; role < 2; ++role) {
+        const int32_t a = fr[4 * s + 1 + role];
+        if (a < c->n_own) ref[fill[a]++] = (int32_t)(2 * s + role);
+      }
+    }
+    std::vector<double> ml(12 * n, 0.0);
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t o = c->perm[s];
+      double* m = &ml[12 * s];
+      if (dipole)
+        for (int k = 0; k < 3; ++k) m[k] = dipole[3 * o + k];
+      if (quadrupole)
+        for (int k = 0; k < 6; ++k) m[3 + k] = quadrupole[6 * o + k];
+    }
+    if (!c->frame) {
+      MDG_CUDA_CHECK(cudaMalloc(&c->frame, (size_t)c->n_cap * sizeof(int4)));
+      MDG_CUDA_CHECK(cudaMalloc(&c->mploc, 3 * (size_t)c->n_cap * sizeof(double4)));
+      MDG_CUDA_CHECK(cudaMalloc(&c->fbuf, 3 * (size_t)c->n_cap * sizeof(double4)));
+      MDG_CUDA_CHECK(cudaMalloc(&c->fref_start, ((size_t)c->n_cap + 1) * sizeof(int32_t)));
+    }
+    if (c->fref) cudaFree(c->fref);
+    c->fref = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&c->fref, ref.size() * sizeof(int32_t)));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->frame, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice,
+                                   c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->mploc, ml.data(), ml.size() * 8, cudaMemcpyHostToDevice,
+                                   c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->fref_start, cnt.data(), cnt.size() * 4,
+                                   cudaMemcpyHostToDevice, c->stream));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->fref, ref.data(), ref.size() * 4, cudaMemcpyHostToDevice,
+                                   c->stream));
+    c->has_frames = true;  // (frame 0 sites copy their multipoles unrotated)
+    c->has_mpoles = true;
+    (void)any;
+    mdg::rotate_multipoles(c);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int mdg_multipoles_upload(mdg_ctx* c, const double* dipole, const double* quadrupole) {
   return guard([&] {
     need_system(c);
@@ -563,6 +639,7 @@ int mdg_multipoles_upload(mdg_ctx* c, const double* dipole, const double* quadru
                                    cudaMemcpyHostToDevice, c->stream));
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     c->has_mpoles = dipole != nullptr || quadrupole != nullptr;
+    c->has_frames = false;  // global-frame multipoles replace any local frames
   });
 }
 
@@ -775,6 +852,7 @@ int mdg_perm_field(mdg_ctx* c, int list_id, double alpha, double cutoff, double 
     need_kernel_cutoff(L, cutoff);
     need(alpha >= 0, "perm_field: alpha must be nonnegative");
     need(L.sites == MDG_SITES_ATOMIC, "perm_field needs a list over atomic sites");
+    mdg::rotate_multipoles(c);
     mdg::run_perm_field(c, list_id, alpha, cutoff, thole_a, exclude, c->field);
     vec_out(c, c->field, ex, ey, ez);
   });
@@ -791,6 +869,7 @@ int mdg_polar_solve_jacobi(mdg_ctx* c, int list_id, double cutoff, double thole_
     need(max_iter >= 1, "jacobi_polarization_solve: max_iter must be >= 1");
     mdg::DevList& L = need_list(c, list_id);
     need_kernel_cutoff(L, cutoff);
+    mdg::rotate_multipoles(c);
     mdg::run_perm_field(c, list_id, 0.0, cutoff, thole_a, 0, c->eperm);
     double resid = 0;
     try {
@@ -818,6 +897,7 @@ int mdg_polar_solve_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, do
     mdg::DevList& L = need_list(c, list_id);
     need_kernel_cutoff(L, cutoff);
     need(L.sites == MDG_SITES_ATOMIC, "pcg needs a list over atomic sites");
+    mdg::rotate_multipoles(c);
     mdg::run_field_tpre(c, list_id, alpha, cutoff, thole_a, exclude_perm);
     double rms = 0;
     try {
@@ -843,7 +923,9 @@ int mdg_mpole_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
     need_kernel_cutoff(L, cutoff);
     need(alpha >= 0, "mpole: alpha must be nonnegative");
     need(L.sites == MDG_SITES_ATOMIC, "mpole needs a list over atomic sites");
+    mdg::rotate_multipoles(c);
     mdg::run_mpole(c, list_id, alpha, cutoff, electric, exclude, false);
+    mdg::frame_torques_to_forces(c);
     vec_out(c, c->force, fx, fy, fz);
     vec_out(c, c->torque, tx, ty, tz);
     mdg::fetch_results(c);
@@ -866,7 +948,9 @@ int mdg_polar_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
     need((mux == nullptr) == (muy == nullptr) && (mux == nullptr) == (muz == nullptr),
          "polar_forces: give all three dipole components or none");
     if (mux) vec_in(c, mux, muy, muz, c->mu);
+    mdg::rotate_multipoles(c);
     mdg::run_polar_force(c, list_id, alpha, cutoff, thole_a, electric, exclude, false);
+    mdg::frame_torques_to_forces(c);
     vec_out(c, c->force, fx, fy, fz);
     vec_out(c, c->torque, tx, ty, tz);
     mdg::fetch_results(c);
@@ -918,6 +1002,7 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
          "amoeba_step: polarization forces need the polarization solve");
     MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
     c->has_polar_force = false;
+    mdg::rotate_multipoles(c);  // local frames at the current positions
     // Two independent chains: [aux] Halgren -> multipoles (after the pruned
     // rows exist) and [main] permanent field + T -> PCG. Joined before the
     // polarization forces, which add to the same force/torque arrays.
@@ -983,6 +1068,7 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
       mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
       c->has_polar_force = true;
     }
+    if ((terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
   });
 }
 

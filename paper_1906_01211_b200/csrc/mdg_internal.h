@@ -128,6 +128,15 @@ struct mdg_ctx {
   int32_t* child_start = nullptr;  // CSR of Halgren children per parent
   int32_t* child = nullptr;
   double4* mp = nullptr;
+  // local multipole frames (frames.cu): (type, zatom, xatom, 0) per site,
+  // local-frame multipoles (mp layout), per-site frame forces (i, z, x) and
+  // the CSR of frame references per atom (2 * site + role)
+  bool has_frames = false;
+  int4* frame = nullptr;
+  double4* mploc = nullptr;
+  double4* fbuf = nullptr;
+  int32_t* fref_start = nullptr;
+  int32_t* fref = nullptr;
 
   // cell grid scratch
   int32_t* cell_of = nullptr;
@@ -322,6 +331,10 @@ void run_polar_force(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
                      double electric, int exclude, bool accumulate);
 void run_polar_force_pruned(mdg_ctx* c, double alpha, double thole_a, double electric,
                             int exclude, bool accumulate);
+// local frames: mp <- R mploc (every entry point that reads multipoles) and
+// torque -> forces on the frame atoms (after the torque kernels)
+void rotate_multipoles(mdg_ctx* c);
+void frame_torques_to_forces(mdg_ctx* c);
 // multi-domain: refresh the halo entries of vec_id through the comm hook
 void exchange_halo(mdg_ctx* c, int vec_id);
 

@@ -135,6 +135,7 @@ SIGNATURES = {
                                           C.c_double, C.c_double, C.c_double] + [_dp] * 9),
     "mdg_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mdg_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_frames_upload": (C.c_int, [C.c_void_p, _ip, _ip, _ip, _dp, _dp]),
     "mdg_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_unpack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
@@ -597,6 +598,21 @@ class Engine:
         ms = C.c_double()
         check(self.lib.mdg_timer_stop(self.ctx, C.byref(ms)))
         return ms.value
+
+    def upload_frames(self, frame_type, zatom, xatom, dipole=None, quadrupole=None):
+        """Local multipole frames (mdg.h mdg_frames_upload): type 0 none,
+        1 z-then-x, 2 bisector; dipole (n, 3) / quadrupole (n, 6) in the
+        local frames. frame_type None removes the frames."""
+        if frame_type is None:
+            check(self.lib.mdg_frames_upload(self.ctx, None, None, None, None, None))
+            return
+        t = np.ascontiguousarray(frame_type, np.int32)
+        z = np.ascontiguousarray(zatom, np.int32)
+        x = np.ascontiguousarray(xatom, np.int32)
+        d = None if dipole is None else _f64(np.asarray(dipole).reshape(-1))
+        q = None if quadrupole is None else _f64(np.asarray(quadrupole).reshape(-1))
+        check(self.lib.mdg_frames_upload(self.ctx, _p(t, _ip), _p(z, _ip), _p(x, _ip), _p(d),
+                                         _p(q)))
 
     def set_deterministic(self, on: bool = True):
         """Full-row pair sums (bitwise reproducible forces/torques) instead of

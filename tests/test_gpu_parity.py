@@ -538,3 +538,34 @@ def test_config4_full_size_properties(mdg):
     assert np.abs(t0 - t1).max() <= 1e-8 * np.sqrt(np.mean(t1 ** 2))
     np.testing.assert_allclose(en0[:3], en1[:3], rtol=1e-9)
     assert 6 <= it0 <= 12 and abs(it0 - it1) <= 1 and rms0 < 1e-5
+
+
+def test_local_frames_match_oracle(engine, oracle, mdg):
+    """Local multipole frames (8(f)#2): rotation to the global frame and the
+    torque -> frame-atom forces vs oracle/frames.py (itself pinned by finite
+    differences); the permanent field and PCG see the rotated multipoles."""
+    from oracle import frames as fr
+    s = amoeba_small(mdg, 343, 21.0, 12)
+    so = to_oracle_system(s)
+    frame, za, xa = fr.water_frames(s.molecule)
+    dl, ql = np.asarray(s.dipole), np.asarray(s.quadrupole)  # taken as local values
+    pos = np.stack([s.x, s.y, s.z], 1)
+    so.dipole, so.quadrupole = fr.rotate(pos, s.box, frame, za, xa, dl, ql)
+    t_o = oracle.build_table(so, 9.0)
+    fo, to, eo, wo = oracle.mpole(so, t_o, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+    fo = fo + fr.torque_forces(pos, s.box, frame, za, xa, to)
+    engine.upload_system(s)
+    engine.upload_frames(frame, za, xa, dl, ql)
+    t = engine.build_neighbor_table(9.0)
+    f, tq, e, w = engine.mpole_forces(t, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+    assert rel(e, eo) <= E_TOL
+    assert force_err_rms(tq, to) <= F_TOL
+    assert force_err_rms(f, fo) <= F_TOL
+    # the field / solve use the rotated multipoles too
+    ep = oracle.perm_field_ewald(so, t_o, 0.5446, 7.0, 0.39, exclude=True)
+    st = engine.polar_solve_pcg(t, mdg.PolarParams(7.0, 0.39), 0.5446, 1e-5, 100, True)
+    assert force_err_rms(engine.fetch_perm_field(), ep) <= F_TOL
+    mu_o, it_o, _ = oracle.pcg(so, t_o, 0.5446, 7.0, 0.39, ep, 1e-5, 100)
+    assert abs(st.iterations - it_o) <= 1
+    assert np.sqrt(np.mean(np.sum((st.mu - mu_o) ** 2, 1))) * mdg.DEBYE < 1e-5
+    engine.upload_frames(None, None, None)

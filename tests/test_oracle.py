@@ -515,3 +515,60 @@ def test_polar_torques_by_rotation(oracle, alpha):
             dn = _epol(oracle, rotate_site(s, i, a, -h), t, alpha)[0]
             assert tq[i, a] == pytest.approx(-(up - dn) / (2 * h),
                                              abs=2e-6 * max(1, np.abs(tq).max()))
+
+
+# ---------------------------------------------------------------- local frames (8(f)#2)
+def water_cluster(n_mol=4, seed=21, box=40.0, spread=6.0):
+    """n_mol rigid waters (O-H 0.9572 A, 104.52 deg) scattered in a cluster
+    in a large box, random local-frame multipoles, frames per water_frames."""
+    from oracle import frames as fr
+    rng = np.random.default_rng(seed)
+    pos = []
+    th = np.deg2rad(104.52) / 2
+    for _ in range(n_mol):
+        o = box / 2 + rng.uniform(-spread / 2, spread / 2, 3)
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        h1 = o + 0.9572 * q @ np.array([np.sin(th), 0, np.cos(th)])
+        h2 = o + 0.9572 * q @ np.array([-np.sin(th), 0, np.cos(th)])
+        pos += [o, h1, h2]
+    pos = np.array(pos)
+    n = len(pos)
+    one = np.ones(n)
+    charge = np.tile([-0.51966, 0.25983, 0.25983], n_mol)
+    s = System((box,) * 3, pos[:, 0].copy(), pos[:, 1].copy(), pos[:, 2].copy(), charge, one,
+               one, one, one, np.tile([0.837, 0.496, 0.496], n_mol))
+    s.molecule = (np.arange(n) // 3).astype(np.int32)
+    dl = rng.normal(0, 0.15, (n, 3))
+    ql = rng.normal(0, 0.1, (n, 6))
+    tr = (ql[:, 0] + ql[:, 3] + ql[:, 5]) / 3
+    ql[:, 0] -= tr
+    ql[:, 3] -= tr
+    ql[:, 5] -= tr
+    frame, za, xa = fr.water_frames(s.molecule)
+    return s, frame, za, xa, dl, ql
+
+
+def _framed(s, frame, za, xa, dl, ql):
+    from oracle import frames as fr
+    q = s.copy()
+    pos = np.stack([q.x, q.y, q.z], 1)
+    q.dipole, q.quadrupole = fr.rotate(pos, q.box, frame, za, xa, dl, ql)
+    return q
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.45])
+def test_frame_forces_are_gradients(oracle, alpha):
+    """With local frames the total force -- translational multipole force plus
+    the frame atoms' share of the torques -- is -dE/dr with the frames
+    rebuilt at every displacement."""
+    from oracle import frames as fr
+    s, frame, za, xa, dl, ql = water_cluster()
+    t = oracle.build_table(s, 9.0)
+    g = _framed(s, frame, za, xa, dl, ql)
+    f, tq, e, _ = oracle.mpole(g, t, alpha, 9.0)
+    pos = np.stack([s.x, s.y, s.z], 1)
+    ftot = f + fr.torque_forces(pos, s.box, frame, za, xa, tq)
+    num = fd_forces(lambda q: oracle.mpole(_framed(q, frame, za, xa, dl, ql), t, alpha, 9.0)[2],
+                    s, h=1e-6)
+    assert np.abs(num - ftot).max() <= 1e-6 * max(1.0, np.abs(ftot).max())
+    assert np.abs(ftot.sum(0)).max() <= 1e-10 * np.abs(ftot).max()
