@@ -257,6 +257,19 @@ class DDEngine:
         if L.dipole is not None or L.quadrupole is not None:
             self.eng.upload_multipoles(L.dipole, L.quadrupole)
 
+    def upload_frames(self, frame, zatom, xatom, dipole, quadrupole):
+        """Local multipole frames (global arrays, global site ids): the
+        rank's owned + halo sites with their frame atoms mapped to local
+        ids (frame atoms belong to the same molecule, so they are local)."""
+        idx = self.plan.local
+        inv = {int(g): k for k, g in enumerate(idx)}
+        fr = np.asarray(frame)[idx]
+        za = np.array([inv[int(g)] if f else 0 for g, f in zip(np.asarray(zatom)[idx], fr)],
+                      np.int32)
+        xa = np.array([inv[int(g)] if f else 0 for g, f in zip(np.asarray(xatom)[idx], fr)],
+                      np.int32)
+        self.eng.upload_frames(fr, za, xa, np.asarray(dipole)[idx], np.asarray(quadrupole)[idx])
+
     # ---- halo traffic
     def exchange(self, vec_id: int):
         if self.comm.size == 1:
