@@ -6,5 +6,6 @@ from .mdvec import (  # noqa: F401
     CharmmParams, ContractViolation, ConvergenceError, CudaError, Engine, EwaldRealParams,
     FieldArrays, ForceAccumulator, HalgrenParams, LjParams, NeighborTable, ParticleSystem,
     PolarizationState, PolarParams, SingularityError, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE, TERM_VDW,
-    fp64_peak_tflops, host_array, load_library, reduce_sites_host,
+    dump_system_json, fp64_peak_tflops, host_array, load_library, load_system_json,
+    reduce_sites_host,
     water_box)

@@ -682,6 +682,56 @@ def device_erfc(x, device: int = 0) -> np.ndarray:
     return out
 
 
+# ---- the reference's system dump format (interop) --------------------------------
+_JSON_ARRAYS = ("x", "y", "z", "charge", "lj_sigma", "lj_epsilon", "hal_r0", "hal_epsilon",
+                "polarizability")
+
+
+def load_system_json(path_or_text: str):
+    """Read the reference's `bench gen` system dump (mdvec::dump_system_json,
+    proj/src/bench.cpp:541-567: version, seed, kind, box, n_sites, the nine
+    site arrays, mu_x/mu_y/mu_z). Returns (ParticleSystem, dipoles (n, 3) or
+    None, metadata dict)."""
+    import json
+    import os
+    text = path_or_text
+    if not text.lstrip().startswith("{") and os.path.exists(path_or_text):
+        with open(path_or_text) as f:
+            text = f.read()
+    j = json.loads(text)
+    if j.get("version") != 1:
+        raise ContractViolation("system dump: unsupported version %r" % j.get("version"))
+    n = int(j["n_sites"])
+    arrs = {}
+    for k in _JSON_ARRAYS:
+        a = np.asarray(j[k], np.float64)
+        if a.shape != (n,):
+            raise ContractViolation(f"system dump: {k} has {a.shape[0]} values, expected {n}")
+        arrs[k] = a
+    b = j["box"]
+    s = ParticleSystem((float(b["lx"]), float(b["ly"]), float(b["lz"])), **arrs)
+    mu = None
+    if all(k in j for k in ("mu_x", "mu_y", "mu_z")):
+        mu = np.stack([np.asarray(j[k], np.float64) for k in ("mu_x", "mu_y", "mu_z")], 1)
+    meta = {k: j[k] for k in ("version", "seed", "kind") if k in j}
+    return s, mu, meta
+
+
+def dump_system_json(s, mu=None, seed: int = 1, kind: str = "uniform-random") -> str:
+    """The same format, written from a ParticleSystem (+ optional dipoles)."""
+    import json
+    j = {"version": 1, "seed": int(seed), "kind": kind,
+         "box": {"lx": float(s.box[0]), "ly": float(s.box[1]), "lz": float(s.box[2])},
+         "n_sites": int(len(s.x))}
+    for k in _JSON_ARRAYS:
+        j[k] = [float(v) for v in np.asarray(getattr(s, k), np.float64)]
+    if mu is not None:
+        mu = np.asarray(mu, np.float64)
+        for a, k in enumerate(("mu_x", "mu_y", "mu_z")):
+            j[k] = [float(v) for v in mu[:, a]]
+    return json.dumps(j, indent=2, sort_keys=True) + "\n"
+
+
 # ---- fixtures ------------------------------------------------------------------------
 def water_box(n_mol: int, box: float, seed: int = 1, model: str = "amoeba") -> ParticleSystem:
     """BASELINE.json 3-site water fixture (mdg_water_generate)."""

@@ -75,3 +75,23 @@ def test_config0_water_golden(oracle, g, mdg):
     f, e, _ = oracle.ewald_real(s, t, 0.35, 9.0, exclude=True)
     assert abs(e - float(g["w0_ew_e"])) <= 1e-10 * abs(e)
     assert np.abs(f - g["w0_ew_f"]).max() <= 1e-11 * np.abs(f).max()
+
+
+@pytest.mark.parametrize("name,kind,n,box,seed", [
+    ("ref_system_uniform.json", "uniform", 40, (9.0, 10.0, 11.0), 7),
+    ("ref_system_lattice.json", "lattice", 27, (12.0, 12.0, 12.0), 3)])
+def test_reference_system_dump_reader(oracle, mdg, name, kind, n, box, seed):
+    """The reference's `bench gen` JSON (written by its own dump_system_json,
+    tests/golden/gen_system_json.cpp) reads back bit-exactly: arrays equal to
+    the oracle's (reference-pinned) generator, dipoles to random_dipoles; and
+    the writer round-trips."""
+    s, mu, meta = mdg.load_system_json(os.path.join(GOLDEN, name))
+    assert meta["seed"] == seed and len(s.x) == n and tuple(s.box) == box
+    o = oracle.generate_system(kind, n, box, seed)
+    for k in FIELDS:
+        assert np.array_equal(getattr(s, k), getattr(o, k)), k
+    assert np.array_equal(mu, oracle.random_dipoles(n, seed))
+    s2, mu2, meta2 = mdg.load_system_json(mdg.dump_system_json(s, mu, seed, meta["kind"]))
+    for k in FIELDS:
+        assert np.array_equal(getattr(s2, k), getattr(s, k)), k
+    assert np.array_equal(mu2, mu) and meta2 == meta
