@@ -179,6 +179,17 @@ int mdg_polar_forces(mdg_ctx* ctx, int list_id, double alpha, double cutoff, dou
                      const double* muz, double* fx, double* fy, double* fz, double* tx,
                      double* ty, double* tz, double* pair_energy, double* virial9);
 
+/* ---- reciprocal-space Ewald -------------------------------- */
+/* Smooth PME for the point charges on a k1 x k2 x k3 grid with order-`order`
+ * B-splines (cuFFT): forces (overwritten), energies3 = (reciprocal, self
+ * -a/sqrt(pi) sum q^2, excluded-pair correction -sum q_i q_j erf(a r)/r over
+ * same-molecule pairs when exclude != 0), virial9 = reciprocal + excluded
+ * (strain derivative, the pair-virial convention). With mdg_ewald_real_forces
+ * at the same alpha the four terms are the full Ewald sum. Single domain. */
+int mdg_ewald_recip(mdg_ctx* ctx, double alpha, int k1, int k2, int k3, int order,
+                    double electric, int exclude, double* fx, double* fy, double* fz,
+                    double* energies3, double* virial9);
+
 /* ---- fused steps (device-resident; the bench's hot path) ----------------- */
 typedef struct {
   double cutoff;    /* LJ and Ewald cutoff (A) */

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -279,6 +280,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->frame, c->mploc, c->fbuf, c->fref_start,
+                  c->excl_start, c->excl,
                   c->fref, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
@@ -304,6 +306,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->timer_b) cudaEventDestroy(c->timer_b);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  mdg::pme_free(c);
   if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
   if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
   if (c->aux_partials) cudaFree(c->aux_partials);
@@ -508,6 +511,30 @@ int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred
       } else {
         par[s] = (int32_t)s;
       }
+    }
+    // same-molecule partners per site (CSR, sorted indices): PME removes these
+    // pairs from the reciprocal sum
+    {
+      std::map<int32_t, std::vector<int32_t>> groups;
+      for (int64_t s = 0; s < n; ++s) groups[mol[s]].push_back((int32_t)s);
+      std::vector<int32_t> xs(n + 1, 0), xl;
+      for (int64_t s = 0; s < n; ++s) xs[s + 1] = (int32_t)groups[mol[s]].size() - 1;
+      for (int64_t s = 0; s < n; ++s) xs[s + 1] += xs[s];
+      xl.resize(std::max<int32_t>(xs[n], 1));
+      for (int64_t s = 0; s < n; ++s) {
+        int32_t k = xs[s];
+        for (int32_t t : groups[mol[s]])
+          if (t != s) xl[k++] = t;
+      }
+      if (c->excl) cudaFree(c->excl);
+      c->excl = nullptr;
+      if (!c->excl_start)
+        MDG_CUDA_CHECK(cudaMalloc(&c->excl_start, ((size_t)c->n_cap + 1) * sizeof(int32_t)));
+      MDG_CUDA_CHECK(cudaMalloc(&c->excl, xl.size() * sizeof(int32_t)));
+      MDG_CUDA_CHECK(cudaMemcpy(c->excl_start, xs.data(), (n + 1) * sizeof(int32_t),
+                                cudaMemcpyHostToDevice));
+      MDG_CUDA_CHECK(cudaMemcpy(c->excl, xl.data(), xl.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice));
     }
     // children CSR (sorted indices) for the chain rule; a parent must be its own parent
     std::vector<int32_t> start(n + 1, 0), child;
@@ -956,6 +983,35 @@ int mdg_polar_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
     mdg::fetch_results(c);
     if (pair_energy) *pair_energy = c->h_results[70];
     if (virial9) std::memcpy(virial9, c->h_results + 71, 9 * sizeof(double));
+  });
+}
+
+int mdg_ewald_recip(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
+                    double electric, int exclude, double* fx, double* fy, double* fz,
+                    double* energies3, double* virial9) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(alpha > 0, "ewald_recip: alpha must be positive");
+    need(order >= 3 && order <= 10, "ewald_recip: B-spline order must be 3..10");
+    need(k1 >= order && k2 >= order && k3 >= order, "ewald_recip: grid smaller than the order");
+    need(c->n_own == c->n, "ewald_recip: single domain only (no distributed FFT)");
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->force, 0, (size_t)c->n * sizeof(double4), c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 80, 0, 18 * sizeof(double), c->stream));
+    mdg::run_pme(c, alpha, k1, k2, k3, order, electric, exclude != 0);
+    vec_out(c, c->force, fx, fy, fz);
+    mdg::fetch_results(c);
+    const double* r = c->h_results;
+    if (energies3) {
+      energies3[0] = r[80];
+      energies3[1] = r[87];
+      energies3[2] = r[88];
+    }
+    if (virial9) {
+      double w[9];
+      sym_virial(r + 81, w);
+      for (int k = 0; k < 9; ++k) virial9[k] = w[k] + r[89 + k];
+    }
   });
 }
 

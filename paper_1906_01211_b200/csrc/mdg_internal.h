@@ -31,8 +31,8 @@ constexpr int kBlock = MDG_BLOCK;  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
 // device result slots: 0-9 nonpolar, 10-19 multipoles, 20-27 PCG, 30 Jacobi,
 // 40 polarization energy, 50-51 count_within, 60-63 list stats,
-// 70-79 polarization forces (pair energy, virial)
-constexpr int kResultSlots = 96;
+// 70-79 polarization forces (pair energy, virial), 80-97 PME (pme.cu)
+constexpr int kResultSlots = 128;
 constexpr int kMaxBlocksRed = 1 << 20;
 
 struct Box {
@@ -132,6 +132,11 @@ struct mdg_ctx {
   // local-frame multipoles (mp layout), per-site frame forces (i, z, x) and
   // the CSR of frame references per atom (2 * site + role)
   bool has_frames = false;
+  // same-molecule partners per site (CSR, sorted indices): PME's removal of
+  // the excluded pairs from the reciprocal sum
+  int32_t* excl_start = nullptr;
+  int32_t* excl = nullptr;
+  void* pme = nullptr;  // PmeState (pme.cu)
   int4* frame = nullptr;
   double4* mploc = nullptr;
   double4* fbuf = nullptr;
@@ -337,6 +342,11 @@ void rotate_multipoles(mdg_ctx* c);
 void frame_torques_to_forces(mdg_ctx* c);
 // multi-domain: refresh the halo entries of vec_id through the comm hook
 void exchange_halo(mdg_ctx* c, int vec_id);
+// smooth PME reciprocal space for point charges (pme.cu): adds forces to
+// c->force; results 80 (recip), 81-86 (virial), 87 (self), 88-97 (excluded)
+void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
+             bool exclude);
+void pme_free(mdg_ctx* c);
 
 
 // permutation helpers (device kernels)

@@ -120,6 +120,8 @@ SIGNATURES = {
     "mdg_polar_forces": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                    _dp, _dp, _dp, _dp]),
+    "mdg_ewald_recip": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_amoeba_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "mdg_fetch_forces": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
@@ -535,6 +537,18 @@ class Engine:
                                         _p(fy), _p(fz), _p(tx), _p(ty), _p(tz), C.byref(e),
                                         _p(w)))
         return (_aos(fx, fy, fz), _aos(tx, ty, tz), e.value, w.reshape(3, 3))
+
+    def ewald_recip(self, alpha: float, grid=(32, 32, 32), order: int = 5,
+                    electric: float = 1.0, exclude: bool = True):
+        """Smooth-PME reciprocal space (mdg.h mdg_ewald_recip): (forces,
+        (E_recip, E_self, E_excluded), virial 3x3)."""
+        fx, fy, fz = self._vec3()
+        e = np.zeros(3)
+        w = np.zeros(9)
+        check(self.lib.mdg_ewald_recip(self.ctx, alpha, int(grid[0]), int(grid[1]), int(grid[2]),
+                                       int(order), electric, int(exclude), _p(fx), _p(fy),
+                                       _p(fz), _p(e), _p(w)))
+        return _aos(fx, fy, fz), e, w.reshape(3, 3)
 
     # ---- fused steps ----------------------------------------------------------------
     def charmm_step(self, t: NeighborTable, p: CharmmParams):

@@ -569,3 +569,46 @@ def test_local_frames_match_oracle(engine, oracle, mdg):
     assert abs(st.iterations - it_o) <= 1
     assert np.sqrt(np.mean(np.sum((st.mu - mu_o) ** 2, 1))) * mdg.DEBYE < 1e-5
     engine.upload_frames(None, None, None)
+
+
+def _charged_molecules(oracle, n_mol=30, L=20.0, seed=3):
+    s = oracle.generate_system("uniform", 3 * n_mol, (L, L, L), seed, 1.0)
+    s.charge[:] = np.tile([-0.8, 0.4, 0.4], n_mol)
+    s.molecule = (np.arange(3 * n_mol) // 3).astype(np.int32)
+    return s
+
+
+def test_pme_matches_direct_ewald_sum(engine, oracle, mdg):
+    """Smooth PME (8(f)#3) vs the direct structure-factor sum (oracle/
+    ewald_recip.py) at PME accuracy; self and excluded-pair terms exact."""
+    from oracle import ewald_recip as er
+    s = _charged_molecules(oracle)
+    L = s.box[0]
+    pos = np.stack([s.x, s.y, s.z], 1)
+    q = np.asarray(s.charge)
+    e_o, f_o, w_o = er.recip(pos, q, s.box, 0.5, kmax=(24, 24, 24), electric=mdg.ELECTRIC)
+    ex_o, fx_o, wx_o = er.excluded_correction(pos, q, s.box, s.molecule, 0.5, mdg.ELECTRIC)
+    engine.upload_system(s)
+    f, e, w = engine.ewald_recip(0.5, (48, 48, 48), 6, mdg.ELECTRIC, True)
+    assert e[0] == pytest.approx(e_o, rel=1e-6)
+    assert e[1] == pytest.approx(er.self_energy(q, 0.5, mdg.ELECTRIC), rel=1e-12)
+    assert e[2] == pytest.approx(ex_o, rel=1e-12)
+    fref = f_o + fx_o
+    assert force_err_max(f, fref) <= 2e-5
+    np.testing.assert_allclose(w, w_o + wx_o, rtol=0, atol=1e-5 * np.abs(w_o).max())
+
+
+def test_full_ewald_is_alpha_independent(engine, oracle, mdg):
+    """Real space (device kernel) + PME + self + excluded pairs: the same
+    total energy and forces for two splitting parameters."""
+    s = _charged_molecules(oracle, seed=4)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.9)
+    tot = []
+    for a in (0.5, 0.6):
+        rs = engine.ewald_real_forces(t, mdg.EwaldRealParams(a, 9.9), exclude=True)
+        f, e, w = engine.ewald_recip(a, (64, 64, 64), 8, 1.0, True)
+        tot.append((rs.energy + e.sum(), rs.forces + f, np.abs(e).max()))
+    # the terms are O(10) and nearly cancel: PME accuracy relative to them
+    assert abs(tot[0][0] - tot[1][0]) <= 1e-6 * tot[0][2]
+    assert force_err_max(tot[0][1], tot[1][1]) <= 2e-5

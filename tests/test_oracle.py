@@ -572,3 +572,35 @@ def test_frame_forces_are_gradients(oracle, alpha):
                     s, h=1e-6)
     assert np.abs(num - ftot).max() <= 1e-6 * max(1.0, np.abs(ftot).max())
     assert np.abs(ftot.sum(0)).max() <= 1e-10 * np.abs(ftot).max()
+
+
+# ---------------------------------------------------------------- reciprocal space (8(f)#3)
+def test_ewald_oracle_is_alpha_independent(oracle):
+    """Real space (oracle mdo_ewald_real) + direct reciprocal sum + self +
+    excluded-pair terms: the full Ewald energy and forces do not depend on
+    the splitting parameter (the oracle/ewald_recip.py pin)."""
+    from oracle import ewald_recip as er
+    n_mol, L = 30, 20.0
+    s = oracle.generate_system("uniform", 3 * n_mol, (L, L, L), 3, 1.0)
+    s.charge[:] = np.tile([-0.8, 0.4, 0.4], n_mol)
+    s.molecule = (np.arange(3 * n_mol) // 3).astype(np.int32)
+    pos = np.stack([s.x, s.y, s.z], 1)
+    t = oracle.build_table(s, 9.9)
+    tot = []
+    for a in (0.5, 0.6):
+        fr_, er_, _ = oracle.ewald_real(s, t, a, 9.9, 1.0, exclude=True)
+        e2, f2, _ = er.recip(pos, s.charge, s.box, a, kmax=(24, 24, 24))
+        e4, f4, _ = er.excluded_correction(pos, s.charge, s.box, s.molecule, a)
+        tot.append((er_ + e2 + er.self_energy(s.charge, a) + e4, fr_ + f2 + f4))
+    assert abs(tot[0][0] - tot[1][0]) <= 1e-11
+    assert np.abs(tot[0][1] - tot[1][1]).max() <= 1e-10
+    # forces are -dE/dr (finite differences of the reciprocal sum)
+    e0, f0, _ = er.recip(pos, s.charge, s.box, 0.5, kmax=(16, 16, 16))
+    h = 1e-6
+    for i, a in ((0, 0), (7, 1), (40, 2)):
+        p1, p2 = pos.copy(), pos.copy()
+        p1[i, a] += h
+        p2[i, a] -= h
+        num = -(er.recip(p1, s.charge, s.box, 0.5, (16, 16, 16))[0] -
+                er.recip(p2, s.charge, s.box, 0.5, (16, 16, 16))[0]) / (2 * h)
+        assert num == pytest.approx(f0[i, a], abs=1e-7)
