@@ -224,6 +224,39 @@ typedef struct {
  * Results stay on the device. */
 int mdg_amoeba_step(mdg_ctx* ctx, int vdw_list, int elec_list, const mdg_amoeba_params* p);
 
+/* ---- MD time loop ----------------------------------------- */
+/* Harmonic bonded terms for flexible molecules (caller-order site ids):
+ * bond energy kb (r - r0)^2, angle energy ka (theta - theta0)^2 (radians,
+ * angles[3k+1] the vertex). Replaces any previous set. */
+int mdg_bonded_upload(mdg_ctx* ctx, int64_t nbonds, const int32_t* bonds, const double* kb,
+                      const double* r0, int64_t nangles, const int32_t* angles,
+                      const double* ka, const double* theta0);
+/* Bonded forces alone (overwrite) and energies2 = (bonds, angles). */
+int mdg_bonded_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz, double* energies2);
+/* Masses (amu; NULL keeps the previous ones) and velocities (A/fs). */
+int mdg_velocities_upload(mdg_ctx* ctx, const double* mass, const double* vx, const double* vy,
+                          const double* vz);
+int mdg_velocities_fetch(mdg_ctx* ctx, double* vx, double* vy, double* vz);
+int mdg_positions_fetch(mdg_ctx* ctx, double* x, double* y, double* z);
+
+typedef struct {
+  int model;             /* 0 CHARMM-style (charmm params), 1 AMOEBA-style */
+  int64_t nsteps;
+  double dt_fs;
+  int rebuild_every;     /* neighbour lists rebuilt every this many steps */
+  int elec_list, vdw_list;              /* list ids (vdw_list: AMOEBA only) */
+  double elec_list_cutoff, vdw_list_cutoff;
+  int bonded;            /* add the uploaded bonded terms */
+} mdg_md_params;
+
+/* nsteps of velocity Verlet on the device (single domain): kick, drift
+ * (positions wrapped into the box), lists rebuilt on schedule, forces of
+ * the selected model (+ bonded), kick. ekin / epot (kcal/mol, NULL to skip)
+ * receive each step's kinetic / potential energy; the AMOEBA model needs
+ * MDG_TERM_POLAR_FORCE with polarization for conservative dynamics. */
+int mdg_md_run(mdg_ctx* ctx, const mdg_md_params* p, const mdg_charmm_params* charmm,
+               const mdg_amoeba_params* amoeba, double* ekin, double* epot);
+
 /* Results of the last step / kernel, copied to host (caller order).
  * energies[4] = {vdw, coulomb or multipole, polarization (0 here), unused}. */
 int mdg_fetch_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz);

@@ -280,7 +280,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->frame, c->mploc, c->fbuf, c->fref_start,
-                  c->excl_start, c->excl,
+                  c->excl_start, c->excl, c->vel, c->bond_ij, c->bond_par, c->angle_ijk,
+                  c->angle_par,
                   c->fref, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
@@ -1044,8 +1045,8 @@ static bool overlap_enabled(mdg_ctx* c) {
   return true;
 }
 
-int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
-  return guard([&] {
+static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  {
     need_system(c);
     need(p != nullptr, "null params");
     mdg::DevList& Lv = need_list(c, vdw_list);
@@ -1125,6 +1126,176 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
       c->has_polar_force = true;
     }
     if ((terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
+  }
+}
+
+int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  return guard([&] { amoeba_step_impl(c, vdw_list, elec_list, p); });
+}
+
+// ---- MD (8(f)#4) -----------------------------------------------------------------
+
+int mdg_bonded_upload(mdg_ctx* c, int64_t nbonds, const int32_t* bonds, const double* kb,
+                      const double* r0, int64_t nangles, const int32_t* angles,
+                      const double* ka, const double* theta0) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(nbonds >= 0 && nangles >= 0, "bonded: negative count");
+    need(nbonds == 0 || (bonds && kb && r0), "bonded: null bond arrays");
+    need(nangles == 0 || (angles && ka && theta0), "bonded: null angle arrays");
+    const int64_t n = c->n;
+    auto site = [&](int32_t o) {
+      need(o >= 0 && o < n, "bonded: site index out of range");
+      return c->iperm[o];
+    };
+    std::vector<int32_t> bij(2 * std::max<int64_t>(nbonds, 1));
+    std::vector<double> bp(2 * std::max<int64_t>(nbonds, 1));
+    for (int64_t k = 0; k < nbonds; ++k) {
+      bij[2 * k] = site(bonds[2 * k]);
+      bij[2 * k + 1] = site(bonds[2 * k + 1]);
+      bp[2 * k] = kb[k];
+      bp[2 * k + 1] = r0[k];
+    }
+    std::vector<int32_t> aijk(4 * std::max<int64_t>(nangles, 1), 0);
+    std::vector<double> ap(2 * std::max<int64_t>(nangles, 1));
+    for (int64_t k = 0; k < nangles; ++k) {
+      for (int t = 0; t < 3; ++t) aijk[4 * k + t] = site(angles[3 * k + t]);
+      ap[2 * k] = ka[k];
+      ap[2 * k + 1] = theta0[k];
+    }
+    for (void** p : {(void**)&c->bond_ij, (void**)&c->bond_par, (void**)&c->angle_ijk,
+                     (void**)&c->angle_par}) {
+      if (*p) cudaFree(*p);
+      *p = nullptr;
+    }
+    MDG_CUDA_CHECK(cudaMalloc(&c->bond_ij, bij.size() * 4));
+    MDG_CUDA_CHECK(cudaMalloc(&c->bond_par, bp.size() * 8));
+    MDG_CUDA_CHECK(cudaMalloc(&c->angle_ijk, aijk.size() * 4));
+    MDG_CUDA_CHECK(cudaMalloc(&c->angle_par, ap.size() * 8));
+    MDG_CUDA_CHECK(cudaMemcpy(c->bond_ij, bij.data(), bij.size() * 4, cudaMemcpyHostToDevice));
+    MDG_CUDA_CHECK(cudaMemcpy(c->bond_par, bp.data(), bp.size() * 8, cudaMemcpyHostToDevice));
+    MDG_CUDA_CHECK(cudaMemcpy(c->angle_ijk, aijk.data(), aijk.size() * 4, cudaMemcpyHostToDevice));
+    MDG_CUDA_CHECK(cudaMemcpy(c->angle_par, ap.data(), ap.size() * 8, cudaMemcpyHostToDevice));
+    c->nbonds = nbonds;
+    c->nangles = nangles;
+  });
+}
+
+int mdg_bonded_forces(mdg_ctx* c, double* fx, double* fy, double* fz, double* energies2) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->force, 0, (size_t)c->n * sizeof(double4), c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 100, 0, 2 * sizeof(double), c->stream));
+    mdg::run_bonded(c);
+    vec_out(c, c->force, fx, fy, fz);
+    mdg::fetch_results(c);
+    if (energies2) {
+      energies2[0] = c->h_results[100];
+      energies2[1] = c->h_results[101];
+    }
+  });
+}
+
+int mdg_velocities_upload(mdg_ctx* c, const double* mass, const double* vx, const double* vy,
+                          const double* vz) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(vx && vy && vz, "velocities: null array");
+    need(mass || c->has_vel, "velocities: masses required on the first upload");
+    const int64_t n = c->n;
+    std::vector<double> inv(n);
+    if (mass) {
+      for (int64_t s = 0; s < n; ++s) {
+        const double m = mass[c->perm[s]];
+        need(m > 0, "velocities: masses must be positive");
+        inv[s] = 1.0 / m;
+      }
+    }
+    if (!c->vel) MDG_CUDA_CHECK(cudaMalloc(&c->vel, (size_t)c->n_cap * sizeof(double4)));
+    std::vector<double> w;
+    if (!mass) {  // keep the stored 1/m
+      std::vector<double4> old(n);
+      MDG_CUDA_CHECK(cudaMemcpy(old.data(), c->vel, n * sizeof(double4), cudaMemcpyDeviceToHost));
+      for (int64_t s = 0; s < n; ++s) inv[s] = old[s].w;
+    }
+    std::vector<double4> v(n);
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t o = c->perm[s];
+      v[s] = make_double4(vx[o], vy[o], vz[o], inv[s]);
+    }
+    MDG_CUDA_CHECK(cudaMemcpy(c->vel, v.data(), n * sizeof(double4), cudaMemcpyHostToDevice));
+    c->has_vel = true;
+  });
+}
+
+int mdg_velocities_fetch(mdg_ctx* c, double* vx, double* vy, double* vz) {
+  return guard([&] {
+    need_system(c);
+    need(c->has_vel, "velocities: none uploaded");
+    vec_out(c, c->vel, vx, vy, vz);
+  });
+}
+
+int mdg_positions_fetch(mdg_ctx* c, double* x, double* y, double* z) {
+  return guard([&] {
+    need_system(c);
+    vec_out(c, c->pos, x, y, z);
+  });
+}
+
+int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
+               const mdg_amoeba_params* ap, double* ekin, double* epot) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(p != nullptr, "md: null params");
+    need(c->has_vel, "md: upload masses and velocities first");
+    need(c->n_own == c->n, "md: single domain only (no migration between domains)");
+    need(p->nsteps >= 0 && p->dt_fs > 0 && p->rebuild_every >= 1, "md: bad step parameters");
+    need(p->model == 0 ? cp != nullptr : (p->model == 1 && ap != nullptr),
+         "md: model 0 needs charmm params, model 1 amoeba params");
+    auto rebuild = [&] {
+      mdg::nlist_build(c, p->elec_list, p->elec_list_cutoff, MDG_SITES_ATOMIC);
+      if (p->model == 1) mdg::nlist_build(c, p->vdw_list, p->vdw_list_cutoff, MDG_SITES_VDW);
+    };
+    double e_nb = 0.0;
+    auto forces = [&] {
+      if (p->model == 0) {
+        mdg::NonpolarArgs a{1, 1, cp->shift, cp->exclude, cp->cutoff, cp->alpha, cp->electric};
+        mdg::run_nonpolar(c, p->elec_list, a);
+      } else {
+        amoeba_step_impl(c, p->vdw_list, p->elec_list, ap);
+      }
+      if (p->bonded) {
+        MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 100, 0, 2 * sizeof(double), c->stream));
+        mdg::run_bonded(c);
+      }
+    };
+    auto potential = [&] {
+      const double* r = c->h_results;
+      e_nb = (p->model == 0) ? r[0] + r[1] : r[0] + r[10] + r[40];
+      return e_nb + (p->bonded ? r[100] + r[101] : 0.0);
+    };
+    const double dt = p->dt_fs;
+    rebuild();
+    forces();
+    for (int64_t s = 0; s < p->nsteps; ++s) {
+      mdg::run_kick(c, 0.5 * dt);
+      mdg::run_drift(c, dt);
+      if ((s + 1) % p->rebuild_every == 0) rebuild();
+      forces();
+      mdg::run_kick(c, 0.5 * dt);
+      if (ekin || epot) {
+        mdg::run_kinetic(c);
+        mdg::fetch_results(c);
+        if (ekin) ekin[s] = c->h_results[102];
+        if (epot) epot[s] = potential();
+      }
+    }
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -137,6 +137,14 @@ struct mdg_ctx {
   int32_t* excl_start = nullptr;
   int32_t* excl = nullptr;
   void* pme = nullptr;  // PmeState (pme.cu)
+  // MD (md.cu): velocities (w = 1/mass) and harmonic bonded terms
+  double4* vel = nullptr;
+  bool has_vel = false;
+  int2* bond_ij = nullptr;
+  double2* bond_par = nullptr;  // (k, r0)
+  int4* angle_ijk = nullptr;    // (i, vertex j, k, 0)
+  double2* angle_par = nullptr; // (k, theta0)
+  int64_t nbonds = 0, nangles = 0;
   int4* frame = nullptr;
   double4* mploc = nullptr;
   double4* fbuf = nullptr;
@@ -347,6 +355,12 @@ void exchange_halo(mdg_ctx* c, int vec_id);
 void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
              bool exclude);
 void pme_free(mdg_ctx* c);
+// MD (md.cu): bonded forces added to c->force (results 100 bonds, 101
+// angles), velocity-Verlet half kick / drift, kinetic energy (result 102)
+void run_bonded(mdg_ctx* c);
+void run_kick(mdg_ctx* c, double half_dt);
+void run_drift(mdg_ctx* c, double dt);
+void run_kinetic(mdg_ctx* c);
 
 
 // permutation helpers (device kernels)

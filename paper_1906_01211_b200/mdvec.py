@@ -123,6 +123,13 @@ SIGNATURES = {
     "mdg_ewald_recip": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "mdg_bonded_upload": (C.c_int, [C.c_void_p, C.c_int64, _ip, _dp, _dp, C.c_int64, _ip, _dp,
+                                    _dp]),
+    "mdg_bonded_forces": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
+    "mdg_velocities_upload": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
+    "mdg_velocities_fetch": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "mdg_positions_fetch": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "mdg_md_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _dp, _dp]),
     "mdg_amoeba_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "mdg_fetch_forces": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_fetch_torques": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
@@ -171,6 +178,14 @@ class AmoebaParams(C.Structure):
 
 
 TERM_VDW, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE = 1, 2, 4, 8
+
+
+class MDParams(C.Structure):
+    """mdg.h mdg_md_params (SURVEY 8(f)#4)."""
+    _fields_ = [("model", C.c_int), ("nsteps", C.c_int64), ("dt_fs", C.c_double),
+                ("rebuild_every", C.c_int), ("elec_list", C.c_int), ("vdw_list", C.c_int),
+                ("elec_list_cutoff", C.c_double), ("vdw_list_cutoff", C.c_double),
+                ("bonded", C.c_int)]
 
 
 _lib = None
@@ -549,6 +564,50 @@ class Engine:
                                        int(order), electric, int(exclude), _p(fx), _p(fy),
                                        _p(fz), _p(e), _p(w)))
         return _aos(fx, fy, fz), e, w.reshape(3, 3)
+
+    # ---- MD (8(f)#4) ---------------------------------------------------------------
+    def upload_bonded(self, bonds=None, kb=None, r0=None, angles=None, ka=None, theta0=None):
+        """Harmonic bonds (m, 2) / angles (m, 3; vertex in the middle),
+        E = k (x - x0)^2 (mdg.h mdg_bonded_upload)."""
+        b = np.zeros((0, 2), np.int32) if bonds is None else np.ascontiguousarray(bonds, np.int32)
+        a = np.zeros((0, 3), np.int32) if angles is None else np.ascontiguousarray(angles, np.int32)
+        kb_ = _f64(np.zeros(0) if kb is None else np.broadcast_to(kb, len(b)))
+        r0_ = _f64(np.zeros(0) if r0 is None else np.broadcast_to(r0, len(b)))
+        ka_ = _f64(np.zeros(0) if ka is None else np.broadcast_to(ka, len(a)))
+        t0_ = _f64(np.zeros(0) if theta0 is None else np.broadcast_to(theta0, len(a)))
+        check(self.lib.mdg_bonded_upload(self.ctx, len(b), _p(b, _ip), _p(kb_), _p(r0_), len(a),
+                                         _p(a, _ip), _p(ka_), _p(t0_)))
+
+    def bonded_forces(self):
+        fx, fy, fz = self._vec3()
+        e = np.zeros(2)
+        check(self.lib.mdg_bonded_forces(self.ctx, _p(fx), _p(fy), _p(fz), _p(e)))
+        return _aos(fx, fy, fz), e
+
+    def upload_velocities(self, v, mass=None):
+        v = np.asarray(v, np.float64)
+        vx, vy, vz = _f64(v[:, 0]), _f64(v[:, 1]), _f64(v[:, 2])
+        m = None if mass is None else _f64(mass)
+        check(self.lib.mdg_velocities_upload(self.ctx, _p(m), _p(vx), _p(vy), _p(vz)))
+
+    def fetch_velocities(self) -> np.ndarray:
+        vx, vy, vz = self._vec3()
+        check(self.lib.mdg_velocities_fetch(self.ctx, _p(vx), _p(vy), _p(vz)))
+        return _aos(vx, vy, vz)
+
+    def fetch_positions(self) -> np.ndarray:
+        x, y, z = self._vec3()
+        check(self.lib.mdg_positions_fetch(self.ctx, _p(x), _p(y), _p(z)))
+        return _aos(x, y, z)
+
+    def md_run(self, p: "MDParams", charmm=None, amoeba=None, energies: bool = True):
+        """Velocity Verlet on the device (mdg.h mdg_md_run); returns per-step
+        (kinetic, potential) energies when `energies`."""
+        ek = np.zeros(max(p.nsteps, 1)) if energies else None
+        ep = np.zeros(max(p.nsteps, 1)) if energies else None
+        check(self.lib.mdg_md_run(self.ctx, C.byref(p), None if charmm is None else C.byref(charmm),
+                                  None if amoeba is None else C.byref(amoeba), _p(ek), _p(ep)))
+        return (ek[: p.nsteps], ep[: p.nsteps]) if energies else None
 
     # ---- fused steps ----------------------------------------------------------------
     def charmm_step(self, t: NeighborTable, p: CharmmParams):

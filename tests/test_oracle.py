@@ -604,3 +604,22 @@ def test_ewald_oracle_is_alpha_independent(oracle):
         num = -(er.recip(p1, s.charge, s.box, 0.5, (16, 16, 16))[0] -
                 er.recip(p2, s.charge, s.box, 0.5, (16, 16, 16))[0]) / (2 * h)
         assert num == pytest.approx(f0[i, a], abs=1e-7)
+
+
+# ---------------------------------------------------------------- MD loop (8(f)#4)
+def test_bonded_oracle_forces_are_gradients(oracle):
+    from oracle import md
+    s, *_ = water_cluster(n_mol=3, seed=5)
+    pos = np.stack([s.x, s.y, s.z], 1) + np.random.default_rng(2).normal(0, 0.05, (9, 3))
+    b, a = md.water_topology(3)
+    args = (b, 529.6, 0.9572, a, 34.05, np.deg2rad(104.52))
+    _, _, f = md.bonded(pos, s.box, *args)
+    h = 1e-6
+    for i in range(9):
+        for k in range(3):
+            p1, p2 = pos.copy(), pos.copy()
+            p1[i, k] += h
+            p2[i, k] -= h
+            e1 = sum(md.bonded(p1, s.box, *args)[:2])
+            e2 = sum(md.bonded(p2, s.box, *args)[:2])
+            assert -(e1 - e2) / (2 * h) == pytest.approx(f[i, k], abs=1e-6)
