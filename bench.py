@@ -227,7 +227,7 @@ def md_timing(wl, steps, barrier, device):
     mms = eng.timer_stop()
     # (throughput only: the synthetic fixture is unrelaxed -- random
     # orientations leave close H...H contacts -- so its trajectory is not
-    # physical; conservation is tested on relaxed boxes in tests/)
+    # physical; NVE conservation is tested in tests/test_gpu_parity.py)
     return {"what": "device velocity Verlet with these forces + flexible-water bonds/angles"
                     + (" + polarization forces" if c["model"] != "charmm" else ""),
             "dt_fs": dt, "steps": steps, "ms_per_step": mms / steps,
