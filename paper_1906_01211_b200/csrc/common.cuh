@@ -143,12 +143,14 @@ __device__ __forceinline__ void ewald_bn(double r, double inv_r, double inv_r2, 
                                          double (&bn)[NMAX + 1]) {
   const double ralpha = alpha * r;
   const double alsq2 = 2.0 * alpha * alpha;
-  double alsq2n = (alpha > 0) ? 1.0 / (1.7724538509055160273 * alpha) : 0.0;
+  // (2a^2)^n / (a sqrt(pi)) = (2a / sqrt(pi)) (2a^2)^(n-1): no division
+  // (the compiler does not hoist a per-pair 1 / (a sqrt(pi)) out of the row)
+  double alsq2n = 1.1283791670955125739 * alpha;
   const double exp2a = exp(-ralpha * ralpha);
   bn[0] = erfc_from_exp(ralpha, exp2a) * inv_r;
 #pragma unroll
   for (int k = 1; k <= NMAX; ++k) {
-    alsq2n *= alsq2;
+    if (k > 1) alsq2n *= alsq2;
     bn[k] = ((double)(2 * k - 1) * bn[k - 1] + alsq2n * exp2a) * inv_r2;
   }
 }

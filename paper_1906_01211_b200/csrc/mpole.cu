@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
       const double4 m0j = ldg4(a.mp + 3 * (size_t)j), m1j = ldg4(a.mp + 3 * (size_t)j + 1);
       const Quad Qj{m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, __ldg(&a.mp[3 * (size_t)j + 2].x)};
       const double djx = m0j.x, djy = m0j.y, djz = m0j.z;
-      const double r = sqrt(r2);
-      const double inv_r = 1.0 / r;
+      const double inv_r = rsqrt(r2);  // one MUFU.RSQ64H + Newton, no division
+      const double r = r2 * inv_r;
       const double inv_r2 = inv_r * inv_r;
       double G[6];
       ewald_bn<5>(r, inv_r, inv_r2, a.alpha, G);

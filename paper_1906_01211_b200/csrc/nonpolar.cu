@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
         fs += 24.0 * eij * (2.0 * s12 - s6) * inv_r2;
       }
       if (COUL) {
-        const double r = sqrt(r2);
-        const double inv_r = 1.0 / r;
+        const double inv_r = rsqrt(r2);  // one MUFU.RSQ64H + Newton, no division
+        const double r = r2 * inv_r;
         const double qq = a.electric * qi * __ldg(&a.pq4[j].z);
         const double ar = a.alpha * r;
         const double ex2 = exp(-ar * ar);

@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
       // (polarizability, pdamp, charge, 1/pdamp) of j in one 32-B load
       const double4 xj = ldg4(a.pq4 + j);
       const double4 pj = make_double4(0.0, 0.0, 0.0, xj.z);
-      const double r = sqrt(r2);
-      const double inv_r = 1.0 / r;
+      const double inv_r = rsqrt(r2);  // one MUFU.RSQ64H + Newton, no division
+      const double r = r2 * inv_r;
       const double inv_r2 = inv_r * inv_r;
       const double b1 = inv_r2 * inv_r;
       const double u = r * ipdi * xj.w;

@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArg
       const double r2 = dist2(x, y, z);
       const double4 pj = ldg4(a.pq4 + j);  // (alpha, pdamp, q)
       const double4 uj = ldg4(a.mu + j);
-      const double r = sqrt(r2);
-      const double inv_r = 1.0 / r;
+      const double inv_r = rsqrt(r2);  // one MUFU.RSQ64H + Newton, no division
+      const double r = r2 * inv_r;
       const double inv_r2 = inv_r * inv_r;
       // Thole lambda3..9 (exponential damping, u = r / (pd_i pd_j))
       const double u = r * ipdi * pj.w;
