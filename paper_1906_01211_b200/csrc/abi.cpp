@@ -142,20 +142,30 @@ static bool is_pinned(const void* p) {
 // Copy caller arrays into the pinned stage and upload them (or, when every
 // array is page-locked, DMA them directly). With `box`, the first three
 // arrays are positions and are checked to lie in [0, L) (the ParticleSystem
-// contract, proj/src/system.cpp) -- on the host, overlapping the DMA.
+// contract, proj/src/system.cpp): page-locked positions on the device after
+// the DMA (one pass over 24 B/site in HBM instead of a host pass competing
+// with the DMA for the same pages), staged ones on the host during the copy.
+// Returns with the caller's arrays no longer in use.
 void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double* box = nullptr) {
   const int64_t n = c->n;
   bool pinned = true;
   for (const double* a : arrays) pinned = pinned && is_pinned(a);
-  if (pinned)
+  if (pinned) {
     for (size_t a = 0; a < arrays.size(); ++a)
       MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage + a * n, arrays[a], n * sizeof(double),
                                      cudaMemcpyHostToDevice, c->stream));
+    if (box) {  // box is the context's (c->lx, c->ly, c->lz)
+      need(mdg::check_box_staged(c) < 0, "ParticleSystem: position outside the box");
+    } else {
+      MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
+    return;
+  }
   std::atomic<bool> bad{false};
   host_parallel(n, [&](int64_t b, int64_t e) {
     for (size_t a = 0; a < arrays.size(); ++a) {
       const double* src = arrays[a];
-      if (!pinned) std::memcpy(c->h_stage + a * n + b, src + b, (e - b) * sizeof(double));
+      std::memcpy(c->h_stage + a * n + b, src + b, (e - b) * sizeof(double));
       if (box && a < 3) {
         const double L = box[a];
         bool ok = true;
@@ -165,9 +175,9 @@ void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double
     }
   });
   need(!bad, "ParticleSystem: position outside the box");
-  if (!pinned)
-    MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
-                                   cudaMemcpyHostToDevice, c->stream));
+  MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage, c->h_stage, arrays.size() * n * sizeof(double),
+                                 cudaMemcpyHostToDevice, c->stream));
+  MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // h_stage free for the next call
 }
 
 // sorted double4 vector -> caller-order SoA host arrays (NULL entries skipped)

@@ -61,7 +61,7 @@ void flush_profile(mdg_ctx* c) {
   c->pending.clear();
 }
 
-int64_t sites_per_block(const void* kernel, int64_t n) {
+int64_t sites_per_block(const void* kernel, int64_t n, int bps_cap, int waves_override) {
   static std::mutex mu;
   static std::map<const void*, int> occ;
   static int sms = 0;
@@ -88,7 +88,8 @@ int64_t sites_per_block(const void* kernel, int64_t n) {
     const char* w = std::getenv("MDG_WAVES");
     return w ? std::max(1, std::atoi(w)) : 16;
   }();
-  const int64_t blocks = (int64_t)sms * nb * waves;
+  if (bps_cap > 0) nb = std::min(nb, bps_cap);
+  const int64_t blocks = (int64_t)sms * nb * (waves_override > 0 ? waves_override : waves);
   return std::max<int64_t>(kWarps, (n + blocks - 1) / blocks);
 }
 
@@ -261,6 +262,28 @@ __global__ void k_pack_positions(int64_t n, const int32_t* __restrict__ perm,
   pos[s].y = y;
   pos[s].z = z;
   if (copy_vsite) vsite[s] = make_double4(x, y, z, pos[s].w);
+}
+
+// position contract 0 <= r < L on the staged caller-order arrays: the lowest
+// offending caller index goes to flag[6] (0x7f7f7f7f: none)
+__global__ void k_check_box(int64_t n, const double* __restrict__ st, double lx, double ly,
+                            double lz, int32_t* __restrict__ flag) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  const double x = st[o], y = st[n + o], z = st[2 * n + o];
+  const bool ok = (x >= 0.0) & (x < lx) & (y >= 0.0) & (y < ly) & (z >= 0.0) & (z < lz);
+  if (!ok) atomicMin(&flag[6], (int32_t)o);
+}
+
+int64_t check_box_staged(mdg_ctx* c) {
+  MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag + 6, 0x7f, sizeof(int32_t), c->stream));
+  MDG_LAUNCH(c, "check_box", grid_for(c->n, 256), 256, 0, k_check_box, c->n, c->d_stage, c->lx,
+             c->ly, c->lz, c->d_flag);
+  int32_t bad = 0;
+  MDG_CUDA_CHECK(cudaMemcpyAsync(&bad, c->d_flag + 6, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  return bad == 0x7f7f7f7f ? -1 : bad;
 }
 
 __global__ void k_set_groups(int64_t n, const int32_t* __restrict__ mol, double4* __restrict__ pos,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -216,6 +217,9 @@ struct mdg_ctx {
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   int64_t last_grid = 0;  // blocks of the last MDG_LAUNCH_SITES launch
+  // shape overrides for MDG_LAUNCH_SITES (0: occupancy limit, 16 waves):
+  // resident blocks per SM and waves, so two streams can share every SM
+  int launch_bps = 0, launch_waves = 0;
 };
 
 namespace mdg {
@@ -250,13 +254,13 @@ inline unsigned grid_for(int64_t n, int block = kBlock) {
 // SM) blocks, each walking a contiguous (Morton-ordered, spatially compact)
 // range of sites with its warps interleaved, so an SM's live neighbour data
 // is a sliding window that stays in L1. Returns sites per block.
-int64_t sites_per_block(const void* kernel, int64_t n);
+int64_t sites_per_block(const void* kernel, int64_t n, int bps_cap = 0, int waves = 0);
 
 // Launch a warp-per-site kernel whose args struct has `ipw` (sites per block)
 // and `partials`; records the grid in ctx->last_grid for the finalize.
 #define MDG_LAUNCH_SITES(ctx, name, n, args, kernel)                             \
   do {                                                                         \
-    const int64_t _ipb = ::mdg::sites_per_block((const void*)(kernel), (n));   \
+    const int64_t _ipb = ::mdg::sites_per_block((const void*)(kernel), (n), (ctx)->launch_bps, (ctx)->launch_waves);   \
     (args).ipw = (int)_ipb;                                                    \
     const int64_t _g = ((n) + _ipb - 1) / _ipb;                                \
     ::mdg::ensure_partials((ctx), _g);                                         \
@@ -264,6 +268,11 @@ int64_t sites_per_block(const void* kernel, int64_t n);
     (ctx)->last_grid = _g;                                                     \
     MDG_LAUNCH((ctx), (name), (unsigned)_g, ::mdg::kBlock, 0, kernel, (args)); \
   } while (0)
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 
 // Launches inside this scope go to the context's aux stream with its own
 // partials buffer (no-op when !on).
@@ -273,8 +282,15 @@ struct AuxScope {
   cudaStream_t s;
   double* p;
   int64_t pb;
+  int bps = 0, waves = 0;
   AuxScope(mdg_ctx* c_, bool on_) : c(c_), on(on_) {
     if (!on) return;
+    static const int aux_bps = env_int("MDG_AUX_BPS", 0);
+    static const int aux_waves = env_int("MDG_AUX_WAVES", 0);
+    bps = c->launch_bps;
+    waves = c->launch_waves;
+    c->launch_bps = aux_bps;
+    c->launch_waves = aux_waves;
     s = c->stream;
     p = c->partials;
     pb = c->partial_blocks;
@@ -289,6 +305,8 @@ struct AuxScope {
     c->stream = s;
     c->partials = p;
     c->partial_blocks = pb;
+    c->launch_bps = bps;
+    c->launch_waves = waves;
   }
   AuxScope(const AuxScope&) = delete;
   AuxScope& operator=(const AuxScope&) = delete;
@@ -376,6 +394,8 @@ void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
 void pack_positions(mdg_ctx* c);
 // pos.w / vsite.w <- mol (after a topology upload)
 void set_groups(mdg_ctx* c);
+// device check of staged positions against the box; first bad caller index or -1
+int64_t check_box_staged(mdg_ctx* c);
 void polar_energy(mdg_ctx* c, double electric, int slot);
 
 }  // namespace mdg

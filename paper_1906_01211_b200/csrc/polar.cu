@@ -583,7 +583,8 @@ static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
 static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
                                double tol_debye, int64_t max_iter, double* last_rms) {
   // the mat-vec's grid (and partials) must be fixed before capture
-  const int64_t ipb = sites_per_block((const void*)k_tmatvec_pre<true>, n);
+  const int64_t ipb =
+      sites_per_block((const void*)k_tmatvec_pre<true>, n, c->launch_bps, c->launch_waves);
   const int64_t g = (n + ipb - 1) / ipb;
   ensure_partials(c, std::max(g, blocks));
   k.ipw = (int)ipb;
@@ -649,6 +650,16 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   const double n_glob = (double)(c->n_global > 0 ? c->n_global : n);
   const int64_t blocks = grid_for(n);
   PrunedList& P = c->plist;
+  // mat-vec shape (MDG_PCG_BPS / MDG_PCG_WAVES): leave room on every SM for
+  // the aux stream's multipole blocks
+  struct Shape {
+    mdg_ctx* c;
+    int b, w;
+    ~Shape() { c->launch_bps = b; c->launch_waves = w; }
+  } shape{c, c->launch_bps, c->launch_waves};
+  static const int pcg_bps = env_int("MDG_PCG_BPS", 0), pcg_waves = env_int("MDG_PCG_WAVES", 0);
+  c->launch_bps = pcg_bps;
+  c->launch_waves = pcg_waves;
   TPArgs k;
   k.n = n;
   ensure_partials(c, blocks);

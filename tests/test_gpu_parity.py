@@ -122,6 +122,26 @@ def test_position_outside_box_rejected(engine, oracle, mdg):
         engine.upload_system(s)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_upload_positions_outside_box_rejected(engine, oracle, mdg, pinned):
+    """The per-step upload keeps the ParticleSystem contract (checked on the
+    device for page-locked buffers, on the host otherwise) and leaves the
+    resident coordinates untouched when it rejects."""
+    s = uniform(oracle, 40, 10.0, 2)
+    engine.upload_system(s)
+    before = engine.fetch_positions()
+    n = len(s.x)
+    xyz = mdg.host_array((3, n)) if pinned else np.empty((3, n))
+    xyz[0], xyz[1], xyz[2] = s.x, s.y, s.z
+    for axis, bad in ((0, 10.0), (1, -1e-300), (2, float("nan"))):
+        xyz[axis][7] = bad
+        with pytest.raises(mdg.ContractViolation):
+            engine.upload_positions(xyz[0], xyz[1], xyz[2])
+        xyz[axis][7] = (s.x, s.y, s.z)[axis][7]
+    np.testing.assert_array_equal(before, engine.fetch_positions())
+    engine.upload_positions(xyz[0], xyz[1], xyz[2])  # valid again
+
+
 # ------------------------------------------------------------------ pair kernels
 def test_lj_closed_form(engine, oracle, mdg):
     """proj/tests/test_kernels.cpp:72-84 (r^2 = 4, sigma = eps = 1): exact."""
