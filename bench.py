@@ -363,6 +363,7 @@ def run_mine(args, world, rank, local):
         xyz[0], xyz[1], xyz[2] = wl.sys.x, wl.sys.y, wl.sys.z
         x, y, z = xyz[0], xyz[1], xyz[2]
         fbuf = m_host_array((3, wl.n))
+        eng.set_force_output(fbuf)  # forces DMA'd while the PCG still runs
         for _ in range(2):
             eng.upload_positions(x, y, z)
             wl.step()

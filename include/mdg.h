@@ -260,6 +260,16 @@ int mdg_md_run(mdg_ctx* ctx, const mdg_md_params* p, const mdg_charmm_params* ch
 /* Results of the last step / kernel, copied to host (caller order).
  * energies[4] = {vdw, coulomb or multipole, polarization (0 here), unused}. */
 int mdg_fetch_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz);
+/* Register page-locked caller arrays (mdg_host_alloc) as the force output:
+ * every later charmm/amoeba step queues the DMA of its final forces into
+ * them as soon as they are complete (for the AMOEBA step without
+ * polarization forces or frames: while the PCG still runs), and an
+ * mdg_fetch_forces with the same pointers called right after the step only
+ * waits for it. The arrays are written asynchronously by each step: read
+ * them after mdg_fetch_forces / mdg_ctx_synchronize. NULLs unregister; a new
+ * system upload unregisters. No counterpart in the reference (its kernels
+ * write caller arrays directly, proj/include/mdvec/kernels.hpp ForceResult). */
+int mdg_set_force_output(mdg_ctx* ctx, double* fx, double* fy, double* fz);
 int mdg_fetch_torques(mdg_ctx* ctx, double* tx, double* ty, double* tz);
 int mdg_fetch_dipoles(mdg_ctx* ctx, double* mux, double* muy, double* muz);
 /* Permanent field (PCG right-hand side) of the last step / PCG solve. */

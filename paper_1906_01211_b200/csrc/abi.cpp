@@ -23,8 +23,11 @@ namespace {
 
 thread_local std::string g_err;
 
+std::atomic<uint64_t> g_api_seq{0};  // API calls so far (process-wide)
+
 template <class F>
 int guard(F&& f) {
+  g_api_seq.fetch_add(1, std::memory_order_relaxed);
   try {
     f();
     return MDG_OK;
@@ -376,6 +379,7 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
     c->lz = lz;
     for (auto& Lst : c->lists) Lst.valid = false;
     c->has_mpoles = c->has_hred = c->has_mol = c->has_frames = false;
+    c->fout[0] = c->fout[1] = c->fout[2] = nullptr;  // sized for the old system
     spatial_sort(c, x, y, z);
     stage_in(c, {x, y, z, charge, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, polarizability});
     mdg::pack_system(c);
@@ -1028,6 +1032,17 @@ int mdg_ewald_recip(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
 
 // ---- fused steps ---------------------------------------------------------------
 
+// Queue the D2H of the final forces into the registered outputs on the
+// current stream (the aux stream while the PCG still runs on the main one).
+static void queue_force_output(mdg_ctx* c) {
+  if (!c->fout[0]) return;
+  mdg::gather_vec_to_caller(c, c->force, c->d_fout);
+  for (int a = 0; a < 3; ++a)
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c->fout[a], c->d_fout + a * c->n, c->n * sizeof(double),
+                                   cudaMemcpyDeviceToHost, c->stream));
+  c->fout_seq = g_api_seq.load(std::memory_order_relaxed);
+}
+
 int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
   return guard([&] {
     need_system(c);
@@ -1038,6 +1053,7 @@ int mdg_charmm_step(mdg_ctx* c, int list_id, const mdg_charmm_params* p) {
     mdg::NonpolarArgs a{1, 1, p->shift, p->exclude, p->cutoff, p->alpha, p->electric};
     mdg::run_nonpolar(c, list_id, a);
     c->pcg_iters = 0;
+    queue_force_output(c);
   });
 }
 
@@ -1108,6 +1124,10 @@ static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_
         MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
       }
     }
+    // forces are final at the end of the aux chain unless polarization
+    // forces or frame torques still add to them
+    const bool late_forces =
+        (polar && (terms & MDG_TERM_POLAR_FORCE)) || (c->has_frames && (terms & MDG_TERM_MPOLE));
     {
       mdg::AuxScope aux(c, ov);
       if (terms & MDG_TERM_MPOLE) {
@@ -1116,6 +1136,7 @@ static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_
       } else {
         mdg::zero_vec(c, c->torque);
       }
+      if (!late_forces) queue_force_output(c);  // overlaps what is left of the PCG
     }
     c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
     c->pcg_rms = 0;
@@ -1136,6 +1157,7 @@ static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_
       c->has_polar_force = true;
     }
     if ((terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
+    if (late_forces) queue_force_output(c);
   }
 }
 
@@ -1336,7 +1358,31 @@ int mdg_timer_stop(mdg_ctx* c, double* ms) {
 int mdg_fetch_forces(mdg_ctx* c, double* fx, double* fy, double* fz) {
   return guard([&] {
     need_system(c);
+    // the step just before this call already DMA'd into these buffers
+    if (c->fout[0] && fx == c->fout[0] && fy == c->fout[1] && fz == c->fout[2] &&
+        c->fout_seq + 1 == g_api_seq.load(std::memory_order_relaxed)) {
+      MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      return;
+    }
     vec_out(c, c->force, fx, fy, fz);
+  });
+}
+
+int mdg_set_force_output(mdg_ctx* c, double* fx, double* fy, double* fz) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // no DMA into the old buffers in flight
+    if (!fx && !fy && !fz) {
+      c->fout[0] = c->fout[1] = c->fout[2] = nullptr;
+      return;
+    }
+    need(is_pinned(fx) && is_pinned(fy) && is_pinned(fz),
+         "set_force_output: buffers must be page-locked (mdg_host_alloc)");
+    if (!c->d_fout) MDG_CUDA_CHECK(cudaMalloc(&c->d_fout, 3 * (size_t)c->n_cap * sizeof(double)));
+    c->fout[0] = fx;
+    c->fout[1] = fy;
+    c->fout[2] = fz;
   });
 }
 

@@ -197,6 +197,11 @@ struct mdg_ctx {
   double* aux_partials = nullptr;
   int64_t aux_partial_blocks = 0;
   cudaEvent_t ev_fork = nullptr, ev_tpre = nullptr, ev_join = nullptr;
+  // registered page-locked force outputs (mdg_set_force_output): the step
+  // DMAs caller-order forces into them as soon as they are final
+  double* fout[3] = {nullptr, nullptr, nullptr};
+  double* d_fout = nullptr;    // 3 n doubles, caller order
+  uint64_t fout_seq = 0;       // API call sequence number of the step that queued it
   // single-domain PCG iterations as one device-side while graph (no host
   // round trip per iteration); rebuilt when its captured arguments change
   cudaGraph_t pcg_graph = nullptr;

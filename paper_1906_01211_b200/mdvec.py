@@ -156,6 +156,7 @@ SIGNATURES = {
     "mdg_probe_erfc": (C.c_int, [C.c_int, _dp, C.c_int64, _dp]),
     "mdg_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64]),
     "mdg_host_free": (C.c_int, [C.c_void_p]),
+    "mdg_set_force_output": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_nlist_count_within": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_int, _i64p,
                                          _i64p]),
     "mdg_water_generate": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp,
@@ -626,6 +627,19 @@ class Engine:
             fx, fy, fz = out[0], out[1], out[2]
         check(self.lib.mdg_fetch_forces(self.ctx, _p(fx), _p(fy), _p(fz)))
         return _aos(fx, fy, fz)
+
+    def set_force_output(self, out=None):
+        """Register a (3, n) page-locked block (host_array) that every later
+        step fills with its forces by DMA, overlapped with the rest of the
+        step (mdg.h mdg_set_force_output); fetch_forces(out=that block) then
+        only waits. None unregisters."""
+        if out is None:
+            check(self.lib.mdg_set_force_output(self.ctx, None, None, None))
+            self._fout = None
+            return
+        assert out.shape == (3, self.n) and out.dtype == np.float64 and out.flags.c_contiguous
+        check(self.lib.mdg_set_force_output(self.ctx, _p(out[0]), _p(out[1]), _p(out[2])))
+        self._fout = out  # keep the buffer alive while registered
 
     def fetch_torques(self) -> np.ndarray:
         tx, ty, tz = self._vec3()

@@ -414,6 +414,44 @@ def test_amoeba_step_composes(engine, oracle, mdg):
     np.testing.assert_allclose(w, hv.virial + wm, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("polar_force", [False, True])
+def test_registered_force_output(engine, mdg, polar_force):
+    """mdg_set_force_output: the step DMAs its final forces into the
+    registered page-locked block (early, beside the PCG, or at the end when
+    polarization forces still add to them); fetch_forces on that block right
+    after the step only waits, and any call in between falls back to a fresh
+    copy -- same bits as the plain fetch either way."""
+    s = amoeba_small(mdg, 343, 21.0, 6)
+    engine.upload_system(s)
+    tv = engine.build_neighbor_table(10.0, list_id=1, sites=mdg.SITES_VDW)
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR
+    if polar_force:
+        terms |= mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
+    n = len(s.x)
+    buf = mdg.host_array((3, n))
+    engine.set_force_output(buf)
+    try:
+        for between in (False, True, False):
+            buf[:] = np.nan
+            engine.amoeba_step(tv, te, p)
+            if between:
+                engine.fetch_energies()
+            f = engine.fetch_forces(out=buf)
+            ref = engine.fetch_forces()
+            assert np.array_equal(f, ref)
+            assert np.isfinite(buf).all()
+        with pytest.raises(mdg.ContractViolation):
+            engine.set_force_output(np.zeros((3, n)))  # pageable: rejected
+    finally:
+        engine.set_force_output(None)
+    engine.amoeba_step(tv, te, p)
+    buf[:] = 0.0
+    f = engine.fetch_forces(out=buf)  # unregistered: plain copy
+    assert np.array_equal(f, engine.fetch_forces())
+
+
 def test_half_rows_match_deterministic_full_rows(engine, mdg):
     """Default mode (each owned pair once, partner force/torque by atomics)
     against the deterministic full-row mode, and the latter bitwise
