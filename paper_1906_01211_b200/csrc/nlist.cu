@@ -206,6 +206,137 @@ __global__ void __launch_bounds__(kBlock) k_nlist_build(
   }
 }
 
+// Cell-per-warp build: every site of a cell has the same candidate runs, so
+// one warp walks them once for up to 32 of the cell's owned sites at a time
+// (site q of the group keeps its row length in lane q): each candidate's id
+// and position are loaded once per group instead of once per site. Rows are
+// identical to k_nlist_build's (same candidate order).
+__global__ void __launch_bounds__(kBlock) k_nlist_cells(
+    int64_t ncell, int64_t n_own, const double4* __restrict__ P, Grid g,
+    const int32_t* __restrict__ start, const int32_t* __restrict__ atoms, Box b, double c2,
+    int32_t cap, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+    const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
+  __shared__ int32_t run_s[kWarps][64], run_p[kWarps][64];
+  __shared__ int32_t site_i[kWarps][32];
+  __shared__ double4 site_p[kWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* rs = run_s[warp];
+  int32_t* rp = run_p[warp];
+  int32_t* si = site_i[warp];
+  double4* sp = site_p[warp];
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < ncell; c += nwarps) {
+    const int32_t c0 = start[c], c1 = start[c + 1];
+    if (c0 == c1) continue;
+    const int cz = (int)(c % g.ncz), cy = (int)((c / g.ncz) % g.ncy),
+              cx = (int)(c / ((int64_t)g.ncz * g.ncy));
+    int xs[kSpan], ys[kSpan], zlo[2], zhi[2];
+    const int nx = axis_cells(cx, g.ncx, xs), ny = axis_cells(cy, g.ncy, ys),
+              nz = axis_runs(cz, g.ncz, zlo, zhi);
+    const int nruns = nx * ny * nz;
+    // interior cell: no candidate is across a periodic boundary and every
+    // |d| < 3 cells < L/2, so wrap1(d) == d bit for bit (rint(d/L) == 0):
+    // the displacement is a plain subtraction
+    const bool interior = g.ncx > 3 * kSpan / 2 && g.ncy > 3 * kSpan / 2 &&
+                          g.ncz > 3 * kSpan / 2 && cx >= kReach && cx + kReach < g.ncx &&
+                          cy >= kReach && cy + kReach < g.ncy && cz >= kReach &&
+                          cz + kReach < g.ncz;
+    __syncwarp();
+    int len0 = 0, len1 = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      int len = 0;
+      if (r < nruns) {
+        const int q = r % nz, ab = r / nz;
+        const int col = (xs[ab / ny] * g.ncy + ys[ab % ny]) * g.ncz;
+        const int32_t s0 = start[col + zlo[q]];
+        rs[r] = s0;
+        len = start[col + zhi[q] + 1] - s0;
+      }
+      if (h == 0) len0 = len; else len1 = len;
+    }
+    int inc0 = len0, inc1 = len1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(0xffffffffu, inc0, o);
+      const int t1 = __shfl_up_sync(0xffffffffu, inc1, o);
+      if (lane >= o) { inc0 += t0; inc1 += t1; }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+    rp[lane] = inc0 - len0;
+    rp[lane + 32] = tot0 + inc1 - len1;
+    const int total = tot0 + __shfl_sync(0xffffffffu, inc1, 31);
+    auto slot_of = [&](int v) {
+      int lo = 0, hi = nruns - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= v) lo = mid; else hi = mid - 1;
+      }
+      return rs[lo] + (v - rp[lo]);
+    };
+    // the cell's owned sites, 32 at a time
+    for (int32_t e0 = c0; e0 < c1; e0 += 32) {
+      const int32_t site = (e0 + lane < c1) ? atoms[e0 + lane] : -1;
+      const bool own = site >= 0 && site < n_own;
+      const unsigned om = __ballot_sync(0xffffffffu, own);
+      const int ns = __popc(om);
+      if (ns == 0) continue;
+      __syncwarp();
+      if (own) {
+        const int q = __popc(om & lanemask_lt());
+        si[q] = site;
+        sp[q] = P[site];
+      }
+      __syncwarp();
+      int k = 0;  // row length of group site `lane`
+      int32_t ja = (lane < total) ? __ldg(atoms + slot_of(lane)) : -1;
+      for (int base = 0; base < total; base += 32) {
+        const int vn = base + 32 + lane;
+        const int32_t jb = (vn < total) ? __ldg(atoms + slot_of(vn)) : -1;
+        double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (ja >= 0) pj = ldg4(P + ja);
+        for (int q = 0; q < ns; ++q) {
+          const int32_t i = si[q];
+          const double4 pi = sp[q];
+          bool in = false;
+          if (ja >= 0 && ja != i) {
+            double dx, dy, dz;
+            if (interior)
+              in = dist2(__dsub_rn(pi.x, pj.x), __dsub_rn(pi.y, pj.y), __dsub_rn(pi.z, pj.z)) <= c2;
+            else
+              in = min_image(b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= c2;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, in);
+          const int kq = __shfl_sync(0xffffffffu, k, q);
+          if (in) {
+            const int32_t pos = kq + __popc(m & lanemask_lt());
+            if (pos < cap) nbr[(size_t)i * (size_t)cap + pos] = ja;
+          }
+          if (lane == q) k += __popc(m);
+        }
+        ja = jb;
+      }
+      if (lane < ns) cnt[si[lane]] = k;
+      // reference capacity rule (see k_nlist_build): rows longer than the
+      // cap count their upper pairs
+      unsigned big = __ballot_sync(0xffffffffu, lane < ns && k > MDG_MAX_NEIGHBORS && k <= cap);
+      while (big) {
+        const int q = __ffs(big) - 1;
+        big &= big - 1;
+        const int kq = __shfl_sync(0xffffffffu, k, q);
+        const int32_t i = si[q];
+        const int32_t* out = nbr + (size_t)i * (size_t)cap;
+        const int32_t oi = perm[i];
+        int32_t upper = 0;
+        for (int e = lane; e < kq; e += 32) upper += (__ldg(perm + out[e]) > oi) ? 1 : 0;
+        upper = warp_allsum_i(upper);
+        if (lane == 0 && upper > MDG_MAX_NEIGHBORS) atomicMin(&flag[0], oi);
+      }
+    }
+  }
+}
+
 // max and sum of counts -> results[slot], results[slot+1]
 // max and sum of cnt[0..n) over the whole GPU in one launch: block partials
 // go to integer atomics in flag[1] (max), flag[2..3] (sum, int64) and the
@@ -395,12 +526,21 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
   const int64_t rows = c->n_own;  // rows for owned sites; candidates span the halo too
   const int64_t ipb = sites_per_block((const void*)k_nlist_build, rows);
   const unsigned ngrid = (unsigned)((rows + ipb - 1) / ipb);
+  // cell-per-warp kernel (MDG_CELL_BUILD=0: the per-site kernel)
+  static const int cell_build = env_int("MDG_CELL_BUILD", 1);
+  const bool use_cells = cell_build != 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     ensure_list_storage(c, L, cap);
     MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int32_t), c->stream));
-    MDG_LAUNCH(c, "nlist_build", ngrid, kBlock, 0, k_nlist_build, rows, (int)ipb, P,
-               c->cell_of, g, c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt, c->d_perm,
-               c->d_flag);
+    if (use_cells) {
+      MDG_LAUNCH(c, "nlist_cells", (unsigned)std::min<int64_t>((ncell + kWarps - 1) / kWarps, 148 * 64),
+                 kBlock, 0, k_nlist_cells, ncell, rows, P, g, c->cell_start, c->cell_atoms, b, c2,
+                 cap, L.nbr, L.cnt, c->d_perm, c->d_flag);
+    } else {
+      MDG_LAUNCH(c, "nlist_build", ngrid, kBlock, 0, k_nlist_build, rows, (int)ipb, P,
+                 c->cell_of, g, c->cell_start, c->cell_atoms, b, c2, cap, L.nbr, L.cnt,
+                 c->d_perm, c->d_flag);
+    }
     count_stats(c, L.cnt, 60);
     int32_t bad_site = 0;
     MDG_CUDA_CHECK(cudaMemcpyAsync(&bad_site, c->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,

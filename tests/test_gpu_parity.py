@@ -30,6 +30,18 @@ def test_pairs_match_brute_force(engine, oracle, seed, n):
     np.testing.assert_array_equal(t.pairs(), oracle.brute_force_pairs(s, 3.4))
 
 
+@pytest.mark.parametrize("n,box,cut", [(4200, 24.0, 9.0), (3000, 30.0, 7.0)])
+def test_pairs_crowded_and_sparse_cells(engine, oracle, n, box, cut):
+    """The cell-per-warp builder serves up to 32 of a cell's sites per sweep
+    of its candidates; crowded cells (first case: ~34 sites per cell, every
+    site a candidate of every cell) take several groups. Both cases give the
+    oracle's pair set."""
+    s = uniform(oracle, n, box, 11, min_sep=0.5)
+    engine.upload_system(s)
+    np.testing.assert_array_equal(engine.build_neighbor_table(cut).pairs(),
+                                  oracle.brute_force_pairs(s, cut))
+
+
 def test_pairs_match_reference_table_water(engine, oracle, mdg):
     """Config-0 water box at the 11 A list: pair set identical to the oracle's
     reference-layout table (itself identical to the reference, test_oracle.py)."""
