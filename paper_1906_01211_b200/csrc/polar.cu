@@ -595,6 +595,11 @@ static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
                                 (uintptr_t)k.trr, (uintptr_t)k.pcap, (uintptr_t)c->partials,
                                 (uintptr_t)ipb, (uintptr_t)max_iter,
                                 (uintptr_t)tol_bits, (uintptr_t)c->stream};
+  {  // the box is captured by value
+    uint64_t w[sizeof(Box) / sizeof(uint64_t)];
+    std::memcpy(w, &k.b, sizeof w);
+    for (uint64_t x : w) key.push_back((uintptr_t)x);
+  }
   if (!c->pcg_exec || key != c->pcg_key) {
     if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
     if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);

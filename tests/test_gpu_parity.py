@@ -575,6 +575,24 @@ def test_pcg_device_loop_max_iter_and_profiled_loop(engine, oracle, mdg):
     np.testing.assert_allclose(a.mu, b.mu, rtol=0, atol=1e-13 * np.abs(a.mu).max())
 
 
+def test_pcg_graph_follows_new_box(engine, mdg):
+    """The captured PCG loop is keyed on everything it holds by value: a new
+    system of the same size in a different box re-captures it (dipoles as
+    from a fresh context)."""
+    pp = mdg.PolarParams(7.0, 0.39)
+    a = amoeba_small(mdg, 343, 21.0, 11)
+    b = amoeba_small(mdg, 343, 23.5, 12)
+    engine.upload_system(a)
+    engine.polar_solve_pcg(engine.build_neighbor_table(9.0), pp, 0.5446, 1e-7, 100, True)
+    engine.upload_system(b)
+    got = engine.polar_solve_pcg(engine.build_neighbor_table(9.0), pp, 0.5446, 1e-7, 100, True)
+    with mdg.Engine(b.n_sites) as e:
+        e.upload_system(b)
+        want = e.polar_solve_pcg(e.build_neighbor_table(9.0), pp, 0.5446, 1e-7, 100, True)
+    assert got.iterations == want.iterations
+    np.testing.assert_array_equal(got.mu, want.mu)
+
+
 def test_config4_full_size_properties(mdg):
     """BASELINE config 4 at full size (999,999 atoms), through size-independent
     properties: the 9 A list's pair count equals a KD-tree count, pair forces
