@@ -1287,7 +1287,7 @@ int mdo_pcg(const mdo_system* s, const mdo_table* t, double alpha, double cutoff
         q[k] = p[k] / s->polarizability[i] - tp[k];
         pq += p[k] * q[k];
       }
-    const double ak = rz / pq;
+    const double ak = pq != 0.0 ? rz / pq : 0.0;  /* p == 0: r == 0, exact already */
     double dsum = 0.0, rz_new = 0.0;
     for (size_t i = 0; i < n; ++i)
       for (int a = 0; a < 3; ++a) {
@@ -1303,7 +1303,7 @@ int mdo_pcg(const mdo_system* s, const mdo_table* t, double alpha, double cutoff
     *iters = it + 1;
     *last_rms = rms;
     if (rms < tol_debye) break;
-    const double bk = rz_new / rz;
+    const double bk = rz != 0.0 ? rz_new / rz : 0.0;
     rz = rz_new;
     for (size_t k = 0; k < m; ++k) p[k] = z[k] + bk * p[k];
   }

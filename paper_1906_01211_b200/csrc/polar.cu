@@ -527,15 +527,17 @@ __global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks
       res[21] = s[0][0];
       res[27] = 0.0;
     } else if (mode == 1) {
+      // p.q == 0 only for p == 0 (r == 0: already exact); a_k = 0 then
+      // leaves mu unchanged and the rms test stops the loop, no 0/0
       res[20] = s[0][0];
-      res[26] = res[21] / s[0][0];
+      res[26] = (s[0][0] != 0.0) ? res[21] / s[0][0] : 0.0;
     } else {
       const double rz_new = s[0][0];
       res[22] = rz_new;
       res[23] = s[1][0];
       const double rms = sqrt(s[1][0] / (double)n) * kDebye;
       res[25] = rms;
-      res[24] = rz_new / res[21];
+      res[24] = (res[21] != 0.0) ? rz_new / res[21] : 0.0;
       res[21] = rz_new;
       res[27] = (rms < tol) ? 1.0 : 0.0;
     }
@@ -706,7 +708,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
       fetch_results(c);
       double pq = c->h_results[20];
       dd_allreduce(c, &pq, 1);
-      put_result(c, 26, rz / pq);  // a_k from global sums
+      put_result(c, 26, pq != 0.0 ? rz / pq : 0.0);  // a_k from global sums
     }
     MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
                c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
@@ -717,7 +719,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
       double v[2] = {c->h_results[22], c->h_results[23]};  // local rz_new, sum |dmu|^2
       dd_allreduce(c, v, 2);
       const double rms = std::sqrt(v[1] / n_glob) * kDebye;
-      put_result(c, 24, v[0] / rz);  // beta
+      put_result(c, 24, rz != 0.0 ? v[0] / rz : 0.0);  // beta
       rz = v[0];
       put_result(c, 21, rz);
       *last_rms = rms;

@@ -593,6 +593,52 @@ def test_pcg_graph_follows_new_box(engine, mdg):
     np.testing.assert_array_equal(got.mu, want.mu)
 
 
+def test_isolated_sites_no_pairs(engine, oracle, mdg):
+    """Edge case: every list row empty (2x2x2 lattice at 20 A spacing). Pair
+    kernels return exact zeros, the PCG starts converged (E = 0, so mu = 0),
+    the fused step composes to zeros -- no NaN from 0/0 in the CG scalars."""
+    s = oracle.generate_system("lattice", 8, (40.0, 40.0, 40.0), 3)
+    engine.upload_system(s)
+    engine.upload_multipoles(np.zeros((8, 3)), np.zeros((8, 6)))
+    t = engine.build_neighbor_table(9.0)
+    assert len(t.pairs()) == 0
+    lj = engine.lj_forces(t, mdg.LjParams(9.0))
+    assert lj.energy == 0.0 and not np.any(lj.forces)
+    hv = engine.halgren_forces(t, mdg.HalgrenParams(9.0))
+    assert hv.energy == 0.0 and not np.any(hv.forces)
+    st = engine.polar_solve_pcg(t, mdg.PolarParams(7.0, 0.39), 0.5446, 1e-5, 100, True)
+    assert np.isfinite(st.mu).all() and not np.any(st.mu)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1,
+                         mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE)
+    engine.amoeba_step(t, t, p)
+    e, w, iters, rms = engine.fetch_energies()
+    assert np.isfinite(e).all() and np.isfinite(w).all() and rms == 0.0
+    f = engine.fetch_forces()
+    assert np.isfinite(f).all() and not np.any(f)
+
+
+def test_rows_longer_than_sort_limit(engine, oracle, mdg):
+    """Rows over 1024 slots are left unsorted; the half-row kernels then
+    split pairs by index in their prologue. Same forces as the deterministic
+    full rows and the oracle."""
+    s = uniform(oracle, 3000, 20.0, 5, min_sep=0.5)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.5)
+    lp = mdg.LjParams(9.5)
+    half = engine.lj_forces(t, lp)
+    engine.set_deterministic(True)
+    try:
+        full = engine.lj_forces(t, lp)
+    finally:
+        engine.set_deterministic(False)
+    np.testing.assert_allclose(half.forces, full.forces, rtol=0,
+                               atol=1e-11 * np.abs(full.forces).max())
+    assert rel(half.energy, full.energy) < 1e-12
+    fo, eo, _ = oracle.lj(s, oracle.build_table(s, 9.5), 9.5)
+    assert rel(half.energy, eo) <= E_TOL
+    assert force_err_rms(half.forces, fo) <= F_TOL
+
+
 def test_config4_full_size_properties(mdg):
     """BASELINE config 4 at full size (999,999 atoms), through size-independent
     properties: the 9 A list's pair count equals a KD-tree count, pair forces

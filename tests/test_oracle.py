@@ -416,6 +416,15 @@ def test_pcg_matches_dense_solve(oracle):
         assert np.abs(mu - x).max() <= 1e-9 * np.abs(x).max()
 
 
+def test_pcg_zero_field_is_converged(oracle):
+    """Edge case: no permanent field (no pairs, or all charges zero) --
+    mu = 0 after one step, no 0/0 in a_k or beta."""
+    s = oracle.generate_system("uniform", 15, (9, 9, 9), 21)
+    t = oracle.build_table(s, 3.0)
+    mu, it, rms = oracle.pcg(s, t, 0.5, 3.0, 0.39, np.zeros((15, 3)), 1e-5, 10)
+    assert np.isfinite(mu).all() and not np.any(mu) and rms == 0.0 and it == 1
+
+
 def test_pcg_agrees_with_jacobi_where_it_converges(oracle):
     s = oracle.generate_system("uniform", 15, (9, 9, 9), 21)
     t = oracle.build_table(s, 3.0)
