@@ -617,6 +617,34 @@ def test_isolated_sites_no_pairs(engine, oracle, mdg):
     assert np.isfinite(f).all() and not np.any(f)
 
 
+@pytest.mark.parametrize("n", [1, 2])
+def test_tiny_systems(mdg, oracle, n):
+    """One and two sites (the reference's smallest systems): list, pair
+    kernels, PCG and the fused step on a context sized exactly n."""
+    from oracle.oracle import System
+    x = np.array([1.0, 3.5])[:n]
+    one = np.ones(n)
+    s = System((10.0, 10.0, 10.0), x.copy(), one * 2.0, one * 2.0, np.array([0.4, -0.4])[:n],
+               one * 3.0, one * 0.1, one * 3.2, one * 0.05, one * 1.1)
+    with mdg.Engine(n) as e:
+        e.upload_system(s)
+        e.upload_multipoles(np.zeros((n, 3)), np.zeros((n, 6)))
+        t = e.build_neighbor_table(4.5)
+        assert len(t.pairs()) == n - 1
+        t_o = oracle.build_table(s, 4.5)
+        fo, eo, _ = oracle.lj(s, t_o, 4.0)
+        g = e.lj_forces(t, mdg.LjParams(4.0))
+        assert rel(g.energy, eo) <= E_TOL and force_err_rms(g.forces, fo) <= F_TOL
+        p = mdg.AmoebaParams(4.0, 0.07, 0.12, 4.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1,
+                             mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR |
+                             mdg.TERM_POLAR_FORCE)
+        e.amoeba_step(t, t, p)
+        en, w, iters, rms = e.fetch_energies()
+        f = e.fetch_forces()
+        assert np.isfinite(en).all() and np.isfinite(f).all() and rms < 1e-5
+        np.testing.assert_allclose(f.sum(0), 0.0, atol=1e-12 * (np.abs(f).max() + 1))
+
+
 def test_rows_longer_than_sort_limit(engine, oracle, mdg):
     """Rows over 1024 slots are left unsorted; the half-row kernels then
     split pairs by index in their prologue. Same forces as the deterministic
