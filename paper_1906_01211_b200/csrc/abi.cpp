@@ -3,6 +3,7 @@
 // spatial sort, list import/export in the reference NeighborTable layout,
 // and the fused steps. No kernels here; they live in the .cu files.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <functional>
@@ -257,6 +258,9 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       dalloc(&c->pos, n);
       dalloc(&c->vsite, n);
       dalloc(&c->vdwp, n);
+      dalloc(&c->vtype, n);
+      dalloc(&c->vtab, (size_t)kMaxVdwTypes);
+      dalloc(&c->ptab, (size_t)kMaxVdwTypes);
       dalloc(&c->polp, n);
       dalloc(&c->mol, n);
       dalloc(&c->hpar, n);
@@ -291,7 +295,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
-  void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->polp, c->mol, c->hpar, c->hfac,
+  void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->vtype, c->vtab, c->ptab, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->frame, c->mploc, c->fbuf, c->fref_start,
                   c->excl_start, c->excl, c->vel, c->bond_ij, c->bond_par, c->angle_ijk,
                   c->angle_par,
@@ -347,6 +351,30 @@ int mdg_system_upload(mdg_ctx* c, int64_t n, double lx, double ly, double lz, co
                                  hal_r0, hal_epsilon, polarizability);
 }
 
+// Distinct (sigma, eps_lj, r0, eps_hal, charge, polarizability) tuples (bitwise) in sorted order:
+// vtype[s] = type of sorted site s, rep[t] = first sorted site of type t.
+// False when there are more than kMaxVdwTypes tuples (per-site gathers then).
+static bool assign_vdw_types(const std::vector<int32_t>& perm, const double* sig,
+                             const double* eps, const double* r0, const double* eh,
+                             const double* q, const double* pol, std::vector<int32_t>& vtype,
+                             std::vector<int32_t>& rep) {
+  std::map<std::array<uint64_t, 6>, int32_t> types;
+  for (size_t s = 0; s < vtype.size(); ++s) {
+    const int64_t o = perm[s];
+    const double v[6] = {sig[o], eps[o], r0[o], eh[o], q[o], pol[o]};
+    std::array<uint64_t, 6> key;
+    std::memcpy(key.data(), v, sizeof v);
+    auto it = types.find(key);
+    if (it == types.end()) {
+      if ((int)types.size() == kMaxVdwTypes) return false;
+      it = types.emplace(key, (int32_t)types.size()).first;
+      rep.push_back((int32_t)s);
+    }
+    vtype[s] = it->second;
+  }
+  return true;
+}
+
 int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_global,
                             double lx, double ly, double lz, const double* x, const double* y,
                             const double* z, const double* charge, const double* lj_sigma,
@@ -382,7 +410,20 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
     c->fout[0] = c->fout[1] = c->fout[2] = nullptr;  // sized for the old system
     spatial_sort(c, x, y, z);
     stage_in(c, {x, y, z, charge, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, polarizability});
+    // vdW parameter types (bitwise-distinct tuples, in sorted order)
+    std::vector<int32_t> vtype(n), rep;
+    c->n_vtypes = 0;
+    if (assign_vdw_types(c->perm, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, charge,
+                         polarizability, vtype, rep) &&
+        !mdg::env_int("MDG_NO_VDW_TYPES", 0)) {
+      MDG_CUDA_CHECK(cudaMemcpyAsync(c->vtype, vtype.data(), n * 4, cudaMemcpyHostToDevice,
+                                     c->stream));
+      c->n_vtypes = (int)rep.size();
+    } else {
+      rep.clear();
+    }
     mdg::pack_system(c);
+    mdg::set_vdw_types(c, rep);
     // identity topology: every site its own group, no reduction
     std::vector<int32_t> ident(n);
     std::iota(ident.begin(), ident.end(), 0);

@@ -27,10 +27,14 @@ __device__ __forceinline__ double dist2(double dx, double dy, double dz) {
 // value as a double), so the pair prologues test exclusions on the gathered
 // position instead of a second gather (Halgren 3.11 -> 2.96 ms). (The
 // permanent-field pass keeps its int32 group gather: measured faster there.)
-__host__ __device__ __forceinline__ double group_bits(int32_t g) { return (double)g; }
+// Bit layout of w: low word = exclusion group, high word = vdW parameter type
+// (mdg_ctx::vtab). Only moved and compared as integers, never used in FP math.
+__device__ __forceinline__ double group_bits(int32_t g, int32_t type) {
+  return __hiloint2double(type, g);
+}
 
 __device__ __forceinline__ bool same_group(const double4& a, const double4& b) {
-  return a.w == b.w;
+  return __double2loint(a.w) == __double2loint(b.w);
 }
 
 // d = r_i - r_j, minimum image; returns r2
@@ -243,12 +247,13 @@ struct Ring {
   int count;   // warp-uniform
 };
 
+// entry w: low word = j (with any flag bit), high word = j's vdW type
 __device__ __forceinline__ void ring_push(Ring& r, bool in, double dx, double dy, double dz,
-                                          int32_t j) {
+                                          int32_t j, int32_t type) {
   const unsigned m = __ballot_sync(0xffffffffu, in);
   if (in) {
     const int pos = (r.head + r.count + __popc(m & lanemask_lt())) & (kRing - 1);
-    r.q[pos] = make_double4(dx, dy, dz, __longlong_as_double((long long)j));
+    r.q[pos] = make_double4(dx, dy, dz, __hiloint2double(type, j));
   }
   r.count += __popc(m);
   __syncwarp();
@@ -264,9 +269,9 @@ __device__ __forceinline__ double4 ring_take(Ring& r, int take, int lane) {
   return e;
 }
 
-__device__ __forceinline__ int32_t ring_j(const double4& e) {
-  return (int32_t)__double_as_longlong(e.w);
-}
+__device__ __forceinline__ int32_t ring_j(const double4& e) { return __double2loint(e.w); }
+
+__device__ __forceinline__ int32_t ring_type(const double4& e) { return __double2hiint(e.w); }
 
 // Walk one site's row with the warp: software-pipelined so the index load of
 // chunk c+2 and the position gather of chunk c+1 are in flight while chunk c
@@ -277,7 +282,10 @@ __device__ __forceinline__ int32_t ring_j(const double4& e) {
 // of in-range entries.
 // `mol` (may be NULL) is gathered with the positions so the exclusion test
 // does not wait on its own load; pro(raw, pj, mol_j, dx, dy, dz).
-template <class Pro, class Body>
+// TYPED: the ring entries also carry j's site type (high word of pj.w) for
+// bodies that read per-type tables (ring_type); off, the entry is (dx, dy,
+// dz, j) only -- the extra live word cost the register-capped field pass.
+template <bool TYPED = false, class Pro, class Body>
 __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt, int lane,
                                        const double4* __restrict__ P,
                                        const int32_t* __restrict__ mol, Ring& ring, Pro&& pro,
@@ -297,7 +305,7 @@ __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt,
     if (base + 64 + lane < cnt) jc = __ldg(row + base + 64 + lane);
     double dx = 0, dy = 0, dz = 0;
     const bool in = (base + lane < cnt) && pro(ja, pa, ma, dx, dy, dz);
-    ring_push(ring, in, dx, dy, dz, ja);
+    ring_push(ring, in, dx, dy, dz, ja, TYPED ? __double2hiint(pa.w) : 0);
     if (ring.count >= 32) {
       body(ring_take(ring, 32, lane), taken + lane);
       taken += 32;

@@ -228,7 +228,8 @@ void run_reduce_sites(mdg_ctx* c) {
 __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
                               const double* __restrict__ st, double4* __restrict__ pos,
                               double4* __restrict__ vsite, double4* __restrict__ vdwp,
-                              double2* __restrict__ polp, double4* __restrict__ pq4) {
+                              double2* __restrict__ polp, double4* __restrict__ pq4,
+                              const int32_t* __restrict__ vtype) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t o = perm[s];
@@ -236,8 +237,9 @@ __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
   const double q = st[3 * n + o];
   // w of pos / vsite: the site's exclusion group (identity until
   // mdg_topology_upload; see set_groups), read by the pair prologues
-  pos[s] = make_double4(x, y, z, group_bits((int32_t)s));
-  vsite[s] = make_double4(x, y, z, group_bits((int32_t)s));
+  const int32_t t = vtype ? vtype[s] : 0;
+  pos[s] = make_double4(x, y, z, group_bits((int32_t)s, t));
+  vsite[s] = make_double4(x, y, z, group_bits((int32_t)s, t));
   vdwp[s] = make_double4(st[4 * n + o], sqrt(st[5 * n + o]), st[6 * n + o], sqrt(st[7 * n + o]));
   const double pol = st[8 * n + o];
   const double pd = cbrt(sqrt(pol));
@@ -247,7 +249,8 @@ __global__ void k_pack_system(int64_t n, const int32_t* __restrict__ perm,
 
 void pack_system(mdg_ctx* c) {
   MDG_LAUNCH(c, "pack_system", grid_for(c->n, 256), 256, 0, k_pack_system, c->n, c->d_perm,
-             c->d_stage, c->pos, c->vsite, c->vdwp, c->polp, c->pq4);
+             c->d_stage, c->pos, c->vsite, c->vdwp, c->polp, c->pq4,
+             c->n_vtypes ? c->vtype : nullptr);
 }
 
 // staging: x y z (caller order); keeps charges
@@ -286,16 +289,42 @@ int64_t check_box_staged(mdg_ctx* c) {
   return bad == 0x7f7f7f7f ? -1 : bad;
 }
 
-__global__ void k_set_groups(int64_t n, const int32_t* __restrict__ mol, double4* __restrict__ pos,
+__global__ void k_set_groups(int64_t n, const int32_t* __restrict__ mol,
+                             const int32_t* __restrict__ vtype, double4* __restrict__ pos,
                              double4* __restrict__ vsite) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
-  pos[s].w = group_bits(mol[s]);
-  vsite[s].w = group_bits(mol[s]);
+  const int32_t t = vtype ? vtype[s] : 0;
+  pos[s].w = group_bits(mol[s], t);
+  vsite[s].w = group_bits(mol[s], t);
+}
+
+__global__ void k_vtab(int nt, const int32_t* __restrict__ rep, const double4* __restrict__ vdwp,
+                       const double4* __restrict__ pq4, double4* __restrict__ vtab,
+                       double4* __restrict__ ptab) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nt) {
+    vtab[t] = vdwp[rep[t]];
+    ptab[t] = pq4[rep[t]];
+  }
+}
+
+// rep[t] = a sorted-order site of type t; vtype already on the device.
+// vtab / ptab are bit copies of those sites' vdwp / pq4 records (the values a
+// gather would read).
+void set_vdw_types(mdg_ctx* c, const std::vector<int32_t>& rep) {
+  c->n_vtypes = (int)rep.size();
+  if (rep.empty()) return;
+  int32_t* d_rep = c->d_idx;  // staging (n >= n_vtypes)
+  MDG_CUDA_CHECK(cudaMemcpyAsync(d_rep, rep.data(), rep.size() * 4, cudaMemcpyHostToDevice,
+                                 c->stream));
+  MDG_LAUNCH(c, "vtab", 1, kMaxVdwTypes, 0, k_vtab, (int)rep.size(), d_rep, c->vdwp, c->pq4,
+             c->vtab, c->ptab);
 }
 
 void set_groups(mdg_ctx* c) {
-  MDG_LAUNCH(c, "set_groups", grid_for(c->n, 256), 256, 0, k_set_groups, c->n, c->mol, c->pos,
+  MDG_LAUNCH(c, "set_groups", grid_for(c->n, 256), 256, 0, k_set_groups, c->n, c->mol,
+             c->n_vtypes ? c->vtype : nullptr, c->pos,
              c->vsite);
 }
 

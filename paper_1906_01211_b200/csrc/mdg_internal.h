@@ -92,6 +92,8 @@ struct PendingEvent {
 
 }  // namespace mdg
 
+constexpr int kMaxVdwTypes = 64;
+
 struct mdg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -121,6 +123,16 @@ struct mdg_ctx {
   double4* pos = nullptr;
   double4* vsite = nullptr;
   double4* vdwp = nullptr;
+  // Site parameter types: when the system has <= kMaxVdwTypes distinct
+  // (sigma, eps_lj, r0, eps_hal, charge, polarizability) tuples, vtab[t] /
+  // ptab[t] hold the vdwp / pq4 records of a representative site and the type rides in the high word of
+  // pos.w / vsite.w, so the LJ / Halgren bodies read j's parameters from a
+  // table every lane shares instead of a 32-B gather per pair (charges and
+  // Thole factors likewise from ptab).
+  int32_t* vtype = nullptr;
+  double4* vtab = nullptr;
+  double4* ptab = nullptr;  // pq4 record of each type's representative site
+  int n_vtypes = 0;  // 0: per-site parameters (vdwp gathers)
   double2* polp = nullptr;
   double4* pq4 = nullptr;  // (polarizability, polarizability^(1/6), charge, alpha^(-1/6))
   int32_t* mol = nullptr;
@@ -392,6 +404,7 @@ void gather_vec_to_caller(mdg_ctx* c, const double4* sorted, double* d_dst_soa);
 void scatter_vec_from_caller(mdg_ctx* c, const double* d_src_soa, double4* sorted);
 void zero_vec(mdg_ctx* c, double4* v);
 void pack_system(mdg_ctx* c);
+void set_vdw_types(mdg_ctx* c, const std::vector<int32_t>& rep);
 double4* vec_by_id(mdg_ctx* c, int vec_id);
 void vec_pack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count, double* d_out);
 void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,

@@ -20,7 +20,9 @@ struct NonpolarKArgs {
   int ipw;
   const double4* __restrict__ pos;
   const double4* __restrict__ vdwp;
+  const double4* __restrict__ vtab;  // vdW type table, or NULL: per-site vdwp of j
   const double4* __restrict__ pq4;  // charges (z)
+  const double4* __restrict__ ptab;  // site-type copy of pq4, or NULL: per-site pq4 of j
   const int32_t* __restrict__ mol;
   ListView L;
   Box b;
@@ -53,7 +55,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       // pair weight: 1/2 for a halo partner (the other domain has the mirror)
       const double w = (HALF && j >= a.n_i) ? 0.5 : 1.0;
       if (LJ) {
-        const double4 vj = ldg4(a.vdwp + j);
+        const double4 vj = a.vtab ? ldg4(a.vtab + ring_type(e)) : ldg4(a.vdwp + j);
         const double sij = 0.5 * (vi.x + vj.x);
         const double eij = vi.y * vj.y;
         const double inv_r2 = 1.0 / r2;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
       if (COUL) {
         const double inv_r = rsqrt(r2);  // one MUFU.RSQ64H + Newton, no division
         const double r = r2 * inv_r;
-        const double qq = a.electric * qi * __ldg(&a.pq4[j].z);
+        const double qq = a.electric * qi * __ldg(&(a.ptab ? a.ptab + ring_type(e) : a.pq4 + j)->z);
         const double ar = a.alpha * r;
         const double ex2 = exp(-ar * ar);
         const double ee = erfc_from_exp(ar, ex2) * inv_r;
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
     };
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
-    run_row(
+    run_row<true>(
         row + start, cnt - start, lane, a.pos, nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
@@ -145,7 +147,9 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.n_i = c->n_own;
   k.pos = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
+  k.vtab = c->n_vtypes ? c->vtab : nullptr;
   k.pq4 = c->pq4;
+  k.ptab = c->n_vtypes ? c->ptab : nullptr;
   k.mol = c->mol;
   k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);
@@ -170,6 +174,7 @@ struct HalgrenKArgs {
   int ipw;
   const double4* __restrict__ site;
   const double4* __restrict__ vdwp;
+  const double4* __restrict__ vtab;  // vdW type table, or NULL: per-site vdwp of j
   const int32_t* __restrict__ mol;
   ListView L;
   Box b;
@@ -200,7 +205,8 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
       const int32_t j = ring_j(e);
       const double dx = e.x, dy = e.y, dz = e.z;
       const double r2 = dist2(dx, dy, dz);
-      const double4 vj = ldg4(a.vdwp + j);
+      // j's parameters: the type table (one line shared by the warp) or j's record
+      const double4 vj = a.vtab ? ldg4(a.vtab + ring_type(e)) : ldg4(a.vdwp + j);
       // proj/src/polar_vec.cpp:78-107: all reciprocals from one division
       const double r = sqrt(r2);
       const double r0 = 0.5 * (vi.z + vj.z);
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
     };
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
-    run_row(
+    run_row<true>(
         row + start, cnt - start, lane, a.site, nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
@@ -311,6 +317,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   const bool reduced = (L.sites == MDG_SITES_VDW);
   k.site = reduced ? c->vsite : c->pos;
   k.vdwp = c->vdwp;
+  k.vtab = c->n_vtypes ? c->vtab : nullptr;
   k.mol = c->mol;
   k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
   k.b = make_box(c->lx, c->ly, c->lz);

@@ -497,6 +497,39 @@ def test_half_rows_match_deterministic_full_rows(engine, mdg):
         np.testing.assert_allclose(a, b, rtol=0, atol=1e-12 * np.abs(b).max())
 
 
+def test_site_type_tables_match_per_site_parameters(engine, mdg, monkeypatch):
+    """Water has two parameter tuples, so the pair bodies read j's vdW
+    parameters, charge and Thole factor from the context's type tables (type
+    in the high word of pos.w); with MDG_NO_VDW_TYPES=1 they gather j's
+    per-site records. Same values, so the deterministic (full-row) results of
+    every kernel are bitwise identical."""
+    engine.set_deterministic(True)
+    out = []
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1,
+                         mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE)
+    for flag in ("0", "1"):
+        monkeypatch.setenv("MDG_NO_VDW_TYPES", flag)
+        s = mdg.water_box(343, 21.72, 5, "amoeba")
+        engine.upload_system(s)
+        tv = engine.build_neighbor_table(10.0, list_id=1, sites=mdg.SITES_VDW)
+        te = engine.build_neighbor_table(9.0, list_id=0)
+        h = engine.halgren_forces(tv, mdg.HalgrenParams(9.0), exclude=True)
+        engine.amoeba_step(tv, te, p)
+        e, w, it, _ = engine.fetch_energies()
+        f = engine.fetch_forces()
+        pf, ptq, pe, _ = engine.polar_forces(te, mdg.PolarParams(7.0, 0.39), 0.5446, mdg.ELECTRIC)
+        s = mdg.water_box(343, 21.72, 5, "charmm")
+        engine.upload_system(s)
+        t = engine.build_neighbor_table(10.0)
+        engine.charmm_step(t, mdg.CharmmParams(9.0, 0.35, mdg.ELECTRIC, 0, 1))
+        ec = engine.fetch_energies()[0]
+        fc = engine.fetch_forces()
+        out.append((h.energy, h.forces.copy(), e, w, it, f, pf, ptq, pe, ec, fc))
+    engine.set_deterministic(False)
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("deterministic", [False, True])
 def test_polar_forces_match_oracle(engine, oracle, mdg, deterministic):
     """Polarization forces/torques/virial at fixed dipoles (8(f)#1) vs the
