@@ -154,19 +154,27 @@ class TorchComm:
         self.rank, self.size = dist.get_rank(), dist.get_world_size()
         self.cuda = dist.get_backend(group) == "nccl"
         self.device = torch.device(f"cuda:{device}") if self.cuda else torch.device("cpu")
+        if self.cuda:
+            # create the NCCL communicator with a collective every rank joins
+            # (batched point-to-point must not be the group's first call)
+            self.allreduce(np.zeros(1))
 
     def exchange(self, sends: dict, recv_counts: dict) -> dict:
-        """sends: peer -> float64 buffer; returns peer -> received buffer."""
-        t = self.torch
-        reqs, out = [], {}
+        """sends: peer -> float64 buffer; returns peer -> received buffer.
+        All receives and sends go out as one batch (ncclGroupStart/End under
+        NCCL): two ranks that each post recv-then-send on the shared pair
+        stream would otherwise wait on each other."""
+        t, dist = self.torch, self.dist
+        ops, out = [], {}
         for q, n in recv_counts.items():
             out[q] = t.empty(n, dtype=t.float64, device=self.device)
-            reqs.append(self.dist.irecv(out[q], src=q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, out[q], q, group=self.group))
         for q, buf in sends.items():
             tb = buf if isinstance(buf, t.Tensor) else t.from_numpy(np.ascontiguousarray(buf))
-            reqs.append(self.dist.isend(tb.to(self.device), dst=q, group=self.group))
-        for r in reqs:
-            r.wait()
+            ops.append(dist.P2POp(dist.isend, tb.to(self.device), q, group=self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
         if self.cuda:
             t.cuda.synchronize(self.device)
         return out
