@@ -309,6 +309,9 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   for (auto& L : c->lists) {
     if (L.nbr) cudaFree(L.nbr);
     if (L.cnt) cudaFree(L.cnt);
+    for (void* p : {(void*)L.inner.nbr, (void*)L.inner.cnt, (void*)L.inner.ref, (void*)L.inner.flag})
+      if (p) cudaFree(p);
+    if (L.inner.hcuts) cudaFreeHost(L.inner.hcuts);
   }
   if (c->plist.nbr) cudaFree(c->plist.nbr);
   if (c->plist.cnt) cudaFree(c->plist.cnt);

@@ -168,6 +168,11 @@ struct ListView {
   bool sorted = false;  // rows ascending in (j & 0x7fffffff)
 };
 
+// Rows a kernel with cutoff rc walks over list `list_id`: the buffered inner
+// list (rows cut to rc + buffer, re-cut on the device when some site has moved
+// more than buffer/2 since the last cut) or the list itself (nlist.cu).
+ListView kernel_rows(mdg_ctx* c, int list_id, double rc);
+
 __device__ __forceinline__ const int32_t* list_row(const ListView& L, int64_t i) {
   return L.nbr + (size_t)i * (size_t)L.cap;
 }

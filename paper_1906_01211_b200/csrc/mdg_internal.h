@@ -62,6 +62,24 @@ struct DevList {
   int32_t max_cnt = 0;
   int64_t version = 0;          // bumped by every (re)build / import
   bool sorted = false;          // every row ascending in j
+  // Buffered inner list (dynamic pruning): the rows cut to kernel cutoff + a
+  // buffer b, valid while no site has moved more than b/2 since the cut
+  // (checked on the device every call; the cut is redone when it fails).
+  struct Inner {
+    double rc = 0;                // cut radius (kernel cutoff + buffer)
+    int64_t src_version = -1;     // source list version it was cut from
+    int32_t* nbr = nullptr;
+    int32_t* cnt = nullptr;
+    size_t elems = 0;
+    double4* ref = nullptr;       // site positions at the cut
+    int32_t* flag = nullptr;      // device: 1 = cut again
+    // cuts done, counted by the cut kernel in mapped page-locked memory (read
+    // by the host without a sync): when most calls need a new cut (sites
+    // moving fast), the buffer only adds a pass, so the rows are bypassed
+    int32_t* hcuts = nullptr;
+    int32_t* dcuts = nullptr;
+    int calls = 0, cuts0 = 0, bypass = 0;
+  } inner;
 };
 
 // Pruned list: the pairs of a source list within a kernel cutoff, compacted

@@ -271,7 +271,7 @@ void run_mpole(mdg_ctx* c, int list_id, double alpha, double cutoff, double elec
   k.mp = c->mp;
   k.pq4 = c->pq4;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
+  k.L = kernel_rows(c, list_id, cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.alpha = alpha;

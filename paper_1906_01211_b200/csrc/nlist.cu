@@ -574,4 +574,138 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
   throw_error(MDG_CUDA, "nlist_build: capacity retry failed");
 }
 
+// ---- buffered inner lists (dynamic pruning) ---------------------------------
+// flag = 1 when some site has moved more than half the buffer since the cut
+// (minimum image: a site wrapped back into the box across a face has moved
+// only its step's distance)
+__global__ void k_moved(int64_t n, Box b, const double4* __restrict__ P,
+                        const double4* __restrict__ ref, double lim2,
+                        int32_t* __restrict__ flag) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool moved = false;
+  if (s < n) {
+    const double4 p = P[s], r = ref[s];
+    double dx, dy, dz;
+    moved = min_image(b, p.x, p.y, p.z, r.x, r.y, r.z, dx, dy, dz) > lim2;
+  }
+  if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+struct CutArgs {
+  int64_t n_rows, n_all;
+  int ipw;
+  const double4* __restrict__ P;
+  ListView src;
+  Box b;
+  double rc2;
+  int32_t* __restrict__ nbr;
+  int32_t* __restrict__ cnt;
+  double4* __restrict__ ref;
+  const int32_t* __restrict__ flag;
+  int32_t* __restrict__ cuts;  // mapped host counter
+  double* __restrict__ partials;  // unused (launch macro contract)
+};
+
+// When *flag: every owned row keeps its slots with r^2 <= rc^2 (the
+// reference's wrap1/dist2 test, order kept: sorted rows stay sorted) and the
+// reference positions are refreshed for all sites. Otherwise returns at once.
+__global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
+  if (*a.flag == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid == 0) atomicAdd_system(a.cuts, 1);
+  for (int64_t s = tid; s < a.n_all; s += (int64_t)gridDim.x * blockDim.x) a.ref[s] = a.P[s];
+  MDG_SITE_LOOP(i, a.n_rows, a.ipw) {
+    const double4 pi = a.P[i];
+    const int c = a.src.cnt[i];
+    const int32_t* row = list_row(a.src, i);
+    int32_t* out = a.nbr + (size_t)i * a.src.cap;
+    int kept = 0;
+    for (int base = 0; base < c; base += 32) {
+      const int k = base + lane;
+      const int32_t j = k < c ? __ldg(row + k) : 0;
+      bool keep = false;
+      if (k < c) {
+        const double4 pj = ldg4(a.P + (j & 0x7fffffff));
+        double dx, dy, dz;
+        keep = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz) <= a.rc2;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) out[kept + __popc(m & lanemask_lt())] = j;
+      kept += __popc(m);
+    }
+    if (lane == 0) a.cnt[i] = kept;
+  }
+}
+
+ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
+  DevList& L = c->lists[list_id];
+  const ListView full{L.nbr, L.cnt, L.cap, L.sorted};
+  // buffer (A): MDG_PRUNE_BUFFER, 0 = walk the full list
+  static const double buf = [] {
+    const char* e = std::getenv("MDG_PRUNE_BUFFER");
+    return e ? std::atof(e) : 0.5;
+  }();
+  const double rcut = rc + buf;
+  if (buf <= 0 || rcut >= L.cutoff) return full;
+  DevList::Inner& I = L.inner;
+  if (!I.hcuts) {
+    MDG_CUDA_CHECK(cudaHostAlloc(&I.hcuts, sizeof(int32_t), cudaHostAllocMapped));
+    *I.hcuts = 0;
+    MDG_CUDA_CHECK(cudaHostGetDevicePointer(&I.dcuts, I.hcuts, 0));
+  }
+  if (I.bypass > 0) {
+    --I.bypass;
+    return full;
+  }
+  if (++I.calls >= 4) {  // cut on 3 or 4 of the last 4 calls: bypass the next 128
+    const int cuts = *(volatile int32_t*)I.hcuts;
+    if (2 * (cuts - I.cuts0) > I.calls) {
+      I.bypass = 128;
+      I.src_version = -1;  // cut afresh afterwards
+    }
+    I.calls = 0;
+    I.cuts0 = cuts;
+    if (I.bypass) return full;
+  }
+  const size_t need = (size_t)c->n_own * (size_t)L.cap;
+  if (need > I.elems) {
+    if (I.nbr) cudaFree(I.nbr);
+    I.nbr = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&I.nbr, need * sizeof(int32_t)));
+    I.elems = need;
+    I.src_version = -1;
+  }
+  if (!I.cnt) MDG_CUDA_CHECK(cudaMalloc(&I.cnt, (size_t)c->n_cap * sizeof(int32_t)));
+  if (!I.ref) MDG_CUDA_CHECK(cudaMalloc(&I.ref, (size_t)c->n_cap * sizeof(double4)));
+  if (!I.flag) MDG_CUDA_CHECK(cudaMalloc(&I.flag, sizeof(int32_t)));
+  const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+  const bool stale = I.src_version != L.version || I.rc != rcut;
+  if (stale) {
+    const int32_t one = 1;  // cut unconditionally
+    MDG_CUDA_CHECK(cudaMemcpyAsync(I.flag, &one, sizeof one, cudaMemcpyHostToDevice, c->stream));
+    I.src_version = L.version;
+    I.rc = rcut;
+  } else {
+    MDG_CUDA_CHECK(cudaMemsetAsync(I.flag, 0, sizeof(int32_t), c->stream));
+    const double half = 0.5 * buf;
+    MDG_LAUNCH(c, "moved", grid_for(c->n, 256), 256, 0, k_moved, c->n,
+               make_box(c->lx, c->ly, c->lz), P, I.ref, half * half, I.flag);
+  }
+  CutArgs k;
+  k.n_rows = c->n_own;
+  k.n_all = c->n;
+  k.P = P;
+  k.src = full;
+  k.b = make_box(c->lx, c->ly, c->lz);
+  k.rc2 = rcut * rcut;
+  k.nbr = I.nbr;
+  k.cnt = I.cnt;
+  k.ref = I.ref;
+  k.flag = I.flag;
+  k.cuts = I.dcuts;
+  MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
+  return ListView{I.nbr, I.cnt, L.cap, L.sorted};
+}
+
 }  // namespace mdg

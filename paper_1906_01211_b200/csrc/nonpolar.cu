@@ -151,7 +151,7 @@ void run_nonpolar(mdg_ctx* c, int list_id, const NonpolarArgs& a) {
   k.pq4 = c->pq4;
   k.ptab = c->n_vtypes ? c->ptab : nullptr;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
+  k.L = kernel_rows(c, list_id, a.cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = a.cutoff * a.cutoff;
   k.alpha = a.alpha;
@@ -319,7 +319,7 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.vdwp = c->vdwp;
   k.vtab = c->n_vtypes ? c->vtab : nullptr;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
+  k.L = kernel_rows(c, list_id, cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.delta = delta;

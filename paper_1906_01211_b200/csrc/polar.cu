@@ -105,7 +105,7 @@ void run_tmatvec(mdg_ctx* c, int list_id, double alpha, double cutoff, double th
   k.pos = c->pos;
   k.polp = c->polp;
   k.pq4 = c->pq4;
-  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.L = kernel_rows(c, list_id, cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.alpha = alpha;
@@ -264,7 +264,7 @@ static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   k.pq4 = c->pq4;
   k.mp = c->mp;
   k.mol = c->mol;
-  k.L = ListView{L.nbr, L.cnt, L.cap};
+  k.L = kernel_rows(c, list_id, cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.alpha = alpha;

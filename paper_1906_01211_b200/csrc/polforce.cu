@@ -295,7 +295,7 @@ void run_polar_force(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
                      double electric, int exclude, bool accumulate) {
   const DevList& L = c->lists[list_id];
   PFArgs k = pf_args(c, alpha, thole_a, electric, accumulate);
-  k.L = ListView{L.nbr, L.cnt, L.cap, L.sorted};
+  k.L = kernel_rows(c, list_id, cutoff);
   k.c2 = cutoff * cutoff;
   launch_polar_force<false>(c, k, exclude && c->has_mol, !c->deterministic);
 }

@@ -530,6 +530,37 @@ def test_site_type_tables_match_per_site_parameters(engine, mdg, monkeypatch):
         assert np.array_equal(a, b)
 
 
+def test_buffered_rows_follow_motion(engine, oracle, mdg):
+    """The kernels walk rows cut to cutoff + 0.5 A (MDG_PRUNE_BUFFER) from the
+    11 A list; the cut is redone on the device once some site has moved more
+    than 0.25 A. Moves of 0.2 A (no new cut) and then 0.45 A in total (new cut)
+    from the build positions: LJ on the unchanged 11 A list still matches the
+    oracle on a table built at the new positions, so no pair that came within
+    the cutoff was dropped."""
+    s = mdg.water_box(1000, 31.04, 11, "charmm")
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(11.0)
+    rng = np.random.default_rng(5)
+    d = rng.normal(size=(s.n_sites, 3))
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    L = s.box[0]
+    for step in (0.2, 0.45):
+        x = np.mod(np.asarray(s.x) + step * d[:, 0], L)
+        y = np.mod(np.asarray(s.y) + step * d[:, 1], L)
+        z = np.mod(np.asarray(s.z) + step * d[:, 2], L)
+        x[x >= L] = 0.0
+        y[y >= L] = 0.0
+        z[z >= L] = 0.0
+        engine.upload_positions(x, y, z)
+        so = to_oracle_system(s)
+        so.x, so.y, so.z = x, y, z
+        t_o = oracle.build_table(so, 11.0)
+        fo, eo, _ = oracle.lj(so, t_o, 9.0, exclude=True)
+        g = engine.lj_forces(t, mdg.LjParams(9.0), exclude=True)
+        assert rel(g.energy, eo) <= E_TOL
+        assert force_err_rms(g.forces, fo) <= F_TOL
+
+
 @pytest.mark.parametrize("deterministic", [False, True])
 def test_polar_forces_match_oracle(engine, oracle, mdg, deterministic):
     """Polarization forces/torques/virial at fixed dipoles (8(f)#1) vs the
