@@ -507,17 +507,29 @@ __global__ void k_cg_dir(int64_t n, const double* __restrict__ res, const double
 // Fixed-order sums of the CG partials plus the scalar recurrences.
 // mode 0: rz0 -> res[21]; mode 1: p.q -> a = rz/pq -> res[26];
 // mode 2: rz_new, dsum -> beta, rms, converged.
-__global__ void k_cg_scalars(const double* __restrict__ partials, int64_t blocks, int mode,
-                             int64_t n, double tol, double* __restrict__ res) {
-  __shared__ double s[2][256];
+constexpr int kScalarThreads = 1024;
+__global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __restrict__ partials,
+                                                               int64_t blocks, int mode, int64_t n,
+                                                               double tol, double* __restrict__ res) {
+  // one block of 1024 threads, 4 independent loads in flight per thread: the
+  // iteration's critical path waits on this sum twice (was 256 threads and
+  // one dependent load chain: ~20 us per call on 2e4 partials)
+  __shared__ double s[2][kScalarThreads];
   const int nv = (mode == 2) ? 2 : 1;
   for (int v = 0; v < nv; ++v) {
-    double acc = 0.0;
-    for (int64_t b = threadIdx.x; b < blocks; b += 256) acc += partials[b * kRedVals + v];
-    s[v][threadIdx.x] = acc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t b = threadIdx.x;
+    for (; b + 3 * kScalarThreads < blocks; b += 4 * kScalarThreads) {
+      a0 += partials[b * kRedVals + v];
+      a1 += partials[(b + kScalarThreads) * kRedVals + v];
+      a2 += partials[(b + 2 * kScalarThreads) * kRedVals + v];
+      a3 += partials[(b + 3 * kScalarThreads) * kRedVals + v];
+    }
+    for (; b < blocks; b += kScalarThreads) a0 += partials[b * kRedVals + v];
+    s[v][threadIdx.x] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
+  for (int w = kScalarThreads / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w)
       for (int v = 0; v < nv; ++v) s[v][threadIdx.x] += s[v][threadIdx.x + w];
     __syncthreads();
@@ -622,11 +634,11 @@ static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
     MDG_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
                                                  cudaStreamCaptureModeRelaxed));
     k_tmatvec_pre<true><<<(unsigned)g, kBlock, 0, c->stream>>>(k);
-    k_cg_scalars<<<1, 256, 0, c->stream>>>(c->partials, g, 1, n, tol_debye, c->results);
+    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, g, 1, n, tol_debye, c->results);
     k_cg_update<<<(unsigned)blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
                                                            c->cg_q, c->mu, c->cg_r, c->cg_z,
                                                            c->partials);
-    k_cg_scalars<<<1, 256, 0, c->stream>>>(c->partials, blocks, 2, n, tol_debye, c->results);
+    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, blocks, 2, n, tol_debye, c->results);
     k_pcg_continue<<<1, 1, 0, c->stream>>>(h, c->results, max_iter);
     k_cg_dir<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->results, c->cg_z, c->cg_p);
     cudaGraph_t captured = nullptr;
@@ -685,7 +697,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   MDG_LAUNCH_SITES(c, "tmatvec_pre", n, k, k_tmatvec_pre<false>);
   MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
              c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
-  MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
+  MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
              c->results);
   double rz = 0.0;  // global r.z (multi-domain path)
   if (dd) {
@@ -702,7 +714,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   for (int64_t it = 1; it <= max_iter; ++it) {
     if (dd) dd_exchange(c, MDG_VEC_P);
     MDG_LAUNCH_SITES(c, "tmatvec_pcg", n, k, k_tmatvec_pre<true>);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, c->last_grid, 1, n,
+    MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, c->last_grid, 1, n,
                tol_debye, c->results);
     if (dd) {
       fetch_results(c);
@@ -712,7 +724,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
     }
     MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
                c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
-    MDG_LAUNCH(c, "cg_scalars", 1, 256, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
+    MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
                c->results);
     fetch_results(c);
     if (dd) {
