@@ -394,77 +394,97 @@ void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
 // in register r of `lane`; strides < 32 exchange by shuffle, larger ones
 // within the lane. R = padded row length / 32 (a power of two).
 template <int R>
+__device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int m, int lane) {
+  int32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = r * 32 + lane;
+    v[r] = (e < m) ? row[e] : 0x7fffffff;
+  }
+#pragma unroll
+  for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & jr) == 0) {
+            const int e = r * 32 + lane;
+            const bool asc = (e & k) == 0;
+            const int32_t a = v[r], b = v[r | jr];
+            if ((a > b) == asc) { v[r] = b; v[r | jr] = a; }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = r * 32 + lane;
+          const int32_t b = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool keep_min = ((e & j) == 0) == ((e & k) == 0);
+          v[r] = keep_min ? min(v[r], b) : max(v[r], b);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = r * 32 + lane;
+    if (e < m) row[e] = v[r];
+  }
+}
+
+// One launch sorts every row of up to 32 RMAX slots, each padded only to the
+// next power of two of its own length (a 9.5 A row of ~330 slots sorts as 512,
+// not as the list's longest row). flag (may be NULL): sort only when *flag
+// (the device-decided cut of kernel_rows).
+template <int RMAX>
 __global__ void __launch_bounds__(kBlock) k_sort_rows(int64_t n, int32_t* __restrict__ nbr,
-                                                    const int32_t* __restrict__ cnt, int32_t cap) {
+                                                    const int32_t* __restrict__ cnt, int32_t cap,
+                                                    const int32_t* __restrict__ flag) {
+  if (flag && *flag == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   for (int64_t i = blockIdx.x * (int64_t)(kBlock / 32) + (threadIdx.x >> 5); i < n; i += warps) {
     const int m = cnt[i];
-    if (m < 2) continue;
+    if (m < 2 || m > 32 * RMAX) continue;
     int32_t* row = nbr + (size_t)i * cap;
-    int32_t v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int e = r * 32 + lane;
-      v[r] = (e < m) ? row[e] : 0x7fffffff;
-    }
-#pragma unroll
-    for (int k = 2; k <= 32 * R; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        if (j >= 32) {
-          const int jr = j >> 5;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            if ((r & jr) == 0) {
-              const int e = r * 32 + lane;
-              const bool asc = (e & k) == 0;
-              const int32_t a = v[r], b = v[r | jr];
-              if ((a > b) == asc) { v[r] = b; v[r | jr] = a; }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const int e = r * 32 + lane;
-            const int32_t b = __shfl_xor_sync(0xffffffffu, v[r], j);
-            const bool keep_min = ((e & j) == 0) == ((e & k) == 0);
-            v[r] = keep_min ? min(v[r], b) : max(v[r], b);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int e = r * 32 + lane;
-      if (e < m) row[e] = v[r];
-    }
+    if (m <= 32) sort_row<1>(row, m, lane);
+    else if (RMAX >= 2 && m <= 64) sort_row<(RMAX >= 2 ? 2 : 1)>(row, m, lane);
+    else if (RMAX >= 4 && m <= 128) sort_row<(RMAX >= 4 ? 4 : 1)>(row, m, lane);
+    else if (RMAX >= 8 && m <= 256) sort_row<(RMAX >= 8 ? 8 : 1)>(row, m, lane);
+    else if (RMAX >= 16 && m <= 512) sort_row<(RMAX >= 16 ? 16 : 1)>(row, m, lane);
+    else if (RMAX >= 32) sort_row<(RMAX >= 32 ? 32 : 1)>(row, m, lane);
   }
 }
 
-static bool sort_rows(mdg_ctx* c, DevList& L, int32_t max_cnt) {
+// Sort the rows (<= 1024 slots) of nbr/cnt in one launch sized by max_cnt.
+// Returns false when sorting is disabled (MDG_SORT_ROWS=0).
+static bool sort_rows(mdg_ctx* c, int32_t* nbr, const int32_t* cnt, int32_t cap,
+                      int32_t max_cnt, const int32_t* flag = nullptr) {
   static const int enabled = [] {
     const char* e = getenv("MDG_SORT_ROWS");
     return e ? atoi(e) : 1;
   }();
   // sorted rows also let the half-row kernels start at the first j > i
-  if (!enabled || max_cnt > 1024) return false;
+  // (row_suffix; rows longer than 1024 stay unsorted and are walked whole)
+  if (!enabled) return false;
   if (max_cnt < 2) return true;
   const int64_t rows = c->n_own;
   const unsigned grid = (unsigned)std::min<int64_t>(148 * 16, (rows + 3) / 4);
-  const int need = (max_cnt + 31) / 32;
+  const int need = (std::min(1024, (int)max_cnt) + 31) / 32;
   if (need <= 1)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<1>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<1>, rows, nbr, cnt, cap, flag);
   else if (need <= 2)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<2>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<2>, rows, nbr, cnt, cap, flag);
   else if (need <= 4)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<4>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<4>, rows, nbr, cnt, cap, flag);
   else if (need <= 8)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<8>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<8>, rows, nbr, cnt, cap, flag);
   else if (need <= 16)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<16>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<16>, rows, nbr, cnt, cap, flag);
   else
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<32>, rows, L.nbr, L.cnt, L.cap);
+    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<32>, rows, nbr, cnt, cap, flag);
   return true;
 }
 
@@ -560,7 +580,9 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
                                     ")");
     }
     if (mx <= cap) {
-      L.sorted = sort_rows(c, L, mx);
+      // rows stay in candidate order here; kernel_rows sorts the rows the
+      // kernels walk (the buffered cut, or this list on its first use)
+      L.sorted = false;
       L.valid = true;
       L.version = ++c->epoch;
       L.cutoff = list_cutoff;
@@ -640,14 +662,20 @@ __global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
 
 ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   DevList& L = c->lists[list_id];
-  const ListView full{L.nbr, L.cnt, L.cap, L.sorted};
+  auto full_rows = [&] {
+    if (!L.sorted) L.sorted = sort_rows(c, L.nbr, L.cnt, L.cap, L.max_cnt);
+    return ListView{L.nbr, L.cnt, L.cap, L.sorted};
+  };
+  const ListView full{L.nbr, L.cnt, L.cap, false};  // cut source: any order
   // buffer (A): MDG_PRUNE_BUFFER, 0 = walk the full list
-  static const double buf = [] {
-    const char* e = std::getenv("MDG_PRUNE_BUFFER");
-    return e ? std::atof(e) : 0.5;
-  }();
+  // (read per call: tests switch it)
+  const char* eb = std::getenv("MDG_PRUNE_BUFFER");
+  const double buf = eb ? std::atof(eb) : 0.5;
+  // small systems: the per-call check and gated launches cost more than the
+  // shorter rows save (MDG_PRUNE_MIN_SITES)
+  const int min_sites = env_int("MDG_PRUNE_MIN_SITES", 50000);
   const double rcut = rc + buf;
-  if (buf <= 0 || rcut >= L.cutoff) return full;
+  if (buf <= 0 || rcut >= L.cutoff || c->n_own < min_sites) return full_rows();
   DevList::Inner& I = L.inner;
   if (!I.hcuts) {
     MDG_CUDA_CHECK(cudaHostAlloc(&I.hcuts, sizeof(int32_t), cudaHostAllocMapped));
@@ -656,7 +684,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   }
   if (I.bypass > 0) {
     --I.bypass;
-    return full;
+    return full_rows();
   }
   if (++I.calls >= 4) {  // cut on 3 or 4 of the last 4 calls: bypass the next 128
     const int cuts = *(volatile int32_t*)I.hcuts;
@@ -666,7 +694,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
     }
     I.calls = 0;
     I.cuts0 = cuts;
-    if (I.bypass) return full;
+    if (I.bypass) return full_rows();
   }
   const size_t need = (size_t)c->n_own * (size_t)L.cap;
   if (need > I.elems) {
@@ -705,7 +733,9 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   k.flag = I.flag;
   k.cuts = I.dcuts;
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
-  return ListView{I.nbr, I.cnt, L.cap, L.sorted};
+  // the cut rows are short: sort them (bucketed by length), when cut
+  const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);
+  return ListView{I.nbr, I.cnt, L.cap, sorted};
 }
 
 }  // namespace mdg

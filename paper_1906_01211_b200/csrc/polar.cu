@@ -336,7 +336,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
     const int32_t mx = (int32_t)c->h_results[62];
     if (mx <= cap) {
       P.valid = true;
-      P.sorted = L.sorted;
+      P.sorted = k.L.sorted;  // the rows walked (buffered cut or the list)
       P.src = list_id;
       P.cutoff = cutoff;
       P.directed = (int64_t)c->h_results[63];

@@ -14,6 +14,10 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
 def pytest_configure(config):
+    # the parity tests run on small systems: let them take the buffered-row
+    # path (nlist.cu kernel_rows) that production sizes (>= 50k sites) take;
+    # tests switch MDG_PRUNE_BUFFER=0 where they need the plain rows
+    os.environ.setdefault("MDG_PRUNE_MIN_SITES", "0")
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")
 

@@ -530,13 +530,15 @@ def test_site_type_tables_match_per_site_parameters(engine, mdg, monkeypatch):
         assert np.array_equal(a, b)
 
 
-def test_buffered_rows_follow_motion(engine, oracle, mdg):
+@pytest.mark.parametrize("buffer", ["0.5", "0"])
+def test_buffered_rows_follow_motion(engine, oracle, mdg, monkeypatch, buffer):
     """The kernels walk rows cut to cutoff + 0.5 A (MDG_PRUNE_BUFFER) from the
     11 A list; the cut is redone on the device once some site has moved more
     than 0.25 A. Moves of 0.2 A (no new cut) and then 0.45 A in total (new cut)
     from the build positions: LJ on the unchanged 11 A list still matches the
     oracle on a table built at the new positions, so no pair that came within
-    the cutoff was dropped."""
+    the cutoff was dropped. Buffer 0: the plain (lazily sorted) 11 A rows."""
+    monkeypatch.setenv("MDG_PRUNE_BUFFER", buffer)
     s = mdg.water_box(1000, 31.04, 11, "charmm")
     engine.upload_system(s)
     t = engine.build_neighbor_table(11.0)
