@@ -166,6 +166,7 @@ struct ListView {
   const int32_t* cnt;
   int32_t cap;
   bool sorted = false;  // rows ascending in (j & 0x7fffffff)
+  bool dense = false;   // buffered cut rows: nearly every slot in range (DIRECT walk)
 };
 
 // Rows a kernel with cutoff rc walks over list `list_id`: the buffered inner
@@ -290,7 +291,12 @@ __device__ __forceinline__ int32_t ring_type(const double4& e) { return __double
 // TYPED: the ring entries also carry j's site type (high word of pj.w) for
 // bodies that read per-type tables (ring_type); off, the entry is (dx, dy,
 // dz, j) only -- the extra live word cost the register-capped field pass.
-template <bool TYPED = false, class Pro, class Body>
+// DIRECT: no compaction -- the in-range lanes run the body on their own slot.
+// For rows that are nearly all in range (the 7 A pruned rows, the buffered
+// cut rows: ~85 %) the ring's shared-memory round trip (32 B in, 32 B out per
+// pair, on the same L1 data pipe as the gathers) costs more than the idle
+// lanes; for full skin rows (~50 % in range) the ring wins.
+template <bool TYPED = false, bool DIRECT = false, class Pro, class Body>
 __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt, int lane,
                                        const double4* __restrict__ P,
                                        const int32_t* __restrict__ mol, Ring& ring, Pro&& pro,
@@ -310,10 +316,18 @@ __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt,
     if (base + 64 + lane < cnt) jc = __ldg(row + base + 64 + lane);
     double dx = 0, dy = 0, dz = 0;
     const bool in = (base + lane < cnt) && pro(ja, pa, ma, dx, dy, dz);
-    ring_push(ring, in, dx, dy, dz, ja, TYPED ? __double2hiint(pa.w) : 0);
-    if (ring.count >= 32) {
-      body(ring_take(ring, 32, lane), taken + lane);
-      taken += 32;
+    if constexpr (DIRECT) {
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (in)
+        body(make_double4(dx, dy, dz, __hiloint2double(TYPED ? __double2hiint(pa.w) : 0, ja)),
+             taken + __popc(m & lanemask_lt()));
+      taken += __popc(m);
+    } else {
+      ring_push(ring, in, dx, dy, dz, ja, TYPED ? __double2hiint(pa.w) : 0);
+      if (ring.count >= 32) {
+        body(ring_take(ring, 32, lane), taken + lane);
+        taken += 32;
+      }
     }
     ja = jb;
     pa = pb;

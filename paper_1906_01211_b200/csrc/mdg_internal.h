@@ -72,7 +72,7 @@ struct DevList {
     int32_t* cnt = nullptr;
     size_t elems = 0;
     double4* ref = nullptr;       // site positions at the cut
-    int32_t* flag = nullptr;      // device: 1 = cut again
+    int32_t* flag = nullptr;      // device: 1 = cut again (motion), 2 = forced (new list)
     // cuts done, counted by the cut kernel in mapped page-locked memory (read
     // by the host without a sync): when most calls need a new cut (sites
     // moving fast), the buffer only adds a pass, so the rows are bypassed

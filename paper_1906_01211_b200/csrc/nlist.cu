@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
   if (*a.flag == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid == 0) atomicAdd_system(a.cuts, 1);
+  if (tid == 0 && *a.flag == 1) atomicAdd_system(a.cuts, 1);  // motion cuts only (2: forced)
   for (int64_t s = tid; s < a.n_all; s += (int64_t)gridDim.x * blockDim.x) a.ref[s] = a.P[s];
   MDG_SITE_LOOP(i, a.n_rows, a.ipw) {
     const double4 pi = a.P[i];
@@ -686,7 +686,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
     --I.bypass;
     return full_rows();
   }
-  if (++I.calls >= 4) {  // cut on 3 or 4 of the last 4 calls: bypass the next 128
+  if (++I.calls >= 4) {  // motion cut on 3 or 4 of the last 4 calls: bypass the next 128
     const int cuts = *(volatile int32_t*)I.hcuts;
     if (2 * (cuts - I.cuts0) > I.calls) {
       I.bypass = 128;
@@ -710,8 +710,9 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   const bool stale = I.src_version != L.version || I.rc != rcut;
   if (stale) {
-    const int32_t one = 1;  // cut unconditionally
-    MDG_CUDA_CHECK(cudaMemcpyAsync(I.flag, &one, sizeof one, cudaMemcpyHostToDevice, c->stream));
+    // cut unconditionally (2: forced, not counted as motion by the bypass)
+    MDG_CUDA_CHECK(cudaMemsetAsync(I.flag, 0, sizeof(int32_t), c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(I.flag, 2, 1, c->stream));
     I.src_version = L.version;
     I.rc = rcut;
   } else {
@@ -735,7 +736,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
   // the cut rows are short: sort them (bucketed by length), when cut
   const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);
-  return ListView{I.nbr, I.cnt, L.cap, sorted};
+  return ListView{I.nbr, I.cnt, L.cap, sorted, true};
 }
 
 }  // namespace mdg

@@ -32,7 +32,7 @@ struct NonpolarKArgs {
 };
 
 // partial slots: 0 E_lj, 1 E_coul, 2..7 virial (xx xy xz yy yz zz)
-template <bool LJ, bool COUL, bool SHIFT, bool EXCL, bool HALF>
+template <bool LJ, bool COUL, bool SHIFT, bool EXCL, bool HALF, bool DIRECT>
 __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kBlock) k_nonpolar(NonpolarKArgs a) {
     };
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
-    run_row<true>(
+    run_row<true, DIRECT>(
         row + start, cnt - start, lane, a.pos, nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
@@ -130,8 +130,13 @@ static void launch_np(mdg_ctx* c, const NonpolarKArgs& k, bool shift, bool excl,
   NonpolarKArgs kk = k;
 #define NP_CASE(S, E)                                                              \
   if (shift == S && excl == E) {                                                 \
-    if (half) MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, true>));  \
-    else MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, false>));      \
+    if (kk.L.dense) {                                                            \
+      if (half) MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, true, true>)); \
+      else MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, false, true>));     \
+    } else {                                                                     \
+      if (half) MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, true, false>)); \
+      else MDG_LAUNCH_SITES(c, name, kk.n_i, kk, (k_nonpolar<LJ, COUL, S, E, false, false>));    \
+    }                                                                            \
     return;                                                                      \
   }
   NP_CASE(false, false)
@@ -188,7 +193,7 @@ struct HalgrenKArgs {
 // in the owned row only (their mirror is the other domain's). Energy and
 // virial are weighted 1 (owned pair) or 1/2 (halo pair), finalize scale 1.
 // !HALF: full rows, each pair in both rows at weight 1/2 (finalize scale).
-template <bool EXCL, bool HALF>
+template <bool EXCL, bool HALF, bool DIRECT>
 __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
     };
     // half rows: a sorted row's pairs with j > i are its suffix
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
-    run_row<true>(
+    run_row<true, DIRECT>(
         row + start, cnt - start, lane, a.site, nullptr, ring,
         [&](int32_t j, const double4& pj, int32_t, double& dx, double& dy, double& dz) {
           const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
@@ -326,16 +331,19 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.gamma = gamma;
   k.force = reduced ? c->force2 : c->force;
   const bool ex = exclude && c->has_mol;
+  const bool dn = k.L.dense;
+#define HAL_LAUNCH(E, H)                                                              \
+  if (dn) MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<E, H, true>));          \
+  else MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<E, H, false>));
   if (c->deterministic) {
-    if (ex) MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<true, false>));
-    else MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<false, false>));
+    if (ex) { HAL_LAUNCH(true, false) } else { HAL_LAUNCH(false, false) }
     finalize_partials(c, c->last_grid, 8, 0, 0.5);
   } else {
     MDG_CUDA_CHECK(cudaMemsetAsync(k.force, 0, (size_t)k.n_i * sizeof(double4), c->stream));
-    if (ex) MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<true, true>));
-    else MDG_LAUNCH_SITES(c, "halgren", k.n_i, k, (k_halgren<false, true>));
+    if (ex) { HAL_LAUNCH(true, true) } else { HAL_LAUNCH(false, true) }
     finalize_partials(c, c->last_grid, 8, 0, 1.0);
   }
+#undef HAL_LAUNCH
   if (reduced) {
     MDG_LAUNCH(c, "chain_rule", grid_for(c->n_own, 256), 256, 0, k_chain_rule, c->n_own, c->force2,
                c->hpar, c->hfac, c->child_start, c->child, c->force);

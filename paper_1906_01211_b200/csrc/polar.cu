@@ -160,7 +160,7 @@ __device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int3
 
 // TPRE: also write the pruned row (all pairs within the cutoff, exclusion
 // flag in bit 31) and its T tensors; the field skips excluded pairs.
-template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE>
+template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE, bool DIRECT = false>
 __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
         ez += cq * dz;
       }
     };
-    const int pn = run_row(
+    const int pn = run_row<false, DIRECT>(
         row, cnt, lane, a.pos, a.mol, ring,
         [&](int32_t& raw, const double4& pj, int32_t mj, double& dx, double& dy, double& dz) {
           const int32_t j = raw & 0x7fffffff;
@@ -327,10 +327,14 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
     k.pcnt = P.cnt;
     k.pcap = cap;
     // rows longer than cap are counted, not written; the retry below grows cap
-    if (mp && ex) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, true, true, true>));
-    else if (mp) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, true, false, true>));
-    else if (ex) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, false, true, true>));
-    else MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, false, false, true>));
+#define TPRE_LAUNCH(M, X)                                                                     \
+  if (k.L.dense) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, M, X, true, true>)); \
+  else MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, M, X, true, false>));
+    if (mp && ex) { TPRE_LAUNCH(true, true) }
+    else if (mp) { TPRE_LAUNCH(true, false) }
+    else if (ex) { TPRE_LAUNCH(false, true) }
+    else { TPRE_LAUNCH(false, false) }
+#undef TPRE_LAUNCH
     count_stats(c, P.cnt, 62);
     fetch_results(c);
     const int32_t mx = (int32_t)c->h_results[62];

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kBlock, MDG_POLFORCE_MINB) k_polar_force(PFArg
       }
     };
     const int start = (HALF && a.L.sorted) ? row_suffix(row, cnt, i, lane) : 0;
-    run_row(
+    run_row<false, PRUNED>(
         row + start, cnt - start, lane, a.pos, nullptr, ring,
         [&](int32_t& raw, const double4& pj, int32_t, double& x, double& y, double& z) {
           const int32_t j = raw & 0x7fffffff;

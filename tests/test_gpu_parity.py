@@ -417,7 +417,10 @@ def test_amoeba_step_composes(engine, oracle, mdg):
     hv = engine.halgren_forces(tv, mdg.HalgrenParams(9.0), exclude=True)
     fm, _, em, wm = engine.mpole_forces(te, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
     st = engine.polar_solve_pcg(te, mdg.PolarParams(7.0, 0.39), 0.5446, 1e-5, 100, True)
-    assert e[0] == hv.energy and e[1] == em
+    # Halgren: the same rows, the same sums. Multipoles: the step walks the
+    # 7 A pruned rows, the standalone call its own cut of the 9 A list --
+    # the same pairs on different lanes, so the sum order differs
+    assert e[0] == hv.energy and rel(e[1], em) <= 1e-12
     # partner forces arrive through atomics (default half-row mode): the sum
     # order, not the terms, can differ between the fused step and its parts
     np.testing.assert_allclose(f, hv.forces + fm, rtol=0, atol=1e-12 * np.abs(f).max())
@@ -656,7 +659,11 @@ def test_pcg_graph_follows_new_box(engine, mdg):
         e.upload_system(b)
         want = e.polar_solve_pcg(e.build_neighbor_table(9.0), pp, 0.5446, 1e-7, 100, True)
     assert got.iterations == want.iterations
-    np.testing.assert_array_equal(got.mu, want.mu)
+    # a stale graph (old box) would be off at ~1e-3; the two contexts may walk
+    # different rows (the reused one can be in its buffered-row bypass after
+    # many rebuilds: nlist.cu kernel_rows), i.e. sum the same pairs on other
+    # lanes
+    np.testing.assert_allclose(got.mu, want.mu, rtol=0, atol=1e-10 * np.abs(want.mu).max())
 
 
 def test_isolated_sites_no_pairs(engine, oracle, mdg):
