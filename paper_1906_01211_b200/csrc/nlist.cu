@@ -686,9 +686,9 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
     --I.bypass;
     return full_rows();
   }
-  if (++I.calls >= 4) {  // motion cut on 3 or 4 of the last 4 calls: bypass the next 128
+  if (++I.calls >= 2) {  // motion cuts on both of the last 2 calls: bypass the next 128
     const int cuts = *(volatile int32_t*)I.hcuts;
-    if (2 * (cuts - I.cuts0) > I.calls) {
+    if (cuts - I.cuts0 >= I.calls) {
       I.bypass = 128;
       I.src_version = -1;  // cut afresh afterwards
     }
