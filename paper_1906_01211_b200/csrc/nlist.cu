@@ -441,13 +441,13 @@ __device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int m, int l
 template <int RMAX>
 __global__ void __launch_bounds__(kBlock) k_sort_rows(int64_t n, int32_t* __restrict__ nbr,
                                                     const int32_t* __restrict__ cnt, int32_t cap,
-                                                    const int32_t* __restrict__ flag) {
+                                                    const int32_t* __restrict__ flag, int lo) {
   if (flag && *flag == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   for (int64_t i = blockIdx.x * (int64_t)(kBlock / 32) + (threadIdx.x >> 5); i < n; i += warps) {
     const int m = cnt[i];
-    if (m < 2 || m > 32 * RMAX) continue;
+    if (m < 2 || m <= lo || m > 32 * RMAX) continue;
     int32_t* row = nbr + (size_t)i * cap;
     if (m <= 32) sort_row<1>(row, m, lane);
     else if (RMAX >= 2 && m <= 64) sort_row<(RMAX >= 2 ? 2 : 1)>(row, m, lane);
@@ -473,18 +473,20 @@ static bool sort_rows(mdg_ctx* c, int32_t* nbr, const int32_t* cnt, int32_t cap,
   const int64_t rows = c->n_own;
   const unsigned grid = (unsigned)std::min<int64_t>(148 * 16, (rows + 3) / 4);
   const int need = (std::min(1024, (int)max_cnt) + 31) / 32;
-  if (need <= 1)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<1>, rows, nbr, cnt, cap, flag);
-  else if (need <= 2)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<2>, rows, nbr, cnt, cap, flag);
-  else if (need <= 4)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<4>, rows, nbr, cnt, cap, flag);
-  else if (need <= 8)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<8>, rows, nbr, cnt, cap, flag);
-  else if (need <= 16)
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<16>, rows, nbr, cnt, cap, flag);
-  else
-    MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<32>, rows, nbr, cnt, cap, flag);
+  // rows up to 512 slots in a 16-register-row launch; only the longer ones
+  // pay the 32-register variant's occupancy
+#define MDG_SORT(R, LO) \
+  MDG_LAUNCH(c, "sort_rows", grid, kBlock, 0, k_sort_rows<R>, rows, nbr, cnt, cap, flag, LO)
+  if (need <= 1) MDG_SORT(1, 0);
+  else if (need <= 2) MDG_SORT(2, 0);
+  else if (need <= 4) MDG_SORT(4, 0);
+  else if (need <= 8) MDG_SORT(8, 0);
+  else if (need <= 16) MDG_SORT(16, 0);
+  else {
+    MDG_SORT(16, 0);
+    MDG_SORT(32, 512);
+  }
+#undef MDG_SORT
   return true;
 }
 
