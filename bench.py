@@ -437,7 +437,7 @@ def run_mine(args, world, rank, local):
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",  # one fixed system; --gpus N splits it (DD)
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded 3-site water fixture, BASELINE.json generator rules)",
@@ -619,7 +619,7 @@ def run_reference(args, world, rank):
         "warmup": args.warmup,
         "ms_per_step": r["s_per_step"] * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded 3-site water fixture)",
