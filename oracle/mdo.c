@@ -122,6 +122,127 @@ static double wrap_into(double p, double L) {
   return p;
 }
 
+/* ------------------------------------------- BASELINE.json water fixtures */
+/* Restatement of the BASELINE.json generator rules (reference
+ * lattice rule proj/src/system.cpp:87-104, seeded vacant slots, uniform
+ * random orientation, O-H 0.9572 A, H-O-H 104.52 deg, the per-config
+ * parameters) with explicitly written distributions, so the CPU arm builds
+ * its fixture without the product library. tests/test_oracle.py checks it
+ * bit-for-bit against mdg_water_generate. */
+static double wf_uniform(mt64* g) { return (double)(mt64_next(g) >> 11) * 0x1.0p-53; }
+static double wf_uniform_ab(mt64* g, double a, double b) { return a + (b - a) * wf_uniform(g); }
+static double wf_normal(mt64* g, double mean, double sd) {
+  double u1 = wf_uniform(g);
+  const double u2 = wf_uniform(g);
+  if (u1 < 1e-300) u1 = 1e-300;
+  return mean + sd * sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+static double wf_wrap(double p, double L) {
+  p -= L * floor(p / L);
+  if (p >= L) p = 0.0;
+  if (p < 0.0) p = 0.0;
+  return p;
+}
+static int cmp_i64(const void* a, const void* b) {
+  const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return (x > y) - (x < y);
+}
+
+int mdo_water_generate(int64_t n_mol, double box, uint64_t seed, int model, double* x,
+                       double* y, double* z, int32_t* molecule, double* charge,
+                       double* lj_sigma, double* lj_epsilon, double* hal_r0,
+                       double* hal_epsilon, double* polarizability, int32_t* hred_parent,
+                       double* hred_factor, double* dipole, double* quadrupole) {
+  if (n_mol < 1 || !(box > 0) || (model != 0 && model != 1)) return 1;
+  mt64* g = (mt64*)malloc(sizeof(mt64));
+  mt64_seed(g, seed);
+  int64_t m = 1;
+  while (m * m * m < n_mol) ++m;
+  const int64_t slots = m * m * m;
+  int64_t* slot = (int64_t*)malloc((size_t)slots * sizeof(int64_t));
+  for (int64_t k = 0; k < slots; ++k) slot[k] = k;
+  if (slots > n_mol) { /* Fisher-Yates on the lattice slots, keep the first n_mol */
+    for (int64_t k = slots - 1; k > 0; --k) {
+      const int64_t j = (int64_t)(mt64_next(g) % (uint64_t)(k + 1));
+      const int64_t t = slot[k]; slot[k] = slot[j]; slot[j] = t;
+    }
+    qsort(slot, (size_t)n_mol, sizeof(int64_t), cmp_i64);
+  }
+  const double sp = box / (double)m, jit = 0.05 * sp;
+  const double bl = 0.9572, half = 0.5 * 104.52 * 3.141592653589793 / 180.0;
+  const double hb[2][3] = {{bl * sin(half), 0.0, bl * cos(half)},
+                           {-bl * sin(half), 0.0, bl * cos(half)}};
+  for (int64_t w = 0; w < n_mol; ++w) {
+    const int64_t sl = slot[w];
+    const int64_t ix = sl / (m * m), iy = (sl / m) % m, iz = sl % m;
+    const double ox = (ix + 0.5) * sp + wf_uniform_ab(g, -jit, jit);
+    const double oy = (iy + 0.5) * sp + wf_uniform_ab(g, -jit, jit);
+    const double oz = (iz + 0.5) * sp + wf_uniform_ab(g, -jit, jit);
+    const double u1 = wf_uniform(g), u2 = wf_uniform(g), u3 = wf_uniform(g);
+    const double tp = 6.283185307179586;
+    const double qa = sqrt(1 - u1) * sin(tp * u2), qb = sqrt(1 - u1) * cos(tp * u2),
+                 qc = sqrt(u1) * sin(tp * u3), qd = sqrt(u1) * cos(tp * u3);
+    const double R[3][3] = {
+        {1 - 2 * (qb * qb + qc * qc), 2 * (qa * qb - qc * qd), 2 * (qa * qc + qb * qd)},
+        {2 * (qa * qb + qc * qd), 1 - 2 * (qa * qa + qc * qc), 2 * (qb * qc - qa * qd)},
+        {2 * (qa * qc - qb * qd), 2 * (qb * qc + qa * qd), 1 - 2 * (qa * qa + qb * qb)}};
+    const int64_t o = 3 * w;
+    x[o] = wf_wrap(ox, box);
+    y[o] = wf_wrap(oy, box);
+    z[o] = wf_wrap(oz, box);
+    for (int h = 0; h < 2; ++h) {
+      double d[3];
+      for (int a = 0; a < 3; ++a) d[a] = R[a][0] * hb[h][0] + R[a][1] * hb[h][1] + R[a][2] * hb[h][2];
+      x[o + 1 + h] = wf_wrap(ox + d[0], box);
+      y[o + 1 + h] = wf_wrap(oy + d[1], box);
+      z[o + 1 + h] = wf_wrap(oz + d[2], box);
+    }
+    for (int k = 0; k < 3; ++k) {
+      const int64_t i = o + k;
+      const int O = (k == 0);
+      if (molecule) molecule[i] = (int32_t)w;
+      if (model == 0) {
+        charge[i] = O ? -0.834 : 0.417;
+        lj_sigma[i] = O ? 3.1507 : 0.0;
+        lj_epsilon[i] = O ? 0.1521 : 0.0;
+        if (hred_parent) hred_parent[i] = (int32_t)i;
+        if (hred_factor) hred_factor[i] = 1.0;
+      } else {
+        charge[i] = O ? -0.51966 : 0.25983;
+        lj_sigma[i] = 0.0;
+        lj_epsilon[i] = 0.0;
+        if (hred_parent) hred_parent[i] = (int32_t)o;
+        if (hred_factor) hred_factor[i] = O ? 1.0 : 0.91;
+      }
+      hal_r0[i] = O ? 3.405 : 2.655;
+      hal_epsilon[i] = O ? 0.110 : 0.0135;
+      polarizability[i] = O ? 0.837 : 0.496;
+    }
+  }
+  const int64_t n = 3 * n_mol;
+  for (int64_t i = 0; i < n; ++i) { /* multipoles: fixed draw order, drawn for both models */
+    const double ct = wf_uniform_ab(g, -1.0, 1.0), ph = 6.283185307179586 * wf_uniform(g);
+    const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+    const double mag = wf_normal(g, 0.15, 0.03);
+    double q[6];
+    for (int k = 0; k < 6; ++k) q[k] = wf_normal(g, 0.0, 0.1);
+    if (dipole) {
+      dipole[3 * i] = model ? mag * st * cos(ph) : 0.0;
+      dipole[3 * i + 1] = model ? mag * st * sin(ph) : 0.0;
+      dipole[3 * i + 2] = model ? mag * ct : 0.0;
+    }
+    if (quadrupole) {
+      const double tr = (q[0] + q[3] + q[5]) / 3.0;
+      double* Q = quadrupole + 6 * i;
+      Q[0] = model ? q[0] - tr : 0.0; Q[1] = model ? q[1] : 0.0; Q[2] = model ? q[2] : 0.0;
+      Q[3] = model ? q[3] - tr : 0.0; Q[4] = model ? q[4] : 0.0; Q[5] = model ? q[5] - tr : 0.0;
+    }
+  }
+  free(slot);
+  free(g);
+  return 0;
+}
+
 /* proj/src/system.cpp:32-55 */
 static void draw_site_params(size_t n, mt64* g, double* charge, double* sig, double* eps,
                              double* r0, double* heps, double* pol) {

@@ -109,6 +109,12 @@ int mdo_jacobi(const mdo_system* s, const mdo_table* t, double cutoff, double th
 /* ---- EXTENSIONS (no reference counterpart) ----------------------------- */
 /* Halgren H-reduction sites: r_red = r_p + f * wrap1(r_i - r_p), re-wrapped
  * into [0, L) (Tinker-HP convention; SURVEY 8(c) gap ledger). */
+/* BASELINE.json 3-site water fixture (same contract as mdg_water_generate). */
+int mdo_water_generate(int64_t n_mol, double box, uint64_t seed, int model, double* x,
+                       double* y, double* z, int32_t* molecule, double* charge,
+                       double* lj_sigma, double* lj_epsilon, double* hal_r0,
+                       double* hal_epsilon, double* polarizability, int32_t* hred_parent,
+                       double* hred_factor, double* dipole, double* quadrupole);
 void mdo_reduce_sites(size_t n, const double* x, const double* y, const double* z,
                       const int32_t* parent, const double* factor, double lx, double ly,
                       double lz, double* xr, double* yr, double* zr);

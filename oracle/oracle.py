@@ -195,6 +195,9 @@ class Oracle:
         L.mdo_reduce_sites.argtypes = [C.c_size_t, _dp, _dp, _dp, _ip, _dp, C.c_double,
                                        C.c_double, C.c_double, _dp, _dp, _dp]
         L.mdo_reduce_forces.argtypes = [C.c_size_t, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.mdo_water_generate.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp,
+                                         _dp, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _dp, _dp,
+                                         _dp]
 
     def _check(self, rc: int):
         if rc != 0:
@@ -214,6 +217,30 @@ class Oracle:
         self._check(self.lib.mdo_generate_system(k, n, *map(float, box), seed, min_sep,
                                                  *(_ptr(a) for a in arrs)))
         return System(tuple(map(float, box)), *arrs)
+
+    def water_box(self, n_mol: int, box: float, seed: int = 1, model: str = "amoeba"):
+        """BASELINE.json 3-site water fixture (mdo_water_generate, the oracle's
+        own restatement; bit-identical to the product's mdg_water_generate,
+        tests/test_oracle.py). Returns (System, hred_parent, hred_factor)."""
+        n = 3 * n_mol
+        f = {k: np.zeros(n) for k in ("x", "y", "z", "charge", "lj_sigma", "lj_epsilon",
+                                      "hal_r0", "hal_epsilon", "polarizability", "hred_factor")}
+        mol = np.zeros(n, np.int32)
+        par = np.zeros(n, np.int32)
+        dip = np.zeros(3 * n)
+        quad = np.zeros(6 * n)
+        self._check(self.lib.mdo_water_generate(
+            n_mol, box, seed, 0 if model == "charmm" else 1, _ptr(f["x"]), _ptr(f["y"]),
+            _ptr(f["z"]), _ptr(mol, _ip), _ptr(f["charge"]), _ptr(f["lj_sigma"]),
+            _ptr(f["lj_epsilon"]), _ptr(f["hal_r0"]), _ptr(f["hal_epsilon"]),
+            _ptr(f["polarizability"]), _ptr(par, _ip), _ptr(f["hred_factor"]), _ptr(dip),
+            _ptr(quad)))
+        amoeba = model != "charmm"
+        s = System((box, box, box), f["x"], f["y"], f["z"], f["charge"], f["lj_sigma"],
+                   f["lj_epsilon"], f["hal_r0"], f["hal_epsilon"], f["polarizability"],
+                   molecule=mol, dipole=dip.reshape(n, 3) if amoeba else None,
+                   quadrupole=quad.reshape(n, 6) if amoeba else None)
+        return s, par, f["hred_factor"]
 
     def random_dipoles(self, n: int, seed: int, magnitude: float = 0.1) -> np.ndarray:
         a = [np.zeros(n) for _ in range(3)]

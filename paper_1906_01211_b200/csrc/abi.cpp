@@ -316,6 +316,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->plist.nbr) cudaFree(c->plist.nbr);
   if (c->plist.cnt) cudaFree(c->plist.cnt);
   if (c->plist.trr) cudaFree(c->plist.trr);
+  if (c->plist.ucl) cudaFree(c->plist.ucl);
+  if (c->plist.ucnt) cudaFree(c->plist.ucnt);
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& pe : c->pending) {
@@ -1133,7 +1135,9 @@ static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_
     // Two independent chains: [aux] Halgren -> multipoles (after the pruned
     // rows exist) and [main] permanent field + T -> PCG. Joined before the
     // polarization forces, which add to the same force/torque arrays.
-    const bool ov = overlap_enabled(c);
+    // one list for both terms: the two chains would cut / sort the same
+    // buffered rows on two unordered streams, so run them on one
+    const bool ov = vdw_list != elec_list && overlap_enabled(c);
     if (ov) {
       MDG_CUDA_CHECK(cudaEventRecord(c->ev_fork, c->stream));
       MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
@@ -1333,6 +1337,18 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
     need(p->nsteps >= 0 && p->dt_fs > 0 && p->rebuild_every >= 1, "md: bad step parameters");
     need(p->model == 0 ? cp != nullptr : (p->model == 1 && ap != nullptr),
          "md: model 0 needs charmm params, model 1 amoeba params");
+    // no per-step force DMA inside the loop (the bonded terms are added after
+    // the step's queue point, and the copies would sit on the critical path);
+    // a fetch after md_run takes the ordinary path
+    struct NoForceOutput {
+      mdg_ctx* c;
+      double* f[3];
+      ~NoForceOutput() {
+        for (int a = 0; a < 3; ++a) c->fout[a] = f[a];
+        c->fout_seq = 0;
+      }
+    } nfo{c, {c->fout[0], c->fout[1], c->fout[2]}};
+    for (int a = 0; a < 3; ++a) c->fout[a] = nullptr;
     auto rebuild = [&] {
       mdg::nlist_build(c, p->elec_list, p->elec_list_cutoff, MDG_SITES_ATOMIC);
       if (p->model == 1) mdg::nlist_build(c, p->vdw_list, p->vdw_list_cutoff, MDG_SITES_VDW);

@@ -96,6 +96,33 @@ struct PrunedList {
   size_t elems = 0;
   int64_t directed = 0;
   bool sorted = false;  // rows ascending in (j & 0x7fffffff) (source sorted)
+  // site clusters (cluster.cu): per cluster of 8 consecutive sites the sorted
+  // union of their rows, j | membership mask << 24; ucnt = entries | wide << 31
+  bool cl_valid = false;
+  int64_t ncl = 0;
+  int32_t ucap = 0;
+  uint32_t* ucl = nullptr;
+  int32_t* ucnt = nullptr;
+  size_t uelems = 0;
+  int64_t ucnt_elems = 0;
+};
+
+// arguments of the cluster mat-vec (cluster.cu)
+struct CLArgs {
+  int64_t n;    // owned sites
+  int64_t ncl;  // clusters
+  int ipw;      // clusters per block (MDG_LAUNCH_SITES)
+  const double4* __restrict__ pos;
+  const double2* __restrict__ polp;
+  const uint32_t* __restrict__ ucl;
+  const int32_t* __restrict__ ucnt;
+  int32_t ucap;
+  const double2* __restrict__ trr;
+  int32_t pcap;
+  Box b;
+  const double4* __restrict__ in;
+  double4* __restrict__ out;
+  double* __restrict__ partials;
 };
 
 struct ProfEntry {
@@ -388,6 +415,13 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
 // the permanent field into c->eperm.
 void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
                     int exclude);
+// Cluster unions of the pruned rows (cluster.cu); false when the cluster
+// mat-vec does not apply (unsorted rows, >= 2^24 sites, MDG_CLUSTER_MATVEC=0).
+bool build_clusters(mdg_ctx* c, double cutoff);
+CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out);
+const void* cl_matvec_kernel(bool pcg);
+void cl_matvec_launch(mdg_ctx* c, CLArgs& k, bool pcg, const char* name);
+void cl_matvec_launch_raw(const CLArgs& k, unsigned grid, cudaStream_t s);
 // PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
 void run_reduce_sites(mdg_ctx* c);

@@ -307,6 +307,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
   int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
   cap = std::max<int32_t>(32, (cap + 31) & ~31);
   if (P.cap > cap) cap = std::min(P.cap, L.cap);
+  P.cl_valid = false;
   const bool mp = c->has_mpoles, ex = exclude && c->has_mol;
   for (int attempt = 0; attempt < 2; ++attempt) {
     const size_t need = (size_t)n * (size_t)cap;
@@ -344,6 +345,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
       P.src = list_id;
       P.cutoff = cutoff;
       P.directed = (int64_t)c->h_results[63];
+      build_clusters(c, cutoff);
       return;
     }
     cap = (mx + 31) & ~31;
@@ -601,18 +603,28 @@ static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
 static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
                                double tol_debye, int64_t max_iter, double* last_rms) {
   // the mat-vec's grid (and partials) must be fixed before capture
-  const int64_t ipb =
-      sites_per_block((const void*)k_tmatvec_pre<true>, n, c->launch_bps, c->launch_waves);
-  const int64_t g = (n + ipb - 1) / ipb;
+  const bool cl = c->plist.cl_valid;
+  const int64_t units = cl ? c->plist.ncl : n;
+  const void* kern = cl ? cl_matvec_kernel(true) : (const void*)k_tmatvec_pre<true>;
+  const int64_t ipb = sites_per_block(kern, units, c->launch_bps, c->launch_waves);
+  const int64_t g = (units + ipb - 1) / ipb;
   ensure_partials(c, std::max(g, blocks));
   k.ipw = (int)ipb;
   k.partials = c->partials;
+  CLArgs kc{};
+  if (cl) {
+    kc = cl_args(c, k.in, k.out);
+    kc.ipw = (int)ipb;
+    kc.partials = c->partials;
+  }
   uint64_t tol_bits;
   std::memcpy(&tol_bits, &tol_debye, sizeof tol_bits);
   std::vector<uintptr_t> key = {(uintptr_t)n, (uintptr_t)k.pnbr, (uintptr_t)k.pcnt,
                                 (uintptr_t)k.trr, (uintptr_t)k.pcap, (uintptr_t)c->partials,
                                 (uintptr_t)ipb, (uintptr_t)max_iter,
-                                (uintptr_t)tol_bits, (uintptr_t)c->stream};
+                                (uintptr_t)tol_bits, (uintptr_t)c->stream, (uintptr_t)cl,
+                                (uintptr_t)kc.ucl, (uintptr_t)kc.ucnt, (uintptr_t)kc.ucap,
+                                (uintptr_t)kc.ncl};
   {  // the box is captured by value
     uint64_t w[sizeof(Box) / sizeof(uint64_t)];
     std::memcpy(w, &k.b, sizeof w);
@@ -637,7 +649,8 @@ static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
     const int64_t launches = c->launches;
     MDG_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
                                                  cudaStreamCaptureModeRelaxed));
-    k_tmatvec_pre<true><<<(unsigned)g, kBlock, 0, c->stream>>>(k);
+    if (cl) cl_matvec_launch_raw(kc, (unsigned)g, c->stream);
+    else k_tmatvec_pre<true><<<(unsigned)g, kBlock, 0, c->stream>>>(k);
     k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, g, 1, n, tol_debye, c->results);
     k_cg_update<<<(unsigned)blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
                                                            c->cg_q, c->mu, c->cg_r, c->cg_z,
@@ -660,6 +673,20 @@ static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
   if (c->h_results[27] == 0.0)
     throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
   return it;
+}
+
+// One PCG mat-vec over the stored tensors: the cluster kernel when the
+// cluster unions are built, else the per-site stream.
+static int64_t matvec_pre(mdg_ctx* c, TPArgs& k, bool pcg, const char* name) {
+  if (c->plist.cl_valid) {
+    CLArgs kc = cl_args(c, k.in, k.out);
+    cl_matvec_launch(c, kc, pcg, name);
+  } else if (pcg) {
+    MDG_LAUNCH_SITES(c, name, k.n, k, k_tmatvec_pre<true>);
+  } else {
+    MDG_LAUNCH_SITES(c, name, k.n, k, k_tmatvec_pre<false>);
+  }
+  return c->last_grid;
 }
 
 // PCG over the stored T tensors. Single domain: every scalar recurrence stays
@@ -698,7 +725,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   if (dd) dd_exchange(c, MDG_VEC_MU);
   k.in = c->mu;
   k.out = c->cg_q;
-  MDG_LAUNCH_SITES(c, "tmatvec_pre", n, k, k_tmatvec_pre<false>);
+  matvec_pre(c, k, false, "tmatvec_pre");
   MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
              c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
   MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
@@ -717,7 +744,7 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   k.out = c->cg_q;
   for (int64_t it = 1; it <= max_iter; ++it) {
     if (dd) dd_exchange(c, MDG_VEC_P);
-    MDG_LAUNCH_SITES(c, "tmatvec_pcg", n, k, k_tmatvec_pre<true>);
+    matvec_pre(c, k, true, "tmatvec_pcg");
     MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, c->last_grid, 1, n,
                tol_debye, c->results);
     if (dd) {

@@ -632,3 +632,23 @@ def test_bonded_oracle_forces_are_gradients(oracle):
             e1 = sum(md.bonded(p1, s.box, *args)[:2])
             e2 = sum(md.bonded(p2, s.box, *args)[:2])
             assert -(e1 - e2) / (2 * h) == pytest.approx(f[i, k], abs=1e-6)
+
+
+# ------------------------------------------------------- water fixture twin
+@pytest.mark.parametrize("model,n_mol,box,seed", [("amoeba", 1000, 31.04, 3),
+                                                  ("charmm", 1000, 31.04, 1),
+                                                  ("amoeba", 333, 21.5, 7)])
+def test_water_fixture_twin_is_bit_identical(oracle, mdg, model, n_mol, box, seed):
+    """The oracle's generator (mdo_water_generate) reproduces the product's
+    mdg_water_generate bit for bit, so the CPU reference arm builds the same
+    fixture without loading the product library."""
+    s, par, fac = oracle.water_box(n_mol, box, seed, model)
+    p = mdg.water_box(n_mol, box, seed, model)
+    for k in ("x", "y", "z", "charge", "lj_sigma", "lj_epsilon", "hal_r0", "hal_epsilon",
+              "polarizability", "molecule"):
+        assert np.array_equal(getattr(s, k), getattr(p, k)), k
+    if model == "amoeba":
+        assert np.array_equal(s.dipole, p.dipole) and np.array_equal(s.quadrupole, p.quadrupole)
+        assert np.array_equal(par, p.hred_parent) and np.array_equal(fac, p.hred_factor)
+        for a, b in zip(oracle.reduce_sites(s, par, fac), mdg.reduce_sites_host(p)):
+            assert np.array_equal(a, b)
