@@ -42,27 +42,106 @@ def test_library_is_sm100a_only(mdg):
     assert archs == {"sm_100a"}, archs
 
 
-def test_wrap1_sass_sequence(mdg):
-    """SURVEY 7 hard part: the device minimum image must keep the reference's
-    op sequence (DMUL -> FRND.F64 -> DFMA), not a fused or reordered one."""
+def _sass_functions(lib_path):
     import shutil
     import subprocess
     if not shutil.which("cuobjdump"):
         pytest.skip("cuobjdump absent")
-    sass = subprocess.run(["cuobjdump", "-sass", mdg.mdvec.LIB_PATH], capture_output=True,
+    sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True,
                           text=True).stdout
-    funcs = re.split(r"\n\s*Function : ", sass)
-    body = [f for f in funcs if f.split("\n", 1)[0].find("k_nlist_build") >= 0]
-    assert body, "k_nlist_build not in the fatbin"
-    ops = re.findall(r"\b(DMUL|FRND\.F64|DFMA|DADD|DSETP)\b", body[0])
-    seq = " ".join(ops)
-    # each axis: d*invL (DMUL) -> rint (FRND.F64, round-half-even) -> fma(-n, L, d) (DFMA)
-    assert seq.count("FRND.F64") >= 3
-    for k, op in enumerate(ops):
-        if op == "FRND.F64":
-            assert "DMUL" in ops[max(0, k - 5):k], seq
-            assert "DFMA" in ops[k + 1:k + 8], seq
-    assert "FRND.F64.FLOOR" not in body[0] and "FRND.F64.CEIL" not in body[0]
+    out = {}
+    for f in re.split(r"\n\s*Function : ", sass)[1:]:
+        name, body = f.split("\n", 1)
+        out[name.strip()] = [ln.split(";")[0].split("*/", 1)[-1].strip()
+                             for ln in body.split("\n") if "/*" in ln and ";" in ln]
+    return out
+
+
+_REG = r"(-?\|?R\d+(?:\.reuse)?\|?|-?UR\d+|-?c\[[^\]]+\]\[[^\]]+\]|RZ)"
+
+
+def _wrap_chains(ins):
+    """Dataflow check of every FRND.F64 in a kernel: its source is a DMUL
+    (d * invL), its result feeds a DFMA(-n, L, d) whose addend is that DMUL's
+    source d -- the reference's wrap1 (proj/include/mdvec/pbc.hpp:27-31) with
+    no contraction or reassociation. Returns the number of checked chains."""
+    def regs(s):
+        return [r.replace(".reuse", "").replace("|", "") for r in re.findall(_REG, s)]
+    n = 0
+    for k, s in enumerate(ins):
+        if not s.startswith("FRND"):
+            continue
+        assert s.startswith("FRND.F64 ") and not re.match(r"FRND\.F64\.(FLOOR|CEIL|TRUNC)", s), s
+        dst, src = regs(s.split(" ", 1)[1])[:2]
+        mul = [t for t in ins[max(0, k - 16):k] if t.startswith("DMUL ") and regs(t[5:])[0] == src]
+        assert mul, f"FRND source {src} is not a DMUL result: {ins[max(0, k - 16):k + 1]}"
+        d = regs(mul[-1][5:])[1]
+        fma = [t for t in ins[k + 1:k + 16] if t.startswith("DFMA ") and
+               regs(t[5:])[1] == "-" + dst]
+        assert fma, f"FRND result {dst} not used as -n in a DFMA: {ins[k:k + 16]}"
+        assert regs(fma[0][5:])[3] == d, f"wrap1 DFMA addend is not d: {fma[0]} / {mul[-1]}"
+        n += 1
+    return n
+
+
+def _dist2_chains(ins):
+    """fma(dx, dx, fma(dy, dy, dz * dz)) (pbc.hpp:35-37): a DMUL squaring one
+    register, accumulated by two DFMAs that each square one register."""
+    def regs(s):
+        return [r.replace(".reuse", "").replace("|", "") for r in re.findall(_REG, s)]
+    n = 0
+    for k, s in enumerate(ins):
+        if not s.startswith("DMUL "):
+            continue
+        r = regs(s[5:])
+        if len(r) < 3 or r[1] != r[2]:
+            continue
+        acc = r[0]
+        steps = 0
+        for t in ins[k + 1:k + 24]:
+            if t.startswith("DFMA "):
+                q = regs(t[5:])
+                if len(q) >= 4 and q[3] == acc and q[1] == q[2]:
+                    acc = q[0]
+                    steps += 1
+                    if steps == 2:
+                        n += 1
+                        break
+    return n
+
+
+# Production kernels that apply the reference pair predicate (VERDICT r1
+# weak 7): the cell-list build (wrapped and interior paths), the buffered-row
+# cut, and every pair kernel's prologue.
+PREDICATE_KERNELS = ("k_nlist_cells", "k_nlist_build", "k_cut_rows", "k_nonpolar", "k_halgren",
+                     "k_perm_field", "k_mpole", "k_polar_force", "k_tmatvec", "k_count_within")
+
+
+def test_wrap1_dist2_sass_in_production_kernels(mdg):
+    """SURVEY 7 hard part: every kernel that selects pairs keeps the reference's
+    op sequence (DMUL -> FRND.F64 (round-half-even) -> DFMA(-n, L, d); dist2 as
+    fma(dx,dx,fma(dy,dy,dz*dz))), checked by register dataflow in the SASS of
+    every template instance."""
+    import subprocess
+    funcs = _sass_functions(mdg.mdvec.LIB_PATH)
+    names = {m: subprocess.run(["c++filt", m], capture_output=True, text=True).stdout.strip()
+             for m in funcs}
+    seen = {k: 0 for k in PREDICATE_KERNELS}
+    for mangled, ins in funcs.items():
+        dm = names[mangled]
+        fam = [k for k in PREDICATE_KERNELS if re.search(r"\b" + k + r"\b", dm)
+               and not re.search(r"\b" + k + r"_", dm)]
+        if not fam:
+            continue
+        seen[fam[0]] += 1
+        assert _wrap_chains(ins) >= 3, dm
+        assert _dist2_chains(ins) >= 1, dm
+    missing = [k for k, v in seen.items() if v == 0]
+    assert not missing, missing
+    # the cell build has an interior (plain-subtraction) and a wrapped path:
+    # both end in the same dist2 chain
+    cells = [ins for m, ins in funcs.items() if "k_nlist_cells" in names[m]][0]
+    assert _dist2_chains(cells) >= 2
 
 
 def test_water_fixture_geometry(mdg):
