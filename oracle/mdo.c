@@ -122,6 +122,89 @@ static double wrap_into(double p, double L) {
   return p;
 }
 
+/* Full rows (every j != i within cutoff, ascending j) of the listed sites
+ * with the reference predicate (wrap1 + dist2, proj/include/mdvec/pbc.hpp:
+ * 27-37): the sampled-row oracle of the config-4 parity tests. Candidates
+ * come from a cell grid of edge >= cutoff (the 27 surrounding cells,
+ * deduplicated; every site when the grid has < 3 cells per axis), so the
+ * predicate alone decides membership. counts[k] = row length of sites[k];
+ * idx receives the rows back to back (CAPACITY if the total exceeds cap). */
+static int cmp_row_i32(const void* a, const void* b) {
+  const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+int mdo_rows_for_sites(const mdo_system* s, double cutoff, const int32_t* sites, size_t ns,
+                       int32_t* counts, int32_t* idx, size_t cap) {
+  const box_t b = make_box(s->lx, s->ly, s->lz);
+  const double c2 = cutoff * cutoff;
+  const double L[3] = {s->lx, s->ly, s->lz};
+  int nc[3];
+  for (int a = 0; a < 3; ++a) {
+    nc[a] = (int)floor(L[a] / cutoff);
+    if (nc[a] < 3) nc[a] = 1;
+  }
+  const size_t ncell = (size_t)nc[0] * nc[1] * nc[2];
+  size_t* start = (size_t*)calloc(ncell + 1, sizeof(size_t));
+  int32_t* cell = (int32_t*)malloc(s->n * sizeof(int32_t));
+  int32_t* bucket = (int32_t*)malloc(s->n * sizeof(int32_t));
+  const double* P[3] = {s->x, s->y, s->z};
+  for (size_t j = 0; j < s->n; ++j) {
+    int c[3];
+    for (int a = 0; a < 3; ++a) {
+      c[a] = (int)(P[a][j] / L[a] * nc[a]);
+      if (c[a] >= nc[a]) c[a] = nc[a] - 1;
+      if (c[a] < 0) c[a] = 0;
+    }
+    cell[j] = (c[0] * nc[1] + c[1]) * nc[2] + c[2];
+    start[cell[j] + 1]++;
+  }
+  for (size_t k = 0; k < ncell; ++k) start[k + 1] += start[k];
+  {
+    size_t* fill = (size_t*)malloc(ncell * sizeof(size_t));
+    memcpy(fill, start, ncell * sizeof(size_t));
+    for (size_t j = 0; j < s->n; ++j) bucket[fill[cell[j]]++] = (int32_t)j;
+    free(fill);
+  }
+  size_t pos = 0;
+  int rc = 0;
+  for (size_t k = 0; k < ns && rc == 0; ++k) {
+    const size_t i = (size_t)sites[k];
+    if (i >= s->n) { rc = fail(1, "rows_for_sites: site out of range"); break; }
+    const int ci[3] = {cell[i] / (nc[1] * nc[2]), (cell[i] / nc[2]) % nc[1], cell[i] % nc[2]};
+    int32_t seen[27];
+    int nseen = 0;
+    const size_t row0 = pos;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int cc[3] = {((ci[0] + dx) % nc[0] + nc[0]) % nc[0],
+                             ((ci[1] + dy) % nc[1] + nc[1]) % nc[1],
+                             ((ci[2] + dz) % nc[2] + nc[2]) % nc[2]};
+          const int32_t id = (cc[0] * nc[1] + cc[1]) * nc[2] + cc[2];
+          int dup = 0;
+          for (int q = 0; q < nseen; ++q) dup |= seen[q] == id;
+          if (dup) continue;
+          seen[nseen++] = id;
+          for (size_t t = start[id]; t < start[id + 1]; ++t) {
+            const size_t j = (size_t)bucket[t];
+            if (j == i) continue;
+            double ddx, ddy, ddz;
+            if (pair_d(s, &b, i, j, &ddx, &ddy, &ddz) <= c2) {
+              if (pos >= cap) { rc = fail(2, "rows_for_sites: capacity"); break; }
+              idx[pos++] = (int32_t)j;
+            }
+          }
+        }
+    qsort(idx + row0, pos - row0, sizeof(int32_t), cmp_row_i32);
+    counts[k] = (int32_t)(pos - row0);
+  }
+  free(start);
+  free(cell);
+  free(bucket);
+  return rc;
+}
+
 /* ------------------------------------------- BASELINE.json water fixtures */
 /* Restatement of the BASELINE.json generator rules (reference
  * lattice rule proj/src/system.cpp:87-104, seeded vacant slots, uniform

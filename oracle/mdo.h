@@ -81,6 +81,9 @@ void mdo_table_free(mdo_table* t);
  * must hold 2*cap int32; *npairs receives the count (CAPACITY if > cap). */
 int mdo_brute_force_pairs(const mdo_system* s, double cutoff, int32_t* out, size_t cap,
                           size_t* npairs);
+/* Full rows of the listed sites, brute force with the reference predicate. */
+int mdo_rows_for_sites(const mdo_system* s, double cutoff, const int32_t* sites, size_t ns,
+                       int32_t* counts, int32_t* idx, size_t cap);
 int mdo_table_pairs(const mdo_table* t, int32_t* out, size_t cap, size_t* npairs);
 
 /* ---- nonpolar kernels (kernels_scalar.cpp:10-94, polar_scalar.cpp:26-67) */

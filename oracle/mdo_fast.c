@@ -77,7 +77,9 @@ static inline void make_gq(double crr, double cdr, const double* d, double cq, c
 }
 
 int mdf_mpole(const mdo_system* s, const mdo_table* t, double alpha, double cutoff,
-              double electric, int exclude, double* f, double* torque, double* energy) {
+              double electric, int exclude, double* f, double* torque, double* energy,
+              double* virial9) {
+  double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}; /* pair virial sum R_a F_b, F on i */
   const size_t n = s->n;
   memset(f, 0, 3 * n * sizeof(double));
   memset(torque, 0, 3 * n * sizeof(double));
@@ -137,6 +139,7 @@ int mdf_mpole(const mdo_system* s, const mdo_table* t, double alpha, double cuto
                          G[4] * 2.0 * (qjr * vi[a] + qir * vj[a]) - sc * R[a];
         f[3 * i + a] -= g;
         f[3 * j + a] += g;
+        for (int b = 0; b < 3; ++b) w[3 * b + a] -= R[b] * g;
       }
       /* torque on i: gmu_i = G1 dj + 2 G2 vj - R (G1 qj + G2 djr + G3 qjr) */
       {
@@ -169,6 +172,7 @@ int mdf_mpole(const mdo_system* s, const mdo_table* t, double alpha, double cuto
     }
   }
   *energy = etot;
+  if (virial9) memcpy(virial9, w, sizeof w);
   return 0;
 }
 

@@ -195,6 +195,8 @@ class Oracle:
         L.mdo_reduce_sites.argtypes = [C.c_size_t, _dp, _dp, _dp, _ip, _dp, C.c_double,
                                        C.c_double, C.c_double, _dp, _dp, _dp]
         L.mdo_reduce_forces.argtypes = [C.c_size_t, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.mdo_rows_for_sites.argtypes = [C.POINTER(MdoSystem), C.c_double, _ip, C.c_size_t, _ip,
+                                         _ip, C.c_size_t]
         L.mdo_water_generate.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp,
                                          _dp, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _dp, _dp,
                                          _dp]
@@ -263,6 +265,40 @@ class Oracle:
                          np.ctypeslib.as_array(t.scale, (t.total,)).copy() if t.total else np.zeros(0))
         finally:
             self.lib.mdo_table_free(C.byref(t))
+
+    def rows_for_sites(self, s: System, cutoff: float, sites) -> list:
+        """Full rows (all j != i within cutoff, ascending) of `sites`, brute
+        force with the reference predicate (mdo_rows_for_sites)."""
+        sites = np.ascontiguousarray(sites, np.int32)
+        st = s.as_struct()
+        counts = np.zeros(len(sites), np.int32)
+        vol = float(np.prod(s.box))
+        cap = int(len(sites) * (s.n / vol * 4.2 * cutoff ** 3 * 2 + 64))
+        idx = np.zeros(cap, np.int32)
+        self._check(self.lib.mdo_rows_for_sites(C.byref(st), cutoff, _ptr(sites, _ip), len(sites),
+                                                _ptr(counts, _ip), _ptr(idx, _ip), cap))
+        ends = np.cumsum(counts)
+        return [idx[e - c:e].copy() for c, e in zip(counts, ends)]
+
+    @staticmethod
+    def table_from_rows(n: int, cutoff: float, sites, rows) -> Table:
+        """A reference-layout table whose only non-empty segments are the given
+        rows (segment of sites[k] = rows[k], padded to 16 with the sentinel)."""
+        nn = np.zeros(n, np.uint32)
+        nn[np.asarray(sites)] = [len(r) for r in rows]
+        p16 = (nn.astype(np.int64) + 15) & ~15
+        off = np.zeros(n, np.uint64)
+        off[1:] = np.cumsum(p16)[:-1]
+        idx = np.zeros(int(p16.sum()), np.int32)
+        scale = np.zeros(len(idx))
+        for site, r in zip(sites, rows):
+            o = int(off[site])
+            k = len(r)
+            idx[o:o + k] = r
+            idx[o + k:o + int(p16[site])] = r[-1] if k else 0
+            scale[o:o + k] = 1.0
+        nv8 = ((nn.astype(np.int64) + 7) & ~7).astype(np.uint32)
+        return Table(cutoff, nn, nv8, p16.astype(np.uint32), off, idx, scale)
 
     def brute_force_pairs(self, s: System, cutoff: float) -> np.ndarray:
         st = s.as_struct()
@@ -591,7 +627,8 @@ class FastPort:
         self.lib = C.CDLL(path or fast_port_path())
         L = self.lib
         L.mdf_mpole.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double, C.c_double,
-                                C.c_double, C.c_int, _dp, _dp, _dp]
+                                C.c_double, C.c_int, _dp, _dp, _dp, _dp]
+        self.last_virial = None
         L.mdf_perm_field.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double,
                                      C.c_double, C.c_double, C.c_int, _dp]
         L.mdf_tmatvec.argtypes = [C.POINTER(MdoSystem), C.POINTER(MdoTable), C.c_double,
@@ -603,8 +640,10 @@ class FastPort:
         f = np.zeros((s.n, 3))
         tq = np.zeros((s.n, 3))
         e = C.c_double()
+        w = np.zeros(9)
         self.lib.mdf_mpole(C.byref(st), C.byref(tt), alpha, cutoff, electric, int(exclude),
-                           _ptr(f), _ptr(tq), C.byref(e))
+                           _ptr(f), _ptr(tq), C.byref(e), _ptr(w))
+        self.last_virial = w.reshape(3, 3)  # pair virial sum d_a F_b (F on i)
         return f, tq, e.value
 
     def perm_field(self, s, t, alpha, cutoff, thole_a, exclude=True, st=None, tt=None):

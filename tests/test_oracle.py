@@ -464,9 +464,10 @@ def test_fast_port_matches_tensor_oracle(oracle):
     s = mpole_system(oracle, n=30, seed=11, cluster=9.0)
     t = oracle.build_table(s, 9.0)
     for alpha in (0.0, 0.5):
-        fo, to, eo, _ = oracle.mpole(s, t, alpha, 8.0, 2.0, exclude=True)
+        fo, to, eo, wo = oracle.mpole(s, t, alpha, 8.0, 2.0, exclude=True)
         f, tq, e = fp.mpole(s, t, alpha, 8.0, 2.0, exclude=True)
         assert e == pytest.approx(eo, rel=1e-12)
+        assert np.abs(fp.last_virial - wo).max() <= 1e-11 * np.abs(wo).max()
         assert np.abs(f - fo).max() <= 1e-11 * np.abs(fo).max()
         assert np.abs(tq - to).max() <= 1e-11 * np.abs(to).max()
         eo = oracle.perm_field_ewald(s, t, alpha, 8.0, 0.39, exclude=True)
@@ -652,3 +653,15 @@ def test_water_fixture_twin_is_bit_identical(oracle, mdg, model, n_mol, box, see
         assert np.array_equal(par, p.hred_parent) and np.array_equal(fac, p.hred_factor)
         for a, b in zip(oracle.reduce_sites(s, par, fac), mdg.reduce_sites_host(p)):
             assert np.array_equal(a, b)
+
+
+def test_rows_for_sites_match_brute_force(oracle):
+    """The sampled-row oracle of the config-4 parity test (cell candidates +
+    the reference predicate) == the O(N^2) brute-force pair set."""
+    for n_mol, box, cut in ((1000, 31.04, 9.0), (300, 20.0, 9.0), (2000, 39.1, 11.0)):
+        s, _, _ = oracle.water_box(n_mol, box, 1, "amoeba")
+        sites = np.arange(0, 3 * n_mol, 7)
+        bf = oracle.brute_force_pairs(s, cut)
+        for i, r in zip(sites, oracle.rows_for_sites(s, cut, sites)):
+            want = np.sort(np.concatenate([bf[bf[:, 0] == i, 1], bf[bf[:, 1] == i, 0]]))
+            np.testing.assert_array_equal(r, want)
