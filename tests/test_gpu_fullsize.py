@@ -212,7 +212,14 @@ def test_config4_sampled_sites_and_energies(oracle, mdg):
     assert np.abs(tq[sites] - to).max() <= F_TOL * np.sqrt(np.mean(tq ** 2))
     # (c) PCG residual at the sampled sites
     ep_s = oracle.perm_field_ewald(ref.so, t_e, ALPHA, 7.0, THOLE, exclude=True)[sites]
-    tmu_s = oracle.tmatvec_ewald(ref.so, t_e, ALPHA, 7.0, THOLE, mu)[sites]
+    # T keeps intramolecular pairs (u-scale 1): one table per site of the
+    # molecule, so no pair is listed in two sampled rows
+    tmu = np.zeros((n, 3))
+    for role in range(3):
+        sel = np.nonzero(sites % 3 == role)[0]
+        t_r = oracle.table_from_rows(n, 9.0, sites[sel], [rows_e[k] for k in sel])
+        tmu[sites[sel]] = oracle.tmatvec_ewald(ref.so, t_r, ALPHA, 7.0, THOLE, mu)[sites[sel]]
+    tmu_s = tmu[sites]
     pol = np.asarray(s.polarizability)[sites][:, None]
     resid = ep_s - (mu[sites] / pol - tmu_s)
     z = pol * resid  # preconditioned residual: the size of the next dipole step

@@ -740,6 +740,46 @@ def test_rows_longer_than_sort_limit(engine, oracle, mdg):
     assert force_err_rms(half.forces, fo) <= F_TOL
 
 
+def test_cut_rows_513_to_1024_slots(engine, oracle, mdg):
+    """Buffered cut rows of 513-1024 slots take the second (32-register) sort
+    launch (nlist.cu): ~610-slot 9.5 A rows here. Half rows + atomics ==
+    deterministic full rows == the oracle."""
+    s = uniform(oracle, 3000, 26.0, 6, min_sep=0.5)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(11.0)
+    lp = mdg.LjParams(9.0)
+    half = engine.lj_forces(t, lp)
+    engine.set_deterministic(True)
+    try:
+        full = engine.lj_forces(t, lp)
+    finally:
+        engine.set_deterministic(False)
+    np.testing.assert_allclose(half.forces, full.forces, rtol=0,
+                               atol=1e-11 * np.abs(full.forces).max())
+    fo, eo, _ = oracle.lj(s, oracle.build_table(s, 11.0), 9.0)
+    assert rel(half.energy, eo) <= E_TOL
+    assert force_err_rms(half.forces, fo) <= F_TOL
+
+
+def test_amoeba_step_one_shared_list(engine, oracle, mdg):
+    """one list for both the vdW and the electrostatic terms. The
+    step then runs its two chains on one stream (no unordered cuts of the
+    same buffered rows); results == the parts."""
+    s = amoeba_small(mdg, 343, 21.0, 6)
+    engine.upload_system(s)
+    te = engine.build_neighbor_table(10.0, list_id=0)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1)
+    for _ in range(3):
+        engine.amoeba_step(te, te, p)
+        e, w, iters, rms = engine.fetch_energies()
+        f = engine.fetch_forces()
+        hv = engine.halgren_forces(te, mdg.HalgrenParams(9.0), exclude=True)
+        fm, _, em, wm = engine.mpole_forces(te, 0.5446, 7.0, mdg.ELECTRIC, exclude=True)
+        assert rel(e[0], hv.energy) <= 1e-12 and rel(e[1], em) <= 1e-12
+        np.testing.assert_allclose(f, hv.forces + fm, rtol=0, atol=1e-12 * np.abs(f).max())
+        assert rms < 1e-5
+
+
 def test_config4_full_size_properties(mdg):
     """BASELINE config 4 at full size (999,999 atoms), through size-independent
     properties: the 9 A list's pair count equals a KD-tree count, pair forces
