@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 REBUILD_EVERY = 20
+METRIC = "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak"
 
 
 def parse():
@@ -426,10 +427,11 @@ def run_mine(args, world, rank, local):
     # 0.5 fs, 300 K start); last, as it moves the engine's coordinates
     md = None
     if not args.no_md:
+        eng.set_force_output(None)  # no per-step force DMA inside the MD loop
         md = md_timing(wl, args.steps, barrier, device)
 
     out = {
-        "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
+        "metric": METRIC,
         "value": world * wl.n * args.steps / (ms * 1e-3),
         "unit": "atom-steps/s",
         "n_gpus": world,
@@ -446,7 +448,7 @@ def run_mine(args, world, rank, local):
                                + ("LJ + Ewald charge 9 A" if wl.c["model"] == "charmm" else
                                   "Halgren 9 A + multipole Ewald 7 A + Thole/Ewald PCG 1e-5 D"),
                    "n_atoms": wl.n, "rebuild_every": REBUILD_EVERY,
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "parallelism": "1 GPU",
                    "l2": "inputs larger than L2 (lists > 126 MB)"},
         "e2e": e2e,
         "with_polar_forces": polar_forces,
@@ -473,33 +475,23 @@ def run_mine(args, world, rank, local):
     return out, wl
 
 
-def run_dd(args, world, rank, local):
-    """N > 1: spatial domain decomposition of the configured box (strong
-    scaling: the same 999,999 atoms over N GPUs)."""
-    import torch
-    import torch.distributed as dist
-
+def run_dd(args, world, rank, local, backend, ndom):
+    """Spatial domain decomposition of the configured box over `ndom` domains
+    (strong scaling: the same system split N ways): one domain per rank over
+    NCCL (backend "nccl", under torchrun), or all N domains in this process on
+    one GPU (backend "local": N ranks emulated on the one device). The PCG
+    exchanges halos and sums its scalars on the device every iteration
+    (csrc/group.cu)."""
     import paper_1906_01211_b200 as m
     from paper_1906_01211_b200 import dd
     c = m.CONFIGS[args.config]
     s = m.water_box(c["n_mol"], c["box"], args.seed, c["model"])
-    halo = max(c.get("vdw_cutoff", c.get("cutoff", 9.0)), c.get("elec_cutoff", 0)) + c["skin"] + 1.5
-    gloo = dist.new_group(backend="gloo")
-    comm = dd.TorchComm(device=local)
-    plans = dd.build_plans(s.x, s.y, s.z, s.molecule, s.box, world, halo)
-    eng = dd.DDEngine(s, comm, local, halo, plans=plans)
-    path = "nccl device buffers" if comm.cuda else "gloo host buffers"
-    ok = eng.check_halo(s)
-    ok_all = comm.allreduce([0.0 if ok else 1.0])[0] == 0.0
-    if not ok_all:  # fall back to host buffers over gloo (same plan, same hooks)
-        eng.comm = dd.TorchComm(group=gloo)
-        path = "gloo host buffers (nccl self-check failed)"
-        assert eng.check_halo(s), "halo exchange self-check failed"
     if c["model"] == "charmm":
+        list_cut = c["cutoff"] + c["skin"]
         params = m.CharmmParams(c["cutoff"], c["alpha"], m.ELECTRIC, 0, 1)
-        lists = [(c["cutoff"] + c["skin"], 0, m.SITES_ATOMIC)]
-        step = lambda t: eng.charmm_step(t, params)  # noqa: E731
+        lists = [(list_cut, 0, m.SITES_ATOMIC)]
     else:
+        list_cut = max(c["vdw_cutoff"], c["elec_cutoff"]) + c["skin"]
         terms = {1: m.TERM_VDW | m.TERM_MPOLE, 2: m.TERM_POLAR}.get(
             args.config, m.TERM_VDW | m.TERM_MPOLE | m.TERM_POLAR)
         params = m.AmoebaParams(c["vdw_cutoff"], 0.07, 0.12, c["elec_cutoff"], c["alpha"],
@@ -507,62 +499,89 @@ def run_dd(args, world, rank, local):
         lists = [(c["elec_cutoff"] + c["skin"], 0, m.SITES_ATOMIC)]
         if terms & m.TERM_VDW:
             lists.append((c["vdw_cutoff"] + c["skin"], 1, m.SITES_VDW))
-        step = lambda t: eng.amoeba_step(t, params)  # noqa: E731
-    tables = eng.build_lists(lists)
+    halo = list_cut + 1.5
+    size = world if backend == "nccl" else ndom
+    g = dd.DomainGroup(s, size, halo, device=local, backend=backend, rank=rank,
+                       list_cutoff=list_cut)
+    assert g.check_halo(s), "halo exchange self-check failed"
+    eng0 = g.domains[0].eng
+
+    def step(tables):
+        if c["model"] == "charmm":
+            g.charmm_step(tables, params)
+        else:
+            g.amoeba_step(tables, params)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    tables = g.build_lists(lists)
     for _ in range(args.warmup):
         step(tables)
-    tables = eng.build_lists(lists)
-    dist.barrier()
-    eng.eng.synchronize()
-    launches0 = eng.eng.launch_count()
+    barrier()
+    eng0.synchronize()
+    launches0 = g.launch_count()
     with ClockSampler(local) as clk:
-        eng.eng.timer_start()
+        eng0.timer_start()
         for k in range(args.steps):
             if k % REBUILD_EVERY == 0:
-                tables = eng.build_lists(lists)
+                tables = g.build_lists(lists)
             step(tables)
-        ms = eng.eng.timer_stop()
-    launches = eng.eng.launch_count() - launches0
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    en, w, iters, rms = eng.energies()
+        ms = eng0.timer_stop()
+    launches = g.launch_count() - launches0
+    ms = max_over_ranks(ms)
+    en, w, iters, rms = g.energies()
 
-    # ---- end to end through the public DD API: every step each rank uploads
-    # its owned coordinates (H2D) and refreshes its halo by exchange, and
-    # reads back its owned forces (D2H) and the all-reduced energies
+    # ---- end to end through the public DD API: every step each domain
+    # uploads its local coordinates (H2D; the halo then refreshed from the
+    # owners by the group exchange), reads back its owned forces (D2H) and
+    # the summed energies
     e2e = None
     if not args.no_e2e:
         x, y, z = np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)
         for _ in range(2):
-            eng.update_positions(x, y, z)
+            g.update_positions(x, y, z)
             step(tables)
-            eng.owned_forces()
-        tables = eng.build_lists(lists)
-        dist.barrier()
-        eng.eng.synchronize()
+            g.owned_forces()
+        tables = g.build_lists(lists)
+        barrier()
+        eng0.synchronize()
         t0 = time.perf_counter()
-        eng.eng.timer_start()
+        eng0.timer_start()
         for k in range(args.steps):
-            eng.update_positions(x, y, z)
+            g.update_positions(x, y, z)
             if k % REBUILD_EVERY == 0:
-                tables = eng.build_lists(lists)
+                tables = g.build_lists(lists)
             step(tables)
-            _, f = eng.owned_forces()
-            eng.energies()
-        e_ms = max(eng.eng.timer_stop(), (time.perf_counter() - t0) * 1e3)
-        t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-        e2e = {"value": eng.n_global * args.steps / (e_ms * 1e-3), "unit": "atom-steps/s",
-               "h2d_bytes_per_step": 24 * eng.n_global,
-               "d2h_bytes_per_step": 24 * eng.n_global + 8 * (4 + 9) * world,
+            g.owned_forces()
+            g.energies()
+        e_ms = max(eng0.timer_stop(), (time.perf_counter() - t0) * 1e3)
+        e_ms = max_over_ranks(e_ms)
+        n_loc = sum(len(d.plan.local) for d in g.domains)
+        n_own = sum(d.plan.n_owned for d in g.domains)
+        e2e = {"value": g.n_global * args.steps / (e_ms * 1e-3), "unit": "atom-steps/s",
+               "h2d_bytes_per_step": 24 * n_loc * (world if backend == "nccl" else 1),
+               "d2h_bytes_per_step": 24 * n_own * (world if backend == "nccl" else 1)
+               + 8 * (4 + 9) * size,
                "ms_per_step": e_ms / args.steps}
+    p0 = g.plans[0]
+    n_gpus = world if backend == "nccl" else 1
     out = {
-        "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
-        "value": eng.n_global * args.steps / (ms * 1e-3),
+        "metric": METRIC,
+        "value": g.n_global * args.steps / (ms * 1e-3),
         "unit": "atom-steps/s",
-        "n_gpus": world,
+        "n_gpus": n_gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
@@ -572,13 +591,16 @@ def run_dd(args, world, rank, local):
         "dtype": "f64",
         "data": "synthetic (seeded 3-site water fixture, BASELINE.json generator rules)",
         "config": {"workload": f"BASELINE config {args.config}: {c['n_mol']} waters "
-                               f"({eng.n_global} atoms), L={c['box']} A, spatial DD",
-                   "n_atoms": eng.n_global, "rebuild_every": REBUILD_EVERY,
-                   "parallelism": f"spatial DD {'x'.join(map(str, plans[0].dims))}, "
-                                  f"halo {halo} A, exchange: {path}",
-                   "owned_sites_rank0": plans[0].n_owned,
-                   "halo_sites_rank0": int(len(plans[0].halo)),
+                               f"({g.n_global} atoms), L={c['box']} A, spatial DD",
+                   "n_atoms": g.n_global, "rebuild_every": REBUILD_EVERY,
+                   "parallelism": f"spatial DD {'x'.join(map(str, p0.dims))} over {size} domains"
+                                  + (f" (NCCL, {world} GPUs)" if backend == "nccl" else
+                                     f" on 1 GPU (LOCAL group: {size} ranks emulated in one "
+                                     "process; no multi-GPU scaling claim)"),
+                   "halo_A": halo, "owned_sites_domain0": p0.n_owned,
+                   "halo_sites_domain0": int(len(p0.halo)),
                    "l2": "inputs larger than L2 (lists > 126 MB)"},
+        "domains": size,
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": None,
@@ -587,30 +609,56 @@ def run_dd(args, world, rank, local):
         "pcg_iters": int(iters),
         "pcg_rms_debye": float(rms),
     }
-    eng.close()
+    g.close()
     return out
+
+
+def _cpu_curve():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_cpu_cost_curve.json")) as f:
+            d = json.load(f)
+        return {"file": "profiles/r2_cpu_cost_curve.json", "cpu_model": d["cpu_model"],
+                "us_per_atom_step": {str(r["n_atoms"]): round(r["us_per_atom_step"], 3)
+                                     for r in d["rows"]}}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def _cpu_sample_text(r, threads):
+    return (f"{'%d independent replicas' % threads if threads > 1 else 'one replica'} of a "
+            f"{r['n_sample_atoms']}-atom box of the same generator/density (reference shards "
+            f"model, proj/src/bench.cpp:330-360); per step: reference Vec list build/20 + "
+            f"Halgren + {r['matvecs_per_step']} tmatxb (oracle/_ref, {r['isa']}), plus "
+            f"multipoles + multipole field from the CPU restatement oracle/mdo_fast.c (not "
+            f"reference: {100 * r['port_share']:.0f}% of the step); reference protocol: "
+            f"{r['warmup']} warm-up, {r['repeats']} interleaved Scalar/Vec repeats, trimmed mean")
 
 
 def cpu_baseline(args, pcg_iters):
     from oracle import cpu_reference
-    steps, warmup = (3, 1) if args.config != 0 else (20, 3)
     threads = 1
-    r = cpu_reference.run(args.config, threads, steps, warmup, args.seed, pcg_iters)
+    r = cpu_reference.run(args.config, threads, 3, 1, args.seed, matvecs=pcg_iters + 1)
     return {"value": r["value"], "unit": "atom-steps/s", "cores": threads, "kind": "reference",
-            "sample": f"{r['n_sample_atoms']}-atom box of the same generator/density, "
-                      f"{steps} steps after {warmup} warm-up; oracle/_ref Vec kernels "
-                      f"({r['isa']}) + closed-form port for multipoles/field",
-            "s_per_step": r["s_per_step"]}
+            "sample": _cpu_sample_text(r, threads), "s_per_step": r["s_per_step"],
+            "cpu_model": r["cpu_model"], "scalar_rel": r.get("scalar"),
+            "size_curve": _cpu_curve()}
 
 
 def run_reference(args, world, rank):
+    """The reference's own CPU implementation of the path on all host cores
+    (oracle/_ref Vec kernels; multipoles from the CPU restatement), same
+    metric and unit as the GPU arm, on a bounded sample of the workload."""
     if rank != 0:
         return None
     from oracle import cpu_reference
     threads = os.cpu_count() or 1
-    r = cpu_reference.run(args.config, threads, args.steps, args.warmup, args.seed, 10)
+    r = cpu_reference.run(args.config, threads, max(3, args.steps // 4), max(1, args.warmup // 3),
+                          args.seed)
+    cfg = {"workload": f"BASELINE config {args.config} (CPU sample: {r['n_sample_atoms']} "
+                       f"atoms per replica; per-atom cost vs size in size_curve)",
+           "threads": threads, "same_config": False}
     return {
-        "metric": "FP64 real-space force evals/sec (atom-steps/s) & % FP64 peak",
+        "metric": METRIC,
         "impl": "reference",
         "value": r["value"],
         "unit": "atom-steps/s",
@@ -619,45 +667,60 @@ def run_reference(args, world, rank):
         "warmup": args.warmup,
         "ms_per_step": r["s_per_step"] * 1e3,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak",  # independent replicas, one per core
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded 3-site water fixture)",
-        "config": {"workload": f"BASELINE config {args.config} (CPU sample: "
-                               f"{r['n_sample_atoms']} atoms per replica)",
-                   "threads": threads},
+        "data": "synthetic (seeded 3-site water fixture, oracle-side generator)",
+        "config": cfg,
         "cpu_baseline": {"value": r["value"], "unit": "atom-steps/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{threads} independent replicas of a "
-                                   f"{r['n_sample_atoms']}-atom box (reference shards model); "
-                                   f"oracle/_ref Vec kernels ({r['isa']}) + closed-form port "
-                                   "for multipoles/field"},
+                         "kind": "reference", "sample": _cpu_sample_text(r, threads),
+                         "cpu_model": r["cpu_model"], "scalar_rel": r.get("scalar"),
+                         "size_curve": _cpu_curve()},
         "e2e": {"value": r["value"], "unit": "atom-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
 
+def relaunch_torchrun(args) -> int:
+    """`bench.py --gpus N` outside torchrun on a box with >= N GPUs: re-run
+    this command as N ranks (one per GPU) under torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
-    if args.impl == "mine" and world > 1:
-        import torch
-        import torch.distributed as dist
-        # MDG_DD_BACKEND=gloo runs the same decomposition with host-buffer
-        # exchanges (e.g. several ranks sharing one GPU in a functional test)
-        local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
-        dist.init_process_group(os.environ.get("MDG_DD_BACKEND", "nccl"))
     if args.impl == "reference":
         out = run_reference(args, world, rank)
         if out is not None:
             print(json.dumps(out), flush=True)
         return
+    if world == 1 and args.gpus > 1:
+        import torch
+        if torch.cuda.device_count() >= args.gpus:
+            sys.exit(relaunch_torchrun(args))
+        # fewer GPUs than requested: the N domains run on this one GPU
+        out = run_dd(args, 1, 0, 0, "local", args.gpus)
+        print(json.dumps(out), flush=True)
+        return
     if world > 1:
-        out = run_dd(args, world, rank, local)
+        import torch
+        import torch.distributed as dist
+        assert args.gpus in (1, world), f"--gpus {args.gpus} under a world of {world} ranks"
+        torch.cuda.set_device(local)
+        # host-side plumbing (barriers, timing max, the NCCL id broadcast); the
+        # data path is the group's own NCCL communicator (csrc/group.cu)
+        dist.init_process_group("gloo")
+        out = run_dd(args, world, rank, local, "nccl", world)
         if rank == 0:
             print(json.dumps(out), flush=True)
-        import torch.distributed as dist
         dist.destroy_process_group()
         return
     out, wl = run_mine(args, world, rank, local)

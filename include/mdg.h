@@ -295,13 +295,56 @@ int mdg_system_upload_owned(mdg_ctx* ctx, int64_t n, int64_t n_owned, int64_t n_
                             const double* z, const double* charge, const double* lj_sigma,
                             const double* lj_epsilon, const double* hal_r0,
                             const double* hal_epsilon, const double* polarizability);
-/* Multi-domain hooks used inside the PCG solve: exchange(user, vec_id) must
- * refresh the halo entries of vec_id (via mdg_vec_pack / mdg_vec_unpack);
- * allreduce(user, vals, n) sums n doubles over all domains in place. Return
- * 0 on success. NULL hooks = single domain. */
-typedef int (*mdg_exchange_fn)(void* user, int vec_id);
-typedef int (*mdg_allreduce_fn)(void* user, double* vals, int n);
-int mdg_set_comm(mdg_ctx* ctx, mdg_exchange_fn exchange, mdg_allreduce_fn allreduce, void* user);
+/* ---- domain groups: the decomposed system's runtime (group.cu) ------------
+ * A group is the set of domain contexts of one spatially decomposed system
+ * (each created with mdg_system_upload_owned: owned sites first, then the
+ * halo). The group refreshes halos and, inside the PCG solve, exchanges the
+ * search direction and sums the CG scalars over all domains on the device:
+ * no host round trip per iteration. No reference counterpart (the reference
+ * is single-process; Tinker-HP's spatial
+ * decomposition). */
+typedef struct mdg_group mdg_group;
+#define MDG_GROUP_LOCAL 0 /* several domains in this process, one device */
+#define MDG_GROUP_NCCL 1  /* one domain per process (rank), NCCL over NVLink */
+
+/* NCCL unique id (128 bytes): rank 0 makes it, every rank passes it to
+ * mdg_group_create_nccl (broadcast out of band, e.g. torch.distributed). */
+int mdg_nccl_unique_id(void* id128);
+/* LOCAL group of n domain contexts on one device. They share the first
+ * context's stream while grouped (restored by mdg_group_destroy). n_global
+ * counts the sites of the whole system (PCG RMS normalisation). */
+int mdg_group_create_local(mdg_group** out, int n, mdg_ctx** ctxs, int64_t n_global);
+/* NCCL group: this process's domain context as rank `rank` of `size`. */
+int mdg_group_create_nccl(mdg_group** out, mdg_ctx* ctx, int rank, int size, const void* id128,
+                          int64_t n_global);
+int mdg_group_destroy(mdg_group* g);
+/* LOCAL halo of domain `domain`: for each of its n_halo halo sites (caller-
+ * order local index halo_site[k]) the owning domain src_domain[k] and the
+ * site's caller-order local index there, src_site[k]. */
+int mdg_group_set_halo_local(mdg_group* g, int domain, int64_t n_halo, const int32_t* halo_site,
+                             const int32_t* src_domain, const int32_t* src_site);
+/* NCCL halo: per peer rank (peers[p]), send_counts[p] owned sites it needs
+ * and recv_counts[p] halo sites it sends, as caller-order local indices
+ * concatenated per peer, in the order both sides agree on (global id). */
+int mdg_group_set_halo_nccl(mdg_group* g, int npeers, const int32_t* peers,
+                            const int64_t* send_counts, const int32_t* send_sites,
+                            const int64_t* recv_counts, const int32_t* recv_sites);
+/* Refresh the halo entries of vec_id (MDG_VEC_*) in every local domain from
+ * their owners (POS also refreshes the Halgren-reduced halo sites). Returns
+ * after completion. */
+int mdg_group_exchange(mdg_group* g, int vec_id);
+/* Sum result slots [slot, slot + nv) over all domains / ranks, in place, on
+ * the device (stream-ordered; nv <= 32). */
+int mdg_group_allreduce_results(mdg_group* g, int slot, int nv);
+/* mdg_amoeba_step for every local domain: per domain Halgren, field + T
+ * tensors and multipoles; one PCG over all domains (halo of the search
+ * direction and summed CG scalars every iteration, on the device); then the
+ * polarization forces after a halo refresh of the dipoles. */
+int mdg_group_amoeba_step(mdg_group* g, int vdw_list, int elec_list, const mdg_amoeba_params* p);
+int mdg_group_charmm_step(mdg_group* g, int list_id, const mdg_charmm_params* p);
+/* Energies and virial summed over all domains (and ranks); PCG record. */
+int mdg_group_fetch_energies(mdg_group* g, double* energies4, double* virial9,
+                             int64_t* pcg_iters, double* pcg_rms);
 /* Pair-sum mode of the Halgren and multipole kernels. Default (0): each
  * owned-owned pair is evaluated once (Newton's third law, as the reference's
  * half lists do) and the partner's force/torque is added with FP64 atomics,

@@ -225,6 +225,10 @@ int64_t pad_count(int64_t n, int64_t m) { return (n + m - 1) & ~(m - 1); }
 
 }  // namespace
 
+namespace mdg {
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace mdg
+
 extern "C" {
 
 const char* mdg_last_error(void) { return g_err.c_str(); }
@@ -330,8 +334,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   mdg::pme_free(c);
-  if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
-  if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
+  mdg::pcg_graph_forget(c);
   if (c->aux_partials) cudaFree(c->aux_partials);
   for (cudaEvent_t e : {c->ev_fork, c->ev_tpre, c->ev_join})
     if (e) cudaEventDestroy(e);
@@ -439,16 +442,6 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
     MDG_CUDA_CHECK(cudaMemsetAsync(c->mp, 0, 3 * n * sizeof(double4), c->stream));
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     c->has_system = true;
-  });
-}
-
-int mdg_set_comm(mdg_ctx* c, mdg_exchange_fn exchange, mdg_allreduce_fn allreduce, void* user) {
-  return guard([&] {
-    need_ctx(c);
-    need((exchange == nullptr) == (allreduce == nullptr), "set_comm: give both hooks or none");
-    c->comm_exchange = exchange;
-    c->comm_allreduce = allreduce;
-    c->comm_user = user;
   });
 }
 
@@ -1117,100 +1110,189 @@ static bool overlap_enabled(mdg_ctx* c) {
   return true;
 }
 
-static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
-  {
-    need_system(c);
-    need(p != nullptr, "null params");
-    mdg::DevList& Lv = need_list(c, vdw_list);
-    mdg::DevList& Le = need_list(c, elec_list);
-    need_kernel_cutoff(Lv, p->vdw_cutoff);
-    need_kernel_cutoff(Le, p->elec_cutoff);
-    need(Le.sites == MDG_SITES_ATOMIC, "electrostatics need a list over atomic sites");
-    const int terms = p->terms ? p->terms : (MDG_TERM_VDW | MDG_TERM_MPOLE | MDG_TERM_POLAR);
-    need(!(terms & MDG_TERM_POLAR_FORCE) || (terms & MDG_TERM_POLAR),
-         "amoeba_step: polarization forces need the polarization solve");
-    MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
-    c->has_polar_force = false;
-    mdg::rotate_multipoles(c);  // local frames at the current positions
-    // Two independent chains: [aux] Halgren -> multipoles (after the pruned
-    // rows exist) and [main] permanent field + T -> PCG. Joined before the
-    // polarization forces, which add to the same force/torque arrays.
-    // one list for both terms: the two chains would cut / sort the same
-    // buffered rows on two unordered streams, so run them on one
-    const bool ov = vdw_list != elec_list && overlap_enabled(c);
-    if (ov) {
-      MDG_CUDA_CHECK(cudaEventRecord(c->ev_fork, c->stream));
-      MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
-    }
-    // the main stream always ends behind the aux chain, also when a later
-    // stage throws (e.g. ConvergenceError from the PCG)
-    struct Join {
-      mdg_ctx* c;
-      bool on;
-      ~Join() {
-        if (!on) return;
-        cudaEventRecord(c->ev_join, c->aux_stream);
-        cudaStreamWaitEvent(c->stream, c->ev_join, 0);
-      }
-    } join{c, ov};
-    {
-      mdg::AuxScope aux(c, ov);
-      if (terms & MDG_TERM_VDW) {
-        mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
-      } else {
-        mdg::zero_vec(c, c->force);
-      }
-    }
-    // With polarization, one pass over the 9 A list prunes it to 7 A, stores
-    // the T tensors and computes the permanent field; the multipole kernel
-    // then runs on the pruned rows.
-    const bool polar = (terms & MDG_TERM_POLAR) != 0;
-    if (polar) {
-      mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
-      if (ov) {
-        MDG_CUDA_CHECK(cudaEventRecord(c->ev_tpre, c->stream));
-        MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
-      }
-    }
-    // forces are final at the end of the aux chain unless polarization
-    // forces or frame torques still add to them
-    const bool late_forces =
-        (polar && (terms & MDG_TERM_POLAR_FORCE)) || (c->has_frames && (terms & MDG_TERM_MPOLE));
-    {
-      mdg::AuxScope aux(c, ov);
-      if (terms & MDG_TERM_MPOLE) {
-        if (polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
-        else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
-      } else {
-        mdg::zero_vec(c, c->torque);
-      }
-      if (!late_forces) queue_force_output(c);  // overlaps what is left of the PCG
-    }
-    c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
-    c->pcg_rms = 0;
-    if (polar) {
-      double rms = 0;
-      c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
-      c->pcg_rms = rms;
-      mdg::polar_energy(c, p->electric, 40);
-    }
-    if (ov) {  // polarization forces add to the aux chain's force/torque
-      MDG_CUDA_CHECK(cudaEventRecord(c->ev_join, c->aux_stream));
-      MDG_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    }
-    if (polar && (terms & MDG_TERM_POLAR_FORCE)) {
-      // the PCG leaves the halo dipoles at mu0: refresh them first
-      mdg::exchange_halo(c, MDG_VEC_MU);
-      mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
-      c->has_polar_force = true;
-    }
-    if ((terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
-    if (late_forces) queue_force_output(c);
+// One domain's AMOEBA step in phases: pre (Halgren + multipoles on the aux
+// stream, permanent field + T tensors on the main one), the PCG (one domain,
+// or all domains of a group together), post (polarization forces, frames,
+// force output). Two independent chains per domain: [aux] Halgren ->
+// multipoles (after the pruned rows exist) and [main] permanent field + T ->
+// PCG, joined before the polarization forces, which add to the same
+// force/torque arrays.
+struct AmoebaPhase {
+  int terms = 0;
+  bool polar = false, late_forces = false, ov = false;
+};
+
+static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  need_system(c);
+  need(p != nullptr, "null params");
+  mdg::DevList& Lv = need_list(c, vdw_list);
+  mdg::DevList& Le = need_list(c, elec_list);
+  need_kernel_cutoff(Lv, p->vdw_cutoff);
+  need_kernel_cutoff(Le, p->elec_cutoff);
+  need(Le.sites == MDG_SITES_ATOMIC, "electrostatics need a list over atomic sites");
+  AmoebaPhase st;
+  st.terms = p->terms ? p->terms : (MDG_TERM_VDW | MDG_TERM_MPOLE | MDG_TERM_POLAR);
+  need(!(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_POLAR),
+       "amoeba_step: polarization forces need the polarization solve");
+  MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
+  c->has_polar_force = false;
+  mdg::rotate_multipoles(c);  // local frames at the current positions
+  // one list for both terms: the two chains would cut / sort the same
+  // buffered rows on two unordered streams, so run them on one
+  st.ov = vdw_list != elec_list && overlap_enabled(c);
+  if (st.ov) {
+    MDG_CUDA_CHECK(cudaEventRecord(c->ev_fork, c->stream));
+    MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
   }
+  {
+    mdg::AuxScope aux(c, st.ov);
+    if (st.terms & MDG_TERM_VDW) {
+      mdg::run_halgren(c, vdw_list, p->vdw_cutoff, p->delta, p->gamma, p->exclude);
+    } else {
+      mdg::zero_vec(c, c->force);
+    }
+  }
+  // With polarization, one pass over the 9 A list prunes it to 7 A, stores
+  // the T tensors and computes the permanent field; the multipole kernel
+  // then runs on the pruned rows.
+  st.polar = (st.terms & MDG_TERM_POLAR) != 0;
+  if (st.polar) {
+    mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
+    if (st.ov) {
+      MDG_CUDA_CHECK(cudaEventRecord(c->ev_tpre, c->stream));
+      MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
+    }
+  }
+  // forces are final at the end of the aux chain unless polarization
+  // forces or frame torques still add to them
+  st.late_forces = (st.polar && (st.terms & MDG_TERM_POLAR_FORCE)) ||
+                   (c->has_frames && (st.terms & MDG_TERM_MPOLE));
+  {
+    mdg::AuxScope aux(c, st.ov);
+    if (st.terms & MDG_TERM_MPOLE) {
+      if (st.polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
+      else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
+    } else {
+      mdg::zero_vec(c, c->torque);
+    }
+    if (!st.late_forces) queue_force_output(c);  // overlaps what is left of the PCG
+  }
+  c->pcg_iters = -1;  // marks an AMOEBA step for mdg_fetch_energies
+  c->pcg_rms = 0;
+  return st;
+}
+
+// the main stream waits for the aux chain (also when a later stage throws,
+// e.g. ConvergenceError from the PCG)
+static void amoeba_join(mdg_ctx* c, const AmoebaPhase& st) {
+  if (!st.ov) return;
+  cudaEventRecord(c->ev_join, c->aux_stream);
+  cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+}
+
+static void amoeba_post(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_params* p) {
+  if (st.polar && (st.terms & MDG_TERM_POLAR_FORCE)) {
+    mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
+    c->has_polar_force = true;
+  }
+  if ((st.terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
+  if (st.late_forces) queue_force_output(c);
+}
+
+static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  need(c == nullptr || c->group == nullptr,
+       "amoeba_step: this context is a domain of a group (mdg_group_amoeba_step)");
+  const AmoebaPhase st = amoeba_pre(c, vdw_list, elec_list, p);
+  if (st.polar) {
+    double rms = 0;
+    try {
+      c->pcg_iters = mdg::run_pcg_pre(c, p->tol_debye, p->max_iter, &rms);
+    } catch (...) {
+      amoeba_join(c, st);
+      throw;
+    }
+    c->pcg_rms = rms;
+    mdg::polar_energy(c, p->electric, 40);
+  }
+  amoeba_join(c, st);
+  amoeba_post(c, st, p);
 }
 
 int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
   return guard([&] { amoeba_step_impl(c, vdw_list, elec_list, p); });
+}
+
+// ---- domain groups (8(e), group.cu): steps and energies over all domains -----
+
+static void energies_of(mdg_ctx* c, double* e4, double* w9);
+
+int mdg_group_amoeba_step(mdg_group* g, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
+  return guard([&] {
+    need(g != nullptr, "group: null");
+    std::vector<mdg_ctx*> doms = mdg::group_domains(g);
+    set_device(doms[0]);
+    mdg::group_refresh(g);
+    std::vector<AmoebaPhase> st;
+    auto join_all = [&] {
+      for (size_t k = 0; k < st.size(); ++k) amoeba_join(doms[k], st[k]);
+    };
+    try {
+      for (mdg_ctx* c : doms) st.push_back(amoeba_pre(c, vdw_list, elec_list, p));
+      if (st[0].polar) {
+        double rms = 0;
+        const int64_t it =
+            mdg::run_pcg_multi(doms, mdg::group_comm(g), p->tol_debye, p->max_iter, &rms);
+        for (mdg_ctx* c : doms) {
+          c->pcg_iters = it;
+          c->pcg_rms = rms;
+          mdg::polar_energy(c, p->electric, 40);
+        }
+      }
+    } catch (...) {
+      join_all();
+      throw;
+    }
+    join_all();
+    // the solve leaves the halo dipoles at mu0: refresh them for the forces
+    if (st[0].polar && (st[0].terms & MDG_TERM_POLAR_FORCE))
+      mdg::group_comm(g)->exchange(MDG_VEC_MU);
+    for (size_t k = 0; k < st.size(); ++k) amoeba_post(doms[k], st[k], p);
+  });
+}
+
+int mdg_group_charmm_step(mdg_group* g, int list_id, const mdg_charmm_params* p) {
+  return guard([&] {
+    need(g != nullptr && p != nullptr, "group: null argument");
+    for (mdg_ctx* c : mdg::group_domains(g)) {
+      need_system(c);
+      mdg::DevList& L = need_list(c, list_id);
+      need_kernel_cutoff(L, p->cutoff);
+      need(L.sites == MDG_SITES_ATOMIC, "charmm step needs a list over atomic sites");
+      mdg::NonpolarArgs a{1, 1, p->shift, p->exclude, p->cutoff, p->alpha, p->electric};
+      mdg::run_nonpolar(c, list_id, a);
+      c->pcg_iters = 0;
+    }
+  });
+}
+
+int mdg_group_fetch_energies(mdg_group* g, double* energies4, double* virial9,
+                             int64_t* pcg_iters, double* pcg_rms) {
+  return guard([&] {
+    need(g != nullptr, "group: null");
+    std::vector<mdg_ctx*> doms = mdg::group_domains(g);
+    double v[13] = {0};
+    for (mdg_ctx* c : doms) {
+      double e[4], w[9];
+      energies_of(c, e, w);
+      for (int k = 0; k < 4; ++k) v[k] += e[k];
+      for (int k = 0; k < 9; ++k) v[4 + k] += w[k];
+    }
+    mdg::group_sum_host(g, v, 13);
+    if (energies4) std::memcpy(energies4, v, 4 * sizeof(double));
+    if (virial9) std::memcpy(virial9, v + 4, 9 * sizeof(double));
+    if (pcg_iters) *pcg_iters = doms[0]->pcg_iters > 0 ? doms[0]->pcg_iters : 0;
+    if (pcg_rms) *pcg_rms = doms[0]->pcg_rms;
+  });
 }
 
 // ---- MD (8(f)#4) -----------------------------------------------------------------
@@ -1468,25 +1550,28 @@ int mdg_fetch_perm_field(mdg_ctx* c, double* ex, double* ey, double* ez) {
 }
 
 // energies: {vdw (lj or halgren), coulomb/multipole, polarization, 0}
+static void energies_of(mdg_ctx* c, double* e4, double* w9) {
+  mdg::fetch_results(c);
+  const double* r = c->h_results;
+  double w[9];
+  sym_virial(r + 2, w);
+  const bool amoeba = c->pcg_iters != 0;
+  e4[0] = r[0];
+  e4[1] = amoeba ? r[10] : r[1];
+  e4[2] = amoeba ? r[40] : 0.0;
+  e4[3] = 0.0;
+  for (int k = 0; k < 9; ++k)
+    w9[k] = w[k] + (amoeba ? r[11 + k] : 0.0) + (c->has_polar_force ? r[71 + k] : 0.0);
+}
+
 int mdg_fetch_energies(mdg_ctx* c, double* energies4, double* virial9, int64_t* pcg_iters,
                        double* pcg_rms) {
   return guard([&] {
     need_system(c);
-    mdg::fetch_results(c);
-    const double* r = c->h_results;
-    double w[9];
-    sym_virial(r + 2, w);
-    const bool amoeba = c->pcg_iters != 0;
-    if (energies4) {
-      energies4[0] = r[0];
-      energies4[1] = amoeba ? r[10] : r[1];
-      energies4[2] = amoeba ? r[40] : 0.0;
-      energies4[3] = 0.0;
-    }
-    if (virial9) {
-      for (int k = 0; k < 9; ++k)
-        virial9[k] = w[k] + (amoeba ? r[11 + k] : 0.0) + (c->has_polar_force ? r[71 + k] : 0.0);
-    }
+    double e[4], w[9];
+    energies_of(c, e, w);
+    if (energies4) std::memcpy(energies4, e, sizeof e);
+    if (virial9) std::memcpy(virial9, w, sizeof w);
     if (pcg_iters) *pcg_iters = c->pcg_iters > 0 ? c->pcg_iters : 0;
     if (pcg_rms) *pcg_rms = c->pcg_rms;
   });

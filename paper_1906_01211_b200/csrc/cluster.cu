@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kBlock) k_cluster_union(CUArgs a) {
 // chunk c is computed.
 template <int G, bool PCG>
 __global__ void MDG_CL_BOUNDS k_tmatvec_cl(CLArgs a) {
+  if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
   __shared__ double4 s_o[kWarps][G];  // o_t (minimum image r_i - r_anchor)
   __shared__ double4 s_p[kWarps][G];  // r_i (wide clusters)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -303,6 +304,7 @@ CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out) {
   k.in = in;
   k.out = out;
   k.partials = c->partials;
+  k.res = c->results;
   return k;
 }
 

@@ -385,11 +385,13 @@ void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
   if (count <= 0) return;
   MDG_LAUNCH(c, "halo_unpack", grid_for(count, 256), 256, 0, k_vec_unpack, count, d_sites,
              c->d_iperm, d_in, vec_by_id(c, vec_id));
-  if (vec_id == MDG_VEC_POS) {
-    if (c->has_hred) run_reduce_sites(c);
-    else MDG_LAUNCH(c, "copy_vsite", grid_for(c->n, 256), 256, 0, k_copy_vsite, c->n, c->pos,
-                    c->vsite);
-  }
+  if (vec_id == MDG_VEC_POS) refresh_vsites(c);
+}
+
+void refresh_vsites(mdg_ctx* c) {
+  if (c->has_hred) run_reduce_sites(c);
+  else MDG_LAUNCH(c, "copy_vsite", grid_for(c->n, 256), 256, 0, k_copy_vsite, c->n, c->pos,
+                  c->vsite);
 }
 
 // -E_pol = 1/2 sum mu . E_perm ; results[slot] = -0.5 * electric * sum

@@ -123,6 +123,19 @@ struct CLArgs {
   const double4* __restrict__ in;
   double4* __restrict__ out;
   double* __restrict__ partials;
+  const double* __restrict__ res;  // PCG: result slots (converged flag 27)
+};
+
+// Communication of a multi-domain PCG solve (group.cu): refresh the halo of
+// a device vector in every local domain, and sum result slots over all
+// domains, both ordered on the domains' stream.
+struct PcgComm {
+  virtual ~PcgComm() = default;
+  virtual void exchange(int vec_id) = 0;
+  virtual void allreduce(int slot, int nv) = 0;
+  virtual bool capturable() const = 0;  // all ops may sit in a while graph
+  virtual int64_t n_global() const = 0;
+  virtual uintptr_t generation() const = 0;  // changes with the halo plans
 };
 
 struct ProfEntry {
@@ -138,6 +151,7 @@ struct PendingEvent {
 }  // namespace mdg
 
 constexpr int kMaxVdwTypes = 64;
+struct mdg_group;
 
 struct mdg_ctx {
   int device = 0;
@@ -151,11 +165,8 @@ struct mdg_ctx {
   int64_t n = 0;
   int64_t n_own = 0;
   int64_t n_global = 0;
-  // multi-domain hooks (NULL = single domain): halo exchange of a device
-  // vector before a mat-vec, and a sum all-reduce of host scalars.
-  int (*comm_exchange)(void* user, int vec_id) = nullptr;
-  int (*comm_allreduce)(void* user, double* vals, int n) = nullptr;
-  void* comm_user = nullptr;
+  // the domain group this context belongs to (group.cu; NULL: single domain)
+  mdg_group* group = nullptr;
   int32_t* d_iperm = nullptr;  // caller -> sorted index
   int32_t* d_idx = nullptr;    // staging for halo index lists
   double lx = 0, ly = 0, lz = 0;
@@ -259,11 +270,6 @@ struct mdg_ctx {
   double* fout[3] = {nullptr, nullptr, nullptr};
   double* d_fout = nullptr;    // 3 n doubles, caller order
   uint64_t fout_seq = 0;       // API call sequence number of the step that queued it
-  // single-domain PCG iterations as one device-side while graph (no host
-  // round trip per iteration); rebuilt when its captured arguments change
-  cudaGraph_t pcg_graph = nullptr;
-  cudaGraphExec_t pcg_exec = nullptr;
-  std::vector<uintptr_t> pcg_key;
 
   // last step
   double energies[4] = {0, 0, 0, 0};
@@ -424,6 +430,19 @@ void cl_matvec_launch(mdg_ctx* c, CLArgs& k, bool pcg, const char* name);
 void cl_matvec_launch_raw(const CLArgs& k, unsigned grid, cudaStream_t s);
 // PCG on the precomputed T tensors of c->plist (c->eperm = right-hand side).
 int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms);
+// The same over several domains (one stream) with halo exchange and summed
+// CG scalars through comm (NULL: one domain).
+int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_debye,
+                      int64_t max_iter, double* last_rms);
+void pcg_graph_forget(const void* owner);
+// domain groups (group.cu)
+PcgComm* group_comm(mdg_group* g);
+std::vector<mdg_ctx*> group_domains(mdg_group* g);
+bool group_is_nccl(mdg_group* g);
+void group_refresh(mdg_group* g);
+void group_sum_host(mdg_group* g, double* v, int nv);
+// vdW sites from the positions (Halgren reduction or copy), after new positions
+void refresh_vsites(mdg_ctx* c);
 void run_reduce_sites(mdg_ctx* c);
 // polarization forces at c->mu (polforce.cu); results slots 70 (pair
 // energy), 71..79 (virial); accumulate adds to c->force / c->torque
@@ -435,8 +454,6 @@ void run_polar_force_pruned(mdg_ctx* c, double alpha, double thole_a, double ele
 // torque -> forces on the frame atoms (after the torque kernels)
 void rotate_multipoles(mdg_ctx* c);
 void frame_torques_to_forces(mdg_ctx* c);
-// multi-domain: refresh the halo entries of vec_id through the comm hook
-void exchange_halo(mdg_ctx* c, int vec_id);
 // smooth PME reciprocal space for point charges (pme.cu): adds forces to
 // c->force; results 80 (recip), 81-86 (virial), 87 (self), 88-97 (excluded)
 void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,

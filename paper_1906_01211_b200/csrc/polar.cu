@@ -367,12 +367,14 @@ struct TPArgs {
   const double4* __restrict__ in;
   double4* __restrict__ out;
   double* __restrict__ partials;
+  const double* __restrict__ res;  // PCG: result slots (converged flag 27)
 };
 
 // E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; the PCG form
 // writes q = p/alpha - T p and the block partial of p.q.
 template <bool PCG>
 __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
+  if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
   const int lane = threadIdx.x & 31;
   double acc[1] = {0.0};
   MDG_SITE_LOOP(i, a.n, a.ipw) {
@@ -432,8 +434,12 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
 }
 
 // ---- PCG vector kernels ------------------------------------------------------
-// result slots: 20 p.q, 21 rz_old, 22 rz_new, 23 sum|dmu|^2, 24 beta, 25 rms (D),
-// 26 a_k, 27 converged flag
+// result slots: 20 p.q, 21 r.z (current), 22 r.z (new), 23 sum|dmu|^2, 24 beta,
+// 25 rms (D), 27 converged flag, 28 iterations. The scalar kernels form the
+// LOCAL sums of a domain; a multi-domain solve sums slots 20-23 over all
+// domains (PcgComm::allreduce) before the recurrences read them, so every
+// domain takes identical steps. Once converged, the kernels of any further
+// (speculatively queued) iteration return at once.
 constexpr double kDebye = 4.80321;
 
 // mu0 = alpha E; r0 = E - mu0/alpha + T mu0 (t = T mu0); z = alpha r; p = z
@@ -472,7 +478,8 @@ __global__ void k_mu0(int64_t n, const double2* __restrict__ polp, const double4
   }
 }
 
-// mu += a p; r -= a q; z = alpha r; partials: r.z, |a p|^2
+// a = r.z / p.q (global sums); mu += a p; r -= a q; z = alpha r;
+// partials: r.z, |a p|^2
 __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* __restrict__ polp,
                                                       const double* __restrict__ res,
                                                       const double4* __restrict__ p,
@@ -481,10 +488,13 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* 
                                                       double4* __restrict__ r,
                                                       double4* __restrict__ z,
                                                       double* __restrict__ partials) {
+  if (res[27] != 0.0) return;
   const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
   double acc[2] = {0.0, 0.0};
   if (i < n) {
-    const double ak = res[26];
+    // p.q == 0 only for p == 0 (r == 0: already exact); a = 0 then leaves mu
+    // unchanged and the rms test stops the loop, no 0/0
+    const double ak = (res[20] != 0.0) ? res[21] / res[20] : 0.0;
     const double al = polp[i].x;
     const double4 pp = p[i], qq = q[i], m = mu[i], rr = r[i];
     const double dx = ak * pp.x, dy = ak * pp.y, dz = ak * pp.z;
@@ -502,6 +512,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* 
 // p = z + beta p
 __global__ void k_cg_dir(int64_t n, const double* __restrict__ res, const double4* __restrict__ z,
                          double4* __restrict__ p) {
+  if (res[27] != 0.0) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
     const double bk = res[24];
@@ -510,13 +521,14 @@ __global__ void k_cg_dir(int64_t n, const double* __restrict__ res, const double
   }
 }
 
-// Fixed-order sums of the CG partials plus the scalar recurrences.
-// mode 0: rz0 -> res[21]; mode 1: p.q -> a = rz/pq -> res[26];
-// mode 2: rz_new, dsum -> beta, rms, converged.
+// Fixed-order local sums of the CG partials: mode 0 r.z -> res[21] (and a
+// fresh converged flag / iteration count); mode 1 p.q -> res[20]; mode 2
+// r.z, sum|dmu|^2 -> res[22], res[23].
 constexpr int kScalarThreads = 1024;
 __global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __restrict__ partials,
-                                                               int64_t blocks, int mode, int64_t n,
-                                                               double tol, double* __restrict__ res) {
+                                                               int64_t blocks, int mode,
+                                                               double* __restrict__ res) {
+  if (mode != 0 && res[27] != 0.0) return;
   // one block of 1024 threads, 4 independent loads in flight per thread: the
   // iteration's critical path waits on this sum twice (was 256 threads and
   // one dependent load chain: ~20 us per call on 2e4 partials)
@@ -544,175 +556,64 @@ __global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __r
     if (mode == 0) {
       res[21] = s[0][0];
       res[27] = 0.0;
+      res[28] = 0.0;
     } else if (mode == 1) {
-      // p.q == 0 only for p == 0 (r == 0: already exact); a_k = 0 then
-      // leaves mu unchanged and the rms test stops the loop, no 0/0
       res[20] = s[0][0];
-      res[26] = (s[0][0] != 0.0) ? res[21] / s[0][0] : 0.0;
     } else {
-      const double rz_new = s[0][0];
-      res[22] = rz_new;
+      res[22] = s[0][0];
       res[23] = s[1][0];
-      const double rms = sqrt(s[1][0] / (double)n) * kDebye;
-      res[25] = rms;
-      res[24] = (res[21] != 0.0) ? rz_new / res[21] : 0.0;
-      res[21] = rz_new;
-      res[27] = (rms < tol) ? 1.0 : 0.0;
     }
   }
 }
 
-// Device-side loop control of the PCG while graph: count the iteration and
-// continue unless converged (res[27]) or at max_iter. res[28] = iterations.
-__global__ void k_pcg_continue(cudaGraphConditionalHandle h, double* __restrict__ res,
-                               int64_t max_iter) {
+// The iteration's scalar recurrences from the (global) sums: beta, the rms
+// dipole step over n_global sites, convergence, the iteration count; in the
+// while graph also the loop condition.
+__global__ void k_cg_finish(cudaGraphConditionalHandle h, int use_cond, double* __restrict__ res,
+                            int64_t max_iter, double n_global, double tol) {
+  if (res[27] != 0.0) {
+    if (use_cond) cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  const double rz_new = res[22];
+  const double rms = sqrt(res[23] / n_global) * kDebye;
+  res[25] = rms;
+  res[24] = (res[21] != 0.0) ? rz_new / res[21] : 0.0;
+  res[21] = rz_new;
   const double it = res[28] + 1.0;
   res[28] = it;
-  cudaGraphSetConditional(h, (res[27] == 0.0 && it < (double)max_iter) ? 1u : 0u);
+  const bool conv = rms < tol;
+  res[27] = conv ? 1.0 : 0.0;
+  if (use_cond) cudaGraphSetConditional(h, (!conv && it < (double)max_iter) ? 1u : 0u);
 }
 
 __global__ void k_set_result(double* __restrict__ res, int slot, double v) { res[slot] = v; }
 
-// host-side value -> device result slot (stream-ordered)
-static void put_result(mdg_ctx* c, int slot, double v) {
-  c->h_results[slot] = v;
-  MDG_CUDA_CHECK(cudaMemcpyAsync(c->results + slot, c->h_results + slot, sizeof(double),
-                                 cudaMemcpyHostToDevice, c->stream));
-}
-
-static void dd_exchange(mdg_ctx* c, int vec_id) {
-  MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-  if (c->comm_exchange(c->comm_user, vec_id) != 0)
-    throw_error(MDG_COMM, "halo exchange callback failed");
-}
-
-void exchange_halo(mdg_ctx* c, int vec_id) {
-  if (c->comm_exchange) dd_exchange(c, vec_id);
-}
-
-static void dd_allreduce(mdg_ctx* c, double* v, int nv) {
-  if (c->comm_allreduce(c->comm_user, v, nv) != 0)
-    throw_error(MDG_COMM, "all-reduce callback failed");
-}
-
-// The iteration loop of run_pcg_pre as a CUDA graph: a while node whose body
-// is [mat-vec + p.q, alpha, update, beta/rms, continue?, direction]; the
-// k_pcg_continue kernel sets the loop condition on the device, so the host
-// launches the graph once and reads back the iteration count and rms. The
-// kernels and their order are those of the host-driven loop below.
-static int64_t pcg_device_loop(mdg_ctx* c, TPArgs& k, int64_t n, int64_t blocks,
-                               double tol_debye, int64_t max_iter, double* last_rms) {
-  // the mat-vec's grid (and partials) must be fixed before capture
-  const bool cl = c->plist.cl_valid;
-  const int64_t units = cl ? c->plist.ncl : n;
-  const void* kern = cl ? cl_matvec_kernel(true) : (const void*)k_tmatvec_pre<true>;
-  const int64_t ipb = sites_per_block(kern, units, c->launch_bps, c->launch_waves);
-  const int64_t g = (units + ipb - 1) / ipb;
-  ensure_partials(c, std::max(g, blocks));
-  k.ipw = (int)ipb;
-  k.partials = c->partials;
-  CLArgs kc{};
-  if (cl) {
-    kc = cl_args(c, k.in, k.out);
-    kc.ipw = (int)ipb;
-    kc.partials = c->partials;
-  }
-  uint64_t tol_bits;
-  std::memcpy(&tol_bits, &tol_debye, sizeof tol_bits);
-  std::vector<uintptr_t> key = {(uintptr_t)n, (uintptr_t)k.pnbr, (uintptr_t)k.pcnt,
-                                (uintptr_t)k.trr, (uintptr_t)k.pcap, (uintptr_t)c->partials,
-                                (uintptr_t)ipb, (uintptr_t)max_iter,
-                                (uintptr_t)tol_bits, (uintptr_t)c->stream, (uintptr_t)cl,
-                                (uintptr_t)kc.ucl, (uintptr_t)kc.ucnt, (uintptr_t)kc.ucap,
-                                (uintptr_t)kc.ncl};
-  {  // the box is captured by value
-    uint64_t w[sizeof(Box) / sizeof(uint64_t)];
-    std::memcpy(w, &k.b, sizeof w);
-    for (uint64_t x : w) key.push_back((uintptr_t)x);
-  }
-  if (!c->pcg_exec || key != c->pcg_key) {
-    if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
-    if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
-    c->pcg_exec = nullptr;
-    c->pcg_graph = nullptr;
-    MDG_CUDA_CHECK(cudaGraphCreate(&c->pcg_graph, 0));
-    cudaGraphConditionalHandle h;
-    MDG_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, c->pcg_graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    MDG_CUDA_CHECK(cudaGraphAddNode(&node, c->pcg_graph, nullptr, 0, &np));
-    cudaGraph_t body = np.conditional.phGraph_out[0];
-    const int64_t launches = c->launches;
-    MDG_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
-                                                 cudaStreamCaptureModeRelaxed));
-    if (cl) cl_matvec_launch_raw(kc, (unsigned)g, c->stream);
-    else k_tmatvec_pre<true><<<(unsigned)g, kBlock, 0, c->stream>>>(k);
-    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, g, 1, n, tol_debye, c->results);
-    k_cg_update<<<(unsigned)blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
-                                                           c->cg_q, c->mu, c->cg_r, c->cg_z,
-                                                           c->partials);
-    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, blocks, 2, n, tol_debye, c->results);
-    k_pcg_continue<<<1, 1, 0, c->stream>>>(h, c->results, max_iter);
-    k_cg_dir<<<grid_for(n, 256), 256, 0, c->stream>>>(n, c->results, c->cg_z, c->cg_p);
-    cudaGraph_t captured = nullptr;
-    MDG_CUDA_CHECK(cudaStreamEndCapture(c->stream, &captured));
-    MDG_CUDA_CHECK(cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
-    c->launches = launches;
-    c->pcg_key = key;
-  }
-  MDG_LAUNCH(c, "set_result", 1, 1, 0, k_set_result, c->results, 28, 0.0);
-  MDG_CUDA_CHECK(cudaGraphLaunch(c->pcg_exec, c->stream));
-  fetch_results(c);
-  const int64_t it = (int64_t)c->h_results[28];
-  c->launches += 6 * it;  // the body's kernels, executed on the device
-  *last_rms = c->h_results[25];
-  if (c->h_results[27] == 0.0)
-    throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
-  return it;
-}
-
-// One PCG mat-vec over the stored tensors: the cluster kernel when the
-// cluster unions are built, else the per-site stream.
-static int64_t matvec_pre(mdg_ctx* c, TPArgs& k, bool pcg, const char* name) {
-  if (c->plist.cl_valid) {
-    CLArgs kc = cl_args(c, k.in, k.out);
-    cl_matvec_launch(c, kc, pcg, name);
-  } else if (pcg) {
-    MDG_LAUNCH_SITES(c, name, k.n, k, k_tmatvec_pre<true>);
-  } else {
-    MDG_LAUNCH_SITES(c, name, k.n, k, k_tmatvec_pre<false>);
-  }
-  return c->last_grid;
-}
-
-// PCG over the stored T tensors. Single domain: every scalar recurrence stays
-// on the device (k_cg_scalars) and the host reads one flag per iteration.
-// Multi-domain (comm hooks set): the halo of mu / p is exchanged before each
-// mat-vec, and the local partial sums are all-reduced on the host before the
-// scalars are formed, so every rank takes identical steps.
-int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
-  const int64_t n = c->n_own;
-  const bool dd = c->comm_allreduce != nullptr;
-  const double n_glob = (double)(c->n_global > 0 ? c->n_global : n);
-  const int64_t blocks = grid_for(n);
-  PrunedList& P = c->plist;
-  // mat-vec shape (MDG_PCG_BPS / MDG_PCG_WAVES): leave room on every SM for
-  // the aux stream's multipole blocks
-  struct Shape {
-    mdg_ctx* c;
-    int b, w;
-    ~Shape() { c->launch_bps = b; c->launch_waves = w; }
-  } shape{c, c->launch_bps, c->launch_waves};
-  static const int pcg_bps = env_int("MDG_PCG_BPS", 0), pcg_waves = env_int("MDG_PCG_WAVES", 0);
-  c->launch_bps = pcg_bps;
-  c->launch_waves = pcg_waves;
+// One domain of a (possibly multi-domain) solve: its mat-vec arguments and
+// launch shapes, fixed before any capture.
+struct PcgDom {
+  mdg_ctx* c;
   TPArgs k;
+  CLArgs kc;
+  bool cl;
+  int64_t g;       // mat-vec grid
+  int64_t blocks;  // vector-kernel grid
+};
+
+static void pcg_dom_setup(PcgDom& d, mdg_ctx* c) {
+  const PrunedList& P = c->plist;
+  const int64_t n = c->n_own;
+  d.c = c;
+  d.blocks = grid_for(n);
+  d.cl = P.cl_valid;
+  const int64_t units = d.cl ? P.ncl : n;
+  const void* kern = d.cl ? cl_matvec_kernel(true) : (const void*)k_tmatvec_pre<true>;
+  const int64_t ipb = sites_per_block(kern, units, c->launch_bps, c->launch_waves);
+  d.g = (units + ipb - 1) / ipb;
+  ensure_partials(c, std::max(d.g, d.blocks));
+  TPArgs& k = d.k;
   k.n = n;
-  ensure_partials(c, blocks);
+  k.ipw = (int)ipb;
   k.pos = c->pos;
   k.polp = c->polp;
   k.pnbr = P.nbr;
@@ -720,60 +621,274 @@ int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last
   k.trr = P.trr;
   k.pcap = P.cap;
   k.b = make_box(c->lx, c->ly, c->lz);
+  k.in = c->cg_p;
+  k.out = c->cg_q;
   k.partials = c->partials;
-  MDG_LAUNCH(c, "cg_mu0", grid_for(n, 256), 256, 0, k_mu0, n, c->polp, c->eperm, c->mu);
-  if (dd) dd_exchange(c, MDG_VEC_MU);
-  k.in = c->mu;
-  k.out = c->cg_q;
-  matvec_pre(c, k, false, "tmatvec_pre");
-  MDG_LAUNCH(c, "cg_init", (unsigned)blocks, kBlock, 0, k_cg_init, n, c->polp, c->eperm,
-             c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
-  MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, blocks, 0, n, tol_debye,
-             c->results);
-  double rz = 0.0;  // global r.z (multi-domain path)
-  if (dd) {
-    fetch_results(c);
-    rz = c->h_results[21];
-    dd_allreduce(c, &rz, 1);
-    put_result(c, 21, rz);
+  k.res = c->results;
+  d.kc = CLArgs{};
+  if (d.cl) {
+    d.kc = cl_args(c, c->cg_p, c->cg_q);
+    d.kc.ipw = (int)ipb;
+    d.kc.partials = c->partials;
+    d.kc.res = c->results;
   }
-  k.in = c->cg_p;
-  k.out = c->cg_q;
-  if (!dd && !c->profile) return pcg_device_loop(c, k, n, blocks, tol_debye, max_iter, last_rms);
-  k.in = c->cg_p;
-  k.out = c->cg_q;
-  for (int64_t it = 1; it <= max_iter; ++it) {
-    if (dd) dd_exchange(c, MDG_VEC_P);
-    matvec_pre(c, k, true, "tmatvec_pcg");
-    MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, c->last_grid, 1, n,
-               tol_debye, c->results);
-    if (dd) {
-      fetch_results(c);
-      double pq = c->h_results[20];
-      dd_allreduce(c, &pq, 1);
-      put_result(c, 26, pq != 0.0 ? rz / pq : 0.0);  // a_k from global sums
+}
+
+// The loop body, launched directly on the domains' stream (raw launches:
+// also used inside stream capture, where the grids must be fixed).
+static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditionalHandle h,
+                     int use_cond, int64_t max_iter, double n_global, double tol) {
+  if (comm) comm->exchange(MDG_VEC_P);
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    if (d.cl) cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
+    else k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
+    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, d.g, 1, c->results);
+  }
+  if (comm) comm->allreduce(20, 1);
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    const int64_t n = c->n_own;
+    k_cg_update<<<(unsigned)d.blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
+                                                             c->cg_q, c->mu, c->cg_r, c->cg_z,
+                                                             c->partials);
+    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, d.blocks, 2, c->results);
+  }
+  if (comm) comm->allreduce(22, 2);
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    // the loop condition is the first domain's (identical on all of them)
+    k_cg_finish<<<1, 1, 0, c->stream>>>(h, use_cond && &d == &ds[0], c->results, max_iter,
+                                        n_global, tol);
+    k_cg_dir<<<grid_for(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->results, c->cg_z,
+                                                             c->cg_p);
+  }
+  for (PcgDom& d : ds) d.c->launches += 6;
+}
+
+// Loop body as a CUDA graph with a device-side while node: the host launches
+// the whole solve once. Rebuilt when a captured argument changes.
+struct PcgGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<uintptr_t> key;
+  ~PcgGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+static std::vector<uintptr_t> pcg_key(const std::vector<PcgDom>& ds, PcgComm* comm,
+                                      int64_t max_iter, double tol, double n_global) {
+  std::vector<uintptr_t> key;
+  auto put = [&](const void* p, size_t bytes) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t o = 0; o < bytes; o += sizeof(uintptr_t)) {
+      uintptr_t w = 0;
+      std::memcpy(&w, b + o, std::min(sizeof w, bytes - o));
+      key.push_back(w);
     }
-    MDG_LAUNCH(c, "cg_update", (unsigned)blocks, kBlock, 0, k_cg_update, n, c->polp, c->results,
-               c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
-    MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, blocks, 2, n, tol_debye,
-               c->results);
-    fetch_results(c);
-    if (dd) {
-      double v[2] = {c->h_results[22], c->h_results[23]};  // local rz_new, sum |dmu|^2
-      dd_allreduce(c, v, 2);
-      const double rms = std::sqrt(v[1] / n_glob) * kDebye;
-      put_result(c, 24, rz != 0.0 ? v[0] / rz : 0.0);  // beta
-      rz = v[0];
-      put_result(c, 21, rz);
-      *last_rms = rms;
-      if (rms < tol_debye) return it;
+  };
+  for (const PcgDom& d : ds) {
+    put(&d.k, sizeof d.k);
+    put(&d.kc, sizeof d.kc);
+    key.push_back((uintptr_t)d.cl);
+    key.push_back((uintptr_t)d.g);
+    key.push_back((uintptr_t)d.blocks);
+    key.push_back((uintptr_t)d.c->stream);
+    key.push_back((uintptr_t)d.c->n_own);
+  }
+  key.push_back((uintptr_t)comm);
+  if (comm) key.push_back(comm->generation());
+  key.push_back((uintptr_t)max_iter);
+  put(&tol, sizeof tol);
+  put(&n_global, sizeof n_global);
+  return key;
+}
+
+static void pcg_graph_launch(PcgGraph& G, std::vector<PcgDom>& ds, PcgComm* comm,
+                             int64_t max_iter, double n_global, double tol) {
+  cudaStream_t s = ds[0].c->stream;
+  std::vector<uintptr_t> key = pcg_key(ds, comm, max_iter, tol, n_global);
+  if (!G.exec || key != G.key) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    G.exec = nullptr;
+    G.graph = nullptr;
+    MDG_CUDA_CHECK(cudaGraphCreate(&G.graph, 0));
+    cudaGraphConditionalHandle h;
+    MDG_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, G.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    MDG_CUDA_CHECK(cudaGraphAddNode(&node, G.graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    std::vector<int64_t> launches;
+    for (PcgDom& d : ds) launches.push_back(d.c->launches);
+    MDG_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+    pcg_body(ds, comm, h, 1, max_iter, n_global, tol);
+    cudaGraph_t captured = nullptr;
+    MDG_CUDA_CHECK(cudaStreamEndCapture(s, &captured));
+    MDG_CUDA_CHECK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+    for (size_t k = 0; k < ds.size(); ++k) ds[k].c->launches = launches[k];
+    G.key = key;
+  }
+  MDG_CUDA_CHECK(cudaGraphLaunch(G.exec, s));
+}
+
+static std::map<const void*, PcgGraph>& pcg_graphs() {
+  static std::map<const void*, PcgGraph> m;  // per first context (or group)
+  return m;
+}
+
+void pcg_graph_forget(const void* owner) { pcg_graphs().erase(owner); }
+
+// PCG over the stored T tensors of every domain's pruned rows (c->eperm =
+// right-hand side), all domains' kernels on one stream (a group shares its
+// stream; NCCL ranks have one domain each). comm == NULL: a single domain.
+// No host round trip per iteration: the loop runs as a device-side while
+// graph when the communication is capturable (single domain, in-process
+// domains); otherwise (NCCL) the host queues iterations in batches ahead of
+// the device, whose kernels return at once after convergence, and reads the
+// converged flag a batch behind.
+int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_debye,
+                      int64_t max_iter, double* last_rms) {
+  mdg_ctx* c0 = doms[0];
+  double n_global = 0;
+  for (mdg_ctx* c : doms) n_global += (double)c->n_own;
+  if (comm) n_global = (double)comm->n_global();
+  else if (c0->n_global > 0) n_global = (double)c0->n_global;
+  // mat-vec shape (MDG_PCG_BPS / MDG_PCG_WAVES): leave room on every SM for
+  // the aux stream's multipole blocks
+  static const int pcg_bps = env_int("MDG_PCG_BPS", 0), pcg_waves = env_int("MDG_PCG_WAVES", 0);
+  std::vector<PcgDom> ds(doms.size());
+  for (size_t k = 0; k < doms.size(); ++k) {
+    mdg_ctx* c = doms[k];
+    const int b = c->launch_bps, w = c->launch_waves;
+    c->launch_bps = pcg_bps;
+    c->launch_waves = pcg_waves;
+    pcg_dom_setup(ds[k], c);
+    c->launch_bps = b;
+    c->launch_waves = w;
+  }
+  // mu0 = alpha E, its halo, T mu0, r0 / z0 / p0 and r0.z0
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    MDG_LAUNCH(c, "cg_mu0", grid_for(c->n_own, 256), 256, 0, k_mu0, c->n_own, c->polp, c->eperm,
+               c->mu);
+  }
+  if (comm) comm->exchange(MDG_VEC_MU);
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    if (d.cl) {
+      CLArgs kc = cl_args(c, c->mu, c->cg_q);
+      cl_matvec_launch(c, kc, false, "tmatvec_pre");
     } else {
-      *last_rms = c->h_results[25];
-      if (c->h_results[27] != 0.0) return it;
+      TPArgs k = d.k;
+      k.in = c->mu;
+      MDG_LAUNCH_SITES(c, "tmatvec_pre", k.n, k, k_tmatvec_pre<false>);
     }
-    MDG_LAUNCH(c, "cg_dir", grid_for(n, 256), 256, 0, k_cg_dir, n, c->results, c->cg_z, c->cg_p);
+    MDG_LAUNCH(c, "cg_init", (unsigned)d.blocks, kBlock, 0, k_cg_init, c->n_own, c->polp,
+               c->eperm, c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
+    MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, d.blocks, 0,
+               c->results);
   }
-  throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
+  if (comm) comm->allreduce(21, 1);
+  const bool graph = !c0->profile && (!comm || comm->capturable());
+  if (graph) {
+    pcg_graph_launch(pcg_graphs()[comm ? (const void*)comm : (const void*)c0], ds, comm,
+                     max_iter, n_global, tol_debye);
+  } else if (c0->profile) {
+    // kernel-by-kernel (named, event-bracketed) host loop, one check per iteration
+    for (int64_t it = 1; it <= max_iter; ++it) {
+      if (comm) comm->exchange(MDG_VEC_P);
+      for (PcgDom& d : ds) {
+        mdg_ctx* c = d.c;
+        if (d.cl) {
+          CLArgs kc = d.kc;
+          cl_matvec_launch(c, kc, true, "tmatvec_pcg");
+        } else {
+          TPArgs k = d.k;
+          MDG_LAUNCH_SITES(c, "tmatvec_pcg", k.n, k, k_tmatvec_pre<true>);
+        }
+        MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials,
+                   c->last_grid, 1, c->results);
+      }
+      if (comm) comm->allreduce(20, 1);
+      for (PcgDom& d : ds) {
+        mdg_ctx* c = d.c;
+        MDG_LAUNCH(c, "cg_update", (unsigned)d.blocks, kBlock, 0, k_cg_update, c->n_own,
+                   c->polp, c->results, c->cg_p, c->cg_q, c->mu, c->cg_r, c->cg_z, c->partials);
+        MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, d.blocks,
+                   2, c->results);
+      }
+      if (comm) comm->allreduce(22, 2);
+      for (PcgDom& d : ds) {
+        mdg_ctx* c = d.c;
+        MDG_LAUNCH(c, "cg_finish", 1, 1, 0, k_cg_finish, cudaGraphConditionalHandle{}, 0,
+                   c->results, max_iter, n_global, tol_debye);
+        MDG_LAUNCH(c, "cg_dir", grid_for(c->n_own, 256), 256, 0, k_cg_dir, c->n_own, c->results,
+                   c->cg_z, c->cg_p);
+      }
+      fetch_results(c0);
+      if (c0->h_results[27] != 0.0) break;
+    }
+  } else {
+    // speculative batches: B iterations queued per batch, the flag of batch
+    // k read (mapped copy behind an event) while batch k+1 runs
+    constexpr int kBatch = 4;
+    constexpr int kSlot = 112;  // two host copies of (27, 28, 25) at 112.. / 116..
+    cudaEvent_t ev[2];
+    for (auto& e : ev) MDG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct Free {
+      cudaEvent_t* e;
+      ~Free() {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+      }
+    } fr{ev};
+    int64_t queued = 0;
+    int batch = 0, pending = 0;
+    bool done = false;
+    while (!done) {
+      if (queued < max_iter) {
+        const int64_t m = std::min<int64_t>(kBatch, max_iter - queued);
+        for (int64_t q = 0; q < m; ++q)
+          pcg_body(ds, comm, cudaGraphConditionalHandle{}, 0, max_iter, n_global, tol_debye);
+        queued += m;
+        double* h = c0->h_results + kSlot + 4 * (batch & 1);
+        for (int s : {27, 28, 25})
+          MDG_CUDA_CHECK(cudaMemcpyAsync(h + (s == 27 ? 0 : s == 28 ? 1 : 2), c0->results + s,
+                                         sizeof(double), cudaMemcpyDeviceToHost, c0->stream));
+        MDG_CUDA_CHECK(cudaEventRecord(ev[batch & 1], c0->stream));
+        ++batch;
+        ++pending;
+      }
+      // wait for the older batch in flight (the newest when nothing more is queued)
+      if (pending == 2 || queued >= max_iter) {
+        const int b = (pending == 2) ? batch - 2 : batch - 1;
+        MDG_CUDA_CHECK(cudaEventSynchronize(ev[b & 1]));
+        --pending;
+        const double* h = c0->h_results + kSlot + 4 * (b & 1);
+        if (h[0] != 0.0 || (queued >= max_iter && pending == 0)) done = true;
+      }
+    }
+    MDG_CUDA_CHECK(cudaStreamSynchronize(c0->stream));
+  }
+  fetch_results(c0);
+  const int64_t it = (int64_t)c0->h_results[28];
+  *last_rms = c0->h_results[25];
+  if (c0->h_results[27] == 0.0)
+    throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
+  return it;
+}
+
+int64_t run_pcg_pre(mdg_ctx* c, double tol_debye, int64_t max_iter, double* last_rms) {
+  return run_pcg_multi({c}, nullptr, tol_debye, max_iter, last_rms);
 }
 
 // ---- Jacobi (reference semantics) ------------------------------------------------

@@ -1,28 +1,28 @@
 """Spatial domain decomposition over 1/2/4/8 GPUs.
 
-One process (context) per GPU. The orthorhombic box is split on a process
-grid (1x1x1, 2x1x1, 2x2x1, 2x2x2, ...); a rank OWNS the molecules whose anchor
-site (the first site of the molecule, the water oxygen) lies in its slab, so
-exclusions and the Halgren reduction parent stay local. Its HALO is every
-other molecule with a site within `halo_width` (list cutoff + intramolecular
-extent) of the slab, periodic images included. Each rank evaluates the rows
-of its owned sites (owned-owned pairs once with atomic partner updates, pairs
-with a halo partner in the owned row only, energy weight 1/2), so its owned
-forces, fields and dipoles are complete from owned + halo data: there is no
-force return. Per step
-the halo coordinates are refreshed; inside the PCG solve the halo of mu (once)
-and of the search direction p (every iteration) is exchanged and the CG
-scalars are all-reduced (mdg_set_comm hooks, called from the C++ solver), so
-every rank takes identical CG steps. Energies and virials are summed over
-ranks once per step.
+The orthorhombic box is split on a process grid (1x1x1, 2x1x1, 2x2x1,
+2x2x2, ...); a domain OWNS the molecules whose anchor site (the first site of
+the molecule, the water oxygen) lies in its subdomain, so exclusions and the
+Halgren reduction parent stay local. Its HALO is every other molecule with a
+site within `halo_width` (list cutoff + intramolecular extent) of the
+subdomain, periodic images included. Each domain evaluates the rows of its
+owned sites (owned-owned pairs once with atomic partner updates, pairs with a
+halo partner in the owned row only, energy weight 1/2), so its owned forces,
+fields and dipoles are complete from owned + halo data: there is no force
+return (DESIGN.md 7 gives the cost comparison with a half-shell halo).
 
-The plan is computed identically on every rank from the global coordinates;
-send/recv lists are ordered by global site index so both sides agree.
+This module builds the plan (identical on every rank, from the global
+coordinates; send/recv lists ordered by global site id so both sides agree)
+and drives the C++ group runtime (csrc/group.cu, include/mdg.h mdg_group_*):
+per step the halo coordinates are refreshed; inside the PCG solve the halo of
+the search direction is exchanged and the CG scalars are summed on the device
+every iteration, with no host round trip. Two backends: LOCAL (every domain
+in this process on one device: the single-GPU emulation of N ranks) and NCCL
+(one domain per torch.distributed rank / GPU).
 """
 from __future__ import annotations
 
 import ctypes as C
-import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -143,121 +143,22 @@ def local_system(s, plan: Plan):
                             hred_parent=par, hred_factor=fac, **kw)
 
 
-# ------------------------------------------------------------------ communicators
-class TorchComm:
-    """torch.distributed: NCCL (device buffers) or gloo (host buffers)."""
+# ------------------------------------------------------------------ the runtime
+class Domain:
+    """One domain: an Engine over its owned + halo sites (local order =
+    plan.local: owned first, then halo, each ascending in global id)."""
 
-    def __init__(self, device: int | None = None, group=None):
-        import torch
-        import torch.distributed as dist
-        self.torch, self.dist, self.group = torch, dist, group
-        self.rank, self.size = dist.get_rank(), dist.get_world_size()
-        self.cuda = dist.get_backend(group) == "nccl"
-        self.device = torch.device(f"cuda:{device}") if self.cuda else torch.device("cpu")
-        if self.cuda:
-            # create the NCCL communicator with a collective every rank joins
-            # (batched point-to-point must not be the group's first call)
-            self.allreduce(np.zeros(1))
-
-    def exchange(self, sends: dict, recv_counts: dict) -> dict:
-        """sends: peer -> float64 buffer; returns peer -> received buffer.
-        All receives and sends go out as one batch (ncclGroupStart/End under
-        NCCL): two ranks that each post recv-then-send on the shared pair
-        stream would otherwise wait on each other."""
-        t, dist = self.torch, self.dist
-        ops, out = [], {}
-        for q, n in recv_counts.items():
-            out[q] = t.empty(n, dtype=t.float64, device=self.device)
-            ops.append(dist.P2POp(dist.irecv, out[q], q, group=self.group))
-        for q, buf in sends.items():
-            tb = buf if isinstance(buf, t.Tensor) else t.from_numpy(np.ascontiguousarray(buf))
-            ops.append(dist.P2POp(dist.isend, tb.to(self.device), q, group=self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-        if self.cuda:
-            t.cuda.synchronize(self.device)
-        return out
-
-    def allreduce(self, vals: np.ndarray) -> np.ndarray:
-        t = self.torch
-        buf = t.from_numpy(np.array(vals, np.float64)).to(self.device)
-        self.dist.all_reduce(buf, group=self.group)
-        return buf.cpu().numpy()
-
-
-class LocalComm:
-    """In-process domains (one thread each), e.g. several contexts on one GPU
-    in a test: a mailbox plus barriers. Sums are formed in rank order."""
-
-    class _Shared:
-        def __init__(self, size):
-            self.size = size
-            self.box = {}
-            self.red = [None] * size
-            self.barrier = threading.Barrier(size)
-
-    def __init__(self, shared, rank):
-        self.s, self.rank, self.size = shared, rank, shared.size
-        self.cuda = False
-
-    @classmethod
-    def group(cls, size):
-        sh = cls._Shared(size)
-        return [cls(sh, r) for r in range(size)]
-
-    def exchange(self, sends, recv_counts):
-        for q, buf in sends.items():
-            self.s.box[(self.rank, q)] = np.array(buf, np.float64)
-        self.s.barrier.wait()
-        out = {q: self.s.box[(q, self.rank)] for q in recv_counts}
-        self.s.barrier.wait()
-        for q in sends:
-            self.s.box.pop((self.rank, q), None)
-        return out
-
-    def allreduce(self, vals):
-        self.s.red[self.rank] = np.array(vals, np.float64)
-        self.s.barrier.wait()
-        tot = np.sum(np.stack(self.s.red), 0)
-        self.s.barrier.wait()
-        return tot
-
-
-# ------------------------------------------------------------------ the rank engine
-EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
-ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
-
-
-class DDEngine:
-    """One rank: an Engine over owned + halo sites with the comm hooks installed."""
-
-    def __init__(self, s, comm, device: int, halo_width: float, plans=None):
-        self.comm = comm
-        self.plans = plans or build_plans(s.x, s.y, s.z, s.molecule, s.box, comm.size,
-                                          halo_width)
-        self.plan = self.plans[comm.rank]
-        self.n_global = len(s.x)
-        self.local = local_system(s, self.plan)
-        self.eng = M.Engine(len(self.plan.local), device=device)
-        self._upload()
-        self._ex = EXCHANGE_FN(self._exchange_cb)
-        self._ar = ALLREDUCE_FN(self._allreduce_cb)
-        if comm.size > 1:
-            M.check(self.eng.lib.mdg_set_comm(self.eng.ctx, C.cast(self._ex, C.c_void_p),
-                                              C.cast(self._ar, C.c_void_p), None))
-        self.recv_counts = {q: 3 * len(v) for q, v in self.plan.recv.items()}
-        self._dev_idx = {}
-        self.error = None
-
-    def _upload(self):
+    def __init__(self, s, plan: Plan, n_global: int, device: int):
+        self.plan = plan
+        self.local = local_system(s, plan)
+        self.eng = M.Engine(len(plan.local), device=device)
         L = self.local
         arrs = [M._f64(getattr(L, k)) for k in ("x", "y", "z", "charge", "lj_sigma",
                                                  "lj_epsilon", "hal_r0", "hal_epsilon",
                                                  "polarizability")]
         self._keep = arrs
         M.check(self.eng.lib.mdg_system_upload_owned(
-            self.eng.ctx, len(arrs[0]), self.plan.n_owned, self.n_global, *map(float, L.box),
+            self.eng.ctx, len(arrs[0]), plan.n_owned, n_global, *map(float, L.box),
             *(M._p(a) for a in arrs)))
         self.eng.n = len(arrs[0])
         self.eng.box = tuple(map(float, L.box))
@@ -266,128 +167,185 @@ class DDEngine:
             self.eng.upload_multipoles(L.dipole, L.quadrupole)
 
     def upload_frames(self, frame, zatom, xatom, dipole, quadrupole):
-        """Local multipole frames (global arrays, global site ids): the
-        rank's owned + halo sites with their frame atoms mapped to local
-        ids (frame atoms belong to the same molecule, so they are local)."""
+        """Local multipole frames (global arrays, global site ids) mapped to
+        local ids (frame atoms belong to the same molecule, so are local)."""
         idx = self.plan.local
-        inv = {int(g): k for k, g in enumerate(idx)}
+        inv = np.full(int(max(idx.max(), np.max(zatom), np.max(xatom))) + 1, -1, np.int64)
+        inv[idx] = np.arange(len(idx))
         fr = np.asarray(frame)[idx]
-        za = np.array([inv[int(g)] if f else 0 for g, f in zip(np.asarray(zatom)[idx], fr)],
-                      np.int32)
-        xa = np.array([inv[int(g)] if f else 0 for g, f in zip(np.asarray(xatom)[idx], fr)],
-                      np.int32)
+        za = np.where(fr != 0, inv[np.asarray(zatom)[idx]], 0).astype(np.int32)
+        xa = np.where(fr != 0, inv[np.asarray(xatom)[idx]], 0).astype(np.int32)
         self.eng.upload_frames(fr, za, xa, np.asarray(dipole)[idx], np.asarray(quadrupole)[idx])
 
-    # ---- halo traffic
+
+def nccl_halo_args(p: Plan):
+    """Arguments of mdg_group_set_halo_nccl for one rank's plan: peer ranks
+    (ascending), per-peer send / recv counts, and the caller-order local
+    indices concatenated per peer. Rank r's sends to q and q's receives from r
+    list the same global sites in the same (ascending global id) order."""
+    peers = sorted(set(p.send) | set(p.recv))
+    sc = np.array([len(p.send.get(q, ())) for q in peers], np.int64)
+    rc = np.array([len(p.recv.get(q, ())) for q in peers], np.int64)
+    ss = np.concatenate([p.send[q] for q in peers if q in p.send] or
+                        [np.zeros(0, np.int32)]).astype(np.int32)
+    rs = np.concatenate([p.recv[q] for q in peers if q in p.recv] or
+                        [np.zeros(0, np.int32)]).astype(np.int32)
+    return np.array(peers, np.int32), sc, ss, rc, rs
+
+
+class HaloStale(RuntimeError):
+    """Sites moved farther than the halo margin allows since the plan was built."""
+
+
+class DomainGroup:
+    """The decomposed system's runtime over the C++ group (mdg_group_*).
+
+    backend "local": every domain in this process on `device` (one context
+    per domain, one shared stream) -- N ranks emulated on one GPU.
+    backend "nccl": this rank's domain only; `rank`/`size` of the
+    torch.distributed default group, which also carries the NCCL unique id.
+    """
+
+    def __init__(self, s, size: int, halo_width: float, device: int = 0, backend: str = "local",
+                 rank: int = 0, plans=None, list_cutoff: float | None = None):
+        self.lib = M.load_library()
+        self.backend, self.size, self.rank = backend, size, rank
+        self.halo_width = float(halo_width)
+        self.n_global = len(s.x)
+        self.box = np.asarray(s.box, float)
+        self.plans = plans or build_plans(s.x, s.y, s.z, s.molecule, s.box, size, halo_width)
+        # sites may move (halo_width - list cutoff - 1 A intramolecular extent) / 2
+        # before the halo can miss a pair (update_positions checks)
+        lc = list_cutoff if list_cutoff is not None else halo_width - 1.5
+        self.margin = max(0.0, (self.halo_width - lc - 1.0) / 2.0)
+        self.ref_xyz = np.stack([np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)], 1).copy()
+        mine = range(size) if backend == "local" else [rank]
+        self.domains = [Domain(s, self.plans[r], self.n_global, device) for r in mine]
+        self.g = C.c_void_p()
+        if backend == "local":
+            ctxs = (C.c_void_p * len(self.domains))(*[d.eng.ctx.value for d in self.domains])
+            M.check(self.lib.mdg_group_create_local(C.byref(self.g), len(self.domains), ctxs,
+                                                    self.n_global))
+            self._set_halo_local()
+        elif backend == "nccl":
+            import torch.distributed as dist
+            uid = C.create_string_buffer(128)
+            if rank == 0:
+                M.check(self.lib.mdg_nccl_unique_id(uid))
+            obj = [bytes(uid.raw) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = C.create_string_buffer(obj[0], 128)
+            M.check(self.lib.mdg_group_create_nccl(C.byref(self.g), self.domains[0].eng.ctx,
+                                                   rank, size, uid, self.n_global))
+            self._set_halo_nccl()
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
+
+    # ---- halo plans
+    def _set_halo_local(self):
+        owner = np.empty(self.n_global, np.int32)
+        where = np.empty(self.n_global, np.int32)  # caller-order local index in the owner
+        for r, p in enumerate(self.plans):
+            owner[p.owned] = r
+            where[p.owned] = np.arange(p.n_owned, dtype=np.int32)
+        for d, p in enumerate(self.plans):
+            halo_local = np.arange(p.n_owned, p.n_owned + len(p.halo), dtype=np.int32)
+            src_dom = np.ascontiguousarray(owner[p.halo])
+            src_site = np.ascontiguousarray(where[p.halo])
+            M.check(self.lib.mdg_group_set_halo_local(
+                self.g, d, len(p.halo), M._p(halo_local, M._ip), M._p(src_dom, M._ip),
+                M._p(src_site, M._ip)))
+
+    def _set_halo_nccl(self):
+        peers, sc, ss, rc, rs = nccl_halo_args(self.plans[self.rank])
+        M.check(self.lib.mdg_group_set_halo_nccl(
+            self.g, len(peers), M._p(peers, M._ip), M._p(sc, M._i64p), M._p(ss, M._ip),
+            M._p(rc, M._i64p), M._p(rs, M._ip)))
+
+    # ---- per step
     def exchange(self, vec_id: int):
-        if self.comm.size == 1:
-            return
-        if getattr(self.comm, "cuda", False):
-            self._exchange_dev(vec_id)
-            return
-        sends = {q: self.eng.vec_pack(vec_id, idx) for q, idx in self.plan.send.items()}
-        recvs = self.comm.exchange(sends, self.recv_counts)
-        for q, buf in recvs.items():
-            self.eng.vec_unpack(vec_id, self.plan.recv[q], np.asarray(buf, np.float64))
+        M.check(self.lib.mdg_group_exchange(self.g, vec_id))
 
-    def _exchange_dev(self, vec_id: int):
-        torch = self.comm.torch
-        dev = self.comm.device
-        if not self._dev_idx:
-            for tag, d in (("s", self.plan.send), ("r", self.plan.recv)):
-                for q, idx in d.items():
-                    self._dev_idx[(tag, q)] = torch.from_numpy(idx).to(dev)
-        sends = {}
-        for q, idx in self.plan.send.items():
-            buf = torch.empty(3 * len(idx), dtype=torch.float64, device=dev)
-            M.check(self.eng.lib.mdg_vec_pack_dev(
-                self.eng.ctx, vec_id, C.c_void_p(self._dev_idx[("s", q)].data_ptr()), len(idx),
-                C.c_void_p(buf.data_ptr())))
-            sends[q] = buf
-        recvs = self.comm.exchange(sends, self.recv_counts)
-        for q, buf in recvs.items():
-            M.check(self.eng.lib.mdg_vec_unpack_dev(
-                self.eng.ctx, vec_id, C.c_void_p(self._dev_idx[("r", q)].data_ptr()),
-                len(self.plan.recv[q]), C.c_void_p(buf.data_ptr())))
+    def upload_frames(self, frame, zatom, xatom, dipole, quadrupole):
+        for d in self.domains:
+            d.upload_frames(frame, zatom, xatom, dipole, quadrupole)
 
-    def _exchange_cb(self, user, vec_id):
-        try:
-            self.exchange(vec_id)
-            return 0
-        except Exception as e:  # surfaced as MDG_COMM by the solver
-            self.error = e
-            return 1
-
-    def _allreduce_cb(self, user, vals, n):
-        try:
-            arr = np.ctypeslib.as_array(vals, (n,))
-            arr[:] = self.comm.allreduce(arr)
-            return 0
-        except Exception as e:
-            self.error = e
-            return 1
-
-    # ---- step
     def build_lists(self, lists):
-        """lists: [(cutoff, list_id, sites), ...] -- rows for owned sites."""
-        return {lid: self.eng.build_neighbor_table(cut, list_id=lid, sites=sites)
-                for cut, lid, sites in lists}
+        """lists: [(cutoff, list_id, sites), ...]: every local domain builds the
+        rows of its owned sites (candidates: owned + halo)."""
+        for d in self.domains:
+            for cut, lid, sites in lists:
+                d.eng.build_neighbor_table(cut, list_id=lid, sites=sites)
+        return {lid: lid for _, lid, _ in lists}
 
     def update_positions(self, x, y, z):
-        """New global coordinates: owned from the caller, halo refreshed by exchange."""
-        own = self.plan.owned
-        n = len(self.plan.local)
-        lx = np.zeros(n)
-        ly = np.zeros(n)
-        lz = np.zeros(n)
-        lx[: len(own)], ly[: len(own)], lz[: len(own)] = x[own], y[own], z[own]
-        lx[len(own):] = np.asarray(x)[self.plan.halo]  # placeholder, overwritten below
-        ly[len(own):] = np.asarray(y)[self.plan.halo]
-        lz[len(own):] = np.asarray(z)[self.plan.halo]
-        self.eng.upload_positions(lx, ly, lz)
+        """New global coordinates: each domain uploads its local sites' (the
+        halo part is then refreshed from the owners by the group exchange)."""
+        xyz = np.stack([np.asarray(x), np.asarray(y), np.asarray(z)], 1)
+        d = xyz - self.ref_xyz
+        d -= self.box * np.round(d / self.box)
+        moved = float(np.sqrt(np.max(np.sum(d * d, 1)))) if len(d) else 0.0
+        if moved > self.margin:
+            raise HaloStale(f"a site moved {moved:.3f} A since the plan was built "
+                            f"(margin {self.margin:.3f} A): rebuild the plan")
+        for dom in self.domains:
+            loc = dom.plan.local
+            dom.eng.upload_positions(np.asarray(x)[loc], np.asarray(y)[loc], np.asarray(z)[loc])
         self.exchange(VEC_POS)
 
     def amoeba_step(self, tables, params):
         vdw = tables.get(1, tables[0])
-        try:
-            self.eng.amoeba_step(vdw, tables[0], params)
-        finally:
-            if self.error is not None:
-                raise self.error
+        M.check(self.lib.mdg_group_amoeba_step(self.g, vdw, tables[0], C.byref(params)))
 
     def charmm_step(self, tables, params):
-        self.eng.charmm_step(tables[0], params)
+        M.check(self.lib.mdg_group_charmm_step(self.g, tables[0], C.byref(params)))
 
     def energies(self):
-        """Global energies and virial (sum over ranks) and the PCG record."""
-        e, w, it, rms = self.eng.fetch_energies()
-        tot = self.comm.allreduce(np.concatenate([e, w.reshape(-1)])) if self.comm.size > 1 \
-            else np.concatenate([e, w.reshape(-1)])
-        return tot[:4], tot[4:].reshape(3, 3), it, rms
+        """Global energies and virial (all domains, all ranks) and the PCG record."""
+        e = np.zeros(4)
+        w = np.zeros(9)
+        it = C.c_int64()
+        rms = C.c_double()
+        M.check(self.lib.mdg_group_fetch_energies(self.g, M._p(e), M._p(w), C.byref(it),
+                                                  C.byref(rms)))
+        return e, w.reshape(3, 3), it.value, rms.value
 
     def owned_forces(self):
-        """(global ids, forces) of the owned sites."""
-        f = self.eng.fetch_forces()
-        return self.plan.owned, f[: self.plan.n_owned]
+        """(global ids, forces) of the owned sites of the local domains."""
+        ids = [d.plan.owned for d in self.domains]
+        f = [d.eng.fetch_forces()[: d.plan.n_owned] for d in self.domains]
+        return np.concatenate(ids), np.concatenate(f)
 
     def owned_dipoles(self):
-        mu = self.eng.fetch_dipoles()
-        return self.plan.owned, mu[: self.plan.n_owned]
+        ids = [d.plan.owned for d in self.domains]
+        mu = [d.eng.fetch_dipoles()[: d.plan.n_owned] for d in self.domains]
+        return np.concatenate(ids), np.concatenate(mu)
 
     def check_halo(self, s) -> bool:
-        """Self-check of the exchange path: refresh the halo coordinates and
-        compare them with the global fixture every rank holds."""
-        if not len(self.plan.halo):
-            return True
-        n_own = self.plan.n_owned
-        halo_local = np.arange(n_own, n_own + len(self.plan.halo), dtype=np.int32)
-        # scramble the halo, then let the exchange restore it
-        self.eng.vec_unpack(VEC_POS, halo_local, np.zeros(3 * len(halo_local)))
+        """Self-check of the exchange path: scramble every local domain's halo
+        coordinates, refresh them from the owners, compare with the fixture."""
+        want_all = np.stack([np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)], 1)
+        for d in self.domains:
+            p = d.plan
+            if len(p.halo):
+                halo_local = np.arange(p.n_owned, p.n_owned + len(p.halo), dtype=np.int32)
+                d.eng.vec_unpack(VEC_POS, halo_local, np.zeros(3 * len(halo_local)))
         self.exchange(VEC_POS)
-        got = self.eng.vec_pack(VEC_POS, halo_local).reshape(-1, 3)
-        want = np.stack([np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)], 1)[self.plan.halo]
-        return bool(np.array_equal(got, want))
+        ok = True
+        for d in self.domains:
+            p = d.plan
+            if len(p.halo):
+                halo_local = np.arange(p.n_owned, p.n_owned + len(p.halo), dtype=np.int32)
+                got = d.eng.vec_pack(VEC_POS, halo_local).reshape(-1, 3)
+                ok &= bool(np.array_equal(got, want_all[p.halo]))
+        return ok
+
+    def launch_count(self) -> int:
+        return sum(d.eng.launch_count() for d in self.domains)
 
     def close(self):
-        self.eng.lib.mdg_set_comm(self.eng.ctx, None, None, None)
-        self.eng.close()
+        if getattr(self, "g", None) and self.g.value:
+            self.lib.mdg_group_destroy(self.g)
+            self.g = C.c_void_p()
+        for d in getattr(self, "domains", []):
+            d.eng.close()

@@ -142,7 +142,19 @@ SIGNATURES = {
     "mdg_profile_report": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "mdg_system_upload_owned": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                           C.c_double, C.c_double, C.c_double] + [_dp] * 9),
-    "mdg_set_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mdg_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "mdg_group_create_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int,
+                                         C.POINTER(C.c_void_p), C.c_int64]),
+    "mdg_group_create_nccl": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_int64]),
+    "mdg_group_destroy": (C.c_int, [C.c_void_p]),
+    "mdg_group_set_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _ip, _ip, _ip]),
+    "mdg_group_set_halo_nccl": (C.c_int, [C.c_void_p, C.c_int, _ip, _i64p, _ip, _i64p, _ip]),
+    "mdg_group_exchange": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_group_allreduce_results": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "mdg_group_amoeba_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "mdg_group_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "mdg_group_fetch_energies": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _dp]),
     "mdg_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_frames_upload": (C.c_int, [C.c_void_p, _ip, _ip, _ip, _dp, _dp]),
     "mdg_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),

@@ -1,11 +1,13 @@
 """Spatial domain decomposition.
 
 CPU: the decomposition plan (ownership, halo completeness, send/recv
-symmetry) and a world-size-2 gloo run of the multi-domain protocol --
-TorchComm halo exchange + all-reduce driving a PCG solve and the pair
-forces/energies on per-rank local systems -- against the single-domain
-oracle. The per-rank compute here is the oracle (test infrastructure); the
-product path (DDEngine over libmdg.so) runs the same plan and hooks on the
+symmetry, the displacement guard) and a world-size-2 gloo run in which
+every rank builds its NCCL halo arguments with the product code
+(dd.nccl_halo_args) and checks them against its peer's over gloo, then runs
+the multi-domain solve protocol of csrc/polar.cu run_pcg_multi (halo refresh
+of the direction, three summed CG scalars per iteration) with the oracle's
+kernels on its local system, against the single-domain oracle. The device
+runtime itself (csrc/group.cu, LOCAL and NCCL backends) is exercised on the
 GPU in tests/test_gpu_dd.py.
 """
 import os
@@ -71,11 +73,27 @@ def _rank_main(rank, size, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
+        import torch
         o = Oracle()
-        comm = dd.TorchComm()
+        comm = _GlooComm(dist, torch)
         s = water(mdg)
         plans = dd.build_plans(s.x, s.y, s.z, s.molecule, s.box, size, HALO)
         p = plans[rank]
+        # the product's NCCL halo arguments agree with the peer's (global ids, order)
+        peers, sc, ss, rc, rs = dd.nccl_halo_args(p)
+        mine = {"send": {}, "recv": {}}
+        so = ro = 0
+        for k, q in enumerate(peers):
+            mine["send"][int(q)] = p.local[ss[so:so + sc[k]]].tolist()
+            mine["recv"][int(q)] = p.local[rs[ro:ro + rc[k]]].tolist()
+            so += sc[k]
+            ro += rc[k]
+        allargs = [None] * size
+        dist.all_gather_object(allargs, mine)
+        for q in range(size):
+            if q != rank:
+                assert allargs[q]["send"].get(rank, []) == mine["recv"].get(q, [])
+                assert allargs[q]["recv"].get(rank, []) == mine["send"].get(q, [])
         loc = to_oracle_system(dd.local_system(s, p))
         n_own = p.n_owned
         alpha, cut, thole = 0.5446, 7.0, 0.39
@@ -99,8 +117,8 @@ def _rank_main(rank, size, port, out_dir):
         fg[p.owned] = f[:n_own]
         fg = comm.allreduce(fg.reshape(-1)).reshape(-1, 3)
 
-        # multi-domain PCG: the protocol of run_pcg_pre with comm hooks
-        # (halo exchange of mu / p before each mat-vec, all-reduced scalars)
+        # multi-domain PCG: the protocol of run_pcg_multi (halo of mu / p before
+        # each mat-vec, r.z / p.q / (r.z, |dmu|^2) summed over the domains)
         E = o.perm_field_ewald(loc, t_all, alpha, cut, thole, exclude=True)
         pol = loc.polarizability[:, None]
 
@@ -145,6 +163,50 @@ def _rank_main(rank, size, port, out_dir):
             np.savez(os.path.join(out_dir, "dd.npz"), f=fg, e=e_tot, mu=mug, it=it)
     finally:
         dist.destroy_process_group()
+
+
+class _GlooComm:
+    """Host-buffer halo exchange + all-reduce over gloo (test transport)."""
+
+    def __init__(self, dist, torch):
+        self.dist, self.torch = dist, torch
+
+    def exchange(self, sends, recv_counts):
+        t, dist = self.torch, self.dist
+        ops, out = [], {}
+        for q, n in recv_counts.items():
+            out[q] = t.empty(n, dtype=t.float64)
+            ops.append(dist.P2POp(dist.irecv, out[q], q))
+        for q, buf in sends.items():
+            ops.append(dist.P2POp(dist.isend, t.from_numpy(np.ascontiguousarray(buf)), q))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return {q: v.numpy() for q, v in out.items()}
+
+    def allreduce(self, vals):
+        buf = self.torch.from_numpy(np.array(vals, np.float64))
+        self.dist.all_reduce(buf)
+        return buf.numpy()
+
+
+def test_halo_stale_guard(mdg):
+    """positions that moved past the halo margin since the plan
+    was built are refused (HaloStale) instead of silently dropping pairs."""
+    from paper_1906_01211_b200 import dd
+    s = water(mdg, 512, 24.8)
+    g = dd.DomainGroup.__new__(dd.DomainGroup)  # plan-level check only (no device)
+    g.box = np.asarray(s.box, float)
+    g.ref_xyz = np.stack([s.x, s.y, s.z], 1).copy()
+    g.margin = 0.25
+    g.domains = []
+    g.exchange = lambda v: None
+    x = np.array(s.x)
+    x[5] = (x[5] + 0.2) % s.box[0]
+    g.update_positions(x, s.y, s.z)  # within the margin
+    x[7] = (x[7] + 0.3) % s.box[0]
+    with pytest.raises(dd.HaloStale):
+        g.update_positions(x, s.y, s.z)
 
 
 def test_gloo_world2_matches_single_domain(tmp_path, oracle, mdg):

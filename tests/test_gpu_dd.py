@@ -1,10 +1,9 @@
-"""GPU: the multi-domain product path (DDEngine over libmdg.so: owned + halo
-contexts, halo exchange and all-reduce hooks inside the C++ PCG solve) with
-2 and 4 domains hosted on ONE GPU -- one context and one host thread per
-domain, exchanging through LocalComm -- against the single-domain engine.
-(No kernel waits on another: the domains synchronise on the host.)"""
-import threading
-
+"""GPU: the multi-domain product path -- the C++ group runtime
+(csrc/group.cu: halo refresh and summed CG scalars on the device inside the
+PCG solve, csrc/polar.cu run_pcg_multi) over owned + halo domain contexts --
+with 2, 4 and 8 domains hosted on ONE GPU (LOCAL backend: one process, one
+shared stream, no kernel waits on another domain's), against the
+single-domain engine; and the NCCL backend at world size 1."""
 import numpy as np
 import pytest
 
@@ -13,60 +12,51 @@ pytestmark = pytest.mark.gpu
 HALO = 12.5  # 11 A vdW list + intramolecular extent + margin
 
 
-def run_domains(mdg, s, size, params, lists, frames=None):
+def run_domains(mdg, s, size, params, lists, frames=None, steps=1):
     from paper_1906_01211_b200 import dd
-    comms = dd.LocalComm.group(size)
-    plans = dd.build_plans(s.x, s.y, s.z, s.molecule, s.box, size, HALO)
-    out = [None] * size
-    errs = []
-
-    def work(r):
-        try:
-            e = dd.DDEngine(s, comms[r], 0, HALO, plans=plans)
-            if frames is not None:
-                e.upload_frames(*frames)
-            tables = e.build_lists(lists)
-            e.amoeba_step(tables, params)
-            en, w, it, rms = e.energies()
-            ids, f = e.owned_forces()
-            _, mu = e.owned_dipoles()
-            out[r] = (ids, f, mu, en, w, it)
-            e.close()
-        except Exception as ex:  # pragma: no cover - reported below
-            errs.append(ex)
-            raise
-
-    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=600)
-    assert not errs, errs
+    g = dd.DomainGroup(s, size, HALO, device=0, backend="local", list_cutoff=11.0)
+    try:
+        assert g.check_halo(s)
+        if frames is not None:
+            g.upload_frames(*frames)
+        tables = g.build_lists(lists)
+        for _ in range(steps):
+            g.amoeba_step(tables, params)
+        en, w, it, rms = g.energies()
+        ids, f = g.owned_forces()
+        _, mu = g.owned_dipoles()
+    finally:
+        g.close()
     n = s.n_sites
     F = np.zeros((n, 3))
     MU = np.zeros((n, 3))
-    for ids, f, mu, *_ in out:
-        F[ids] = f
-        MU[ids] = mu
-    return F, MU, out[0][3], out[0][4], out[0][5]
+    F[ids] = f
+    MU[ids] = mu
+    return F, MU, en, w, it
 
 
-@pytest.mark.parametrize("size,polar_forces", [(2, False), (4, False), (2, True)])
+def single(mdg, s, p, frames=None):
+    with mdg.Engine(s.n_sites) as e:
+        e.upload_system(s)
+        if frames is not None:
+            e.upload_frames(*frames)
+        te = e.build_neighbor_table(9.0, list_id=0)
+        tv = e.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+        e.amoeba_step(tv, te, p)
+        en0, w0, it0, _ = e.fetch_energies()
+        return en0, w0, it0, e.fetch_forces(), e.fetch_dipoles()
+
+
+
+@pytest.mark.parametrize("size,polar_forces", [(2, False), (4, False), (8, False), (2, True)])
 def test_domains_match_single_gpu(mdg, size, polar_forces):
     s = mdg.water_box(1728, 37.26, 5, "amoeba")
     terms = (mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
              if polar_forces else 0)
     p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
     lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
-    with mdg.Engine(s.n_sites) as e:
-        e.upload_system(s)
-        te = e.build_neighbor_table(9.0, list_id=0)
-        tv = e.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
-        e.amoeba_step(tv, te, p)
-        en0, w0, it0, _ = e.fetch_energies()
-        f0 = e.fetch_forces()
-        mu0 = e.fetch_dipoles()
-    F, MU, en, w, it = run_domains(mdg, s, size, p, lists)
+    en0, w0, it0, f0, mu0 = single(mdg, s, p)
+    F, MU, en, w, it = run_domains(mdg, s, size, p, lists, steps=2)
     rms = np.sqrt(np.mean(f0 ** 2))
     assert np.abs(F - f0).max() <= 1e-8 * rms
     for k in range(3):
@@ -79,7 +69,7 @@ def test_domains_match_single_gpu(mdg, size, polar_forces):
 
 def test_domains_with_local_frames(mdg):
     """Local multipole frames in the decomposed step (frame atoms mapped to
-    each rank's local ids) match the single engine."""
+    each domain's local ids) match the single engine."""
     from oracle import frames as fr
     s = mdg.water_box(1728, 37.26, 6, "amoeba")
     frame, za, xa = fr.water_frames(s.molecule)
@@ -87,17 +77,77 @@ def test_domains_with_local_frames(mdg):
     terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
     p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
     lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
-    with mdg.Engine(s.n_sites) as e:
-        e.upload_system(s)
-        e.upload_frames(*frames)
-        te = e.build_neighbor_table(9.0, list_id=0)
-        tv = e.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
-        e.amoeba_step(tv, te, p)
-        en0, w0, it0, _ = e.fetch_energies()
-        f0 = e.fetch_forces()
+    en0, w0, it0, f0, _ = single(mdg, s, p, frames)
     F, MU, en, w, it = run_domains(mdg, s, 2, p, lists, frames)
     rms = np.sqrt(np.mean(f0 ** 2))
     assert np.abs(F - f0).max() <= 1e-8 * rms
     for k in range(3):
         assert en[k] == pytest.approx(en0[k], rel=1e-9)
     assert abs(it - it0) <= 1
+
+
+def test_domains_follow_new_positions(mdg):
+    """Positions moved within the halo margin: owned coordinates uploaded per
+    domain, halos refreshed by the group exchange; == the single engine at
+    the new coordinates."""
+    from paper_1906_01211_b200 import dd
+    s = mdg.water_box(1728, 37.26, 7, "amoeba")
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, 0)
+    lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
+    rng = np.random.default_rng(3)
+    g = dd.DomainGroup(s, 2, HALO, backend="local", list_cutoff=11.0)
+    try:
+        tables = g.build_lists(lists)
+        g.amoeba_step(tables, p)
+        L = s.box[0]
+        x = np.mod(np.asarray(s.x) + rng.uniform(-0.2, 0.2, s.n_sites), L)
+        y = np.mod(np.asarray(s.y) + rng.uniform(-0.2, 0.2, s.n_sites), L)
+        z = np.mod(np.asarray(s.z) + rng.uniform(-0.2, 0.2, s.n_sites), L)
+        g.update_positions(x, y, z)
+        tables = g.build_lists(lists)
+        g.amoeba_step(tables, p)
+        en, _, it, _ = g.energies()
+        ids, f = g.owned_forces()
+    finally:
+        g.close()
+    s2 = mdg.water_box(1728, 37.26, 7, "amoeba")
+    s2.x, s2.y, s2.z = x, y, z
+    en0, _, it0, f0, _ = single(mdg, s2, p)
+    F = np.zeros_like(f0)
+    F[ids] = f
+    assert np.abs(F - f0).max() <= 1e-8 * np.sqrt(np.mean(f0 ** 2))
+    assert en[0] == pytest.approx(en0[0], rel=1e-9) and abs(it - it0) <= 1
+
+
+def test_nccl_group_world_size_one(mdg):
+    """The NCCL backend (ncclCommInitRank, in-place ncclAllReduce of the CG
+    scalars, batched speculative iterations) at world size 1 on this GPU ==
+    the single engine."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1906_01211_b200 import dd
+    s = mdg.water_box(1000, 31.04, 8, "amoeba")
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, 0)
+    en0, w0, it0, f0, mu0 = single(mdg, s, p)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29611")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        g = dd.DomainGroup(s, 1, HALO, backend="nccl", rank=0, list_cutoff=11.0)
+        try:
+            tables = g.build_lists([(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)])
+            g.amoeba_step(tables, p)
+            en, w, it, rms = g.energies()
+            ids, f = g.owned_forces()
+        finally:
+            g.close()
+    finally:
+        dist.destroy_process_group()
+    F = np.zeros_like(f0)
+    F[ids] = f
+    assert np.abs(F - f0).max() <= 1e-12 * np.abs(f0).max()
+    assert it == it0 and rms < 1e-5
+    for k in range(3):
+        assert en[k] == pytest.approx(en0[k], rel=1e-12)
