@@ -333,6 +333,12 @@ int mdg_group_set_halo_nccl(mdg_group* g, int npeers, const int32_t* peers,
  * their owners (POS also refreshes the Halgren-reduced halo sites). Returns
  * after completion. */
 int mdg_group_exchange(mdg_group* g, int vec_id);
+/* Snapshot every domain's owned positions as the plan's reference, and the
+ * largest minimum-image displacement of any owned site since (max over all
+ * domains / ranks): the halo misses no pair while it stays below half the
+ * halo margin (halo width - list cutoff - intramolecular extent). */
+int mdg_group_set_reference(mdg_group* g);
+int mdg_group_max_displacement(mdg_group* g, double* out);
 /* Sum result slots [slot, slot + nv) over all domains / ranks, in place, on
  * the device (stream-ordered; nv <= 32). */
 int mdg_group_allreduce_results(mdg_group* g, int slot, int nv);
@@ -371,6 +377,13 @@ int mdg_vec_unpack_dev(mdg_ctx* ctx, int vec_id, const int32_t* d_sites, int64_t
                        const double* d_in);
 
 /* ---- instrumentation ---------------------------------------------------- */
+/* Fault injection, the analogue of the reference bench's
+ * debug_perturb_vectorized (proj/include/mdvec/bench.hpp:42-44,
+ * proj/src/bench.cpp:244-255): delta is added to the x force of the first
+ * site returned by mdg_fetch_forces and to energies[0] of
+ * mdg_fetch_energies, so a parity check downstream must flag the results.
+ * 0 (default) disables it. */
+int mdg_set_debug_perturb(mdg_ctx* ctx, double delta);
 /* CUDA events on the context stream: start records, stop records, waits and
  * returns the elapsed device milliseconds. */
 int mdg_timer_start(mdg_ctx* ctx);

@@ -1504,9 +1504,18 @@ int mdg_fetch_forces(mdg_ctx* c, double* fx, double* fy, double* fz) {
     if (c->fout[0] && fx == c->fout[0] && fy == c->fout[1] && fz == c->fout[2] &&
         c->fout_seq + 1 == g_api_seq.load(std::memory_order_relaxed)) {
       MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+      if (fx && c->debug_perturb != 0.0) fx[0] += c->debug_perturb;
       return;
     }
     vec_out(c, c->force, fx, fy, fz);
+    if (fx && c->debug_perturb != 0.0) fx[0] += c->debug_perturb;
+  });
+}
+
+int mdg_set_debug_perturb(mdg_ctx* c, double delta) {
+  return guard([&] {
+    need_ctx(c);
+    c->debug_perturb = delta;
   });
 }
 
@@ -1570,6 +1579,7 @@ int mdg_fetch_energies(mdg_ctx* c, double* energies4, double* virial9, int64_t* 
     need_system(c);
     double e[4], w[9];
     energies_of(c, e, w);
+    e[0] += c->debug_perturb;
     if (energies4) std::memcpy(energies4, e, sizeof e);
     if (virial9) std::memcpy(virial9, w, sizeof w);
     if (pcg_iters) *pcg_iters = c->pcg_iters > 0 ? c->pcg_iters : 0;

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kBlock) k_cluster_union(CUArgs a) {
     if (!__any_sync(0xffffffffu, live)) break;
     const bool hit = live && cur == m;
     const unsigned bm = (__ballot_sync(0xffffffffu, hit) >> (G * g)) & ((1u << G) - 1u);
+    MDG_DASSERT(!live || s < a.ucap);
     if (k == 0 && live) out[s] = (uint32_t)m | (bm << 24);
     s += live;
     h += hit;
@@ -149,6 +150,7 @@ __global__ void MDG_CL_BOUNDS k_tmatvec_cl(CLArgs a) {
     const int32_t craw = a.ucnt[cl];
     const bool wide = craw < 0;
     const int ucount = craw & 0x7fffffff;
+    MDG_DASSERT(ucount <= a.ucap);
     const uint32_t* urow = a.ucl + (size_t)cl * a.ucap;
     const double2* tp[G];
     double ex[G], ey[G], ez[G];

@@ -8,6 +8,17 @@
 
 #include "mdg_internal.h"
 
+// Debug build (make debug: -DMDG_DEBUG, libmdg_debug.so): device asserts on
+// list / ring / slot bounds, and a full check of every list the kernels walk
+// (debug.cu). The substitute for compute-sanitizer, which is closed on this
+// pool. Compiled out of the product build.
+#ifdef MDG_DEBUG
+#include <cassert>
+#define MDG_DASSERT(c) assert(c)
+#else
+#define MDG_DASSERT(c) ((void)0)
+#endif
+
 namespace mdg {
 
 // proj/include/mdvec/pbc.hpp:27-31, op for op: DMUL, FRND (round-half-even
@@ -257,6 +268,7 @@ struct Ring {
 __device__ __forceinline__ void ring_push(Ring& r, bool in, double dx, double dy, double dz,
                                           int32_t j, int32_t type) {
   const unsigned m = __ballot_sync(0xffffffffu, in);
+  MDG_DASSERT(r.count >= 0 && r.count + __popc(m) <= kRing);
   if (in) {
     const int pos = (r.head + r.count + __popc(m & lanemask_lt())) & (kRing - 1);
     r.q[pos] = make_double4(dx, dy, dz, __hiloint2double(type, j));
@@ -267,6 +279,7 @@ __device__ __forceinline__ void ring_push(Ring& r, bool in, double dx, double dy
 
 // Take `take` (<= 32) entries; lane l gets entry l when l < take.
 __device__ __forceinline__ double4 ring_take(Ring& r, int take, int lane) {
+  MDG_DASSERT(take >= 0 && take <= 32 && take <= r.count);
   double4 e = make_double4(0, 0, 0, 0);
   if (lane < take) e = r.q[(r.head + lane) & (kRing - 1)];
   r.head = (r.head + take) & (kRing - 1);
@@ -301,6 +314,7 @@ __device__ __forceinline__ int run_row(const int32_t* __restrict__ row, int cnt,
                                        const double4* __restrict__ P,
                                        const int32_t* __restrict__ mol, Ring& ring, Pro&& pro,
                                        Body&& body) {
+  MDG_DASSERT(cnt >= 0);
   int32_t ja = (lane < cnt) ? __ldg(row + lane) : 0;
   double4 pa = ldg4(P + (ja & 0x7fffffff));
   int32_t ma = mol ? __ldg(mol + (ja & 0x7fffffff)) : 0;

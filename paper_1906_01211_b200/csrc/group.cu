@@ -30,6 +30,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -130,6 +131,22 @@ __global__ void k_unpack3(int64_t n, const int32_t* __restrict__ idx, const doub
   a->z = in[3 * k + 2];
 }
 
+// max |minimum image (pos - ref)|^2 over the owned sites, as ordered bits
+__global__ void k_max_disp2(int64_t n, Box b, const double4* __restrict__ pos,
+                            const double4* __restrict__ ref, unsigned long long* __restrict__ out) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (s < n) {
+    const double4 p = pos[s], r = ref[s];
+    double dx, dy, dz;
+    d2 = min_image(b, p.x, p.y, p.z, r.x, r.y, r.z, dx, dy, dz);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(d2));
+}
+
 void refresh_vsites(mdg_ctx* c);  // core.cu: vdW sites after new halo positions
 
 }  // namespace mdg
@@ -165,6 +182,8 @@ struct mdg_group : PcgComm {
   double* d_rbuf = nullptr;
   int64_t nsend = 0, nrecv = 0;
   double* d_sum = nullptr;  // energy / virial all-reduce buffer
+  std::vector<double4*> ref;  // per domain: positions when the plan was made
+  unsigned long long* d_disp = nullptr;
 
   cudaStream_t stream() const { return dom[0]->stream; }
 
@@ -342,8 +361,9 @@ int mdg_group_destroy(mdg_group* g) {
       cudaFree(h.src);
     }
     for (void* p : {(void*)g->d_vecs, (void*)g->d_res, (void*)g->d_send, (void*)g->d_recv,
-                    (void*)g->d_sbuf, (void*)g->d_rbuf, (void*)g->d_sum})
+                    (void*)g->d_sbuf, (void*)g->d_rbuf, (void*)g->d_sum, (void*)g->d_disp})
       if (p) cudaFree(p);
+    for (double4* r : g->ref) cudaFree(r);
     if (g->comm) nccl().CommDestroy(g->comm);
     delete g;
   });
@@ -438,6 +458,47 @@ int mdg_group_exchange(mdg_group* g, int vec_id) {
     if (g->backend == MDG_GROUP_LOCAL) refresh_tables(g);
     g->exchange_vec(vec_id, false);
     MDG_CUDA_CHECK(cudaStreamSynchronize(g->stream()));
+  });
+}
+
+int mdg_group_set_reference(mdg_group* g) {
+  return gguard([&] {
+    gneed(g != nullptr, "group: null");
+    MDG_CUDA_CHECK(cudaSetDevice(g->dom[0]->device));
+    g->ref.resize(g->dom.size(), nullptr);
+    for (size_t d = 0; d < g->dom.size(); ++d) {
+      mdg_ctx* c = g->dom[d];
+      if (!g->ref[d]) MDG_CUDA_CHECK(cudaMalloc(&g->ref[d], (size_t)c->n_cap * sizeof(double4)));
+      MDG_CUDA_CHECK(cudaMemcpyAsync(g->ref[d], c->pos, (size_t)c->n_own * sizeof(double4),
+                                     cudaMemcpyDeviceToDevice, c->stream));
+    }
+    MDG_CUDA_CHECK(cudaStreamSynchronize(g->stream()));
+  });
+}
+
+int mdg_group_max_displacement(mdg_group* g, double* out) {
+  return gguard([&] {
+    gneed(g != nullptr && out != nullptr, "group: null");
+    gneed(g->ref.size() == g->dom.size(), "max_displacement: no reference (mdg_group_set_reference)");
+    MDG_CUDA_CHECK(cudaSetDevice(g->dom[0]->device));
+    if (!g->d_disp) MDG_CUDA_CHECK(cudaMalloc(&g->d_disp, sizeof(unsigned long long)));
+    cudaStream_t s = g->stream();
+    MDG_CUDA_CHECK(cudaMemsetAsync(g->d_disp, 0, sizeof(unsigned long long), s));
+    for (size_t d = 0; d < g->dom.size(); ++d) {
+      mdg_ctx* c = g->dom[d];
+      c->launches++;
+      k_max_disp2<<<grid_for(c->n_own, 256), 256, 0, c->stream>>>(
+          c->n_own, make_box(c->lx, c->ly, c->lz), c->pos, g->ref[d], g->d_disp);
+    }
+    double d2 = 0.0;
+    if (g->backend == MDG_GROUP_NCCL && g->size > 1)
+      nccl_check(nccl().AllReduce(g->d_disp, g->d_disp, 1, ncclUint64, ncclMax, g->comm, s),
+                 "ncclAllReduce");
+    unsigned long long bits = 0;
+    MDG_CUDA_CHECK(cudaMemcpyAsync(&bits, g->d_disp, sizeof bits, cudaMemcpyDeviceToHost, s));
+    MDG_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::memcpy(&d2, &bits, sizeof d2);
+    *out = std::sqrt(d2);
   });
 }
 

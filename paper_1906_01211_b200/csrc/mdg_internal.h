@@ -257,6 +257,9 @@ struct mdg_ctx {
   int64_t epoch = 0;  // source of DevList::version
   // full-row (bitwise reproducible) pair sums instead of half rows + atomics
   bool deterministic = false;
+  // fault injection (mdg_set_debug_perturb): added to the first returned
+  // force component and energy, so the parity checks' failure path is tested
+  double debug_perturb = 0.0;
   bool overlap = true;  // AMOEBA step on two streams (mdg_set_overlap)
   bool has_polar_force = false;  // last AMOEBA step added polarization forces
   // second stream of the AMOEBA step: Halgren + multipoles run beside the
@@ -441,6 +444,11 @@ std::vector<mdg_ctx*> group_domains(mdg_group* g);
 bool group_is_nccl(mdg_group* g);
 void group_refresh(mdg_group* g);
 void group_sum_host(mdg_group* g, double* v, int nv);
+// debug builds (-DMDG_DEBUG): device-assert every row's count <= cap, every
+// neighbour index in [0, n_all) and != the row's site, ascending when sorted
+// (debug.cu); a no-op in the product build
+void debug_check_rows(mdg_ctx* c, const char* what, const int32_t* nbr, const int32_t* cnt,
+                      int32_t cap, int64_t rows, int64_t n_all, bool sorted);
 // vdW sites from the positions (Halgren reduction or copy), after new positions
 void refresh_vsites(mdg_ctx* c);
 void run_reduce_sites(mdg_ctx* c);

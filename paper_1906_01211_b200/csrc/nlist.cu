@@ -591,6 +591,7 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
       L.sites = sites;
       L.max_cnt = mx;
       L.half_pairs = sum / 2;
+      debug_check_rows(c, "list", L.nbr, L.cnt, L.cap, rows, c->n, false);
       return;
     }
     cap = (mx + 31) & ~31;
@@ -738,6 +739,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
   // the cut rows are short: sort them (bucketed by length), when cut
   const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);
+  debug_check_rows(c, "inner", I.nbr, I.cnt, L.cap, c->n_own, c->n, sorted);
   return ListView{I.nbr, I.cnt, L.cap, sorted, true};
 }
 

@@ -345,6 +345,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
       P.src = list_id;
       P.cutoff = cutoff;
       P.directed = (int64_t)c->h_results[63];
+      debug_check_rows(c, "pruned", P.nbr, P.cnt, P.cap, n, c->n, P.sorted);
       build_clusters(c, cutoff);
       return;
     }
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
   MDG_SITE_LOOP(i, a.n, a.ipw) {
     const double4 pi = a.pos[i];
     const int cnt = a.pcnt[i];
+    MDG_DASSERT(cnt >= 0 && cnt <= a.pcap);
     const int32_t* row = a.pnbr + (size_t)i * a.pcap;
     const double2* trow = a.trr + (size_t)i * a.pcap;
     double ex = 0, ey = 0, ez = 0;

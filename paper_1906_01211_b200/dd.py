@@ -218,7 +218,6 @@ class DomainGroup:
         # before the halo can miss a pair (update_positions checks)
         lc = list_cutoff if list_cutoff is not None else halo_width - 1.5
         self.margin = max(0.0, (self.halo_width - lc - 1.0) / 2.0)
-        self.ref_xyz = np.stack([np.asarray(s.x), np.asarray(s.y), np.asarray(s.z)], 1).copy()
         mine = range(size) if backend == "local" else [rank]
         self.domains = [Domain(s, self.plans[r], self.n_global, device) for r in mine]
         self.g = C.c_void_p()
@@ -240,6 +239,7 @@ class DomainGroup:
             self._set_halo_nccl()
         else:
             raise ValueError(f"unknown backend {backend!r}")
+        M.check(self.lib.mdg_group_set_reference(self.g))
 
     # ---- halo plans
     def _set_halo_local(self):
@@ -280,18 +280,22 @@ class DomainGroup:
 
     def update_positions(self, x, y, z):
         """New global coordinates: each domain uploads its local sites' (the
-        halo part is then refreshed from the owners by the group exchange)."""
-        xyz = np.stack([np.asarray(x), np.asarray(y), np.asarray(z)], 1)
-        d = xyz - self.ref_xyz
-        d -= self.box * np.round(d / self.box)
-        moved = float(np.sqrt(np.max(np.sum(d * d, 1)))) if len(d) else 0.0
-        if moved > self.margin:
-            raise HaloStale(f"a site moved {moved:.3f} A since the plan was built "
-                            f"(margin {self.margin:.3f} A): rebuild the plan")
+        halo part is then refreshed from the owners by the group exchange).
+        Raises HaloStale when a site has moved past half the halo margin since
+        the plan was built (checked on the device, max over all domains)."""
         for dom in self.domains:
             loc = dom.plan.local
             dom.eng.upload_positions(np.asarray(x)[loc], np.asarray(y)[loc], np.asarray(z)[loc])
+        moved = self.max_displacement()
+        if moved > self.margin:
+            raise HaloStale(f"a site moved {moved:.3f} A since the plan was built "
+                            f"(margin {self.margin:.3f} A): rebuild the plan")
         self.exchange(VEC_POS)
+
+    def max_displacement(self) -> float:
+        v = C.c_double()
+        M.check(self.lib.mdg_group_max_displacement(self.g, C.byref(v)))
+        return v.value
 
     def amoeba_step(self, tables, params):
         vdw = tables.get(1, tables[0])

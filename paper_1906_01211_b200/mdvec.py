@@ -152,10 +152,13 @@ SIGNATURES = {
     "mdg_group_set_halo_nccl": (C.c_int, [C.c_void_p, C.c_int, _ip, _i64p, _ip, _i64p, _ip]),
     "mdg_group_exchange": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_group_allreduce_results": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "mdg_group_set_reference": (C.c_int, [C.c_void_p]),
+    "mdg_group_max_displacement": (C.c_int, [C.c_void_p, _dp]),
     "mdg_group_amoeba_step": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "mdg_group_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_group_fetch_energies": (C.c_int, [C.c_void_p, _dp, _dp, _i64p, _dp]),
     "mdg_set_deterministic": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_set_debug_perturb": (C.c_int, [C.c_void_p, C.c_double]),
     "mdg_frames_upload": (C.c_int, [C.c_void_p, _ip, _ip, _ip, _dp, _dp]),
     "mdg_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
@@ -717,6 +720,11 @@ class Engine:
         """Full-row pair sums (bitwise reproducible forces/torques) instead of
         the default half rows with atomic partner updates (mdg.h)."""
         check(self.lib.mdg_set_deterministic(self.ctx, int(on)))
+
+    def set_debug_perturb(self, delta: float = 0.0):
+        """Fault injection (reference debug_perturb_vectorized): delta added to
+        the first returned force component and energy."""
+        check(self.lib.mdg_set_debug_perturb(self.ctx, float(delta)))
 
     def set_overlap(self, on: bool = True):
         """AMOEBA step on two streams (default) or one (mdg.h)."""

@@ -1,7 +1,7 @@
 """Spatial domain decomposition.
 
 CPU: the decomposition plan (ownership, halo completeness, send/recv
-symmetry, the displacement guard) and a world-size-2 gloo run in which
+symmetry) and a world-size-2 gloo run in which
 every rank builds its NCCL halo arguments with the product code
 (dd.nccl_halo_args) and checks them against its peer's over gloo, then runs
 the multi-domain solve protocol of csrc/polar.cu run_pcg_multi (halo refresh
@@ -188,25 +188,6 @@ class _GlooComm:
         buf = self.torch.from_numpy(np.array(vals, np.float64))
         self.dist.all_reduce(buf)
         return buf.numpy()
-
-
-def test_halo_stale_guard(mdg):
-    """positions that moved past the halo margin since the plan
-    was built are refused (HaloStale) instead of silently dropping pairs."""
-    from paper_1906_01211_b200 import dd
-    s = water(mdg, 512, 24.8)
-    g = dd.DomainGroup.__new__(dd.DomainGroup)  # plan-level check only (no device)
-    g.box = np.asarray(s.box, float)
-    g.ref_xyz = np.stack([s.x, s.y, s.z], 1).copy()
-    g.margin = 0.25
-    g.domains = []
-    g.exchange = lambda v: None
-    x = np.array(s.x)
-    x[5] = (x[5] + 0.2) % s.box[0]
-    g.update_positions(x, s.y, s.z)  # within the margin
-    x[7] = (x[7] + 0.3) % s.box[0]
-    with pytest.raises(dd.HaloStale):
-        g.update_positions(x, s.y, s.z)
 
 
 def test_gloo_world2_matches_single_domain(tmp_path, oracle, mdg):

@@ -100,14 +100,18 @@ def test_domains_follow_new_positions(mdg):
         tables = g.build_lists(lists)
         g.amoeba_step(tables, p)
         L = s.box[0]
-        x = np.mod(np.asarray(s.x) + rng.uniform(-0.2, 0.2, s.n_sites), L)
-        y = np.mod(np.asarray(s.y) + rng.uniform(-0.2, 0.2, s.n_sites), L)
-        z = np.mod(np.asarray(s.z) + rng.uniform(-0.2, 0.2, s.n_sites), L)
+        # within the halo margin ((12.5 - 11 - 1) / 2 = 0.25 A)
+        x = np.mod(np.asarray(s.x) + rng.uniform(-0.12, 0.12, s.n_sites), L)
+        y = np.mod(np.asarray(s.y) + rng.uniform(-0.12, 0.12, s.n_sites), L)
+        z = np.mod(np.asarray(s.z) + rng.uniform(-0.12, 0.12, s.n_sites), L)
         g.update_positions(x, y, z)
         tables = g.build_lists(lists)
         g.amoeba_step(tables, p)
         en, _, it, _ = g.energies()
         ids, f = g.owned_forces()
+        # past the margin: refused
+        with pytest.raises(dd.HaloStale):
+            g.update_positions(np.mod(x + 0.3, L), y, z)
     finally:
         g.close()
     s2 = mdg.water_box(1728, 37.26, 7, "amoeba")

@@ -201,6 +201,30 @@ def test_nonpolar_random(engine, oracle, mdg, seed, n):
         np.testing.assert_allclose(g.virial, wo, rtol=0, atol=1e-9 * np.abs(wo).max() + 1e-300)
 
 
+@pytest.mark.parametrize("delta", [0.0, 1e-6])
+def test_debug_perturb_is_detected(engine, oracle, mdg, delta):
+    """Fault injection (the reference bench's debug_perturb_vectorized,
+    proj/src/bench.cpp:244-255): a perturbation of the returned force / energy
+    makes the parity checks fail; none passes them."""
+    s = mdg.water_box(343, 21.72, 1, "charmm")
+    so = to_oracle_system(s)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(10.0)
+    engine.set_debug_perturb(delta)
+    try:
+        engine.charmm_step(t, mdg.CharmmParams(9.0, 0.35, mdg.ELECTRIC, 0, 1))
+        f = engine.fetch_forces()
+        en = engine.fetch_energies()[0]
+    finally:
+        engine.set_debug_perturb(0.0)
+    to = oracle.build_table(so, 10.0)
+    flj, elj, _ = oracle.lj(so, to, 9.0, exclude=True)
+    fe, ee, _ = oracle.ewald_real(so, to, 0.35, 9.0, mdg.ELECTRIC, exclude=True)
+    ok = (force_err_rms(f, flj + fe) <= F_TOL and rel(en[0], elj) <= E_TOL
+          and rel(en[1], ee) <= E_TOL)
+    assert ok == (delta == 0.0)
+
+
 def test_lj_shift(engine, oracle, mdg):
     """proj/tests/test_kernels.cpp:288-310"""
     s = uniform(oracle, 200, 12.0, 9)
