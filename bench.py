@@ -254,6 +254,30 @@ def ncu_executed(name):
         return None
 
 
+def fp64_step_fraction(config, ms_per_step, pcg_iters, steps, peak_tflops, n_gpus):
+    """The metric's "% FP64 peak" at the step level: executed FP64 flops of one
+    config-4 step (ncu dadd + dmul + 2 dfma over every kernel of the step,
+    profiles/r2_ncu_fp64_step.json: fixed part + per PCG iteration x this
+    run's iterations + the list rebuild / 20) / the measured step time / the
+    FP64 peak of the GPUs used (the single-GPU count: halo work that
+    N > 1 domains repeat is not counted)."""
+    if config != 4:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_fp64_step.json")) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    rebuilds = -(-steps // REBUILD_EVERY)
+    flops = (d["per_eval_fixed_flops"] + d["per_pcg_iteration_flops"] * pcg_iters
+             + d["per_rebuild_flops"] * rebuilds / steps)
+    achieved = flops / (ms_per_step * 1e-3) / 1e12
+    peak = peak_tflops * n_gpus
+    return {"executed_flops_per_step": flops, "achieved_tflops": round(achieved, 3),
+            "peak_tflops": round(peak, 3), "frac": round(achieved / peak, 4),
+            "source": "profiles/r2_ncu_fp64_step.json (ncu --metrics, HEAD of round 2)"}
+
+
 def roofline_of(wl, name, cnt, tot_ms, step_ms, fp64_peak):
     work = wl.algorithmic_work(name)
     if work is None:
@@ -461,6 +485,8 @@ def run_mine(args, world, rank, local):
         "pcg_iters": int(iters),
         "pcg_rms_debye": float(rms),
         "fp64_peak_tflops_measured": round(peak, 3),
+        "fp64_step": fp64_step_fraction(args.config, ms / args.steps, int(iters), args.steps,
+                                        peak, 1),
         # profiled pass (same K steps, events around every launch)
         "kernel_ms": {k: round(v[1] / max(v[0], 1), 4) for k, v in sorted(prof.items())},
         "kernel_share": {k: round(v[1] / prof_ms, 4) for k, v in sorted(prof.items())},
@@ -608,6 +634,8 @@ def run_dd(args, world, rank, local, backend, ndom):
         "energies_kcal_mol": [float(v) for v in en[:3]],
         "pcg_iters": int(iters),
         "pcg_rms_debye": float(rms),
+        "fp64_step": fp64_step_fraction(args.config, ms / args.steps, int(iters), args.steps,
+                                        m.fp64_peak_tflops(local), n_gpus),
     }
     g.close()
     return out

@@ -291,8 +291,7 @@ static void cufft_check(cufftResult r, const char* what) {
 
 // results: 80 recip energy, 81..86 virial (xx xy xz yy yz zz), 87 self,
 // 88 excluded-pair energy, 89..97 excluded-pair virial (row-major)
-void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
-             bool exclude) {
+void pme_setup(mdg_ctx* c, int k1, int k2, int k3, int order) {
   PmeState* s = (PmeState*)c->pme;
   if (!s) c->pme = s = new PmeState();
   if (s->k1 != k1 || s->k2 != k2 || s->k3 != k3 || s->p != order || s->l1 != c->lx ||
@@ -333,6 +332,12 @@ void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double
   }
   cufft_check(cufftSetStream(s->fwd, c->stream), "stream");
   cufft_check(cufftSetStream(s->inv, c->stream), "stream");
+}
+
+void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
+             bool exclude) {
+  pme_setup(c, k1, k2, k3, order);
+  PmeState* s = (PmeState*)c->pme;
   const PmeGeom g{k1, k2, k3, order, c->lx, c->ly, c->lz};
   const int64_t n = c->n;
   MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)k1 * k2 * k3 * sizeof(double), c->stream));
@@ -358,4 +363,374 @@ void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double
   }
 }
 
+
+// ---- permanent multipoles (q, mu, Theta) --------------------------------------
+// Site operator M = q + mu.grad + Q:grad grad (the real-space kernels'
+// convention, Q = Theta/3): the grid holds sum_j M_j(grad_j) W_j(k) with
+// W_j(k) = prod_a M_p(u_ja - k_a) and grad_a = (K_a/L_a) d/du_a; after the
+// convolution the potential phi and its derivatives to third order are
+// gathered at every site: E = 1/2 sum M_i phi_i (from the convolution),
+// F_i = -M_i grad phi_i, tau_i = grad phi_i x mu_i + 2 (Q G - G Q)_{zy,xz,yx}
+// with G = grad grad phi_i. Self energy and the excluded (same-molecule)
+// pairs' erf-kernel interaction complete the Ewald sum.
+// Oracle: oracle/ewald_mpole.py (direct structure-factor sum).
+
+// th[d][j] = d-th derivative of M_p at w + j (grid point iu - j), d = 0..3
+__device__ __forceinline__ void bspline_d3(double w, int p, double (*th)[kMaxOrder]) {
+  double c[kMaxOrder];         // M_n(w + j), built up n = 2..p
+  double lo[4][kMaxOrder];     // M_{p-3}, M_{p-2}, M_{p-1}, M_p
+  c[0] = w;
+  c[1] = 1.0 - w;
+  for (int j = 2; j < kMaxOrder; ++j) c[j] = 0.0;
+  auto save = [&](int n) {
+    const int k = n - (p - 3);
+    if (k >= 0 && k < 4)
+      for (int j = 0; j < kMaxOrder; ++j) lo[k][j] = (j < n) ? c[j] : 0.0;
+  };
+  save(2);
+  for (int n = 3; n <= p; ++n) {
+    const double inv = 1.0 / (double)(n - 1);
+    double prev = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const double cj = (j < n - 1) ? c[j] : 0.0;
+      const double x = w + j;
+      const double v = (x * cj + ((double)n - x) * prev) * inv;
+      prev = cj;
+      c[j] = v;
+    }
+    save(n);
+  }
+  // M^(d)(x) = sum_l (-1)^l C(d, l) M_{p-d}(x - l)
+  const double bin[4][4] = {{1, 0, 0, 0}, {1, -1, 0, 0}, {1, -2, 1, 0}, {1, -3, 3, -1}};
+  for (int d = 0; d < 4; ++d)
+    for (int j = 0; j < p; ++j) {
+      double v = 0.0;
+      for (int l = 0; l <= d; ++l)
+        if (j - l >= 0) v += bin[d][l] * lo[3 - d][j - l];
+      th[d][j] = v;
+    }
+}
+
+__global__ void k_pme_spread_mp(int64_t n, PmeGeom g, const double4* __restrict__ pos,
+                                const double4* __restrict__ pq4, const double4* __restrict__ mp,
+                                double* __restrict__ grid) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 r = pos[i];
+  const double q = pq4[i].z;
+  const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
+  const double qzz = mp[3 * i + 2].x;
+  const double s1 = g.k1 / g.l1, s2 = g.k2 / g.l2, s3 = g.k3 / g.l3;
+  // operator coefficients in fractional derivatives
+  const double d1 = m0.x * s1, d2 = m0.y * s2, d3 = m0.z * s3;
+  const double q11 = m0.w * s1 * s1, q22 = m1.z * s2 * s2, q33 = qzz * s3 * s3;
+  const double q12 = 2.0 * m1.x * s1 * s2, q13 = 2.0 * m1.y * s1 * s3, q23 = 2.0 * m1.w * s2 * s3;
+  int i1, i2, i3;
+  double w1, w2, w3;
+  frac(r.x, g.l1, g.k1, i1, w1);
+  frac(r.y, g.l2, g.k2, i2, w2);
+  frac(r.z, g.l3, g.k3, i3, w3);
+  double a[4][kMaxOrder], b[4][kMaxOrder], t[4][kMaxOrder];
+  bspline_d3(w1, g.p, a);
+  bspline_d3(w2, g.p, b);
+  bspline_d3(w3, g.p, t);
+  for (int ia = 0; ia < g.p; ++ia) {
+    const int x = (i1 - ia + g.k1) % g.k1;
+    for (int ib = 0; ib < g.p; ++ib) {
+      const int y = (i2 - ib + g.k2) % g.k2;
+      // terms by the z-derivative order they multiply
+      const double c0 = q * a[0][ia] * b[0][ib] + d1 * a[1][ia] * b[0][ib] +
+                        d2 * a[0][ia] * b[1][ib] + q11 * a[2][ia] * b[0][ib] +
+                        q22 * a[0][ia] * b[2][ib] + q12 * a[1][ia] * b[1][ib];
+      const double c1 = d3 * a[0][ia] * b[0][ib] + q13 * a[1][ia] * b[0][ib] +
+                        q23 * a[0][ia] * b[1][ib];
+      const double c2 = q33 * a[0][ia] * b[0][ib];
+      double* row = grid + ((size_t)x * g.k2 + y) * g.k3;
+      for (int ic = 0; ic < g.p; ++ic)
+        atomicAdd(row + (i3 - ic + g.k3) % g.k3, c0 * t[0][ic] + c1 * t[1][ic] + c2 * t[2][ic]);
+    }
+  }
+}
+
+// phi derivatives at each site -> forces, torques (accumulated); partials:
+// 0 energy 1/2 sum M_i phi_i (check of the convolution energy)
+__global__ void __launch_bounds__(kBlock) k_pme_gather_mp(int64_t n, PmeGeom g,
+                                                         const double4* __restrict__ pos,
+                                                         const double4* __restrict__ pq4,
+                                                         const double4* __restrict__ mp,
+                                                         const double* __restrict__ phi,
+                                                         double electric,
+                                                         double4* __restrict__ force,
+                                                         double4* __restrict__ torque,
+                                                         double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < n) {
+    const double4 r = pos[i];
+    int i1, i2, i3;
+    double w1, w2, w3;
+    frac(r.x, g.l1, g.k1, i1, w1);
+    frac(r.y, g.l2, g.k2, i2, w2);
+    frac(r.z, g.l3, g.k3, i3, w3);
+    double a[4][kMaxOrder], b[4][kMaxOrder], t[4][kMaxOrder];
+    bspline_d3(w1, g.p, a);
+    bspline_d3(w2, g.p, b);
+    bspline_d3(w3, g.p, t);
+    // fractional derivatives: f[dx][dy][dz] for dx + dy + dz <= 3
+    double f0 = 0, fx = 0, fy = 0, fz = 0, fxx = 0, fyy = 0, fzz = 0, fxy = 0, fxz = 0, fyz = 0;
+    double fxxx = 0, fyyy = 0, fzzz = 0, fxxy = 0, fxxz = 0, fxyy = 0, fyyz = 0, fxzz = 0,
+           fyzz = 0, fxyz = 0;
+    for (int ia = 0; ia < g.p; ++ia) {
+      const int x = (i1 - ia + g.k1) % g.k1;
+      for (int ib = 0; ib < g.p; ++ib) {
+        const int y = (i2 - ib + g.k2) % g.k2;
+        const double* row = phi + ((size_t)x * g.k2 + y) * g.k3;
+        double z0 = 0, z1 = 0, z2 = 0, z3 = 0;  // sums over z with t0..t3
+        for (int ic = 0; ic < g.p; ++ic) {
+          const double ph = __ldg(row + (i3 - ic + g.k3) % g.k3);
+          z0 += t[0][ic] * ph;
+          z1 += t[1][ic] * ph;
+          z2 += t[2][ic] * ph;
+          z3 += t[3][ic] * ph;
+        }
+        const double a0 = a[0][ia], a1 = a[1][ia], a2 = a[2][ia], a3 = a[3][ia];
+        const double b0 = b[0][ib], b1 = b[1][ib], b2 = b[2][ib], b3 = b[3][ib];
+        f0 += a0 * b0 * z0;
+        fx += a1 * b0 * z0;
+        fy += a0 * b1 * z0;
+        fz += a0 * b0 * z1;
+        fxx += a2 * b0 * z0;
+        fyy += a0 * b2 * z0;
+        fzz += a0 * b0 * z2;
+        fxy += a1 * b1 * z0;
+        fxz += a1 * b0 * z1;
+        fyz += a0 * b1 * z1;
+        fxxx += a3 * b0 * z0;
+        fyyy += a0 * b3 * z0;
+        fzzz += a0 * b0 * z3;
+        fxxy += a2 * b1 * z0;
+        fxxz += a2 * b0 * z1;
+        fxyy += a1 * b2 * z0;
+        fyyz += a0 * b2 * z1;
+        fxzz += a1 * b0 * z2;
+        fyzz += a0 * b1 * z2;
+        fxyz += a1 * b1 * z1;
+      }
+    }
+    const double s1 = g.k1 / g.l1, s2 = g.k2 / g.l2, s3 = g.k3 / g.l3;
+    // Cartesian gradient G1, Hessian G2, third derivatives G3
+    const double g1x = s1 * fx, g1y = s2 * fy, g1z = s3 * fz;
+    const double hxx = s1 * s1 * fxx, hyy = s2 * s2 * fyy, hzz = s3 * s3 * fzz;
+    const double hxy = s1 * s2 * fxy, hxz = s1 * s3 * fxz, hyz = s2 * s3 * fyz;
+    const double txxx = s1 * s1 * s1 * fxxx, tyyy = s2 * s2 * s2 * fyyy, tzzz = s3 * s3 * s3 * fzzz;
+    const double txxy = s1 * s1 * s2 * fxxy, txxz = s1 * s1 * s3 * fxxz;
+    const double txyy = s1 * s2 * s2 * fxyy, tyyz = s2 * s2 * s3 * fyyz;
+    const double txzz = s1 * s3 * s3 * fxzz, tyzz = s2 * s3 * s3 * fyzz;
+    const double txyz = s1 * s2 * s3 * fxyz;
+    const double q = pq4[i].z;
+    const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
+    const double dx = m0.x, dy = m0.y, dz = m0.z;
+    const double Qxx = m0.w, Qxy = m1.x, Qxz = m1.y, Qyy = m1.z, Qyz = m1.w,
+                 Qzz = mp[3 * i + 2].x;
+    acc[0] = 0.5 * electric *
+             (q * f0 + dx * g1x + dy * g1y + dz * g1z + Qxx * hxx + Qyy * hyy + Qzz * hzz +
+              2.0 * (Qxy * hxy + Qxz * hxz + Qyz * hyz));
+    // F_a = -(q g1_a + sum_b H_ab d_b + sum_bc Q_bc T_abc)
+    const double Fx = q * g1x + hxx * dx + hxy * dy + hxz * dz + Qxx * txxx + Qyy * txyy +
+                      Qzz * txzz + 2.0 * (Qxy * txxy + Qxz * txxz + Qyz * txyz);
+    const double Fy = q * g1y + hxy * dx + hyy * dy + hyz * dz + Qxx * txxy + Qyy * tyyy +
+                      Qzz * tyzz + 2.0 * (Qxy * txyy + Qxz * txyz + Qyz * tyyz);
+    const double Fz = q * g1z + hxz * dx + hyz * dy + hzz * dz + Qxx * txxz + Qyy * tyyz +
+                      Qzz * tzzz + 2.0 * (Qxy * txyz + Qxz * txzz + Qyz * tyzz);
+    double4 f = force[i];
+    f.x -= electric * Fx;
+    f.y -= electric * Fy;
+    f.z -= electric * Fz;
+    force[i] = f;
+    // tau = grad phi x mu + 2 (M_zy, M_xz, M_yx), M = Q H - H Q
+    double tx = g1y * dz - g1z * dy, ty = g1z * dx - g1x * dz, tz = g1x * dy - g1y * dx;
+    const double Mzy = (Qxz * hxy + Qyz * hyy + Qzz * hyz) - (hxz * Qxy + hyz * Qyy + hzz * Qyz);
+    const double Mxz = (Qxx * hxz + Qxy * hyz + Qxz * hzz) - (hxx * Qxz + hxy * Qyz + hxz * Qzz);
+    const double Myx = (Qxy * hxx + Qyy * hxy + Qyz * hxz) - (hxy * Qxx + hyy * Qxy + hyz * Qxz);
+    tx += 2.0 * Mzy;
+    ty += 2.0 * Mxz;
+    tz += 2.0 * Myx;
+    double4 tq = torque[i];
+    tq.x += electric * tx;
+    tq.y += electric * ty;
+    tq.z += electric * tz;
+    torque[i] = tq;
+  }
+  block_store_partials<1>(acc, partials);
+}
+
+// partials: 0 sum q^2, 1 sum |mu|^2, 2 sum Q:Q
+__global__ void __launch_bounds__(kBlock) k_pme_self_mp(int64_t n, const double4* __restrict__ pq4,
+                                                       const double4* __restrict__ mp,
+                                                       double* __restrict__ partials) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double acc[3] = {0, 0, 0};
+  if (i < n) {
+    const double q = pq4[i].z;
+    const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
+    const double zz = mp[3 * i + 2].x;
+    acc[0] = q * q;
+    acc[1] = m0.x * m0.x + m0.y * m0.y + m0.z * m0.z;
+    acc[2] = m0.w * m0.w + m1.z * m1.z + zz * zz +
+             2.0 * (m1.x * m1.x + m1.y * m1.y + m1.w * m1.w);
+  }
+  block_store_partials<3>(acc, partials);
+}
+
+// Excluded (same-molecule) pairs: remove their erf(a r)/r-kernel multipole
+// interaction (B_n = bare - erfc). One thread per site over its partners:
+// i-side force and torque in full, energy halved (each pair seen twice).
+__global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, double alpha,
+                                                           double electric,
+                                                           const double4* __restrict__ pos,
+                                                           const double4* __restrict__ pq4,
+                                                           const double4* __restrict__ mp,
+                                                           const int32_t* __restrict__ xs,
+                                                           const int32_t* __restrict__ xl,
+                                                           double4* __restrict__ force,
+                                                           double4* __restrict__ torque,
+                                                           double* __restrict__ partials) {
+  double acc[1] = {0.0};
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double4 pi = pos[i];
+    const double qi = pq4[i].z;
+    const double4 m0i = mp[3 * i], m1i = mp[3 * i + 1];
+    const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
+    const double Qi[6] = {m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, mp[3 * i + 2].x};
+    double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+    for (int32_t k = xs[i]; k < xs[i + 1]; ++k) {
+      const int32_t j = xl[k];
+      const double4 pj = pos[j];
+      double x, y, z;
+      const double r2 = min_image(bx, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
+      const double r = sqrt(r2);
+      const double inv_r = 1.0 / r, inv_r2 = inv_r * inv_r;
+      double G[6];
+      ewald_bn<5>(r, inv_r, inv_r2, alpha, G);
+      double bare = inv_r;
+      for (int q = 0; q < 6; ++q) {
+        if (q > 0) bare *= (double)(2 * q - 1) * inv_r2;
+        G[q] = electric * (bare - G[q]);  // erf kernel
+      }
+      const double qj = pq4[j].z;
+      const double4 m0j = mp[3 * (size_t)j], m1j = mp[3 * (size_t)j + 1];
+      const double djx = m0j.x, djy = m0j.y, djz = m0j.z;
+      const double Qj[6] = {m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, mp[3 * (size_t)j + 2].x};
+      auto qv = [](const double* Q, double a, double b, double c, double& ox, double& oy,
+                   double& oz) {
+        ox = Q[0] * a + Q[1] * b + Q[2] * c;
+        oy = Q[1] * a + Q[3] * b + Q[4] * c;
+        oz = Q[2] * a + Q[4] * b + Q[5] * c;
+      };
+      double vix, viy, viz, vjx, vjy, vjz;
+      qv(Qi, x, y, z, vix, viy, viz);
+      qv(Qj, x, y, z, vjx, vjy, vjz);
+      const double dir = dix * x + diy * y + diz * z, djr = djx * x + djy * y + djz * z;
+      const double qir = x * vix + y * viy + z * viz, qjr = x * vjx + y * vjy + z * vjz;
+      const double dij = dix * djx + diy * djy + diz * djz;
+      const double diqj = dix * vjx + diy * vjy + diz * vjz;
+      const double djqi = djx * vix + djy * viy + djz * viz;
+      const double qiqj = Qi[0] * Qj[0] + Qi[3] * Qj[3] + Qi[5] * Qj[5] +
+                          2.0 * (Qi[1] * Qj[1] + Qi[2] * Qj[2] + Qi[4] * Qj[4]);
+      const double qvv = vix * vjx + viy * vjy + viz * vjz;
+      const double C0 = qi * qj, C1 = qi * djr - qj * dir + dij;
+      const double C2 = qi * qjr + qj * qir - dir * djr + 2.0 * (diqj - djqi + qiqj);
+      const double C3 = -dir * qjr + qir * djr - 4.0 * qvv, C4 = qir * qjr;
+      acc[0] -= 0.5 * (C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4]);
+      double a1x, a1y, a1z, a2x, a2y, a2z, b1x, b1y, b1z, b2x, b2y, b2z;
+      qv(Qj, dix, diy, diz, a1x, a1y, a1z);
+      qv(Qi, djx, djy, djz, a2x, a2y, a2z);
+      qv(Qi, vjx, vjy, vjz, b1x, b1y, b1z);
+      qv(Qj, vix, viy, viz, b2x, b2y, b2z);
+      const double s = C0 * G[1] + C1 * G[2] + C2 * G[3] + C3 * G[4] + C4 * G[5];
+      const double gx = G[1] * (qi * djx - qj * dix) +
+                        G[2] * (2.0 * (qi * vjx + qj * vix) - djr * dix - dir * djx + 2.0 * (a1x - a2x)) +
+                        G[3] * (-qjr * dix - 2.0 * dir * vjx + 2.0 * djr * vix + qir * djx - 4.0 * (b1x + b2x)) +
+                        G[4] * 2.0 * (qjr * vix + qir * vjx) - s * x;
+      const double gy = G[1] * (qi * djy - qj * diy) +
+                        G[2] * (2.0 * (qi * vjy + qj * viy) - djr * diy - dir * djy + 2.0 * (a1y - a2y)) +
+                        G[3] * (-qjr * diy - 2.0 * dir * vjy + 2.0 * djr * viy + qir * djy - 4.0 * (b1y + b2y)) +
+                        G[4] * 2.0 * (qjr * viy + qir * vjy) - s * y;
+      const double gz = G[1] * (qi * djz - qj * diz) +
+                        G[2] * (2.0 * (qi * vjz + qj * viz) - djr * diz - dir * djz + 2.0 * (a1z - a2z)) +
+                        G[3] * (-qjr * diz - 2.0 * dir * vjz + 2.0 * djr * viz + qir * djz - 4.0 * (b1z + b2z)) +
+                        G[4] * 2.0 * (qjr * viz + qir * vjz) - s * z;
+      // removing the pair: F_i += dU/dR (the pair force on i is -dU/dR)
+      fx += gx;
+      fy += gy;
+      fz += gz;
+      const double c1 = G[1] * qj + G[2] * djr + G[3] * qjr;
+      const double gmx = G[1] * djx + 2.0 * G[2] * vjx - c1 * x;
+      const double gmy = G[1] * djy + 2.0 * G[2] * vjy - c1 * y;
+      const double gmz = G[1] * djz + 2.0 * G[2] * vjz - c1 * z;
+      double ux = gmy * diz - gmz * diy, uy = gmz * dix - gmx * diz, uz = gmx * diy - gmy * dix;
+      const double crr = G[2] * qj + G[3] * djr + G[4] * qjr, g2 = 2.0 * G[2], g3 = 2.0 * G[3];
+      const double Hxx = crr * x * x - G[2] * (2.0 * djx * x) + g2 * Qj[0] - g3 * (2.0 * x * vjx);
+      const double Hyy = crr * y * y - G[2] * (2.0 * djy * y) + g2 * Qj[3] - g3 * (2.0 * y * vjy);
+      const double Hzz = crr * z * z - G[2] * (2.0 * djz * z) + g2 * Qj[5] - g3 * (2.0 * z * vjz);
+      const double Hxy = crr * x * y - G[2] * (djx * y + x * djy) + g2 * Qj[1] - g3 * (x * vjy + vjx * y);
+      const double Hxz = crr * x * z - G[2] * (djx * z + x * djz) + g2 * Qj[2] - g3 * (x * vjz + vjx * z);
+      const double Hyz = crr * y * z - G[2] * (djy * z + y * djz) + g2 * Qj[4] - g3 * (y * vjz + vjy * z);
+      const double Mzy = (Qi[2] * Hxy + Qi[4] * Hyy + Qi[5] * Hyz) - (Hxz * Qi[1] + Hyz * Qi[3] + Hzz * Qi[4]);
+      const double Mxz = (Qi[0] * Hxz + Qi[1] * Hyz + Qi[2] * Hzz) - (Hxx * Qi[2] + Hxy * Qi[4] + Hxz * Qi[5]);
+      const double Myx = (Qi[1] * Hxx + Qi[3] * Hxy + Qi[4] * Hxz) - (Hxy * Qi[0] + Hyy * Qi[1] + Hyz * Qi[2]);
+      ux += 2.0 * Mzy;
+      uy += 2.0 * Mxz;
+      uz += 2.0 * Myx;
+      tx -= ux;
+      ty -= uy;
+      tz -= uz;
+    }
+    double4 f = force[i];
+    f.x += fx;
+    f.y += fy;
+    f.z += fz;
+    force[i] = f;
+    double4 t = torque[i];
+    t.x += tx;
+    t.y += ty;
+    t.z += tz;
+    torque[i] = t;
+  }
+  block_store_partials<1>(acc, partials);
+}
+
+// results: 80 recip energy (convolution), 87 self, 88 excluded, 98 recip
+// energy from the gathered potentials (check); force / torque ADDED to
+void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
+                   double electric, bool exclude) {
+  pme_setup(c, k1, k2, k3, order);
+  PmeState* s = (PmeState*)c->pme;
+  const PmeGeom g{k1, k2, k3, order, c->lx, c->ly, c->lz};
+  const int64_t n = c->n;
+  MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)k1 * k2 * k3 * sizeof(double), c->stream));
+  MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos, c->pq4,
+             c->mp, s->grid);
+  cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
+  const int64_t total = (int64_t)k1 * k2 * (k3 / 2 + 1);
+  const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
+  ensure_partials(c, std::max<int64_t>(blocks, grid_for(n)));
+  MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, alpha, s->bmod,
+             s->spec, c->partials);
+  finalize_partials(c, blocks, 1, 80, electric);
+  cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
+  MDG_LAUNCH(c, "pme_gather_mp", grid_for(n), kBlock, 0, k_pme_gather_mp, n, g, c->pos, c->pq4,
+             c->mp, s->grid, electric, c->force, c->torque, c->partials);
+  finalize_partials(c, grid_for(n), 1, 98, 1.0);
+  MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
+             c->partials);
+  finalize_partials(c, grid_for(n), 3, 99, 1.0);  // 99 q^2, 100 mu^2, 101 Q:Q (host combines)
+  if (exclude && c->has_mol && c->excl_start) {
+    MDG_LAUNCH(c, "pme_excluded_mp", grid_for(n), kBlock, 0, k_pme_excluded_mp, n,
+               make_box(c->lx, c->ly, c->lz), alpha, electric, c->pos, c->pq4, c->mp,
+               c->excl_start, c->excl, c->force, c->torque, c->partials);
+    finalize_partials(c, grid_for(n), 1, 88, 1.0);
+  }
+}
 }  // namespace mdg
