@@ -190,6 +190,20 @@ int mdg_ewald_recip(mdg_ctx* ctx, double alpha, int k1, int k2, int k3, int orde
                     double electric, int exclude, double* fx, double* fy, double* fz,
                     double* energies3, double* virial9);
 
+/* Smooth PME for the permanent multipoles (charge, dipole, quadrupole;
+ * 8(f)#3): site operator q + mu.grad + Q:grad grad spread with B-splines of
+ * order 5..10 and their derivatives, cuFFT, potential derivatives to third
+ * order gathered per site. forces and torques (overwritten, global frame;
+ * with local frames the torques are NOT turned into frame forces here),
+ * energies3 = (reciprocal, self -a/sqrt(pi) sum [q^2 + 2a^2|mu|^2/3 +
+ * 8a^4 Q:Q/5], excluded-pair correction: minus the erf(a r)/r-kernel
+ * interaction of same-molecule pairs when exclude != 0). With
+ * mdg_mpole_forces at the same alpha the four terms are the full multipole
+ * Ewald sum. Single domain. */
+int mdg_ewald_recip_mpole(mdg_ctx* ctx, double alpha, int k1, int k2, int k3, int order,
+                          double electric, int exclude, double* fx, double* fy, double* fz,
+                          double* tx, double* ty, double* tz, double* energies3);
+
 /* ---- fused steps (device-resident; the bench's hot path) ----------------- */
 typedef struct {
   double cutoff;    /* LJ and Ewald cutoff (A) */

@@ -1040,6 +1040,37 @@ int mdg_polar_forces(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   });
 }
 
+int mdg_ewald_recip_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
+                          double electric, int exclude, double* fx, double* fy, double* fz,
+                          double* tx, double* ty, double* tz, double* energies3) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(alpha > 0, "ewald_recip_mpole: alpha must be positive");
+    need(order >= 5 && order <= 10,
+         "ewald_recip_mpole: B-spline order must be 5..10 (third derivatives)");
+    need(k1 >= order && k2 >= order && k3 >= order,
+         "ewald_recip_mpole: grid smaller than the order");
+    need(c->n_own == c->n, "ewald_recip_mpole: single domain only (no distributed FFT)");
+    mdg::rotate_multipoles(c);
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->force, 0, (size_t)c->n * sizeof(double4), c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->torque, 0, (size_t)c->n * sizeof(double4), c->stream));
+    MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 80, 0, 27 * sizeof(double), c->stream));
+    mdg::run_pme_mpole(c, alpha, k1, k2, k3, order, electric, exclude != 0);
+    vec_out(c, c->force, fx, fy, fz);
+    vec_out(c, c->torque, tx, ty, tz);
+    mdg::fetch_results(c);
+    const double* r = c->h_results;
+    if (energies3) {
+      const double a2 = alpha * alpha;
+      energies3[0] = r[80];
+      energies3[1] = -electric * alpha / std::sqrt(M_PI) *
+                     (r[104] + 2.0 / 3.0 * a2 * r[105] + 8.0 / 5.0 * a2 * a2 * r[106]);
+      energies3[2] = r[88];
+    }
+  });
+}
+
 int mdg_ewald_recip(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
                     double electric, int exclude, double* fx, double* fy, double* fz,
                     double* energies3, double* virial9) {

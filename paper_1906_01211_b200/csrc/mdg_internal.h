@@ -467,6 +467,11 @@ void frame_torques_to_forces(mdg_ctx* c);
 void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
              bool exclude);
 void pme_free(mdg_ctx* c);
+// smooth PME for permanent multipoles (q, mu, Theta): adds forces and torques;
+// results 80 (recip), 88 (excluded pairs), 98 (recip from the gathered
+// potentials), 104-106 (sums of q^2, |mu|^2, Q:Q for the self energy)
+void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
+                   double electric, bool exclude);
 // MD (md.cu): bonded forces added to c->force (results 100 bonds, 101
 // angles), velocity-Verlet half kick / drift, kinetic energy (result 102)
 void run_bonded(mdg_ctx* c);

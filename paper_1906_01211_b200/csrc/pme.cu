@@ -701,8 +701,9 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
   block_store_partials<1>(acc, partials);
 }
 
-// results: 80 recip energy (convolution), 87 self, 88 excluded, 98 recip
-// energy from the gathered potentials (check); force / torque ADDED to
+// results: 80 recip energy (convolution), 88 excluded, 98 recip energy from
+// the gathered potentials (check), 104-106 sums of q^2, |mu|^2, Q:Q for the
+// self energy (formed on the host); force / torque ADDED to
 void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
                    double electric, bool exclude) {
   pme_setup(c, k1, k2, k3, order);
@@ -725,7 +726,7 @@ void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
   finalize_partials(c, grid_for(n), 1, 98, 1.0);
   MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
              c->partials);
-  finalize_partials(c, grid_for(n), 3, 99, 1.0);  // 99 q^2, 100 mu^2, 101 Q:Q (host combines)
+  finalize_partials(c, grid_for(n), 3, 104, 1.0);  // 104 q^2, 105 mu^2, 106 Q:Q (host combines)
   if (exclude && c->has_mol && c->excl_start) {
     MDG_LAUNCH(c, "pme_excluded_mp", grid_for(n), kBlock, 0, k_pme_excluded_mp, n,
                make_box(c->lx, c->ly, c->lz), alpha, electric, c->pos, c->pq4, c->mp,

@@ -122,6 +122,9 @@ SIGNATURES = {
                                    _dp, _dp, _dp, _dp]),
     "mdg_ewald_recip": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp]),
+    "mdg_ewald_recip_mpole": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp,
+                                        _dp, _dp]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_bonded_upload": (C.c_int, [C.c_void_p, C.c_int64, _ip, _dp, _dp, C.c_int64, _ip, _dp,
                                     _dp]),
@@ -582,6 +585,18 @@ class Engine:
         return _aos(fx, fy, fz), e, w.reshape(3, 3)
 
     # ---- MD (8(f)#4) ---------------------------------------------------------------
+    def ewald_recip_mpole(self, alpha: float, grid=(48, 48, 48), order: int = 6,
+                          electric: float = 1.0, exclude: bool = True):
+        """Smooth PME of the permanent multipoles: (forces, torques,
+        (E_recip, E_self, E_excluded)) -- mdg_ewald_recip_mpole."""
+        fx, fy, fz = self._vec3()
+        tx, ty, tz = self._vec3()
+        e = np.zeros(3)
+        check(self.lib.mdg_ewald_recip_mpole(self.ctx, float(alpha), *map(int, grid), int(order),
+                                             float(electric), int(exclude), _p(fx), _p(fy),
+                                             _p(fz), _p(tx), _p(ty), _p(tz), _p(e)))
+        return np.stack([fx, fy, fz], 1), np.stack([tx, ty, tz], 1), e
+
     def upload_bonded(self, bonds=None, kb=None, r0=None, angles=None, ka=None, theta0=None):
         """Harmonic bonds (m, 2) / angles (m, 3; vertex in the middle),
         E = k (x - x0)^2 (mdg.h mdg_bonded_upload)."""

@@ -897,6 +897,49 @@ def test_pme_matches_direct_ewald_sum(engine, oracle, mdg):
     np.testing.assert_allclose(w, w_o + wx_o, rtol=0, atol=1e-5 * np.abs(w_o).max())
 
 
+def test_mpole_pme_matches_direct_ewald_sum(engine, mdg):
+    """Smooth PME of the permanent multipoles (q, mu, Theta; 8(f)#3) vs the
+    direct structure-factor sum (oracle/ewald_mpole.py): energy, forces and
+    torques at PME accuracy; self and excluded-pair terms exact."""
+    from oracle import ewald_mpole as em
+    s = mdg.water_box(64, 12.4, 3, "amoeba")
+    pos = np.stack([s.x, s.y, s.z], 1)
+    q, mu, q6 = np.asarray(s.charge), np.asarray(s.dipole), np.asarray(s.quadrupole)
+    a = 0.5446
+    e_o, f_o, t_o = em.recip(pos, q, mu, q6, s.box, a, kmax=(12, 12, 12), electric=mdg.ELECTRIC)
+    ex_o, fx_o, tx_o = em.excluded_correction(pos, q, mu, q6, s.box, s.molecule, a,
+                                              mdg.ELECTRIC, pair=em.mpole_pair)
+    engine.upload_system(s)
+    # PME converges spectrally in grid and order (measured at this alpha:
+    # 48^3 / order 8: 1e-8 energy, 9e-7 forces; 64^3 / order 10: 9e-12, 1.3e-9)
+    f, t, e = engine.ewald_recip_mpole(a, (64, 64, 64), 10, mdg.ELECTRIC, True)
+    assert e[0] == pytest.approx(e_o, rel=1e-9)
+    assert e[1] == pytest.approx(em.self_energy(q, mu, q6, a, mdg.ELECTRIC), rel=1e-12)
+    assert e[2] == pytest.approx(ex_o, rel=1e-10)
+    assert force_err_max(f, f_o + fx_o) <= 1e-7
+    assert force_err_max(t, t_o + tx_o) <= 1e-7
+    f8, t8, e8 = engine.ewald_recip_mpole(a, (48, 48, 48), 8, mdg.ELECTRIC, True)
+    assert force_err_max(f8, f_o + fx_o) <= 1e-5  # the coarser grid at PME accuracy
+
+
+def test_full_mpole_ewald_is_alpha_independent(engine, mdg):
+    """Real-space multipoles (device kernel) + multipole PME + self + excluded
+    pairs: the same total energy, forces and torques for two splitting
+    parameters (the real-space sum converged within the 6 A cutoff)."""
+    s = mdg.water_box(64, 12.4, 4, "amoeba")
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(6.0)
+    out = []
+    for a in (0.8, 0.9):
+        fr, tr, er, _ = engine.mpole_forces(t, a, 6.0, mdg.ELECTRIC, exclude=True)
+        fk, tk, ek = engine.ewald_recip_mpole(a, (96, 96, 96), 10, mdg.ELECTRIC, True)
+        out.append((er + ek.sum(), fr + fk, tr + tk))
+    (e1, f1, t1), (e2, f2, t2) = out
+    assert e1 == pytest.approx(e2, rel=1e-8)
+    assert force_err_max(f1, f2) <= 1e-7
+    assert force_err_max(t1, t2) <= 1e-7
+
+
 def test_full_ewald_is_alpha_independent(engine, oracle, mdg):
     """Real space (device kernel) + PME + self + excluded pairs: the same
     total energy and forces for two splitting parameters."""
