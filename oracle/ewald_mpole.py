@@ -49,8 +49,9 @@ def quad3(q6):
     return Q
 
 
-def recip(pos, q, mu, quad6, box, alpha, kmax=(10, 10, 10), electric=1.0):
-    """(energy, forces (n,3), torques (n,3)) of the reciprocal sum."""
+def recip(pos, q, mu, quad6, box, alpha, kmax=(10, 10, 10), electric=1.0, energy_only=False):
+    """(energy, forces (n,3), torques (n,3)) of the reciprocal sum (forces
+    and torques None with energy_only)."""
     pos = np.asarray(pos, float)
     q = np.asarray(q, float)
     mu = np.zeros((len(q), 3)) if mu is None else np.asarray(mu, float)
@@ -65,6 +66,8 @@ def recip(pos, q, mu, quad6, box, alpha, kmax=(10, 10, 10), electric=1.0):
     E = np.exp(1j * tpi * (pos @ m.T))                                  # (n, M)
     S = np.sum(F * E, 0)                                                # (M,)
     e = 0.5 * electric * float(np.sum(g * np.abs(S) ** 2))
+    if energy_only:
+        return e, None, None
     # derivatives of phi at the sites: Re[E_i conj(S) (2 pi i m)^k] g
     base = (E * np.conj(S)[None, :]) * g[None, :]                       # (n, M)
     d1 = np.real((1j * tpi) * base) @ m                                 # grad phi (n, 3)

@@ -665,3 +665,72 @@ def test_rows_for_sites_match_brute_force(oracle):
         for i, r in zip(sites, oracle.rows_for_sites(s, cut, sites)):
             want = np.sort(np.concatenate([bf[bf[:, 0] == i, 1], bf[bf[:, 1] == i, 0]]))
             np.testing.assert_array_equal(r, want)
+
+
+# ------------------------------------------------ multipole Ewald oracle (8(f)#3)
+def _mp_water(oracle):
+    s, _, _ = oracle.water_box(27, 10.2, 3, "amoeba")
+    return s
+
+
+def test_mpole_ewald_oracle_forces_torques_by_fd(oracle):
+    """oracle/ewald_mpole.py: reciprocal + self + excluded forces == -dE/dr and
+    torques == -dE/dtheta (finite differences / rotations of one site)."""
+    from oracle import ewald_mpole as em
+    s = _mp_water(oracle)
+    pos = np.stack([s.x, s.y, s.z], 1)
+
+    def energy(p, mu=s.dipole, q6=s.quadrupole):
+        e = em.recip(p, s.charge, mu, q6, s.box, 0.6, kmax=(8, 8, 8), energy_only=True)[0]
+        return e + em.excluded_correction(p, s.charge, mu, q6, s.box, s.molecule, 0.6,
+                                          pair=em.mpole_pair)[0]
+
+    _, f, t = em.recip(pos, s.charge, s.dipole, s.quadrupole, s.box, 0.6, kmax=(8, 8, 8))
+    _, fx, tx = em.excluded_correction(pos, s.charge, s.dipole, s.quadrupole, s.box,
+                                       s.molecule, 0.6, pair=em.mpole_pair)
+    f, t = f + fx, t + tx
+    h = 1e-5
+    for i, k in ((0, 0), (4, 1), (13, 2)):
+        p = pos.copy()
+        p[i, k] += h
+        ep = energy(p)
+        p[i, k] -= 2 * h
+        assert f[i, k] == pytest.approx(-(ep - energy(p)) / (2 * h), rel=1e-6, abs=1e-9)
+
+    def rot(ax, th):
+        ax = np.asarray(ax, float) / np.linalg.norm(ax)
+        K = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+        return np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+
+    for i, ax in ((2, (0, 0, 1)), (7, (1, 1, 0))):
+        vals = []
+        for th in (h, -h):
+            R = rot(ax, th)
+            m2 = s.dipole.copy()
+            m2[i] = R @ s.dipole[i]
+            Q = R @ em.quad3(s.quadrupole)[i] @ R.T
+            q6 = s.quadrupole.copy()
+            q6[i] = [Q[0, 0], Q[0, 1], Q[0, 2], Q[1, 1], Q[1, 2], Q[2, 2]]
+            vals.append(energy(pos, m2, q6))
+        ax = np.asarray(ax, float) / np.linalg.norm(ax)
+        assert t[i] @ ax == pytest.approx(-(vals[0] - vals[1]) / (2 * h), rel=1e-5, abs=1e-9)
+
+
+def test_mpole_ewald_total_is_alpha_independent(oracle):
+    """Real space (mdo.c tensor multipoles, exclusions) + reciprocal + self +
+    excluded pairs: one energy for two splitting parameters (both sums
+    converged: erfc(a rc) < 1e-9, k-space tail < 1e-12)."""
+    from oracle import ewald_mpole as em
+    s = _mp_water(oracle)
+    pos = np.stack([s.x, s.y, s.z], 1)
+    t = oracle.build_table(s, 4.9)
+    tot = []
+    for a in (0.95, 1.05):
+        er = oracle.mpole(s, t, a, 4.9, 1.0, exclude=True)[2]
+        ek = em.recip(pos, s.charge, s.dipole, s.quadrupole, s.box, a, kmax=(17, 17, 17),
+                      energy_only=True)[0]
+        es = em.self_energy(s.charge, s.dipole, s.quadrupole, a)
+        ex = em.excluded_correction(pos, s.charge, s.dipole, s.quadrupole, s.box, s.molecule,
+                                    a, pair=em.mpole_pair)[0]
+        tot.append(er + ek + es + ex)
+    assert tot[0] == pytest.approx(tot[1], rel=2e-7)
