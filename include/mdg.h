@@ -204,6 +204,19 @@ int mdg_ewald_recip_mpole(mdg_ctx* ctx, double alpha, int k1, int k2, int k3, in
                           double electric, int exclude, double* fx, double* fy, double* fz,
                           double* tx, double* ty, double* tz, double* energies3);
 
+/* Reciprocal-space Ewald in the AMOEBA-style step and mdg_polar_solve_pcg
+ * (8(f)#3), single domain: with a k1 x k2 x k3 grid and B-spline order 5..10
+ * set, the permanent field (PCG right-hand side) gains the multipoles'
+ * reciprocal field, the Ewald self field 4a^3/(3 sqrt(pi)) mu and (with the
+ * call's exclusions) minus the erf-kernel field of same-molecule partners;
+ * the PCG operator gains the reciprocal + self field of the dipoles (one
+ * smooth-PME pass per iteration); the step's multipole term gains
+ * mdg_ewald_recip_mpole's energy, forces and torques. The polarization
+ * energy -1/2 mu.E_perm is then the full Ewald one. Reciprocal-space
+ * polarization FORCES are not built (MDG_TERM_POLAR_FORCE is refused).
+ * k1 = 0 switches it off (default). */
+int mdg_set_ewald_recip(mdg_ctx* ctx, int k1, int k2, int k3, int order);
+
 /* ---- fused steps (device-resident; the bench's hot path) ----------------- */
 typedef struct {
   double cutoff;    /* LJ and Ewald cutoff (A) */

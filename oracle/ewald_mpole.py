@@ -185,3 +185,76 @@ def mpole_pair(R, G, qi, di, Qi, qj, dj, Qj):
     tj = torque(dj, Qj, gm, make_gq(G[2] * qi - G[3] * dir_ + G[4] * qir, G[2], di,
                                      2.0 * G[2], Qi, -2.0 * G[3], vi))
     return u, fi, ti, tj
+
+
+# ---------------------------------------------------------- polarization fields
+def self_field_coef(alpha):
+    """Ewald self field of a dipole at its own site: E = 4 a^3 / (3 sqrt(pi)) mu."""
+    return 4.0 * alpha ** 3 / (3.0 * SQRT_PI)
+
+
+def field_recip(pos, q, mu, quad6, box, alpha, kmax=(10, 10, 10)):
+    """Reciprocal-space field -grad phi at every site from the multipoles
+    (q, mu, Q) plus the self field of the site's own dipole."""
+    pos = np.asarray(pos, float)
+    q = np.asarray(q, float)
+    mu_ = np.zeros((len(q), 3)) if mu is None else np.asarray(mu, float)
+    Q = np.zeros((len(q), 3, 3)) if quad6 is None else quad3(quad6)
+    box = np.asarray(box, float)
+    V = float(np.prod(box))
+    m, m2 = _kvecs(box, kmax)
+    g = np.exp(-np.pi ** 2 * m2 / alpha ** 2) / (np.pi * V * m2)
+    tpi = 2.0 * np.pi
+    mQm = np.einsum("ka,iab,kb->ik", m, Q, m)
+    F = q[:, None] + 1j * tpi * (mu_ @ m.T) - tpi ** 2 * mQm
+    E = np.exp(1j * tpi * (pos @ m.T))
+    S = np.sum(F * E, 0)
+    base = (E * np.conj(S)[None, :]) * g[None, :]
+    grad = np.real((1j * tpi) * base) @ m
+    return -grad + self_field_coef(alpha) * mu_
+
+
+def tmat_recip_dense(pos, box, alpha, kmax=(10, 10, 10)):
+    """Dense (3n x 3n) reciprocal + self operator: field at i from unit
+    dipoles at j, -sum_m g (2 pi)^2 m m^T cos(2 pi m.(r_i - r_j)) (j = i
+    included) + 4 a^3 / (3 sqrt(pi)) on the diagonal."""
+    pos = np.asarray(pos, float)
+    n = len(pos)
+    box = np.asarray(box, float)
+    V = float(np.prod(box))
+    m, m2 = _kvecs(box, kmax)
+    g = np.exp(-np.pi ** 2 * m2 / alpha ** 2) / (np.pi * V * m2)
+    ph = 2.0 * np.pi * (pos @ m.T)                       # (n, M)
+    c, s = np.cos(ph), np.sin(ph)
+    w = g * (2.0 * np.pi) ** 2                           # (M,)
+    T = np.zeros((n, 3, n, 3))
+    for a in range(3):
+        for b in range(3):
+            wab = w * m[:, a] * m[:, b]
+            # cos(x_i - x_j) = c_i c_j + s_i s_j
+            T[:, a, :, b] = -((c * wab) @ c.T + (s * wab) @ s.T)
+    T = T.reshape(3 * n, 3 * n)
+    return T + self_field_coef(alpha) * np.eye(3 * n)
+
+
+def excluded_field_erf(pos, q, mu, quad6, box, molecule, alpha):
+    """erf(a r)/r-kernel field at i of its same-molecule partners' multipoles
+    (contained in the reciprocal field, excluded from the real-space one)."""
+    pos = np.asarray(pos, float)
+    box = np.asarray(box, float)
+    n = len(q)
+    mu_ = np.zeros((n, 3)) if mu is None else np.asarray(mu, float)
+    Q = np.zeros((n, 3, 3)) if quad6 is None else quad3(quad6)
+    mol = np.asarray(molecule)
+    e = np.zeros((n, 3))
+    for i in range(n):
+        for j in range(n):
+            if j == i or mol[i] != mol[j]:
+                continue
+            R = pos[i] - pos[j]
+            R -= box * np.rint(R / box)
+            B = _bn_erf(np.sqrt(R @ R), alpha, 3)
+            QR = Q[j] @ R
+            cc = B[1] * q[j] + B[2] * (mu_[j] @ R) + B[3] * (R @ QR)
+            e[i] += cc * R - B[1] * mu_[j] - 2.0 * B[2] * QR
+    return e

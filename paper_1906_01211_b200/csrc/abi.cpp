@@ -445,6 +445,23 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
   });
 }
 
+int mdg_set_ewald_recip(mdg_ctx* c, int k1, int k2, int k3, int order) {
+  return guard([&] {
+    need_ctx(c);
+    if (k1 <= 0) {
+      c->pol_recip = mdg::PolarRecip{};
+      return;
+    }
+    need(order >= 5 && order <= 10, "ewald_recip: B-spline order must be 5..10");
+    need(k2 > 0 && k3 > 0 && k1 >= order && k2 >= order && k3 >= order,
+         "ewald_recip: grid smaller than the order");
+    c->pol_recip.k1 = k1;
+    c->pol_recip.k2 = k2;
+    c->pol_recip.k3 = k3;
+    c->pol_recip.order = order;
+  });
+}
+
 int mdg_set_deterministic(mdg_ctx* c, int on) {
   return guard([&] {
     need_ctx(c);
@@ -980,6 +997,12 @@ int mdg_polar_solve_pcg(mdg_ctx* c, int list_id, double alpha, double cutoff, do
     need(L.sites == MDG_SITES_ATOMIC, "pcg needs a list over atomic sites");
     mdg::rotate_multipoles(c);
     mdg::run_field_tpre(c, list_id, alpha, cutoff, thole_a, exclude_perm);
+    if (c->pol_recip.on()) {
+      need(alpha > 0, "pcg: reciprocal space needs alpha > 0");
+      c->pol_recip.alpha = alpha;
+      c->pol_recip.exclude = exclude_perm != 0;
+      mdg::pme_field(c, 0, nullptr, c->eperm);
+    }
     double rms = 0;
     try {
       const int64_t it = mdg::run_pcg_pre(c, tol_debye, max_iter, &rms);
@@ -1165,7 +1188,15 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   st.terms = p->terms ? p->terms : (MDG_TERM_VDW | MDG_TERM_MPOLE | MDG_TERM_POLAR);
   need(!(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_POLAR),
        "amoeba_step: polarization forces need the polarization solve");
-  MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, 80 * sizeof(double), c->stream));
+  const bool recip = c->pol_recip.on();
+  need(!recip || !(st.terms & MDG_TERM_POLAR_FORCE),
+       "amoeba_step: reciprocal-space polarization forces are not built (mdg_set_ewald_recip)");
+  need(!recip || c->n_own == c->n, "amoeba_step: reciprocal space is single-domain only");
+  MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, (recip ? 107 : 80) * sizeof(double), c->stream));
+  c->pol_recip.alpha = p->alpha;
+  c->pol_recip.electric = p->electric;
+  c->pol_recip.exclude = p->exclude != 0;
+  c->recip_in_step = false;
   c->has_polar_force = false;
   mdg::rotate_multipoles(c);  // local frames at the current positions
   // one list for both terms: the two chains would cut / sort the same
@@ -1189,6 +1220,7 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   st.polar = (st.terms & MDG_TERM_POLAR) != 0;
   if (st.polar) {
     mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
+    if (recip) mdg::pme_field(c, 0, nullptr, c->eperm);  // + reciprocal + self field
     if (st.ov) {
       MDG_CUDA_CHECK(cudaEventRecord(c->ev_tpre, c->stream));
       MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
@@ -1203,6 +1235,11 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
     if (st.terms & MDG_TERM_MPOLE) {
       if (st.polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
       else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
+      if (recip) {  // + the multipoles' reciprocal-space sum (own PME state)
+        const mdg::PolarRecip& R = c->pol_recip;
+        mdg::run_pme_mpole(c, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric, R.exclude);
+        c->recip_in_step = true;
+      }
     } else {
       mdg::zero_vec(c, c->torque);
     }
@@ -1598,6 +1635,11 @@ static void energies_of(mdg_ctx* c, double* e4, double* w9) {
   const bool amoeba = c->pcg_iters != 0;
   e4[0] = r[0];
   e4[1] = amoeba ? r[10] : r[1];
+  if (amoeba && c->recip_in_step) {  // + reciprocal, self and excluded-pair terms
+    const double a = c->pol_recip.alpha, a2 = a * a;
+    e4[1] += r[80] + r[88] - c->pol_recip.electric * a / std::sqrt(M_PI) *
+                                 (r[104] + 2.0 / 3.0 * a2 * r[105] + 8.0 / 5.0 * a2 * a2 * r[106]);
+  }
   e4[2] = amoeba ? r[40] : 0.0;
   e4[3] = 0.0;
   for (int k = 0; k < 9; ++k)

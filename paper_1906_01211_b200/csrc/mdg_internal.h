@@ -138,6 +138,15 @@ struct PcgComm {
   virtual uintptr_t generation() const = 0;  // changes with the halo plans
 };
 
+// reciprocal-space Ewald in the AMOEBA step (mdg_set_ewald_recip): grid,
+// B-spline order, the step's alpha (set per call), excluded pairs removed
+struct PolarRecip {
+  int k1 = 0, k2 = 0, k3 = 0, order = 0;
+  double alpha = 0.0, electric = 1.0;
+  bool exclude = true;
+  bool on() const { return k1 > 0; }
+};
+
 struct ProfEntry {
   int64_t count = 0;
   double ms = 0;
@@ -205,7 +214,10 @@ struct mdg_ctx {
   // the excluded pairs from the reciprocal sum
   int32_t* excl_start = nullptr;
   int32_t* excl = nullptr;
-  void* pme = nullptr;  // PmeState (pme.cu)
+  void* pme = nullptr;      // PmeState (pme.cu): charges / permanent multipoles
+  void* pme_pol = nullptr;  // PmeState of the polarization fields (main stream)
+  mdg::PolarRecip pol_recip;  // mdg_set_ewald_recip
+  bool recip_in_step = false;  // last AMOEBA step added the multipole PME terms
   // MD (md.cu): velocities (w = 1/mass) and harmonic bonded terms
   double4* vel = nullptr;
   bool has_vel = false;
@@ -472,6 +484,11 @@ void pme_free(mdg_ctx* c);
 // potentials), 104-106 (sums of q^2, |mu|^2, Q:Q for the self energy)
 void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
                    double electric, bool exclude);
+// reciprocal + self Ewald field (c->pol_recip): mode 0 adds the permanent
+// multipoles' field (and removes the excluded pairs' erf part) to out; mode 1
+// adds v's dipole field to out; mode 2 (PCG) subtracts it from out and writes
+// the block partials of v.out
+void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out);
 // MD (md.cu): bonded forces added to c->force (results 100 bonds, 101
 // angles), velocity-Verlet half kick / drift, kinetic energy (result 102)
 void run_bonded(mdg_ctx* c);

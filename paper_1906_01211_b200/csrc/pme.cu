@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(kBlock) k_pme_convolve(PmeGeom g, double alpha
                                                         const double* __restrict__ bmod,
                                                         cufftDoubleComplex* __restrict__ s,
                                                         double* __restrict__ partials) {
+  // partials == NULL: the convolution alone (the induced-dipole field)
   const int kzh = g.k3 / 2 + 1;
   const int64_t total = (int64_t)g.k1 * g.k2 * kzh;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kBlock) k_pme_convolve(PmeGeom g, double alpha
     acc[6] += em * (1.0 - f * m3 * m3);
     s[e] = make_cuDoubleComplex(v.x * G, v.y * G);
   }
-  block_store_partials<7>(acc, partials);
+  if (partials) block_store_partials<7>(acc, partials);
 }
 
 __global__ void k_pme_gather(int64_t n, PmeGeom g, const double4* __restrict__ pos,
@@ -271,8 +272,8 @@ struct PmeState {
   bool plans = false;
 };
 
-void pme_free(mdg_ctx* c) {
-  PmeState* s = (PmeState*)c->pme;
+static void pme_free_slot(void** slot) {
+  PmeState* s = (PmeState*)*slot;
   if (!s) return;
   if (s->plans) {
     cufftDestroy(s->fwd);
@@ -282,7 +283,12 @@ void pme_free(mdg_ctx* c) {
   cudaFree(s->spec);
   cudaFree(s->bmod);
   delete s;
-  c->pme = nullptr;
+  *slot = nullptr;
+}
+
+void pme_free(mdg_ctx* c) {
+  pme_free_slot(&c->pme);
+  pme_free_slot(&c->pme_pol);
 }
 
 static void cufft_check(cufftResult r, const char* what) {
@@ -291,9 +297,9 @@ static void cufft_check(cufftResult r, const char* what) {
 
 // results: 80 recip energy, 81..86 virial (xx xy xz yy yz zz), 87 self,
 // 88 excluded-pair energy, 89..97 excluded-pair virial (row-major)
-void pme_setup(mdg_ctx* c, int k1, int k2, int k3, int order) {
-  PmeState* s = (PmeState*)c->pme;
-  if (!s) c->pme = s = new PmeState();
+static PmeState* pme_state(mdg_ctx* c, void** slot, int k1, int k2, int k3, int order) {
+  PmeState* s = (PmeState*)*slot;
+  if (!s) *slot = s = new PmeState();
   if (s->k1 != k1 || s->k2 != k2 || s->k3 != k3 || s->p != order || s->l1 != c->lx ||
       s->l2 != c->ly || s->l3 != c->lz) {
     if (s->plans) {
@@ -332,6 +338,11 @@ void pme_setup(mdg_ctx* c, int k1, int k2, int k3, int order) {
   }
   cufft_check(cufftSetStream(s->fwd, c->stream), "stream");
   cufft_check(cufftSetStream(s->inv, c->stream), "stream");
+  return s;
+}
+
+void pme_setup(mdg_ctx* c, int k1, int k2, int k3, int order) {
+  pme_state(c, &c->pme, k1, k2, k3, order);
 }
 
 void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
@@ -733,5 +744,183 @@ void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
                c->excl_start, c->excl, c->force, c->torque, c->partials);
     finalize_partials(c, grid_for(n), 1, 88, 1.0);
   }
+}
+
+// ---- reciprocal-space electric fields for the polarization (8(f)#3) ----------
+// E_i = -grad phi(r_i) from (a) the permanent multipoles (the PCG right-hand
+// side) or (b) a dipole vector v (the PCG operator), plus the Ewald self field
+// (4 a^3 / (3 sqrt(pi))) mu_i; the real-space kernels' Thole-damped erfc
+// tensors then complete the full Ewald + Thole field. Own PME state
+// (c->pme_pol): the permanent-multipole PME of the step runs on the aux
+// stream at the same time.
+
+// dipoles only: grid += sum_a v_a (K_a/L_a) dW/du_a
+__global__ void k_pme_spread_dip(int64_t n, PmeGeom g, const double4* __restrict__ pos,
+                                 const double4* __restrict__ v, double* __restrict__ grid,
+                                 const double* __restrict__ res, int skip_converged) {
+  if (skip_converged && res[27] != 0.0) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 r = pos[i];
+  const double4 m = v[i];
+  const double d1 = m.x * g.k1 / g.l1, d2 = m.y * g.k2 / g.l2, d3 = m.z * g.k3 / g.l3;
+  int i1, i2, i3;
+  double w1, w2, w3;
+  frac(r.x, g.l1, g.k1, i1, w1);
+  frac(r.y, g.l2, g.k2, i2, w2);
+  frac(r.z, g.l3, g.k3, i3, w3);
+  double t1[kMaxOrder], t2[kMaxOrder], t3[kMaxOrder], e1[kMaxOrder], e2[kMaxOrder],
+      e3[kMaxOrder];
+  bspline(w1, g.p, t1, e1);
+  bspline(w2, g.p, t2, e2);
+  bspline(w3, g.p, t3, e3);
+  for (int a = 0; a < g.p; ++a) {
+    const int x = (i1 - a + g.k1) % g.k1;
+    for (int b = 0; b < g.p; ++b) {
+      const int y = (i2 - b + g.k2) % g.k2;
+      const double c0 = d1 * e1[a] * t2[b] + d2 * t1[a] * e2[b];
+      const double c1 = d3 * t1[a] * t2[b];
+      double* row = grid + ((size_t)x * g.k2 + y) * g.k3;
+      for (int c = 0; c < g.p; ++c)
+        atomicAdd(row + (i3 - c + g.k3) % g.k3, c0 * t3[c] + c1 * e3[c]);
+    }
+  }
+}
+
+// mode 0 (permanent): out += E + cself mu_perm (dipole of mp)
+// mode 1 (add): out += E + cself v
+// mode 2 (PCG): out -= E + cself v, partials p.out (p = v)
+__global__ void __launch_bounds__(kBlock) k_pme_gather_field(int64_t n, PmeGeom g,
+                                                            const double4* __restrict__ pos,
+                                                            const double* __restrict__ phi,
+                                                            const double4* __restrict__ v,
+                                                            const double4* __restrict__ mp,
+                                                            double cself, int mode,
+                                                            double4* __restrict__ out,
+                                                            double* __restrict__ partials,
+                                                            const double* __restrict__ res) {
+  if (mode == 2 && res[27] != 0.0) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double acc[1] = {0.0};
+  if (i < n) {
+    const double4 r = pos[i];
+    int i1, i2, i3;
+    double w1, w2, w3;
+    frac(r.x, g.l1, g.k1, i1, w1);
+    frac(r.y, g.l2, g.k2, i2, w2);
+    frac(r.z, g.l3, g.k3, i3, w3);
+    double t1[kMaxOrder], t2[kMaxOrder], t3[kMaxOrder], d1[kMaxOrder], d2[kMaxOrder],
+        d3[kMaxOrder];
+    bspline(w1, g.p, t1, d1);
+    bspline(w2, g.p, t2, d2);
+    bspline(w3, g.p, t3, d3);
+    double gx = 0, gy = 0, gz = 0;
+    for (int a = 0; a < g.p; ++a) {
+      const int x = (i1 - a + g.k1) % g.k1;
+      for (int b = 0; b < g.p; ++b) {
+        const int y = (i2 - b + g.k2) % g.k2;
+        const double* row = phi + ((size_t)x * g.k2 + y) * g.k3;
+        for (int c = 0; c < g.p; ++c) {
+          const double ph = __ldg(row + (i3 - c + g.k3) % g.k3);
+          gx += d1[a] * t2[b] * t3[c] * ph;
+          gy += t1[a] * d2[b] * t3[c] * ph;
+          gz += t1[a] * t2[b] * d3[c] * ph;
+        }
+      }
+    }
+    const double4 m = (mode == 0) ? mp[3 * i] : v[i];
+    const double ex = -gx * g.k1 / g.l1 + cself * m.x;
+    const double ey = -gy * g.k2 / g.l2 + cself * m.y;
+    const double ez = -gz * g.k3 / g.l3 + cself * m.z;
+    double4 o = out[i];
+    if (mode == 2) {
+      o.x -= ex;
+      o.y -= ey;
+      o.z -= ez;
+      acc[0] = m.x * o.x + m.y * o.y + m.z * o.z;
+    } else {
+      o.x += ex;
+      o.y += ey;
+      o.z += ez;
+    }
+    out[i] = o;
+  }
+  if (mode == 2) block_store_partials<1>(acc, partials);
+}
+
+// out_i -= erf(a r)/r-kernel field at i of the multipoles of its same-molecule
+// partners (excluded from the real-space field, contained in the reciprocal one)
+__global__ void k_field_excl_erf(int64_t n, Box bx, double alpha, const double4* __restrict__ pos,
+                                 const double4* __restrict__ pq4, const double4* __restrict__ mp,
+                                 const int32_t* __restrict__ xs, const int32_t* __restrict__ xl,
+                                 double4* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 pi = pos[i];
+  double ex = 0, ey = 0, ez = 0;
+  for (int32_t k = xs[i]; k < xs[i + 1]; ++k) {
+    const int32_t j = xl[k];
+    const double4 pj = pos[j];
+    double x, y, z;
+    const double r2 = min_image(bx, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, x, y, z);
+    const double r = sqrt(r2);
+    const double inv_r = 1.0 / r, inv_r2 = inv_r * inv_r;
+    double B[4];
+    ewald_bn<3>(r, inv_r, inv_r2, alpha, B);
+    double bare = inv_r;
+    for (int q = 0; q < 4; ++q) {
+      if (q > 0) bare *= (double)(2 * q - 1) * inv_r2;
+      B[q] = bare - B[q];
+    }
+    const double qj = pq4[j].z;
+    const double4 m0 = mp[3 * (size_t)j], m1 = mp[3 * (size_t)j + 1];
+    const double qzz = mp[3 * (size_t)j + 2].x;
+    const double qx = m0.w * x + m1.x * y + m1.y * z;
+    const double qy = m1.x * x + m1.z * y + m1.w * z;
+    const double qz = m1.y * x + m1.w * y + qzz * z;
+    const double dr = m0.x * x + m0.y * y + m0.z * z;
+    const double qr = x * qx + y * qy + z * qz;
+    const double cc = B[1] * qj + B[2] * dr + B[3] * qr;
+    ex += cc * x - B[1] * m0.x - 2.0 * B[2] * qx;
+    ey += cc * y - B[1] * m0.y - 2.0 * B[2] * qy;
+    ez += cc * z - B[1] * m0.z - 2.0 * B[2] * qz;
+  }
+  double4 o = out[i];
+  o.x -= ex;
+  o.y -= ey;
+  o.z -= ez;
+  out[i] = o;
+}
+
+// Reciprocal + self field added to (mode 0/1) or, in PCG form, subtracted from
+// `out` with the partials of p.out (mode 2). v: the dipole vector (modes 1/2).
+// The launches are capture-safe (fixed grids, no host sync).
+void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out) {
+  const PolarRecip& R = c->pol_recip;
+  PmeState* s = pme_state(c, &c->pme_pol, R.k1, R.k2, R.k3, R.order);
+  const PmeGeom g{R.k1, R.k2, R.k3, R.order, c->lx, c->ly, c->lz};
+  const int64_t n = c->n_own;
+  const double a = R.alpha;
+  const double cself = 4.0 * a * a * a / (3.0 * std::sqrt(M_PI));
+  MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)R.k1 * R.k2 * R.k3 * sizeof(double),
+                                 c->stream));
+  if (mode == 0)
+    MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos,
+               c->pq4, c->mp, s->grid);
+  else
+    MDG_LAUNCH(c, "pme_spread_dip", grid_for(n, 128), 128, 0, k_pme_spread_dip, n, g, c->pos,
+               v, s->grid, c->results, mode == 2 ? 1 : 0);
+  cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
+  const int64_t total = (int64_t)R.k1 * R.k2 * (R.k3 / 2 + 1);
+  const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
+  MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, a, s->bmod,
+             s->spec, (double*)nullptr);
+  cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
+  MDG_LAUNCH(c, "pme_gather_field", grid_for(n), kBlock, 0, k_pme_gather_field, n, g, c->pos,
+             s->grid, v, c->mp, cself, mode, out, c->partials, c->results);
+  if (mode == 0 && R.exclude && c->has_mol && c->excl_start)
+    MDG_LAUNCH(c, "field_excl_erf", grid_for(n, 128), 128, 0, k_field_excl_erf, n,
+               make_box(c->lx, c->ly, c->lz), a, c->pos, c->pq4, c->mp, c->excl_start,
+               c->excl, out);
 }
 }  // namespace mdg

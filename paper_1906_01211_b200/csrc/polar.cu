@@ -645,7 +645,12 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
     mdg_ctx* c = d.c;
     if (d.cl) cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
     else k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
-    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, d.g, 1, c->results);
+    int64_t pb = d.g;
+    if (c->pol_recip.on()) {  // q -= reciprocal + self field of p; partials p.q
+      pme_field(c, 2, c->cg_p, c->cg_q);
+      pb = grid_for(c->n_own);
+    }
+    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, pb, 1, c->results);
   }
   if (comm) comm->allreduce(20, 1);
   for (PcgDom& d : ds) {
@@ -760,6 +765,8 @@ void pcg_graph_forget(const void* owner) { pcg_graphs().erase(owner); }
 int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_debye,
                       int64_t max_iter, double* last_rms) {
   mdg_ctx* c0 = doms[0];
+  if (c0->pol_recip.on() && (doms.size() > 1 || comm || c0->n_own != c0->n))
+    throw_error(MDG_CONTRACT, "reciprocal-space polarization: single domain only");
   double n_global = 0;
   for (mdg_ctx* c : doms) n_global += (double)c->n_own;
   if (comm) n_global = (double)comm->n_global();
@@ -794,13 +801,15 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
       k.in = c->mu;
       MDG_LAUNCH_SITES(c, "tmatvec_pre", k.n, k, k_tmatvec_pre<false>);
     }
+    if (c->pol_recip.on()) pme_field(c, 1, c->mu, c->cg_q);  // + reciprocal + self field
     MDG_LAUNCH(c, "cg_init", (unsigned)d.blocks, kBlock, 0, k_cg_init, c->n_own, c->polp,
                c->eperm, c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
     MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, d.blocks, 0,
                c->results);
   }
   if (comm) comm->allreduce(21, 1);
-  const bool graph = !c0->profile && (!comm || comm->capturable());
+  // (the reciprocal-space field's cuFFT calls stay out of the while graph)
+  const bool graph = !c0->profile && (!comm || comm->capturable()) && !c0->pol_recip.on();
   if (graph) {
     pcg_graph_launch(pcg_graphs()[comm ? (const void*)comm : (const void*)c0], ds, comm,
                      max_iter, n_global, tol_debye);
@@ -817,8 +826,13 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
           TPArgs k = d.k;
           MDG_LAUNCH_SITES(c, "tmatvec_pcg", k.n, k, k_tmatvec_pre<true>);
         }
-        MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials,
-                   c->last_grid, 1, c->results);
+        int64_t pb = c->last_grid;
+        if (c->pol_recip.on()) {
+          pme_field(c, 2, c->cg_p, c->cg_q);
+          pb = grid_for(c->n_own);
+        }
+        MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, pb, 1,
+                   c->results);
       }
       if (comm) comm->allreduce(20, 1);
       for (PcgDom& d : ds) {

@@ -125,6 +125,7 @@ SIGNATURES = {
     "mdg_ewald_recip_mpole": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                         _dp, _dp]),
+    "mdg_set_ewald_recip": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_bonded_upload": (C.c_int, [C.c_void_p, C.c_int64, _ip, _dp, _dp, C.c_int64, _ip, _dp,
                                     _dp]),
@@ -585,6 +586,11 @@ class Engine:
         return _aos(fx, fy, fz), e, w.reshape(3, 3)
 
     # ---- MD (8(f)#4) ---------------------------------------------------------------
+    def set_ewald_recip(self, grid=(0, 0, 0), order: int = 6):
+        """Reciprocal-space Ewald in amoeba_step / polar_solve_pcg
+        (mdg_set_ewald_recip); grid (0, 0, 0) switches it off."""
+        check(self.lib.mdg_set_ewald_recip(self.ctx, *map(int, grid), int(order)))
+
     def ewald_recip_mpole(self, alpha: float, grid=(48, 48, 48), order: int = 6,
                           electric: float = 1.0, exclude: bool = True):
         """Smooth PME of the permanent multipoles: (forces, torques,

@@ -940,6 +940,89 @@ def test_full_mpole_ewald_is_alpha_independent(engine, mdg):
     assert force_err_max(t1, t2) <= 1e-7
 
 
+def _full_ewald_polar_oracle(oracle, s, alpha, cutoff, thole=0.39, kmax=(10, 10, 10)):
+    """Exact (dense) solution of (alpha^-1 - T_real - T_recip - self) mu =
+    E_real + E_recip + self - E_excluded(erf) on a small box."""
+    from oracle import ewald_mpole as em
+    so = to_oracle_system(s)
+    t = oracle.build_table(so, cutoff)
+    pos = np.stack([s.x, s.y, s.z], 1)
+    n = s.n_sites
+    e_full = (oracle.perm_field_ewald(so, t, alpha, cutoff, thole, exclude=True)
+              + em.field_recip(pos, s.charge, s.dipole, s.quadrupole, s.box, alpha, kmax)
+              - em.excluded_field_erf(pos, s.charge, s.dipole, s.quadrupole, s.box,
+                                      s.molecule, alpha))
+    T = np.zeros((3 * n, 3 * n))
+    for k in range(3 * n):
+        u = np.zeros(3 * n)
+        u[k] = 1.0
+        T[:, k] = oracle.tmatvec_ewald(so, t, alpha, cutoff, thole, u.reshape(n, 3)).reshape(-1)
+    T += em.tmat_recip_dense(pos, s.box, alpha, kmax)
+    A = np.diag(np.repeat(1.0 / np.asarray(s.polarizability), 3)) - T
+    mu = np.linalg.solve(A, e_full.reshape(-1)).reshape(n, 3)
+    return mu, e_full
+
+
+def test_pcg_with_reciprocal_space_matches_dense_solve(engine, oracle, mdg):
+    """8(f)#3: the PCG with the reciprocal-space + self field in its operator
+    and right-hand side (one smooth-PME pass per iteration) == the dense
+    solve of the full Ewald + Thole system (oracle/ewald_mpole.py)."""
+    s = mdg.water_box(27, 10.2, 5, "amoeba")
+    a = 0.5446
+    mu_o, e_o = _full_ewald_polar_oracle(oracle, s, a, 5.0)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(5.0)
+    engine.set_ewald_recip((40, 40, 40), 8)
+    try:
+        st = engine.polar_solve_pcg(t, mdg.PolarParams(5.0, 0.39), alpha=a, tol_debye=1e-9,
+                                    max_iter=200, exclude_perm=True)
+        ep = engine.fetch_perm_field()
+    finally:
+        engine.set_ewald_recip((0, 0, 0))
+    assert force_err_max(ep, e_o) <= 1e-7
+    d = np.sqrt(np.mean(np.sum((st.mu - mu_o) ** 2, 1))) * mdg.DEBYE
+    assert d < 1e-7
+
+
+def test_amoeba_step_with_reciprocal_space(engine, oracle, mdg):
+    """The AMOEBA step with mdg_set_ewald_recip: multipole energy / forces /
+    torques include the reciprocal, self and excluded-pair terms; the
+    polarization energy is -1/2 mu.E_full of the full-Ewald solution."""
+    from oracle import ewald_mpole as em
+    from oracle.oracle import FastPort
+    s = mdg.water_box(27, 10.2, 6, "amoeba")
+    a = 0.5446
+    so = to_oracle_system(s)
+    pos = np.stack([s.x, s.y, s.z], 1)
+    t_o = oracle.build_table(so, 5.0)
+    fp = FastPort()
+    fm, tm, em_real = fp.mpole(so, t_o, a, 5.0, mdg.ELECTRIC, True)
+    ek, fk, tk = em.recip(pos, s.charge, s.dipole, s.quadrupole, s.box, a, (10, 10, 10),
+                          mdg.ELECTRIC)
+    ex, fx, tx = em.excluded_correction(pos, s.charge, s.dipole, s.quadrupole, s.box,
+                                        s.molecule, a, mdg.ELECTRIC, pair=em.mpole_pair)
+    es = em.self_energy(s.charge, s.dipole, s.quadrupole, a, mdg.ELECTRIC)
+    mu_o, e_o = _full_ewald_polar_oracle(oracle, s, a, 5.0)
+    engine.upload_system(s)
+    te = engine.build_neighbor_table(5.0, list_id=0)
+    p = mdg.AmoebaParams(4.5, 0.07, 0.12, 5.0, a, mdg.ELECTRIC, 0.39, 1e-9, 200, 1,
+                         mdg.TERM_MPOLE | mdg.TERM_POLAR)
+    engine.set_ewald_recip((40, 40, 40), 8)
+    try:
+        engine.amoeba_step(te, te, p)
+        e, w, it, rms = engine.fetch_energies()
+        f, tq, mu = engine.fetch_forces(), engine.fetch_torques(), engine.fetch_dipoles()
+    finally:
+        engine.set_ewald_recip((0, 0, 0))
+    # the terms cancel (|E| ~ 60 of |terms| ~ 2500): PME accuracy on the terms
+    scale = abs(em_real) + abs(ek) + abs(es) + abs(ex)
+    assert abs(e[1] - (em_real + ek + es + ex)) <= 1e-8 * scale
+    assert force_err_max(f, fm + fk + fx) <= 1e-6
+    assert force_err_max(tq, tm + tk + tx) <= 1e-6
+    assert np.sqrt(np.mean(np.sum((mu - mu_o) ** 2, 1))) * mdg.DEBYE < 1e-7
+    assert rel(e[2], -0.5 * mdg.ELECTRIC * float(np.sum(mu_o * e_o))) <= 1e-7
+
+
 def test_full_ewald_is_alpha_independent(engine, oracle, mdg):
     """Real space (device kernel) + PME + self + excluded pairs: the same
     total energy and forces for two splitting parameters."""
