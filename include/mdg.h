@@ -284,6 +284,14 @@ typedef struct {
 int mdg_md_run(mdg_ctx* ctx, const mdg_md_params* p, const mdg_charmm_params* charmm,
                const mdg_amoeba_params* amoeba, double* ekin, double* epot);
 
+/* Spatial re-sort on the device: the sites are re-keyed by their current
+ * ~2 A Morton cells and every per-site array is permuted (index arrays
+ * remapped), restoring the gathers' locality after the sites have moved.
+ * mdg_md_run does it at every list rebuild (MDG_RESORT=0 disables). The
+ * caller-order interface is unchanged; neighbour lists are invalidated
+ * (rebuild them). Single domain only. */
+int mdg_resort(mdg_ctx* ctx);
+
 /* Results of the last step / kernel, copied to host (caller order).
  * energies[4] = {vdw, coulomb or multipole, polarization (0 here), unused}. */
 int mdg_fetch_forces(mdg_ctx* ctx, double* fx, double* fy, double* fz);

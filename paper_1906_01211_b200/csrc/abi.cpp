@@ -1499,7 +1499,11 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
       }
     } nfo{c, {c->fout[0], c->fout[1], c->fout[2]}};
     for (int a = 0; a < 3; ++a) c->fout[a] = nullptr;
+    // re-sort the sites by their current cells at every rebuild (the
+    // gathers keep their locality as molecules diffuse); MDG_RESORT=0 off
+    static const int resort = mdg::env_int("MDG_RESORT", 1);
     auto rebuild = [&] {
+      if (resort) mdg::resort_sites(c);
       mdg::nlist_build(c, p->elec_list, p->elec_list_cutoff, MDG_SITES_ATOMIC);
       if (p->model == 1) mdg::nlist_build(c, p->vdw_list, p->vdw_list_cutoff, MDG_SITES_VDW);
     };
@@ -1538,6 +1542,14 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
       }
     }
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int mdg_resort(mdg_ctx* c) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    mdg::resort_sites(c);
   });
 }
 

@@ -461,6 +461,8 @@ void group_sum_host(mdg_group* g, double* v, int nv);
 // (debug.cu); a no-op in the product build
 void debug_check_rows(mdg_ctx* c, const char* what, const int32_t* nbr, const int32_t* cnt,
                       int32_t cap, int64_t rows, int64_t n_all, bool sorted);
+// device spatial re-sort of every per-site array (resort.cu); invalidates lists
+void resort_sites(mdg_ctx* c);
 // vdW sites from the positions (Halgren reduction or copy), after new positions
 void refresh_vsites(mdg_ctx* c);
 void run_reduce_sites(mdg_ctx* c);

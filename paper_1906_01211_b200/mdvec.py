@@ -126,6 +126,7 @@ SIGNATURES = {
                                         C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                         _dp, _dp]),
     "mdg_set_ewald_recip": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "mdg_resort": (C.c_int, [C.c_void_p]),
     "mdg_charmm_step": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "mdg_bonded_upload": (C.c_int, [C.c_void_p, C.c_int64, _ip, _dp, _dp, C.c_int64, _ip, _dp,
                                     _dp]),
@@ -586,6 +587,11 @@ class Engine:
         return _aos(fx, fy, fz), e, w.reshape(3, 3)
 
     # ---- MD (8(f)#4) ---------------------------------------------------------------
+    def resort(self):
+        """Re-sort the sites spatially on the device (mdg_resort); lists must
+        be rebuilt afterwards."""
+        check(self.lib.mdg_resort(self.ctx))
+
     def set_ewald_recip(self, grid=(0, 0, 0), order: int = 6):
         """Reciprocal-space Ewald in amoeba_step / polar_solve_pcg
         (mdg_set_ewald_recip); grid (0, 0, 0) switches it off."""

@@ -1103,6 +1103,58 @@ def test_md_trajectory_matches_oracle(engine, oracle, mdg):
     np.testing.assert_allclose(ep, ep_o, rtol=1e-9)
 
 
+def test_resort_keeps_every_result(engine, oracle, mdg):
+    """mdg_resort (device spatial re-sort) on a system with
+    topology, H reduction, local frames, bonds/angles and velocities: the
+    caller-order results of the AMOEBA step (energies, forces, torques,
+    dipoles), the bonded forces and the coordinates / velocities are the same
+    after the re-sort (to FP64 summation order), including after the sites
+    were moved far from their cells."""
+    from oracle import frames as fr
+    s = mdg.water_box(512, 24.8, 3, "amoeba")
+    frame, za, xa = fr.water_frames(s.molecule)
+    n_mol = s.n_sites // 3
+    bonds = np.stack([np.repeat(np.arange(n_mol) * 3, 2),
+                      (np.arange(n_mol)[:, None] * 3 + np.array([1, 2])).ravel()], 1)
+    angles = np.stack([np.arange(n_mol) * 3 + 1, np.arange(n_mol) * 3,
+                       np.arange(n_mol) * 3 + 2], 1)
+    mass = np.tile([15.999, 1.008, 1.008], n_mol)
+    vel = np.random.default_rng(4).normal(size=(s.n_sites, 3)) * 0.005
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-6, 100, 1,
+                         mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE)
+    engine.upload_system(s)
+    engine.upload_frames(frame, za, xa, np.asarray(s.dipole), np.asarray(s.quadrupole))
+    engine.upload_bonded(bonds, 529.6, 0.9572, angles, 34.05, np.deg2rad(104.52))
+    engine.upload_velocities(vel, mass)
+    # move every molecule to another molecule's place: the stored order no
+    # longer follows space
+    perm = np.random.default_rng(5).permutation(n_mol)
+    xyz = np.stack([s.x, s.y, s.z], 1).reshape(n_mol, 3, 3)[perm].reshape(-1, 3)
+    engine.upload_positions(xyz[:, 0], xyz[:, 1], xyz[:, 2])
+
+    def results():
+        tv = engine.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+        te = engine.build_neighbor_table(9.0, list_id=0)
+        engine.amoeba_step(tv, te, p)
+        e, w, it, rms = engine.fetch_energies()
+        fb, eb = engine.bonded_forces()
+        return (e, w, engine.fetch_forces(), engine.fetch_torques(), engine.fetch_dipoles(),
+                fb, eb, engine.fetch_positions(), engine.fetch_velocities())
+
+    before = results()
+    engine.resort()
+    after = results()
+    e0, w0, f0, t0, mu0, fb0, eb0, x0, v0 = before
+    e1, w1, f1, t1, mu1, fb1, eb1, x1, v1 = after
+    np.testing.assert_allclose(e1[:3], e0[:3], rtol=1e-11)
+    np.testing.assert_allclose(w1, w0, rtol=1e-10, atol=1e-10 * np.abs(w0).max())
+    assert force_err_max(f1, f0) <= 1e-11
+    assert force_err_max(t1, t0) <= 1e-11
+    assert np.abs(mu1 - mu0).max() <= 1e-10 * np.abs(mu0).max()
+    assert force_err_max(fb1, fb0) <= 1e-12 and np.allclose(eb1, eb0, rtol=1e-12)
+    assert np.array_equal(x1, x0) and np.array_equal(v1, v0)
+
+
 def test_md_energy_conservation(engine, mdg):
     """NVE: 2,000 steps of 0.25 fs -- the total energy stays flat."""
     s, mass, vel, b, a = _md_water(mdg, seed=4)
