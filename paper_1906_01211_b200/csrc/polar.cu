@@ -435,6 +435,169 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
   if (PCG) block_store_partials<1>(acc, a.partials);
 }
 
+// ---- TMA-staged mat-vec --------------------------------------------------------
+// The same product as k_tmatvec_pre, with each row's indices and pair
+// tensors brought into shared memory by bulk asynchronous copies (TMA,
+// cp.async.bulk + mbarrier transaction counts): while a warp computes row k
+// from shared memory, the copy engine is already fetching row k + 1, so the
+// row stream's HBM latency leaves the dependence chain (ncu on the LDG
+// version: the largest stall is the index load feeding the gathers) and the
+// only LSU global traffic left is the neighbour gathers. Two stages per
+// warp; lane 0 arms the stage's barrier and issues both copies.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+// dynamic shared memory of one block: barriers, then per warp two stages of
+// {tensors[cap] double2, indices[cap] int32}
+__host__ __device__ inline size_t tma_stage_bytes(int32_t cap) { return (size_t)cap * 20; }
+__host__ __device__ inline size_t tma_warp_bytes(int32_t cap) { return (2 * tma_stage_bytes(cap) + 127) & ~(size_t)127; }
+__host__ __device__ inline size_t tma_smem_bytes(int32_t cap) { return 128 + kWarps * tma_warp_bytes(cap); }
+
+template <bool PCG>
+__global__ void __launch_bounds__(kBlock) k_tmatvec_tma(TPArgs a) {
+  if (PCG && a.res[27] != 0.0) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t cap = a.pcap;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * w;
+  unsigned char* wb = smem + 128 + (size_t)w * tma_warp_bytes(cap);
+  const size_t sb = tma_stage_bytes(cap);
+  auto srr = [&](int st) { return reinterpret_cast<double2*>(wb + st * sb); };
+  auto sidx = [&](int st) { return reinterpret_cast<int32_t*>(wb + st * sb + (size_t)cap * 16); };
+  const int64_t first = (int64_t)blockIdx.x * a.ipw + w;
+  const int64_t end = min((int64_t)a.n, ((int64_t)blockIdx.x + 1) * a.ipw);
+  if (lane == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int64_t site, int st) {  // lane 0
+    const int c = a.pcnt[site];
+    const uint32_t bi = (uint32_t)((c * 4 + 15) & ~15), br = (uint32_t)c * 16u;
+    mbar_arm(&bar[st], bi + br);
+    if (c > 0) {
+      bulk_load(srr(st), a.trr + (size_t)site * cap, br, &bar[st]);
+      bulk_load(sidx(st), a.pnbr + (size_t)site * cap, bi, &bar[st]);
+    }
+  };
+  if (lane == 0 && first < end) issue(first, 0);
+  uint32_t phases = 0u;  // bit st: parity of stage st's next completion
+  double acc[1] = {0.0};
+  int k = 0;
+  for (int64_t i = first; i < end; i += kWarps, ++k) {
+    const int st = k & 1;
+    const int64_t nxt = i + kWarps;
+    if (lane == 0 && nxt < end) {
+      // stage st ^ 1 was last read by the generic proxy in iteration k - 1
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nxt, st ^ 1);
+    }
+    const double4 pi = a.pos[i];
+    const int cnt = a.pcnt[i];
+    MDG_DASSERT(cnt >= 0 && cnt <= cap);
+    mbar_wait(&bar[st], (phases >> st) & 1u);
+    phases ^= 1u << st;
+    const int32_t* row = sidx(st);
+    const double2* trow = srr(st);
+    double ex = 0, ey = 0, ez = 0;
+    for (int k0 = lane; k0 < cnt; k0 += 32) {
+      const int32_t j = row[k0] & 0x7fffffff;
+      const double2 rr = trow[k0];
+      const double4 pj = ldg4(a.pos + j);
+      const double4 mj = ldg4(a.in + j);
+      double dx, dy, dz;
+      min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
+      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
+      ex += rr.y * dot * dx - rr.x * mj.x;
+      ey += rr.y * dot * dy - rr.x * mj.y;
+      ez += rr.y * dot * dz - rr.x * mj.z;
+    }
+    ex = warp_allsum(ex);
+    ey = warp_allsum(ey);
+    ez = warp_allsum(ez);
+    if (lane == 0) {
+      if (PCG) {
+        const double4 p = a.in[i];
+        const double inva = 1.0 / a.polp[i].x;
+        const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
+        a.out[i] = make_double4(qx, qy, qz, 0.0);
+        acc[0] += p.x * qx + p.y * qy + p.z * qz;
+      } else {
+        a.out[i] = make_double4(ex, ey, ez, 0.0);
+      }
+    }
+    __syncwarp();
+  }
+  if (PCG) block_store_partials<1>(acc, a.partials);
+}
+
+// launch shape of the TMA mat-vec: (sites per block, blocks, smem bytes)
+struct TmaShape {
+  int64_t ipb = 0, grid = 0;
+  size_t smem = 0;
+};
+
+static TmaShape tma_shape(mdg_ctx* c, int64_t n, int32_t cap) {
+  TmaShape t;
+  t.smem = tma_smem_bytes(cap);
+  static size_t configured = 0;
+  if (t.smem > configured) {
+    for (const void* f : {(const void*)k_tmatvec_tma<true>, (const void*)k_tmatvec_tma<false>})
+      MDG_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)t.smem));
+    configured = t.smem;
+  }
+  int occ = 0, sms = 0, dev = 0;
+  MDG_CUDA_CHECK(cudaGetDevice(&dev));
+  MDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tmatvec_tma<true>, kBlock,
+                                                               t.smem));
+  static const int waves = env_int("MDG_TMA_WAVES", 16);
+  const int64_t blocks = (int64_t)sms * std::max(1, occ) * waves;
+  t.ipb = std::max<int64_t>(kWarps, (n + blocks - 1) / blocks);
+  t.grid = (n + t.ipb - 1) / t.ipb;
+  ensure_partials(c, t.grid);
+  return t;
+}
+
+static bool use_tma(const PrunedList& P) {
+  static const int on = env_int("MDG_TMA_MATVEC", 0);  // opt-in: measured slower (DESIGN 4)
+  return on && tma_smem_bytes(P.cap) <= 200 * 1024;
+}
+
 // ---- PCG vector kernels ------------------------------------------------------
 // result slots: 20 p.q, 21 r.z (current), 22 r.z (new), 23 sum|dmu|^2, 24 beta,
 // 25 rms (D), 27 converged flag, 28 iterations. The scalar kernels form the
@@ -598,6 +761,8 @@ struct PcgDom {
   TPArgs k;
   CLArgs kc;
   bool cl;
+  bool tma = false;
+  size_t smem = 0;
   int64_t g;       // mat-vec grid
   int64_t blocks;  // vector-kernel grid
 };
@@ -608,9 +773,15 @@ static void pcg_dom_setup(PcgDom& d, mdg_ctx* c) {
   d.c = c;
   d.blocks = grid_for(n);
   d.cl = P.cl_valid;
+  d.tma = !d.cl && use_tma(P);
   const int64_t units = d.cl ? P.ncl : n;
   const void* kern = d.cl ? cl_matvec_kernel(true) : (const void*)k_tmatvec_pre<true>;
-  const int64_t ipb = sites_per_block(kern, units, c->launch_bps, c->launch_waves);
+  int64_t ipb = sites_per_block(kern, units, c->launch_bps, c->launch_waves);
+  if (d.tma) {
+    const TmaShape t = tma_shape(c, n, P.cap);
+    ipb = t.ipb;
+    d.smem = t.smem;
+  }
   d.g = (units + ipb - 1) / ipb;
   ensure_partials(c, std::max(d.g, d.blocks));
   TPArgs& k = d.k;
@@ -644,6 +815,7 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
   for (PcgDom& d : ds) {
     mdg_ctx* c = d.c;
     if (d.cl) cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
+    else if (d.tma) k_tmatvec_tma<true><<<(unsigned)d.g, kBlock, d.smem, c->stream>>>(d.k);
     else k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
     int64_t pb = d.g;
     if (c->pol_recip.on()) {  // q -= reciprocal + self field of p; partials p.q
@@ -796,6 +968,10 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
     if (d.cl) {
       CLArgs kc = cl_args(c, c->mu, c->cg_q);
       cl_matvec_launch(c, kc, false, "tmatvec_pre");
+    } else if (d.tma) {
+      TPArgs k = d.k;
+      k.in = c->mu;
+      MDG_LAUNCH(c, "tmatvec_pre", (unsigned)d.g, kBlock, d.smem, k_tmatvec_tma<false>, k);
     } else {
       TPArgs k = d.k;
       k.in = c->mu;
@@ -822,6 +998,9 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
         if (d.cl) {
           CLArgs kc = d.kc;
           cl_matvec_launch(c, kc, true, "tmatvec_pcg");
+        } else if (d.tma) {
+          MDG_LAUNCH(c, "tmatvec_pcg", (unsigned)d.g, kBlock, d.smem, k_tmatvec_tma<true>, d.k);
+          c->last_grid = d.g;
         } else {
           TPArgs k = d.k;
           MDG_LAUNCH_SITES(c, "tmatvec_pcg", k.n, k, k_tmatvec_pre<true>);
