@@ -212,9 +212,11 @@ int mdg_ewald_recip_mpole(mdg_ctx* ctx, double alpha, int k1, int k2, int k3, in
  * the PCG operator gains the reciprocal + self field of the dipoles (one
  * smooth-PME pass per iteration); the step's multipole term gains
  * mdg_ewald_recip_mpole's energy, forces and torques. The polarization
- * energy -1/2 mu.E_perm is then the full Ewald one. Reciprocal-space
- * polarization FORCES are not built (MDG_TERM_POLAR_FORCE is refused).
- * k1 = 0 switches it off (default). */
+ * energy -1/2 mu.E_perm is then the full Ewald one. With
+ * MDG_TERM_POLAR_FORCE (and MDG_TERM_MPOLE) the reciprocal-space forces and
+ * torques of multipoles + polarization come from one pass over the
+ * permanent + induced set after the solve (torques on the permanent
+ * multipoles only). k1 = 0 switches it off (default). */
 int mdg_set_ewald_recip(mdg_ctx* ctx, int k1, int k2, int k3, int order);
 
 /* ---- fused steps (device-resident; the bench's hot path) ----------------- */

@@ -1189,9 +1189,9 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   need(!(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_POLAR),
        "amoeba_step: polarization forces need the polarization solve");
   const bool recip = c->pol_recip.on();
-  need(!recip || !(st.terms & MDG_TERM_POLAR_FORCE),
-       "amoeba_step: reciprocal-space polarization forces are not built (mdg_set_ewald_recip)");
   need(!recip || c->n_own == c->n, "amoeba_step: reciprocal space is single-domain only");
+  need(!recip || !(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_MPOLE),
+       "amoeba_step: reciprocal-space polarization forces come with the multipole term");
   MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, (recip ? 107 : 80) * sizeof(double), c->stream));
   c->pol_recip.alpha = p->alpha;
   c->pol_recip.electric = p->electric;
@@ -1235,9 +1235,13 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
     if (st.terms & MDG_TERM_MPOLE) {
       if (st.polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
       else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
-      if (recip) {  // + the multipoles' reciprocal-space sum (own PME state)
+      if (recip) {  // + the multipoles' reciprocal-space sum (own PME state);
+        // with polarization forces its forces / torques come from the
+        // permanent + induced pass after the solve (amoeba_post)
         const mdg::PolarRecip& R = c->pol_recip;
-        mdg::run_pme_mpole(c, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric, R.exclude);
+        const bool combined = st.polar && (st.terms & MDG_TERM_POLAR_FORCE);
+        mdg::run_pme_mpole(c, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric, R.exclude,
+                           nullptr, !combined);
         c->recip_in_step = true;
       }
     } else {
@@ -1261,6 +1265,14 @@ static void amoeba_join(mdg_ctx* c, const AmoebaPhase& st) {
 static void amoeba_post(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_params* p) {
   if (st.polar && (st.terms & MDG_TERM_POLAR_FORCE)) {
     mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
+    if (c->pol_recip.on() && (st.terms & MDG_TERM_MPOLE)) {
+      // reciprocal space of multipoles + polarization at fixed dipoles: the
+      // forces of the permanent + induced set (E_mpole,rec + E_pol,rec =
+      // Q[M + mu], the mu-only self terms being position-independent)
+      const mdg::PolarRecip& R = c->pol_recip;
+      mdg::run_pme_mpole(c, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric, R.exclude, c->mu,
+                         true);
+    }
     c->has_polar_force = true;
   }
   if ((st.terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);

@@ -484,8 +484,12 @@ void pme_free(mdg_ctx* c);
 // smooth PME for permanent multipoles (q, mu, Theta): adds forces and torques;
 // results 80 (recip), 88 (excluded pairs), 98 (recip from the gathered
 // potentials), 104-106 (sums of q^2, |mu|^2, Q:Q for the self energy)
+// ind != NULL: the permanent + induced set (the polarization forces' pass:
+// forces of the whole set, torques on the permanent multipoles, no energies;
+// excluded pairs keep their induced-induced part); forces == false: energies only
 void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
-                   double electric, bool exclude);
+                   double electric, bool exclude, const double4* ind = nullptr,
+                   bool forces = true);
 // reciprocal + self Ewald field (c->pol_recip): mode 0 adds the permanent
 // multipoles' field (and removes the excluded pairs' erf part) to out; mode 1
 // adds v's dipole field to out; mode 2 (PCG) subtracts it from out and writes

@@ -424,12 +424,19 @@ __device__ __forceinline__ void bspline_d3(double w, int p, double (*th)[kMaxOrd
 
 __global__ void k_pme_spread_mp(int64_t n, PmeGeom g, const double4* __restrict__ pos,
                                 const double4* __restrict__ pq4, const double4* __restrict__ mp,
-                                double* __restrict__ grid) {
+                                double* __restrict__ grid, const double4* __restrict__ ind) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double4 r = pos[i];
   const double q = pq4[i].z;
-  const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
+  double4 m0 = mp[3 * i];
+  const double4 m1 = mp[3 * i + 1];
+  if (ind) {  // + induced dipoles (the polarization forces' combined set)
+    const double4 u = ind[i];
+    m0.x += u.x;
+    m0.y += u.y;
+    m0.z += u.z;
+  }
   const double qzz = mp[3 * i + 2].x;
   const double s1 = g.k1 / g.l1, s2 = g.k2 / g.l2, s3 = g.k3 / g.l3;
   // operator coefficients in fractional derivatives
@@ -473,7 +480,9 @@ __global__ void __launch_bounds__(kBlock) k_pme_gather_mp(int64_t n, PmeGeom g,
                                                          double electric,
                                                          double4* __restrict__ force,
                                                          double4* __restrict__ torque,
-                                                         double* __restrict__ partials) {
+                                                         double* __restrict__ partials,
+                                                         const double4* __restrict__ ind,
+                                                         int write_forces) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double acc[1] = {0.0};
   if (i < n) {
@@ -540,7 +549,11 @@ __global__ void __launch_bounds__(kBlock) k_pme_gather_mp(int64_t n, PmeGeom g,
     const double txyz = s1 * s2 * s3 * fxyz;
     const double q = pq4[i].z;
     const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
-    const double dx = m0.x, dy = m0.y, dz = m0.z;
+    // forces act on the whole dipole (permanent + induced); torques only on
+    // the permanent one (induced dipoles are not attached to the frame)
+    const double4 u = ind ? ind[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const double dx = m0.x + u.x, dy = m0.y + u.y, dz = m0.z + u.z;
+    const double px = m0.x, py = m0.y, pz = m0.z;
     const double Qxx = m0.w, Qxy = m1.x, Qxz = m1.y, Qyy = m1.z, Qyz = m1.w,
                  Qzz = mp[3 * i + 2].x;
     acc[0] = 0.5 * electric *
@@ -553,24 +566,28 @@ __global__ void __launch_bounds__(kBlock) k_pme_gather_mp(int64_t n, PmeGeom g,
                       Qzz * tyzz + 2.0 * (Qxy * txyy + Qxz * txyz + Qyz * tyyz);
     const double Fz = q * g1z + hxz * dx + hyz * dy + hzz * dz + Qxx * txxz + Qyy * tyyz +
                       Qzz * tzzz + 2.0 * (Qxy * txyz + Qxz * txzz + Qyz * tyzz);
-    double4 f = force[i];
-    f.x -= electric * Fx;
-    f.y -= electric * Fy;
-    f.z -= electric * Fz;
-    force[i] = f;
+    if (write_forces) {
+      double4 f = force[i];
+      f.x -= electric * Fx;
+      f.y -= electric * Fy;
+      f.z -= electric * Fz;
+      force[i] = f;
+    }
     // tau = grad phi x mu + 2 (M_zy, M_xz, M_yx), M = Q H - H Q
-    double tx = g1y * dz - g1z * dy, ty = g1z * dx - g1x * dz, tz = g1x * dy - g1y * dx;
+    double tx = g1y * pz - g1z * py, ty = g1z * px - g1x * pz, tz = g1x * py - g1y * px;
     const double Mzy = (Qxz * hxy + Qyz * hyy + Qzz * hyz) - (hxz * Qxy + hyz * Qyy + hzz * Qyz);
     const double Mxz = (Qxx * hxz + Qxy * hyz + Qxz * hzz) - (hxx * Qxz + hxy * Qyz + hxz * Qzz);
     const double Myx = (Qxy * hxx + Qyy * hxy + Qyz * hxz) - (hxy * Qxx + hyy * Qxy + hyz * Qxz);
     tx += 2.0 * Mzy;
     ty += 2.0 * Mxz;
     tz += 2.0 * Myx;
-    double4 tq = torque[i];
-    tq.x += electric * tx;
-    tq.y += electric * ty;
-    tq.z += electric * tz;
-    torque[i] = tq;
+    if (write_forces) {
+      double4 tq = torque[i];
+      tq.x += electric * tx;
+      tq.y += electric * ty;
+      tq.z += electric * tz;
+      torque[i] = tq;
+    }
   }
   block_store_partials<1>(acc, partials);
 }
@@ -593,9 +610,86 @@ __global__ void __launch_bounds__(kBlock) k_pme_self_mp(int64_t n, const double4
   block_store_partials<3>(acc, partials);
 }
 
+// One multipole pair (i-side), the real-space kernels' closed form
+// (csrc/mpole.cu) with radial functions G[0..5]: energy U, g = dU/dR,
+// gm = dU/dd_i, GQ = dU/dQ_i (xx, xy, xz, yy, yz, zz).
+struct MpSite {
+  double q, dx, dy, dz, Q[6];
+};
+
+__device__ __forceinline__ double mp_pair(const MpSite& a, const MpSite& b, const double* G,
+                                          double x, double y, double z, double* g, double* gm,
+                                          double* GQ) {
+  auto qv = [](const double* Q, double u, double v, double w, double& ox, double& oy,
+               double& oz) {
+    ox = Q[0] * u + Q[1] * v + Q[2] * w;
+    oy = Q[1] * u + Q[3] * v + Q[4] * w;
+    oz = Q[2] * u + Q[4] * v + Q[5] * w;
+  };
+  const double qi = a.q, dix = a.dx, diy = a.dy, diz = a.dz;
+  const double qj = b.q, djx = b.dx, djy = b.dy, djz = b.dz;
+  const double* Qi = a.Q;
+  const double* Qj = b.Q;
+  double vix, viy, viz, vjx, vjy, vjz;
+  qv(Qi, x, y, z, vix, viy, viz);
+  qv(Qj, x, y, z, vjx, vjy, vjz);
+  const double dir = dix * x + diy * y + diz * z, djr = djx * x + djy * y + djz * z;
+  const double qir = x * vix + y * viy + z * viz, qjr = x * vjx + y * vjy + z * vjz;
+  const double dij = dix * djx + diy * djy + diz * djz;
+  const double diqj = dix * vjx + diy * vjy + diz * vjz;
+  const double djqi = djx * vix + djy * viy + djz * viz;
+  const double qiqj = Qi[0] * Qj[0] + Qi[3] * Qj[3] + Qi[5] * Qj[5] +
+                      2.0 * (Qi[1] * Qj[1] + Qi[2] * Qj[2] + Qi[4] * Qj[4]);
+  const double qvv = vix * vjx + viy * vjy + viz * vjz;
+  const double C0 = qi * qj, C1 = qi * djr - qj * dir + dij;
+  const double C2 = qi * qjr + qj * qir - dir * djr + 2.0 * (diqj - djqi + qiqj);
+  const double C3 = -dir * qjr + qir * djr - 4.0 * qvv, C4 = qir * qjr;
+  double a1x, a1y, a1z, a2x, a2y, a2z, b1x, b1y, b1z, b2x, b2y, b2z;
+  qv(Qj, dix, diy, diz, a1x, a1y, a1z);
+  qv(Qi, djx, djy, djz, a2x, a2y, a2z);
+  qv(Qi, vjx, vjy, vjz, b1x, b1y, b1z);
+  qv(Qj, vix, viy, viz, b2x, b2y, b2z);
+  const double s = C0 * G[1] + C1 * G[2] + C2 * G[3] + C3 * G[4] + C4 * G[5];
+  g[0] = G[1] * (qi * djx - qj * dix) +
+         G[2] * (2.0 * (qi * vjx + qj * vix) - djr * dix - dir * djx + 2.0 * (a1x - a2x)) +
+         G[3] * (-qjr * dix - 2.0 * dir * vjx + 2.0 * djr * vix + qir * djx - 4.0 * (b1x + b2x)) +
+         G[4] * 2.0 * (qjr * vix + qir * vjx) - s * x;
+  g[1] = G[1] * (qi * djy - qj * diy) +
+         G[2] * (2.0 * (qi * vjy + qj * viy) - djr * diy - dir * djy + 2.0 * (a1y - a2y)) +
+         G[3] * (-qjr * diy - 2.0 * dir * vjy + 2.0 * djr * viy + qir * djy - 4.0 * (b1y + b2y)) +
+         G[4] * 2.0 * (qjr * viy + qir * vjy) - s * y;
+  g[2] = G[1] * (qi * djz - qj * diz) +
+         G[2] * (2.0 * (qi * vjz + qj * viz) - djr * diz - dir * djz + 2.0 * (a1z - a2z)) +
+         G[3] * (-qjr * diz - 2.0 * dir * vjz + 2.0 * djr * viz + qir * djz - 4.0 * (b1z + b2z)) +
+         G[4] * 2.0 * (qjr * viz + qir * vjz) - s * z;
+  const double c1 = G[1] * qj + G[2] * djr + G[3] * qjr;
+  gm[0] = G[1] * djx + 2.0 * G[2] * vjx - c1 * x;
+  gm[1] = G[1] * djy + 2.0 * G[2] * vjy - c1 * y;
+  gm[2] = G[1] * djz + 2.0 * G[2] * vjz - c1 * z;
+  const double crr = G[2] * qj + G[3] * djr + G[4] * qjr, g2 = 2.0 * G[2], g3 = 2.0 * G[3];
+  GQ[0] = crr * x * x - G[2] * (2.0 * djx * x) + g2 * Qj[0] - g3 * (2.0 * x * vjx);
+  GQ[3] = crr * y * y - G[2] * (2.0 * djy * y) + g2 * Qj[3] - g3 * (2.0 * y * vjy);
+  GQ[5] = crr * z * z - G[2] * (2.0 * djz * z) + g2 * Qj[5] - g3 * (2.0 * z * vjz);
+  GQ[1] = crr * x * y - G[2] * (djx * y + x * djy) + g2 * Qj[1] - g3 * (x * vjy + vjx * y);
+  GQ[2] = crr * x * z - G[2] * (djx * z + x * djz) + g2 * Qj[2] - g3 * (x * vjz + vjx * z);
+  GQ[4] = crr * y * z - G[2] * (djy * z + y * djz) + g2 * Qj[4] - g3 * (y * vjz + vjy * z);
+  return C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4];
+}
+
+__device__ __forceinline__ MpSite mp_site(const double4* mp, const double4* pq4, int64_t i,
+                                          const double4* ind) {
+  const double4 m0 = mp[3 * i], m1 = mp[3 * i + 1];
+  const double4 u = ind ? ind[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+  return MpSite{pq4[i].z, m0.x + u.x, m0.y + u.y, m0.z + u.z,
+                {m0.w, m1.x, m1.y, m1.z, m1.w, mp[3 * i + 2].x}};
+}
+
 // Excluded (same-molecule) pairs: remove their erf(a r)/r-kernel multipole
 // interaction (B_n = bare - erfc). One thread per site over its partners:
 // i-side force and torque in full, energy halved (each pair seen twice).
+// With induced dipoles (ind != NULL, the polarization forces): the combined
+// set's interaction minus the induced-induced part (mutual induction keeps
+// every pair in real space), torques on the permanent multipoles only.
 __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, double alpha,
                                                            double electric,
                                                            const double4* __restrict__ pos,
@@ -605,15 +699,15 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
                                                            const int32_t* __restrict__ xl,
                                                            double4* __restrict__ force,
                                                            double4* __restrict__ torque,
-                                                           double* __restrict__ partials) {
+                                                           double* __restrict__ partials,
+                                                           const double4* __restrict__ ind,
+                                                           int write_forces) {
   double acc[1] = {0.0};
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
     const double4 pi = pos[i];
-    const double qi = pq4[i].z;
-    const double4 m0i = mp[3 * i], m1i = mp[3 * i + 1];
-    const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
-    const double Qi[6] = {m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, mp[3 * i + 2].x};
+    const MpSite si = mp_site(mp, pq4, i, ind);
+    const double4 m0i = mp[3 * i];
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
     for (int32_t k = xs[i]; k < xs[i + 1]; ++k) {
       const int32_t j = xl[k];
@@ -629,68 +723,34 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
         if (q > 0) bare *= (double)(2 * q - 1) * inv_r2;
         G[q] = electric * (bare - G[q]);  // erf kernel
       }
-      const double qj = pq4[j].z;
-      const double4 m0j = mp[3 * (size_t)j], m1j = mp[3 * (size_t)j + 1];
-      const double djx = m0j.x, djy = m0j.y, djz = m0j.z;
-      const double Qj[6] = {m0j.w, m1j.x, m1j.y, m1j.z, m1j.w, mp[3 * (size_t)j + 2].x};
-      auto qv = [](const double* Q, double a, double b, double c, double& ox, double& oy,
-                   double& oz) {
-        ox = Q[0] * a + Q[1] * b + Q[2] * c;
-        oy = Q[1] * a + Q[3] * b + Q[4] * c;
-        oz = Q[2] * a + Q[4] * b + Q[5] * c;
-      };
-      double vix, viy, viz, vjx, vjy, vjz;
-      qv(Qi, x, y, z, vix, viy, viz);
-      qv(Qj, x, y, z, vjx, vjy, vjz);
-      const double dir = dix * x + diy * y + diz * z, djr = djx * x + djy * y + djz * z;
-      const double qir = x * vix + y * viy + z * viz, qjr = x * vjx + y * vjy + z * vjz;
-      const double dij = dix * djx + diy * djy + diz * djz;
-      const double diqj = dix * vjx + diy * vjy + diz * vjz;
-      const double djqi = djx * vix + djy * viy + djz * viz;
-      const double qiqj = Qi[0] * Qj[0] + Qi[3] * Qj[3] + Qi[5] * Qj[5] +
-                          2.0 * (Qi[1] * Qj[1] + Qi[2] * Qj[2] + Qi[4] * Qj[4]);
-      const double qvv = vix * vjx + viy * vjy + viz * vjz;
-      const double C0 = qi * qj, C1 = qi * djr - qj * dir + dij;
-      const double C2 = qi * qjr + qj * qir - dir * djr + 2.0 * (diqj - djqi + qiqj);
-      const double C3 = -dir * qjr + qir * djr - 4.0 * qvv, C4 = qir * qjr;
-      acc[0] -= 0.5 * (C0 * G[0] + C1 * G[1] + C2 * G[2] + C3 * G[3] + C4 * G[4]);
-      double a1x, a1y, a1z, a2x, a2y, a2z, b1x, b1y, b1z, b2x, b2y, b2z;
-      qv(Qj, dix, diy, diz, a1x, a1y, a1z);
-      qv(Qi, djx, djy, djz, a2x, a2y, a2z);
-      qv(Qi, vjx, vjy, vjz, b1x, b1y, b1z);
-      qv(Qj, vix, viy, viz, b2x, b2y, b2z);
-      const double s = C0 * G[1] + C1 * G[2] + C2 * G[3] + C3 * G[4] + C4 * G[5];
-      const double gx = G[1] * (qi * djx - qj * dix) +
-                        G[2] * (2.0 * (qi * vjx + qj * vix) - djr * dix - dir * djx + 2.0 * (a1x - a2x)) +
-                        G[3] * (-qjr * dix - 2.0 * dir * vjx + 2.0 * djr * vix + qir * djx - 4.0 * (b1x + b2x)) +
-                        G[4] * 2.0 * (qjr * vix + qir * vjx) - s * x;
-      const double gy = G[1] * (qi * djy - qj * diy) +
-                        G[2] * (2.0 * (qi * vjy + qj * viy) - djr * diy - dir * djy + 2.0 * (a1y - a2y)) +
-                        G[3] * (-qjr * diy - 2.0 * dir * vjy + 2.0 * djr * viy + qir * djy - 4.0 * (b1y + b2y)) +
-                        G[4] * 2.0 * (qjr * viy + qir * vjy) - s * y;
-      const double gz = G[1] * (qi * djz - qj * diz) +
-                        G[2] * (2.0 * (qi * vjz + qj * viz) - djr * diz - dir * djz + 2.0 * (a1z - a2z)) +
-                        G[3] * (-qjr * diz - 2.0 * dir * vjz + 2.0 * djr * viz + qir * djz - 4.0 * (b1z + b2z)) +
-                        G[4] * 2.0 * (qjr * viz + qir * vjz) - s * z;
+      const MpSite sj = mp_site(mp, pq4, j, ind);
+      double g[3], gm[3], GQ[6];
+      const double u = mp_pair(si, sj, G, x, y, z, g, gm, GQ);
+      acc[0] -= 0.5 * u;
       // removing the pair: F_i += dU/dR (the pair force on i is -dU/dR)
-      fx += gx;
-      fy += gy;
-      fz += gz;
-      const double c1 = G[1] * qj + G[2] * djr + G[3] * qjr;
-      const double gmx = G[1] * djx + 2.0 * G[2] * vjx - c1 * x;
-      const double gmy = G[1] * djy + 2.0 * G[2] * vjy - c1 * y;
-      const double gmz = G[1] * djz + 2.0 * G[2] * vjz - c1 * z;
-      double ux = gmy * diz - gmz * diy, uy = gmz * dix - gmx * diz, uz = gmx * diy - gmy * dix;
-      const double crr = G[2] * qj + G[3] * djr + G[4] * qjr, g2 = 2.0 * G[2], g3 = 2.0 * G[3];
-      const double Hxx = crr * x * x - G[2] * (2.0 * djx * x) + g2 * Qj[0] - g3 * (2.0 * x * vjx);
-      const double Hyy = crr * y * y - G[2] * (2.0 * djy * y) + g2 * Qj[3] - g3 * (2.0 * y * vjy);
-      const double Hzz = crr * z * z - G[2] * (2.0 * djz * z) + g2 * Qj[5] - g3 * (2.0 * z * vjz);
-      const double Hxy = crr * x * y - G[2] * (djx * y + x * djy) + g2 * Qj[1] - g3 * (x * vjy + vjx * y);
-      const double Hxz = crr * x * z - G[2] * (djx * z + x * djz) + g2 * Qj[2] - g3 * (x * vjz + vjx * z);
-      const double Hyz = crr * y * z - G[2] * (djy * z + y * djz) + g2 * Qj[4] - g3 * (y * vjz + vjy * z);
-      const double Mzy = (Qi[2] * Hxy + Qi[4] * Hyy + Qi[5] * Hyz) - (Hxz * Qi[1] + Hyz * Qi[3] + Hzz * Qi[4]);
-      const double Mxz = (Qi[0] * Hxz + Qi[1] * Hyz + Qi[2] * Hzz) - (Hxx * Qi[2] + Hxy * Qi[4] + Hxz * Qi[5]);
-      const double Myx = (Qi[1] * Hxx + Qi[3] * Hxy + Qi[4] * Hxz) - (Hxy * Qi[0] + Hyy * Qi[1] + Hyz * Qi[2]);
+      fx += g[0];
+      fy += g[1];
+      fz += g[2];
+      if (ind) {  // keep the induced-induced part
+        const double4 ui = ind[i], uj = ind[j];
+        const MpSite a{0.0, ui.x, ui.y, ui.z, {0, 0, 0, 0, 0, 0}};
+        const MpSite b{0.0, uj.x, uj.y, uj.z, {0, 0, 0, 0, 0, 0}};
+        double h[3], hm[3], HQ[6];
+        mp_pair(a, b, G, x, y, z, h, hm, HQ);
+        fx -= h[0];
+        fy -= h[1];
+        fz -= h[2];
+      }
+      // torque on the permanent multipoles of i: gm x d_perm + quadrupole term
+      double ux = gm[1] * m0i.z - gm[2] * m0i.y, uy = gm[2] * m0i.x - gm[0] * m0i.z,
+             uz = gm[0] * m0i.y - gm[1] * m0i.x;
+      const double* Qi = si.Q;
+      const double Mzy = (Qi[2] * GQ[1] + Qi[4] * GQ[3] + Qi[5] * GQ[4]) -
+                         (GQ[2] * Qi[1] + GQ[4] * Qi[3] + GQ[5] * Qi[4]);
+      const double Mxz = (Qi[0] * GQ[2] + Qi[1] * GQ[4] + Qi[2] * GQ[5]) -
+                         (GQ[0] * Qi[2] + GQ[1] * Qi[4] + GQ[2] * Qi[5]);
+      const double Myx = (Qi[1] * GQ[0] + Qi[3] * GQ[1] + Qi[4] * GQ[2]) -
+                         (GQ[1] * Qi[0] + GQ[3] * Qi[1] + GQ[4] * Qi[2]);
       ux += 2.0 * Mzy;
       uy += 2.0 * Mxz;
       uz += 2.0 * Myx;
@@ -698,16 +758,18 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
       ty -= uy;
       tz -= uz;
     }
-    double4 f = force[i];
-    f.x += fx;
-    f.y += fy;
-    f.z += fz;
-    force[i] = f;
-    double4 t = torque[i];
-    t.x += tx;
-    t.y += ty;
-    t.z += tz;
-    torque[i] = t;
+    if (write_forces) {
+      double4 f = force[i];
+      f.x += fx;
+      f.y += fy;
+      f.z += fz;
+      force[i] = f;
+      double4 t = torque[i];
+      t.x += tx;
+      t.y += ty;
+      t.z += tz;
+      torque[i] = t;
+    }
   }
   block_store_partials<1>(acc, partials);
 }
@@ -716,33 +778,36 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
 // the gathered potentials (check), 104-106 sums of q^2, |mu|^2, Q:Q for the
 // self energy (formed on the host); force / torque ADDED to
 void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
-                   double electric, bool exclude) {
-  pme_setup(c, k1, k2, k3, order);
-  PmeState* s = (PmeState*)c->pme;
+                   double electric, bool exclude, const double4* ind, bool forces) {
+  // the combined-set pass runs on the main stream after the solve: own state
+  PmeState* s = pme_state(c, ind ? &c->pme_pol : &c->pme, k1, k2, k3, order);
   const PmeGeom g{k1, k2, k3, order, c->lx, c->ly, c->lz};
   const int64_t n = c->n;
+  const int wf = forces ? 1 : 0;
   MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)k1 * k2 * k3 * sizeof(double), c->stream));
   MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos, c->pq4,
-             c->mp, s->grid);
+             c->mp, s->grid, ind);
   cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
   const int64_t total = (int64_t)k1 * k2 * (k3 / 2 + 1);
   const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
   ensure_partials(c, std::max<int64_t>(blocks, grid_for(n)));
   MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, alpha, s->bmod,
-             s->spec, c->partials);
-  finalize_partials(c, blocks, 1, 80, electric);
+             s->spec, ind ? (double*)nullptr : c->partials);
+  if (!ind) finalize_partials(c, blocks, 1, 80, electric);
   cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
   MDG_LAUNCH(c, "pme_gather_mp", grid_for(n), kBlock, 0, k_pme_gather_mp, n, g, c->pos, c->pq4,
-             c->mp, s->grid, electric, c->force, c->torque, c->partials);
-  finalize_partials(c, grid_for(n), 1, 98, 1.0);
-  MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
-             c->partials);
-  finalize_partials(c, grid_for(n), 3, 104, 1.0);  // 104 q^2, 105 mu^2, 106 Q:Q (host combines)
+             c->mp, s->grid, electric, c->force, c->torque, c->partials, ind, wf);
+  if (!ind) {
+    finalize_partials(c, grid_for(n), 1, 98, 1.0);
+    MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
+               c->partials);
+    finalize_partials(c, grid_for(n), 3, 104, 1.0);  // 104 q^2, 105 mu^2, 106 Q:Q (host combines)
+  }
   if (exclude && c->has_mol && c->excl_start) {
     MDG_LAUNCH(c, "pme_excluded_mp", grid_for(n), kBlock, 0, k_pme_excluded_mp, n,
                make_box(c->lx, c->ly, c->lz), alpha, electric, c->pos, c->pq4, c->mp,
-               c->excl_start, c->excl, c->force, c->torque, c->partials);
-    finalize_partials(c, grid_for(n), 1, 88, 1.0);
+               c->excl_start, c->excl, c->force, c->torque, c->partials, ind, wf);
+    if (!ind) finalize_partials(c, grid_for(n), 1, 88, 1.0);
   }
 }
 
@@ -906,7 +971,7 @@ void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out) {
                                  c->stream));
   if (mode == 0)
     MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos,
-               c->pq4, c->mp, s->grid);
+               c->pq4, c->mp, s->grid, (const double4*)nullptr);
   else
     MDG_LAUNCH(c, "pme_spread_dip", grid_for(n, 128), 128, 0, k_pme_spread_dip, n, g, c->pos,
                v, s->grid, c->results, mode == 2 ? 1 : 0);

@@ -1023,6 +1023,50 @@ def test_amoeba_step_with_reciprocal_space(engine, oracle, mdg):
     assert rel(e[2], -0.5 * mdg.ELECTRIC * float(np.sum(mu_o * e_o))) <= 1e-7
 
 
+def test_polar_forces_with_reciprocal_space_by_fd(engine, oracle, mdg):
+    """Multipole + polarization forces with reciprocal space (the permanent +
+    induced set's PME pass after the solve) == -dE/dx of the oracle's full
+    Ewald energy E_mpole + E_pol (dense solve re-done at every displaced
+    geometry: the variational polarization energy)."""
+    from oracle import ewald_mpole as em
+    from oracle.oracle import FastPort
+    s = mdg.water_box(27, 10.2, 7, "amoeba")
+    a = 0.5446
+    fp = FastPort()
+
+    def energy(x):
+        q = mdg.water_box(27, 10.2, 7, "amoeba")
+        q.x, q.y, q.z = x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy()
+        so = to_oracle_system(q)
+        e_real = fp.mpole(so, oracle.build_table(so, 5.0), a, 5.0, mdg.ELECTRIC, True)[2]
+        e_rec = em.recip(x, q.charge, q.dipole, q.quadrupole, q.box, a, (10, 10, 10),
+                         mdg.ELECTRIC, energy_only=True)[0]
+        e_ex = em.excluded_correction(x, q.charge, q.dipole, q.quadrupole, q.box, q.molecule,
+                                      a, mdg.ELECTRIC, pair=em.mpole_pair)[0]
+        mu, e_full = _full_ewald_polar_oracle(oracle, q, a, 5.0)
+        return e_real + e_rec + e_ex - 0.5 * mdg.ELECTRIC * float(np.sum(mu * e_full))
+
+    engine.upload_system(s)
+    te = engine.build_neighbor_table(5.0, list_id=0)
+    p = mdg.AmoebaParams(4.5, 0.07, 0.12, 5.0, a, mdg.ELECTRIC, 0.39, 1e-10, 300, 1,
+                         mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE)
+    engine.set_ewald_recip((48, 48, 48), 10)
+    try:
+        engine.amoeba_step(te, te, p)
+        f = engine.fetch_forces()
+    finally:
+        engine.set_ewald_recip((0, 0, 0))
+    x0 = np.stack([s.x, s.y, s.z], 1)
+    h = 1e-4
+    fmax = np.abs(f).max()
+    for i, k in ((0, 0), (10, 1), (41, 2), (70, 0)):
+        xp, xm = x0.copy(), x0.copy()
+        xp[i, k] += h
+        xm[i, k] -= h
+        num = -(energy(xp) - energy(xm)) / (2 * h)
+        assert abs(f[i, k] - num) <= 1e-6 * fmax, (i, k, f[i, k], num)
+
+
 def test_full_ewald_is_alpha_independent(engine, oracle, mdg):
     """Real space (device kernel) + PME + self + excluded pairs: the same
     total energy and forces for two splitting parameters."""
