@@ -54,6 +54,8 @@ def parse():
                     help="skip the extra timing of device-resident MD steps")
     ap.add_argument("--no-polar-forces", action="store_true",
                     help="skip the extra timing of the step with polarization forces")
+    ap.add_argument("--no-recip", action="store_true",
+                    help="skip the extra timing of the step with reciprocal-space Ewald")
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
 
@@ -176,6 +178,19 @@ class Workload:
         if kernel in PER_PAIR_FLOPS:
             return "fp64", PER_PAIR_FLOPS[kernel] * directed / 2.0
         return "hbm", stream_bytes(kernel, self.n, directed)
+
+
+def fft_size(x: float) -> int:
+    """Smallest 2^a 3^b 5^c >= x (cuFFT-friendly grid)."""
+    n = max(8, int(np.ceil(x)))
+    while True:
+        k = n
+        for p in (2, 3, 5):
+            while k % p == 0:
+                k //= p
+        if k == 1:
+            return n
+        n += 1
 
 
 def hbm_peak():
@@ -446,6 +461,30 @@ def run_mine(args, world, rank, local):
                         "value": world * wl.n * args.steps / (pms * 1e-3),
                         "unit": "atom-steps/s", "ms_per_step": pms / args.steps}
 
+    # ---- 8(f)#3 extension, beside the headline: the same step with full
+    # Ewald (reciprocal space for the multipoles and inside the PCG)
+    with_recip = None
+    if getattr(wl.p, "terms", 0) & m_.TERM_POLAR and not args.no_recip:
+        grid = fft_size(wl.c["box"] / 1.0)
+        eng.set_ewald_recip((grid, grid, grid), 5)
+        try:
+            wl.step()
+            wl.rebuild()
+            if barrier:
+                barrier()
+            eng.synchronize()
+            eng.timer_start()
+            wl.run(args.steps)
+            rms_ = eng.timer_stop()
+            er, _, ir, _ = eng.fetch_energies()
+        finally:
+            eng.set_ewald_recip((0, 0, 0))
+        with_recip = {"what": f"same step + reciprocal-space Ewald (smooth PME {grid}^3, order 5: "
+                              "multipole energy/forces/torques, the PCG right-hand side and "
+                              "operator)", "value": world * wl.n * args.steps / (rms_ * 1e-3),
+                      "unit": "atom-steps/s", "ms_per_step": rms_ / args.steps,
+                      "pcg_iters": int(ir), "energies_kcal_mol": [float(v) for v in er[:3]]}
+
     # ---- 8(f)#4 extension, beside the headline: the same forces driving
     # device-resident MD (velocity Verlet, flexible water bonds/angles,
     # 0.5 fs, 300 K start); last, as it moves the engine's coordinates
@@ -476,6 +515,7 @@ def run_mine(args, world, rank, local):
                    "l2": "inputs larger than L2 (lists > 126 MB)"},
         "e2e": e2e,
         "with_polar_forces": polar_forces,
+        "with_ewald_recip": with_recip,
         "md": md,
         "gpu_launches": launches,
         "roofline": roof,
