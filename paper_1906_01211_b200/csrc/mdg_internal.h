@@ -73,6 +73,7 @@ struct DevList {
     size_t elems = 0;
     double4* ref = nullptr;       // site positions at the cut
     int32_t* flag = nullptr;      // device: 1 = cut again (motion), 2 = forced (new list)
+    int32_t* gen = nullptr;       // device: cuts done (the cluster unions' staleness test)
     // cuts done, counted by the cut kernel in mapped page-locked memory (read
     // by the host without a sync): when most calls need a new cut (sites
     // moving fast), the buffer only adds a pass, so the rows are bypassed
@@ -96,15 +97,19 @@ struct PrunedList {
   size_t elems = 0;
   int64_t directed = 0;
   bool sorted = false;  // rows ascending in (j & 0x7fffffff) (source sorted)
-  // site clusters (cluster.cu): per cluster of 8 consecutive sites the sorted
-  // union of their rows, j | membership mask << 24; ucnt = entries | wide << 31
+  // site clusters (cluster.cu): per cluster of 4 consecutive sites the sorted
+  // union of their inner rows, rebuilt when those rows are cut again
   bool cl_valid = false;
   int64_t ncl = 0;
   int32_t ucap = 0;
-  uint32_t* ucl = nullptr;
+  int32_t* ucl = nullptr;
   int32_t* ucnt = nullptr;
+  int32_t* ugen = nullptr;  // device: inner-row generation the unions were built from
   size_t uelems = 0;
   int64_t ucnt_elems = 0;
+  double ucut = 0.0;
+  uintptr_t ukey[3] = {0, 0, 0};
+  bool ubuilt = false;  // the union buffers hold the unions of the keyed rows
 };
 
 // arguments of the cluster mat-vec (cluster.cu)
@@ -114,12 +119,13 @@ struct CLArgs {
   int ipw;      // clusters per block (MDG_LAUNCH_SITES)
   const double4* __restrict__ pos;
   const double2* __restrict__ polp;
-  const uint32_t* __restrict__ ucl;
+  const int32_t* __restrict__ ucl;
   const int32_t* __restrict__ ucnt;
   int32_t ucap;
   const double2* __restrict__ trr;
   int32_t pcap;
   Box b;
+  double c2;  // the pruned rows' cutoff^2 (their predicate, replayed per pair)
   const double4* __restrict__ in;
   double4* __restrict__ out;
   double* __restrict__ partials;
@@ -436,9 +442,10 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
 // the permanent field into c->eperm.
 void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
                     int exclude);
-// Cluster unions of the pruned rows (cluster.cu); false when the cluster
-// mat-vec does not apply (unsorted rows, >= 2^24 sites, MDG_CLUSTER_MATVEC=0).
-bool build_clusters(mdg_ctx* c, double cutoff);
+// Cluster unions of the rows k_perm_field<TPRE> walked (cluster.cu), rebuilt
+// on the device when `gen` (the rows' cut generation) moved; leaves
+// plist.cl_valid false when the cluster mat-vec does not apply
+void build_clusters(mdg_ctx* c, double cutoff, const struct ListView& rows, const int32_t* gen);
 CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out);
 const void* cl_matvec_kernel(bool pcg);
 void cl_matvec_launch(mdg_ctx* c, CLArgs& k, bool pcg, const char* name);

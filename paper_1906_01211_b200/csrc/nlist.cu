@@ -628,6 +628,7 @@ struct CutArgs {
   double4* __restrict__ ref;
   const int32_t* __restrict__ flag;
   int32_t* __restrict__ cuts;  // mapped host counter
+  int32_t* __restrict__ gen;   // device cut generation
   double* __restrict__ partials;  // unused (launch macro contract)
 };
 
@@ -639,6 +640,7 @@ __global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid == 0 && *a.flag == 1) atomicAdd_system(a.cuts, 1);  // motion cuts only (2: forced)
+  if (tid == 0) atomicAdd(a.gen, 1);  // every cut: the rows' generation
   for (int64_t s = tid; s < a.n_all; s += (int64_t)gridDim.x * blockDim.x) a.ref[s] = a.P[s];
   MDG_SITE_LOOP(i, a.n_rows, a.ipw) {
     const double4 pi = a.P[i];
@@ -710,6 +712,10 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   if (!I.cnt) MDG_CUDA_CHECK(cudaMalloc(&I.cnt, (size_t)c->n_cap * sizeof(int32_t)));
   if (!I.ref) MDG_CUDA_CHECK(cudaMalloc(&I.ref, (size_t)c->n_cap * sizeof(double4)));
   if (!I.flag) MDG_CUDA_CHECK(cudaMalloc(&I.flag, sizeof(int32_t)));
+  if (!I.gen) {
+    MDG_CUDA_CHECK(cudaMalloc(&I.gen, sizeof(int32_t)));
+    MDG_CUDA_CHECK(cudaMemsetAsync(I.gen, 0, sizeof(int32_t), c->stream));
+  }
   const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
   const bool stale = I.src_version != L.version || I.rc != rcut;
   if (stale) {
@@ -736,6 +742,7 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   k.ref = I.ref;
   k.flag = I.flag;
   k.cuts = I.dcuts;
+  k.gen = I.gen;
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
   // the cut rows are short: sort them (bucketed by length), when cut
   const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);

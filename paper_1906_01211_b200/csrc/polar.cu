@@ -346,7 +346,7 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
       P.cutoff = cutoff;
       P.directed = (int64_t)c->h_results[63];
       debug_check_rows(c, "pruned", P.nbr, P.cnt, P.cap, n, c->n, P.sorted);
-      build_clusters(c, cutoff);
+      build_clusters(c, cutoff, k.L, k.L.dense ? L.inner.gen : nullptr);
       return;
     }
     cap = (mx + 31) & ~31;

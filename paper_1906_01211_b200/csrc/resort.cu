@@ -222,6 +222,7 @@ void resort_sites(mdg_ctx* c) {
   }
   c->plist.valid = false;
   c->plist.cl_valid = false;
+  c->plist.ubuilt = false;
   c->fout_seq = 0;
 }
 
