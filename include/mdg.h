@@ -276,20 +276,39 @@ typedef struct {
   int elec_list, vdw_list;              /* list ids (vdw_list: AMOEBA only) */
   double elec_list_cutoff, vdw_list_cutoff;
   int bonded;            /* add the uploaded bonded terms */
+  /* integrator (zero-initialised fields keep velocity Verlet) */
+  int integrator;        /* MDG_INTEGRATOR_VERLET or MDG_INTEGRATOR_BAOAB_RESPA */
+  int inner_steps;       /* BAOAB-RESPA: bonded sub-steps per outer step (>= 1) */
+  double friction_ps;    /* BAOAB-RESPA: Langevin friction (1/ps); 0 = NVE RESPA */
+  double temperature_k;  /* BAOAB-RESPA: bath temperature (K) */
+  uint64_t seed;         /* BAOAB-RESPA: noise stream (counter-based, per caller site) */
 } mdg_md_params;
 
-/* nsteps of velocity Verlet on the device (single domain): kick, drift
- * (positions wrapped into the box), lists rebuilt on schedule, forces of
- * the selected model (+ bonded), kick. ekin / epot (kcal/mol, NULL to skip)
- * receive each step's kinetic / potential energy; the AMOEBA model needs
- * MDG_TERM_POLAR_FORCE with polarization for conservative dynamics. */
+#define MDG_INTEGRATOR_VERLET 0
+#define MDG_INTEGRATOR_BAOAB_RESPA 1
+
+/* nsteps on the device (single domain).
+ * Velocity Verlet: kick, drift (positions wrapped into the box), lists
+ * rebuilt on schedule, forces of the selected model (+ bonded), kick.
+ * BAOAB-RESPA (the multi-timestep Langevin scheme of the paper's Rel2,
+ * /root/reference/PAPER.md:782-783, two levels): the nonbonded model is the
+ * outer level at dt_fs, the bonded terms the inner level at
+ * dt_fs / inner_steps:
+ *   B_out(dt/2) [ B_in(h/2) A(h/2) O(h) A(h/2) F_in B_in(h/2) ] x inner_steps
+ *   F_out B_out(dt/2)
+ * with O: v = c1 v + sqrt((1 - c1^2) kT / m) xi, c1 = exp(-friction h), xi
+ * a SplitMix64/Box-Muller deviate of (seed, inner-step counter, caller site,
+ * component). ekin / epot (kcal/mol, NULL to skip) receive each step's
+ * kinetic / potential energy; the AMOEBA model needs MDG_TERM_POLAR_FORCE
+ * with polarization for conservative dynamics. */
 int mdg_md_run(mdg_ctx* ctx, const mdg_md_params* p, const mdg_charmm_params* charmm,
                const mdg_amoeba_params* amoeba, double* ekin, double* epot);
 
 /* Spatial re-sort on the device: the sites are re-keyed by their current
  * ~2 A Morton cells and every per-site array is permuted (index arrays
  * remapped), restoring the gathers' locality after the sites have moved.
- * mdg_md_run does it at every list rebuild (MDG_RESORT=0 disables). The
+ * mdg_md_run does it at every 20th list rebuild, counted across calls
+ * (MDG_RESORT=k: every k-th; 0 disables). The
  * caller-order interface is unchanged; neighbour lists are invalidated
  * (rebuild them). Single domain only. */
 int mdg_resort(mdg_ctx* ctx);
@@ -355,6 +374,8 @@ int mdg_group_create_local(mdg_group** out, int n, mdg_ctx** ctxs, int64_t n_glo
 int mdg_group_create_nccl(mdg_group** out, mdg_ctx* ctx, int rank, int size, const void* id128,
                           int64_t n_global);
 int mdg_group_destroy(mdg_group* g);
+/* mdg_ctx_destroy of a grouped context fails with MDG_CONTRACT: destroy the
+ * group first. */
 /* LOCAL halo of domain `domain`: for each of its n_halo halo sites (caller-
  * order local index halo_site[k]) the owning domain src_domain[k] and the
  * site's caller-order local index there, src_site[k]. */

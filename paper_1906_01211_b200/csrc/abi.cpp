@@ -296,12 +296,16 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
 
 int mdg_ctx_destroy(mdg_ctx* c) {
   if (!c) return MDG_OK;
+  if (c->group) {  // the group still references this context (and owns its stream)
+    mdg::set_error("mdg_ctx_destroy: context is in a domain group; call mdg_group_destroy first");
+    return MDG_CONTRACT;
+  }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
   void* ptrs[] = {c->d_perm, c->d_iperm, c->d_idx, c->pos, c->vsite, c->vdwp, c->vtype, c->vtab, c->ptab, c->polp, c->mol, c->hpar, c->hfac,
                   c->child_start, c->child, c->mp, c->frame, c->mploc, c->fbuf, c->fref_start,
-                  c->excl_start, c->excl, c->vel, c->bond_ij, c->bond_par, c->angle_ijk,
+                  c->excl_start, c->excl, c->vel, c->fbond, c->bond_ij, c->bond_par, c->angle_ijk,
                   c->angle_par,
                   c->fref, c->cell_of, c->cell_start, c->cell_fill,
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
@@ -1306,6 +1310,16 @@ int mdg_amoeba_step(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_pa
 
 static void energies_of(mdg_ctx* c, double* e4, double* w9);
 
+// reciprocal, self and excluded-pair multipole terms of the last AMOEBA step
+// (host results already fetched)
+static double recip_energy(const mdg_ctx* c) {
+  if (!c->recip_in_step) return 0.0;
+  const double* r = c->h_results;
+  const double a = c->pol_recip.alpha, a2 = a * a;
+  return r[80] + r[88] - c->pol_recip.electric * a / std::sqrt(M_PI) *
+                             (r[104] + 2.0 / 3.0 * a2 * r[105] + 8.0 / 5.0 * a2 * a2 * r[106]);
+}
+
 int mdg_group_amoeba_step(mdg_group* g, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
   return guard([&] {
     need(g != nullptr, "group: null");
@@ -1511,46 +1525,94 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
       }
     } nfo{c, {c->fout[0], c->fout[1], c->fout[2]}};
     for (int a = 0; a < 3; ++a) c->fout[a] = nullptr;
-    // re-sort the sites by their current cells at every rebuild (the
-    // gathers keep their locality as molecules diffuse); MDG_RESORT=0 off
-    static const int resort = mdg::env_int("MDG_RESORT", 1);
+    // re-sort the sites by their current cells every MDG_RESORT-th list
+    // rebuild (the gathers keep their locality as molecules diffuse: water
+    // moves ~1 A per ps, the sort cells are 2 A; 0 = never). The default 20
+    // is every 200 fs at the usual 10 fs between rebuilds; a re-sort costs
+    // about a third of a config-4 step.
+    const int resort = mdg::env_int("MDG_RESORT", 20);
     auto rebuild = [&] {
-      if (resort) mdg::resort_sites(c);
+      // counted across mdg_md_run calls (a trajectory run in chunks)
+      if (resort > 0 && ++c->md_rebuilds % resort == 0) mdg::resort_sites(c);
       mdg::nlist_build(c, p->elec_list, p->elec_list_cutoff, MDG_SITES_ATOMIC);
       if (p->model == 1) mdg::nlist_build(c, p->vdw_list, p->vdw_list_cutoff, MDG_SITES_VDW);
     };
     double e_nb = 0.0;
-    auto forces = [&] {
+    auto forces = [&](bool with_bonded) {
       if (p->model == 0) {
         mdg::NonpolarArgs a{1, 1, cp->shift, cp->exclude, cp->cutoff, cp->alpha, cp->electric};
         mdg::run_nonpolar(c, p->elec_list, a);
       } else {
         amoeba_step_impl(c, p->vdw_list, p->elec_list, ap);
       }
-      if (p->bonded) {
+      if (with_bonded) {
         MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 100, 0, 2 * sizeof(double), c->stream));
         mdg::run_bonded(c);
       }
     };
     auto potential = [&] {
       const double* r = c->h_results;
-      e_nb = (p->model == 0) ? r[0] + r[1] : r[0] + r[10] + r[40];
+      e_nb = (p->model == 0) ? r[0] + r[1] : r[0] + r[10] + r[40] + recip_energy(c);
       return e_nb + (p->bonded ? r[100] + r[101] : 0.0);
     };
-    const double dt = p->dt_fs;
-    rebuild();
-    forces();
-    for (int64_t s = 0; s < p->nsteps; ++s) {
-      mdg::run_kick(c, 0.5 * dt);
-      mdg::run_drift(c, dt);
-      if ((s + 1) % p->rebuild_every == 0) rebuild();
-      forces();
-      mdg::run_kick(c, 0.5 * dt);
+    auto report = [&](int64_t s) {
       if (ekin || epot) {
         mdg::run_kinetic(c);
         mdg::fetch_results(c);
         if (ekin) ekin[s] = c->h_results[102];
         if (epot) epot[s] = potential();
+      }
+    };
+    const double dt = p->dt_fs;
+    if (p->integrator == MDG_INTEGRATOR_VERLET) {
+      rebuild();
+      forces(p->bonded);
+      for (int64_t s = 0; s < p->nsteps; ++s) {
+        mdg::run_kick(c, 0.5 * dt);
+        mdg::run_drift(c, dt);
+        if ((s + 1) % p->rebuild_every == 0) rebuild();
+        forces(p->bonded);
+        mdg::run_kick(c, 0.5 * dt);
+        report(s);
+      }
+    } else {
+      // BAOAB-RESPA: c->force holds the outer (nonbonded) forces, c->fbond
+      // the inner (bonded) ones
+      need(p->integrator == MDG_INTEGRATOR_BAOAB_RESPA, "md: unknown integrator");
+      need(p->inner_steps >= 1, "md: BAOAB-RESPA needs inner_steps >= 1");
+      need(p->friction_ps >= 0 && p->temperature_k >= 0, "md: negative friction or temperature");
+      if (!c->fbond) MDG_CUDA_CHECK(cudaMalloc(&c->fbond, (size_t)c->n_cap * sizeof(double4)));
+      const bool bonded = p->bonded && (c->nbonds > 0 || c->nangles > 0);
+      auto inner_forces = [&] {
+        MDG_CUDA_CHECK(cudaMemsetAsync(c->fbond, 0, (size_t)c->n * sizeof(double4), c->stream));
+        MDG_CUDA_CHECK(cudaMemsetAsync(c->results + 100, 0, 2 * sizeof(double), c->stream));
+        if (bonded) mdg::run_bonded(c, c->fbond);
+      };
+      const double h = dt / p->inner_steps;
+      const double c1 = std::exp(-p->friction_ps * 1e-3 * h);
+      const double kt = 0.0019872041 * p->temperature_k;  // kcal/mol
+      const bool langevin = p->friction_ps > 0;
+      rebuild();
+      forces(false);  // the bonded terms are the inner level
+      inner_forces();
+      uint64_t counter = 0;
+      for (int64_t s = 0; s < p->nsteps; ++s) {
+        mdg::run_kick(c, 0.5 * dt);
+        for (int k = 0; k < p->inner_steps; ++k) {
+          mdg::run_kick(c, 0.5 * h, c->fbond);
+          mdg::run_drift(c, 0.5 * h);
+          if (langevin) mdg::run_ostep(c, c1, kt, p->seed, counter++);
+          mdg::run_drift(c, 0.5 * h);
+          inner_forces();
+          mdg::run_kick(c, 0.5 * h, c->fbond);
+        }
+        if ((s + 1) % p->rebuild_every == 0) {
+          rebuild();
+          inner_forces();  // a re-sort permuted the sites under c->fbond
+        }
+        forces(false);  // the bonded terms are the inner level
+        mdg::run_kick(c, 0.5 * dt);
+        report(s);
       }
     }
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -1659,11 +1721,7 @@ static void energies_of(mdg_ctx* c, double* e4, double* w9) {
   const bool amoeba = c->pcg_iters != 0;
   e4[0] = r[0];
   e4[1] = amoeba ? r[10] : r[1];
-  if (amoeba && c->recip_in_step) {  // + reciprocal, self and excluded-pair terms
-    const double a = c->pol_recip.alpha, a2 = a * a;
-    e4[1] += r[80] + r[88] - c->pol_recip.electric * a / std::sqrt(M_PI) *
-                                 (r[104] + 2.0 / 3.0 * a2 * r[105] + 8.0 / 5.0 * a2 * a2 * r[106]);
-  }
+  if (amoeba) e4[1] += recip_energy(c);
   e4[2] = amoeba ? r[40] : 0.0;
   e4[3] = 0.0;
   for (int k = 0; k < 9; ++k)

@@ -1,7 +1,10 @@
 // md.cu -- the MD time loop around the force kernels:
-// harmonic bonded terms for flexible molecules and a device-resident
-// velocity-Verlet integrator (kick / drift / kick), so a trajectory runs
-// without host round trips for coordinates.
+// harmonic bonded terms for flexible molecules and the device-resident
+// integrator steps -- kick (B), drift (A) and the Langevin velocity update
+// (O) -- that mdg_md_run composes into velocity Verlet or a two-level
+// BAOAB-RESPA (the multi-timestep scheme of /root/reference/PAPER.md:782-783,
+// bonded terms in the inner level), so a trajectory runs without host round
+// trips for coordinates.
 //
 // Units: kcal/mol, A, amu, fs. a = F/m * kAccel with kAccel = 4.184e-4
 // (1 kcal/mol = 4.184e-4 amu A^2 / fs^2). Bond energy k (r - r0)^2, angle
@@ -93,6 +96,38 @@ __global__ void k_kick(int64_t n, double hdt, const double4* __restrict__ force,
   vel[i] = v;
 }
 
+// Counter-based normal deviates for the Langevin O step, reproducible on the
+// host (oracle/md.py restates them): SplitMix64 of (seed, step counter,
+// caller site id, component) -> two 32-bit uniforms -> Box-Muller.
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ double gauss(uint64_t key) {
+  const uint64_t h = splitmix64(key);
+  const double u1 = (double)((h >> 32) + 1) * 0x1p-32;  // (0, 1]
+  const double u2 = (double)(h & 0xffffffffull) * 0x1p-32;
+  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+// O: v = c1 v + c2 sqrt(kT/m) xi (kt_acc = kB T * kAccel; vel.w = 1/m)
+__global__ void k_ostep(int64_t n, double c1, double c2, double kt_acc, uint64_t seed,
+                        uint64_t counter, const int32_t* __restrict__ perm,
+                        double4* __restrict__ vel) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double4 v = vel[i];
+  const double s = c2 * sqrt(kt_acc * v.w);
+  const uint64_t base = splitmix64(seed + splitmix64(counter)) + 3ull * (uint64_t)perm[i];
+  v.x = c1 * v.x + s * gauss(base);
+  v.y = c1 * v.y + s * gauss(base + 1);
+  v.z = c1 * v.z + s * gauss(base + 2);
+  vel[i] = v;
+}
+
 __device__ __forceinline__ double wrap_box(double p, double L) {
   p -= L * floor(p / L);
   return (p >= L || p < 0.0) ? 0.0 : p;
@@ -125,23 +160,33 @@ __global__ void __launch_bounds__(kBlock) k_kinetic(int64_t n, const double4* __
 }
 
 // results: 100 bond energy, 101 angle energy, 102 kinetic energy
-void run_bonded(mdg_ctx* c) {
+void run_bonded(mdg_ctx* c) { run_bonded(c, c->force); }
+
+void run_bonded(mdg_ctx* c, double4* out) {
   const Box b = make_box(c->lx, c->ly, c->lz);
   ensure_partials(c, std::max(grid_for(c->nbonds), grid_for(c->nangles)));
   if (c->nbonds > 0) {
     MDG_LAUNCH(c, "bonds", grid_for(c->nbonds), kBlock, 0, k_bonds, c->nbonds, b, c->pos,
-               c->bond_ij, c->bond_par, c->force, c->partials);
+               c->bond_ij, c->bond_par, out, c->partials);
     finalize_partials(c, grid_for(c->nbonds), 1, 100, 1.0);
   }
   if (c->nangles > 0) {
     MDG_LAUNCH(c, "angles", grid_for(c->nangles), kBlock, 0, k_angles, c->nangles, b, c->pos,
-               c->angle_ijk, c->angle_par, c->force, c->partials);
+               c->angle_ijk, c->angle_par, out, c->partials);
     finalize_partials(c, grid_for(c->nangles), 1, 101, 1.0);
   }
 }
 
-void run_kick(mdg_ctx* c, double half_dt) {
-  MDG_LAUNCH(c, "kick", grid_for(c->n, 256), 256, 0, k_kick, c->n, half_dt, c->force, c->vel);
+void run_kick(mdg_ctx* c, double half_dt) { run_kick(c, half_dt, c->force); }
+
+void run_kick(mdg_ctx* c, double half_dt, const double4* force) {
+  MDG_LAUNCH(c, "kick", grid_for(c->n, 256), 256, 0, k_kick, c->n, half_dt, force, c->vel);
+}
+
+void run_ostep(mdg_ctx* c, double c1, double kt, uint64_t seed, uint64_t counter) {
+  MDG_LAUNCH(c, "ostep", grid_for(c->n, 256), 256, 0, k_ostep, c->n, c1,
+             std::sqrt(std::max(0.0, 1.0 - c1 * c1)), kt * kAccel, seed, counter, c->d_perm,
+             c->vel);
 }
 
 void run_drift(mdg_ctx* c, double dt) {

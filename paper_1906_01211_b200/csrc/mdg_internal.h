@@ -226,6 +226,8 @@ struct mdg_ctx {
   bool recip_in_step = false;  // last AMOEBA step added the multipole PME terms
   // MD (md.cu): velocities (w = 1/mass) and harmonic bonded terms
   double4* vel = nullptr;
+  double4* fbond = nullptr;  // inner-level (bonded) forces of BAOAB-RESPA
+  int64_t md_rebuilds = 0;   // list rebuilds inside mdg_md_run (re-sort cadence)
   bool has_vel = false;
   int2* bond_ij = nullptr;
   double2* bond_par = nullptr;  // (k, r0)
@@ -505,7 +507,11 @@ void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out);
 // MD (md.cu): bonded forces added to c->force (results 100 bonds, 101
 // angles), velocity-Verlet half kick / drift, kinetic energy (result 102)
 void run_bonded(mdg_ctx* c);
+void run_bonded(mdg_ctx* c, double4* out);  // adds into out
 void run_kick(mdg_ctx* c, double half_dt);
+void run_kick(mdg_ctx* c, double half_dt, const double4* force);
+// Langevin O step: v = c1 v + sqrt(1 - c1^2) sqrt(kT/m) xi (kt in kcal/mol)
+void run_ostep(mdg_ctx* c, double c1, double kt, uint64_t seed, uint64_t counter);
 void run_drift(mdg_ctx* c, double dt);
 void run_kinetic(mdg_ctx* c);
 

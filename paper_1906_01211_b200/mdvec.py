@@ -201,12 +201,20 @@ class AmoebaParams(C.Structure):
 TERM_VDW, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE = 1, 2, 4, 8
 
 
+INTEGRATOR_VERLET = 0
+INTEGRATOR_BAOAB_RESPA = 1
+
+
 class MDParams(C.Structure):
     """mdg.h mdg_md_params (SURVEY 8(f)#4)."""
     _fields_ = [("model", C.c_int), ("nsteps", C.c_int64), ("dt_fs", C.c_double),
                 ("rebuild_every", C.c_int), ("elec_list", C.c_int), ("vdw_list", C.c_int),
                 ("elec_list_cutoff", C.c_double), ("vdw_list_cutoff", C.c_double),
-                ("bonded", C.c_int)]
+                ("bonded", C.c_int),
+                # zero defaults keep velocity Verlet
+                ("integrator", C.c_int), ("inner_steps", C.c_int),
+                ("friction_ps", C.c_double), ("temperature_k", C.c_double),
+                ("seed", C.c_uint64)]
 
 
 _lib = None
@@ -644,8 +652,8 @@ class Engine:
         return _aos(x, y, z)
 
     def md_run(self, p: "MDParams", charmm=None, amoeba=None, energies: bool = True):
-        """Velocity Verlet on the device (mdg.h mdg_md_run); returns per-step
-        (kinetic, potential) energies when `energies`."""
+        """Velocity Verlet or BAOAB-RESPA on the device (mdg.h mdg_md_run);
+        returns per-step (kinetic, potential) energies when `energies`."""
         ek = np.zeros(max(p.nsteps, 1)) if energies else None
         ep = np.zeros(max(p.nsteps, 1)) if energies else None
         check(self.lib.mdg_md_run(self.ctx, C.byref(p), None if charmm is None else C.byref(charmm),

@@ -230,3 +230,31 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cpp", ".cu", ".h", ".cuh", "Makefile")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not bad.search(src), f
+
+
+def test_param_struct_layouts_match_header(mdg, tmp_path):
+    """The ctypes parameter structs have the size and field offsets of the C
+    structs in include/mdg.h (compiled here with gcc)."""
+    import subprocess
+    structs = {"mdg_charmm_params": mdg.CharmmParams, "mdg_amoeba_params": mdg.AmoebaParams,
+               "mdg_md_params": mdg.MDParams}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mdg.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o",
+                    str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True,
+                               text=True).stdout.splitlines():
+        cname, key, val = line.split()
+        got[(cname, key)] = int(val)
+    for cname, cls in structs.items():
+        assert got[(cname, "size")] == C.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)

@@ -1113,10 +1113,12 @@ def test_bonded_forces_match_oracle(engine, oracle, mdg):
     assert force_err_max(f, fo) <= 1e-12
 
 
-def test_md_trajectory_matches_oracle(engine, oracle, mdg):
+def test_md_trajectory_matches_oracle(engine, oracle, mdg, monkeypatch):
     """20 velocity-Verlet steps of flexible CHARMM-style water on the device
-    against the numpy integrator driven by the oracle's forces."""
+    against the numpy integrator driven by the oracle's forces (the sites
+    re-sorted on the device at each of the two list rebuilds)."""
     from oracle import md
+    monkeypatch.setenv("MDG_RESORT", "1")
     s, mass, vel, b, a = _md_water(mdg)
     so = to_oracle_system(s)
     bond_args = (b, 529.6, 0.9572, a, 34.05, np.deg2rad(104.52))
