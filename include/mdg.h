@@ -374,6 +374,14 @@ int mdg_group_create_local(mdg_group** out, int n, mdg_ctx** ctxs, int64_t n_glo
 int mdg_group_create_nccl(mdg_group** out, mdg_ctx* ctx, int rank, int size, const void* id128,
                           int64_t n_global);
 int mdg_group_destroy(mdg_group* g);
+/* Interior/halo overlap inside the PCG: each iteration's halo refresh of the
+ * search direction runs on the group's communication stream while the
+ * mat-vec of the sites whose pruned rows hold no halo site runs on the
+ * domains' stream; the boundary sites follow once the halo is in. Default:
+ * on for NCCL groups, off for LOCAL ones (one device: the pull kernel is too
+ * small to hide anything); the environment variable MDG_DD_OVERLAP=0/1 sets
+ * the default. */
+int mdg_group_set_overlap(mdg_group* g, int on);
 /* mdg_ctx_destroy of a grouped context fails with MDG_CONTRACT: destroy the
  * group first. */
 /* LOCAL halo of domain `domain`: for each of its n_halo halo sites (caller-

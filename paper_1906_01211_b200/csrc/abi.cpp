@@ -311,7 +311,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
                   c->results,
-                  c->d_stage};
+                  c->d_stage, c->dd_sites, c->dd_flags, c->dd_nsel, c->dd_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& L : c->lists) {

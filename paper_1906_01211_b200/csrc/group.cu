@@ -184,12 +184,36 @@ struct mdg_group : PcgComm {
   double* d_sum = nullptr;  // energy / virial all-reduce buffer
   std::vector<double4*> ref;  // per domain: positions when the plan was made
   unsigned long long* d_disp = nullptr;
+  // interior/halo overlap: the halo refresh of the PCG direction runs on
+  // its own (highest-priority) stream while the interior rows are computed
+  bool ov = false;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
 
   cudaStream_t stream() const { return dom[0]->stream; }
 
-  void exchange(int vec_id) override { exchange_vec(vec_id, vec_id == MDG_VEC_P); }
+  void exchange(int vec_id) override { exchange_vec(vec_id, vec_id == MDG_VEC_P, stream()); }
 
-  void exchange_vec(int vec_id, bool skip_converged) {
+  bool overlap() const override {
+    if (!ov) return false;
+    if (backend == MDG_GROUP_NCCL) return size > 1;
+    for (const LocalHalo& h : lh)
+      if (h.n) return true;
+    return false;
+  }
+
+  void exchange_begin(int vec_id) override {
+    MDG_CUDA_CHECK(cudaEventRecord(ev_ready, stream()));
+    MDG_CUDA_CHECK(cudaStreamWaitEvent(cstream, ev_ready, 0));
+    exchange_vec(vec_id, vec_id == MDG_VEC_P, cstream);
+    MDG_CUDA_CHECK(cudaEventRecord(ev_done, cstream));
+  }
+
+  void exchange_end() override { MDG_CUDA_CHECK(cudaStreamWaitEvent(stream(), ev_done, 0)); }
+
+  // the refresh ops, queued on stream s (the domains' stream, or the
+  // communication stream between exchange_begin / exchange_end)
+  void exchange_vec(int vec_id, bool skip_converged, cudaStream_t s) {
     if (size == 1 && backend == MDG_GROUP_NCCL) return;
     if (backend == MDG_GROUP_LOCAL) {
       const int nd = (int)dom.size();
@@ -197,7 +221,7 @@ struct mdg_group : PcgComm {
         mdg_ctx* c = dom[d];
         if (lh[d].n == 0) continue;
         c->launches++;
-        k_halo_pull<<<grid_for(lh[d].n, 256), 256, 0, c->stream>>>(
+        k_halo_pull<<<grid_for(lh[d].n, 256), 256, 0, s>>>(
             lh[d].n, lh[d].dst, lh[d].src, d_vecs + (size_t)vec_id * nd, vec_by_id(c, vec_id),
             c->results, skip_converged ? 1 : 0);
       }
@@ -207,27 +231,37 @@ struct mdg_group : PcgComm {
       double4* v = vec_by_id(c, vec_id);
       if (nsend) {
         c->launches++;
-        k_pack3<<<grid_for(nsend, 256), 256, 0, c->stream>>>(nsend, d_send, v, d_sbuf,
-                                                             c->results, skip_converged ? 1 : 0);
+        k_pack3<<<grid_for(nsend, 256), 256, 0, s>>>(nsend, d_send, v, d_sbuf, c->results,
+                                                     skip_converged ? 1 : 0);
       }
       nccl_check(N.GroupStart(), "ncclGroupStart");
       for (const Peer& p : peers) {
         if (p.nrecv)
-          nccl_check(N.Recv(d_rbuf + 3 * p.roff, 3 * p.nrecv, ncclDouble, p.rank, comm, c->stream),
+          nccl_check(N.Recv(d_rbuf + 3 * p.roff, 3 * p.nrecv, ncclDouble, p.rank, comm, s),
                      "ncclRecv");
         if (p.nsend)
-          nccl_check(N.Send(d_sbuf + 3 * p.soff, 3 * p.nsend, ncclDouble, p.rank, comm, c->stream),
+          nccl_check(N.Send(d_sbuf + 3 * p.soff, 3 * p.nsend, ncclDouble, p.rank, comm, s),
                      "ncclSend");
       }
       nccl_check(N.GroupEnd(), "ncclGroupEnd");
       if (nrecv) {
         c->launches++;
-        k_unpack3<<<grid_for(nrecv, 256), 256, 0, c->stream>>>(nrecv, d_recv, d_rbuf, v,
-                                                               c->results, skip_converged ? 1 : 0);
+        k_unpack3<<<grid_for(nrecv, 256), 256, 0, s>>>(nrecv, d_recv, d_rbuf, v, c->results,
+                                                       skip_converged ? 1 : 0);
       }
     }
     if (vec_id == MDG_VEC_POS)
       for (mdg_ctx* c : dom) refresh_vsites(c);
+  }
+
+  void init_overlap(bool on) {
+    ov = on;
+    if (cstream) return;
+    int lo = 0, hi = 0;
+    MDG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    MDG_CUDA_CHECK(cudaStreamCreateWithPriority(&cstream, cudaStreamNonBlocking, hi));
+    MDG_CUDA_CHECK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+    MDG_CUDA_CHECK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   }
 
   void allreduce(int slot, int nv) override {
@@ -317,6 +351,9 @@ int mdg_group_create_local(mdg_group** out, int n, mdg_ctx** ctxs, int64_t n_glo
     g->lh.resize(n);
     MDG_CUDA_CHECK(cudaSetDevice(ctxs[0]->device));
     refresh_tables(g);
+    // in one process the halo pull is a small kernel beside the mat-vec:
+    // the split costs more than it hides (MDG_DD_OVERLAP=1 turns it on)
+    g->init_overlap(env_int("MDG_DD_OVERLAP", 0) != 0);
     *out = g;
   });
 }
@@ -343,6 +380,8 @@ int mdg_group_create_nccl(mdg_group** out, mdg_ctx* ctx, int rank, int size, con
     g->lh.resize(1);
     ctx->group = g;
     MDG_CUDA_CHECK(cudaMalloc(&g->d_sum, 32 * sizeof(double)));
+    // between GPUs the send/receive latency is worth hiding (MDG_DD_OVERLAP=0 off)
+    g->init_overlap(env_int("MDG_DD_OVERLAP", 1) != 0);
     *out = g;
   });
 }
@@ -364,8 +403,20 @@ int mdg_group_destroy(mdg_group* g) {
                     (void*)g->d_sbuf, (void*)g->d_rbuf, (void*)g->d_sum, (void*)g->d_disp})
       if (p) cudaFree(p);
     for (double4* r : g->ref) cudaFree(r);
+    if (g->cstream) cudaStreamSynchronize(g->cstream);
+    if (g->ev_ready) cudaEventDestroy(g->ev_ready);
+    if (g->ev_done) cudaEventDestroy(g->ev_done);
+    if (g->cstream) cudaStreamDestroy(g->cstream);
     if (g->comm) nccl().CommDestroy(g->comm);
     delete g;
+  });
+}
+
+int mdg_group_set_overlap(mdg_group* g, int on) {
+  return gguard([&] {
+    gneed(g != nullptr, "group: null");
+    MDG_CUDA_CHECK(cudaSetDevice(g->dom[0]->device));
+    g->init_overlap(on != 0);
   });
 }
 
@@ -456,7 +507,7 @@ int mdg_group_exchange(mdg_group* g, int vec_id) {
     gneed(vec_id >= 0 && vec_id < 6, "group_exchange: unknown vector id");
     MDG_CUDA_CHECK(cudaSetDevice(g->dom[0]->device));
     if (g->backend == MDG_GROUP_LOCAL) refresh_tables(g);
-    g->exchange_vec(vec_id, false);
+    g->exchange_vec(vec_id, false, g->stream());
     MDG_CUDA_CHECK(cudaStreamSynchronize(g->stream()));
   });
 }

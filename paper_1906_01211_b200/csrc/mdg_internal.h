@@ -142,6 +142,13 @@ struct PcgComm {
   virtual bool capturable() const = 0;  // all ops may sit in a while graph
   virtual int64_t n_global() const = 0;
   virtual uintptr_t generation() const = 0;  // changes with the halo plans
+  // Interior/halo overlap: exchange_begin issues the refresh on the group's
+  // communication stream (after everything queued so far on the domains'
+  // stream), exchange_end makes the domains' stream wait for it; between the
+  // two, the mat-vec of the sites whose rows hold no halo site runs.
+  virtual bool overlap() const { return false; }
+  virtual void exchange_begin(int vec_id) { exchange(vec_id); }
+  virtual void exchange_end() {}
 };
 
 // reciprocal-space Ewald in the AMOEBA step (mdg_set_ewald_recip): grid,
@@ -182,6 +189,14 @@ struct mdg_ctx {
   int64_t n_global = 0;
   // the domain group this context belongs to (group.cu; NULL: single domain)
   mdg_group* group = nullptr;
+  // interior / boundary split of the owned sites (domain groups with
+  // interior/halo overlap): boundary sites (a halo site in their pruned row)
+  // first, then the interior ones; dd_nsel = number of boundary sites
+  int32_t* dd_sites = nullptr;
+  uint8_t* dd_flags = nullptr;
+  int* dd_nsel = nullptr;
+  void* dd_tmp = nullptr;
+  size_t dd_tmp_bytes = 0;
   int32_t* d_iperm = nullptr;  // caller -> sorted index
   int32_t* d_idx = nullptr;    // staging for halo index lists
   double lx = 0, ly = 0, lz = 0;

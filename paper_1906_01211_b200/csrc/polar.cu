@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 
 // field_tpre: 6 resident blocks per SM (<= 85 registers) measured fastest
@@ -369,6 +371,12 @@ struct TPArgs {
   double4* __restrict__ out;
   double* __restrict__ partials;
   const double* __restrict__ res;  // PCG: result slots (converged flag 27)
+  // site subset (interior/halo overlap): 0 all n sites; 1 the boundary sites
+  // sites[0, *nsel); 2 the interior sites sites[*nsel, n). The grid is sized
+  // for n either way (warps past the subset return).
+  int part;
+  const int32_t* __restrict__ sites;
+  const int* __restrict__ nsel;
 };
 
 // E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; the PCG form
@@ -378,7 +386,15 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
   if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
   const int lane = threadIdx.x & 31;
   double acc[1] = {0.0};
-  MDG_SITE_LOOP(i, a.n, a.ipw) {
+  int64_t nsub = a.n;
+  const int32_t* map = nullptr;
+  if (a.part) {
+    const int64_t nb = *a.nsel;
+    nsub = a.part == 1 ? nb : a.n - nb;
+    map = a.part == 1 ? a.sites : a.sites + nb;
+  }
+  MDG_SITE_LOOP(w, nsub, a.ipw) {
+    const int64_t i = map ? (int64_t)map[w] : w;
     const double4 pi = a.pos[i];
     const int cnt = a.pcnt[i];
     MDG_DASSERT(cnt >= 0 && cnt <= a.pcap);
@@ -798,6 +814,9 @@ static void pcg_dom_setup(PcgDom& d, mdg_ctx* c) {
   k.out = c->cg_q;
   k.partials = c->partials;
   k.res = c->results;
+  k.part = 0;
+  k.sites = nullptr;
+  k.nsel = nullptr;
   d.kc = CLArgs{};
   if (d.cl) {
     d.kc = cl_args(c, c->cg_p, c->cg_q);
@@ -807,17 +826,94 @@ static void pcg_dom_setup(PcgDom& d, mdg_ctx* c) {
   }
 }
 
+// boundary flag of an owned site: its pruned row holds a halo site (warp per
+// site; the top bit of a row entry is a pair flag, not part of the index)
+__global__ void __launch_bounds__(kBlock) k_boundary_flags(int64_t n_own, int ipw,
+                                                           const int32_t* __restrict__ pnbr,
+                                                           const int32_t* __restrict__ pcnt,
+                                                           int32_t pcap,
+                                                           uint8_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  MDG_SITE_LOOP(i, n_own, ipw) {
+    const int cnt = pcnt[i];
+    const int32_t* row = pnbr + (size_t)i * pcap;
+    bool halo = false;
+    for (int k = lane; k < cnt; k += 32) halo |= (row[k] & 0x7fffffff) >= n_own;
+    const bool any = __any_sync(0xffffffffu, halo);
+    if (lane == 0) flag[i] = any ? 1 : 0;
+  }
+}
+
+// Interior/boundary split of a domain's owned sites for the overlapped
+// exchange: c->dd_sites = the boundary sites in site order, then the
+// interior ones in reverse site order (CUB's partition writes the rejected
+// part backwards); *c->dd_nsel = the boundary count. Deterministic, and no
+// host sync: the count stays on the device for the mat-vec launches.
+static void split_sites(mdg_ctx* c) {
+  const PrunedList& P = c->plist;
+  const int64_t n = c->n_own;
+  if (!c->dd_sites) {
+    MDG_CUDA_CHECK(cudaMalloc(&c->dd_sites, (size_t)c->n_cap * sizeof(int32_t)));
+    MDG_CUDA_CHECK(cudaMalloc(&c->dd_flags, (size_t)c->n_cap));
+    MDG_CUDA_CHECK(cudaMalloc(&c->dd_nsel, sizeof(int)));
+  }
+  const int ipw = sites_per_warp(n);
+  MDG_LAUNCH(c, "dd_split", warp_grid(n, ipw), kBlock, 0, k_boundary_flags, n,
+             ipw * (int)kWarps, P.nbr, P.cnt, P.cap, c->dd_flags);
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t bytes = 0;
+  MDG_CUDA_CHECK(cub::DevicePartition::Flagged(nullptr, bytes, it, c->dd_flags, c->dd_sites,
+                                               c->dd_nsel, (int)n, c->stream));
+  if (bytes > c->dd_tmp_bytes) {
+    if (c->dd_tmp) MDG_CUDA_CHECK(cudaFree(c->dd_tmp));
+    MDG_CUDA_CHECK(cudaMalloc(&c->dd_tmp, bytes));
+    c->dd_tmp_bytes = bytes;
+  }
+  MDG_CUDA_CHECK(cub::DevicePartition::Flagged(c->dd_tmp, bytes, it, c->dd_flags, c->dd_sites,
+                                               c->dd_nsel, (int)n, c->stream));
+}
+
 // The loop body, launched directly on the domains' stream (raw launches:
 // also used inside stream capture, where the grids must be fixed).
+// Overlapped exchange (comm->overlap(), plain mat-vec): the interior sites'
+// rows run while the halo of p is refreshed on the communication stream,
+// then the boundary sites'; their block partials sit side by side
+// (2 g blocks, a fixed order).
 static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditionalHandle h,
                      int use_cond, int64_t max_iter, double n_global, double tol) {
-  if (comm) comm->exchange(MDG_VEC_P);
+  bool ov = comm && comm->overlap();
+  for (const PcgDom& d : ds) ov = ov && !d.cl && !d.tma && d.c->dd_sites;
+  if (ov) {
+    comm->exchange_begin(MDG_VEC_P);
+    for (PcgDom& d : ds) {
+      TPArgs k = d.k;
+      k.part = 2;
+      k.sites = d.c->dd_sites;
+      k.nsel = d.c->dd_nsel;
+      k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, d.c->stream>>>(k);
+    }
+    comm->exchange_end();
+  } else if (comm) {
+    comm->exchange(MDG_VEC_P);
+  }
   for (PcgDom& d : ds) {
     mdg_ctx* c = d.c;
-    if (d.cl) cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
-    else if (d.tma) k_tmatvec_tma<true><<<(unsigned)d.g, kBlock, d.smem, c->stream>>>(d.k);
-    else k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
-    int64_t pb = d.g;
+    if (ov) {
+      TPArgs k = d.k;
+      k.part = 1;
+      k.sites = c->dd_sites;
+      k.nsel = c->dd_nsel;
+      k.partials = c->partials + (size_t)d.g * kRedVals;  // blocks g .. 2g - 1
+      k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(k);
+      c->launches++;
+    } else if (d.cl) {
+      cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
+    } else if (d.tma) {
+      k_tmatvec_tma<true><<<(unsigned)d.g, kBlock, d.smem, c->stream>>>(d.k);
+    } else {
+      k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
+    }
+    int64_t pb = ov ? 2 * d.g : d.g;
     if (c->pol_recip.on()) {  // q -= reciprocal + self field of p; partials p.q
       pme_field(c, 2, c->cg_p, c->cg_q);
       pb = grid_for(c->n_own);
@@ -879,6 +975,7 @@ static std::vector<uintptr_t> pcg_key(const std::vector<PcgDom>& ds, PcgComm* co
   }
   key.push_back((uintptr_t)comm);
   if (comm) key.push_back(comm->generation());
+  if (comm) key.push_back((uintptr_t)comm->overlap());
   key.push_back((uintptr_t)max_iter);
   put(&tol, sizeof tol);
   put(&n_global, sizeof n_global);
@@ -947,6 +1044,7 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
   // the aux stream's multipole blocks
   static const int pcg_bps = env_int("MDG_PCG_BPS", 0), pcg_waves = env_int("MDG_PCG_WAVES", 0);
   std::vector<PcgDom> ds(doms.size());
+  const bool ov = comm && comm->overlap();
   for (size_t k = 0; k < doms.size(); ++k) {
     mdg_ctx* c = doms[k];
     const int b = c->launch_bps, w = c->launch_waves;
@@ -955,6 +1053,11 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
     pcg_dom_setup(ds[k], c);
     c->launch_bps = b;
     c->launch_waves = w;
+    if (ov && !ds[k].cl && !ds[k].tma) {
+      split_sites(c);  // after the pruned rows of this step
+      ensure_partials(c, 2 * ds[k].g);
+      ds[k].k.partials = c->partials;  // (ensure_partials may have moved it)
+    }
   }
   // mu0 = alpha E, its halo, T mu0, r0 / z0 / p0 and r0.z0
   for (PcgDom& d : ds) {

@@ -204,10 +204,13 @@ class DomainGroup:
     per domain, one shared stream) -- N ranks emulated on one GPU.
     backend "nccl": this rank's domain only; `rank`/`size` of the
     torch.distributed default group, which also carries the NCCL unique id.
+    overlap: interior/halo overlap in the PCG (None: the engine's default,
+    on for NCCL, off for LOCAL).
     """
 
     def __init__(self, s, size: int, halo_width: float, device: int = 0, backend: str = "local",
-                 rank: int = 0, plans=None, list_cutoff: float | None = None):
+                 rank: int = 0, plans=None, list_cutoff: float | None = None,
+                 overlap: bool | None = None):
         self.lib = M.load_library()
         self.backend, self.size, self.rank = backend, size, rank
         self.halo_width = float(halo_width)
@@ -239,6 +242,8 @@ class DomainGroup:
             self._set_halo_nccl()
         else:
             raise ValueError(f"unknown backend {backend!r}")
+        if overlap is not None:  # interior/halo overlap (mdg.h mdg_group_set_overlap)
+            M.check(self.lib.mdg_group_set_overlap(self.g, int(bool(overlap))))
         M.check(self.lib.mdg_group_set_reference(self.g))
 
     # ---- halo plans

@@ -153,6 +153,7 @@ SIGNATURES = {
     "mdg_group_create_nccl": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int64]),
     "mdg_group_destroy": (C.c_int, [C.c_void_p]),
+    "mdg_group_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_group_set_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _ip, _ip, _ip]),
     "mdg_group_set_halo_nccl": (C.c_int, [C.c_void_p, C.c_int, _ip, _i64p, _ip, _i64p, _ip]),
     "mdg_group_exchange": (C.c_int, [C.c_void_p, C.c_int]),

@@ -12,9 +12,10 @@ pytestmark = pytest.mark.gpu
 HALO = 12.5  # 11 A vdW list + intramolecular extent + margin
 
 
-def run_domains(mdg, s, size, params, lists, frames=None, steps=1):
+def run_domains(mdg, s, size, params, lists, frames=None, steps=1, overlap=None, launches=None):
     from paper_1906_01211_b200 import dd
-    g = dd.DomainGroup(s, size, HALO, device=0, backend="local", list_cutoff=11.0)
+    g = dd.DomainGroup(s, size, HALO, device=0, backend="local", list_cutoff=11.0,
+                       overlap=overlap)
     try:
         assert g.check_halo(s)
         if frames is not None:
@@ -25,6 +26,8 @@ def run_domains(mdg, s, size, params, lists, frames=None, steps=1):
         en, w, it, rms = g.energies()
         ids, f = g.owned_forces()
         _, mu = g.owned_dipoles()
+        if launches is not None:
+            launches.append(g.launch_count())
     finally:
         g.close()
     n = s.n_sites
@@ -65,6 +68,34 @@ def test_domains_match_single_gpu(mdg, size, polar_forces):
     assert abs(it - it0) <= 1
     d = np.sqrt(np.mean(np.sum((MU - mu0) ** 2, 1))) * mdg.DEBYE
     assert d < 1e-5
+
+
+@pytest.mark.parametrize("size", [2, 8])
+def test_interior_halo_overlap_matches(mdg, size):
+    """Interior/halo overlap (mdg_group_set_overlap: each PCG iteration's
+    halo refresh on the communication stream while the rows without halo
+    sites run, then the boundary rows) gives the results of the serial
+    exchange and of the single engine; the split adds the boundary
+    mat-vec launches (and the per-step split)."""
+    s = mdg.water_box(1728, 37.26, 7, "amoeba")
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1, terms)
+    lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
+    en0, w0, it0, f0, mu0 = single(mdg, s, p)
+    runs, launches = {}, []
+    for ov in (False, True):
+        runs[ov] = run_domains(mdg, s, size, p, lists, steps=2, overlap=ov, launches=launches)
+    F0, MU0, e0, _, i0 = runs[False]
+    F1, MU1, e1, w1, i1 = runs[True]
+    assert i1 == i0
+    assert launches[1] > launches[0]
+    rms = np.sqrt(np.mean(f0 ** 2))
+    assert np.abs(F1 - F0).max() <= 1e-10 * rms
+    assert np.abs(MU1 - MU0).max() <= 1e-10 * np.abs(MU0).max()
+    assert np.abs(F1 - f0).max() <= 1e-8 * rms
+    for k in range(3):
+        assert e1[k] == pytest.approx(en0[k], rel=1e-9)
+    assert abs(i1 - it0) <= 1
 
 
 def test_domains_with_local_frames(mdg):
