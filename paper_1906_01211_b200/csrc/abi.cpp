@@ -1193,7 +1193,11 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   need(!(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_POLAR),
        "amoeba_step: polarization forces need the polarization solve");
   const bool recip = c->pol_recip.on();
-  need(!recip || c->n_own == c->n, "amoeba_step: reciprocal space is single-domain only");
+  // domains of a group: the reciprocal-space passes run over all domains
+  // together (mdg_group_amoeba_step, replicated grid)
+  const bool recip_here = recip && c->group == nullptr;
+  need(!recip || c->n_own == c->n || c->group != nullptr,
+       "amoeba_step: reciprocal space of a domain runs through its group");
   need(!recip || !(st.terms & MDG_TERM_POLAR_FORCE) || (st.terms & MDG_TERM_MPOLE),
        "amoeba_step: reciprocal-space polarization forces come with the multipole term");
   MDG_CUDA_CHECK(cudaMemsetAsync(c->results, 0, (recip ? 107 : 80) * sizeof(double), c->stream));
@@ -1224,7 +1228,7 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   st.polar = (st.terms & MDG_TERM_POLAR) != 0;
   if (st.polar) {
     mdg::run_field_tpre(c, elec_list, p->alpha, p->elec_cutoff, p->thole_a, p->exclude);
-    if (recip) mdg::pme_field(c, 0, nullptr, c->eperm);  // + reciprocal + self field
+    if (recip_here) mdg::pme_field(c, 0, nullptr, c->eperm);  // + reciprocal + self field
     if (st.ov) {
       MDG_CUDA_CHECK(cudaEventRecord(c->ev_tpre, c->stream));
       MDG_CUDA_CHECK(cudaStreamWaitEvent(c->aux_stream, c->ev_tpre, 0));
@@ -1233,13 +1237,14 @@ static AmoebaPhase amoeba_pre(mdg_ctx* c, int vdw_list, int elec_list, const mdg
   // forces are final at the end of the aux chain unless polarization
   // forces or frame torques still add to them
   st.late_forces = (st.polar && (st.terms & MDG_TERM_POLAR_FORCE)) ||
-                   (c->has_frames && (st.terms & MDG_TERM_MPOLE));
+                   (c->has_frames && (st.terms & MDG_TERM_MPOLE)) ||
+                   (recip && !recip_here && (st.terms & MDG_TERM_MPOLE));
   {
     mdg::AuxScope aux(c, st.ov);
     if (st.terms & MDG_TERM_MPOLE) {
       if (st.polar) mdg::run_mpole_pruned(c, p->alpha, p->electric, p->exclude, true);
       else mdg::run_mpole(c, elec_list, p->alpha, p->elec_cutoff, p->electric, p->exclude, true);
-      if (recip) {  // + the multipoles' reciprocal-space sum (own PME state);
+      if (recip_here) {  // + the multipoles' reciprocal-space sum (own PME state);
         // with polarization forces its forces / torques come from the
         // permanent + induced pass after the solve (amoeba_post)
         const mdg::PolarRecip& R = c->pol_recip;
@@ -1266,10 +1271,12 @@ static void amoeba_join(mdg_ctx* c, const AmoebaPhase& st) {
   cudaStreamWaitEvent(c->stream, c->ev_join, 0);
 }
 
-static void amoeba_post(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_params* p) {
+// post, first part: the real-space polarization forces (and, single
+// domain, the combined reciprocal pass); amoeba_post_frames completes
+static void amoeba_post_polar(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_params* p) {
   if (st.polar && (st.terms & MDG_TERM_POLAR_FORCE)) {
     mdg::run_polar_force_pruned(c, p->alpha, p->thole_a, p->electric, p->exclude, true);
-    if (c->pol_recip.on() && (st.terms & MDG_TERM_MPOLE)) {
+    if (c->pol_recip.on() && c->group == nullptr && (st.terms & MDG_TERM_MPOLE)) {
       // reciprocal space of multipoles + polarization at fixed dipoles: the
       // forces of the permanent + induced set (E_mpole,rec + E_pol,rec =
       // Q[M + mu], the mu-only self terms being position-independent)
@@ -1279,8 +1286,16 @@ static void amoeba_post(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_para
     }
     c->has_polar_force = true;
   }
+}
+
+static void amoeba_post_frames(mdg_ctx* c, const AmoebaPhase& st) {
   if ((st.terms & MDG_TERM_MPOLE) || c->has_polar_force) mdg::frame_torques_to_forces(c);
   if (st.late_forces) queue_force_output(c);
+}
+
+static void amoeba_post(mdg_ctx* c, const AmoebaPhase& st, const mdg_amoeba_params* p) {
+  amoeba_post_polar(c, st, p);
+  amoeba_post_frames(c, st);
 }
 
 static void amoeba_step_impl(mdg_ctx* c, int vdw_list, int elec_list, const mdg_amoeba_params* p) {
@@ -1330,8 +1345,13 @@ int mdg_group_amoeba_step(mdg_group* g, int vdw_list, int elec_list, const mdg_a
     auto join_all = [&] {
       for (size_t k = 0; k < st.size(); ++k) amoeba_join(doms[k], st[k]);
     };
+    const bool recip = doms[0]->pol_recip.on();
+    mdg::PcgComm* comm = mdg::group_comm(g);
     try {
       for (mdg_ctx* c : doms) st.push_back(amoeba_pre(c, vdw_list, elec_list, p));
+      // reciprocal space over all domains (replicated grid): the permanent
+      // field before the solve
+      if (recip && st[0].polar) mdg::pme_field_multi(doms, comm, 0);
       if (st[0].polar) {
         double rms = 0;
         const int64_t it =
@@ -1348,9 +1368,22 @@ int mdg_group_amoeba_step(mdg_group* g, int vdw_list, int elec_list, const mdg_a
     }
     join_all();
     // the solve leaves the halo dipoles at mu0: refresh them for the forces
-    if (st[0].polar && (st[0].terms & MDG_TERM_POLAR_FORCE))
-      mdg::group_comm(g)->exchange(MDG_VEC_MU);
-    for (size_t k = 0; k < st.size(); ++k) amoeba_post(doms[k], st[k], p);
+    if (st[0].polar && (st[0].terms & MDG_TERM_POLAR_FORCE)) comm->exchange(MDG_VEC_MU);
+    for (size_t k = 0; k < st.size(); ++k) amoeba_post_polar(doms[k], st[k], p);
+    if (recip && (st[0].terms & MDG_TERM_MPOLE)) {
+      // the multipoles' reciprocal sum (energy; forces and torques unless the
+      // combined permanent + induced pass below gives them), after the aux
+      // chains joined: these passes add to the same force / torque arrays
+      const mdg::PolarRecip& R = doms[0]->pol_recip;
+      const bool combined = st[0].polar && (st[0].terms & MDG_TERM_POLAR_FORCE);
+      mdg::run_pme_mpole_multi(doms, comm, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric,
+                               R.exclude, false, !combined);
+      if (combined)
+        mdg::run_pme_mpole_multi(doms, comm, p->alpha, R.k1, R.k2, R.k3, R.order, p->electric,
+                                 R.exclude, true, true);
+      for (mdg_ctx* c : doms) c->recip_in_step = true;
+    }
+    for (size_t k = 0; k < st.size(); ++k) amoeba_post_frames(doms[k], st[k]);
   });
 }
 

@@ -131,6 +131,22 @@ __global__ void k_unpack3(int64_t n, const int32_t* __restrict__ idx, const doub
   a->z = in[3 * k + 2];
 }
 
+// replicated-grid reciprocal space on one device: g[0] += g[1] + ... (a
+// fixed order)
+constexpr int kMaxGridDoms = 16;
+struct GridPtrs {
+  double* g[kMaxGridDoms];
+};
+
+__global__ void k_grid_sum(size_t count, GridPtrs p, int nd) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = p.g[0][i];
+    for (int d = 1; d < nd; ++d) s += p.g[d][i];
+    p.g[0][i] = s;
+  }
+}
+
 // max |minimum image (pos - ref)|^2 over the owned sites, as ordered bits
 __global__ void k_max_disp2(int64_t n, Box b, const double4* __restrict__ pos,
                             const double4* __restrict__ ref, unsigned long long* __restrict__ out) {
@@ -193,6 +209,24 @@ struct mdg_group : PcgComm {
   cudaStream_t stream() const { return dom[0]->stream; }
 
   void exchange(int vec_id) override { exchange_vec(vec_id, vec_id == MDG_VEC_P, stream()); }
+
+  void grid_sum(double* const* grids, int n, size_t count) override {
+    if (backend == MDG_GROUP_LOCAL) {
+      if (n <= 1) return;
+      if (n > kMaxGridDoms) throw_error(MDG_CONTRACT, "group: too many domains for the grid sum");
+      GridPtrs p{};
+      for (int d = 0; d < n; ++d) p.g[d] = grids[d];
+      dom[0]->launches++;
+      k_grid_sum<<<148 * 8, 256, 0, stream()>>>(count, p, n);
+    } else if (size > 1) {
+      nccl_check(nccl().AllReduce(grids[0], grids[0], count, ncclDouble, ncclSum, comm, stream()),
+                 "ncclAllReduce (grid)");
+    }
+  }
+  bool grid_shared() const override { return backend == MDG_GROUP_LOCAL; }
+  bool recip_root(int d) const override {
+    return backend == MDG_GROUP_LOCAL ? d == 0 : rank == 0;
+  }
 
   bool overlap() const override {
     if (!ov) return false;

@@ -146,6 +146,13 @@ struct PcgComm {
   // communication stream (after everything queued so far on the domains'
   // stream), exchange_end makes the domains' stream wait for it; between the
   // two, the mat-vec of the sites whose rows hold no halo site runs.
+  // replicated-grid reciprocal space (pme.cu PmeDoms): sum the domains'
+  // grids (count doubles each). grid_shared: one device, the sum lands in
+  // grids[0] and every domain reads it; else each rank's grid is all-reduced
+  // in place. recip_root: the domain that carries the convolution energy.
+  virtual void grid_sum(double* const* grids, int n, size_t count) {}
+  virtual bool grid_shared() const { return false; }
+  virtual bool recip_root(int dom) const { return dom == 0; }
   virtual bool overlap() const { return false; }
   virtual void exchange_begin(int vec_id) { exchange(vec_id); }
   virtual void exchange_end() {}
@@ -519,6 +526,13 @@ void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
 // adds v's dipole field to out; mode 2 (PCG) subtracts it from out and writes
 // the block partials of v.out
 void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out);
+// the same over the domains of a group (replicated grid summed through comm;
+// comm == NULL: one domain). mode 0: v = none, out = eperm; 1: v = mu,
+// out = cg_q; 2: v = cg_p, out = cg_q. ind: the permanent + induced set (mu).
+void pme_field_multi(const std::vector<mdg_ctx*>& doms, PcgComm* comm, int mode);
+void run_pme_mpole_multi(const std::vector<mdg_ctx*>& doms, PcgComm* comm, double alpha, int k1,
+                         int k2, int k3, int order, double electric, bool exclude, bool ind,
+                         bool forces);
 // MD (md.cu): bonded forces added to c->force (results 100 bonds, 101
 // angles), velocity-Verlet half kick / drift, kinetic energy (result 102)
 void run_bonded(mdg_ctx* c);

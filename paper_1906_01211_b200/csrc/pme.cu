@@ -777,38 +777,106 @@ __global__ void __launch_bounds__(kBlock) k_pme_excluded_mp(int64_t n, Box bx, d
 // results: 80 recip energy (convolution), 88 excluded, 98 recip energy from
 // the gathered potentials (check), 104-106 sums of q^2, |mu|^2, Q:Q for the
 // self energy (formed on the host); force / torque ADDED to
+// ---- replicated-grid reciprocal space over the domains of a group ----------
+// Each domain spreads its owned sites into its own grid; the grids are
+// summed (comm->grid_sum: on one device into the first domain's grid, which
+// every domain then reads; across NCCL ranks an in-place all-reduce of each
+// rank's grid); the summed grid is transformed once per device; every
+// domain gathers its owned sites from it. The energy of the convolution is
+// taken on one domain (comm->recip_root); self and excluded-pair terms are
+// per owned site. A single domain is the case comm == NULL.
+struct PmeDoms {
+  std::vector<mdg_ctx*> doms;
+  std::vector<PmeState*> st;
+  PcgComm* comm;
+  bool shared;  // one device: the first domain's grid serves all
+  PmeGeom g;
+  size_t count;
+
+  PmeDoms(const std::vector<mdg_ctx*>& d, PcgComm* cm, bool pol, int k1, int k2, int k3,
+          int order)
+      : doms(d), comm(cm) {
+    for (mdg_ctx* c : doms)
+      st.push_back(pme_state(c, pol ? &c->pme_pol : &c->pme, k1, k2, k3, order));
+    mdg_ctx* c0 = doms[0];
+    g = PmeGeom{k1, k2, k3, order, c0->lx, c0->ly, c0->lz};
+    count = (size_t)k1 * k2 * k3;
+    shared = comm && comm->grid_shared();
+  }
+  void clear(size_t k) {
+    MDG_CUDA_CHECK(cudaMemsetAsync(st[k]->grid, 0, count * sizeof(double), doms[k]->stream));
+  }
+  void sum() {
+    if (!comm) return;
+    std::vector<double*> grids;
+    for (PmeState* s : st) grids.push_back(s->grid);
+    comm->grid_sum(grids.data(), (int)grids.size(), count);
+  }
+  // the domains that transform (one per device)
+  bool solves(size_t k) const { return !shared || k == 0; }
+  bool root(size_t k) const { return comm ? comm->recip_root((int)k) : k == 0; }
+  const double* phi(size_t k) const { return shared ? st[0]->grid : st[k]->grid; }
+  // forward FFT, convolution (energy into `slot` of the root when >= 0),
+  // inverse FFT
+  void solve(double alpha, double electric, int slot) {
+    const int64_t total = (int64_t)g.k1 * g.k2 * (g.k3 / 2 + 1);
+    const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
+    for (size_t k = 0; k < doms.size(); ++k) {
+      if (!solves(k)) continue;
+      mdg_ctx* c = doms[k];
+      PmeState* s = st[k];
+      cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
+      const bool energy = slot >= 0 && root(k);
+      if (energy) ensure_partials(c, blocks);
+      MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, alpha,
+                 s->bmod, s->spec, energy ? c->partials : (double*)nullptr);
+      if (energy) finalize_partials(c, blocks, 1, slot, electric);
+      cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
+    }
+  }
+};
+
+void run_pme_mpole_multi(const std::vector<mdg_ctx*>& doms, PcgComm* comm, double alpha, int k1,
+                         int k2, int k3, int order, double electric, bool exclude, bool ind,
+                         bool forces) {
+  // the combined-set pass runs on the main stream after the solve: own state
+  PmeDoms P(doms, comm, ind, k1, k2, k3, order);
+  const int wf = forces ? 1 : 0;
+  for (size_t k = 0; k < doms.size(); ++k) {
+    mdg_ctx* c = doms[k];
+    P.clear(k);
+    MDG_LAUNCH(c, "pme_spread_mp", grid_for(c->n_own, 128), 128, 0, k_pme_spread_mp, c->n_own,
+               P.g, c->pos, c->pq4, c->mp, P.st[k]->grid, ind ? c->mu : (const double4*)nullptr);
+  }
+  P.sum();
+  P.solve(alpha, electric, ind ? -1 : 80);
+  for (size_t k = 0; k < doms.size(); ++k) {
+    mdg_ctx* c = doms[k];
+    const int64_t n = c->n_own;
+    const double4* mu = ind ? c->mu : nullptr;
+    ensure_partials(c, grid_for(n));
+    MDG_LAUNCH(c, "pme_gather_mp", grid_for(n), kBlock, 0, k_pme_gather_mp, n, P.g, c->pos,
+               c->pq4, c->mp, P.phi(k), electric, c->force, c->torque, c->partials, mu, wf);
+    if (!ind) {
+      finalize_partials(c, grid_for(n), 1, 98, 1.0);
+      MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
+                 c->partials);
+      finalize_partials(c, grid_for(n), 3, 104, 1.0);  // 104 q^2, 105 mu^2, 106 Q:Q
+    }
+    if (exclude && c->has_mol && c->excl_start) {
+      MDG_LAUNCH(c, "pme_excluded_mp", grid_for(n), kBlock, 0, k_pme_excluded_mp, n,
+                 make_box(c->lx, c->ly, c->lz), alpha, electric, c->pos, c->pq4, c->mp,
+                 c->excl_start, c->excl, c->force, c->torque, c->partials, mu, wf);
+      if (!ind) finalize_partials(c, grid_for(n), 1, 88, 1.0);
+    }
+  }
+}
+
 void run_pme_mpole(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order,
                    double electric, bool exclude, const double4* ind, bool forces) {
-  // the combined-set pass runs on the main stream after the solve: own state
-  PmeState* s = pme_state(c, ind ? &c->pme_pol : &c->pme, k1, k2, k3, order);
-  const PmeGeom g{k1, k2, k3, order, c->lx, c->ly, c->lz};
-  const int64_t n = c->n;
-  const int wf = forces ? 1 : 0;
-  MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)k1 * k2 * k3 * sizeof(double), c->stream));
-  MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos, c->pq4,
-             c->mp, s->grid, ind);
-  cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
-  const int64_t total = (int64_t)k1 * k2 * (k3 / 2 + 1);
-  const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
-  ensure_partials(c, std::max<int64_t>(blocks, grid_for(n)));
-  MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, alpha, s->bmod,
-             s->spec, ind ? (double*)nullptr : c->partials);
-  if (!ind) finalize_partials(c, blocks, 1, 80, electric);
-  cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
-  MDG_LAUNCH(c, "pme_gather_mp", grid_for(n), kBlock, 0, k_pme_gather_mp, n, g, c->pos, c->pq4,
-             c->mp, s->grid, electric, c->force, c->torque, c->partials, ind, wf);
-  if (!ind) {
-    finalize_partials(c, grid_for(n), 1, 98, 1.0);
-    MDG_LAUNCH(c, "pme_self_mp", grid_for(n), kBlock, 0, k_pme_self_mp, n, c->pq4, c->mp,
-               c->partials);
-    finalize_partials(c, grid_for(n), 3, 104, 1.0);  // 104 q^2, 105 mu^2, 106 Q:Q (host combines)
-  }
-  if (exclude && c->has_mol && c->excl_start) {
-    MDG_LAUNCH(c, "pme_excluded_mp", grid_for(n), kBlock, 0, k_pme_excluded_mp, n,
-               make_box(c->lx, c->ly, c->lz), alpha, electric, c->pos, c->pq4, c->mp,
-               c->excl_start, c->excl, c->force, c->torque, c->partials, ind, wf);
-    if (!ind) finalize_partials(c, grid_for(n), 1, 88, 1.0);
-  }
+  if (ind && ind != c->mu) throw_error(MDG_CONTRACT, "run_pme_mpole: induced set must be c->mu");
+  run_pme_mpole_multi({c}, nullptr, alpha, k1, k2, k3, order, electric, exclude, ind != nullptr,
+                      forces);
 }
 
 // ---- reciprocal-space electric fields for the polarization (8(f)#3) ----------
@@ -960,32 +1028,46 @@ __global__ void k_field_excl_erf(int64_t n, Box bx, double alpha, const double4*
 // Reciprocal + self field added to (mode 0/1) or, in PCG form, subtracted from
 // `out` with the partials of p.out (mode 2). v: the dipole vector (modes 1/2).
 // The launches are capture-safe (fixed grids, no host sync).
-void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out) {
-  const PolarRecip& R = c->pol_recip;
-  PmeState* s = pme_state(c, &c->pme_pol, R.k1, R.k2, R.k3, R.order);
-  const PmeGeom g{R.k1, R.k2, R.k3, R.order, c->lx, c->ly, c->lz};
-  const int64_t n = c->n_own;
+void pme_field_multi(const std::vector<mdg_ctx*>& doms, PcgComm* comm, int mode) {
+  const PolarRecip& R = doms[0]->pol_recip;
+  PmeDoms P(doms, comm, true, R.k1, R.k2, R.k3, R.order);
   const double a = R.alpha;
   const double cself = 4.0 * a * a * a / (3.0 * std::sqrt(M_PI));
-  MDG_CUDA_CHECK(cudaMemsetAsync(s->grid, 0, (size_t)R.k1 * R.k2 * R.k3 * sizeof(double),
-                                 c->stream));
-  if (mode == 0)
-    MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, g, c->pos,
-               c->pq4, c->mp, s->grid, (const double4*)nullptr);
-  else
-    MDG_LAUNCH(c, "pme_spread_dip", grid_for(n, 128), 128, 0, k_pme_spread_dip, n, g, c->pos,
-               v, s->grid, c->results, mode == 2 ? 1 : 0);
-  cufft_check(cufftExecD2Z(s->fwd, s->grid, s->spec), "D2Z");
-  const int64_t total = (int64_t)R.k1 * R.k2 * (R.k3 / 2 + 1);
-  const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
-  MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, a, s->bmod,
-             s->spec, (double*)nullptr);
-  cufft_check(cufftExecZ2D(s->inv, s->spec, s->grid), "Z2D");
-  MDG_LAUNCH(c, "pme_gather_field", grid_for(n), kBlock, 0, k_pme_gather_field, n, g, c->pos,
-             s->grid, v, c->mp, cself, mode, out, c->partials, c->results);
-  if (mode == 0 && R.exclude && c->has_mol && c->excl_start)
-    MDG_LAUNCH(c, "field_excl_erf", grid_for(n, 128), 128, 0, k_field_excl_erf, n,
-               make_box(c->lx, c->ly, c->lz), a, c->pos, c->pq4, c->mp, c->excl_start,
-               c->excl, out);
+  auto vin = [&](mdg_ctx* c) -> const double4* {
+    return mode == 0 ? nullptr : mode == 1 ? c->mu : c->cg_p;
+  };
+  for (size_t k = 0; k < doms.size(); ++k) {
+    mdg_ctx* c = doms[k];
+    const int64_t n = c->n_own;
+    // (inside the PCG the partials already cover grid_for(n): no reallocation)
+    if (mode == 0) ensure_partials(c, grid_for(n));
+    P.clear(k);
+    if (mode == 0)
+      MDG_LAUNCH(c, "pme_spread_mp", grid_for(n, 128), 128, 0, k_pme_spread_mp, n, P.g, c->pos,
+                 c->pq4, c->mp, P.st[k]->grid, (const double4*)nullptr);
+    else
+      MDG_LAUNCH(c, "pme_spread_dip", grid_for(n, 128), 128, 0, k_pme_spread_dip, n, P.g,
+                 c->pos, vin(c), P.st[k]->grid, c->results, mode == 2 ? 1 : 0);
+  }
+  P.sum();
+  P.solve(a, 1.0, -1);
+  for (size_t k = 0; k < doms.size(); ++k) {
+    mdg_ctx* c = doms[k];
+    const int64_t n = c->n_own;
+    double4* out = mode == 0 ? c->eperm : c->cg_q;
+    MDG_LAUNCH(c, "pme_gather_field", grid_for(n), kBlock, 0, k_pme_gather_field, n, P.g, c->pos,
+               P.phi(k), vin(c), c->mp, cself, mode, out, c->partials, c->results);
+    if (mode == 0 && R.exclude && c->has_mol && c->excl_start)
+      MDG_LAUNCH(c, "field_excl_erf", grid_for(n, 128), 128, 0, k_field_excl_erf, n,
+                 make_box(c->lx, c->ly, c->lz), a, c->pos, c->pq4, c->mp, c->excl_start,
+                 c->excl, out);
+  }
+}
+
+void pme_field(mdg_ctx* c, int mode, const double4* v, double4* out) {
+  const bool std_args = mode == 0 ? (v == nullptr && out == c->eperm)
+                                  : (v == (mode == 1 ? c->mu : c->cg_p) && out == c->cg_q);
+  if (!std_args) throw_error(MDG_CONTRACT, "pme_field: unexpected vectors");
+  pme_field_multi({c}, nullptr, mode);
 }
 }  // namespace mdg

@@ -873,6 +873,12 @@ static void split_sites(mdg_ctx* c) {
                                                c->dd_nsel, (int)n, c->stream));
 }
 
+static std::vector<mdg_ctx*> pcg_ctxs(const std::vector<PcgDom>& ds) {
+  std::vector<mdg_ctx*> v;
+  for (const PcgDom& d : ds) v.push_back(d.c);
+  return v;
+}
+
 // The loop body, launched directly on the domains' stream (raw launches:
 // also used inside stream capture, where the grids must be fixed).
 // Overlapped exchange (comm->overlap(), plain mat-vec): the interior sites'
@@ -913,11 +919,14 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
     } else {
       k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(d.k);
     }
-    int64_t pb = ov ? 2 * d.g : d.g;
-    if (c->pol_recip.on()) {  // q -= reciprocal + self field of p; partials p.q
-      pme_field(c, 2, c->cg_p, c->cg_q);
-      pb = grid_for(c->n_own);
-    }
+  }
+  // q -= reciprocal + self field of p (all domains' grids summed); the
+  // gather rewrites the partials of p.q
+  const bool recip = ds[0].c->pol_recip.on();
+  if (recip) pme_field_multi(pcg_ctxs(ds), comm, 2);
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
+    const int64_t pb = recip ? grid_for(c->n_own) : ov ? 2 * d.g : d.g;
     k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, pb, 1, c->results);
   }
   if (comm) comm->allreduce(20, 1);
@@ -1034,8 +1043,17 @@ void pcg_graph_forget(const void* owner) { pcg_graphs().erase(owner); }
 int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_debye,
                       int64_t max_iter, double* last_rms) {
   mdg_ctx* c0 = doms[0];
-  if (c0->pol_recip.on() && (doms.size() > 1 || comm || c0->n_own != c0->n))
-    throw_error(MDG_CONTRACT, "reciprocal-space polarization: single domain only");
+  if (c0->pol_recip.on()) {
+    if (!comm && (doms.size() > 1 || c0->n_own != c0->n))
+      throw_error(MDG_CONTRACT, "reciprocal-space polarization of domains needs their group");
+    for (mdg_ctx* c : doms) {
+      const PolarRecip &a = c->pol_recip, &b = c0->pol_recip;
+      if (a.k1 != b.k1 || a.k2 != b.k2 || a.k3 != b.k3 || a.order != b.order ||
+          a.alpha != b.alpha || a.exclude != b.exclude || c->lx != c0->lx || c->ly != c0->ly ||
+          c->lz != c0->lz)
+        throw_error(MDG_CONTRACT, "reciprocal space: the domains' grids / boxes differ");
+    }
+  }
   double n_global = 0;
   for (mdg_ctx* c : doms) n_global += (double)c->n_own;
   if (comm) n_global = (double)comm->n_global();
@@ -1080,7 +1098,10 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
       k.in = c->mu;
       MDG_LAUNCH_SITES(c, "tmatvec_pre", k.n, k, k_tmatvec_pre<false>);
     }
-    if (c->pol_recip.on()) pme_field(c, 1, c->mu, c->cg_q);  // + reciprocal + self field
+  }
+  if (c0->pol_recip.on()) pme_field_multi(doms, comm, 1);  // + reciprocal + self field
+  for (PcgDom& d : ds) {
+    mdg_ctx* c = d.c;
     MDG_LAUNCH(c, "cg_init", (unsigned)d.blocks, kBlock, 0, k_cg_init, c->n_own, c->polp,
                c->eperm, c->cg_q, c->mu, c->cg_r, c->cg_z, c->cg_p, c->partials);
     MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, d.blocks, 0,
@@ -1108,11 +1129,11 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
           TPArgs k = d.k;
           MDG_LAUNCH_SITES(c, "tmatvec_pcg", k.n, k, k_tmatvec_pre<true>);
         }
-        int64_t pb = c->last_grid;
-        if (c->pol_recip.on()) {
-          pme_field(c, 2, c->cg_p, c->cg_q);
-          pb = grid_for(c->n_own);
-        }
+      }
+      if (c0->pol_recip.on()) pme_field_multi(doms, comm, 2);
+      for (PcgDom& d : ds) {
+        mdg_ctx* c = d.c;
+        const int64_t pb = c0->pol_recip.on() ? grid_for(c->n_own) : c->last_grid;
         MDG_LAUNCH(c, "cg_scalars", 1, kScalarThreads, 0, k_cg_scalars, c->partials, pb, 1,
                    c->results);
       }

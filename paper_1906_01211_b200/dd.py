@@ -275,6 +275,15 @@ class DomainGroup:
         for d in self.domains:
             d.upload_frames(frame, zatom, xatom, dipole, quadrupole)
 
+    def set_ewald_recip(self, grid=(0, 0, 0), order: int = 6):
+        """Reciprocal-space Ewald in the decomposed AMOEBA step (every domain
+        the same grid): each domain spreads its owned sites, the grids are
+        summed over the domains (one device: a kernel; NCCL: an all-reduce),
+        the sum is transformed once per device and every domain gathers its
+        owned sites -- a replicated grid, not a distributed FFT."""
+        for d in self.domains:
+            d.eng.set_ewald_recip(grid, order)
+
     def build_lists(self, lists):
         """lists: [(cutoff, list_id, sites), ...]: every local domain builds the
         rows of its owned sites (candidates: owned + halo)."""

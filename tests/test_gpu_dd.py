@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 HALO = 12.5  # 11 A vdW list + intramolecular extent + margin
 
 
-def run_domains(mdg, s, size, params, lists, frames=None, steps=1, overlap=None, launches=None):
+def run_domains(mdg, s, size, params, lists, frames=None, steps=1, overlap=None, launches=None,
+                recip=None):
     from paper_1906_01211_b200 import dd
     g = dd.DomainGroup(s, size, HALO, device=0, backend="local", list_cutoff=11.0,
                        overlap=overlap)
@@ -20,6 +21,8 @@ def run_domains(mdg, s, size, params, lists, frames=None, steps=1, overlap=None,
         assert g.check_halo(s)
         if frames is not None:
             g.upload_frames(*frames)
+        if recip is not None:
+            g.set_ewald_recip(*recip)
         tables = g.build_lists(lists)
         for _ in range(steps):
             g.amoeba_step(tables, params)
@@ -38,11 +41,13 @@ def run_domains(mdg, s, size, params, lists, frames=None, steps=1, overlap=None,
     return F, MU, en, w, it
 
 
-def single(mdg, s, p, frames=None):
+def single(mdg, s, p, frames=None, recip=None):
     with mdg.Engine(s.n_sites) as e:
         e.upload_system(s)
         if frames is not None:
             e.upload_frames(*frames)
+        if recip is not None:
+            e.set_ewald_recip(*recip)
         te = e.build_neighbor_table(9.0, list_id=0)
         tv = e.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
         e.amoeba_step(tv, te, p)
@@ -96,6 +101,31 @@ def test_interior_halo_overlap_matches(mdg, size):
     for k in range(3):
         assert e1[k] == pytest.approx(en0[k], rel=1e-9)
     assert abs(i1 - it0) <= 1
+
+
+@pytest.mark.parametrize("size,polar_forces", [(2, True), (4, False), (8, True)])
+def test_domains_with_reciprocal_space(mdg, size, polar_forces):
+    """Full Ewald in the decomposed step (replicated grid: owned sites spread
+    per domain, grids summed, one transform, owned sites gathered): the
+    multipole PME, the reciprocal field in the PCG operator and right-hand
+    side and (with polarization forces) the combined permanent + induced
+    pass match the single engine with the same grid."""
+    s = mdg.water_box(1728, 37.26, 8, "amoeba")
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR
+    if polar_forces:
+        terms |= mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-6, 100, 1, terms)
+    lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
+    recip = ((40, 40, 40), 5)
+    en0, w0, it0, f0, mu0 = single(mdg, s, p, recip=recip)
+    F, MU, en, w, it = run_domains(mdg, s, size, p, lists, steps=2, recip=recip)
+    rms = np.sqrt(np.mean(f0 ** 2))
+    assert np.abs(F - f0).max() <= 1e-8 * rms
+    for k in range(3):
+        assert en[k] == pytest.approx(en0[k], rel=1e-9)
+    assert abs(it - it0) <= 1
+    d = np.sqrt(np.mean(np.sum((MU - mu0) ** 2, 1))) * mdg.DEBYE
+    assert d < 1e-6
 
 
 def test_domains_with_local_frames(mdg):
