@@ -381,20 +381,22 @@ struct TPArgs {
 
 // E_i = sum_j rr5 (v_j . R) R - rr3 v_j from the stored tensors; the PCG form
 // writes q = p/alpha - T p and the block partial of p.q.
-template <bool PCG>
+// SUB: the site subset of a.part (interior/halo overlap); its own
+// instantiation, so the plain mat-vec keeps its code
+template <bool PCG, bool SUB = false>
 __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
   if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
   const int lane = threadIdx.x & 31;
   double acc[1] = {0.0};
   int64_t nsub = a.n;
   const int32_t* map = nullptr;
-  if (a.part) {
+  if (SUB) {
     const int64_t nb = *a.nsel;
     nsub = a.part == 1 ? nb : a.n - nb;
     map = a.part == 1 ? a.sites : a.sites + nb;
   }
   MDG_SITE_LOOP(w, nsub, a.ipw) {
-    const int64_t i = map ? (int64_t)map[w] : w;
+    const int64_t i = SUB ? (int64_t)map[w] : w;
     const double4 pi = a.pos[i];
     const int cnt = a.pcnt[i];
     MDG_DASSERT(cnt >= 0 && cnt <= a.pcap);
@@ -896,7 +898,7 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
       k.part = 2;
       k.sites = d.c->dd_sites;
       k.nsel = d.c->dd_nsel;
-      k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, d.c->stream>>>(k);
+      k_tmatvec_pre<true, true><<<(unsigned)d.g, kBlock, 0, d.c->stream>>>(k);
     }
     comm->exchange_end();
   } else if (comm) {
@@ -910,7 +912,7 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
       k.sites = c->dd_sites;
       k.nsel = c->dd_nsel;
       k.partials = c->partials + (size_t)d.g * kRedVals;  // blocks g .. 2g - 1
-      k_tmatvec_pre<true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(k);
+      k_tmatvec_pre<true, true><<<(unsigned)d.g, kBlock, 0, c->stream>>>(k);
       c->launches++;
     } else if (d.cl) {
       cl_matvec_launch_raw(d.kc, (unsigned)d.g, c->stream);
