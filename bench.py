@@ -205,13 +205,14 @@ def hbm_peak():
 AUX_KERNELS = {"halgren", "chain_rule", "mpole"}
 
 
-def md_timing(wl, steps, barrier, device, respa=False):
+def md_timing(wl, steps, barrier, device, respa=False, aspc=False):
     """K steps of the workload on the device (mdg_md_run): ms/step and
     ns/day (flexible water: harmonic O-H bonds and H-O-H angles; AMOEBA runs
     include the polarization forces). Velocity Verlet at dt = 0.5 fs, or
     (respa) BAOAB-RESPA at the paper's 2 fs outer step with
     the bonded terms in 4 inner steps of 0.5 fs and a 1/ps Langevin bath at
-    300 K."""
+    300 K. aspc: the AMOEBA PCG starts from the ASPC-extrapolated dipoles
+    (the paper's Beeman/ASPC setup) instead of alpha E."""
     m = wl.m
     eng = wl.eng
     n_mol = wl.n // 3
@@ -249,6 +250,8 @@ def md_timing(wl, steps, barrier, device, respa=False):
         p = m.MDParams(1, steps, dt, 20, 0, 1, c["elec_cutoff"] + c["skin"],
                        c["vdw_cutoff"] + c["skin"], 1)
         kw = {"amoeba": ap}
+    if aspc and c["model"] != "charmm":
+        p.predictor = m.PREDICT_ASPC
     if respa:
         dt = p.dt_fs = 2.0
         p.integrator = m.INTEGRATOR_BAOAB_RESPA
@@ -266,14 +269,18 @@ def md_timing(wl, steps, barrier, device, respa=False):
     eng.timer_start()
     eng.md_run(p, energies=False, **kw)
     mms = eng.timer_stop()
+    last_iters = int(eng.fetch_energies()[2]) if c["model"] != "charmm" else None
     # (NVE conservation of both integrators and models is tested in
     # tests/test_md_integrator.py and tests/test_gpu_parity.py)
     what = ("device BAOAB-RESPA (outer: these forces; inner x4: flexible-water bonds/angles; "
             "Langevin 1/ps, 300 K)" if respa else
             "device velocity Verlet with these forces + flexible-water bonds/angles")
+    if p.predictor:
+        what += "; ASPC dipole predictor"
     return {"what": what + ("" if c["model"] == "charmm" else
                             " + polarization forces; multipoles x0.1 in local water frames"),
             "dt_fs": dt, "steps": steps, "ms_per_step": mms / steps,
+            "pcg_iters_last_step": last_iters,
             "ns_per_day": steps * dt * 1e-6 / (mms * 1e-3) * 86400.0}
 
 
@@ -516,10 +523,12 @@ def run_mine(args, world, rank, local):
     # device-resident MD (flexible water bonds/angles, 300 K start): velocity
     # Verlet at 0.5 fs, then BAOAB-RESPA at 2 fs; last, as it moves the
     # engine's coordinates
-    md = md_respa = None
+    md = md_respa = md_aspc = None
     if not args.no_md:
         eng.set_force_output(None)  # no per-step force DMA inside the MD loop
         md = md_timing(wl, args.steps, barrier, device)
+        if wl.c["model"] != "charmm":
+            md_aspc = md_timing(wl, args.steps, barrier, device, aspc=True)
         md_respa = md_timing(wl, args.steps, barrier, device, respa=True)
 
     out = {
@@ -546,6 +555,7 @@ def run_mine(args, world, rank, local):
         "with_polar_forces": polar_forces,
         "with_ewald_recip": with_recip,
         "md": md,
+        "md_aspc": md_aspc,
         "md_respa": md_respa,
         "gpu_launches": launches,
         "roofline": roof,

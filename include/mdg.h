@@ -282,7 +282,15 @@ typedef struct {
   double friction_ps;    /* BAOAB-RESPA: Langevin friction (1/ps); 0 = NVE RESPA */
   double temperature_k;  /* BAOAB-RESPA: bath temperature (K) */
   uint64_t seed;         /* BAOAB-RESPA: noise stream (counter-based, per caller site) */
+  int predictor;         /* AMOEBA: PCG start, MDG_PREDICT_NONE (alpha E) or _ASPC */
 } mdg_md_params;
+
+/* ASPC (Kolafa 2004, k = 4): the PCG of each step starts from the dipoles
+ * extrapolated from the last 6 converged ones (the paper's "Beeman/ASPC"
+ * production setup); the solve still runs to its tolerance. The history is
+ * kept within one mdg_md_run call and cleared by a re-sort. */
+#define MDG_PREDICT_NONE 0
+#define MDG_PREDICT_ASPC 1
 
 #define MDG_INTEGRATOR_VERLET 0
 #define MDG_INTEGRATOR_BAOAB_RESPA 1

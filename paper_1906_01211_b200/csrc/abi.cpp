@@ -311,7 +311,8 @@ int mdg_ctx_destroy(mdg_ctx* c) {
                   c->cell_atoms, c->d_flag, c->force, c->force2, c->torque, c->field, c->eperm,
                   c->mu, c->cg_r, c->cg_z, c->cg_p, c->cg_q, c->vin, c->pq4, c->partials,
                   c->results,
-                  c->d_stage, c->dd_sites, c->dd_flags, c->dd_nsel, c->dd_tmp};
+                  c->d_stage, c->dd_sites, c->dd_flags, c->dd_nsel, c->dd_tmp,
+                  c->aspc_hist};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& L : c->lists) {
@@ -1544,6 +1545,8 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
     need(c->has_vel, "md: upload masses and velocities first");
     need(c->n_own == c->n, "md: single domain only (no migration between domains)");
     need(p->nsteps >= 0 && p->dt_fs > 0 && p->rebuild_every >= 1, "md: bad step parameters");
+    need(p->predictor == MDG_PREDICT_NONE || p->predictor == MDG_PREDICT_ASPC,
+         "md: unknown dipole predictor");
     need(p->model == 0 ? cp != nullptr : (p->model == 1 && ap != nullptr),
          "md: model 0 needs charmm params, model 1 amoeba params");
     // no per-step force DMA inside the loop (the bonded terms are added after
@@ -1558,6 +1561,17 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
       }
     } nfo{c, {c->fout[0], c->fout[1], c->fout[2]}};
     for (int a = 0; a < 3; ++a) c->fout[a] = nullptr;
+    // ASPC dipole prediction for the PCG start (model 1, p->predictor)
+    struct AspcScope {
+      mdg_ctx* c;
+      ~AspcScope() {
+        c->aspc_on = false;
+        c->aspc_count = 0;
+      }
+    } aspc{c};
+    c->aspc_on = p->model == 1 && p->predictor == MDG_PREDICT_ASPC;
+    c->aspc_count = 0;
+    c->aspc_head = 0;
     // re-sort the sites by their current cells every MDG_RESORT-th list
     // rebuild (the gathers keep their locality as molecules diffuse: water
     // moves ~1 A per ps, the sort cells are 2 A; 0 = never). The default 20

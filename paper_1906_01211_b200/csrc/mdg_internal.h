@@ -28,7 +28,8 @@ namespace mdg {
 #ifndef MDG_BLOCK
 #define MDG_BLOCK 128
 #endif
-constexpr int kBlock = MDG_BLOCK;  // pair-kernel block: 4 warps = 4 site groups
+constexpr int kBlock = MDG_BLOCK;
+constexpr int kAspcDepth = 6;  // ASPC k = 4  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
 // device result slots: 0-9 nonpolar, 10-19 multipoles, 20-27 PCG, 30 Jacobi,
 // 40 polarization energy, 50-51 count_within, 60-63 list stats,
@@ -250,6 +251,11 @@ struct mdg_ctx {
   double4* vel = nullptr;
   double4* fbond = nullptr;  // inner-level (bonded) forces of BAOAB-RESPA
   int64_t md_rebuilds = 0;   // list rebuilds inside mdg_md_run (re-sort cadence)
+  // ASPC dipole predictor of mdg_md_run (polar.cu k_mu0_aspc): a ring of the
+  // last kAspcDepth converged dipole vectors (n_cap each)
+  bool aspc_on = false;
+  double4* aspc_hist = nullptr;
+  int aspc_head = 0, aspc_count = 0;
   bool has_vel = false;
   int2* bond_ij = nullptr;
   double2* bond_par = nullptr;  // (k, r0)

@@ -661,6 +661,39 @@ __global__ void k_mu0(int64_t n, const double2* __restrict__ polp, const double4
   }
 }
 
+// ASPC predictor (Kolafa, J. Comput. Chem. 25, 335 (2004); the
+// "Beeman/ASPC" setup of /root/reference/PAPER.md:783): the start of the
+// solve extrapolated from the last converged dipoles, newest first,
+// mu0 = sum_j B_j mu(t - j), B_j = (-1)^(j+1) j C(2k+4, k+2-j) / C(2k+2, k+1)
+// with k = 4 (6 vectors): 22/7, -55/14, 55/21, -22/21, 5/21, -1/42. With
+// fewer stored vectors the latest one is the start. The solve still runs to
+// its tolerance: only the iteration count changes.
+struct AspcHist {
+  const double4* h[kAspcDepth];  // newest first
+  int count;
+};
+
+__global__ void k_mu0_aspc(int64_t n, AspcHist hist, double4* __restrict__ mu) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (hist.count < kAspcDepth) {
+    const double4 v = hist.h[0][i];
+    mu[i] = make_double4(v.x, v.y, v.z, 0.0);
+    return;
+  }
+  constexpr double B[kAspcDepth] = {22.0 / 7.0,   -55.0 / 14.0, 55.0 / 21.0,
+                                    -22.0 / 21.0, 5.0 / 21.0,   -1.0 / 42.0};
+  double x = 0, y = 0, z = 0;
+#pragma unroll
+  for (int j = 0; j < kAspcDepth; ++j) {
+    const double4 v = hist.h[j][i];
+    x += B[j] * v.x;
+    y += B[j] * v.y;
+    z += B[j] * v.z;
+  }
+  mu[i] = make_double4(x, y, z, 0.0);
+}
+
 // a = r.z / p.q (global sums); mu += a p; r -= a q; z = alpha r;
 // partials: r.z, |a p|^2
 __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* __restrict__ polp,
@@ -1079,11 +1112,22 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
       ds[k].k.partials = c->partials;  // (ensure_partials may have moved it)
     }
   }
-  // mu0 = alpha E, its halo, T mu0, r0 / z0 / p0 and r0.z0
+  // mu0 = alpha E (or the ASPC prediction), its halo, T mu0, r0 / z0 / p0
+  // and r0.z0
+  const bool predict = doms.size() == 1 && !comm && c0->aspc_on && c0->aspc_count > 0;
   for (PcgDom& d : ds) {
     mdg_ctx* c = d.c;
-    MDG_LAUNCH(c, "cg_mu0", grid_for(c->n_own, 256), 256, 0, k_mu0, c->n_own, c->polp, c->eperm,
-               c->mu);
+    if (predict) {
+      AspcHist h{};
+      h.count = c->aspc_count;
+      for (int j = 0; j < kAspcDepth; ++j)
+        h.h[j] = c->aspc_hist + (size_t)((c->aspc_head - 1 - j + 2 * kAspcDepth) % kAspcDepth) *
+                                    c->n_cap;
+      MDG_LAUNCH(c, "cg_mu0", grid_for(c->n_own, 256), 256, 0, k_mu0_aspc, c->n_own, h, c->mu);
+    } else {
+      MDG_LAUNCH(c, "cg_mu0", grid_for(c->n_own, 256), 256, 0, k_mu0, c->n_own, c->polp,
+                 c->eperm, c->mu);
+    }
   }
   if (comm) comm->exchange(MDG_VEC_MU);
   for (PcgDom& d : ds) {
@@ -1205,6 +1249,16 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
   *last_rms = c0->h_results[25];
   if (c0->h_results[27] == 0.0)
     throw_error(MDG_CONVERGENCE, "polar_solve_pcg: no convergence after max_iter");
+  if (doms.size() == 1 && !comm && c0->aspc_on) {  // keep the converged dipoles
+    if (!c0->aspc_hist)
+      MDG_CUDA_CHECK(cudaMalloc(&c0->aspc_hist,
+                                (size_t)kAspcDepth * c0->n_cap * sizeof(double4)));
+    MDG_CUDA_CHECK(cudaMemcpyAsync(c0->aspc_hist + (size_t)c0->aspc_head * c0->n_cap, c0->mu,
+                                   (size_t)c0->n_own * sizeof(double4),
+                                   cudaMemcpyDeviceToDevice, c0->stream));
+    c0->aspc_head = (c0->aspc_head + 1) % kAspcDepth;
+    c0->aspc_count = std::min(c0->aspc_count + 1, kAspcDepth);
+  }
   return it;
 }
 

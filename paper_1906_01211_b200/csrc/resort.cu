@@ -191,6 +191,9 @@ void resort_sites(mdg_ctx* c) {
   // results of the last step stay fetchable
   for (double4* v : {c->force, c->torque, c->mu, c->eperm})
     permute_array<double4, 1>(c, ord, v, tmp);
+  // the ASPC history of converged dipoles (mdg_md_run)
+  for (int j = 0; j < c->aspc_count; ++j)
+    permute_array<double4, 1>(c, ord, c->aspc_hist + (size_t)j * c->n_cap, tmp);
   if (c->has_frames) {
     permute_array<double4, 3>(c, ord, c->mploc, tmp);
     permute_array<int4, 1>(c, ord, c->frame, tmp);

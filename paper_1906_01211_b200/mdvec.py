@@ -204,6 +204,8 @@ TERM_VDW, TERM_MPOLE, TERM_POLAR, TERM_POLAR_FORCE = 1, 2, 4, 8
 
 INTEGRATOR_VERLET = 0
 INTEGRATOR_BAOAB_RESPA = 1
+PREDICT_NONE = 0
+PREDICT_ASPC = 1
 
 
 class MDParams(C.Structure):
@@ -215,7 +217,7 @@ class MDParams(C.Structure):
                 # zero defaults keep velocity Verlet
                 ("integrator", C.c_int), ("inner_steps", C.c_int),
                 ("friction_ps", C.c_double), ("temperature_k", C.c_double),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("predictor", C.c_int)]
 
 
 _lib = None

@@ -234,3 +234,30 @@ def test_amoeba_respa_nve_conserves_energy(engine, mdg):
     et = ek + ep
     assert np.all(np.isfinite(et))
     assert (et.max() - et.min()) <= 3e-3 * ek.mean(), (et.max() - et.min(), ek.mean())
+
+
+@pytest.mark.gpu
+def test_aspc_predictor_same_dynamics_fewer_iterations(engine, mdg, monkeypatch):
+    """ASPC (mdg_md_params.predictor): the PCG of each MD step starts from
+    dipoles extrapolated from the last six converged ones. The solve still
+    runs to its tolerance, so the trajectory is the one without the
+    predictor to within that tolerance, in fewer iterations. The sites are
+    re-sorted at every list rebuild (the stored dipoles follow them)."""
+    monkeypatch.setenv("MDG_RESORT", "1")
+    out = {}
+    for pred in (mdg.PREDICT_NONE, mdg.PREDICT_ASPC):
+        _amoeba_water(engine, mdg)
+        p = mdg.MDParams(1, 40, 0.25, 10, 0, 1, 7.3, 9.3, 1)
+        p.predictor = pred
+        try:
+            ek, ep = engine.md_run(p, amoeba=_amoeba_params(mdg))
+            e, w, it, rms = engine.fetch_energies()
+            out[pred] = (engine.fetch_positions(), ek + ep, it)
+        finally:
+            engine.upload_frames(None, None, None)
+    (x0, e0, it0), (x1, e1, it1) = out[mdg.PREDICT_NONE], out[mdg.PREDICT_ASPC]
+    d = x1 - x0
+    d -= 18.6 * np.rint(d / 18.6)
+    assert np.abs(d).max() <= 1e-6
+    np.testing.assert_allclose(e1, e0, rtol=1e-7)
+    assert it1 < it0, (it1, it0)
