@@ -211,6 +211,9 @@ class DomainGroup:
     def __init__(self, s, size: int, halo_width: float, device: int = 0, backend: str = "local",
                  rank: int = 0, plans=None, list_cutoff: float | None = None,
                  overlap: bool | None = None):
+        self._args = dict(size=size, halo_width=halo_width, device=device, backend=backend,
+                          rank=rank, list_cutoff=list_cutoff, overlap=overlap)
+        self._frames = self._recip = None
         self.lib = M.load_library()
         self.backend, self.size, self.rank = backend, size, rank
         self.halo_width = float(halo_width)
@@ -272,8 +275,25 @@ class DomainGroup:
         M.check(self.lib.mdg_group_exchange(self.g, vec_id))
 
     def upload_frames(self, frame, zatom, xatom, dipole, quadrupole):
+        self._frames = (frame, zatom, xatom, dipole, quadrupole)
         for d in self.domains:
             d.upload_frames(frame, zatom, xatom, dipole, quadrupole)
+
+    def replan(self, s):
+        """Molecule migration by re-planning: after sites moved past the
+        halo margin (HaloStale), rebuild the decomposition from the global
+        system `s` at its current coordinates -- ownership by the anchor
+        site's subdomain, halos, contexts, the group -- and re-apply the
+        frames and the reciprocal-space grid. Collective over the ranks of an
+        NCCL group (every rank passes the same global coordinates). The
+        neighbour lists are rebuilt by the caller (build_lists)."""
+        frames, recip = self._frames, self._recip
+        self.close()
+        self.__init__(s, **self._args)
+        if frames is not None:
+            self.upload_frames(*frames)
+        if recip is not None:
+            self.set_ewald_recip(*recip)
 
     def set_ewald_recip(self, grid=(0, 0, 0), order: int = 6):
         """Reciprocal-space Ewald in the decomposed AMOEBA step (every domain
@@ -281,6 +301,7 @@ class DomainGroup:
         summed over the domains (one device: a kernel; NCCL: an all-reduce),
         the sum is transformed once per device and every domain gathers its
         owned sites -- a replicated grid, not a distributed FFT."""
+        self._recip = (grid, order)
         for d in self.domains:
             d.eng.set_ewald_recip(grid, order)
 

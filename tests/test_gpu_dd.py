@@ -216,3 +216,50 @@ def test_nccl_group_world_size_one(mdg):
     assert it == it0 and rms < 1e-5
     for k in range(3):
         assert en[k] == pytest.approx(en0[k], rel=1e-12)
+
+
+def test_domains_replan_after_migration(mdg):
+    """Molecules moved past the halo margin (whole molecules shifted by 3 A,
+    so many change domain): update_positions refuses, replan rebuilds the
+    decomposition at the new coordinates (frames and reciprocal space
+    re-applied), and the step equals the single engine there."""
+    from oracle import frames as fr
+    from paper_1906_01211_b200 import dd
+    s = mdg.water_box(1728, 37.26, 9, "amoeba")
+    frame, za, xa = fr.water_frames(s.molecule)
+    frames = (frame, za, xa, np.asarray(s.dipole), np.asarray(s.quadrupole))
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-6, 100, 1, terms)
+    lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
+    recip = ((40, 40, 40), 5)
+    L = s.box[0]
+    mol = np.asarray(s.molecule)
+    shift = np.random.default_rng(2).uniform(-3, 3, (mol.max() + 1, 3))[mol]
+    x = np.mod(np.asarray(s.x) + shift[:, 0], L)
+    y = np.mod(np.asarray(s.y) + shift[:, 1], L)
+    z = np.mod(np.asarray(s.z) + shift[:, 2], L)
+    s2 = mdg.water_box(1728, 37.26, 9, "amoeba")
+    s2.x, s2.y, s2.z = x, y, z
+    g = dd.DomainGroup(s, 2, HALO, backend="local", list_cutoff=11.0)
+    try:
+        g.upload_frames(*frames)
+        g.set_ewald_recip(*recip)
+        g.amoeba_step(g.build_lists(lists), p)
+        owned_before = [d.plan.owned.copy() for d in g.domains]
+        with pytest.raises(dd.HaloStale):
+            g.update_positions(x, y, z)
+        g.replan(s2)
+        assert any(not np.array_equal(d.plan.owned, o) for d, o in zip(g.domains, owned_before))
+        assert g.check_halo(s2)
+        g.amoeba_step(g.build_lists(lists), p)
+        en, _, it, _ = g.energies()
+        ids, f = g.owned_forces()
+    finally:
+        g.close()
+    en0, _, it0, f0, _ = single(mdg, s2, p, frames, recip)
+    F = np.zeros_like(f0)
+    F[ids] = f
+    assert np.abs(F - f0).max() <= 1e-8 * np.sqrt(np.mean(f0 ** 2))
+    for k in range(3):
+        assert en[k] == pytest.approx(en0[k], rel=1e-9)
+    assert abs(it - it0) <= 1
