@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-recip", action="store_true",
                     help="skip the extra timing of the step with reciprocal-space Ewald")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dd-nccl", action="store_true",
+                    help="run the decomposed NCCL path even at one rank (under torchrun "
+                         "--nproc-per-node 1): a self-test of the multi-GPU code path")
     return ap.parse_args()
 
 
@@ -818,7 +821,7 @@ def main():
         out = run_dd(args, 1, 0, 0, "local", args.gpus)
         print(json.dumps(out), flush=True)
         return
-    if world > 1:
+    if world > 1 or (args.dd_nccl and "MASTER_ADDR" in os.environ):
         import torch
         import torch.distributed as dist
         assert args.gpus in (1, world), f"--gpus {args.gpus} under a world of {world} ranks"

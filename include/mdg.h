@@ -78,6 +78,10 @@ int mdg_system_upload(mdg_ctx* ctx, int64_t n, double lx, double ly, double lz,
                       const double* hal_epsilon, const double* polarizability);
 /* New coordinates for the same sites (one MD step's input). Lists are kept. */
 int mdg_positions_upload(mdg_ctx* ctx, const double* x, const double* y, const double* z);
+/* Domain contexts: the owned sites' coordinates only (n_own entries, the
+ * owned part of the caller order); the halo follows from
+ * mdg_group_exchange(g, MDG_VEC_POS). */
+int mdg_positions_upload_owned(mdg_ctx* ctx, const double* x, const double* y, const double* z);
 /* Topology (no reference counterpart): molecule ids (exclusion groups; NULL =
  * every site its own group) and the Halgren reduction parent/factor (NULL =
  * no reduction: vdW sites = atoms). */

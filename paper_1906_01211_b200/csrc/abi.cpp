@@ -150,8 +150,11 @@ static bool is_pinned(const void* p) {
 // the DMA (one pass over 24 B/site in HBM instead of a host pass competing
 // with the DMA for the same pages), staged ones on the host during the copy.
 // Returns with the caller's arrays no longer in use.
-void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double* box = nullptr) {
-  const int64_t n = c->n;
+// (count >= 0: the first `count` caller-order sites only, staged with stride
+// count -- the owned sites of a domain)
+void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double* box = nullptr,
+              int64_t count = -1) {
+  const int64_t n = count >= 0 ? count : c->n;
   bool pinned = true;
   for (const double* a : arrays) pinned = pinned && is_pinned(a);
   if (pinned) {
@@ -159,7 +162,7 @@ void stage_in(mdg_ctx* c, const std::vector<const double*>& arrays, const double
       MDG_CUDA_CHECK(cudaMemcpyAsync(c->d_stage + a * n, arrays[a], n * sizeof(double),
                                      cudaMemcpyHostToDevice, c->stream));
     if (box) {  // box is the context's (c->lx, c->ly, c->lz)
-      need(mdg::check_box_staged(c) < 0, "ParticleSystem: position outside the box");
+      need(mdg::check_box_staged(c, n) < 0, "ParticleSystem: position outside the box");
     } else {
       MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     }
@@ -565,6 +568,17 @@ int mdg_positions_upload(mdg_ctx* c, const double* x, const double* y, const dou
     const double L[3] = {c->lx, c->ly, c->lz};
     stage_in(c, {x, y, z}, L);
     mdg::pack_positions(c);
+  });
+}
+
+int mdg_positions_upload_owned(mdg_ctx* c, const double* x, const double* y, const double* z) {
+  return guard([&] {
+    need_system(c);
+    set_device(c);
+    need(x && y && z, "null position array");
+    const double L[3] = {c->lx, c->ly, c->lz};
+    stage_in(c, {x, y, z}, L, c->n_own);
+    mdg::pack_positions(c, c->n_own);
   });
 }
 

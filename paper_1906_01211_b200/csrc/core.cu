@@ -278,9 +278,10 @@ __global__ void k_check_box(int64_t n, const double* __restrict__ st, double lx,
   if (!ok) atomicMin(&flag[6], (int32_t)o);
 }
 
-int64_t check_box_staged(mdg_ctx* c) {
+int64_t check_box_staged(mdg_ctx* c, int64_t count) {
+  const int64_t n = count >= 0 ? count : c->n;
   MDG_CUDA_CHECK(cudaMemsetAsync(c->d_flag + 6, 0x7f, sizeof(int32_t), c->stream));
-  MDG_LAUNCH(c, "check_box", grid_for(c->n, 256), 256, 0, k_check_box, c->n, c->d_stage, c->lx,
+  MDG_LAUNCH(c, "check_box", grid_for(n, 256), 256, 0, k_check_box, n, c->d_stage, c->lx,
              c->ly, c->lz, c->d_flag);
   int32_t bad = 0;
   MDG_CUDA_CHECK(cudaMemcpyAsync(&bad, c->d_flag + 6, sizeof(int32_t), cudaMemcpyDeviceToHost,
@@ -333,9 +334,12 @@ __global__ void k_copy_vsite(int64_t n, const double4* __restrict__ pos, double4
   if (s < n) vsite[s] = pos[s];
 }
 
-void pack_positions(mdg_ctx* c) {
-  MDG_LAUNCH(c, "pack_positions", grid_for(c->n, 256), 256, 0, k_pack_positions, c->n,
-             c->d_perm, c->d_stage, c->pos, c->vsite, c->has_hred ? 0 : 1);
+void pack_positions(mdg_ctx* c, int64_t count) {
+  // count >= 0: the owned sites (sorted first, and first in caller order),
+  // staged with stride count; the halo comes from the group's exchange
+  const int64_t n = count >= 0 ? count : c->n;
+  MDG_LAUNCH(c, "pack_positions", grid_for(n, 256), 256, 0, k_pack_positions, n, c->d_perm,
+             c->d_stage, c->pos, c->vsite, c->has_hred ? 0 : 1);
   if (c->has_hred) run_reduce_sites(c);
 }
 

@@ -185,6 +185,8 @@ struct mdg_group : PcgComm {
   std::vector<LocalHalo> lh;
   double4** d_vecs = nullptr;  // [6][ndom] vector base pointers
   double** d_res = nullptr;    // [ndom] result slots
+  std::vector<double4*> h_vecs;  // host copies of the two tables
+  std::vector<double*> h_res;
   // NCCL
   ncclComm_t comm = nullptr;
   struct Peer {
@@ -343,12 +345,17 @@ void refresh_tables(mdg_group* g) {
   for (int v = 0; v < 6; ++v)
     for (int d = 0; d < nd; ++d) vecs[(size_t)v * nd + d] = vec_by_id(g->dom[d], v);
   for (int d = 0; d < nd; ++d) res[d] = g->dom[d]->results;
+  // unchanged tables: no copy (a synchronous copy per exchange would stall
+  // the host's run-ahead)
+  if (g->d_vecs && vecs == g->h_vecs && res == g->h_res) return;
   if (!g->d_vecs) MDG_CUDA_CHECK(cudaMalloc(&g->d_vecs, vecs.size() * sizeof(double4*)));
   if (!g->d_res) MDG_CUDA_CHECK(cudaMalloc(&g->d_res, res.size() * sizeof(double*)));
   MDG_CUDA_CHECK(cudaMemcpy(g->d_vecs, vecs.data(), vecs.size() * sizeof(double4*),
                             cudaMemcpyHostToDevice));
   MDG_CUDA_CHECK(cudaMemcpy(g->d_res, res.data(), res.size() * sizeof(double*),
                             cudaMemcpyHostToDevice));
+  g->h_vecs = vecs;
+  g->h_res = res;
 }
 
 }  // namespace
@@ -541,8 +548,8 @@ int mdg_group_exchange(mdg_group* g, int vec_id) {
     gneed(vec_id >= 0 && vec_id < 6, "group_exchange: unknown vector id");
     MDG_CUDA_CHECK(cudaSetDevice(g->dom[0]->device));
     if (g->backend == MDG_GROUP_LOCAL) refresh_tables(g);
+    // stream-ordered: the next step (or a fetch) sees the refreshed halo
     g->exchange_vec(vec_id, false, g->stream());
-    MDG_CUDA_CHECK(cudaStreamSynchronize(g->stream()));
   });
 }
 

@@ -562,11 +562,11 @@ double4* vec_by_id(mdg_ctx* c, int vec_id);
 void vec_pack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count, double* d_out);
 void vec_unpack(mdg_ctx* c, int vec_id, const int32_t* d_sites, int64_t count,
                 const double* d_in);
-void pack_positions(mdg_ctx* c);
+void pack_positions(mdg_ctx* c, int64_t count = -1);
 // pos.w / vsite.w <- mol (after a topology upload)
 void set_groups(mdg_ctx* c);
 // device check of staged positions against the box; first bad caller index or -1
-int64_t check_box_staged(mdg_ctx* c);
+int64_t check_box_staged(mdg_ctx* c, int64_t count = -1);
 void polar_energy(mdg_ctx* c, double electric, int slot);
 
 }  // namespace mdg

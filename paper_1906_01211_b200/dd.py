@@ -319,8 +319,14 @@ class DomainGroup:
         Raises HaloStale when a site has moved past half the halo margin since
         the plan was built (checked on the device, max over all domains)."""
         for dom in self.domains:
-            loc = dom.plan.local
-            dom.eng.upload_positions(np.asarray(x)[loc], np.asarray(y)[loc], np.asarray(z)[loc])
+            # owned coordinates only, gathered into page-locked buffers (DMA'd
+            # without staging); the halo comes from the owners below
+            own = dom.plan.owned
+            if getattr(dom, "_xyz", None) is None:
+                dom._xyz = M.host_array((3, len(own)))
+            for a, v in enumerate((x, y, z)):
+                np.take(np.asarray(v, np.float64), own, out=dom._xyz[a])
+            dom.eng.upload_positions_owned(dom._xyz[0], dom._xyz[1], dom._xyz[2])
         moved = self.max_displacement()
         if moved > self.margin:
             raise HaloStale(f"a site moved {moved:.3f} A since the plan was built "

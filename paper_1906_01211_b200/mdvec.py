@@ -153,6 +153,7 @@ SIGNATURES = {
     "mdg_group_create_nccl": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int64]),
     "mdg_group_destroy": (C.c_int, [C.c_void_p]),
+    "mdg_positions_upload_owned": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_group_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_group_set_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _ip, _ip, _ip]),
     "mdg_group_set_halo_nccl": (C.c_int, [C.c_void_p, C.c_int, _ip, _i64p, _ip, _i64p, _ip]),
@@ -438,6 +439,12 @@ class Engine:
     def upload_positions(self, x, y, z):
         x, y, z = _f64(x), _f64(y), _f64(z)
         check(self.lib.mdg_positions_upload(self.ctx, _p(x), _p(y), _p(z)))
+
+    def upload_positions_owned(self, x, y, z):
+        """A domain context's owned coordinates (mdg_positions_upload_owned);
+        page-locked arrays (host_array) are DMA'd without a staging copy."""
+        x, y, z = _f64(x), _f64(y), _f64(z)
+        check(self.lib.mdg_positions_upload_owned(self.ctx, _p(x), _p(y), _p(z)))
 
     def upload_topology(self, molecule=None, hred_parent=None, hred_factor=None):
         m = None if molecule is None else np.ascontiguousarray(molecule, np.int32)
