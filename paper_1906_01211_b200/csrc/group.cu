@@ -24,6 +24,13 @@
 //    loaded at run time (dlopen libnccl.so.2 -- the copy torch already
 //    loaded, else the system one). Iterations are queued in batches ahead of
 //    the device (polar.cu).
+// Two further operations serve the solve:
+//  * interior/halo overlap (exchange_begin / exchange_end): the refresh runs
+//    on the group's own highest-priority stream while the domains' stream
+//    computes the rows without halo sites (polar.cu pcg_body);
+//  * the replicated reciprocal-space grid (grid_sum): LOCAL adds the other
+//    domains' grids into the first one (one fixed-order kernel), NCCL
+//    all-reduces each rank's grid in place (pme.cu PmeDoms).
 // Reference: none (the reference is single-process);
 // the model is Tinker-HP's spatial decomposition.
 #include <dlfcn.h>
