@@ -269,9 +269,11 @@ def md_timing(wl, steps, barrier, device, respa=False, aspc=False):
     if barrier:
         barrier()
     eng.synchronize()
+    r0 = eng.md_rebuild_count()
     eng.timer_start()
     eng.md_run(p, energies=False, **kw)
     mms = eng.timer_stop()
+    rebuilds = eng.md_rebuild_count() - r0
     last_iters = int(eng.fetch_energies()[2]) if c["model"] != "charmm" else None
     # (NVE conservation of both integrators and models is tested in
     # tests/test_md_integrator.py and tests/test_gpu_parity.py)
@@ -284,6 +286,9 @@ def md_timing(wl, steps, barrier, device, respa=False, aspc=False):
                             " + polarization forces; multipoles x0.1 in local water frames"),
             "dt_fs": dt, "steps": steps, "ms_per_step": mms / steps,
             "pcg_iters_last_step": last_iters,
+            # incl. the one at the start of the call; more than steps /
+            # rebuild_every + 1 when sites moved fast (motion-triggered)
+            "list_rebuilds": rebuilds, "rebuild_every": p.rebuild_every,
             "ns_per_day": steps * dt * 1e-6 / (mms * 1e-3) * 86400.0}
 
 

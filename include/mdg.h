@@ -315,6 +315,12 @@ typedef struct {
  * with polarization for conservative dynamics. */
 int mdg_md_run(mdg_ctx* ctx, const mdg_md_params* p, const mdg_charmm_params* charmm,
                const mdg_amoeba_params* amoeba, double* ekin, double* epot);
+/* List rebuilds done by mdg_md_run so far (all calls): rebuild_every is the
+ * longest interval; a rebuild comes earlier when the device has seen a site
+ * move 0.6 x the motion its list tolerates (half of list cutoff minus the
+ * kernel's cutoff and row buffer) since the build. A list walked past that
+ * tolerance would miss pairs: result reads then fail with MDG_CONTRACT. */
+int mdg_md_rebuild_count(mdg_ctx* ctx, int64_t* count);
 
 /* Spatial re-sort on the device: the sites are re-keyed by their current
  * ~2 A Morton cells and every per-site array is permuted (index arrays

@@ -285,6 +285,9 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       dalloc(&c->results, mdg::kResultSlots);
       MDG_CUDA_CHECK(cudaMemset(c->results, 0, mdg::kResultSlots * sizeof(double)));
       MDG_CUDA_CHECK(cudaMallocHost(&c->h_results, mdg::kResultSlots * sizeof(double)));
+      MDG_CUDA_CHECK(cudaHostAlloc(&c->h_warn, sizeof(int32_t), cudaHostAllocMapped));
+      *c->h_warn = 0;
+      MDG_CUDA_CHECK(cudaHostGetDevicePointer(&c->d_warn, c->h_warn, 0));
       c->stage_bytes = 12 * n * sizeof(double);
       MDG_CUDA_CHECK(cudaMallocHost(&c->h_stage, c->stage_bytes));
       dalloc(&c->d_stage, 12 * n);
@@ -321,6 +324,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   for (auto& L : c->lists) {
     if (L.nbr) cudaFree(L.nbr);
     if (L.cnt) cudaFree(L.cnt);
+    if (L.ref0) cudaFree(L.ref0);
     for (void* p : {(void*)L.inner.nbr, (void*)L.inner.cnt, (void*)L.inner.ref, (void*)L.inner.flag})
       if (p) cudaFree(p);
     if (L.inner.hcuts) cudaFreeHost(L.inner.hcuts);
@@ -331,6 +335,7 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->plist.ucl) cudaFree(c->plist.ucl);
   if (c->plist.ucnt) cudaFree(c->plist.ucnt);
   if (c->h_results) cudaFreeHost(c->h_results);
+  if (c->h_warn) cudaFreeHost(c->h_warn);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto& pe : c->pending) {
     cudaEventDestroy(pe.a);
@@ -891,6 +896,7 @@ int mdg_nlist_import(mdg_ctx* c, int list_id, double list_cutoff, int sites,
     L.sites = sites;
     L.max_cnt = mx;
     L.half_pairs = sum / 2;
+    mdg::list_snapshot(c, list_id);
   });
 }
 
@@ -1592,9 +1598,18 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
     // is every 200 fs at the usual 10 fs between rebuilds; a re-sort costs
     // about a third of a config-4 step.
     const int resort = mdg::env_int("MDG_RESORT", 20);
+    // a rebuild is due on schedule, or early when the device has flagged a
+    // site past 0.6 x its list's tolerable motion (read without a sync: the
+    // flag may lag the device by the steps the host has queued ahead)
+    // (the warning carries the generation of the lists it is about: a late
+    // one about lists already replaced is ignored)
+    auto due = [&](int64_t s) {
+      return (s + 1) % p->rebuild_every == 0 || *(volatile int32_t*)c->h_warn == c->list_gen;
+    };
     auto rebuild = [&] {
       // counted across mdg_md_run calls (a trajectory run in chunks)
-      if (resort > 0 && ++c->md_rebuilds % resort == 0) mdg::resort_sites(c);
+      ++c->md_rebuilds;
+      if (resort > 0 && c->md_rebuilds % resort == 0) mdg::resort_sites(c);
       mdg::nlist_build(c, p->elec_list, p->elec_list_cutoff, MDG_SITES_ATOMIC);
       if (p->model == 1) mdg::nlist_build(c, p->vdw_list, p->vdw_list_cutoff, MDG_SITES_VDW);
     };
@@ -1631,7 +1646,7 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
       for (int64_t s = 0; s < p->nsteps; ++s) {
         mdg::run_kick(c, 0.5 * dt);
         mdg::run_drift(c, dt);
-        if ((s + 1) % p->rebuild_every == 0) rebuild();
+        if (due(s)) rebuild();
         forces(p->bonded);
         mdg::run_kick(c, 0.5 * dt);
         report(s);
@@ -1667,7 +1682,7 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
           inner_forces();
           mdg::run_kick(c, 0.5 * h, c->fbond);
         }
-        if ((s + 1) % p->rebuild_every == 0) {
+        if (due(s)) {
           rebuild();
           inner_forces();  // a re-sort permuted the sites under c->fbond
         }
@@ -1676,7 +1691,16 @@ int mdg_md_run(mdg_ctx* c, const mdg_md_params* p, const mdg_charmm_params* cp,
         report(s);
       }
     }
-    MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    mdg::fetch_results(c);
+    mdg::check_lists_fresh(c);  // (rebuild_every too long for this motion)
+  });
+}
+
+int mdg_md_rebuild_count(mdg_ctx* c, int64_t* count) {
+  return guard([&] {
+    need_ctx(c);
+    need(count != nullptr, "md_rebuild_count: null output");
+    *count = c->md_rebuilds;
   });
 }
 
@@ -1795,6 +1819,7 @@ int mdg_fetch_energies(mdg_ctx* c, double* energies4, double* virial9, int64_t* 
     need_system(c);
     double e[4], w[9];
     energies_of(c, e, w);
+    mdg::check_lists_fresh(c);
     e[0] += c->debug_perturb;
     if (energies4) std::memcpy(energies4, e, sizeof e);
     if (virial9) std::memcpy(virial9, w, sizeof w);

@@ -29,7 +29,8 @@ namespace mdg {
 #define MDG_BLOCK 128
 #endif
 constexpr int kBlock = MDG_BLOCK;
-constexpr int kAspcDepth = 6;  // ASPC k = 4  // pair-kernel block: 4 warps = 4 site groups
+constexpr int kAspcDepth = 6;  // ASPC k = 4
+constexpr int kStaleSlot = 120;  // results 120..123: list l outdated (nlist.cu)  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
 // device result slots: 0-9 nonpolar, 10-19 multipoles, 20-27 PCG, 30 Jacobi,
 // 40 polarization energy, 50-51 count_within, 60-63 list stats,
@@ -58,6 +59,7 @@ struct DevList {
   int32_t cap = 0;              // ELL width (slots per site)
   int32_t* nbr = nullptr;
   int32_t* cnt = nullptr;
+  double4* ref0 = nullptr;      // site positions at the build (staleness check)
   size_t nbr_elems = 0;
   int64_t half_pairs = 0;
   int32_t max_cnt = 0;
@@ -251,6 +253,13 @@ struct mdg_ctx {
   double4* vel = nullptr;
   double4* fbond = nullptr;  // inner-level (bonded) forces of BAOAB-RESPA
   int64_t md_rebuilds = 0;   // list rebuilds inside mdg_md_run (re-sort cadence)
+  // early warning of list staleness (nlist.cu): set by the device when a site
+  // has moved more than 0.6 x the tolerable motion since its list was built;
+  // mapped page-locked memory, read by mdg_md_run without a sync to rebuild
+  // ahead of schedule
+  int32_t* h_warn = nullptr;
+  int32_t* d_warn = nullptr;
+  int32_t list_gen = 0;  // bumped by every list build: the warning names the lists it is about
   // ASPC dipole predictor of mdg_md_run (polar.cu k_mu0_aspc): a ring of the
   // last kAspcDepth converged dipole vectors (n_cap each)
   bool aspc_on = false;
@@ -518,6 +527,10 @@ void frame_torques_to_forces(mdg_ctx* c);
 void run_pme(mdg_ctx* c, double alpha, int k1, int k2, int k3, int order, double electric,
              bool exclude);
 void pme_free(mdg_ctx* c);
+// list staleness (nlist.cu): positions snapshot at build / import; host check
+// of the fetched results (throws MDG_CONTRACT)
+void list_snapshot(mdg_ctx* c, int list_id);
+void check_lists_fresh(const mdg_ctx* c);
 // smooth PME for permanent multipoles (q, mu, Theta): adds forces and torques;
 // results 80 (recip), 88 (excluded pairs), 98 (recip from the gathered
 // potentials), 104-106 (sums of q^2, |mu|^2, Q:Q for the self energy)

@@ -591,6 +591,7 @@ void nlist_build(mdg_ctx* c, int list_id, double list_cutoff, int sites) {
       L.sites = sites;
       L.max_cnt = mx;
       L.half_pairs = sum / 2;
+      list_snapshot(c, list_id);
       debug_check_rows(c, "list", L.nbr, L.cnt, L.cap, rows, c->n, false);
       return;
     }
@@ -630,6 +631,13 @@ struct CutArgs {
   int32_t* __restrict__ cuts;  // mapped host counter
   int32_t* __restrict__ gen;   // device cut generation
   double* __restrict__ partials;  // unused (launch macro contract)
+  // list staleness: sites' positions when the source list was built, the
+  // largest motion the cut can tolerate (squared), the sticky result slot
+  const double4* __restrict__ ref0;
+  double lim0_2, warn0_2;
+  double* __restrict__ stale;
+  int32_t* __restrict__ warn;
+  int32_t gen0;  // list generation the warning refers to
 };
 
 // When *flag: every owned row keeps its slots with r^2 <= rc^2 (the
@@ -644,6 +652,13 @@ __global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
   for (int64_t s = tid; s < a.n_all; s += (int64_t)gridDim.x * blockDim.x) a.ref[s] = a.P[s];
   MDG_SITE_LOOP(i, a.n_rows, a.ipw) {
     const double4 pi = a.P[i];
+    if (lane == 0 && a.ref0) {  // the source list misses pairs once a site moved too far
+      const double4 r0 = a.ref0[i];
+      double dx, dy, dz;
+      const double d2 = min_image(a.b, pi.x, pi.y, pi.z, r0.x, r0.y, r0.z, dx, dy, dz);
+      if (d2 > a.lim0_2) *a.stale = 1.0;
+      if (d2 > a.warn0_2 && a.warn) *a.warn = a.gen0;
+    }
     const int c = a.src.cnt[i];
     const int32_t* row = list_row(a.src, i);
     int32_t* out = a.nbr + (size_t)i * a.src.cap;
@@ -665,10 +680,56 @@ __global__ void __launch_bounds__(kBlock) k_cut_rows(CutArgs a) {
   }
 }
 
+// A kernel walking list rows with cutoff rc sees every pair within rc only
+// while no site has moved more than (list cutoff - rc) / 2 since the list
+// was built: past that, result slot kStaleSlot + list id turns 1 (sticky
+// until the list is rebuilt; the host raises MDG_CONTRACT at its next read
+// of the results, check_lists_fresh).
+__global__ void k_list_motion(int64_t n, Box b, const double4* __restrict__ P,
+                              const double4* __restrict__ ref0, double lim2, double warn2,
+                              double* __restrict__ stale, int32_t* __restrict__ warn,
+                              int32_t gen) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (s < n) {
+    const double4 p = P[s], r = ref0[s];
+    double dx, dy, dz;
+    d2 = min_image(b, p.x, p.y, p.z, r.x, r.y, r.z, dx, dy, dz);
+  }
+  if (__any_sync(0xffffffffu, d2 > lim2) && (threadIdx.x & 31) == 0) *stale = 1.0;
+  if (__any_sync(0xffffffffu, d2 > warn2) && (threadIdx.x & 31) == 0 && warn) *warn = gen;
+}
+
+// positions at the build of list_id (the staleness reference)
+void list_snapshot(mdg_ctx* c, int list_id) {
+  DevList& L = c->lists[list_id];
+  if (!L.ref0) MDG_CUDA_CHECK(cudaMalloc(&L.ref0, (size_t)c->n_cap * sizeof(double4)));
+  const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+  MDG_CUDA_CHECK(cudaMemcpyAsync(L.ref0, P, (size_t)c->n * sizeof(double4),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+  MDG_CUDA_CHECK(cudaMemsetAsync(c->results + kStaleSlot + list_id, 0, sizeof(double), c->stream));
+  ++c->list_gen;
+}
+
+void check_lists_fresh(const mdg_ctx* c) {
+  for (int l = 0; l < MDG_MAX_LISTS; ++l)
+    if (c->h_results[kStaleSlot + l] != 0.0)
+      throw_error(MDG_CONTRACT, "neighbour list " + std::to_string(l) +
+                                    " outdated: sites moved more than half its skin since it was "
+                                    "built (rebuild it more often)");
+}
+
 ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   DevList& L = c->lists[list_id];
   auto full_rows = [&] {
     if (!L.sorted) L.sorted = sort_rows(c, L.nbr, L.cnt, L.cap, L.max_cnt);
+    if (L.ref0 && L.cutoff > rc) {
+      const double lim = 0.5 * (L.cutoff - rc);
+      const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
+      MDG_LAUNCH(c, "list_motion", grid_for(c->n, 256), 256, 0, k_list_motion, c->n,
+                 make_box(c->lx, c->ly, c->lz), P, (const double4*)L.ref0, lim * lim,
+                 0.36 * lim * lim, c->results + kStaleSlot + list_id, c->d_warn, c->list_gen);
+    }
     return ListView{L.nbr, L.cnt, L.cap, L.sorted};
   };
   const ListView full{L.nbr, L.cnt, L.cap, false};  // cut source: any order
@@ -743,6 +804,12 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   k.flag = I.flag;
   k.cuts = I.dcuts;
   k.gen = I.gen;
+  k.ref0 = L.ref0;
+  k.lim0_2 = 0.25 * (L.cutoff - rcut) * (L.cutoff - rcut);
+  k.warn0_2 = 0.36 * k.lim0_2;  // 0.6 x the tolerable motion
+  k.stale = c->results + kStaleSlot + list_id;
+  k.warn = c->d_warn;
+  k.gen0 = c->list_gen;
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
   // the cut rows are short: sort them (bucketed by length), when cut
   const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);

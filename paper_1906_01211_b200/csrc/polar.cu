@@ -1245,6 +1245,7 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
     MDG_CUDA_CHECK(cudaStreamSynchronize(c0->stream));
   }
   fetch_results(c0);
+  check_lists_fresh(c0);
   const int64_t it = (int64_t)c0->h_results[28];
   *last_rms = c0->h_results[25];
   if (c0->h_results[27] == 0.0)

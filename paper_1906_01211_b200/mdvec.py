@@ -153,6 +153,7 @@ SIGNATURES = {
     "mdg_group_create_nccl": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p, C.c_int, C.c_int,
                                         C.c_void_p, C.c_int64]),
     "mdg_group_destroy": (C.c_int, [C.c_void_p]),
+    "mdg_md_rebuild_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "mdg_positions_upload_owned": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "mdg_group_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_group_set_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, _ip, _ip, _ip]),
@@ -669,6 +670,12 @@ class Engine:
         check(self.lib.mdg_md_run(self.ctx, C.byref(p), None if charmm is None else C.byref(charmm),
                                   None if amoeba is None else C.byref(amoeba), _p(ek), _p(ep)))
         return (ek[: p.nsteps], ep[: p.nsteps]) if energies else None
+
+    def md_rebuild_count(self) -> int:
+        """List rebuilds done by md_run so far (mdg_md_rebuild_count)."""
+        v = C.c_int64()
+        check(self.lib.mdg_md_rebuild_count(self.ctx, C.byref(v)))
+        return v.value
 
     # ---- fused steps ----------------------------------------------------------------
     def charmm_step(self, t: NeighborTable, p: CharmmParams):

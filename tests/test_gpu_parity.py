@@ -1212,3 +1212,39 @@ def test_md_energy_conservation(engine, mdg):
     et = ek + ep
     assert np.all(np.isfinite(et))
     assert (et.max() - et.min()) <= 2e-3 * ek.mean()
+
+
+@pytest.mark.parametrize("buffered", [False, True])
+def test_outdated_list_is_reported(engine, oracle, mdg, monkeypatch, buffered):
+    """A list walked after its sites moved more than half its skin (list
+    cutoff - kernel cutoff, less the row buffer on the buffered path) would
+    miss pairs: the next read of the results raises ContractViolation, and a
+    rebuild clears it. Motion within the bound is accepted."""
+    monkeypatch.setenv("MDG_PRUNE_MIN_SITES", "0" if buffered else "100000000")
+    s = mdg.water_box(1000, 31.04, 1, "amoeba")
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1,
+                         mdg.TERM_VDW | mdg.TERM_MPOLE)
+    engine.upload_system(s)
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    tv = engine.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+    engine.amoeba_step(tv, te, p)
+    engine.fetch_energies()
+    L = 31.04
+    rng = np.random.default_rng(1)
+    # within the bound: 0.3 A (the buffered bound is (9 - 7.5) / 2 = 0.75 A)
+    small = [np.mod(np.asarray(getattr(s, k)) + rng.uniform(-0.3, 0.3, s.n_sites) / np.sqrt(3), L)
+             for k in ("x", "y", "z")]
+    engine.upload_positions(*small)
+    engine.amoeba_step(tv, te, p)
+    engine.fetch_energies()
+    # past it: one site moved 1.6 A
+    big = [a.copy() for a in small]
+    big[0][5] = np.mod(big[0][5] + 1.6, L)
+    engine.upload_positions(*big)
+    engine.amoeba_step(tv, te, p)
+    with pytest.raises(mdg.ContractViolation):
+        engine.fetch_energies()
+    te = engine.build_neighbor_table(9.0, list_id=0)
+    tv = engine.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+    engine.amoeba_step(tv, te, p)
+    engine.fetch_energies()

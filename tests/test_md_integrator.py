@@ -120,13 +120,13 @@ def test_respa_nve_conserves_energy_at_a_longer_outer_step(engine, mdg):
     0.25 fs: 1.07)."""
     ch = mdg.CharmmParams(8.0, 0.45, mdg.ELECTRIC, 1, 1)
     _setup(engine, mdg, seed=4)
-    ek, ep = engine.md_run(_respa(mdg, 1000, 1.0, 4, 0.0, 0.0, 0, 20), charmm=ch)
+    ek, ep = engine.md_run(_respa(mdg, 1000, 1.0, 4, 0.0, 0.0, 0, 5), charmm=ch)
     et = ek + ep
     assert np.all(np.isfinite(et))
     assert (et.max() - et.min()) <= 3e-3 * ek.mean(), (et.max() - et.min(), ek.mean())
     spread_respa = et[:250].max() - et[:250].min()
     _setup(engine, mdg, seed=4)
-    ek, ep = engine.md_run(mdg.MDParams(0, 250, 1.0, 20, 0, 1, 9.3, 0.0, 1), charmm=ch)
+    ek, ep = engine.md_run(mdg.MDParams(0, 250, 1.0, 5, 0, 1, 9.3, 0.0, 1), charmm=ch)
     et = ek + ep
     assert spread_respa <= 0.3 * (et.max() - et.min()), (spread_respa, et.max() - et.min())
 
@@ -162,7 +162,7 @@ def test_respa_bad_parameters_are_contract_violations(engine, mdg):
             engine.md_run(bad, charmm=ch)
 
 
-def _amoeba_water(engine, mdg, scale=0.1, n_mol=216, box=18.6):
+def _amoeba_water(engine, mdg, scale=0.1, n_mol=512, box=24.8):
     """The AMOEBA water fixture with its random multipoles at `scale` in
     local water frames (z-then-x on H, bisector on O), bonds/angles and
     300 K velocities. At full scale the random multipoles collapse H...O
@@ -207,7 +207,7 @@ def test_amoeba_nve_conserves_energy(engine, mdg):
     PCG's 1e-6 D tolerance)."""
     _amoeba_water(engine, mdg)
     try:
-        ek, ep = engine.md_run(mdg.MDParams(1, 2000, 0.25, 20, 0, 1, 7.3, 9.3, 1),
+        ek, ep = engine.md_run(mdg.MDParams(1, 2000, 0.25, 20, 0, 1, 9.0, 11.0, 1),
                                amoeba=_amoeba_params(mdg))
     finally:
         engine.upload_frames(None, None, None)
@@ -224,7 +224,7 @@ def test_amoeba_respa_nve_conserves_energy(engine, mdg):
     steps of 1 fs (bonded terms in 4 sub-steps) keep the total energy within
     3e-3 of the kinetic energy."""
     _amoeba_water(engine, mdg)
-    p = mdg.MDParams(1, 500, 1.0, 10, 0, 1, 7.3, 9.3, 1)
+    p = mdg.MDParams(1, 500, 1.0, 5, 0, 1, 9.0, 11.0, 1)
     p.integrator = mdg.INTEGRATOR_BAOAB_RESPA
     p.inner_steps = 4
     try:
@@ -247,7 +247,7 @@ def test_aspc_predictor_same_dynamics_fewer_iterations(engine, mdg, monkeypatch)
     out = {}
     for pred in (mdg.PREDICT_NONE, mdg.PREDICT_ASPC):
         _amoeba_water(engine, mdg)
-        p = mdg.MDParams(1, 40, 0.25, 10, 0, 1, 7.3, 9.3, 1)
+        p = mdg.MDParams(1, 40, 0.25, 10, 0, 1, 9.0, 11.0, 1)
         p.predictor = pred
         try:
             ek, ep = engine.md_run(p, amoeba=_amoeba_params(mdg))
@@ -257,7 +257,27 @@ def test_aspc_predictor_same_dynamics_fewer_iterations(engine, mdg, monkeypatch)
             engine.upload_frames(None, None, None)
     (x0, e0, it0), (x1, e1, it1) = out[mdg.PREDICT_NONE], out[mdg.PREDICT_ASPC]
     d = x1 - x0
-    d -= 18.6 * np.rint(d / 18.6)
+    d -= 24.8 * np.rint(d / 24.8)
     assert np.abs(d).max() <= 1e-6
     np.testing.assert_allclose(e1, e0, rtol=1e-7)
     assert it1 < it0, (it1, it0)
+
+
+@pytest.mark.gpu
+def test_md_rebuilds_lists_early_when_sites_move_fast(engine, mdg):
+    """A rebuild interval too long for the motion (1 fs steps, rebuild_every
+    200, a 9.3 A list over an 8 A cutoff): mdg_md_run rebuilds early when the
+    device flags a site past 0.6 x the list's tolerable motion, the run
+    completes without an outdated-list error, and it matches the run with a
+    short schedule to the dynamics' chaos over 100 fs."""
+    out = {}
+    for every in (200, 5):
+        _setup(engine, mdg, seed=6)
+        r0 = engine.md_rebuild_count()
+        ek, ep = engine.md_run(mdg.MDParams(0, 100, 1.0, every, 0, 1, 9.3, 0.0, 1),
+                               charmm=mdg.CharmmParams(8.0, 0.45, mdg.ELECTRIC, 1, 1))
+        out[every] = (engine.md_rebuild_count() - r0, ek + ep)
+    n_auto, e_auto = out[200]
+    n_fixed, e_fixed = out[5]
+    assert 1 < n_auto < n_fixed, (n_auto, n_fixed)
+    np.testing.assert_allclose(e_auto[:20], e_fixed[:20], rtol=1e-6)

@@ -49,11 +49,13 @@ for k in range(steps // chunk):
         p.temperature_k = 300.0
         p.seed = 1000 + k
     eng.synchronize()
+    rb0 = eng.md_rebuild_count()
     eng.timer_start()
     r = eng.md_run(p, amoeba=ap, energies=(k % 5 == 0))
     ms = eng.timer_stop() / chunk
     e, w, it, rms = eng.fetch_energies()
-    row = {"step": (k + 1) * chunk, "ms_per_step": ms, "pcg_iters": int(it)}
+    row = {"step": (k + 1) * chunk, "ms_per_step": ms, "pcg_iters": int(it),
+           "list_rebuilds": eng.md_rebuild_count() - rb0}
     if r is not None:
         ek, ep = r
         row["T_K"] = float(2 * ek[-1] / (3 * wl.n * 0.0019872041))
