@@ -448,6 +448,16 @@ int mdg_set_deterministic(mdg_ctx* ctx, int on);
  * (kernel-by-kernel profiling). MDG_OVERLAP=0 sets the default of new
  * contexts. Results are the same either way. */
 int mdg_set_overlap(mdg_ctx* ctx, int on);
+/* PCG on site clusters (default 0; MDG_CLUSTER_MATVEC=1 sets the default of
+ * new contexts): per cluster of 3 consecutive sites (a water molecule in the
+ * molecule-keyed site order) the union of the sites' buffered rows, the field
+ * pass writing each site's pair tensors into the union's slots, and a PCG
+ * mat-vec that streams those with one gather of j per union entry (bulk
+ * asynchronous copies into shared memory). Measured on config 4 at parity
+ * with the per-site rows in the mat-vec and slower in the field pass
+ * (DESIGN.md section 4). Applies only to buffered cut rows without an
+ * overlapped domain exchange. The dipoles agree to rounding either way. */
+int mdg_set_cluster_matvec(mdg_ctx* ctx, int on);
 /* Gather 3 doubles per listed caller-order site of vec_id into out[3*count]
  * (x,y,z interleaved) / scatter them back. Host buffers. */
 int mdg_vec_pack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count, double* out);

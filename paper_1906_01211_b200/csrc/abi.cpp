@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -248,6 +249,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       c->device = device;
       if (const char* d = getenv("MDG_DETERMINISTIC")) c->deterministic = atoi(d) != 0;
       if (const char* o = getenv("MDG_OVERLAP")) c->overlap = atoi(o) != 0;
+      if (const char* o = getenv("MDG_CLUSTER_MATVEC")) c->cluster_matvec = atoi(o) != 0;
       set_device(c);
       c->n_cap = n_capacity;
       c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
@@ -332,8 +334,10 @@ int mdg_ctx_destroy(mdg_ctx* c) {
   if (c->plist.nbr) cudaFree(c->plist.nbr);
   if (c->plist.cnt) cudaFree(c->plist.cnt);
   if (c->plist.trr) cudaFree(c->plist.trr);
-  if (c->plist.ucl) cudaFree(c->plist.ucl);
   if (c->plist.ucnt) cudaFree(c->plist.ucnt);
+  if (c->plist.ugen) cudaFree(c->plist.ugen);
+  if (c->plist.cmap) cudaFree(c->plist.cmap);
+  if (c->plist.cst) cudaFree(c->plist.cst);
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_warn) cudaFreeHost(c->h_warn);
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -428,6 +432,7 @@ int mdg_system_upload_owned(mdg_ctx* c, int64_t n, int64_t n_owned, int64_t n_gl
     c->lz = lz;
     for (auto& Lst : c->lists) Lst.valid = false;
     c->has_mpoles = c->has_hred = c->has_mol = c->has_frames = false;
+    c->mol_sorted = false;
     c->fout[0] = c->fout[1] = c->fout[2] = nullptr;  // sized for the old system
     spatial_sort(c, x, y, z);
     stage_in(c, {x, y, z, charge, lj_sigma, lj_epsilon, hal_r0, hal_epsilon, polarizability});
@@ -499,6 +504,13 @@ int mdg_set_overlap(mdg_ctx* c, int on) {
   return guard([&] {
     need_ctx(c);
     c->overlap = on != 0;
+  });
+}
+
+int mdg_set_cluster_matvec(mdg_ctx* c, int on) {
+  return guard([&] {
+    need_ctx(c);
+    c->cluster_matvec = on != 0;
   });
 }
 
@@ -654,6 +666,25 @@ int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred
     c->has_hred = hred_parent != nullptr;
     mdg::set_groups(c);
     if (c->has_hred) mdg::run_reduce_sites(c);
+    // molecule-keyed site order (one domain): a molecule's sites consecutive,
+    // so the PCG's 3-site clusters are water molecules (cluster.cu)
+    static const int mol_order = mdg::env_int("MDG_MOL_ORDER", 1);
+    if (molecule && mol_order && c->n_own == c->n && !c->group && mdg::mol_order_fits(c)) {
+      std::unordered_map<int32_t, int32_t> first;  // molecule -> lowest caller index
+      first.reserve((size_t)n);
+      for (int64_t s = 0; s < n; ++s) {
+        auto it = first.emplace(mol[s], c->perm[s]).first;
+        it->second = std::min(it->second, c->perm[s]);
+      }
+      std::vector<int32_t> rep(n);
+      for (int64_t s = 0; s < n; ++s) rep[s] = c->iperm[first[mol[s]]];
+      int32_t* d_rep = nullptr;
+      MDG_CUDA_CHECK(cudaMalloc(&d_rep, (size_t)n * sizeof(int32_t)));
+      MDG_CUDA_CHECK(cudaMemcpyAsync(d_rep, rep.data(), (size_t)n * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, c->stream));
+      mdg::resort_sites(c, d_rep);  // synchronises the stream
+      MDG_CUDA_CHECK(cudaFree(d_rep));
+    }
     MDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
   });
 }

@@ -1,25 +1,32 @@
 // cluster.cu -- the PCG mat-vec on site clusters (the north-star "atom-tile"
 // kernel for the solve's hot loop).
 //
-// A cluster is 4 consecutive sites of the spatially sorted order (a compact
-// blob of ~40 A^3). Its union list U_c is the sorted union of the 4 sites'
-// buffered inner rows (the rows cut to 7 A + 0.5 A that k_perm_field<TPRE>
-// walks), built when those rows are cut again -- on the device, gated by the
-// cut's own flag, so in the static benchmark once per list rebuild and in
-// dynamics once per re-cut -- by k_cluster_union.
+// A cluster is kCl = 3 consecutive sites of the sorted order. With molecules
+// uploaded the order is molecule-keyed (abi.cpp mdg_topology_upload,
+// resort.cu), so for water a cluster is one molecule: three sites within 1 A
+// whose 7 A rows are nearly the same set. Per cluster:
+//   U75   the sorted union of the three sites' buffered inner rows (the rows
+//         cut to 7 A + 0.5 A that the field pass walks), built by
+//         k_cluster_union when those rows are cut again -- on the device,
+//         gated by the cut's own generation counter, so in the static
+//         benchmark once per list rebuild and in dynamics once per re-cut --
+//         together with each row slot's position in U75 (cmap) and zero pair
+//         tensors for the (site, entry) slots no row holds;
+//   ct    per site of the cluster and entry of U75 the pair tensor (rr3, rr5),
+//         written by the field pass (polar.cu k_perm_field<CLMAP>) through
+//         cmap every step: the tensor within the cutoff, zero beyond.
+// On config 4 U75 has 216 entries per molecule (the three 7 A rows hold 435
+// pairs), so the mat-vec gathers j's position and direction once per 2.0
+// pairs instead of once per pair, for 26 B of streamed index + tensors per
+// pair (20 B in the per-site rows). The per-site stream was bound by the L1
+// data pipe on those gathers (82 %), not by HBM.
 //
-// The mat-vec maps a warp onto 8 union entries x 4 cluster sites per step:
-// lane 4s + t handles the pair (site t, U_c[s]). The 4 lanes of an entry load
-// the same j, so one warp-wide gather touches 8 records instead of 32
-// (~3x fewer L1 wavefronts per pair than the per-site stream, which is bound
-// by the L1 data pipe on those gathers). Each lane tests its pair with the
-// reference predicate, op for op the one k_perm_field used to build the
-// pruned rows (same minimum image of the same operands, same cutoff^2), so the
-// in-range pairs of site t are exactly its pruned row, in the same (ascending
-// j) order; the pair tensor is read at rank popc(ballot & earlier lanes of
-// the same t) past the row's running base. A lane accumulates the field of
-// its own site t only (3 doubles); the lanes of a site are summed once per
-// cluster (xor 4, 8, 16).
+// The mat-vec (k_tmatvec_cl) is warp per cluster, lane per entry: each lane
+// streams the entry's index and three tensors (site-major, so every load is
+// a coalesced 512-B warp access), gathers j's position and direction once,
+// forms the three minimum-image separations (the operands and operations of
+// the field pass) and accumulates the field at all three sites; the 9 sums
+// are reduced once per cluster.
 //
 // Reference counterpart: dipole_field_matvec_vectorized
 // (proj/src/polar_vec.cpp:131-204), whose per-site gather/select of j
@@ -31,18 +38,23 @@
 namespace mdg {
 
 #ifndef MDG_CL_MINB
-#define MDG_CL_MINB 4
+#define MDG_CL_MINB 6
+#endif
+#ifndef MDG_CL_UNROLL
+#define MDG_CL_UNROLL 2
 #endif
 
-constexpr int kCl = 4;  // sites per cluster
+constexpr int kGrp = 4;  // lanes per cluster in the union merge (kCl used)
+static_assert(kCl <= kGrp, "cluster larger than its merge group");
 
 struct CUArgs {
   int64_t n;      // sites with rows (owned)
   int64_t ncl;    // clusters
   ListView rows;  // the rows the union covers (inner rows, ascending)
-  int32_t* __restrict__ ucl;  // [ncl][ucap]
+  ClChunk* __restrict__ cst;   // [ncl][nch]
   int32_t* __restrict__ ucnt;  // [ncl]
-  int32_t ucap;
+  int32_t nch, tcap;
+  uint16_t* __restrict__ cmap;  // [n][rows.cap]: row slot -> union position
   const int32_t* __restrict__ gen;   // the rows' cut generation (NULL: rebuild)
   const int32_t* __restrict__ ugen;  // the generation the unions hold
 };
@@ -51,37 +63,43 @@ __device__ __forceinline__ int32_t row_elem(const int4& v, int k) {
   return (k == 0) ? v.x : (k == 1) ? v.y : (k == 2) ? v.z : v.w;
 }
 
-// One warp merges 8 clusters at a time: lane 4 g + k holds the head of row k
-// of cluster 8 w + g; each iteration emits the group minimum and advances
-// the rows whose head equals it. Rows are read 4 entries per 128-bit load,
-// the next 4 prefetched.
+// One warp merges 8 clusters at a time: lane 4 g + k (k < kCl) holds the
+// head of row k of cluster 8 w + g; each iteration emits the group minimum
+// and advances the rows whose head equals it, recording the slot's union
+// position; a site whose row does not hold the entry gets a zero tensor
+// there. Rows are read 4 entries per 128-bit load, the next 4 prefetched.
+// Entries past tcap are counted, not stored (the host retries larger).
 __global__ void __launch_bounds__(kBlock) k_cluster_union(CUArgs a) {
   if (a.gen && *a.gen == *a.ugen) return;  // the rows were not cut again
-  constexpr int NG = 32 / kCl;
+  constexpr int NG = 32 / kGrp;
   const int lane = threadIdx.x & 31;
-  const int g = lane / kCl, k = lane % kCl;
+  const int g = lane / kGrp, k = lane % kGrp;
   const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const int64_t cl = warp * NG + g;
   const int64_t i = cl * kCl + k;
-  const bool vi = cl < a.ncl && i < a.n;
+  const bool vc = k < kCl && cl < a.ncl;  // a site slot of the cluster's tensors
+  const bool vi = vc && i < a.n;          // ... of a site with a row
   const int len = vi ? a.rows.cnt[i] : 0;
   const int4* row = reinterpret_cast<const int4*>(a.rows.nbr + (size_t)(vi ? i : 0) * a.rows.cap);
+  uint16_t* map = a.cmap + (size_t)(vi ? i : 0) * a.rows.cap;
+  ClChunk* cc = a.cst + (size_t)(cl < a.ncl ? cl : 0) * a.nch;
   int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
   if (len > 0) b0 = __ldcs(row);
   if (len > 4) b1 = __ldcs(row + 1);
   int h = 0;
   int32_t cur = (len > 0) ? (b0.x & 0x7fffffff) : INT_MAX;
-  int32_t* out = a.ucl + (size_t)(cl < a.ncl ? cl : 0) * a.ucap;
   int s = 0;
   for (;;) {
     int32_t m = cur;
 #pragma unroll
-    for (int o = 1; o < kCl; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 1; o < kGrp; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     const bool live = m != INT_MAX;
     if (!__any_sync(0xffffffffu, live)) break;
     const bool hit = live && cur == m;
-    MDG_DASSERT(!live || s < a.ucap);
-    if (k == 0 && live) out[s] = m;
+    const bool st = live && s < a.tcap;
+    if (k == 0 && st) cc[s >> 5].idx[s & 31] = m;
+    if (hit) map[h] = (uint16_t)min(s, 65535);
+    else if (vc && st) cc[s >> 5].ten[k][s & 31] = make_double2(0.0, 0.0);
     s += live;
     h += hit;
     if (hit && (h & 3) == 0) {
@@ -91,6 +109,15 @@ __global__ void __launch_bounds__(kBlock) k_cluster_union(CUArgs a) {
     const int32_t nx = row_elem(b0, h & 3) & 0x7fffffff;
     cur = hit ? ((h < len) ? nx : INT_MAX) : cur;
   }
+  // pad to whole 32-entry chunks (at least one): index = the cluster's first
+  // site, tensors zero, so the mat-vec computes every lane of a chunk unmasked
+  if (cl < a.ncl && s <= a.tcap) {
+    const int padded = max(32, (s + 31) & ~31);
+    for (int e = s; e < padded; ++e) {
+      if (k == 0) cc[e >> 5].idx[e & 31] = (int32_t)(cl * kCl);
+      if (vc) cc[e >> 5].ten[k][e & 31] = make_double2(0.0, 0.0);
+    }
+  }
   if (k == 0 && cl < a.ncl) a.ucnt[cl] = s;
 }
 
@@ -98,91 +125,224 @@ __global__ void k_cluster_gen(const int32_t* __restrict__ gen, int32_t* __restri
   *ugen = gen ? *gen : -1;
 }
 
-// E_i = sum_j rr5 (v_j . R) R - rr3 v_j over the cluster's union; the PCG
-// form writes q = p/alpha - T p and the block partial of p.q (as
-// k_tmatvec_pre).
+// E_i = sum_j rr5 (v_j . R) R - rr3 v_j at the kCl sites of each cluster over
+// its entries; the PCG form writes q = p/alpha - T p and the block partial of
+// p.q (as k_tmatvec_pre). The chunk padding, and sites whose row does not
+// hold the entry or holds it beyond the cutoff, carry rr = 0 and contribute
+// exactly 0.
+//
+// The stream (indices and tensors of each 32-entry chunk, and on a cluster's
+// first chunk its sites' positions, directions and polarizabilities) reaches
+// shared memory by bulk asynchronous copies (TMA engine, mbarrier
+// transaction counts), kClStages chunks ahead of the warp; the gathers of j
+// for chunk k + 1 are issued before chunk k computes. Register-level
+// pipelining of the same stream was undone by the compiler's scheduling
+// (ncu: long-scoreboard stalls on the loads of the chunk being computed).
+//
+// Minimum image: fma(-rint((x_t - x_j)/L), L, x_t - x_j), the field pass's
+// wrap1 without its final t >= L/2 correction, which never fires within the
+// cutoff (< L/2): the same bits for every pair with a nonzero tensor.
+#ifndef MDG_CL_STAGES
+#define MDG_CL_STAGES 4
+#endif
+constexpr int kClStages = MDG_CL_STAGES;
+
+struct __align__(128) ClStage {
+  ClChunk ch;            // the chunk: tensors per cluster site, indices
+  double4 spos[kCl];     // first chunk of a cluster: its sites' positions,
+  double4 sin[kCl];      // PCG directions p
+  double2 spol[kCl];     // and (polarizability, ...)
+};
+
+struct ClCur {
+  int32_t q;     // the warp's q-th cluster (first + q kWarps)
+  int32_t base;  // first entry of the chunk
+  int32_t cnt;   // the cluster's entry count
+};
+
 template <bool PCG>
 __global__ void __launch_bounds__(kBlock, MDG_CL_MINB) k_tmatvec_cl(CLArgs a) {
   if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
-  const int lane = threadIdx.x & 31;
-  const int t = lane & (kCl - 1), sl = lane / kCl;
-  const unsigned same_t = 0x11111111u << t;
-  const unsigned earlier = lanemask_lt() & same_t;
+  __shared__ ClStage st_mem[kWarps][kClStages];
+  __shared__ uint64_t bar_mem[kWarps][kClStages];
+  __shared__ double4 cs_mem[kWarps][3 * kCl];  // the current cluster: pos, p, polp
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  ClStage* st = st_mem[w];
+  uint64_t* bar = bar_mem[w];
+  double4* cs = cs_mem[w];
   double acc1[1] = {0.0};
-  MDG_SITE_LOOP(cl, a.ncl, a.ipw) {
-    const int64_t i = cl * kCl + t;
-    const bool vi = i < a.n;
-    const double4 pi = a.pos[vi ? i : cl * kCl];
-    const int ucount = a.ucnt[cl];
-    MDG_DASSERT(ucount >= 0 && ucount <= a.ucap);
-    const int32_t* urow = a.ucl + (size_t)cl * a.ucap;
-    const double2* trow = a.trr + (size_t)(vi ? i : 0) * a.pcap;
-    int base = 0;
-    double ex = 0, ey = 0, ez = 0;
-    for (int s0 = 0; s0 < ucount; s0 += 32 / kCl) {
-      const int s = s0 + sl;
-      const bool vs = s < ucount;
-      const int32_t j = vs ? __ldg(urow + s) : (int32_t)(cl * kCl);
-      const double4 pj = ldg4(a.pos + j);
-      const double4 mj = ldg4(a.in + j);
-      double dx, dy, dz;
-      // the pruned rows' predicate (k_perm_field): same operands, same ops
-      const double r2 = min_image(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, dx, dy, dz);
-      const bool in = vs && vi && j != (int32_t)i && r2 <= a.c2;
-      const unsigned bm = __ballot_sync(0xffffffffu, in);
-      double2 rr = make_double2(0.0, 0.0);
-      if (in) rr = __ldcs(trow + base + __popc(bm & earlier));
-      base += __popc(bm & same_t);
-      const double dot = mj.x * dx + mj.y * dy + mj.z * dz;
-      const double t5 = rr.y * dot;
-      ex += t5 * dx - rr.x * mj.x;
-      ey += t5 * dy - rr.x * mj.y;
-      ez += t5 * dz - rr.x * mj.z;
-    }
+  const int32_t first = (int32_t)((int64_t)blockIdx.x * a.ipw + w);
+  const int32_t end = (int32_t)min(a.ncl, ((int64_t)blockIdx.x + 1) * a.ipw);
+  const int32_t nq = first < end ? (end - first + kWarps - 1) / kWarps : 0;
+  if (nq > 0) {
+    if (lane == 0) {
 #pragma unroll
-    for (int o = kCl; o < 32; o <<= 1) {
-      ex += __shfl_xor_sync(0xffffffffu, ex, o);
-      ey += __shfl_xor_sync(0xffffffffu, ey, o);
-      ez += __shfl_xor_sync(0xffffffffu, ez, o);
+      for (int s = 0; s < kClStages; ++s) mbar_init(&bar[s]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (lane < kCl && vi) {
-      MDG_DASSERT(base <= a.pcap);
-      if (PCG) {
-        const double4 p = a.in[i];
-        const double inva = 1.0 / a.polp[i].x;
-        const double qx = p.x * inva - ex, qy = p.y * inva - ey, qz = p.z * inva - ez;
-        a.out[i] = make_double4(qx, qy, qz, 0.0);
-        acc1[0] += p.x * qx + p.y * qy + p.z * qz;
-      } else {
-        a.out[i] = make_double4(ex, ey, ez, 0.0);
+    __syncwarp();
+    // entry counts of the warp's clusters, 32 at a time, one per lane
+    auto counts = [&](int32_t q0) {
+      const int32_t q = q0 + lane;
+      return q < nq ? __ldg(a.ucnt + first + (int64_t)q * kWarps) : 0;
+    };
+    auto advance = [&](ClCur& c, int32_t& batch) {
+      if (c.base + 32 < c.cnt) {
+        c.base += 32;
+        return;
       }
+      ++c.q;
+      c.base = 0;
+      if ((c.q & 31) == 0) batch = counts(c.q);
+      c.cnt = __shfl_sync(0xffffffffu, batch, c.q & 31);
+    };
+    // lane 0: the copies of chunk c into stage s
+    auto issue = [&](const ClCur& c, int s) {
+      const int64_t cl = first + (int64_t)c.q * kWarps;
+      const int64_t i0 = cl * kCl;
+      const int ns = c.base == 0 ? (int)min((int64_t)kCl, a.n - i0) : 0;
+      ClStage& S = st[s];
+      mbar_arm(&bar[s], (uint32_t)(sizeof(ClChunk) + ns * (PCG ? 80 : 32)));
+      bulk_load(&S.ch, a.cst + (size_t)cl * a.nch + (c.base >> 5), sizeof(ClChunk), &bar[s]);
+      if (ns > 0) {
+        bulk_load(S.spos, a.pos + i0, 32 * ns, &bar[s]);
+        if (PCG) {
+          bulk_load(S.sin, a.in + i0, 32 * ns, &bar[s]);
+          bulk_load(S.spol, a.polp + i0, 16 * ns, &bar[s]);
+        }
+      }
+    };
+    uint32_t phase = 0u;  // bit s: parity of stage s's next completion
+    auto wait = [&](int s) {
+      mbar_wait(&bar[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+    };
+    int32_t pbatch = counts(0), cbatch = pbatch;
+    ClCur prod{0, 0, __shfl_sync(0xffffffffu, pbatch, 0)};
+    ClCur cons = prod;
+#pragma unroll
+    for (int s = 0; s < kClStages - 1; ++s) {
+      if (prod.q < nq) {
+        if (lane == 0) issue(prod, s);
+        advance(prod, pbatch);
+      }
+    }
+    wait(0);
+    double4 p0, m0, p1, m1;
+    {
+      const int32_t j = st[0].ch.idx[lane];
+      p0 = ldg4(a.pos + j);
+      m0 = ldg4(a.in + j);
+    }
+    ClCur next = cons;
+    int32_t nbatch = cbatch;
+    advance(next, nbatch);
+    double ex[kCl], ey[kCl], ez[kCl];
+#pragma unroll
+    for (int t = 0; t < kCl; ++t) ex[t] = ey[t] = ez[t] = 0.0;
+    static_assert((kClStages & (kClStages - 1)) == 0, "stages: a power of two");
+    for (int k = 0; cons.q < nq; ++k) {
+      const int cur = k & (kClStages - 1), nxt = (k + 1) & (kClStages - 1);
+      // refill the stage chunk k - 1 used
+      if (prod.q < nq) {
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(prod, (k + kClStages - 1) & (kClStages - 1));
+        }
+        advance(prod, pbatch);
+      }
+      // the next chunk's gathers
+      if (next.q < nq) {
+        wait(nxt);
+        const int32_t j = st[nxt].ch.idx[lane];
+        p1 = ldg4(a.pos + j);
+        m1 = ldg4(a.in + j);
+      }
+      const ClStage& S = st[cur];
+      if (cons.base == 0) {  // a new cluster: keep its site records
+        if (lane < kCl) {
+          cs[lane] = S.spos[lane];
+          if (PCG) {
+            cs[kCl + lane] = S.sin[lane];
+            const double2 pp = S.spol[lane];
+            cs[2 * kCl + lane] = make_double4(pp.x, pp.y, 0.0, 0.0);
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int t = 0; t < kCl; ++t) {
+        const double2 r = S.ch.ten[t][lane];
+        const double4 pi = cs[t];
+        const double ox = __dsub_rn(pi.x, p0.x), oy = __dsub_rn(pi.y, p0.y),
+                     oz = __dsub_rn(pi.z, p0.z);
+        const double dx = __fma_rn(-rint(__dmul_rn(ox, a.b.ix)), a.b.lx, ox);
+        const double dy = __fma_rn(-rint(__dmul_rn(oy, a.b.iy)), a.b.ly, oy);
+        const double dz = __fma_rn(-rint(__dmul_rn(oz, a.b.iz)), a.b.lz, oz);
+        const double dot = m0.x * dx + m0.y * dy + m0.z * dz;
+        ex[t] += r.y * dot * dx - r.x * m0.x;
+        ey[t] += r.y * dot * dy - r.x * m0.y;
+        ez[t] += r.y * dot * dz - r.x * m0.z;
+      }
+      if (next.q != cons.q) {  // the cluster's last chunk: reduce, write, reset
+        double mx = 0, my = 0, mz = 0;  // lane t < kCl keeps site t's sums
+#pragma unroll
+        for (int t = 0; t < kCl; ++t) {
+          const double sx = warp_allsum(ex[t]), sy = warp_allsum(ey[t]), sz = warp_allsum(ez[t]);
+          if (lane == t) {
+            mx = sx;
+            my = sy;
+            mz = sz;
+          }
+          ex[t] = ey[t] = ez[t] = 0.0;
+        }
+        const int64_t i = (first + (int64_t)cons.q * kWarps) * kCl + lane;
+        if (lane < kCl && i < a.n) {
+          if (PCG) {
+            const double4 p = cs[kCl + lane];
+            const double inva = 1.0 / cs[2 * kCl + lane].x;
+            const double qx = p.x * inva - mx, qy = p.y * inva - my, qz = p.z * inva - mz;
+            a.out[i] = make_double4(qx, qy, qz, 0.0);
+            acc1[0] += p.x * qx + p.y * qy + p.z * qz;
+          } else {
+            a.out[i] = make_double4(mx, my, mz, 0.0);
+          }
+        }
+        __syncwarp();
+      }
+      cons = next;
+      advance(next, nbatch);
+      p0 = p1;
+      m0 = m1;
     }
   }
   if (PCG) block_store_partials<1>(acc1, a.partials);
 }
 
-void build_clusters(mdg_ctx* c, double cutoff, const ListView& rows, const int32_t* gen) {
+bool build_clusters(mdg_ctx* c, double cutoff, const ListView& rows, const int32_t* gen,
+                    int32_t tcap, bool force) {
   PrunedList& P = c->plist;
-  static const int enabled = env_int("MDG_CLUSTER_MATVEC", 0);  // opt-in: measured slower (DESIGN 4)
-  if (!enabled || !P.valid || !P.sorted || !rows.sorted || !rows.dense || !gen ||
-      c->n_own == 0) {
-    P.cl_valid = false;
-    return;
-  }
+  P.cl_valid = false;
+  // (the mat-vec's minimum image relies on cutoff < L/2; union positions in 16 bits)
+  if (!c->cluster_matvec || !rows.sorted || !rows.dense || !gen || c->n_own == 0 ||
+      group_overlap(c) || !(2.0 * cutoff < std::min(c->lx, std::min(c->ly, c->lz))) ||
+      tcap > 65504)
+    return false;
   const int64_t n = c->n_own;
   const int64_t ncl = (n + kCl - 1) / kCl;
-  // the union of kCl rows is at most their total length
-  const int32_t ucap = (int32_t)std::min<int64_t>((int64_t)kCl * rows.cap, (int64_t)1 << 30);
-  // rebuild unconditionally when the union buffer is new / for other rows;
+  const int32_t nch = tcap / 32;
+  // rebuild unconditionally when the buffers are new / for other rows;
   // otherwise the device compares the rows' cut generation with the unions'
-  const uintptr_t key[3] = {(uintptr_t)rows.nbr, (uintptr_t)rows.cap, (uintptr_t)ncl};
-  bool force = !P.ubuilt || P.ukey[0] != key[0] || P.ukey[1] != key[1] || P.ukey[2] != key[2];
-  const size_t need = (size_t)ncl * (size_t)ucap;
-  if (need > P.uelems) {
-    if (P.ucl) cudaFree(P.ucl);
-    P.ucl = nullptr;
-    MDG_CUDA_CHECK(cudaMalloc(&P.ucl, need * sizeof(int32_t)));
-    P.uelems = need;
+  const uintptr_t key[4] = {(uintptr_t)rows.nbr, (uintptr_t)rows.cap, (uintptr_t)ncl,
+                            (uintptr_t)tcap};
+  for (int q = 0; q < 4; ++q) force = force || !P.ubuilt || P.ukey[q] != key[q];
+  const size_t need = (size_t)ncl * (size_t)nch;
+  if (need > P.celems) {
+    if (P.cst) cudaFree(P.cst);
+    P.cst = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&P.cst, need * sizeof(ClChunk)));
+    P.celems = need;
     force = true;
   }
   if (!P.ugen) {
@@ -196,25 +356,37 @@ void build_clusters(mdg_ctx* c, double cutoff, const ListView& rows, const int32
     P.ucnt_elems = ncl;
     force = true;
   }
+  const size_t mneed = (size_t)n * (size_t)rows.cap;
+  if (mneed > P.melems) {
+    if (P.cmap) cudaFree(P.cmap);
+    P.cmap = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&P.cmap, mneed * sizeof(uint16_t)));
+    P.melems = mneed;
+    force = true;
+  }
   CUArgs a;
   a.n = n;
   a.ncl = ncl;
   a.rows = rows;
-  a.ucl = P.ucl;
+  a.cst = P.cst;
   a.ucnt = P.ucnt;
-  a.ucap = ucap;
+  a.nch = nch;
+  a.tcap = tcap;
+  a.cmap = P.cmap;
   a.gen = force ? nullptr : gen;
   a.ugen = P.ugen;
-  const int64_t warps = (ncl + 32 / kCl - 1) / (32 / kCl);
+  const int64_t warps = (ncl + 32 / kGrp - 1) / (32 / kGrp);
   const unsigned grid = (unsigned)((warps * 32 + kBlock - 1) / kBlock);
   MDG_LAUNCH(c, "cluster_union", grid, kBlock, 0, k_cluster_union, a);
   MDG_LAUNCH(c, "cluster_gen", 1, 1, 0, k_cluster_gen, gen, P.ugen);
-  P.ucap = ucap;
   P.ncl = ncl;
   P.ucut = cutoff;
-  for (int q = 0; q < 3; ++q) P.ukey[q] = key[q];
+  P.mstride = rows.cap;
+  P.tcap = tcap;
+  P.nch = nch;
+  for (int q = 0; q < 4; ++q) P.ukey[q] = key[q];
   P.ubuilt = true;
-  P.cl_valid = true;
+  return true;
 }
 
 CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out) {
@@ -225,13 +397,10 @@ CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out) {
   k.ipw = 0;
   k.pos = c->pos;
   k.polp = c->polp;
-  k.ucl = P.ucl;
+  k.cst = P.cst;
   k.ucnt = P.ucnt;
-  k.ucap = P.ucap;
-  k.trr = P.trr;
-  k.pcap = P.cap;
+  k.nch = P.nch;
   k.b = make_box(c->lx, c->ly, c->lz);
-  k.c2 = P.ucut * P.ucut;  // as k_perm_field's c2
   k.in = in;
   k.out = out;
   k.partials = c->partials;

@@ -616,6 +616,7 @@ namespace mdg {
 PcgComm* group_comm(mdg_group* g) { return g; }
 std::vector<mdg_ctx*> group_domains(mdg_group* g) { return g->dom; }
 bool group_is_nccl(mdg_group* g) { return g->backend == MDG_GROUP_NCCL; }
+bool group_overlap(const mdg_ctx* c) { return c->group && c->group->ov; }
 void group_refresh(mdg_group* g) {
   if (g->backend == MDG_GROUP_LOCAL) refresh_tables(g);
 }

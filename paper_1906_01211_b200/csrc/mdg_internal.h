@@ -30,10 +30,11 @@ namespace mdg {
 #endif
 constexpr int kBlock = MDG_BLOCK;
 constexpr int kAspcDepth = 6;  // ASPC k = 4
+constexpr int kCl = 3;         // sites per cluster (cluster.cu): one water molecule
 constexpr int kStaleSlot = 120;  // results 120..123: list l outdated (nlist.cu)  // pair-kernel block: 4 warps = 4 site groups
 constexpr int kRedVals = 16;     // per-block partial slots (energies + virial)
 // device result slots: 0-9 nonpolar, 10-19 multipoles, 20-27 PCG, 30 Jacobi,
-// 40 polarization energy, 50-51 count_within, 60-63 list stats,
+// 40 polarization energy, 50-51 count_within, 60-65 list stats,
 // 70-79 polarization forces (pair energy, virial), 80-97 PME (pme.cu)
 constexpr int kResultSlots = 128;
 constexpr int kMaxBlocksRed = 1 << 20;
@@ -89,6 +90,13 @@ struct DevList {
 // Pruned list: the pairs of a source list within a kernel cutoff, compacted
 // per site (same sliced-ELL layout), j | 0x80000000 when i, j share a
 // molecule; trr holds the Ewald/Thole T pair tensor (rr3, rr5) per slot.
+// one 32-entry chunk of a cluster's stream (cluster.cu): the entries' pair
+// tensors per cluster site, then their indices -- one bulk copy of 1664 B
+struct ClChunk {
+  double2 ten[kCl][32];
+  int32_t idx[32];
+};
+
 struct PrunedList {
   bool valid = false;
   int src = -1;
@@ -100,18 +108,27 @@ struct PrunedList {
   size_t elems = 0;
   int64_t directed = 0;
   bool sorted = false;  // rows ascending in (j & 0x7fffffff) (source sorted)
-  // site clusters (cluster.cu): per cluster of 4 consecutive sites the sorted
-  // union of their inner rows, rebuilt when those rows are cut again
+  // site clusters (cluster.cu): kCl consecutive sites (a water molecule in
+  // the molecule-keyed order). Per cluster, nch chunks (ClChunk) hold U75,
+  // the sorted union of the sites' buffered inner rows (indices), and per
+  // site the pair tensors (rr3, rr5) with each entry -- written by the field
+  // pass every step through cmap[i * mstride + h] (the U75 position of slot
+  // h of site i's row), zero beyond the cutoff or when the entry is not in
+  // the site's row. The unions and maps are rebuilt when the rows are cut.
   bool cl_valid = false;
   int64_t ncl = 0;
-  int32_t ucap = 0;
-  int32_t* ucl = nullptr;
   int32_t* ucnt = nullptr;
   int32_t* ugen = nullptr;  // device: inner-row generation the unions were built from
-  size_t uelems = 0;
   int64_t ucnt_elems = 0;
   double ucut = 0.0;
-  uintptr_t ukey[3] = {0, 0, 0};
+  uintptr_t ukey[4] = {0, 0, 0, 0};
+  uint16_t* cmap = nullptr;
+  size_t melems = 0;
+  int32_t mstride = 0;  // rows.cap of the mapped rows
+  int32_t tcap = 0;     // entries per cluster (nch * 32)
+  int32_t nch = 0;
+  ClChunk* cst = nullptr;
+  size_t celems = 0;    // chunks allocated
   bool ubuilt = false;  // the union buffers hold the unions of the keyed rows
 };
 
@@ -122,13 +139,10 @@ struct CLArgs {
   int ipw;      // clusters per block (MDG_LAUNCH_SITES)
   const double4* __restrict__ pos;
   const double2* __restrict__ polp;
-  const int32_t* __restrict__ ucl;
-  const int32_t* __restrict__ ucnt;
-  int32_t ucap;
-  const double2* __restrict__ trr;
-  int32_t pcap;
+  const ClChunk* __restrict__ cst;   // [ncl][nch]
+  const int32_t* __restrict__ ucnt;  // [ncl] entries
+  int32_t nch;
   Box b;
-  double c2;  // the pruned rows' cutoff^2 (their predicate, replayed per pair)
   const double4* __restrict__ in;
   double4* __restrict__ out;
   double* __restrict__ partials;
@@ -318,6 +332,10 @@ struct mdg_ctx {
   // force component and energy, so the parity checks' failure path is tested
   double debug_perturb = 0.0;
   bool overlap = true;  // AMOEBA step on two streams (mdg_set_overlap)
+  // PCG on site clusters (cluster.cu; mdg_set_cluster_matvec, MDG_CLUSTER_MATVEC)
+  bool cluster_matvec = false;
+  // site order molecule-keyed (resort.cu): a molecule's sites consecutive
+  bool mol_sorted = false;
   bool has_polar_force = false;  // last AMOEBA step added polarization forces
   // second stream of the AMOEBA step: Halgren + multipoles run beside the
   // permanent field + PCG (independent work); its own block partials
@@ -481,10 +499,17 @@ void run_mpole_pruned(mdg_ctx* c, double alpha, double electric, int exclude, bo
 // the permanent field into c->eperm.
 void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
                     int exclude);
-// Cluster unions of the rows k_perm_field<TPRE> walked (cluster.cu), rebuilt
-// on the device when `gen` (the rows' cut generation) moved; leaves
-// plist.cl_valid false when the cluster mat-vec does not apply
-void build_clusters(mdg_ctx* c, double cutoff, const struct ListView& rows, const int32_t* gen);
+// Cluster unions (U75) of the rows the field pass walks, their slot maps
+// and the zero tensors of the slots no row fills (cluster.cu); rebuilt on the
+// device when `gen` (the rows' cut generation) moved, unconditionally when
+// `force`. tcap: the entry capacity per cluster, a multiple of 32 (entries
+// past it are counted, not stored: the caller retries larger). Returns false when the
+// cluster path does not apply.
+bool build_clusters(mdg_ctx* c, double cutoff, const struct ListView& rows, const int32_t* gen,
+                    int32_t tcap, bool force);
+void count_stats_n(mdg_ctx* c, const int32_t* cnt, int64_t n, int slot);
+// an NCCL / LOCAL group runs the interior/halo overlapped exchange (per-site rows)
+bool group_overlap(const mdg_ctx* c);
 CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out);
 const void* cl_matvec_kernel(bool pcg);
 void cl_matvec_launch(mdg_ctx* c, CLArgs& k, bool pcg, const char* name);
@@ -508,7 +533,10 @@ void group_sum_host(mdg_group* g, double* v, int nv);
 void debug_check_rows(mdg_ctx* c, const char* what, const int32_t* nbr, const int32_t* cnt,
                       int32_t cap, int64_t rows, int64_t n_all, bool sorted);
 // device spatial re-sort of every per-site array (resort.cu); invalidates lists
-void resort_sites(mdg_ctx* c);
+// rep (device, may be NULL): per site, the sorted index of its molecule's
+// representative -> molecule-keyed order (also kept by later re-sorts)
+void resort_sites(mdg_ctx* c, const int32_t* rep = nullptr);
+bool mol_order_fits(const mdg_ctx* c);
 // vdW sites from the positions (Halgren reduction or copy), after new positions
 void refresh_vsites(mdg_ctx* c);
 void run_reduce_sites(mdg_ctx* c);

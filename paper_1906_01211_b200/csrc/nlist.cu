@@ -382,11 +382,13 @@ __global__ void k_count_stats(int64_t n, const int32_t* __restrict__ cnt,
   }
 }
 
-void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) {
-  const unsigned blocks = (unsigned)std::min<int64_t>(296, std::max<int64_t>(1, grid_for(c->n_own, 256)));
-  MDG_LAUNCH(c, "count_stats", blocks, 256, 0, k_count_stats, c->n_own, cnt, c->results, slot,
+void count_stats_n(mdg_ctx* c, const int32_t* cnt, int64_t n, int slot) {
+  const unsigned blocks = (unsigned)std::min<int64_t>(296, std::max<int64_t>(1, grid_for(n, 256)));
+  MDG_LAUNCH(c, "count_stats", blocks, 256, 0, k_count_stats, n, cnt, c->results, slot,
              c->d_flag);
 }
+
+void count_stats(mdg_ctx* c, const int32_t* cnt, int slot) { count_stats_n(c, cnt, c->n_own, slot); }
 
 // Sort every row ascending by j: with Morton-ordered sites, consecutive j of
 // a sorted row share cache lines, so the pair kernels' 32-lane gathers touch

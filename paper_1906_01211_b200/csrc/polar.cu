@@ -14,6 +14,7 @@
 // recomputing erfc/exp/sqrt/div: the solve is HBM-bound.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include <cub/cub.cuh>
@@ -137,17 +138,20 @@ struct FKArgs {
   int32_t pcap;
   double* __restrict__ partials;  // unused (launch macro contract)
   const double4* __restrict__ pq4;
+  // CLMAP: the pair tensors go to the site clusters' U75 slots (cluster.cu)
+  const uint16_t* __restrict__ cmap;  // row slot -> union position
+  int32_t mstride;
+  ClChunk* __restrict__ cst;  // cluster chunks: site i's tensors in cst[i / kCl][*].ten[i % kCl]
+  int32_t nch, tcap;
 };
 
-// Field at i of the multipole of j, R = r_i - r_j (Tinker's stored Q = Theta/3):
+// Field at i of the multipole (qj, m0.xyz = dipole, m0.w m1 qzz = Q) of j,
+// R = r_i - r_j (Tinker's stored Q = Theta/3):
 // E = R (rr3 q + rr5 mu.R + rr7 R.Q.R) - rr3 mu - 2 rr5 Q R
-__device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int32_t j, double qj,
-                                            double dx, double dy, double dz, double rr3,
-                                            double rr5, double rr7, double& ex, double& ey,
-                                            double& ez) {
-  const double4 m0 = ldg4(mp + 3 * (size_t)j);
-  const double4 m1 = ldg4(mp + 3 * (size_t)j + 1);
-  const double qzz = __ldg(&mp[3 * (size_t)j + 2].x);
+__device__ __forceinline__ void mpole_field_v(const double4& m0, const double4& m1, double qzz,
+                                              double qj, double dx, double dy, double dz,
+                                              double rr3, double rr5, double rr7, double& ex,
+                                              double& ey, double& ez) {
   const double qx = m0.w * dx + m1.x * dy + m1.y * dz;
   const double qy = m1.x * dx + m1.z * dy + m1.w * dz;
   const double qz = m1.y * dx + m1.w * dy + qzz * dz;
@@ -160,10 +164,24 @@ __device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int3
   ez += cc * dz - rr3 * m0.z - t5 * qz;
 }
 
+__device__ __forceinline__ void mpole_field(const double4* __restrict__ mp, int32_t j, double qj,
+                                            double dx, double dy, double dz, double rr3,
+                                            double rr5, double rr7, double& ex, double& ey,
+                                            double& ez) {
+  const double4 m0 = ldg4(mp + 3 * (size_t)j);
+  const double4 m1 = ldg4(mp + 3 * (size_t)j + 1);
+  const double qzz = __ldg(&mp[3 * (size_t)j + 2].x);
+  mpole_field_v(m0, m1, qzz, qj, dx, dy, dz, rr3, rr5, rr7, ex, ey, ez);
+}
+
 // TPRE: also write the pruned row (all pairs within the cutoff, exclusion
 // flag in bit 31) and its T tensors; the field skips excluded pairs.
-template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE, bool DIRECT = false>
+// CLMAP (with TPRE, DIRECT): the tensors of row slot h go to the site's
+// cluster slot cmap[h] (cluster.cu), a zero tensor when the pair is beyond
+// the cutoff, instead of beside the pruned row.
+template <bool EWALD, bool MPOLE, bool EXCL, bool TPRE, bool DIRECT = false, bool CLMAP = false>
 __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
+  static_assert(!CLMAP || (TPRE && DIRECT), "cluster slots need the direct TPRE walk");
   __shared__ double4 ring_mem[kWarps][kRing];
   const int lane = threadIdx.x & 31;
   Ring ring{ring_mem[threadIdx.x >> 5], 0, 0};
@@ -174,7 +192,11 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     int32_t* prow = TPRE ? a.pnbr + (size_t)i * a.pcap : nullptr;
-    double2* trow = TPRE ? a.trr + (size_t)i * a.pcap : nullptr;
+    double2* trow = (TPRE && !CLMAP) ? a.trr + (size_t)i * a.pcap : nullptr;
+    const uint16_t* mrow = CLMAP ? a.cmap + (size_t)i * a.mstride : nullptr;
+    ClChunk* cch = CLMAP ? a.cst + (size_t)(i / kCl) * a.nch : nullptr;
+    const int ct_site = (int)(i % kCl);
+    int rslot = lane - 32;  // CLMAP: the row slot of this lane's chunk
     double ex = 0, ey = 0, ez = 0;
     auto body = [&](const double4& e, int slot) {
       const int32_t raw = ring_j(e);
@@ -223,7 +245,11 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
       }
       if (TPRE && slot < a.pcap) {  // overflow -> host retries larger
         prow[slot] = raw;
-        trow[slot] = make_double2(rr3, rr5);
+        if (!CLMAP) trow[slot] = make_double2(rr3, rr5);
+      }
+      if (CLMAP) {
+        const int m = mrow[rslot];
+        if (m < a.tcap) cch[m >> 5].ten[ct_site][m & 31] = make_double2(rr3, rr5);
       }
       if (EXCL && raw < 0) return;
       if (MPOLE) {
@@ -243,6 +269,13 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
           const bool same = mj == mi;
           if (!TPRE && EXCL && same) in = false;
           raw = (TPRE && same) ? (j | (int32_t)0x80000000) : j;
+          if (CLMAP) {
+            rslot += 32;
+            if (!in) {
+              const int m = mrow[rslot];
+              if (m < a.tcap) cch[m >> 5].ten[ct_site][m & 31] = make_double2(0.0, 0.0);
+            }
+          }
           return in;
         },
         body);
@@ -257,7 +290,7 @@ __global__ void __launch_bounds__(kBlock, MDG_PF_MINB) k_perm_field(FKArgs a) {
 }
 
 static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, double thole_a,
-                     double4* out) {
+                     double4* out, const ListView* rows = nullptr) {
   const DevList& L = c->lists[list_id];
   FKArgs k;
   k.n_i = c->n_own;
@@ -266,7 +299,7 @@ static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   k.pq4 = c->pq4;
   k.mp = c->mp;
   k.mol = c->mol;
-  k.L = kernel_rows(c, list_id, cutoff);
+  k.L = rows ? *rows : kernel_rows(c, list_id, cutoff);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.alpha = alpha;
@@ -276,6 +309,11 @@ static FKArgs f_args(mdg_ctx* c, int list_id, double alpha, double cutoff, doubl
   k.trr = nullptr;
   k.pcnt = nullptr;
   k.pcap = 0;
+  k.cmap = nullptr;
+  k.mstride = 0;
+  k.cst = nullptr;
+  k.nch = 0;
+  k.tcap = 0;
   return k;
 }
 
@@ -305,53 +343,91 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
   PrunedList& P = c->plist;
   const int64_t n = c->n_own;
   const double vol = c->lx * c->ly * c->lz;
-  const double expect = (double)c->n_global / vol * 4.18879020478639 * cutoff * cutoff * cutoff;
+  const double dens = (double)c->n_global / vol * 4.18879020478639;
+  const double expect = dens * cutoff * cutoff * cutoff;
   int32_t cap = (int32_t)std::min<double>(L.cap, 1.3 * expect + 40.0);
   cap = std::max<int32_t>(32, (cap + 31) & ~31);
   if (P.cap > cap) cap = std::min(P.cap, L.cap);
-  P.cl_valid = false;
   const bool mp = c->has_mpoles, ex = exclude && c->has_mol;
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  // site clusters: the unions of the rows walked (gated on the device by the
+  // rows' cut generation) before the pass, which writes the tensors into
+  // their cluster slots instead of beside the pruned rows
+  const ListView rows = kernel_rows(c, list_id, cutoff);
+  const double rb = cutoff + 0.5;  // the buffered rows' radius (kernel_rows)
+  int32_t tcap = (int32_t)std::max<double>(32.0, 1.3 * dens * rb * rb * rb + 64.0);
+  tcap = (tcap + 31) & ~31;
+  if (P.tcap > tcap) tcap = P.tcap;
+  bool force = false;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    const bool cl = build_clusters(c, cutoff, rows, rows.dense ? L.inner.gen : nullptr, tcap,
+                                   force);
     const size_t need = (size_t)n * (size_t)cap;
-    if (need > P.elems) {
+    if (need > P.elems || (!cl && !P.trr)) {
       if (P.nbr) cudaFree(P.nbr);
       if (P.trr) cudaFree(P.trr);
       P.nbr = nullptr;
       P.trr = nullptr;
       MDG_CUDA_CHECK(cudaMalloc(&P.nbr, need * sizeof(int32_t)));
-      MDG_CUDA_CHECK(cudaMalloc(&P.trr, need * sizeof(double2)));
+      // per-site tensors only for the per-site mat-vec
+      if (!cl) MDG_CUDA_CHECK(cudaMalloc(&P.trr, need * sizeof(double2)));
       P.elems = need;
     }
     if (!P.cnt) MDG_CUDA_CHECK(cudaMalloc(&P.cnt, (size_t)c->n_cap * sizeof(int32_t)));
     P.cap = cap;
-    FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, c->eperm);
+    FKArgs k = f_args(c, list_id, alpha, cutoff, thole_a, c->eperm, &rows);
     k.pnbr = P.nbr;
     k.trr = P.trr;
     k.pcnt = P.cnt;
     k.pcap = cap;
-    // rows longer than cap are counted, not written; the retry below grows cap
+    if (cl) {
+      k.cmap = P.cmap;
+      k.mstride = P.mstride;
+      k.cst = P.cst;
+      k.nch = P.nch;
+      k.tcap = P.tcap;
+#define TPRE_CL(M, X) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, M, X, true, true, true>));
+      if (mp && ex) { TPRE_CL(true, true) }
+      else if (mp) { TPRE_CL(true, false) }
+      else if (ex) { TPRE_CL(false, true) }
+      else { TPRE_CL(false, false) }
+#undef TPRE_CL
+      count_stats_n(c, P.ucnt, P.ncl, 64);
+    } else {
+      // rows longer than cap are counted, not written; the retry below grows cap
 #define TPRE_LAUNCH(M, X)                                                                     \
   if (k.L.dense) MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, M, X, true, true>)); \
   else MDG_LAUNCH_SITES(c, "field_tpre", n, k, (k_perm_field<true, M, X, true, false>));
-    if (mp && ex) { TPRE_LAUNCH(true, true) }
-    else if (mp) { TPRE_LAUNCH(true, false) }
-    else if (ex) { TPRE_LAUNCH(false, true) }
-    else { TPRE_LAUNCH(false, false) }
+      if (mp && ex) { TPRE_LAUNCH(true, true) }
+      else if (mp) { TPRE_LAUNCH(true, false) }
+      else if (ex) { TPRE_LAUNCH(false, true) }
+      else { TPRE_LAUNCH(false, false) }
 #undef TPRE_LAUNCH
+    }
     count_stats(c, P.cnt, 62);
     fetch_results(c);
     const int32_t mx = (int32_t)c->h_results[62];
-    if (mx <= cap) {
+    const int32_t umx = cl ? (int32_t)c->h_results[64] : 0;
+    if (mx <= cap && umx <= tcap) {
       P.valid = true;
-      P.sorted = k.L.sorted;  // the rows walked (buffered cut or the list)
+      P.sorted = rows.sorted;  // the rows walked (buffered cut or the list)
       P.src = list_id;
       P.cutoff = cutoff;
       P.directed = (int64_t)c->h_results[63];
+      P.cl_valid = cl;
+      static const int cl_stats = env_int("MDG_CL_STATS", 0);
+      if (cl_stats && cl)
+        std::fprintf(stderr, "[mdg] clusters %lld (mol order %d): U75 entries max %d mean %.1f, "
+                     "tcap %d; pruned rows max %d mean %.1f\n", (long long)P.ncl,
+                     (int)c->mol_sorted, umx, c->h_results[65] / (double)P.ncl, tcap, mx,
+                     c->h_results[63] / (double)n);
       debug_check_rows(c, "pruned", P.nbr, P.cnt, P.cap, n, c->n, P.sorted);
-      build_clusters(c, cutoff, k.L, k.L.dense ? L.inner.gen : nullptr);
       return;
     }
-    cap = (mx + 31) & ~31;
+    if (mx > cap) cap = (mx + 31) & ~31;
+    if (umx > tcap) {
+      tcap = (umx + 31) & ~31;
+      force = true;  // the unions' zero tensors in the new layout
+    }
   }
   throw_error(MDG_CUDA, "field_tpre: capacity retry failed");
 }
@@ -462,41 +538,6 @@ __global__ void __launch_bounds__(kBlock) k_tmatvec_pre(TPArgs a) {
 // version: the largest stall is the index load feeding the gathers) and the
 // only LSU global traffic left is the neighbour gathers. Two stages per
 // warp; lane 0 arms the stage's barrier and issues both copies.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
-                                          uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-        "selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  }
-}
-
 // dynamic shared memory of one block: barriers, then per warp two stages of
 // {tensors[cap] double2, indices[cap] int32}
 __host__ __device__ inline size_t tma_stage_bytes(int32_t cap) { return (size_t)cap * 20; }

@@ -39,6 +39,35 @@ __global__ void k_morton_keys(int64_t n, const double4* __restrict__ pos, Box b,
   val[s] = (int32_t)s;
 }
 
+// Molecule-keyed order (sites of a molecule consecutive, molecules in
+// Morton order, so a 3-site cluster of cluster.cu is one water): the key of
+// a site is the Morton key of its molecule's representative site `rep`, then
+// rep itself (ties of two molecules in one cell stay apart). rep: the given
+// array (the first molecule sort, abi.cpp), or else the first site of the
+// site's run of equal molecule ids in the current order (the order already
+// molecule-keyed: runs are molecules). The key needs the cell code in 33
+// bits (<= 2048 cells per edge; checked by the caller).
+__global__ void k_morton_keys_mol(int64_t n, const double4* __restrict__ pos,
+                                  const int32_t* __restrict__ mol,
+                                  const int32_t* __restrict__ rep_in, Box b, int nx, int ny,
+                                  int nz, uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int64_t r = s;
+  if (rep_in) {
+    r = rep_in[s];
+  } else {
+    const int32_t m = mol[s];
+    for (int k = 0; k < 64 && r > 0 && mol[r - 1] == m; ++k) --r;
+  }
+  const double4 p = pos[r];
+  const int cx = min(nx - 1, (int)(p.x / b.lx * nx));
+  const int cy = min(ny - 1, (int)(p.y / b.ly * ny));
+  const int cz = min(nz - 1, (int)(p.z / b.lz * nz));
+  key[s] = (spread3_dev(cx) | spread3_dev(cy) << 1 | spread3_dev(cz) << 2) << 31 | (uint64_t)r;
+  val[s] = (int32_t)s;
+}
+
 __global__ void k_inverse(int64_t n, const int32_t* __restrict__ ord, int32_t* __restrict__ inv) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s < n) inv[ord[s]] = (int32_t)s;
@@ -154,11 +183,18 @@ void permute_csr(mdg_ctx* c, const int32_t* ord, const int32_t* inv, int32_t* st
 
 }  // namespace
 
-void resort_sites(mdg_ctx* c) {
+bool mol_order_fits(const mdg_ctx* c) {
+  const int nx = std::max(1, (int)(c->lx / 2.0)), ny = std::max(1, (int)(c->ly / 2.0)),
+            nz = std::max(1, (int)(c->lz / 2.0));
+  return c->n < ((int64_t)1 << 31) && std::max(nx, std::max(ny, nz)) <= 2048;
+}
+
+void resort_sites(mdg_ctx* c, const int32_t* rep) {
   if (c->n_own != c->n || c->group)
     throw_error(MDG_CONTRACT, "resort: single domain only (halo maps use sorted indices)");
   const int64_t n = c->n;
   if (n < 2) return;
+  const bool molkey = (rep || c->mol_sorted) && mol_order_fits(c);
   static thread_local Scratch sk, sv, sk2, sv2, sinv, stmp, scub, c1, c2, c3;
   uint64_t* key = (uint64_t*)sk.get(n * sizeof(uint64_t));
   int32_t* val = (int32_t*)sv.get(n * sizeof(int32_t));
@@ -167,8 +203,12 @@ void resort_sites(mdg_ctx* c) {
   int32_t* inv = (int32_t*)sinv.get(n * sizeof(int32_t));
   const int nx = std::max(1, (int)(c->lx / 2.0)), ny = std::max(1, (int)(c->ly / 2.0)),
             nz = std::max(1, (int)(c->lz / 2.0));
-  MDG_LAUNCH(c, "resort_keys", grid_for(n, 256), 256, 0, k_morton_keys, n, c->pos,
-             make_box(c->lx, c->ly, c->lz), nx, ny, nz, key, val);
+  if (molkey)
+    MDG_LAUNCH(c, "resort_keys", grid_for(n, 256), 256, 0, k_morton_keys_mol, n, c->pos, c->mol,
+               rep, make_box(c->lx, c->ly, c->lz), nx, ny, nz, key, val);
+  else
+    MDG_LAUNCH(c, "resort_keys", grid_for(n, 256), 256, 0, k_morton_keys, n, c->pos,
+               make_box(c->lx, c->ly, c->lz), nx, ny, nz, key, val);
   size_t tb = 0;
   MDG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, val, ord, n, 0, 63,
                                                  c->stream));
@@ -227,6 +267,7 @@ void resort_sites(mdg_ctx* c) {
   c->plist.cl_valid = false;
   c->plist.ubuilt = false;
   c->fout_seq = 0;
+  c->mol_sorted = molkey;
 }
 
 }  // namespace mdg

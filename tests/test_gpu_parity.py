@@ -412,6 +412,41 @@ def test_pcg_matches_oracle(engine, oracle, mdg):
     assert force_err_rms(engine.fetch_perm_field(), ep) <= F_TOL
 
 
+def test_cluster_matvec_pcg_matches_oracle_and_per_site(engine, oracle, mdg):
+    """The opt-in cluster PCG (3-site clusters = water molecules in the
+    molecule-keyed order, union rows, TMA-staged mat-vec): the oracle's
+    iterations (+-1) and dipoles within 1e-5 D, and the per-site path's
+    dipoles, field and energies to rounding, over two steps (the second
+    reuses the unions)."""
+    s = amoeba_small(mdg, 1000, 31.04, 9)
+    so = to_oracle_system(s)
+    t_o = oracle.build_table(so, 9.0)
+    ep = oracle.perm_field_ewald(so, t_o, 0.5446, 7.0, 0.39, exclude=True)
+    mu_o, it_o, _ = oracle.pcg(so, t_o, 0.5446, 7.0, 0.39, ep, 1e-5, 100)
+    engine.upload_system(s)
+    t = engine.build_neighbor_table(9.0)
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-5, 100, 1)
+    res = {}
+    try:
+        for on in (False, True):
+            engine.set_cluster_matvec(on)
+            for _ in range(2):
+                engine.amoeba_step(t, t, p)
+                e, w, iters, rms = engine.fetch_energies()
+                res[on] = (e, iters, engine.fetch_dipoles(), engine.fetch_perm_field(),
+                           engine.fetch_forces())
+    finally:
+        engine.set_cluster_matvec(False)
+    e1, it1, mu1, ep1, f1 = res[True]
+    e0, it0, mu0, ep0, f0 = res[False]
+    assert abs(it1 - it_o) <= 1 and it1 == it0
+    assert np.sqrt(np.mean(np.sum((mu1 - mu_o) ** 2, 1))) * mdg.DEBYE < 1e-5
+    np.testing.assert_allclose(mu1, mu0, rtol=0, atol=1e-10 * np.abs(mu0).max())
+    np.testing.assert_allclose(ep1, ep0, rtol=0, atol=1e-12 * np.abs(ep0).max())
+    assert rel(e1[2], e0[2]) <= 1e-10
+    np.testing.assert_allclose(f1, f0, rtol=0, atol=1e-12 * np.abs(f0).max())
+
+
 def test_mpole_matches_oracle(engine, oracle, mdg):
     """Real-space multipole energy/forces/torques/virial vs the T-tensor oracle."""
     s = amoeba_small(mdg, 343, 21.0, 5)

@@ -1,0 +1,21 @@
+"""Summarise an ncu report: python tools/ncu_summary.py REPORT.ncu-rep"""
+import csv, io, subprocess, sys
+
+WANT = [("gpu__time_duration.sum", "ms"), ("dram__bytes_read.sum", "rd"), ("dram__bytes_write.sum", "wr"),
+        ("launch__registers_per_thread", "regs"), ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps%"),
+        ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%"),
+        ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64%"),
+        ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "l1wf%"),
+        ("l1tex__throughput.avg.pct_of_peak_sustained_active", "l1%"),
+        ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2%"),
+        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%")]
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+h = rows[0]
+for r in rows[2:]:
+    name = r[h.index("Kernel Name")][:60]
+    vals = []
+    for k, lab in WANT:
+        if k in h:
+            vals.append("%s=%s" % (lab, r[h.index(k)]))
+    print(name, " ".join(vals))
