@@ -57,10 +57,14 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
   double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   MDG_SITE_LOOP(i, a.n_i, a.ipw) {
     const double4 pi = a.pos[i];
+    // i's multipole times the electric constant: every output is linear in
+    // it, so the pair factors G_n need no scaling (6 multiplies per pair)
+    const double ec = a.electric;
     const double4 m0i = a.mp[3 * i], m1i = a.mp[3 * i + 1];
-    const double qi = a.pq4[i].z;
-    const double dix = m0i.x, diy = m0i.y, diz = m0i.z;
-    const Quad Qi{m0i.w, m1i.x, m1i.y, m1i.z, m1i.w, a.mp[3 * i + 2].x};
+    const double qi = ec * a.pq4[i].z;
+    const double dix = ec * m0i.x, diy = ec * m0i.y, diz = ec * m0i.z;
+    const Quad Qi{ec * m0i.w, ec * m1i.x, ec * m1i.y, ec * m1i.z, ec * m1i.w,
+                  ec * a.mp[3 * i + 2].x};
     const int cnt = a.L.cnt[i];
     const int32_t* row = list_row(a.L, i);
     double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
@@ -77,8 +81,6 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
       const double inv_r2 = inv_r * inv_r;
       double G[6];
       ewald_bn<5>(r, inv_r, inv_r2, a.alpha, G);
-#pragma unroll
-      for (int q = 0; q < 6; ++q) G[q] *= a.electric;
 
       double vix, viy, viz, vjx, vjy, vjz;
       qmul(Qi, x, y, z, vix, viy, viz);
@@ -148,28 +150,36 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
       tx += gmy * diz - gmz * diy;
       ty += gmz * dix - gmx * diz;
       tz += gmx * diy - gmy * dix;
-      // quadrupole torque: GQ = dU/dQi (symmetric); tau_a = -eps_abc (Qi GQ - GQ Qi)_bc
+      // quadrupole torque: GQ = dU/dQi (symmetric), tau = 2 axial(Qi GQ - GQ Qi)
+      // with axial(M) = (M_zy, M_xz, M_yx). GQ = crr RR' - G2 (dj R' + R dj')
+      // + 2 G2 Qj - 2 G3 (R vj' + vj R'), and for a symmetric u v' + v u' the
+      // axial vector is v x (Qi u) + u x (Qi v), so
+      //   tau/2 = crr R x vi - G2 (R x Qi dj + dj x vi) + 2 G2 X
+      //           - 2 G3 (vj x vi + R x Qi vj),  X = axial(Qi Qj - Qj Qi).
+      // (The partner: the same with i <-> j, R -> -R; X changes sign.)
       const double crr = G[2] * qj + G[3] * djr + G[4] * qjr;  // coefficient of R R^T
-      const double g2 = 2.0 * G[2];
-      const double g3 = 2.0 * G[3];
-      Quad GQ;
-      GQ.xx = crr * x * x - G[2] * (2.0 * djx * x) + g2 * Qj.xx - g3 * (2.0 * x * vjx);
-      GQ.yy = crr * y * y - G[2] * (2.0 * djy * y) + g2 * Qj.yy - g3 * (2.0 * y * vjy);
-      GQ.zz = crr * z * z - G[2] * (2.0 * djz * z) + g2 * Qj.zz - g3 * (2.0 * z * vjz);
-      GQ.xy = crr * x * y - G[2] * (djx * y + x * djy) + g2 * Qj.xy - g3 * (x * vjy + vjx * y);
-      GQ.xz = crr * x * z - G[2] * (djx * z + x * djz) + g2 * Qj.xz - g3 * (x * vjz + vjx * z);
-      GQ.yz = crr * y * z - G[2] * (djy * z + y * djz) + g2 * Qj.yz - g3 * (y * vjz + vjy * z);
-      // M = Qi GQ - GQ Qi (antisymmetric); tau = (M_zy - M_yz, M_xz - M_zx, M_yx - M_xy)
-      //   = 2 (M_zy, M_xz, M_yx)
-      const double Mzy = (Qi.xz * GQ.xy + Qi.yz * GQ.yy + Qi.zz * GQ.yz) -
-                         (GQ.xz * Qi.xy + GQ.yz * Qi.yy + GQ.zz * Qi.yz);
-      const double Mxz = (Qi.xx * GQ.xz + Qi.xy * GQ.yz + Qi.xz * GQ.zz) -
-                         (GQ.xx * Qi.xz + GQ.xy * Qi.yz + GQ.xz * Qi.zz);
-      const double Myx = (Qi.xy * GQ.xx + Qi.yy * GQ.xy + Qi.yz * GQ.xz) -
-                         (GQ.xy * Qi.xx + GQ.yy * Qi.xy + GQ.yz * Qi.xz);
-      tx += 2.0 * Mzy;
-      ty += 2.0 * Mxz;
-      tz += 2.0 * Myx;
+      const double Xx = (Qi.xz * Qj.xy + Qi.yz * Qj.yy + Qi.zz * Qj.yz) -
+                        (Qj.xz * Qi.xy + Qj.yz * Qi.yy + Qj.zz * Qi.yz);
+      const double Xy = (Qi.xx * Qj.xz + Qi.xy * Qj.yz + Qi.xz * Qj.zz) -
+                        (Qj.xx * Qi.xz + Qj.xy * Qi.yz + Qj.xz * Qi.zz);
+      const double Xz = (Qi.xy * Qj.xx + Qi.yy * Qj.xy + Qi.yz * Qj.xz) -
+                        (Qj.xy * Qi.xx + Qj.yy * Qi.xy + Qj.yz * Qi.xz);
+      const double g2 = 2.0 * G[2], g3 = 2.0 * G[3];
+      // vj x vi (the partner uses vi x vj = -(vj x vi))
+      const double wx = vjy * viz - vjz * viy, wy = vjz * vix - vjx * viz,
+                   wz = vjx * viy - vjy * vix;
+      // R x (crr vi - G2 a2 - 2 G3 b1) - G2 dj x vi + 2 G2 X - 2 G3 (vj x vi)
+      {
+        const double ux_ = crr * vix - G[2] * a2x - g3 * b1x;
+        const double uy_ = crr * viy - G[2] * a2y - g3 * b1y;
+        const double uz_ = crr * viz - G[2] * a2z - g3 * b1z;
+        const double qx = (y * uz_ - z * uy_) - G[2] * (djy * viz - djz * viy) + g2 * Xx - g3 * wx;
+        const double qy = (z * ux_ - x * uz_) - G[2] * (djz * vix - djx * viz) + g2 * Xy - g3 * wy;
+        const double qz = (x * uy_ - y * ux_) - G[2] * (djx * viy - djy * vix) + g2 * Xz - g3 * wz;
+        tx += 2.0 * qx;
+        ty += 2.0 * qy;
+        tz += 2.0 * qz;
+      }
       if (jside) {
         // partner j: same formulas with (qi, di, Qi) <-> (qj, dj, Qj), R -> -R
         const double c1j = G[1] * qi - G[2] * dir + G[3] * qir;
@@ -179,23 +189,15 @@ __global__ void __launch_bounds__(kBlock, MDG_MPOLE_MINB) k_mpole(MKArgs a) {
         double ux = hy * djz - hz * djy;
         double uy = hz * djx - hx * djz;
         double uz = hx * djy - hy * djx;
+        // tau_j/2 = crj R x vj + G2 (R x Qj di + di x vj) - 2 G2 X
+        //           - 2 G3 (vi x vj + R x Qj vi)
         const double crj = G[2] * qi - G[3] * dir + G[4] * qir;
-        Quad H;
-        H.xx = crj * x * x + G[2] * (2.0 * dix * x) + g2 * Qi.xx - g3 * (2.0 * x * vix);
-        H.yy = crj * y * y + G[2] * (2.0 * diy * y) + g2 * Qi.yy - g3 * (2.0 * y * viy);
-        H.zz = crj * z * z + G[2] * (2.0 * diz * z) + g2 * Qi.zz - g3 * (2.0 * z * viz);
-        H.xy = crj * x * y + G[2] * (dix * y + x * diy) + g2 * Qi.xy - g3 * (x * viy + vix * y);
-        H.xz = crj * x * z + G[2] * (dix * z + x * diz) + g2 * Qi.xz - g3 * (x * viz + vix * z);
-        H.yz = crj * y * z + G[2] * (diy * z + y * diz) + g2 * Qi.yz - g3 * (y * viz + viy * z);
-        const double Nzy = (Qj.xz * H.xy + Qj.yz * H.yy + Qj.zz * H.yz) -
-                           (H.xz * Qj.xy + H.yz * Qj.yy + H.zz * Qj.yz);
-        const double Nxz = (Qj.xx * H.xz + Qj.xy * H.yz + Qj.xz * H.zz) -
-                           (H.xx * Qj.xz + H.xy * Qj.yz + H.xz * Qj.zz);
-        const double Nyx = (Qj.xy * H.xx + Qj.yy * H.xy + Qj.yz * H.xz) -
-                           (H.xy * Qj.xx + H.yy * Qj.xy + H.yz * Qj.xz);
-        ux += 2.0 * Nzy;
-        uy += 2.0 * Nxz;
-        uz += 2.0 * Nyx;
+        const double ux_ = crj * vjx + G[2] * a1x - g3 * b2x;
+        const double uy_ = crj * vjy + G[2] * a1y - g3 * b2y;
+        const double uz_ = crj * vjz + G[2] * a1z - g3 * b2z;
+        ux += 2.0 * ((y * uz_ - z * uy_) + G[2] * (diy * vjz - diz * vjy) - g2 * Xx + g3 * wx);
+        uy += 2.0 * ((z * ux_ - x * uz_) + G[2] * (diz * vjx - dix * vjz) - g2 * Xy + g3 * wy);
+        uz += 2.0 * ((x * uy_ - y * ux_) + G[2] * (dix * vjy - diy * vjx) - g2 * Xz + g3 * wz);
         atomicAdd(&a.force[j].x, gx);
         atomicAdd(&a.force[j].y, gy);
         atomicAdd(&a.force[j].z, gz);
