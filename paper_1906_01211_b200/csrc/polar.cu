@@ -675,9 +675,9 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(int64_t n, const double2* __
                                                     double4* __restrict__ z,
                                                     double4* __restrict__ p,
                                                     double* __restrict__ partials) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
   double acc[1] = {0.0};
-  if (i < n) {
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kBlock) {
     const double al = polp[i].x;
     const double4 E = e[i], T = t[i], m = mu[i];
     const double inva = 1.0 / al;
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(int64_t n, const double2* __
     const double4 zz = make_double4(al * rx, al * ry, al * rz, 0.0);
     z[i] = zz;
     p[i] = zz;
-    acc[0] = rx * zz.x + ry * zz.y + rz * zz.z;
+    acc[0] += rx * zz.x + ry * zz.y + rz * zz.z;
   }
   block_store_partials<1>(acc, partials);
 }
@@ -746,12 +746,13 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* 
                                                       double4* __restrict__ z,
                                                       double* __restrict__ partials) {
   if (res[27] != 0.0) return;
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
   double acc[2] = {0.0, 0.0};
-  if (i < n) {
-    // p.q == 0 only for p == 0 (r == 0: already exact); a = 0 then leaves mu
-    // unchanged and the rms test stops the loop, no 0/0
-    const double ak = (res[20] != 0.0) ? res[21] / res[20] : 0.0;
+  // p.q == 0 only for p == 0 (r == 0: already exact); a = 0 then leaves mu
+  // unchanged and the rms test stops the loop, no 0/0
+  const double ak = (res[20] != 0.0) ? res[21] / res[20] : 0.0;
+  // grid-stride (a grid of a few blocks per SM): few partials for the sum
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kBlock) {
     const double al = polp[i].x;
     const double4 pp = p[i], qq = q[i], m = mu[i], rr = r[i];
     const double dx = ak * pp.x, dy = ak * pp.y, dz = ak * pp.z;
@@ -760,8 +761,8 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(int64_t n, const double2* 
     r[i] = make_double4(rx, ry, rz, 0.0);
     const double zx = al * rx, zy = al * ry, zz = al * rz;
     z[i] = make_double4(zx, zy, zz, 0.0);
-    acc[0] = rx * zx + ry * zy + rz * zz;
-    acc[1] = dx * dx + dy * dy + dz * dz;
+    acc[0] += rx * zx + ry * zy + rz * zz;
+    acc[1] += dx * dx + dy * dy + dz * dz;
   }
   block_store_partials<2>(acc, partials);
 }
@@ -781,10 +782,33 @@ __global__ void k_cg_dir(int64_t n, const double* __restrict__ res, const double
 // Fixed-order local sums of the CG partials: mode 0 r.z -> res[21] (and a
 // fresh converged flag / iteration count); mode 1 p.q -> res[20]; mode 2
 // r.z, sum|dmu|^2 -> res[22], res[23].
+__device__ __forceinline__ void cg_finish(cudaGraphConditionalHandle h, int use_cond,
+                                          double* __restrict__ res, int64_t max_iter,
+                                          double n_global, double tol) {
+  if (res[27] != 0.0) {
+    if (use_cond) cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  const double rz_new = res[22];
+  const double rms = sqrt(res[23] / n_global) * kDebye;
+  res[25] = rms;
+  res[24] = (res[21] != 0.0) ? rz_new / res[21] : 0.0;
+  res[21] = rz_new;
+  const double it = res[28] + 1.0;
+  res[28] = it;
+  const bool conv = rms < tol;
+  res[27] = conv ? 1.0 : 0.0;
+  if (use_cond) cudaGraphSetConditional(h, (!conv && it < (double)max_iter) ? 1u : 0u);
+}
+
 constexpr int kScalarThreads = 1024;
-__global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __restrict__ partials,
-                                                               int64_t blocks, int mode,
-                                                               double* __restrict__ res) {
+// FINISH (mode 2, one domain): then the convergence test and the loop
+// condition in the same kernel (no separate one-thread launch)
+template <bool FINISH = false>
+__global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(
+    const double* __restrict__ partials, int64_t blocks, int mode, double* __restrict__ res,
+    cudaGraphConditionalHandle h = {}, int use_cond = 0, int64_t max_iter = 0,
+    double n_global = 0.0, double tol = 0.0) {
   if (mode != 0 && res[27] != 0.0) return;
   // one block of 1024 threads, 4 independent loads in flight per thread: the
   // iteration's critical path waits on this sum twice (was 256 threads and
@@ -819,6 +843,7 @@ __global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __r
     } else {
       res[22] = s[0][0];
       res[23] = s[1][0];
+      if (FINISH) cg_finish(h, use_cond, res, max_iter, n_global, tol);
     }
   }
 }
@@ -828,20 +853,7 @@ __global__ void __launch_bounds__(kScalarThreads) k_cg_scalars(const double* __r
 // while graph also the loop condition.
 __global__ void k_cg_finish(cudaGraphConditionalHandle h, int use_cond, double* __restrict__ res,
                             int64_t max_iter, double n_global, double tol) {
-  if (res[27] != 0.0) {
-    if (use_cond) cudaGraphSetConditional(h, 0u);
-    return;
-  }
-  const double rz_new = res[22];
-  const double rms = sqrt(res[23] / n_global) * kDebye;
-  res[25] = rms;
-  res[24] = (res[21] != 0.0) ? rz_new / res[21] : 0.0;
-  res[21] = rz_new;
-  const double it = res[28] + 1.0;
-  res[28] = it;
-  const bool conv = rms < tol;
-  res[27] = conv ? 1.0 : 0.0;
-  if (use_cond) cudaGraphSetConditional(h, (!conv && it < (double)max_iter) ? 1u : 0u);
+  cg_finish(h, use_cond, res, max_iter, n_global, tol);
 }
 
 __global__ void k_set_result(double* __restrict__ res, int slot, double v) { res[slot] = v; }
@@ -863,7 +875,17 @@ static void pcg_dom_setup(PcgDom& d, mdg_ctx* c) {
   const PrunedList& P = c->plist;
   const int64_t n = c->n_own;
   d.c = c;
-  d.blocks = grid_for(n);
+  // vector kernels: grid-stride over a few blocks per SM, so their block
+  // partials (the CG sums) stay few
+  {
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      MDG_CUDA_CHECK(cudaGetDevice(&dev));
+      MDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    d.blocks = std::max<int64_t>(1, std::min<int64_t>(grid_for(n), (int64_t)sms * 8));
+  }
   d.cl = P.cl_valid;
   d.tma = !d.cl && use_tma(P);
   const int64_t units = d.cl ? P.ncl : n;
@@ -1012,18 +1034,23 @@ static void pcg_body(std::vector<PcgDom>& ds, PcgComm* comm, cudaGraphConditiona
     k_cg_update<<<(unsigned)d.blocks, kBlock, 0, c->stream>>>(n, c->polp, c->results, c->cg_p,
                                                              c->cg_q, c->mu, c->cg_r, c->cg_z,
                                                              c->partials);
-    k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, d.blocks, 2, c->results);
+    if (comm)
+      k_cg_scalars<<<1, kScalarThreads, 0, c->stream>>>(c->partials, d.blocks, 2, c->results);
+    else  // one domain: the convergence test in the same kernel
+      k_cg_scalars<true><<<1, kScalarThreads, 0, c->stream>>>(
+          c->partials, d.blocks, 2, c->results, h, use_cond, max_iter, n_global, tol);
   }
   if (comm) comm->allreduce(22, 2);
   for (PcgDom& d : ds) {
     mdg_ctx* c = d.c;
     // the loop condition is the first domain's (identical on all of them)
-    k_cg_finish<<<1, 1, 0, c->stream>>>(h, use_cond && &d == &ds[0], c->results, max_iter,
-                                        n_global, tol);
+    if (comm)
+      k_cg_finish<<<1, 1, 0, c->stream>>>(h, use_cond && &d == &ds[0], c->results, max_iter,
+                                          n_global, tol);
     k_cg_dir<<<grid_for(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->results, c->cg_z,
                                                              c->cg_p);
   }
-  for (PcgDom& d : ds) d.c->launches += 6;
+  for (PcgDom& d : ds) d.c->launches += comm ? 6 : 5;
 }
 
 // Loop body as a CUDA graph with a device-side while node: the host launches
