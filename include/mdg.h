@@ -458,6 +458,14 @@ int mdg_set_overlap(mdg_ctx* ctx, int on);
  * (DESIGN.md section 4). Applies only to buffered cut rows without an
  * overlapped domain exchange. The dipoles agree to rounding either way. */
 int mdg_set_cluster_matvec(mdg_ctx* ctx, int on);
+/* Halgren on site clusters (default 1; MDG_CLUSTER_HALGREN=0 sets the
+ * default of new contexts): per cluster of 3 consecutive sites (a water
+ * molecule in the molecule-keyed order) the union of the sites' buffered
+ * half rows, walked once with a lane per union entry -- j's record gathered
+ * and its partner force added once for the three sites. The per-site half
+ * rows otherwise (in deterministic mode and for unbuffered rows). The same
+ * pairs either way. */
+int mdg_set_cluster_halgren(mdg_ctx* ctx, int on);
 /* Gather 3 doubles per listed caller-order site of vec_id into out[3*count]
  * (x,y,z interleaved) / scatter them back. Host buffers. */
 int mdg_vec_pack(mdg_ctx* ctx, int vec_id, const int32_t* sites, int64_t count, double* out);

@@ -250,6 +250,7 @@ int mdg_ctx_create(mdg_ctx** out, int device, int64_t n_capacity, int32_t max_pa
       if (const char* d = getenv("MDG_DETERMINISTIC")) c->deterministic = atoi(d) != 0;
       if (const char* o = getenv("MDG_OVERLAP")) c->overlap = atoi(o) != 0;
       if (const char* o = getenv("MDG_CLUSTER_MATVEC")) c->cluster_matvec = atoi(o) != 0;
+      if (const char* o = getenv("MDG_CLUSTER_HALGREN")) c->cluster_halgren = atoi(o) != 0;
       set_device(c);
       c->n_cap = n_capacity;
       c->max_pairs = max_pairs_per_atom > 0 ? max_pairs_per_atom : 2 * MDG_MAX_NEIGHBORS;
@@ -327,7 +328,9 @@ int mdg_ctx_destroy(mdg_ctx* c) {
     if (L.nbr) cudaFree(L.nbr);
     if (L.cnt) cudaFree(L.cnt);
     if (L.ref0) cudaFree(L.ref0);
-    for (void* p : {(void*)L.inner.nbr, (void*)L.inner.cnt, (void*)L.inner.ref, (void*)L.inner.flag})
+    for (void* p : {(void*)L.inner.nbr, (void*)L.inner.cnt, (void*)L.inner.ref, (void*)L.inner.flag,
+                     (void*)L.inner.gen, (void*)L.inner.uidx, (void*)L.inner.ucnt,
+                     (void*)L.inner.ugen})
       if (p) cudaFree(p);
     if (L.inner.hcuts) cudaFreeHost(L.inner.hcuts);
   }
@@ -511,6 +514,13 @@ int mdg_set_cluster_matvec(mdg_ctx* c, int on) {
   return guard([&] {
     need_ctx(c);
     c->cluster_matvec = on != 0;
+  });
+}
+
+int mdg_set_cluster_halgren(mdg_ctx* c, int on) {
+  return guard([&] {
+    need_ctx(c);
+    c->cluster_halgren = on != 0;
   });
 }
 

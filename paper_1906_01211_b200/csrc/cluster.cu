@@ -121,6 +121,58 @@ __global__ void __launch_bounds__(kBlock) k_cluster_union(CUArgs a) {
   if (k == 0 && cl < a.ncl) a.ucnt[cl] = s;
 }
 
+// Plain unions (no maps, no tensors) of a list's buffered rows for the
+// cluster pair kernels: the merge of k_cluster_union writing the sorted
+// union of each cluster's kCl rows into uidx[cl * ucap ...].
+struct RUArgs {
+  int64_t n, ncl;
+  ListView rows;
+  int32_t* __restrict__ uidx;
+  int32_t* __restrict__ ucnt;
+  int32_t ucap;
+  const int32_t* __restrict__ gen;
+  const int32_t* __restrict__ ugen;
+};
+
+__global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a) {
+  if (a.gen && *a.gen == *a.ugen) return;  // the rows were not cut again
+  constexpr int NG = 32 / kGrp;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / kGrp, k = lane % kGrp;
+  const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int64_t cl = warp * NG + g;
+  const int64_t i = cl * kCl + k;
+  const bool vi = k < kCl && cl < a.ncl && i < a.n;
+  const int len = vi ? a.rows.cnt[i] : 0;
+  const int4* row = reinterpret_cast<const int4*>(a.rows.nbr + (size_t)(vi ? i : 0) * a.rows.cap);
+  int32_t* out = a.uidx + (size_t)(cl < a.ncl ? cl : 0) * a.ucap;
+  int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+  if (len > 0) b0 = __ldcs(row);
+  if (len > 4) b1 = __ldcs(row + 1);
+  int h = 0;
+  int32_t cur = (len > 0) ? (b0.x & 0x7fffffff) : INT_MAX;
+  int s = 0;
+  for (;;) {
+    int32_t m = cur;
+#pragma unroll
+    for (int o = 1; o < kGrp; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const bool live = m != INT_MAX;
+    if (!__any_sync(0xffffffffu, live)) break;
+    const bool hit = live && cur == m;
+    MDG_DASSERT(!live || s < a.ucap);
+    if (k == 0 && live) out[s] = m;
+    s += live;
+    h += hit;
+    if (hit && (h & 3) == 0) {
+      b0 = b1;
+      if (h + 4 < len) b1 = __ldcs(row + (h >> 2) + 1);
+    }
+    const int32_t nx = row_elem(b0, h & 3) & 0x7fffffff;
+    cur = hit ? ((h < len) ? nx : INT_MAX) : cur;
+  }
+  if (k == 0 && cl < a.ncl) a.ucnt[cl] = s;
+}
+
 __global__ void k_cluster_gen(const int32_t* __restrict__ gen, int32_t* __restrict__ ugen) {
   *ugen = gen ? *gen : -1;
 }
@@ -386,6 +438,57 @@ bool build_clusters(mdg_ctx* c, double cutoff, const ListView& rows, const int32
   P.nch = nch;
   for (int q = 0; q < 4; ++q) P.ukey[q] = key[q];
   P.ubuilt = true;
+  return true;
+}
+
+bool build_row_unions(mdg_ctx* c, int list_id, const ListView& rows) {
+  DevList& L = c->lists[list_id];
+  DevList::Inner& I = L.inner;
+  if (!c->cluster_halgren || c->deterministic || !rows.sorted || !rows.dense || !I.gen ||
+      c->n_own == 0)
+    return false;
+  const int64_t n = c->n_own;
+  const int64_t ncl = (n + kCl - 1) / kCl;
+  const int32_t ucap = (int32_t)std::min<int64_t>((int64_t)kCl * rows.cap, (int64_t)1 << 30);
+  const uintptr_t key[3] = {(uintptr_t)rows.nbr, (uintptr_t)rows.cap, (uintptr_t)ncl};
+  bool force = !I.ubuilt;
+  for (int q = 0; q < 3; ++q) force = force || I.ukey[q] != key[q];
+  const size_t need = (size_t)ncl * (size_t)ucap;
+  if (need > I.uelems) {
+    if (I.uidx) cudaFree(I.uidx);
+    I.uidx = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&I.uidx, need * sizeof(int32_t)));
+    I.uelems = need;
+    force = true;
+  }
+  if (!I.ugen) {
+    MDG_CUDA_CHECK(cudaMalloc(&I.ugen, sizeof(int32_t)));
+    force = true;
+  }
+  if (ncl > I.ucnt_elems) {
+    if (I.ucnt) cudaFree(I.ucnt);
+    I.ucnt = nullptr;
+    MDG_CUDA_CHECK(cudaMalloc(&I.ucnt, (size_t)ncl * sizeof(int32_t)));
+    I.ucnt_elems = ncl;
+    force = true;
+  }
+  RUArgs a;
+  a.n = n;
+  a.ncl = ncl;
+  a.rows = rows;
+  a.uidx = I.uidx;
+  a.ucnt = I.ucnt;
+  a.ucap = ucap;
+  a.gen = force ? nullptr : I.gen;
+  a.ugen = I.ugen;
+  const int64_t warps = (ncl + 32 / kGrp - 1) / (32 / kGrp);
+  const unsigned grid = (unsigned)((warps * 32 + kBlock - 1) / kBlock);
+  MDG_LAUNCH(c, "row_union", grid, kBlock, 0, k_row_union, a);
+  MDG_LAUNCH(c, "cluster_gen", 1, 1, 0, k_cluster_gen, I.gen, I.ugen);
+  I.ucap = ucap;
+  I.ncl = ncl;
+  for (int q = 0; q < 3; ++q) I.ukey[q] = key[q];
+  I.ubuilt = true;
   return true;
 }
 

@@ -84,6 +84,18 @@ struct DevList {
     int32_t* hcuts = nullptr;
     int32_t* dcuts = nullptr;
     int calls = 0, cuts0 = 0, bypass = 0;
+    // site-cluster unions of these rows (cluster.cu build_row_unions): per
+    // cluster of kCl consecutive sites the sorted union of their rows,
+    // rebuilt on the device when the rows are cut again
+    int32_t* uidx = nullptr;
+    int32_t* ucnt = nullptr;
+    int32_t* ugen = nullptr;
+    size_t uelems = 0;
+    int64_t ucnt_elems = 0;
+    int32_t ucap = 0;
+    int64_t ncl = 0;
+    uintptr_t ukey[3] = {0, 0, 0};
+    bool ubuilt = false;
   } inner;
 };
 
@@ -334,6 +346,8 @@ struct mdg_ctx {
   bool overlap = true;  // AMOEBA step on two streams (mdg_set_overlap)
   // PCG on site clusters (cluster.cu; mdg_set_cluster_matvec, MDG_CLUSTER_MATVEC)
   bool cluster_matvec = false;
+  // Halgren on site clusters (nonpolar.cu k_halgren_cl; MDG_CLUSTER_HALGREN)
+  bool cluster_halgren = true;
   // site order molecule-keyed (resort.cu): a molecule's sites consecutive
   bool mol_sorted = false;
   bool has_polar_force = false;  // last AMOEBA step added polarization forces
@@ -508,6 +522,10 @@ void run_field_tpre(mdg_ctx* c, int list_id, double alpha, double cutoff, double
 bool build_clusters(mdg_ctx* c, double cutoff, const struct ListView& rows, const int32_t* gen,
                     int32_t tcap, bool force);
 void count_stats_n(mdg_ctx* c, const int32_t* cnt, int64_t n, int slot);
+// The cluster unions of list `list_id`'s buffered rows `rows` (L.inner), for
+// the cluster pair kernels (Halgren); false when they do not apply (rows not
+// buffered / sorted, deterministic mode, disabled)
+bool build_row_unions(mdg_ctx* c, int list_id, const struct ListView& rows);
 // an NCCL / LOCAL group runs the interior/halo overlapped exchange (per-site rows)
 bool group_overlap(const mdg_ctx* c);
 CLArgs cl_args(mdg_ctx* c, const double4* in, double4* out);

@@ -262,6 +262,7 @@ void resort_sites(mdg_ctx* c, const int32_t* rep) {
   for (auto& L : c->lists) {
     L.valid = false;
     L.inner.src_version = -1;
+    L.inner.ubuilt = false;
   }
   c->plist.valid = false;
   c->plist.cl_valid = false;

@@ -170,6 +170,7 @@ SIGNATURES = {
     "mdg_frames_upload": (C.c_int, [C.c_void_p, _ip, _ip, _ip, _dp, _dp]),
     "mdg_set_overlap": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_set_cluster_matvec": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_set_cluster_halgren": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_vec_pack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_unpack": (C.c_int, [C.c_void_p, C.c_int, _ip, C.c_int64, _dp]),
     "mdg_vec_pack_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
@@ -786,6 +787,10 @@ class Engine:
     def set_cluster_matvec(self, on: bool = True):
         """PCG mat-vec on 3-site clusters (opt-in) or per-site rows (mdg.h)."""
         check(self.lib.mdg_set_cluster_matvec(self.ctx, int(on)))
+
+    def set_cluster_halgren(self, on: bool = True):
+        """Halgren on 3-site clusters (default) or per-site half rows (mdg.h)."""
+        check(self.lib.mdg_set_cluster_halgren(self.ctx, int(on)))
 
     def launch_count(self) -> int:
         return int(self.lib.mdg_launch_count(self.ctx))

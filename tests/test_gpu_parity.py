@@ -447,6 +447,34 @@ def test_cluster_matvec_pcg_matches_oracle_and_per_site(engine, oracle, mdg):
     np.testing.assert_allclose(f1, f0, rtol=0, atol=1e-12 * np.abs(f0).max())
 
 
+def test_cluster_halgren_matches_per_site_and_oracle(engine, oracle, mdg):
+    """Halgren on 3-site clusters (the default) against the per-site half rows
+    and the oracle: energy, forces and virial, over two steps (the second
+    reuses the unions), with the H reduction and exclusions of the AMOEBA
+    water fixture (molecules straddle the periodic boundary)."""
+    s = amoeba_small(mdg, 1000, 31.04, 12)
+    so = to_oracle_system(s)
+    so.x, so.y, so.z = oracle.reduce_sites(so, s.hred_parent, s.hred_factor)
+    fred, eo, wo = oracle.halgren(so, oracle.build_table(so, 11.0), 9.0, exclude=True)
+    fo = oracle.reduce_forces(s.hred_parent, s.hred_factor, fred)
+    engine.upload_system(s)
+    tv = engine.build_neighbor_table(11.0, list_id=1, sites=mdg.SITES_VDW)
+    out = {}
+    try:
+        for on in (False, True):
+            engine.set_cluster_halgren(on)
+            for _ in range(2):
+                out[on] = engine.halgren_forces(tv, mdg.HalgrenParams(9.0), exclude=True)
+    finally:
+        engine.set_cluster_halgren(True)
+    a, b = out[True], out[False]
+    assert rel(a.energy, b.energy) <= 1e-12
+    np.testing.assert_allclose(a.forces, b.forces, rtol=0, atol=1e-12 * np.abs(b.forces).max())
+    np.testing.assert_allclose(a.virial, b.virial, rtol=0, atol=1e-12 * np.abs(b.virial).max())
+    assert rel(a.energy, eo) <= E_TOL
+    assert force_err_rms(a.forces, fo) <= F_TOL
+
+
 def test_mpole_matches_oracle(engine, oracle, mdg):
     """Real-space multipole energy/forces/torques/virial vs the T-tensor oracle."""
     s = amoeba_small(mdg, 343, 21.0, 5)
