@@ -298,9 +298,9 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_MINB) k_halgren(HalgrenKAr
 
 // Halgren on site clusters (cluster.cu build_row_unions): warp per cluster
 // of kCl consecutive sites (a water molecule in the molecule-keyed order),
-// lane per entry j of the sorted union of the sites' buffered rows -- the
-// entries past the cluster's first site, so each pair once, in the cluster
-// of its lower index (the per-site half rows' rule: j > i). j's record is
+// lane per entry j of the union of the sites' buffered rows past the
+// cluster's first site (cluster.cu k_row_union), so each pair once, in the
+// cluster of its lower index (the per-site half rows' rule: j > i). j's record is
 // gathered and its partner force added with FP64 atomics once for the kCl
 // sites (2.15 pairs per entry on config 4, against one per pair in the
 // per-site rows); the sites' forces are summed once per cluster. Every pair
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kBlock, MDG_HALGREN_CL_MINB) k_halgren_cl(Halg
     __syncwarp();
     const int ucount = a.ucnt[cl];
     const int32_t* urow = a.uidx + (size_t)cl * a.ucap;
-    const int start = row_suffix(urow, ucount, i0, lane);  // the entries > i0
+    const int start = 0;  // the half union: every entry is past the cluster's first site
     double fx[kCl], fy[kCl], fz[kCl];
 #pragma unroll
     for (int t = 0; t < kCl; ++t) fx[t] = fy[t] = fz[t] = 0.0;
