@@ -248,161 +248,178 @@ struct ClCur {
   int32_t cnt;   // the cluster's entry count
 };
 
+// Warp-specialized: warp 0 of the block is the producer -- it walks the
+// chunk sequences of the three consumer warps and issues each chunk's bulk
+// copy into the consumer's stage ring as soon as the consumer has released
+// the stage (full / empty mbarrier pairs); warps 1-3 only wait, gather and
+// compute. (With every warp issuing its own copies the kernel was
+// issue-bound at ~310 instructions per chunk, most of them the copy and
+// cursor bookkeeping.)
+constexpr int kClConsumers = kWarps - 1;
+
 template <bool PCG>
 __global__ void __launch_bounds__(kBlock, MDG_CL_MINB) k_tmatvec_cl(CLArgs a) {
   if (PCG && a.res[27] != 0.0) return;  // converged (speculative iteration)
-  __shared__ ClStage st_mem[kWarps][kClStages];
-  __shared__ uint64_t bar_mem[kWarps][kClStages];
-  __shared__ double4 cs_mem[kWarps][3 * kCl];  // the current cluster: pos, p, polp
+  __shared__ ClStage st_mem[kClConsumers][kClStages];
+  __shared__ uint64_t full_mem[kClConsumers][kClStages], empty_mem[kClConsumers][kClStages];
+  __shared__ double4 cs_mem[kClConsumers][3 * kCl];  // the current cluster: pos, p, polp
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  ClStage* st = st_mem[w];
-  uint64_t* bar = bar_mem[w];
-  double4* cs = cs_mem[w];
   double acc1[1] = {0.0};
-  const int32_t first = (int32_t)((int64_t)blockIdx.x * a.ipw + w);
-  const int32_t end = (int32_t)min(a.ncl, ((int64_t)blockIdx.x + 1) * a.ipw);
-  const int32_t nq = first < end ? (end - first + kWarps - 1) / kWarps : 0;
-  if (nq > 0) {
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < kClStages; ++s) mbar_init(&bar[s]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    // entry counts of the warp's clusters, 32 at a time, one per lane
-    auto counts = [&](int32_t q0) {
-      const int32_t q = q0 + lane;
-      return q < nq ? __ldg(a.ucnt + first + (int64_t)q * kWarps) : 0;
-    };
-    auto advance = [&](ClCur& c, int32_t& batch) {
-      if (c.base + 32 < c.cnt) {
-        c.base += 32;
-        return;
+  const int64_t b0 = (int64_t)blockIdx.x * a.ipw;
+  const int32_t end = (int32_t)min(a.ncl, b0 + a.ipw);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < kClConsumers; ++c)
+      for (int s = 0; s < kClStages; ++s) {
+        mbar_init(&full_mem[c][s]);
+        mbar_init(&empty_mem[c][s]);
       }
-      ++c.q;
-      c.base = 0;
-      if ((c.q & 31) == 0) batch = counts(c.q);
-      c.cnt = __shfl_sync(0xffffffffu, batch, c.q & 31);
-    };
-    // lane 0: the copies of chunk c into stage s
-    auto issue = [&](const ClCur& c, int s) {
-      const int64_t cl = first + (int64_t)c.q * kWarps;
-      const int64_t i0 = cl * kCl;
-      const int ns = c.base == 0 ? (int)min((int64_t)kCl, a.n - i0) : 0;
-      ClStage& S = st[s];
-      mbar_arm(&bar[s], (uint32_t)(sizeof(ClChunk) + ns * (PCG ? 80 : 32)));
-      bulk_load(&S.ch, a.cst + (size_t)cl * a.nch + (c.base >> 5), sizeof(ClChunk), &bar[s]);
-      if (ns > 0) {
-        bulk_load(S.spos, a.pos + i0, 32 * ns, &bar[s]);
-        if (PCG) {
-          bulk_load(S.sin, a.in + i0, 32 * ns, &bar[s]);
-          bulk_load(S.spol, a.polp + i0, 16 * ns, &bar[s]);
-        }
-      }
-    };
-    uint32_t phase = 0u;  // bit s: parity of stage s's next completion
-    auto wait = [&](int s) {
-      mbar_wait(&bar[s], (phase >> s) & 1u);
-      phase ^= 1u << s;
-    };
-    int32_t pbatch = counts(0), cbatch = pbatch;
-    ClCur prod{0, 0, __shfl_sync(0xffffffffu, pbatch, 0)};
-    ClCur cons = prod;
-#pragma unroll
-    for (int s = 0; s < kClStages - 1; ++s) {
-      if (prod.q < nq) {
-        if (lane == 0) issue(prod, s);
-        advance(prod, pbatch);
-      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // consumer c's clusters: b0 + c, b0 + c + 3, ...; a chunk = (q, base, cnt)
+  auto cl_of = [&](int c, int32_t q) { return (int32_t)(b0 + c + (int64_t)q * kClConsumers); };
+  auto advance = [&](int c, ClCur& u) {
+    if (u.base + 32 < u.cnt) {
+      u.base += 32;
+      return;
     }
-    wait(0);
-    double4 p0, m0, p1, m1;
-    {
-      const int32_t j = st[0].ch.idx[lane];
-      p0 = ldg4(a.pos + j);
-      m0 = ldg4(a.in + j);
+    ++u.q;
+    u.base = 0;
+    const int32_t cl = cl_of(c, u.q);
+    u.cnt = cl < end ? __ldg(a.ucnt + cl) : 0;
+  };
+  if (w == 0) {
+    // ---- producer
+    ClCur u[kClConsumers];
+    int k[kClConsumers];
+    bool live[kClConsumers];
+    for (int c = 0; c < kClConsumers; ++c) {
+      const int32_t cl = cl_of(c, 0);
+      live[c] = cl < end;
+      u[c] = ClCur{0, 0, live[c] ? __ldg(a.ucnt + cl) : 0};
+      k[c] = 0;
     }
-    ClCur next = cons;
-    int32_t nbatch = cbatch;
-    advance(next, nbatch);
-    double ex[kCl], ey[kCl], ez[kCl];
-#pragma unroll
-    for (int t = 0; t < kCl; ++t) ex[t] = ey[t] = ez[t] = 0.0;
-    static_assert((kClStages & (kClStages - 1)) == 0, "stages: a power of two");
-    for (int k = 0; cons.q < nq; ++k) {
-      const int cur = k & (kClStages - 1), nxt = (k + 1) & (kClStages - 1);
-      // refill the stage chunk k - 1 used
-      if (prod.q < nq) {
-        __syncwarp();
+    for (;;) {
+      bool any = false;
+      for (int c = 0; c < kClConsumers; ++c) {
+        if (!live[c]) continue;
+        any = true;
+        const int s = k[c] & (kClStages - 1);
+        mbar_wait(&empty_mem[c][s], ((k[c] / kClStages) & 1) ^ 1);  // the consumer released it
         if (lane == 0) {
+          const int64_t cl = cl_of(c, u[c].q);
+          const int64_t i0 = cl * kCl;
+          const int ns = u[c].base == 0 ? (int)min((int64_t)kCl, a.n - i0) : 0;
+          ClStage& S = st_mem[c][s];
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(prod, (k + kClStages - 1) & (kClStages - 1));
-        }
-        advance(prod, pbatch);
-      }
-      // the next chunk's gathers
-      if (next.q < nq) {
-        wait(nxt);
-        const int32_t j = st[nxt].ch.idx[lane];
-        p1 = ldg4(a.pos + j);
-        m1 = ldg4(a.in + j);
-      }
-      const ClStage& S = st[cur];
-      if (cons.base == 0) {  // a new cluster: keep its site records
-        if (lane < kCl) {
-          cs[lane] = S.spos[lane];
-          if (PCG) {
-            cs[kCl + lane] = S.sin[lane];
-            const double2 pp = S.spol[lane];
-            cs[2 * kCl + lane] = make_double4(pp.x, pp.y, 0.0, 0.0);
+          mbar_arm(&full_mem[c][s], (uint32_t)(sizeof(ClChunk) + ns * (PCG ? 80 : 32)));
+          bulk_load(&S.ch, a.cst + (size_t)cl * a.nch + (u[c].base >> 5), sizeof(ClChunk),
+                    &full_mem[c][s]);
+          if (ns > 0) {
+            bulk_load(S.spos, a.pos + i0, 32 * ns, &full_mem[c][s]);
+            if (PCG) {
+              bulk_load(S.sin, a.in + i0, 32 * ns, &full_mem[c][s]);
+              bulk_load(S.spol, a.polp + i0, 16 * ns, &full_mem[c][s]);
+            }
           }
         }
-        __syncwarp();
+        ++k[c];
+        advance(c, u[c]);
+        live[c] = cl_of(c, u[c].q) < end;
       }
+      if (!any) break;
+    }
+  } else {
+    // ---- consumer c
+    const int c = w - 1;
+    ClStage* st = st_mem[c];
+    uint64_t* full = full_mem[c];
+    uint64_t* empty = empty_mem[c];
+    double4* cs = cs_mem[c];
+    if (cl_of(c, 0) < end) {
+      ClCur cons{0, 0, __ldg(a.ucnt + cl_of(c, 0))};
+      ClCur next = cons;
+      advance(c, next);
+      mbar_wait(&full[0], 0);
+      double4 p0, m0, p1, m1;
+      {
+        const int32_t j = st[0].ch.idx[lane];
+        p0 = ldg4(a.pos + j);
+        m0 = ldg4(a.in + j);
+      }
+      double ex[kCl], ey[kCl], ez[kCl];
 #pragma unroll
-      for (int t = 0; t < kCl; ++t) {
-        const double2 r = S.ch.ten[t][lane];
-        const double4 pi = cs[t];
-        const double ox = __dsub_rn(pi.x, p0.x), oy = __dsub_rn(pi.y, p0.y),
-                     oz = __dsub_rn(pi.z, p0.z);
-        const double dx = __fma_rn(-rint(__dmul_rn(ox, a.b.ix)), a.b.lx, ox);
-        const double dy = __fma_rn(-rint(__dmul_rn(oy, a.b.iy)), a.b.ly, oy);
-        const double dz = __fma_rn(-rint(__dmul_rn(oz, a.b.iz)), a.b.lz, oz);
-        const double dot = m0.x * dx + m0.y * dy + m0.z * dz;
-        ex[t] += r.y * dot * dx - r.x * m0.x;
-        ey[t] += r.y * dot * dy - r.x * m0.y;
-        ez[t] += r.y * dot * dz - r.x * m0.z;
-      }
-      if (next.q != cons.q) {  // the cluster's last chunk: reduce, write, reset
-        double mx = 0, my = 0, mz = 0;  // lane t < kCl keeps site t's sums
+      for (int t = 0; t < kCl; ++t) ex[t] = ey[t] = ez[t] = 0.0;
+      for (int kc = 0;; ++kc) {
+        const int slot = kc & (kClStages - 1), nslot = (kc + 1) & (kClStages - 1);
+        const bool more = cl_of(c, next.q) < end;
+        if (more) {  // the next chunk's gathers, in flight during this one's math
+          mbar_wait(&full[nslot], ((kc + 1) / kClStages) & 1);
+          const int32_t j = st[nslot].ch.idx[lane];
+          p1 = ldg4(a.pos + j);
+          m1 = ldg4(a.in + j);
+        }
+        const ClStage& S = st[slot];
+        if (cons.base == 0) {  // a new cluster: keep its site records
+          if (lane < kCl) {
+            cs[lane] = S.spos[lane];
+            if (PCG) {
+              cs[kCl + lane] = S.sin[lane];
+              const double2 pp = S.spol[lane];
+              cs[2 * kCl + lane] = make_double4(pp.x, pp.y, 0.0, 0.0);
+            }
+          }
+          __syncwarp();
+        }
 #pragma unroll
         for (int t = 0; t < kCl; ++t) {
-          const double sx = warp_allsum(ex[t]), sy = warp_allsum(ey[t]), sz = warp_allsum(ez[t]);
-          if (lane == t) {
-            mx = sx;
-            my = sy;
-            mz = sz;
-          }
-          ex[t] = ey[t] = ez[t] = 0.0;
-        }
-        const int64_t i = (first + (int64_t)cons.q * kWarps) * kCl + lane;
-        if (lane < kCl && i < a.n) {
-          if (PCG) {
-            const double4 p = cs[kCl + lane];
-            const double inva = 1.0 / cs[2 * kCl + lane].x;
-            const double qx = p.x * inva - mx, qy = p.y * inva - my, qz = p.z * inva - mz;
-            a.out[i] = make_double4(qx, qy, qz, 0.0);
-            acc1[0] += p.x * qx + p.y * qy + p.z * qz;
-          } else {
-            a.out[i] = make_double4(mx, my, mz, 0.0);
-          }
+          const double2 r = S.ch.ten[t][lane];
+          const double4 pi = cs[t];
+          const double ux = __dsub_rn(pi.x, p0.x), uy = __dsub_rn(pi.y, p0.y),
+                       uz = __dsub_rn(pi.z, p0.z);
+          const double dx = __fma_rn(-rint(__dmul_rn(ux, a.b.ix)), a.b.lx, ux);
+          const double dy = __fma_rn(-rint(__dmul_rn(uy, a.b.iy)), a.b.ly, uy);
+          const double dz = __fma_rn(-rint(__dmul_rn(uz, a.b.iz)), a.b.lz, uz);
+          const double dot = m0.x * dx + m0.y * dy + m0.z * dz;
+          ex[t] += r.y * dot * dx - r.x * m0.x;
+          ey[t] += r.y * dot * dy - r.x * m0.y;
+          ez[t] += r.y * dot * dz - r.x * m0.z;
         }
         __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // the stage may be refilled
+        if (next.q != cons.q) {  // the cluster's last chunk: reduce, write, reset
+          double mx = 0, my = 0, mz = 0;  // lane t < kCl keeps site t's sums
+#pragma unroll
+          for (int t = 0; t < kCl; ++t) {
+            const double sx = warp_allsum(ex[t]), sy = warp_allsum(ey[t]),
+                         sz = warp_allsum(ez[t]);
+            if (lane == t) {
+              mx = sx;
+              my = sy;
+              mz = sz;
+            }
+            ex[t] = ey[t] = ez[t] = 0.0;
+          }
+          const int64_t i = (int64_t)cl_of(c, cons.q) * kCl + lane;
+          if (lane < kCl && i < a.n) {
+            if (PCG) {
+              const double4 p = cs[kCl + lane];
+              const double inva = 1.0 / cs[2 * kCl + lane].x;
+              const double qx = p.x * inva - mx, qy = p.y * inva - my, qz = p.z * inva - mz;
+              a.out[i] = make_double4(qx, qy, qz, 0.0);
+              acc1[0] += p.x * qx + p.y * qy + p.z * qz;
+            } else {
+              a.out[i] = make_double4(mx, my, mz, 0.0);
+            }
+          }
+          __syncwarp();
+        }
+        if (!more) break;
+        cons = next;
+        advance(c, next);
+        p0 = p1;
+        m0 = m1;
       }
-      cons = next;
-      advance(next, nbatch);
-      p0 = p1;
-      m0 = m1;
     }
   }
   if (PCG) block_store_partials<1>(acc1, a.partials);
