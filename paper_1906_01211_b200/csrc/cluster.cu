@@ -136,74 +136,64 @@ struct RUArgs {
 
 // Half unions: warp per cluster; the entries past the cluster's first site
 // of row 0, then those of row 1 not in row 0, then those of row 2 in neither,
-// compacted by ballot and stored coalesced. Not sorted as a whole (three
-// sorted runs): the cluster kernels test j > i per pair. Membership: the
-// chunk's 32 values (ascending across the lanes) against a sliding 32-entry
-// window of the other sorted row held one entry per lane -- a 5-step
-// shuffle search per window, the window advancing monotonically along the
-// row. (A sequential 3-way merge by lane groups: 2.5 ms per build on config
-// 4; per-value binary search in memory: 1.4 ms, instruction-bound.)
-__device__ __forceinline__ bool in_row_window(const int32_t* __restrict__ r, int& p, int end,
-                                              int32_t x, bool v, int lane) {
-  // chunk maximum (the valid lanes are a prefix and ascending)
-  const unsigned vm = __ballot_sync(0xffffffffu, v);
-  if (vm == 0) return false;
-  const int32_t xmax = __shfl_sync(0xffffffffu, x, 31 - __clz(vm));
-  bool found = false;
-  for (;;) {
-    const int32_t w = (p + lane < end) ? (__ldg(r + p + lane) & 0x7fffffff) : INT_MAX;
-    int pos = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const int32_t c = __shfl_sync(0xffffffffu, w, pos + step - 1);
-      if (c < x) pos += step;
-    }
-    const int32_t at = __shfl_sync(0xffffffffu, w, pos & 31);
-    found |= v && pos < 32 && at == x;
-    const int32_t wmax = __shfl_sync(0xffffffffu, w, 31);
-    if (wmax >= xmax || p + 32 >= end) break;
-    p += 32;
-  }
-  return found;
+// compacted by ballot and stored coalesced. The rows need no order:
+// membership through a per-warp open-addressing hash set in shared memory
+// (rows 0 and 1 inserted, load <= 1/2), so the cut that feeds it skips the
+// row sort (kernel_rows want_sorted = false). (A sequential 3-way merge of
+// sorted rows by lane groups took 2.5 ms per build on config 4, per-value
+// binary search 1.4 ms, a sliding-window shuffle search 1.15 ms -- plus the
+// 2.6 ms sort of the rows they needed.)
+__device__ __forceinline__ uint32_t hslot(int32_t x, int tbits) {
+  return ((uint32_t)x * 0x9E3779B1u) >> (32 - tbits);
 }
 
-__global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a) {
+__global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a, int tbits) {
   if (a.gen && *a.gen == *a.ugen) return;  // the rows were not cut again
+  extern __shared__ int32_t hmem[];
+  int32_t* tab = hmem + ((size_t)(threadIdx.x >> 5) << tbits);
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const int64_t nw = (int64_t)gridDim.x * kWarps;
   for (int64_t cl = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); cl < a.ncl; cl += nw) {
     const int64_t i0 = cl * kCl;
     const int nv = (int)min((int64_t)kCl, a.n - i0);
-    const int32_t* r[kCl];
-    int st[kCl], en[kCl];
-#pragma unroll
-    for (int t = 0; t < kCl; ++t) {
-      r[t] = a.rows.nbr + (size_t)(t < nv ? i0 + t : i0) * a.rows.cap;
-      en[t] = t < nv ? a.rows.cnt[i0 + t] : 0;
-      st[t] = t < nv ? row_suffix(r[t], en[t], i0, lane) : 0;
-    }
+    // this cluster's table: a power of two >= 2 x the keys rows 0 and 1 can
+    // insert (load <= 1/2), within the T allocated (cleared per cluster)
+    const int need = a.rows.cnt[i0] + (nv > 1 ? a.rows.cnt[i0 + 1] : 0);
+    int tb = 6;
+    while (tb < tbits && (1 << tb) < 2 * need) ++tb;
+    const int Tc = 1 << tb;
+    __syncwarp();
+    for (int e = lane; e < Tc; e += 32) tab[e] = -1;
+    __syncwarp();
     int32_t* out = a.uidx + (size_t)cl * a.ucap;
     int s = 0;
-#pragma unroll
-    for (int t = 0; t < kCl; ++t) {
-      int pq[kCl];
-#pragma unroll
-      for (int q = 0; q < kCl; ++q) pq[q] = st[q];
-      for (int b = st[t]; b < en[t]; b += 32) {
-        const int k = b + lane;
-        const bool v = k < en[t];
-        const int32_t x = v ? (__ldg(r[t] + k) & 0x7fffffff) : INT_MAX;
-        bool keep = v && x > (int32_t)i0;
-#pragma unroll
-        for (int q = 0; q < t; ++q)
-          if (__any_sync(0xffffffffu, keep) && in_row_window(r[q], pq[q], en[q], x, v, lane))
-            keep = false;
+    for (int t = 0; t < nv; ++t) {
+      const int32_t* r = a.rows.nbr + (size_t)(i0 + t) * a.rows.cap;
+      const int len = a.rows.cnt[i0 + t];
+      for (int b = 0; b < len; b += 32) {
+        const int32_t x = (b + lane < len) ? (__ldg(r + b + lane) & 0x7fffffff) : -1;
+        bool keep = x > (int32_t)i0;
+        if (keep && t > 0) {  // in an earlier row?
+          for (uint32_t h = hslot(x, tb);; h = (h + 1) & (Tc - 1)) {
+            const int32_t v = tab[h];
+            if (v == x) {
+              keep = false;
+              break;
+            }
+            if (v < 0) break;
+          }
+        }
+        if (keep && t + 1 < nv) {  // for the later rows' tests
+          for (uint32_t h = hslot(x, tb);; h = (h + 1) & (Tc - 1))
+            if (atomicCAS(&tab[h], -1, x) == -1) break;
+        }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         MDG_DASSERT(s + __popc(m) <= a.ucap);
         if (keep) out[s + __popc(m & lt)] = x;
         s += __popc(m);
       }
+      __syncwarp();  // this row's inserts before the next row's probes
     }
     if (lane == 0) a.ucnt[cl] = s;
   }
@@ -497,8 +487,7 @@ bool build_clusters(mdg_ctx* c, double cutoff, const ListView& rows, const int32
 bool build_row_unions(mdg_ctx* c, int list_id, const ListView& rows) {
   DevList& L = c->lists[list_id];
   DevList::Inner& I = L.inner;
-  if (!c->cluster_halgren || c->deterministic || !rows.sorted || !rows.dense || !I.gen ||
-      c->n_own == 0)
+  if (!c->cluster_halgren || c->deterministic || !rows.dense || !I.gen || c->n_own == 0)
     return false;
   const int64_t n = c->n_own;
   const int64_t ncl = (n + kCl - 1) / kCl;
@@ -534,8 +523,19 @@ bool build_row_unions(mdg_ctx* c, int list_id, const ListView& rows) {
   a.ucap = ucap;
   a.gen = force ? nullptr : I.gen;
   a.ugen = I.ugen;
+  // hash table per warp: 2048 slots (8 KB), enough for two rows of up to
+  // 1024 entries (the inserted keys) at load <= 1/2 when rows are that long
+  const int tbits = 11;
+  if (2 * (int64_t)L.max_cnt >= (1 << tbits)) return false;  // an empty slot always left
+  const size_t smem = (size_t)kWarps * ((size_t)1 << tbits) * sizeof(int32_t);
+  static size_t configured = 0;
+  if (smem > configured) {
+    MDG_CUDA_CHECK(cudaFuncSetAttribute(k_row_union, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    configured = smem;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((ncl + kWarps - 1) / kWarps, 148 * 64);
-  MDG_LAUNCH(c, "row_union", grid, kBlock, 0, k_row_union, a);
+  MDG_LAUNCH(c, "row_union", grid, kBlock, smem, k_row_union, a, tbits);
   MDG_LAUNCH(c, "cluster_gen", 1, 1, 0, k_cluster_gen, I.gen, I.ugen);
   I.ucap = ucap;
   I.ncl = ncl;

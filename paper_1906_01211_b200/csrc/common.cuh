@@ -225,7 +225,9 @@ struct ListView {
 // Rows a kernel with cutoff rc walks over list `list_id`: the buffered inner
 // list (rows cut to rc + buffer, re-cut on the device when some site has moved
 // more than buffer/2 since the last cut) or the list itself (nlist.cu).
-ListView kernel_rows(mdg_ctx* c, int list_id, double rc);
+// want_sorted false: the caller walks the rows in any order (the cluster
+// kernels' hash-built unions), so a cut skips the row sort.
+ListView kernel_rows(mdg_ctx* c, int list_id, double rc, bool want_sorted = true);
 
 __device__ __forceinline__ const int32_t* list_row(const ListView& L, int64_t i) {
   return L.nbr + (size_t)i * (size_t)L.cap;

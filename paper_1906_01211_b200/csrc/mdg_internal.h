@@ -84,6 +84,7 @@ struct DevList {
     int32_t* hcuts = nullptr;
     int32_t* dcuts = nullptr;
     int calls = 0, cuts0 = 0, bypass = 0;
+    bool cut_sorted = true;  // the last cut sorted its rows (kernel_rows want_sorted)
     // site-cluster unions of these rows (cluster.cu build_row_unions): per
     // cluster of kCl consecutive sites the sorted union of their rows,
     // rebuilt on the device when the rows are cut again
@@ -524,7 +525,7 @@ bool build_clusters(mdg_ctx* c, double cutoff, const struct ListView& rows, cons
 void count_stats_n(mdg_ctx* c, const int32_t* cnt, int64_t n, int slot);
 // The cluster unions of list `list_id`'s buffered rows `rows` (L.inner), for
 // the cluster pair kernels (Halgren); false when they do not apply (rows not
-// buffered / sorted, deterministic mode, disabled)
+// buffered, deterministic mode, disabled)
 bool build_row_unions(mdg_ctx* c, int list_id, const struct ListView& rows);
 // an NCCL / LOCAL group runs the interior/halo overlapped exchange (per-site rows)
 bool group_overlap(const mdg_ctx* c);

@@ -721,7 +721,7 @@ void check_lists_fresh(const mdg_ctx* c) {
                                     "built (rebuild it more often)");
 }
 
-ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
+ListView kernel_rows(mdg_ctx* c, int list_id, double rc, bool want_sorted) {
   DevList& L = c->lists[list_id];
   auto full_rows = [&] {
     if (!L.sorted) L.sorted = sort_rows(c, L.nbr, L.cnt, L.cap, L.max_cnt);
@@ -780,7 +780,9 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
     MDG_CUDA_CHECK(cudaMemsetAsync(I.gen, 0, sizeof(int32_t), c->stream));
   }
   const double4* P = (L.sites == MDG_SITES_VDW) ? c->vsite : c->pos;
-  const bool stale = I.src_version != L.version || I.rc != rcut;
+  // rows cut without a sort do not serve a caller that needs them sorted
+  const bool stale =
+      I.src_version != L.version || I.rc != rcut || (want_sorted && !I.cut_sorted);
   if (stale) {
     // cut unconditionally (2: forced, not counted as motion by the bypass)
     MDG_CUDA_CHECK(cudaMemsetAsync(I.flag, 0, sizeof(int32_t), c->stream));
@@ -813,8 +815,11 @@ ListView kernel_rows(mdg_ctx* c, int list_id, double rc) {
   k.warn = c->d_warn;
   k.gen0 = c->list_gen;
   MDG_LAUNCH_SITES(c, "cut_rows", k.n_rows, k, k_cut_rows);
-  // the cut rows are short: sort them (bucketed by length), when cut
-  const bool sorted = sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);
+  // the cut rows are short: sort them (bucketed by length), when cut -- unless
+  // the caller walks them in any order (then a later cut for a caller that
+  // needs them sorted is forced, above)
+  if (stale) I.cut_sorted = want_sorted;
+  const bool sorted = I.cut_sorted && sort_rows(c, I.nbr, I.cnt, L.cap, L.max_cnt, I.flag);
   debug_check_rows(c, "inner", I.nbr, I.cnt, L.cap, c->n_own, c->n, sorted);
   return ListView{I.nbr, I.cnt, L.cap, sorted, true};
 }

@@ -455,7 +455,9 @@ void run_halgren(mdg_ctx* c, int list_id, double cutoff, double delta, double ga
   k.vdwp = c->vdwp;
   k.vtab = c->n_vtypes ? c->vtab : nullptr;
   k.mol = c->mol;
-  k.L = kernel_rows(c, list_id, cutoff);
+  // the cluster kernel walks hash-built unions: its rows need no sort
+  const bool want_cl = c->cluster_halgren && !c->deterministic;
+  k.L = kernel_rows(c, list_id, cutoff, !want_cl);
   k.b = make_box(c->lx, c->ly, c->lz);
   k.c2 = cutoff * cutoff;
   k.delta = delta;
