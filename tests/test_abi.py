@@ -114,6 +114,7 @@ def _dist2_chains(ins):
 # weak 7): the cell-list build (wrapped and interior paths), the buffered-row
 # cut, and every pair kernel's prologue.
 PREDICATE_KERNELS = ("k_nlist_cells", "k_nlist_build", "k_cut_rows", "k_nonpolar", "k_halgren",
+                     "k_halgren_cl",
                      "k_perm_field", "k_mpole", "k_polar_force", "k_tmatvec", "k_count_within")
 
 
