@@ -475,6 +475,36 @@ def test_cluster_halgren_matches_per_site_and_oracle(engine, oracle, mdg):
     assert force_err_rms(a.forces, fo) <= F_TOL
 
 
+@pytest.mark.parametrize("seed", [3, 8])
+def test_irregular_molecules_order_and_cluster_halgren(engine, oracle, mdg, seed):
+    """Molecule-keyed site order and Halgren clusters with irregular
+    molecules: random molecule ids (1-5 sites, not contiguous in the caller's
+    order, sites far apart), n not a multiple of 3. Exclusions follow the
+    molecules; the cluster kernel, the per-site half rows and the oracle
+    agree, and caller-order results are unaffected by the re-ordering."""
+    rng = np.random.default_rng(seed)
+    s = uniform(oracle, 1000, 24.0, seed)
+    s.molecule = rng.integers(0, 330, s.n).astype(np.int32)
+    so = to_oracle_system(s)
+    fo, eo, wo = oracle.halgren(so, oracle.build_table(so, 7.0), 6.0, exclude=True)
+    engine.upload_system(s)
+    engine.upload_topology(s.molecule)
+    t = engine.build_neighbor_table(7.0)
+    out = {}
+    try:
+        for on in (True, False):
+            engine.set_cluster_halgren(on)
+            out[on] = engine.halgren_forces(t, mdg.HalgrenParams(6.0), exclude=True)
+    finally:
+        engine.set_cluster_halgren(True)
+    for g in out.values():
+        assert rel(g.energy, eo) <= E_TOL
+        assert force_err_rms(g.forces, fo) <= F_TOL
+    np.testing.assert_allclose(out[True].forces, out[False].forces, rtol=0,
+                               atol=1e-12 * np.abs(fo).max())
+    np.testing.assert_array_equal(t.pairs(), oracle.brute_force_pairs(s, 7.0))
+
+
 def test_mpole_matches_oracle(engine, oracle, mdg):
     """Real-space multipole energy/forces/torques/virial vs the T-tensor oracle."""
     s = amoeba_small(mdg, 343, 21.0, 5)
