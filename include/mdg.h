@@ -84,7 +84,11 @@ int mdg_positions_upload(mdg_ctx* ctx, const double* x, const double* y, const d
 int mdg_positions_upload_owned(mdg_ctx* ctx, const double* x, const double* y, const double* z);
 /* Topology (no reference counterpart): molecule ids (exclusion groups; NULL =
  * every site its own group) and the Halgren reduction parent/factor (NULL =
- * no reduction: vdW sites = atoms). */
+ * no reduction: vdW sites = atoms). With molecule ids, a one-domain context
+ * re-orders its resident sites so each molecule's sites are consecutive
+ * (the molecule tiles of the Halgren / PCG cluster kernels; MDG_MOL_ORDER=0
+ * keeps the site order): neighbour lists built before must be built again.
+ * The caller-order interface is unaffected. */
 int mdg_topology_upload(mdg_ctx* ctx, const int32_t* molecule, const int32_t* hred_parent,
                         const double* hred_factor);
 /* Permanent multipoles (no reference counterpart): dipole[3n] (x,y,z per
