@@ -676,10 +676,11 @@ int mdg_topology_upload(mdg_ctx* c, const int32_t* molecule, const int32_t* hred
     c->has_hred = hred_parent != nullptr;
     mdg::set_groups(c);
     if (c->has_hred) mdg::run_reduce_sites(c);
-    // molecule-keyed site order (one domain): a molecule's sites consecutive,
-    // so the PCG's 3-site clusters are water molecules (cluster.cu)
+    // molecule-keyed site order (a domain's owned and halo parts each): a
+    // molecule's sites consecutive, so the 3-site clusters are water
+    // molecules (cluster.cu)
     static const int mol_order = mdg::env_int("MDG_MOL_ORDER", 1);
-    if (molecule && mol_order && c->n_own == c->n && !c->group && mdg::mol_order_fits(c)) {
+    if (molecule && mol_order && !c->group && mdg::mol_order_fits(c)) {
       std::unordered_map<int32_t, int32_t> first;  // molecule -> lowest caller index
       first.reserve((size_t)n);
       for (int64_t s = 0; s < n; ++s) {

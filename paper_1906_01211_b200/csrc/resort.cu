@@ -190,8 +190,11 @@ bool mol_order_fits(const mdg_ctx* c) {
 }
 
 void resort_sites(mdg_ctx* c, const int32_t* rep) {
-  if (c->n_own != c->n || c->group)
-    throw_error(MDG_CONTRACT, "resort: single domain only (halo maps use sorted indices)");
+  // a domain's owned and halo parts are each re-ordered in place (owned
+  // sites first); only before its group exists (the halo maps are in sorted
+  // indices)
+  if (c->group || (c->n_own != c->n && !rep))
+    throw_error(MDG_CONTRACT, "resort: not for a domain in a group (halo maps use sorted indices)");
   const int64_t n = c->n;
   if (n < 2) return;
   const bool molkey = (rep || c->mol_sorted) && mol_order_fits(c);
@@ -209,11 +212,19 @@ void resort_sites(mdg_ctx* c, const int32_t* rep) {
   else
     MDG_LAUNCH(c, "resort_keys", grid_for(n, 256), 256, 0, k_morton_keys, n, c->pos,
                make_box(c->lx, c->ly, c->lz), nx, ny, nz, key, val);
-  size_t tb = 0;
-  MDG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, val, ord, n, 0, 63,
-                                                 c->stream));
-  MDG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(scub.get(tb), tb, key, key2, val, ord, n, 0, 63,
-                                                 c->stream));
+  // owned sites, then the halo, each sorted by its keys
+  const int64_t parts[2][2] = {{0, c->n_own}, {c->n_own, n}};
+  for (const auto& pr : parts) {
+    const int64_t m = pr[1] - pr[0];
+    if (m <= 0) continue;
+    size_t tb = 0;
+    MDG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key + pr[0], key2 + pr[0],
+                                                   val + pr[0], ord + pr[0], (int)m, 0, 64,
+                                                   c->stream));
+    MDG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(scub.get(tb), tb, key + pr[0], key2 + pr[0],
+                                                   val + pr[0], ord + pr[0], (int)m, 0, 64,
+                                                   c->stream));
+  }
   MDG_LAUNCH(c, "resort_inverse", grid_for(n, 256), 256, 0, k_inverse, n, ord, inv);
   void* tmp = stmp.get((size_t)n * 3 * sizeof(double4));
   // per-site records
