@@ -157,9 +157,16 @@ __global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a, int tbits) {
   for (int64_t cl = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); cl < a.ncl; cl += nw) {
     const int64_t i0 = cl * kCl;
     const int nv = (int)min((int64_t)kCl, a.n - i0);
-    // this cluster's table: a power of two >= 2 x the keys rows 0 and 1 can
-    // insert (load <= 1/2), within the T allocated (cleared per cluster)
-    const int need = a.rows.cnt[i0] + (nv > 1 ? a.rows.cnt[i0 + 1] : 0);
+    // this cluster's table: a power of two >= 2 x the keys rows 0 and 1
+    // insert (their entries past i0: counted first), within the T allocated
+    // (cleared per cluster)
+    int need = 0;
+    for (int t = 0; t + 1 < nv; ++t) {
+      const int32_t* r = a.rows.nbr + (size_t)(i0 + t) * a.rows.cap;
+      const int len = a.rows.cnt[i0 + t];
+      for (int b = lane; b < len; b += 32) need += (__ldg(r + b) & 0x7fffffff) > (int32_t)i0;
+    }
+    need = warp_allsum_i(need);
     int tb = 6;
     while (tb < tbits && (1 << tb) < 2 * need) ++tb;
     const int Tc = 1 << tb;
@@ -171,8 +178,19 @@ __global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a, int tbits) {
     for (int t = 0; t < nv; ++t) {
       const int32_t* r = a.rows.nbr + (size_t)(i0 + t) * a.rows.cap;
       const int len = a.rows.cnt[i0 + t];
-      for (int b = 0; b < len; b += 32) {
-        const int32_t x = (b + lane < len) ? (__ldg(r + b + lane) & 0x7fffffff) : -1;
+      // 4 chunks' entries loaded up front (one at a time, the loop was
+      // latency-bound on them)
+      for (int b4 = 0; b4 < len; b4 += 128) {
+        int32_t xs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = b4 + 32 * u + lane;
+          xs[u] = k < len ? (__ldg(r + k) & 0x7fffffff) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+        if (b4 + 32 * u >= len) break;  // warp-uniform
+        const int32_t x = xs[u];
         bool keep = x > (int32_t)i0;
         if (keep && t > 0) {  // in an earlier row?
           for (uint32_t h = hslot(x, tb);; h = (h + 1) & (Tc - 1)) {
@@ -192,6 +210,7 @@ __global__ void __launch_bounds__(kBlock) k_row_union(RUArgs a, int tbits) {
         MDG_DASSERT(s + __popc(m) <= a.ucap);
         if (keep) out[s + __popc(m & lt)] = x;
         s += __popc(m);
+        }
       }
       __syncwarp();  // this row's inserts before the next row's probes
     }
