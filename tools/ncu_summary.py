@@ -11,11 +11,18 @@ WANT = [("gpu__time_duration.sum", "ms"), ("dram__bytes_read.sum", "rd"), ("dram
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%")]
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-h = rows[0]
+h, units = rows[0], rows[1]
+SCALE = {("ms", "usecond"): 1e-3, ("ms", "us"): 1e-3, ("ms", "nsecond"): 1e-6, ("ms", "ns"): 1e-6, ("rd", "Mbyte"): 1e-3, ("wr", "Mbyte"): 1e-3,
+         ("rd", "Kbyte"): 1e-6, ("wr", "Kbyte"): 1e-6}
 for r in rows[2:]:
     name = r[h.index("Kernel Name")][:60]
     vals = []
     for k, lab in WANT:
         if k in h:
-            vals.append("%s=%s" % (lab, r[h.index(k)]))
-    print(name, " ".join(vals))
+            i = h.index(k)
+            v = r[i]
+            f = SCALE.get((lab, units[i]))
+            if f is not None:
+                v = "%g" % (float(v.replace(",", "")) * f)
+            vals.append("%s=%s" % (lab, v))
+    print(name, " ".join(vals), "(ms, GB)")
