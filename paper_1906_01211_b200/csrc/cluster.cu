@@ -1,32 +1,36 @@
-// cluster.cu -- the PCG mat-vec on site clusters (the north-star "atom-tile"
-// kernel for the solve's hot loop).
+// cluster.cu -- site clusters: the north-star "atom tiles" as molecules.
 //
 // A cluster is kCl = 3 consecutive sites of the sorted order. With molecules
 // uploaded the order is molecule-keyed (abi.cpp mdg_topology_upload,
-// resort.cu), so for water a cluster is one molecule: three sites within 1 A
-// whose 7 A rows are nearly the same set. Per cluster:
+// resort.cu), so for water a cluster is one molecule: three sites within
+// 1 A whose rows are nearly the same set.
+//
+// Halgren (nonpolar.cu k_halgren_cl, the default): k_row_union builds, when
+// the buffered 9.5 A rows are cut again, each cluster's half union -- the
+// entries past its first site of row 0, then of row 1 not in row 0, then of
+// row 2 in neither -- through a per-warp shared-memory hash set, so the rows
+// need no sort; the kernel then gathers j's record and adds its partner force
+// once per entry for the three sites.
+//
+// PCG (opt-in, mdg_set_cluster_matvec): per cluster
 //   U75   the sorted union of the three sites' buffered inner rows (the rows
 //         cut to 7 A + 0.5 A that the field pass walks), built by
-//         k_cluster_union when those rows are cut again -- on the device,
-//         gated by the cut's own generation counter, so in the static
-//         benchmark once per list rebuild and in dynamics once per re-cut --
-//         together with each row slot's position in U75 (cmap) and zero pair
-//         tensors for the (site, entry) slots no row holds;
-//   ct    per site of the cluster and entry of U75 the pair tensor (rr3, rr5),
-//         written by the field pass (polar.cu k_perm_field<CLMAP>) through
-//         cmap every step: the tensor within the cutoff, zero beyond.
+//         k_cluster_union when those rows are cut again (gated by the cut's
+//         generation counter), with each row slot's position in U75 (cmap)
+//         and zero pair tensors for the (site, entry) slots no row holds,
+//         in 32-entry chunks (ClChunk: per site the tensors, then the indices);
+//   ct    per site and entry the pair tensor (rr3, rr5), written by the field
+//         pass (polar.cu k_perm_field<CLMAP>) through cmap every step: the
+//         tensor within the cutoff, zero beyond.
 // On config 4 U75 has 216 entries per molecule (the three 7 A rows hold 435
-// pairs), so the mat-vec gathers j's position and direction once per 2.0
-// pairs instead of once per pair, for 26 B of streamed index + tensors per
-// pair (20 B in the per-site rows). The per-site stream was bound by the L1
-// data pipe on those gathers (82 %), not by HBM.
-//
-// The mat-vec (k_tmatvec_cl) is warp per cluster, lane per entry: each lane
-// streams the entry's index and three tensors (site-major, so every load is
-// a coalesced 512-B warp access), gathers j's position and direction once,
-// forms the three minimum-image separations (the operands and operations of
-// the field pass) and accumulates the field at all three sites; the 9 sums
-// are reduced once per cluster.
+// pairs): the mat-vec gathers j's position and direction once per 2.0 pairs
+// instead of once per pair, for 26 B of streamed index + tensors per pair
+// (20 B in the per-site rows, whose stream is bound by the L1 data pipe on
+// the gathers). k_tmatvec_cl is warp-specialized: a producer warp per block
+// copies the chunks into the three consumer warps' stage rings (TMA bulk
+// copies, full / empty mbarriers); the consumers gather and compute, lane per
+// entry, the 9 sums reduced once per cluster. Measured at parity with the
+// per-site stream.
 //
 // Reference counterpart: dipole_field_matvec_vectorized
 // (proj/src/polar_vec.cpp:131-204), whose per-site gather/select of j
@@ -39,9 +43,6 @@ namespace mdg {
 
 #ifndef MDG_CL_MINB
 #define MDG_CL_MINB 6
-#endif
-#ifndef MDG_CL_UNROLL
-#define MDG_CL_UNROLL 2
 #endif
 
 constexpr int kGrp = 4;  // lanes per cluster in the union merge (kCl used)
