@@ -1097,6 +1097,9 @@ static std::vector<uintptr_t> pcg_key(const std::vector<PcgDom>& ds, PcgComm* co
 static void pcg_graph_launch(PcgGraph& G, std::vector<PcgDom>& ds, PcgComm* comm,
                              int64_t max_iter, double n_global, double tol) {
   cudaStream_t s = ds[0].c->stream;
+  for (const PcgDom& d : ds)  // a moved partials buffer would be written after its free
+    if (d.k.partials != d.c->partials || (d.cl && d.kc.partials != d.c->partials))
+      throw_error(MDG_CUDA, "pcg: loop arguments hold a stale partials buffer");
   std::vector<uintptr_t> key = pcg_key(ds, comm, max_iter, tol, n_global);
   if (!G.exec || key != G.key) {
     if (G.exec) cudaGraphExecDestroy(G.exec);
@@ -1222,6 +1225,13 @@ int64_t run_pcg_multi(std::vector<mdg_ctx*> doms, PcgComm* comm, double tol_deby
                c->results);
   }
   if (comm) comm->allreduce(21, 1);
+  // the T mu0 launch above sizes its own grid (site-loop shape of the
+  // non-PCG kernel) and may have grown -- moved -- the partials since
+  // pcg_dom_setup: the loop kernels (and the graph key) take the current one
+  for (PcgDom& d : ds) {
+    d.k.partials = d.c->partials;
+    if (d.cl) d.kc.partials = d.c->partials;
+  }
   // (the reciprocal-space field's cuFFT calls stay out of the while graph)
   const bool graph = !c0->profile && (!comm || comm->capturable()) && !c0->pol_recip.on();
   if (graph) {
