@@ -57,6 +57,10 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*ErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -76,6 +80,8 @@ static const NcclApi& nccl() {
     sym(api.Send, "ncclSend");
     sym(api.Recv, "ncclRecv");
     sym(api.AllReduce, "ncclAllReduce");
+    sym(api.Reduce, "ncclReduce");
+    sym(api.Broadcast, "ncclBroadcast");
     sym(api.ErrorString, "ncclGetErrorString");
   });
   if (!api.AllReduce || !api.Send || !api.CommInitRank)
@@ -151,6 +157,24 @@ __global__ void k_grid_sum(size_t count, GridPtrs p, int nd) {
     double s = p.g[0][i];
     for (int d = 1; d < nd; ++d) s += p.g[d][i];
     p.g[0][i] = s;
+  }
+}
+
+// slab-decomposed reciprocal space on one device: element i of the grid, in
+// part p's planes [off[p], off[p+1]), <- the sum over the domains' grids (the
+// same fixed order as k_grid_sum), written into part p's own grid
+struct SlabOff {
+  int64_t o[kMaxGridDoms + 1];
+};
+
+__global__ void k_slab_reduce(size_t count, GridPtrs p, int nd, SlabOff off) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int part = 0;
+    while (part + 1 < nd && (int64_t)i >= off.o[part + 1]) ++part;
+    double s = p.g[0][i];
+    for (int d = 1; d < nd; ++d) s += p.g[d][i];
+    p.g[part][i] = s;
   }
 }
 
@@ -233,6 +257,81 @@ struct mdg_group : PcgComm {
     }
   }
   bool grid_shared() const override { return backend == MDG_GROUP_LOCAL; }
+
+  // slab-decomposed reciprocal space (MDG_PME_SLAB=1; default: replicated
+  // grid). LOCAL: the domains are the parts, the transposes are device
+  // copies on the one stream. NCCL: the ranks are the parts; grouped
+  // ncclReduce / ncclSend+ncclRecv / ncclBroadcast per part.
+  int slab_parts() const override {
+    const char* e = getenv("MDG_PME_SLAB");
+    if (!e || atoi(e) == 0) return 0;
+    const int P = backend == MDG_GROUP_LOCAL ? (int)dom.size() : size;
+    if (P > kMaxGridDoms) throw_error(MDG_CONTRACT, "group: too many parts for the slab FFT");
+    return P;
+  }
+  int slab_part(int d) const override { return backend == MDG_GROUP_LOCAL ? d : rank; }
+  void slab_reduce(double* const* grids, int n, const int64_t* off) override {
+    const int P = slab_parts();
+    if (backend == MDG_GROUP_LOCAL) {
+      if (n <= 1) return;
+      GridPtrs p{};
+      SlabOff o{};
+      for (int d = 0; d < n; ++d) p.g[d] = grids[d];
+      for (int q = 0; q <= P; ++q) o.o[q] = off[q];
+      dom[0]->launches++;
+      k_slab_reduce<<<148 * 8, 256, 0, stream()>>>((size_t)off[P], p, n, o);
+    } else {
+      nccl_check(nccl().GroupStart(), "ncclGroupStart");
+      for (int q = 0; q < P; ++q)
+        nccl_check(nccl().Reduce(grids[0] + off[q], grids[0] + off[q], off[q + 1] - off[q],
+                                 ncclDouble, ncclSum, q, comm, stream()),
+                   "ncclReduce (slab)");
+      nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    }
+  }
+  void slab_alltoall(cufftDoubleComplex* const* src, cufftDoubleComplex* const* dst, int n,
+                     const int64_t* soff, const int64_t* doff, const int64_t* cnt) override {
+    const int P = slab_parts();
+    const size_t z = sizeof(cufftDoubleComplex);
+    if (backend == MDG_GROUP_LOCAL) {
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < P; ++q)
+          if (cnt[p * P + q])
+            MDG_CUDA_CHECK(cudaMemcpyAsync(dst[q] + doff[q * P + p], src[p] + soff[p * P + q],
+                                           cnt[p * P + q] * z, cudaMemcpyDeviceToDevice,
+                                           stream()));
+    } else {
+      const int r = rank;
+      nccl_check(nccl().GroupStart(), "ncclGroupStart");
+      for (int q = 0; q < P; ++q) {
+        if (cnt[r * P + q])
+          nccl_check(nccl().Send(src[0] + soff[r * P + q], 2 * cnt[r * P + q], ncclDouble, q,
+                                 comm, stream()),
+                     "ncclSend (slab)");
+        if (cnt[q * P + r])
+          nccl_check(nccl().Recv(dst[0] + doff[r * P + q], 2 * cnt[q * P + r], ncclDouble, q,
+                                 comm, stream()),
+                     "ncclRecv (slab)");
+      }
+      nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    }
+  }
+  void slab_allgather(double* const* grids, int n, const int64_t* off) override {
+    const int P = slab_parts();
+    if (backend == MDG_GROUP_LOCAL) {
+      for (int q = 1; q < n; ++q)
+        MDG_CUDA_CHECK(cudaMemcpyAsync(grids[0] + off[q], grids[q] + off[q],
+                                       (off[q + 1] - off[q]) * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, stream()));
+    } else {
+      nccl_check(nccl().GroupStart(), "ncclGroupStart");
+      for (int q = 0; q < P; ++q)
+        nccl_check(nccl().Broadcast(grids[0] + off[q], grids[0] + off[q], off[q + 1] - off[q],
+                                    ncclDouble, q, comm, stream()),
+                   "ncclBroadcast (slab)");
+      nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    }
+  }
   bool recip_root(int d) const override {
     return backend == MDG_GROUP_LOCAL ? d == 0 : rank == 0;
   }

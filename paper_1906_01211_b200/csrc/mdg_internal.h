@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <cstdint>
 #include <cstdlib>
@@ -184,6 +185,21 @@ struct PcgComm {
   virtual bool grid_shared() const { return false; }
   virtual bool recip_root(int dom) const { return dom == 0; }
   virtual bool overlap() const { return false; }
+  // slab-decomposed reciprocal space (pme.cu PmeDoms, MDG_PME_SLAB=1):
+  // slab_parts() parts (0: the replicated grid above), local domain d is
+  // part slab_part(d). grids / bufs: the LOCAL domains' buffers, in domain
+  // order. slab_reduce: part p's grid holds, in its planes [off[p],
+  // off[p+1]) (doubles), the sum of every domain's grid. slab_alltoall: part
+  // p's src[soff[p*P+q], +cnt[p*P+q]) lands in part q's dst at
+  // doff[q*P+p] (complex counts). slab_allgather: every local grid (one per
+  // device) holds every part's planes.
+  virtual int slab_parts() const { return 0; }
+  virtual int slab_part(int dom) const { return dom; }
+  virtual void slab_reduce(double* const* grids, int n, const int64_t* off) {}
+  virtual void slab_alltoall(cufftDoubleComplex* const* src, cufftDoubleComplex* const* dst,
+                             int n, const int64_t* soff, const int64_t* doff,
+                             const int64_t* cnt) {}
+  virtual void slab_allgather(double* const* grids, int n, const int64_t* off) {}
   virtual void exchange_begin(int vec_id) { exchange(vec_id); }
   virtual void exchange_end() {}
 };

@@ -95,18 +95,22 @@ __global__ void k_pme_spread(int64_t n, PmeGeom g, const double4* __restrict__ p
 __global__ void __launch_bounds__(kBlock) k_pme_convolve(PmeGeom g, double alpha,
                                                         const double* __restrict__ bmod,
                                                         cufftDoubleComplex* __restrict__ s,
-                                                        double* __restrict__ partials) {
-  // partials == NULL: the convolution alone (the induced-dipole field)
+                                                        double* __restrict__ partials,
+                                                        int y0 = 0, int ny = -1) {
+  // partials == NULL: the convolution alone (the induced-dipole field).
+  // s holds the ky window [y0, y0 + ny) as [k1][ny][k3/2+1] (the whole
+  // spectrum when ny < 0; a slab-decomposed part's columns otherwise)
   const int kzh = g.k3 / 2 + 1;
-  const int64_t total = (int64_t)g.k1 * g.k2 * kzh;
+  if (ny < 0) ny = g.k2;
+  const int64_t total = (int64_t)g.k1 * ny * kzh;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   const double V = g.l1 * g.l2 * g.l3;
   const double pa = M_PI * M_PI / (alpha * alpha);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int kz = (int)(e % kzh);
-    const int ky = (int)((e / kzh) % g.k2);
-    const int kx = (int)(e / ((int64_t)kzh * g.k2));
+    const int ky = y0 + (int)((e / kzh) % ny);
+    const int kx = (int)(e / ((int64_t)kzh * ny));
     const int mx = (kx <= g.k1 / 2) ? kx : kx - g.k1;
     const int my = (ky <= g.k2 / 2) ? ky : ky - g.k2;
     const double m1 = mx / g.l1, m2 = my / g.l2, m3 = kz / g.l3;
@@ -270,7 +274,30 @@ struct PmeState {
   double* bmod = nullptr;
   cufftHandle fwd = 0, inv = 0;
   bool plans = false;
+  // slab decomposition (PcgComm::slab_parts): this domain is part `sl_part`
+  // of `sl_parts`; it owns the x-planes [x0, x1) of the real grid and, after
+  // the transpose, the ky columns [y0, y1) of the spectrum
+  int sl_parts = 0, sl_part = -1;
+  cufftHandle pf = 0, pi = 0, px = 0;  // 2D D2Z / Z2D over (y, z); 1D Z2Z along x
+  cufftDoubleComplex* sa = nullptr;  // [nx][k2][k3/2+1]: the part's planes
+  cufftDoubleComplex* sx = nullptr;  // the same, packed by destination part
+  cufftDoubleComplex* sb = nullptr;  // [k1][ny][k3/2+1]: the part's columns
 };
+
+static void slab_free(PmeState* s) {
+  if (s->sl_parts > 0) {
+    cufftDestroy(s->pf);
+    cufftDestroy(s->pi);
+    if (s->px) cufftDestroy(s->px);
+  }
+  cudaFree(s->sa);
+  cudaFree(s->sx);
+  cudaFree(s->sb);
+  s->sa = s->sx = s->sb = nullptr;
+  s->pf = s->pi = s->px = 0;
+  s->sl_parts = 0;
+  s->sl_part = -1;
+}
 
 static void pme_free_slot(void** slot) {
   PmeState* s = (PmeState*)*slot;
@@ -279,6 +306,7 @@ static void pme_free_slot(void** slot) {
     cufftDestroy(s->fwd);
     cufftDestroy(s->inv);
   }
+  slab_free(s);
   cudaFree(s->grid);
   cudaFree(s->spec);
   cudaFree(s->bmod);
@@ -307,6 +335,7 @@ static PmeState* pme_state(mdg_ctx* c, void** slot, int k1, int k2, int k3, int 
       cufftDestroy(s->inv);
       s->plans = false;
     }
+    slab_free(s);
     cudaFree(s->grid);
     cudaFree(s->spec);
     cudaFree(s->bmod);
@@ -793,6 +822,13 @@ struct PmeDoms {
   PmeGeom g;
   size_t count;
 
+  // slab decomposition: P parts, part p owns x-planes [x0[p], x0[p+1]) of
+  // the real grid and ky columns [y0[p], y0[p+1]) of the spectrum; kzh =
+  // k3/2+1 complex per (x, y) line
+  int P = 0;
+  std::vector<int> x0, y0;
+  int64_t kzh = 0;
+
   PmeDoms(const std::vector<mdg_ctx*>& d, PcgComm* cm, bool pol, int k1, int k2, int k3,
           int order)
       : doms(d), comm(cm) {
@@ -802,12 +838,130 @@ struct PmeDoms {
     g = PmeGeom{k1, k2, k3, order, c0->lx, c0->ly, c0->lz};
     count = (size_t)k1 * k2 * k3;
     shared = comm && comm->grid_shared();
+    P = comm ? comm->slab_parts() : 0;
+    if (P > 0) slab_setup();
+  }
+  int part(size_t k) const { return comm->slab_part((int)k); }
+  int64_t nx(int p) const { return x0[p + 1] - x0[p]; }
+  int64_t ny(int p) const { return y0[p + 1] - y0[p]; }
+  void slab_setup() {
+    if (g.k1 < P || g.k2 < P)
+      throw_error(MDG_CONTRACT, "pme: slab decomposition needs K1, K2 >= the number of parts");
+    kzh = g.k3 / 2 + 1;
+    for (int p = 0; p <= P; ++p) {
+      x0.push_back((int)((int64_t)p * g.k1 / P));
+      y0.push_back((int)((int64_t)p * g.k2 / P));
+    }
+    for (size_t k = 0; k < doms.size(); ++k) {
+      PmeState* s = st[k];
+      const int p = part(k);
+      mdg_ctx* c = doms[k];
+      if (s->sl_parts != P || s->sl_part != p) {
+        slab_free(s);
+        const size_t na = (size_t)nx(p) * g.k2 * kzh, nb = (size_t)g.k1 * ny(p) * kzh;
+        MDG_CUDA_CHECK(cudaMalloc(&s->sa, na * sizeof(cufftDoubleComplex)));
+        MDG_CUDA_CHECK(cudaMalloc(&s->sx, na * sizeof(cufftDoubleComplex)));
+        MDG_CUDA_CHECK(cudaMalloc(&s->sb, nb * sizeof(cufftDoubleComplex)));
+        int n2[2] = {g.k2, g.k3};
+        cufft_check(cufftPlanMany(&s->pf, 2, n2, nullptr, 1, 0, nullptr, 1, 0, CUFFT_D2Z,
+                                  (int)nx(p)),
+                    "plan slab D2Z");
+        cufft_check(cufftPlanMany(&s->pi, 2, n2, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2D,
+                                  (int)nx(p)),
+                    "plan slab Z2D");
+        // along x over the part's columns: element (x, col) at x * B + col
+        int n1[1] = {g.k1};
+        const int B = (int)(ny(p) * kzh);
+        cufft_check(cufftPlanMany(&s->px, 1, n1, n1, B, 1, n1, B, 1, CUFFT_Z2Z, B),
+                    "plan slab x");
+        s->sl_parts = P;
+        s->sl_part = p;
+      }
+      cufft_check(cufftSetStream(s->pf, c->stream), "stream");
+      cufft_check(cufftSetStream(s->pi, c->stream), "stream");
+      cufft_check(cufftSetStream(s->px, c->stream), "stream");
+    }
+  }
+  // offsets of the transposes: forward, part p's packed planes go to part q
+  // (block [nx_p][ny_q][kzh] at nx_p * y0[q] * kzh in p's send buffer) and
+  // land as rows x0[p].. of q's column buffer
+  void slab_offsets(std::vector<int64_t>& soff, std::vector<int64_t>& doff,
+                    std::vector<int64_t>& cnt, std::vector<int64_t>& cntT) const {
+    soff.assign(P * P, 0);
+    doff.assign(P * P, 0);
+    cnt.assign(P * P, 0);
+    cntT.assign(P * P, 0);
+    for (int p = 0; p < P; ++p)
+      for (int q = 0; q < P; ++q) {
+        soff[p * P + q] = nx(p) * y0[q] * kzh;
+        cnt[p * P + q] = nx(p) * ny(q) * kzh;
+        doff[q * P + p] = (int64_t)x0[p] * ny(q) * kzh;
+        cntT[q * P + p] = cnt[p * P + q];
+      }
+  }
+  void slab_solve(double alpha, double electric, int slot) {
+    std::vector<double*> grids;
+    std::vector<cufftDoubleComplex*> sx, sb;
+    for (PmeState* s : st) {
+      grids.push_back(s->grid);
+      sx.push_back(s->sx);
+      sb.push_back(s->sb);
+    }
+    const int n = (int)doms.size();
+    const int64_t plane = (int64_t)g.k2 * g.k3;
+    std::vector<int64_t> off(P + 1);
+    for (int p = 0; p <= P; ++p) off[p] = x0[p] * plane;
+    comm->slab_reduce(grids.data(), n, off.data());
+    std::vector<int64_t> soff, doff, cnt, cntT;
+    slab_offsets(soff, doff, cnt, cntT);
+    const size_t z = sizeof(cufftDoubleComplex);
+    // 2D transforms of the part's planes, packed by destination part
+    for (int k = 0; k < n; ++k) {
+      PmeState* s = st[k];
+      const int p = part(k);
+      cufft_check(cufftExecD2Z(s->pf, s->grid + off[p], s->sa), "slab D2Z");
+      for (int q = 0; q < P; ++q)
+        if (nx(p) && ny(q))
+          MDG_CUDA_CHECK(cudaMemcpy2DAsync(s->sx + soff[p * P + q], ny(q) * kzh * z,
+                                           s->sa + y0[q] * kzh, g.k2 * kzh * z, ny(q) * kzh * z,
+                                           nx(p), cudaMemcpyDeviceToDevice, doms[k]->stream));
+    }
+    comm->slab_alltoall(sx.data(), sb.data(), n, soff.data(), doff.data(), cnt.data());
+    // along x, convolution on the part's columns (its energy share into
+    // `slot`: the domains' slots are summed), back along x
+    for (int k = 0; k < n; ++k) {
+      mdg_ctx* c = doms[k];
+      PmeState* s = st[k];
+      const int p = part(k);
+      cufft_check(cufftExecZ2Z(s->px, s->sb, s->sb, CUFFT_FORWARD), "slab x fwd");
+      const int64_t total = (int64_t)g.k1 * ny(p) * kzh;
+      const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(grid_for(total), 148 * 32));
+      const bool energy = slot >= 0;
+      if (energy) ensure_partials(c, blocks);
+      MDG_LAUNCH(c, "pme_convolve", (unsigned)blocks, kBlock, 0, k_pme_convolve, g, alpha,
+                 s->bmod, s->sb, energy ? c->partials : (double*)nullptr, y0[p], (int)ny(p));
+      if (energy) finalize_partials(c, blocks, 1, slot, electric);
+      cufft_check(cufftExecZ2Z(s->px, s->sb, s->sb, CUFFT_INVERSE), "slab x inv");
+    }
+    comm->slab_alltoall(sb.data(), sx.data(), n, doff.data(), soff.data(), cntT.data());
+    for (int k = 0; k < n; ++k) {
+      PmeState* s = st[k];
+      const int p = part(k);
+      for (int q = 0; q < P; ++q)
+        if (nx(p) && ny(q))
+          MDG_CUDA_CHECK(cudaMemcpy2DAsync(s->sa + y0[q] * kzh, g.k2 * kzh * z,
+                                           s->sx + soff[p * P + q], ny(q) * kzh * z,
+                                           ny(q) * kzh * z, nx(p), cudaMemcpyDeviceToDevice,
+                                           doms[k]->stream));
+      cufft_check(cufftExecZ2D(s->pi, s->sa, s->grid + off[p]), "slab Z2D");
+    }
+    comm->slab_allgather(grids.data(), n, off.data());
   }
   void clear(size_t k) {
     MDG_CUDA_CHECK(cudaMemsetAsync(st[k]->grid, 0, count * sizeof(double), doms[k]->stream));
   }
   void sum() {
-    if (!comm) return;
+    if (!comm || P > 0) return;  // slab: reduced onto the parts in slab_solve
     std::vector<double*> grids;
     for (PmeState* s : st) grids.push_back(s->grid);
     comm->grid_sum(grids.data(), (int)grids.size(), count);
@@ -819,6 +973,7 @@ struct PmeDoms {
   // forward FFT, convolution (energy into `slot` of the root when >= 0),
   // inverse FFT
   void solve(double alpha, double electric, int slot) {
+    if (P > 0) return slab_solve(alpha, electric, slot);
     const int64_t total = (int64_t)g.k1 * g.k2 * (g.k3 / 2 + 1);
     const int64_t blocks = std::min<int64_t>(grid_for(total), 148 * 32);
     for (size_t k = 0; k < doms.size(); ++k) {

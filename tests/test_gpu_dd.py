@@ -128,6 +128,69 @@ def test_domains_with_reciprocal_space(mdg, size, polar_forces):
     assert d < 1e-6
 
 
+@pytest.mark.parametrize("size,polar_forces", [(2, True), (3, False), (8, True)])
+def test_domains_slab_fft(mdg, monkeypatch, size, polar_forces):
+    """Slab-decomposed reciprocal space (MDG_PME_SLAB=1): grids reduced onto
+    x-slabs, 2D transforms per slab, transpose to ky columns, 1D transforms
+    along x and the convolution per part, and back; the parts' energy shares
+    summed. Uneven slabs (42 x 36 x 30 over 3 and 8 parts) == the single
+    engine's 3D transform at the same grid."""
+    monkeypatch.setenv("MDG_PME_SLAB", "1")
+    s = mdg.water_box(1728, 37.26, 8, "amoeba")
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR
+    if polar_forces:
+        terms |= mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-6, 100, 1, terms)
+    lists = [(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)]
+    recip = ((42, 36, 30), 5)
+    en0, w0, it0, f0, mu0 = single(mdg, s, p, recip=recip)
+    F, MU, en, w, it = run_domains(mdg, s, size, p, lists, steps=2, recip=recip)
+    rms = np.sqrt(np.mean(f0 ** 2))
+    assert np.abs(F - f0).max() <= 1e-8 * rms
+    for k in range(3):
+        assert en[k] == pytest.approx(en0[k], rel=1e-9)
+    assert abs(it - it0) <= 1
+    d = np.sqrt(np.mean(np.sum((MU - mu0) ** 2, 1))) * mdg.DEBYE
+    assert d < 1e-6
+
+
+def test_nccl_group_slab_fft_world_size_one(mdg, monkeypatch):
+    """The NCCL slab path (grouped ncclReduce, ncclSend/ncclRecv transposes,
+    ncclBroadcast) at world size 1 with full Ewald == the single engine."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1906_01211_b200 import dd
+    monkeypatch.setenv("MDG_PME_SLAB", "1")
+    s = mdg.water_box(1000, 31.04, 8, "amoeba")
+    terms = mdg.TERM_VDW | mdg.TERM_MPOLE | mdg.TERM_POLAR | mdg.TERM_POLAR_FORCE
+    p = mdg.AmoebaParams(9.0, 0.07, 0.12, 7.0, 0.5446, mdg.ELECTRIC, 0.39, 1e-6, 100, 1, terms)
+    recip = ((36, 36, 36), 5)
+    en0, w0, it0, f0, mu0 = single(mdg, s, p, recip=recip)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29613"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        g = dd.DomainGroup(s, 1, HALO, backend="nccl", rank=0, list_cutoff=11.0)
+        try:
+            g.set_ewald_recip(*recip)
+            tables = g.build_lists([(9.0, 0, mdg.SITES_ATOMIC), (11.0, 1, mdg.SITES_VDW)])
+            g.amoeba_step(tables, p)
+            en, w, it, rms = g.energies()
+            ids, f = g.owned_forces()
+        finally:
+            g.close()
+    finally:
+        dist.destroy_process_group()
+    F = np.zeros_like(f0)
+    F[ids] = f
+    assert np.abs(F - f0).max() <= 1e-8 * np.sqrt(np.mean(f0 ** 2))
+    assert abs(it - it0) <= 1
+    for k in range(3):
+        assert en[k] == pytest.approx(en0[k], rel=1e-9)
+
+
 def test_domains_with_local_frames(mdg):
     """Local multipole frames in the decomposed step (frame atoms mapped to
     each domain's local ids) match the single engine."""

@@ -55,4 +55,7 @@ for size in (2, 4):
                       "pcg_iters": int(it)}
     print(size, out[str(size)], flush=True)
     g.close()
-json.dump(out, open(f"gpurun_out/dd_recip_c{cfg}.json", "w"), indent=1)
+import os  # noqa: E402
+slab = os.environ.get("MDG_PME_SLAB", "0")
+out["pme_slab"] = slab
+json.dump(out, open(f"gpurun_out/dd_recip_c{cfg}_slab{slab}.json", "w"), indent=1)
