@@ -258,13 +258,17 @@ struct mdg_group : PcgComm {
   }
   bool grid_shared() const override { return backend == MDG_GROUP_LOCAL; }
 
-  // slab-decomposed reciprocal space (MDG_PME_SLAB=1; default: replicated
-  // grid). LOCAL: the domains are the parts, the transposes are device
-  // copies on the one stream. NCCL: the ranks are the parts; grouped
-  // ncclReduce / ncclSend+ncclRecv / ncclBroadcast per part.
+  // slab-decomposed reciprocal space. Default: on for NCCL at world size
+  // > 1 (each rank transforms 1/P of the grid instead of all of it), off
+  // for LOCAL (one device: the parts' transforms serialise on one stream,
+  // the replicated grid transforms once); MDG_PME_SLAB=1 / 0 forces it.
+  // LOCAL: the domains are the parts, the transposes are device copies on
+  // the one stream. NCCL: the ranks are the parts; grouped ncclReduce /
+  // ncclSend+ncclRecv / ncclBroadcast per part.
   int slab_parts() const override {
     const char* e = getenv("MDG_PME_SLAB");
-    if (!e || atoi(e) == 0) return 0;
+    const bool on = e ? atoi(e) != 0 : (backend != MDG_GROUP_LOCAL && size > 1);
+    if (!on) return 0;
     const int P = backend == MDG_GROUP_LOCAL ? (int)dom.size() : size;
     if (P > kMaxGridDoms) throw_error(MDG_CONTRACT, "group: too many parts for the slab FFT");
     return P;
